@@ -1,0 +1,339 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 EXACT-MPPI hot path (BASELINE.json metric: MPPI control steps/sec and
+point-footprint SDF evals/sec).
+
+Workload (N=1 and every N): config 2 of BASELINE.json — 12-vertex L polygon, diff-drive,
+K=4096, T=50, N=10k dense static clutter, synthetic, seeded.
+A step is one full MPPI control cycle (noise, rollouts, exact SDF over K*T*N pairs, softmax
+update, validation, shift). At N GPUs the K rollouts are sharded over the ranks (strong
+scaling) with one NCCL all-gather of the softmax partials per step.
+
+  value  device time per step (CUDA events on the library's stream) with inputs resident in
+         HBM; L2 is flushed (256 MiB write) before every timed step, outside the events.
+  e2e    the same step through the C ABI with host buffers (cloud, state in; decision,
+         nominal out), host<->device copies inside the timed region (wall clock).
+
+`--impl reference` times the reference's own CPU implementation (MppiController::control_cycle
+of the unmodified reference built into oracle/_ref) on this host's cores.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+F_POLY = lambda B: 12 + 19 * B  # noqa: E731  algorithmic ops per point-pose pair
+F_RECT = lambda R: 9 + 16 * R   # noqa: E731
+
+
+def ops_per_pair(fp) -> int:
+    return F_POLY(fp.count()) if fp.is_polygon() else F_RECT(fp.count())
+
+
+def fp32_peak_tflops(sm_count: int = 148) -> tuple[float, str]:
+    """FP32 SIMT peak = 2 flops/FMA x 128 lanes x SMs x max SM clock. MEASURED_PEAKS.json holds
+    only HBM and bf16 peaks, so this is derived from its measured sm_max_mhz (1965 MHz)."""
+    mhz = 1965.0
+    src = "derived: 256 ops/SM/clk x %d SMs x sm_max_mhz" % sm_count
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            mhz = float(json.load(f).get("sm_max_mhz", mhz))
+        src += " (MEASURED_PEAKS.json)"
+    except Exception:
+        src += " (fallback 1965 MHz)"
+    return 256.0 * sm_count * mhz * 1e6 / 1e12, src
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index, self.rows, self.proc = index, [], None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "50"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc:
+            time.sleep(0.12)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        rows = [r for r in self.rows if len(r) == 6 and r[0].isdigit()]
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[2 + i] == "Active"})
+        return {"sm_mhz": statistics.median(float(r[0]) for r in rows),
+                "sm_max_mhz": max(float(r[1]) for r in rows), "reasons": reasons,
+                "samples": len(rows)}
+
+
+def dist_setup():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch.distributed as dist
+        import torch
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    return world, rank, local
+
+
+def allreduce_max(x: float, world: int) -> float:
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def cpu_reference_sample(wl, seconds: float = 12.0, k_sample: int = 512):
+    """The reference's own control_cycle (oracle/_ref: unmodified sources, all host threads) on
+    a K-subsample of the workload, extrapolated linearly in K (the step is K-parallel)."""
+    from tests import oracle_bindings as ob
+    import copy
+    p = copy.deepcopy(wl.params)
+    p.rollouts = min(k_sample, wl.params.rollouts)
+    threads = os.cpu_count() or 1
+    if ob.reference_available():
+        ref = ob.Reference(wl.footprint, wl.model, wl.limits, p, threads=threads)
+        ref.set_cloud(wl.cloud)
+        kind = "reference"
+        step = lambda: ref.controller_cycle(wl.q0, None, None, wl.guidance, use_stored_cloud=True)  # noqa
+    else:  # C restatement, single-threaded
+        orc = ob.Oracle(wl.footprint, wl.model, wl.limits, p)
+        nom, up = wl.zero_state()
+        threads = 1
+        kind = "port"
+        cyc = [0]
+
+        def step():
+            orc.control_cycle(wl.q0, wl.cloud, None, wl.guidance, nom, up, cyc[0])
+            cyc[0] += 1
+    times = []
+    t_end = time.perf_counter() + seconds
+    while time.perf_counter() < t_end or len(times) < 2:
+        t0 = time.perf_counter()
+        step()
+        times.append(time.perf_counter() - t0)
+        if len(times) >= 50:
+            break
+    t_sample = statistics.median(times)
+    t_full = t_sample * wl.params.rollouts / p.rollouts
+    return {"value": 1.0 / t_full, "unit": "steps/s", "cores": threads, "kind": kind,
+            "sample": (f"{len(times)} MppiController::control_cycle calls at K={p.rollouts} of "
+                       f"{wl.params.rollouts} (T={p.horizon}, N={wl.n_points}), median "
+                       f"{t_sample * 1e3:.1f} ms, extrapolated linearly in K"),
+            "sec_per_step": t_full}
+
+
+def run_reference(args, world, rank):
+    from paper_2605_29663_b200 import workloads as W
+    if rank != 0:
+        return
+    wl = W.cfg2()
+    base = cpu_reference_sample(wl, seconds=max(6.0, min(30.0, 0.05 * (args.steps + args.warmup))))
+    v = base["value"]
+    line = {"metric": "MPPI control steps/sec", "value": v, "unit": "steps/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 / v,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "impl": "reference",
+            "config": {"workload": wl.name, "K": wl.params.rollouts, "T": wl.params.horizon,
+                       "N": wl.n_points, "footprint": "l_shape_12 polygon (B=12)", "model": "diff"},
+            "cpu_baseline": {k: base[k] for k in ("value", "unit", "cores", "kind", "sample")},
+            "e2e": {"value": v, "unit": "steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "sdf_evals_per_s": wl.params.rollouts * wl.params.horizon * wl.n_points * v}
+    print(json.dumps(line), flush=True)
+
+
+def run_ours(args, world, rank, local):
+    import torch
+    from paper_2605_29663_b200 import workloads as W
+    from paper_2605_29663_b200.api import Engine
+
+    wl = W.cfg2()
+    K, T, N = wl.params.rollouts, wl.params.horizon, wl.n_points
+    D = wl.model.control_dim()
+    torch.cuda.set_device(local)
+    eng = Engine(wl.model, wl.limits, wl.footprint, wl.params, n_cap=N, guide_cap=8, device=local)
+    if world > 1:
+        import torch.distributed as dist
+        obj = [Engine.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        eng.attach_comm(rank, world, obj[0])
+    ext = torch.cuda.ExternalStream(eng.stream_ptr())
+    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device="cuda")
+    obstacles = wl.obstacles()
+
+    # ---- device-resident steps (value)
+    nom, up = wl.zero_state()
+    eng.stage(wl.q0, obstacles, wl.guidance, nom, up, 0)
+    eng.run_resident(max(3, args.warmup))
+    torch.cuda.synchronize()
+    eng.step_stats()  # drop the warm-up launches from the SDF accumulation
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(args.steps)]
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        for i in range(args.steps):
+            with torch.cuda.stream(ext):
+                flush.zero_()  # L2 flush (256 MiB > 126 MB L2), outside the timed events
+                evs[i][0].record(ext)
+            eng.run_resident(1)
+            with torch.cuda.stream(ext):
+                evs[i][1].record(ext)
+            if (i + 1) % 16 == 0 or i + 1 == args.steps:
+                torch.cuda.synchronize()
+        torch.cuda.synchronize()
+        step_ms = [a.elapsed_time(b) for a, b in evs]
+    stats = eng.step_stats()  # SDF kernel mean over exactly the timed steps
+    ms_local = float(np.mean(step_ms))
+    ms = allreduce_max(ms_local, world)
+    value = 1e3 / ms
+    dec = eng.read_resident()
+
+    # ---- end to end through the C ABI with host buffers (e2e)
+    nom, up = wl.zero_state()
+    for c in range(max(3, args.warmup)):
+        eng.control_cycle_raw(wl.q0, obstacles, wl.guidance, nom, up, c)
+    if world > 1:
+        torch.distributed.barrier()
+    t0 = time.perf_counter()
+    for c in range(args.steps):
+        eng.control_cycle_raw(wl.q0, obstacles, wl.guidance, nom, up, 1000 + c)
+    e2e_s = allreduce_max((time.perf_counter() - t0) / args.steps, world)
+    h2d = 104 + 8 * T * D + 16 * wl.guidance.path.shape[0] + 16 * N + N
+    d2h = 64 + 8 * (T + T * D + 3)
+
+    fp = wl.footprint
+    F = ops_per_pair(fp)
+    pairs = K // world * T * N
+    peak, peak_src = fp32_peak_tflops(torch.cuda.get_device_properties(local).multi_processor_count)
+    sdf_avg_ms = stats["sdf_ms"]
+    achieved = pairs * F / (sdf_avg_ms * 1e-3) / 1e12
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", "r01_sdf_grid_dram_bytes.json")
+    if os.path.exists(prof):
+        try:
+            traffic = json.load(open(prof)).get("dram_bytes_per_launch")
+        except Exception:
+            traffic = None
+    line = {
+        "metric": "MPPI control steps/sec", "value": value, "unit": "steps/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic",
+        "config": {"workload": wl.name, "K": K, "T": T, "N": N, "footprint": "l_shape_12 polygon (B=12)",
+                   "model": "diff", "parallelism": f"rollout-sharded x{world}",
+                   "l2": "flushed (256 MiB write) before every timed step"},
+        "sdf_evals_per_s": K * T * N / (ms * 1e-3),
+        "e2e": {"value": 1.0 / e2e_s, "unit": "steps/s", "h2d_bytes_per_step": h2d,
+                "d2h_bytes_per_step": d2h},
+        "gpu_launches": stats["launches_per_step"] * args.steps,
+        "roofline": {"bound": "fp32", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                     "frac": achieved / peak, "traffic": traffic,
+                     "kernel": "k_sdf_grid (per-pose exact SDF min, exact culling)",
+                     "sdf_kernel_ms": sdf_avg_ms,
+                     "algorithmic": f"K*T*N pairs x {F} ops/pair (SURVEY §8(d), unpruned)",
+                     "peak_source": peak_src},
+        "clocks": clk.summary(),
+        "decision": {"validated": dec.validated, "argmin": dec.argmin,
+                     "best_cost": dec.best_cost},
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        base = cpu_reference_sample(wl, seconds=10.0)
+        line["cpu_baseline"] = {k: base[k] for k in ("value", "unit", "cores", "kind", "sample")}
+    if rank == 0 and not args.no_sdf_batch:
+        line["sdf_batch"] = bench_sdf_batch(args, torch, peak, peak_src)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+
+
+def bench_sdf_batch(args, torch, peak, peak_src):
+    """Config 4: 64-vertex concave star vs 1,000 poses x 10^6 points (10^9 pairs), every pair
+    evaluated (k_sdf_pairs, per-pose min), inputs resident; FP32 roofline of that kernel."""
+    from paper_2605_29663_b200 import workloads as W
+    from paper_2605_29663_b200.api import Engine
+    fp, poses, pts = W.cfg4()
+    wl = W.cfg1(K=8, T=2)
+    eng = Engine(wl.model, wl.limits, fp, wl.params, n_cap=16, guide_cap=4)
+    eng.sdf_stage(poses, pts)
+    eng.sdf_run_resident(2, False)
+    eng.step_stats()
+    n = max(3, min(20, args.steps // 10))
+    eng.sdf_run_resident(n, False)
+    st = eng.step_stats()
+    ms = st["sdf_ms"]
+    pairs = poses.shape[0] * pts.shape[0]
+    F = ops_per_pair(fp)
+    achieved = pairs * F / (ms * 1e-3) / 1e12
+    eng.sdf_run_resident(1, True)
+    st2 = eng.step_stats()
+    return {"workload": "cfg4_star64_P1000_N1e6", "pairs": pairs, "kernel_ms_min_only": ms,
+            "kernel_ms_with_pairs": st2["sdf_ms"], "sdf_evals_per_s": pairs / (ms * 1e-3),
+            "roofline": {"bound": "fp32", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                         "frac": achieved / peak, "kernel": "k_sdf_pairs<POLYGON,64>",
+                         "algorithmic": f"P*N pairs x {F} ops/pair (every pair evaluated)",
+                         "peak_source": peak_src}}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=20)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-sdf-batch", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(3, args.warmup)
+    world, rank, local = dist_setup()
+    if args.impl == "reference":
+        run_reference(args, world, rank)
+    else:
+        run_ours(args, world, rank, local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,235 @@
+/*
+ * exm_b200.h — C ABI of the B200-native EXACT-MPPI rollout + exact-SDF hot path.
+ *
+ * Everything here is plain C: POD structs, host pointers and sizes, status codes.
+ * No CUDA, torch or C++ types cross this boundary. The library (libexm_b200.so)
+ * owns every device buffer, stream, CUDA graph and NCCL communicator behind an
+ * opaque handle; the caller owns every host buffer it passes in.
+ *
+ * Each entry point names the reference interface it replaces
+ * (paths relative to the reference tree, proj/...). The reference is a C++20 CPU
+ * library with no FFI; the drop-in is a replacement translation unit for
+ * proj/src/controller.cpp that implements proj/include/exactmppi/controller.hpp on
+ * top of these calls.
+ *
+ * Array layouts (all row-major, host memory):
+ *   points        pts_xy[2*i + {0,1}]                   world frame, N entries
+ *   mask          mask[i] != 0 marks a valid point     (ObstacleSet::mask, geometry.hpp:88-97)
+ *   guidance      guide_xy[2*j + {0,1}]                 polyline, P >= 1 points
+ *   controls      u[h*dim + c]                          NominalSequence, T x dim
+ *   perturbations eps[(r*T + h)*dim + c]                 K x T x dim (RolloutBatch::at, controller.hpp:60-63)
+ *   states        states[(r*(T+1) + h)*3 + {x,y,theta}]
+ *   d_min         d_min[r*T + h]
+ * dim is MotionModel::control_dim() (kinematics.cpp:14-26): diff/ackermann 2, omni 3,
+ * spin/parallel 1.
+ *
+ * Threading mirrors MppiController (controller.hpp:138-139): one handle is not safe for
+ * concurrent use; distinct handles may be used from distinct threads.
+ */
+#ifndef EXM_B200_H
+#define EXM_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define EXM_ABI_VERSION 1
+
+typedef int32_t exm_status;
+enum {
+  EXM_OK = 0,
+  EXM_ERR_INVALID_ARGUMENT = 1, /* reference: std::invalid_argument */
+  EXM_ERR_CUDA = 2,
+  EXM_ERR_NCCL = 3,
+  EXM_ERR_UNSUPPORTED = 4,
+  EXM_ERR_INTERNAL = 5
+};
+
+/* FootprintSpec::shape alternatives (geometry.hpp:41-85). */
+enum { EXM_FOOTPRINT_RECT_COVER = 0, EXM_FOOTPRINT_POLYGON = 1 };
+
+/* Polygon: count vertices (x[i], y[i]); CCW expected, CW is reversed with a warning
+ * exactly like PolygonFootprint::make (geometry.cpp:79-110).
+ * Rectangle cover: count boxes, centre (x[i], y[i]), half extents (hx[i], hy[i])
+ * (RectangleCover::make, geometry.cpp:66-77). */
+typedef struct exm_footprint {
+  int32_t kind;
+  int32_t count;
+  const double* x;
+  const double* y;
+  const double* hx; /* rect cover only */
+  const double* hy; /* rect cover only */
+} exm_footprint;
+
+/* ModelTag (kinematics.hpp:13). */
+enum {
+  EXM_MODEL_DIFF = 0,
+  EXM_MODEL_ACKERMANN = 1,
+  EXM_MODEL_OMNI = 2,
+  EXM_MODEL_SPIN = 3,
+  EXM_MODEL_PARALLEL = 4
+};
+
+/* MotionModel (kinematics.hpp:16-28). */
+typedef struct exm_model {
+  int32_t tag;
+  int32_t reserved;
+  double wheelbase;
+} exm_model;
+
+/* KinematicLimits / ComponentLimit (kinematics.hpp:51-63). */
+typedef struct exm_limits {
+  double vel_min[3];
+  double vel_max[3];
+  double acc_min[3];
+  double acc_max[3];
+  double steer_max;
+} exm_limits;
+
+/* MppiParams + TaskWeights (controller.hpp:13-35). */
+typedef struct exm_params {
+  int32_t rollouts; /* K */
+  int32_t horizon;  /* T */
+  double dt;
+  double lambda;
+  double sigma[3];
+  double d_safe;
+  double w_coll;
+  double w_rep;
+  double w_inf;
+  double w_goal_pos;
+  double w_goal_head;
+  double w_xtrack;
+  double w_progress;
+  double w_ctrl;
+  uint64_t seed;
+} exm_params;
+
+/* ControlDecision + CycleDiagnostics (controller.hpp:66-77), plus the argmin rollout
+ * (index of beta) which the reference computes implicitly (controller.cpp:315). */
+typedef struct exm_decision {
+  double command[3];
+  int32_t validated;
+  int32_t argmin;
+  double best_cost;      /* beta over augmented costs */
+  double weight_entropy; /* -sum w log w */
+  double nominal_cost;   /* cost of the validated sequence */
+  double* nominal_dmin;  /* caller buffer of T doubles, or NULL */
+} exm_decision;
+
+typedef struct exm_handle exm_handle;
+
+/* ---- library ----------------------------------------------------------------- */
+int32_t exm_abi_version(void);
+/* Thread-local message of the last failing call (reference exception text). */
+const char* exm_last_error(void);
+
+/* ---- lifetime ----------------------------------------------------------------
+ * Replaces MppiController::MppiController (controller.hpp:141-142, controller.cpp:284-294):
+ * validates the footprint (geometry.cpp:66-110), the model (kinematics.cpp:9-12) and the
+ * params (MppiParams::validate, controller.cpp:13-23), prepares the footprint
+ * (prepare, geometry.cpp:230-258) and sizes device buffers for (K, T, n_cap, guide_cap).
+ * device < 0 selects the current CUDA device. */
+exm_status exm_create(const exm_footprint* footprint, const exm_model* model,
+                      const exm_limits* limits, const exm_params* params, int32_t n_cap,
+                      int32_t guide_cap, int32_t device, exm_handle** out);
+void exm_destroy(exm_handle* h);
+
+/* ---- the MPPI step -------------------------------------------------------------
+ * Replaces MppiController::control_cycle (controller.hpp:146-147, controller.cpp:304-365).
+ * The controller state the reference keeps in the object (nominal_, u_prev_, cycle_;
+ * controller.hpp:167-169) is passed in and out explicitly: nominal_inout (T x dim) and
+ * u_prev_inout (dim) are read, then overwritten with the shifted/held nominal and the
+ * command. cycle is the RNG key of sample_perturbations (controller.cpp:306).
+ * eps_or_null: NULL draws perturbations on the device from (params.seed, cycle) exactly as
+ * sample_perturbations keys them; non-NULL injects a K x T x dim array (parity mode).
+ * Sharded handles (exm_attach_comm) process rollouts [rank*K/G, (rank+1)*K/G) and exchange
+ * softmax partials with one NCCL all-gather; every rank returns the same decision. */
+exm_status exm_control_cycle(exm_handle* h, const double q0[3], const double* pts_xy,
+                             const uint8_t* mask, int32_t n_points, const double* guide_xy,
+                             int32_t n_guide, const double goal[3], double* nominal_inout,
+                             double* u_prev_inout, uint64_t cycle, const double* eps_or_null,
+                             exm_decision* out);
+
+/* Replaces evaluate_rollouts (controller.hpp:116-121, controller.cpp:178-220): rollouts,
+ * clamped controls, states, per-step min signed distance, costs and unsafe flags for the
+ * given perturbations (K x T x dim, required). Any output pointer may be NULL. */
+exm_status exm_evaluate_rollouts(exm_handle* h, const double q0[3], const double* nominal,
+                                 const double* eps, const double* pts_xy, const uint8_t* mask,
+                                 int32_t n_points, const double* guide_xy, int32_t n_guide,
+                                 const double goal[3], const double* u_prev,
+                                 double* controls_out, double* states_out, double* dmin_out,
+                                 double* costs_out, uint8_t* unsafe_out);
+
+/* Replaces sample_perturbations (controller.hpp:107-108, controller.cpp:78-96), computed on
+ * the device: eps_out[K*T*dim] = sigma_c * gaussian_at(seed, cycle, r, h, c). */
+exm_status exm_sample_perturbations(exm_handle* h, uint64_t seed, uint64_t cycle,
+                                    double* eps_out);
+
+/* Replaces validate_nominal (controller.hpp:125-129, controller.cpp:254-282). */
+exm_status exm_validate_nominal(exm_handle* h, const double* nominal, const double q0[3],
+                                const double* pts_xy, const uint8_t* mask, int32_t n_points,
+                                const double* guide_xy, int32_t n_guide, const double goal[3],
+                                const double* u_prev, int32_t* valid_out, double* dmin_out,
+                                double* cost_out);
+
+/* ---- signed distance ------------------------------------------------------------
+ * Replaces min_signed_distance_at (geometry.hpp:150-152, geometry.cpp:357-375) for a batch
+ * of world poses (P x {x,y,theta}) against one cloud, and optionally emits every per-pair
+ * signed distance (per_pair[p*N + i], body-frame sd of point i at pose p; masked points
+ * report +inf). per_pose_min has the reference semantics: min over valid points, or
+ * kEmptyMaskDistance (1e6) when the mask is empty. Either output may be NULL. */
+exm_status exm_sdf_batch(exm_handle* h, const double* poses, int32_t n_poses,
+                         const double* pts_xy, const uint8_t* mask, int32_t n_points,
+                         float* per_pair, double* per_pose_min);
+
+/* exm_sdf_batch in three phases for serving loops and benchmarks: stage the poses and the
+ * cloud once (host -> device, recentred at the poses' centroid in FP64), run the kernel
+ * n_steps times on the resident inputs (want_pairs: also write every per-pair value on the
+ * device), read the last results back. */
+exm_status exm_sdf_stage(exm_handle* h, const double* poses, int32_t n_poses,
+                         const double* pts_xy, const uint8_t* mask, int32_t n_points);
+exm_status exm_sdf_run_resident(exm_handle* h, int32_t n_steps, int32_t want_pairs);
+exm_status exm_sdf_read(exm_handle* h, float* per_pair, double* per_pose_min);
+
+/* Replaces batch_signed_distance (geometry.hpp:142-143, geometry.cpp:298-318): body-frame
+ * queries, one signed distance each. */
+exm_status exm_batch_signed_distance(exm_handle* h, const double* queries, int32_t n,
+                                     double* out);
+
+/* ---- multi-GPU (one process per GPU) ----------------------------------------------
+ * The reference's only parallelism is a std::thread fork-join over rollouts
+ * (controller.cpp:207-218). Here rollouts are sharded over ranks; rank 0 creates the id,
+ * the caller broadcasts it (e.g. torch.distributed), every rank attaches. */
+exm_status exm_nccl_unique_id(uint8_t id_out[128]);
+exm_status exm_attach_comm(exm_handle* h, int32_t rank, int32_t world, const uint8_t id[128]);
+
+/* ---- resident-input stepping (benchmark / serving loop) -----------------------------
+ * Stage the inputs of a control step once (host -> device), then run n_steps control
+ * cycles on the resident inputs (receding horizon: the nominal and rate anchor evolve,
+ * the cycle key advances). Timing is left to the caller, who records events on the
+ * handle's stream (exm_stream). */
+exm_status exm_stage_inputs(exm_handle* h, const double q0[3], const double* pts_xy,
+                            const uint8_t* mask, int32_t n_points, const double* guide_xy,
+                            int32_t n_guide, const double goal[3], const double* nominal,
+                            const double* u_prev, uint64_t cycle);
+exm_status exm_run_resident(exm_handle* h, int32_t n_steps);
+exm_status exm_read_resident(exm_handle* h, double* nominal_out, double* u_prev_out,
+                             exm_decision* out);
+/* cudaStream_t of the handle, as an opaque pointer. */
+void* exm_stream(exm_handle* h);
+/* Kernel accounting: kernels launched per step, the SDF kernel's mean device time per step
+ * (ms; CUDA events recorded around every SDF launch on the handle's stream) over all
+ * exm_run_resident / exm_sdf_run_resident steps since the previous exm_step_stats call (or of
+ * the last exm_control_cycle), and the point-pose pairs one SDF launch covers (poses x
+ * points). Synchronises the stream and resets the accumulation. */
+exm_status exm_step_stats(exm_handle* h, int32_t* launches_per_step, float* sdf_ms,
+                          int64_t* sdf_pairs);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* EXM_B200_H */

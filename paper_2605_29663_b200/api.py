@@ -1,0 +1,564 @@
+"""Host-side mirror of the reference's controller API (proj/include/exactmppi/*.hpp), backed by
+the B200 C ABI. Names, argument meaning and error behaviour follow the reference:
+
+  reference (C++)                               here
+  FootprintSpec / PolygonFootprint::make /      FootprintSpec.polygon / .rect_cover
+    RectangleCover::make (geometry.hpp:41-85)   (validation in the library; ValueError)
+  MotionModel (kinematics.hpp:16-28)            MotionModel
+  KinematicLimits (kinematics.hpp:51-63)        KinematicLimits
+  MppiParams / TaskWeights (controller.hpp:13-35) MppiParams / TaskWeights
+  Guidance (controller.hpp:38-41)               Guidance
+  ObstacleSet (geometry.hpp:88-97)              ObstacleSet
+  MppiController (controller.hpp:140-170)       MppiController
+  evaluate_rollouts (controller.hpp:116-121)    Controller handle .evaluate_rollouts
+  sample_perturbations (controller.hpp:107)     .sample_perturbations
+  validate_nominal (controller.hpp:125-129)     .validate_nominal
+  batch_signed_distance (geometry.hpp:142)      .batch_signed_distance
+  min_signed_distance_at (geometry.hpp:150)     .min_signed_distance_at
+
+std::invalid_argument maps to ValueError. Arrays are numpy float64 (uint8 masks).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import json
+import math
+from dataclasses import dataclass, field
+from typing import Sequence
+
+import numpy as np
+
+from . import _abi
+from ._abi import check, dptr, fptr, u8ptr
+
+K_EMPTY_MASK_DISTANCE = 1e6  # geometry.hpp:37
+K_PADDED_COORDINATE = 1e9    # geometry.hpp:35
+
+
+# ------------------------------------------------------------------------------ types
+@dataclass
+class FootprintSpec:
+    """Exactly one of a simple polygon (CCW, validated by the library) or a rectangle cover."""
+    kind: int
+    a: np.ndarray  # polygon: vertices (n,2); cover: centres (n,2)
+    b: np.ndarray | None = None  # cover: half extents (n,2)
+    name: str = ""
+
+    @staticmethod
+    def polygon(vertices, name: str = "polygon") -> "FootprintSpec":
+        v = np.ascontiguousarray(np.asarray(vertices, dtype=np.float64).reshape(-1, 2))
+        return FootprintSpec(_abi.FOOTPRINT_POLYGON, v, None, name)
+
+    @staticmethod
+    def rect_cover(centers, half_extents, name: str = "cover") -> "FootprintSpec":
+        c = np.ascontiguousarray(np.asarray(centers, dtype=np.float64).reshape(-1, 2))
+        h = np.ascontiguousarray(np.asarray(half_extents, dtype=np.float64).reshape(-1, 2))
+        return FootprintSpec(_abi.FOOTPRINT_RECT_COVER, c, h, name)
+
+    @staticmethod
+    def from_json(obj) -> "FootprintSpec":
+        """Fixture schema of proj/fixtures/footprints/*.json (scenario_io.cpp footprint block)."""
+        if isinstance(obj, str):
+            with open(obj) as f:
+                obj = json.load(f)
+        if obj["kind"] == "polygon":
+            return FootprintSpec.polygon(obj["vertices"], obj.get("name", ""))
+        rects = obj["rectangles"]
+        return FootprintSpec.rect_cover([r["center"] for r in rects],
+                                        [r["half_extent"] for r in rects], obj.get("name", ""))
+
+    def is_polygon(self) -> bool:
+        return self.kind == _abi.FOOTPRINT_POLYGON
+
+    def count(self) -> int:
+        return int(self.a.shape[0])
+
+    def all_vertices(self) -> np.ndarray:
+        if self.is_polygon():
+            return self.a.copy()
+        out = []
+        for (cx, cy), (hx, hy) in zip(self.a, self.b):
+            out += [(cx - hx, cy - hy), (cx + hx, cy - hy), (cx + hx, cy + hy), (cx - hx, cy + hy)]
+        return np.array(out)
+
+    def bounding_radius(self) -> float:
+        return float(np.max(np.hypot(*self.all_vertices().T)))
+
+    def _c(self):
+        """exm_footprint view; keeps the numpy buffers alive via the returned tuple."""
+        cols = [np.ascontiguousarray(self.a[:, 0]), np.ascontiguousarray(self.a[:, 1])]
+        if self.b is not None:
+            cols += [np.ascontiguousarray(self.b[:, 0]), np.ascontiguousarray(self.b[:, 1])]
+        else:
+            cols += [None, None]
+        fp = _abi.ExmFootprint(self.kind, self.count(), dptr(cols[0]), dptr(cols[1]),
+                               dptr(cols[2]), dptr(cols[3]))
+        return fp, cols
+
+
+@dataclass
+class MotionModel:
+    tag: int = _abi.MODEL_DIFF
+    wheelbase: float = 0.0
+
+    @staticmethod
+    def diff():
+        return MotionModel(_abi.MODEL_DIFF)
+
+    @staticmethod
+    def ackermann(wheelbase: float):
+        if wheelbase <= 0.0:
+            raise ValueError("ackermann wheelbase must be positive")
+        return MotionModel(_abi.MODEL_ACKERMANN, wheelbase)
+
+    @staticmethod
+    def omni():
+        return MotionModel(_abi.MODEL_OMNI)
+
+    @staticmethod
+    def spin():
+        return MotionModel(_abi.MODEL_SPIN)
+
+    @staticmethod
+    def parallel():
+        return MotionModel(_abi.MODEL_PARALLEL)
+
+    @staticmethod
+    def from_name(name: str, wheelbase: float = 0.0):
+        table = {"diff": MotionModel.diff, "omni": MotionModel.omni, "spin": MotionModel.spin,
+                 "parallel": MotionModel.parallel}
+        if name == "ackermann":
+            return MotionModel.ackermann(wheelbase)
+        if name not in table:
+            raise ValueError("unknown motion model: " + name)
+        return table[name]()
+
+    def control_dim(self) -> int:
+        return {0: 2, 1: 2, 2: 3, 3: 1, 4: 1}[self.tag]
+
+    def _c(self):
+        return _abi.ExmModel(self.tag, 0, self.wheelbase)
+
+
+@dataclass
+class ComponentLimit:
+    vel_min: float = -1.0
+    vel_max: float = 1.0
+    acc_min: float = -1e9
+    acc_max: float = 1e9
+
+
+@dataclass
+class KinematicLimits:
+    component: list = field(default_factory=lambda: [ComponentLimit() for _ in range(3)])
+    steer_max: float = 0.6
+
+    @staticmethod
+    def unbounded():
+        return KinematicLimits([ComponentLimit(-1e9, 1e9, -1e18, 1e18) for _ in range(3)], 1e9)
+
+    @staticmethod
+    def from_json(obj):
+        lim = KinematicLimits()
+        for key, attr in (("vel_min", "vel_min"), ("vel_max", "vel_max"), ("acc_min", "acc_min"),
+                          ("acc_max", "acc_max")):
+            for i, v in enumerate(obj.get(key, [])):
+                setattr(lim.component[i], attr, float(v))
+        lim.steer_max = float(obj.get("steer_max", lim.steer_max))
+        return lim
+
+    def _c(self):
+        c = self.component
+        return _abi.ExmLimits((C.c_double * 3)(*[x.vel_min for x in c]),
+                              (C.c_double * 3)(*[x.vel_max for x in c]),
+                              (C.c_double * 3)(*[x.acc_min for x in c]),
+                              (C.c_double * 3)(*[x.acc_max for x in c]), self.steer_max)
+
+
+@dataclass
+class TaskWeights:
+    goal_pos: float = 1.0
+    goal_head: float = 0.5
+    xtrack: float = 2.0
+    progress: float = 2.0
+
+
+@dataclass
+class MppiParams:
+    rollouts: int = 1000
+    horizon: int = 50
+    dt: float = 0.1
+    lambda_: float = 1.0
+    sigma: tuple = (0.3, 0.3, 0.3)
+    d_safe: float = 0.1
+    w_coll: float = 1e6
+    w_rep: float = 50.0
+    w_inf: float = 1e9
+    task: TaskWeights = field(default_factory=TaskWeights)
+    w_ctrl: float = 0.02
+    seed: int = 0
+
+    @staticmethod
+    def from_json(obj, **override):
+        p = MppiParams(rollouts=int(obj["rollouts"]), horizon=int(obj["horizon"]),
+                       dt=float(obj["dt"]), lambda_=float(obj["lambda"]),
+                       sigma=tuple(list(obj["sigma"]) + [0.3] * (3 - len(obj["sigma"]))),
+                       d_safe=float(obj["d_safe"]), w_coll=float(obj["w_coll"]),
+                       w_rep=float(obj["w_rep"]), w_inf=float(obj["w_inf"]),
+                       task=TaskWeights(float(obj["w_goal_pos"]), float(obj["w_goal_head"]),
+                                        float(obj["w_xtrack"]), float(obj["w_progress"])),
+                       w_ctrl=float(obj["w_ctrl"]))
+        for k, v in override.items():
+            setattr(p, k, v)
+        return p
+
+    def _c(self):
+        s = list(self.sigma) + [0.3] * (3 - len(self.sigma))
+        return _abi.ExmParams(self.rollouts, self.horizon, self.dt, self.lambda_,
+                              (C.c_double * 3)(*s[:3]), self.d_safe, self.w_coll, self.w_rep,
+                              self.w_inf, self.task.goal_pos, self.task.goal_head,
+                              self.task.xtrack, self.task.progress, self.w_ctrl,
+                              int(self.seed) & 0xFFFFFFFFFFFFFFFF)
+
+
+@dataclass
+class Guidance:
+    path: np.ndarray
+    goal: np.ndarray
+
+    def __post_init__(self):
+        self.path = np.ascontiguousarray(np.asarray(self.path, dtype=np.float64).reshape(-1, 2))
+        self.goal = np.ascontiguousarray(np.asarray(self.goal, dtype=np.float64).reshape(3))
+
+
+@dataclass
+class ObstacleSet:
+    points: np.ndarray
+    mask: np.ndarray
+
+    def __post_init__(self):
+        self.points = np.ascontiguousarray(np.asarray(self.points, dtype=np.float64).reshape(-1, 2))
+        self.mask = np.ascontiguousarray(np.asarray(self.mask, dtype=np.uint8).reshape(-1))
+
+    @staticmethod
+    def padded(valid_points, capacity: int) -> "ObstacleSet":
+        v = np.asarray(valid_points, dtype=np.float64).reshape(-1, 2)
+        if v.shape[0] > capacity:
+            raise ValueError("more valid points than obstacle-set capacity")
+        pts = np.full((capacity, 2), K_PADDED_COORDINATE)
+        pts[: v.shape[0]] = v
+        mask = np.zeros(capacity, np.uint8)
+        mask[: v.shape[0]] = 1
+        return ObstacleSet(pts, mask)
+
+    @staticmethod
+    def all_masked(capacity: int) -> "ObstacleSet":
+        return ObstacleSet.padded(np.zeros((0, 2)), capacity)
+
+    def capacity(self) -> int:
+        return int(self.points.shape[0])
+
+    def valid_count(self) -> int:
+        return int(np.count_nonzero(self.mask))
+
+
+@dataclass
+class ControlDecision:
+    command: np.ndarray
+    validated: bool
+    nominal: np.ndarray
+    best_cost: float
+    weight_entropy: float
+    nominal_cost: float
+    nominal_d_min: np.ndarray
+    argmin: int
+
+
+@dataclass
+class RolloutBatch:
+    rollouts: int
+    horizon: int
+    perturbations: np.ndarray  # (K, T, dim)
+    controls: np.ndarray       # (K, T, dim)
+    states: np.ndarray         # (K, T+1, 3)
+    d_min: np.ndarray          # (K, T)
+    costs: np.ndarray          # (K,)
+    unsafe: np.ndarray         # (K,) uint8
+
+
+# ------------------------------------------------------------------------------ engine
+class Engine:
+    """One device handle (libexm_b200.so). Sized at construction for (K, T, n_cap, guide_cap)."""
+
+    def __init__(self, model: MotionModel, limits: KinematicLimits, footprint: FootprintSpec,
+                 params: MppiParams, n_cap: int = 1024, guide_cap: int = 64, device: int = 0):
+        self.lib = _abi.load_library()
+        self.model, self.limits, self.footprint, self.params = model, limits, footprint, params
+        self.dim = model.control_dim()
+        self.n_cap, self.guide_cap = int(n_cap), int(guide_cap)
+        fp, keep = footprint._c()
+        self._keep = keep
+        h = C.POINTER(_abi.ExmHandle)()
+        m, l, p = model._c(), limits._c(), params._c()
+        check(self.lib.exm_create(C.byref(fp), C.byref(m), C.byref(l), C.byref(p), self.n_cap,
+                                  self.guide_cap, int(device), C.byref(h)))
+        self.h = h
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.lib.exm_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # -- helpers
+    def _cloud(self, obstacles: ObstacleSet | np.ndarray, mask=None):
+        if isinstance(obstacles, ObstacleSet):
+            pts, mask = obstacles.points, obstacles.mask
+        else:
+            pts = np.ascontiguousarray(np.asarray(obstacles, np.float64).reshape(-1, 2))
+        if mask is not None:
+            mask = np.ascontiguousarray(np.asarray(mask, np.uint8).reshape(-1))
+        if pts.shape[0] > self.n_cap:
+            raise ValueError("point count exceeds obstacle-set capacity")
+        return pts, mask
+
+    def _vec3(self, v):
+        return np.ascontiguousarray(np.asarray(v, np.float64).reshape(3))
+
+    def _u(self, u):
+        out = np.zeros(3)
+        u = np.asarray(u, np.float64).reshape(-1)
+        out[: u.size] = u
+        return out
+
+    # -- reference free functions
+    def sample_perturbations(self, seed: int, cycle: int) -> np.ndarray:
+        P = self.params
+        eps = np.empty((P.rollouts, P.horizon, self.dim))
+        check(self.lib.exm_sample_perturbations(self.h, seed, cycle, dptr(eps)))
+        return eps
+
+    def evaluate_rollouts(self, q0, nominal, perturbations, obstacles, guidance: Guidance,
+                          u_prev) -> RolloutBatch:
+        P = self.params
+        K, T, D = P.rollouts, P.horizon, self.dim
+        eps = np.ascontiguousarray(np.asarray(perturbations, np.float64))
+        if eps.size != K * T * D:
+            raise ValueError("perturbation array does not match K*T")
+        nom = np.ascontiguousarray(np.asarray(nominal, np.float64).reshape(-1))
+        if nom.size != T * D:
+            raise ValueError("nominal length does not match horizon")
+        pts, mask = self._cloud(obstacles)
+        controls = np.empty((K, T, D))
+        states = np.empty((K, T + 1, 3))
+        dmin = np.empty((K, T))
+        costs = np.empty(K)
+        unsafe = np.empty(K, np.uint8)
+        check(self.lib.exm_evaluate_rollouts(
+            self.h, dptr(self._vec3(q0)), dptr(nom), dptr(eps), dptr(pts), u8ptr(mask),
+            pts.shape[0], dptr(guidance.path), guidance.path.shape[0], dptr(guidance.goal),
+            dptr(self._u(u_prev)), dptr(controls), dptr(states), dptr(dmin), dptr(costs),
+            u8ptr(unsafe)))
+        return RolloutBatch(K, T, eps.reshape(K, T, D), controls, states, dmin, costs, unsafe)
+
+    def validate_nominal(self, nominal, q0, obstacles, guidance: Guidance, u_prev):
+        T, D = self.params.horizon, self.dim
+        nom = np.ascontiguousarray(np.asarray(nominal, np.float64).reshape(-1))
+        if nom.size != T * D:
+            raise ValueError("nominal length does not match horizon")
+        pts, mask = self._cloud(obstacles)
+        valid = C.c_int32()
+        dmin = np.empty(T)
+        cost = C.c_double()
+        check(self.lib.exm_validate_nominal(
+            self.h, dptr(nom), dptr(self._vec3(q0)), dptr(pts), u8ptr(mask), pts.shape[0],
+            dptr(guidance.path), guidance.path.shape[0], dptr(guidance.goal),
+            dptr(self._u(u_prev)), C.byref(valid), dptr(dmin), C.byref(cost)))
+        return bool(valid.value), dmin, float(cost.value)
+
+    def control_cycle_raw(self, q0, obstacles, guidance: Guidance, nominal: np.ndarray,
+                          u_prev: np.ndarray, cycle: int, eps=None) -> ControlDecision:
+        """One MPPI step with explicit controller state (nominal and u_prev updated in place)."""
+        T = self.params.horizon
+        pts, mask = self._cloud(obstacles)
+        dmin = np.empty(T)
+        dec = _abi.ExmDecision()
+        dec.nominal_dmin = dptr(dmin)
+        eps_arr = None
+        if eps is not None:
+            eps_arr = np.ascontiguousarray(np.asarray(eps, np.float64))
+        check(self.lib.exm_control_cycle(
+            self.h, dptr(self._vec3(q0)), dptr(pts), u8ptr(mask), pts.shape[0],
+            dptr(guidance.path), guidance.path.shape[0], dptr(guidance.goal), dptr(nominal),
+            dptr(u_prev), int(cycle), dptr(eps_arr), C.byref(dec)))
+        return ControlDecision(np.array(dec.command[: self.dim]), bool(dec.validated),
+                               nominal.reshape(T, self.dim).copy(), dec.best_cost,
+                               dec.weight_entropy, dec.nominal_cost, dmin, dec.argmin)
+
+    def batch_signed_distance(self, queries) -> np.ndarray:
+        q = np.ascontiguousarray(np.asarray(queries, np.float64).reshape(-1, 2))
+        out = np.empty(q.shape[0])
+        check(self.lib.exm_batch_signed_distance(self.h, dptr(q), q.shape[0], dptr(out)))
+        return out
+
+    def sdf_batch(self, poses, points, mask=None, per_pair: bool = False):
+        """Per-pose min_signed_distance_at (and optionally every per-pair value, float32)."""
+        ps = np.ascontiguousarray(np.asarray(poses, np.float64).reshape(-1, 3))
+        pts = np.ascontiguousarray(np.asarray(points, np.float64).reshape(-1, 2))
+        m = None if mask is None else np.ascontiguousarray(np.asarray(mask, np.uint8))
+        mins = np.empty(ps.shape[0])
+        pairs = np.empty((ps.shape[0], pts.shape[0]), np.float32) if per_pair else None
+        check(self.lib.exm_sdf_batch(self.h, dptr(ps), ps.shape[0], dptr(pts), u8ptr(m),
+                                     pts.shape[0], fptr(pairs), dptr(mins)))
+        return (mins, pairs) if per_pair else mins
+
+    def min_signed_distance_at(self, pose, obstacles: ObstacleSet) -> float:
+        return float(self.sdf_batch(np.asarray(pose).reshape(1, 3), obstacles.points,
+                                    obstacles.mask)[0])
+
+    # -- resident stepping (benchmarks / serving loops)
+    def stage(self, q0, obstacles, guidance: Guidance, nominal, u_prev, cycle: int = 0):
+        pts, mask = self._cloud(obstacles)
+        nom = np.ascontiguousarray(np.asarray(nominal, np.float64).reshape(-1))
+        check(self.lib.exm_stage_inputs(self.h, dptr(self._vec3(q0)), dptr(pts), u8ptr(mask),
+                                        pts.shape[0], dptr(guidance.path),
+                                        guidance.path.shape[0], dptr(guidance.goal), dptr(nom),
+                                        dptr(self._u(u_prev)), int(cycle)))
+
+    def run_resident(self, n_steps: int):
+        check(self.lib.exm_run_resident(self.h, int(n_steps)))
+
+    def read_resident(self):
+        T, D = self.params.horizon, self.dim
+        nom = np.empty(T * D)
+        up = np.empty(3)
+        dmin = np.empty(T)
+        dec = _abi.ExmDecision()
+        dec.nominal_dmin = dptr(dmin)
+        check(self.lib.exm_read_resident(self.h, dptr(nom), dptr(up), C.byref(dec)))
+        return ControlDecision(np.array(dec.command[:D]), bool(dec.validated), nom.reshape(T, D),
+                               dec.best_cost, dec.weight_entropy, dec.nominal_cost, dmin,
+                               dec.argmin)
+
+    def sdf_stage(self, poses, points, mask=None):
+        ps = np.ascontiguousarray(np.asarray(poses, np.float64).reshape(-1, 3))
+        pts = np.ascontiguousarray(np.asarray(points, np.float64).reshape(-1, 2))
+        m = None if mask is None else np.ascontiguousarray(np.asarray(mask, np.uint8))
+        check(self.lib.exm_sdf_stage(self.h, dptr(ps), ps.shape[0], dptr(pts), u8ptr(m),
+                                     pts.shape[0]))
+        self._sdf_shape = (ps.shape[0], pts.shape[0])
+
+    def sdf_run_resident(self, n_steps: int, want_pairs: bool):
+        check(self.lib.exm_sdf_run_resident(self.h, int(n_steps), 1 if want_pairs else 0))
+
+    def sdf_read(self, per_pair: bool = False):
+        P, N = self._sdf_shape
+        mins = np.empty(P)
+        pairs = np.empty((P, N), np.float32) if per_pair else None
+        check(self.lib.exm_sdf_read(self.h, fptr(pairs), dptr(mins)))
+        return mins, pairs
+
+    def stream_ptr(self) -> int:
+        return int(self.lib.exm_stream(self.h) or 0)
+
+    def step_stats(self):
+        n = C.c_int32()
+        ms = C.c_float()
+        pairs = C.c_int64()
+        check(self.lib.exm_step_stats(self.h, C.byref(n), C.byref(ms), C.byref(pairs)))
+        return {"launches_per_step": n.value, "sdf_ms": ms.value, "sdf_pairs": pairs.value}
+
+    # -- multi-GPU
+    @staticmethod
+    def nccl_unique_id() -> bytes:
+        lib = _abi.load_library()
+        buf = (C.c_uint8 * 128)()
+        check(lib.exm_nccl_unique_id(buf))
+        return bytes(buf)
+
+    def attach_comm(self, rank: int, world: int, uid: bytes | None):
+        buf = (C.c_uint8 * 128)(*(uid or bytes(128)))
+        check(self.lib.exm_attach_comm(self.h, int(rank), int(world), buf))
+
+
+class MppiController:
+    """MppiController (controller.hpp:140-170): the object keeps nominal_, u_prev_ and cycle_
+    (controller.hpp:167-169); each control_cycle runs one MPPI step on the B200."""
+
+    def __init__(self, model: MotionModel, limits: KinematicLimits, footprint: FootprintSpec,
+                 params: MppiParams, threads: int = 1, n_cap: int = 1024, guide_cap: int = 64,
+                 device: int = 0):
+        del threads  # the reference's std::thread count; the GPU path has no equivalent knob
+        self.engine = Engine(model, limits, footprint, params, n_cap, guide_cap, device)
+        self._model, self._params = model, params
+        self.dim = model.control_dim()
+        self._nominal = np.zeros(params.horizon * self.dim)
+        self._u_prev = np.zeros(3)
+        self._cycle = 0
+
+    def warm_start(self, measured):  # controller.cpp:296-300
+        lim = self.engine.limits
+        m = np.zeros(3)
+        m[: self.dim] = np.asarray(measured, np.float64).reshape(-1)[: self.dim]
+        u = _clamp_control(self._model, lim, self._params.dt, m, m)
+        self._nominal = np.tile(u[: self.dim], self._params.horizon).astype(np.float64)
+        self._u_prev = u.copy()
+
+    def set_rate_anchor(self, u):
+        self._u_prev = np.zeros(3)
+        self._u_prev[: self.dim] = np.asarray(u, np.float64).reshape(-1)[: self.dim]
+
+    def control_cycle(self, q0, obstacles: ObstacleSet, guidance: Guidance,
+                      eps=None) -> ControlDecision:
+        d = self.engine.control_cycle_raw(q0, obstacles, guidance, self._nominal, self._u_prev,
+                                          self._cycle, eps)
+        self._cycle += 1
+        return d
+
+    def nominal(self) -> np.ndarray:
+        return self._nominal.reshape(self._params.horizon, self.dim).copy()
+
+    def last_command(self) -> np.ndarray:
+        return self._u_prev[: self.dim].copy()
+
+    def cycle_index(self) -> int:
+        return self._cycle
+
+    def params(self) -> MppiParams:
+        return self._params
+
+    def model(self) -> MotionModel:
+        return self._model
+
+
+def _clamp_control(model: MotionModel, lim: KinematicLimits, dt: float, u, prev):
+    """clamp_control (kinematics.cpp:99-117) for the host-side warm start only."""
+    out = np.zeros(3)
+    for i in range(model.control_dim()):
+        c = lim.component[i]
+        lo, hi = c.vel_min, c.vel_max
+        if model.tag == _abi.MODEL_ACKERMANN and i == 1:
+            lo, hi = max(lo, -lim.steer_max), min(hi, lim.steer_max)
+        v = lo if u[i] < lo else (hi if hi < u[i] else u[i])
+        a, b = prev[i] + c.acc_min * dt, prev[i] + c.acc_max * dt
+        out[i] = a if v < a else (b if b < v else v)
+    return out
+
+
+def pose_array(poses: Sequence) -> np.ndarray:
+    return np.ascontiguousarray(np.asarray(poses, np.float64).reshape(-1, 3))
+
+
+def wrap_angle(a: float) -> float:  # geometry.cpp:17-23
+    tau = 2.0 * math.pi
+    a = math.fmod(a, tau)
+    if a <= -math.pi:
+        a += tau
+    if a > math.pi:
+        a -= tau
+    return a

@@ -1,0 +1,984 @@
+// exm_abi.cu — host side of libexm_b200.so: the C ABI of include/exm_b200.h.
+//
+// A handle owns: the prepared FP32 footprint table (kernel parameter), device buffers
+// sized at create for (K, T, n_cap, guide_cap), one non-blocking stream, two captured CUDA
+// graphs of the control step (device-drawn noise / injected noise), pinned staging buffers
+// for the host<->device copies of one step, and optionally an NCCL communicator (loaded with
+// dlopen so the process shares whatever libnccl torch already mapped).
+//
+// Every failure returns a status and sets a thread-local message; there is no CPU fallback.
+#include <dlfcn.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/exm_b200.h"
+#include "exm_common.cuh"
+
+using namespace exm;
+
+namespace {
+
+thread_local std::string g_err;
+
+exm_status fail(exm_status s, const std::string& msg) {
+  g_err = msg;
+  return s;
+}
+
+#define EXM_CUDA(call)                                                                   \
+  do {                                                                                   \
+    cudaError_t e_ = (call);                                                             \
+    if (e_ != cudaSuccess)                                                               \
+      return fail(EXM_ERR_CUDA, std::string(#call) + ": " + cudaGetErrorString(e_));     \
+  } while (0)
+
+// ---- minimal NCCL surface, resolved at attach time -------------------------------------
+typedef struct {
+  char internal[128];
+} nccl_uid_t;
+typedef void* nccl_comm_t;
+typedef int (*fn_get_uid)(nccl_uid_t*);
+typedef int (*fn_init_rank)(nccl_comm_t*, int, nccl_uid_t, int);
+typedef int (*fn_allgather)(const void*, void*, size_t, int, nccl_comm_t, cudaStream_t);
+typedef int (*fn_destroy)(nccl_comm_t);
+typedef const char* (*fn_errstr)(int);
+constexpr int kNcclDouble = 8;  // ncclFloat64
+
+struct NcclApi {
+  void* lib = nullptr;
+  fn_get_uid get_uid = nullptr;
+  fn_init_rank init_rank = nullptr;
+  fn_allgather allgather = nullptr;
+  fn_destroy destroy = nullptr;
+  fn_errstr errstr = nullptr;
+  bool load() {
+    if (lib) return true;
+    const char* names[] = {"libnccl.so.2", "libnccl.so"};
+    for (const char* n : names) {
+      lib = dlopen(n, RTLD_NOW | RTLD_GLOBAL);
+      if (lib) break;
+    }
+    if (!lib) return false;
+    get_uid = reinterpret_cast<fn_get_uid>(dlsym(lib, "ncclGetUniqueId"));
+    init_rank = reinterpret_cast<fn_init_rank>(dlsym(lib, "ncclCommInitRank"));
+    allgather = reinterpret_cast<fn_allgather>(dlsym(lib, "ncclAllGather"));
+    destroy = reinterpret_cast<fn_destroy>(dlsym(lib, "ncclCommDestroy"));
+    errstr = reinterpret_cast<fn_errstr>(dlsym(lib, "ncclGetErrorString"));
+    return get_uid && init_rank && allgather && destroy;
+  }
+};
+NcclApi g_nccl;
+
+template <class T>
+cudaError_t dalloc(T** p, size_t count) {
+  *p = nullptr;
+  if (count == 0) count = 1;
+  return cudaMalloc(reinterpret_cast<void**>(p), count * sizeof(T));
+}
+
+template <class T>
+cudaError_t halloc(T** p, size_t count) {
+  *p = nullptr;
+  if (count == 0) count = 1;
+  return cudaMallocHost(reinterpret_cast<void**>(p), count * sizeof(T));
+}
+
+int model_dim(int tag) {  // kinematics.cpp:14-26
+  switch (tag) {
+    case EXM_MODEL_DIFF:
+    case EXM_MODEL_ACKERMANN: return 2;
+    case EXM_MODEL_OMNI: return 3;
+    case EXM_MODEL_SPIN:
+    case EXM_MODEL_PARALLEL: return 1;
+  }
+  return 0;
+}
+
+// ---- footprint validation + FP32 table (geometry.cpp:66-110, :127-131, :230-258) -------
+int orientation(double ax, double ay, double bx, double by, double cx, double cy) {
+  const double v = (bx - ax) * (cy - ay) - (by - ay) * (cx - ax);
+  return v > 0.0 ? 1 : (v < 0.0 ? -1 : 0);
+}
+bool within(double ax, double ay, double bx, double by, double px, double py) {
+  return std::min(ax, bx) <= px && px <= std::max(ax, bx) && std::min(ay, by) <= py &&
+         py <= std::max(ay, by);
+}
+bool segments_cross(const std::vector<double>& x, const std::vector<double>& y, size_t i,
+                    size_t j) {
+  const size_t n = x.size();
+  const double ax = x[i], ay = y[i], bx = x[(i + 1) % n], by = y[(i + 1) % n];
+  const double cx = x[j], cy = y[j], dx = x[(j + 1) % n], dy = y[(j + 1) % n];
+  const int o1 = orientation(ax, ay, bx, by, cx, cy), o2 = orientation(ax, ay, bx, by, dx, dy);
+  const int o3 = orientation(cx, cy, dx, dy, ax, ay), o4 = orientation(cx, cy, dx, dy, bx, by);
+  if (o1 != o2 && o3 != o4) return true;
+  return (o1 == 0 && within(ax, ay, bx, by, cx, cy)) || (o2 == 0 && within(ax, ay, bx, by, dx, dy)) ||
+         (o3 == 0 && within(cx, cy, dx, dy, ax, ay)) || (o4 == 0 && within(cx, cy, dx, dy, bx, by));
+}
+
+exm_status build_footprint(const exm_footprint* fp, FpDev* out) {
+  std::memset(out, 0, sizeof *out);
+  if (!fp) return fail(EXM_ERR_INVALID_ARGUMENT, "footprint is null");
+  const int n = fp->count;
+  double radius = 0.0;
+  if (fp->kind == EXM_FOOTPRINT_POLYGON) {
+    if (n < 3 || !fp->x || !fp->y)
+      return fail(EXM_ERR_INVALID_ARGUMENT, "polygon needs at least 3 vertices");
+    std::vector<double> x(fp->x, fp->x + n), y(fp->y, fp->y + n);
+    for (int i = 0; i < n; ++i)
+      if (!std::isfinite(x[i]) || !std::isfinite(y[i]))
+        return fail(EXM_ERR_INVALID_ARGUMENT, "polygon has non-finite vertex");
+    for (int i = 0; i < n; ++i) {
+      const double ex = x[(i + 1) % n] - x[i], ey = y[(i + 1) % n] - y[i];
+      if (std::sqrt(ex * ex + ey * ey) == 0.0)
+        return fail(EXM_ERR_INVALID_ARGUMENT, "polygon has a zero-length edge");
+    }
+    for (int i = 0; i < n; ++i)
+      for (int j = i + 1; j < n; ++j) {
+        if (j == i + 1 || (i == 0 && j == n - 1)) continue;
+        if (segments_cross(x, y, i, j))
+          return fail(EXM_ERR_INVALID_ARGUMENT, "polygon boundary self-intersects");
+      }
+    double area2 = 0.0;
+    for (int i = 0; i < n; ++i) area2 += x[i] * y[(i + 1) % n] - y[i] * x[(i + 1) % n];
+    if (area2 < 0.0) {
+      std::fprintf(stderr, "[exactmppi] warning: polygon given clockwise, reversing to CCW\n");
+      std::reverse(x.begin(), x.end());
+      std::reverse(y.begin(), y.end());
+    }
+    if (n > kMaxEdges)
+      return fail(EXM_ERR_UNSUPPORTED, "polygon has more than 64 edges (kernel-parameter table)");
+    out->kind = EXM_FOOTPRINT_POLYGON;
+    out->count = n;
+    for (int i = 0; i < n; ++i) {
+      const double vx = x[i], vy = y[i];
+      const double ex = x[(i + 1) % n] - vx, ey = y[(i + 1) % n] - vy;
+      const double inv = 1.0 / (ex * ex + ey * ey);
+      float* e = out->e[i];
+      e[0] = static_cast<float>(vx);
+      e[1] = static_cast<float>(vy);
+      e[2] = static_cast<float>(ex);
+      e[3] = static_cast<float>(ey);
+      e[4] = static_cast<float>(ex * inv);
+      e[5] = static_cast<float>(ey * inv);
+      e[6] = static_cast<float>(-(vx * ex + vy * ey) * inv);
+      e[7] = static_cast<float>(vy + ey);
+      radius = std::max(radius, std::sqrt(vx * vx + vy * vy));
+    }
+  } else if (fp->kind == EXM_FOOTPRINT_RECT_COVER) {
+    if (n < 1 || !fp->x || !fp->y || !fp->hx || !fp->hy)
+      return fail(EXM_ERR_INVALID_ARGUMENT, "rectangle cover must be nonempty");
+    if (n > kMaxEdges)
+      return fail(EXM_ERR_UNSUPPORTED, "rectangle cover has more than 64 boxes");
+    out->kind = EXM_FOOTPRINT_RECT_COVER;
+    out->count = n;
+    for (int i = 0; i < n; ++i) {
+      const double cx = fp->x[i], cy = fp->y[i], hx = fp->hx[i], hy = fp->hy[i];
+      if (!std::isfinite(cx) || !std::isfinite(cy) || !std::isfinite(hx) || !std::isfinite(hy))
+        return fail(EXM_ERR_INVALID_ARGUMENT, "rectangle cover has non-finite entries");
+      if (hx <= 0.0 || hy <= 0.0)
+        return fail(EXM_ERR_INVALID_ARGUMENT, "rectangle half-extents must be strictly positive");
+      float* e = out->e[i];
+      e[0] = static_cast<float>(cx);
+      e[1] = static_cast<float>(cy);
+      e[2] = static_cast<float>(hx);
+      e[3] = static_cast<float>(hy);
+      const double xs[2] = {cx - hx, cx + hx}, ys[2] = {cy - hy, cy + hy};
+      for (double vx : xs)
+        for (double vy : ys) radius = std::max(radius, std::sqrt(vx * vx + vy * vy));
+    }
+  } else {
+    return fail(EXM_ERR_INVALID_ARGUMENT, "unknown footprint kind");
+  }
+  out->radius = static_cast<float>(radius);
+  return EXM_OK;
+}
+
+exm_status check_params(const exm_params* p) {  // MppiParams::validate, controller.cpp:13-23
+  if (p->rollouts < 1) return fail(EXM_ERR_INVALID_ARGUMENT, "mppi: rollouts must be >= 1");
+  if (p->horizon < 1) return fail(EXM_ERR_INVALID_ARGUMENT, "mppi: horizon must be >= 1");
+  if (!(p->dt > 0.0)) return fail(EXM_ERR_INVALID_ARGUMENT, "mppi: dt must be positive");
+  if (!(p->lambda > 0.0)) return fail(EXM_ERR_INVALID_ARGUMENT, "mppi: lambda must be positive");
+  for (double s : p->sigma)
+    if (s <= 0.0) return fail(EXM_ERR_INVALID_ARGUMENT, "mppi: sigma components must be positive");
+  if (p->d_safe < 0.0) return fail(EXM_ERR_INVALID_ARGUMENT, "mppi: d_safe must be nonnegative");
+  if (p->w_coll < 0.0 || p->w_rep < 0.0 || p->w_inf < 0.0)
+    return fail(EXM_ERR_INVALID_ARGUMENT, "mppi: penalty weights must be nonnegative");
+  return EXM_OK;
+}
+
+struct EventPair {
+  cudaEvent_t a = nullptr, b = nullptr;
+};
+
+}  // namespace
+
+struct exm_handle {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  FpDev fp{};
+  StepConst sc{};
+  int K = 0, T = 0, D = 0, n_cap = 0, guide_cap = 0;
+  // sharding
+  int rank = 0, world = 1;
+  nccl_comm_t comm = nullptr;
+  // device buffers
+  StepDyn* d_dyn = nullptr;
+  double* d_nominal = nullptr;
+  double* d_guide = nullptr;
+  double* d_pts = nullptr;
+  uint8_t* d_mask = nullptr;
+  float2* d_tmp = nullptr;
+  float2* d_cloud = nullptr;
+  int* d_cell_start = nullptr;
+  GridMeta* d_grid = nullptr;
+  double* d_eps = nullptr;
+  float4* d_poses = nullptr;
+  double* d_base = nullptr;
+  float* d_dmin = nullptr;
+  double* d_partials = nullptr;
+  double* d_upd = nullptr;
+  float4* d_val_poses = nullptr;
+  double* d_val_base = nullptr;
+  float* d_val_dmin = nullptr;
+  // contiguous output block: DecisionDev | nominal_dmin[T] | nominal[T*D] | u_prev[3]
+  unsigned char* d_out = nullptr;
+  size_t out_bytes = 0;
+  // evaluate_rollouts extras (lazy)
+  double* d_controls = nullptr;
+  double* d_states = nullptr;
+  double* d_cost = nullptr;
+  uint8_t* d_unsafe = nullptr;
+  // pinned staging
+  StepDyn* h_dyn = nullptr;
+  double* h_nominal = nullptr;
+  double* h_guide = nullptr;
+  double* h_pts = nullptr;
+  uint8_t* h_mask = nullptr;
+  unsigned char* h_out = nullptr;
+  // graphs: [0] device noise, [1] injected noise
+  cudaGraphExec_t exec[2] = {nullptr, nullptr};
+  cudaGraphNode_t ev_node[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};
+  EventPair graph_ev;
+  // per-step SDF timing ring (resident runs)
+  std::vector<EventPair> ring;
+  int ring_used = 0;
+  EventPair step_ev;
+  int last_steps = 0;
+  // SDF batch workspace (grown on demand)
+  int sb_poses_cap = 0, sb_points_cap = 0;
+  size_t sb_pairs_cap = 0;
+  float4* sb_poses = nullptr;
+  double* sb_pts64 = nullptr;
+  float2* sb_pts = nullptr;
+  uint8_t* sb_mask = nullptr;
+  unsigned* sb_keys = nullptr;
+  double* sb_min = nullptr;
+  float* sb_pairs = nullptr;
+  int sb_P = 0, sb_N = 0, sb_has_mask = 0, sb_last_pairs = 0;
+  int launches_per_step = 0;
+  int64_t last_pairs = 0;
+};
+
+namespace {
+
+DecisionDev* out_dec(exm_handle* h) { return reinterpret_cast<DecisionDev*>(h->d_out); }
+double* out_dmin(exm_handle* h) { return reinterpret_cast<double*>(h->d_out + sizeof(DecisionDev)); }
+double* out_nominal(exm_handle* h) { return out_dmin(h) + h->T; }
+double* out_uprev(exm_handle* h) { return out_nominal(h) + h->T * h->D; }
+
+void set_shard(exm_handle* h) {
+  StepConst& sc = h->sc;
+  sc.k_local = h->K / h->world;
+  sc.r_offset = h->rank * sc.k_local;
+  sc.nblocks_local = (sc.k_local + kBlockRollouts - 1) / kBlockRollouts;
+  sc.block_offset = h->rank * sc.nblocks_local;
+  sc.nblocks_total = sc.nblocks_local * h->world;
+}
+
+void destroy_graphs(exm_handle* h) {
+  for (auto& e : h->exec)
+    if (e) {
+      cudaGraphExecDestroy(e);
+      e = nullptr;
+    }
+}
+
+// The control step: [noise] -> cloud prep -> rollout -> SDF -> block partials ->
+// [all-gather] -> merge/update/validation rollout -> validation SDF -> finalize.
+exm_status enqueue_step(exm_handle* h, bool draw_noise, const EventPair* ev, cudaStream_t s,
+                        bool capturing) {
+  const StepConst& sc = h->sc;
+  int launches = 0;
+  if (draw_noise) {
+    EXM_CUDA(launch_noise(sc, h->d_dyn, h->d_eps, s));
+    ++launches;
+  }
+  EXM_CUDA(launch_cloud_prep(h->d_pts, h->d_mask, h->d_dyn, h->fp.radius, h->d_tmp, h->d_cloud,
+                             h->d_cell_start, h->d_grid, s));
+  EXM_CUDA(launch_rollout(sc, h->d_dyn, h->d_nominal, h->d_guide, h->guide_cap, h->d_eps,
+                          h->d_poses, h->d_base, nullptr, nullptr, s));
+  if (ev) EXM_CUDA(capturing ? cudaEventRecordWithFlags(ev->a, s, cudaEventRecordExternal)
+                             : cudaEventRecord(ev->a, s));
+  EXM_CUDA(launch_sdf_grid(h->fp, h->d_poses, sc.k_local * sc.T, h->d_grid, h->d_cell_start,
+                           h->d_cloud, h->d_dmin, s));
+  if (ev) EXM_CUDA(capturing ? cudaEventRecordWithFlags(ev->b, s, cudaEventRecordExternal)
+                             : cudaEventRecord(ev->b, s));
+  EXM_CUDA(launch_block_partials(sc, h->d_base, h->d_dmin, h->d_eps, h->d_partials, nullptr,
+                                 nullptr, s));
+  launches += 4;
+  if (h->world > 1) {
+    const size_t count = static_cast<size_t>(sc.nblocks_local) * partial_stride(sc.T, sc.D);
+    const int rc = g_nccl.allgather(h->d_partials + static_cast<size_t>(sc.block_offset) *
+                                                        partial_stride(sc.T, sc.D),
+                                    h->d_partials, count, kNcclDouble, h->comm, s);
+    if (rc != 0)
+      return fail(EXM_ERR_NCCL, std::string("ncclAllGather: ") + (g_nccl.errstr ? g_nccl.errstr(rc) : "error"));
+  }
+  EXM_CUDA(launch_update(sc, h->d_partials, h->d_nominal, h->d_dyn, h->d_guide, h->guide_cap,
+                         h->d_upd, h->d_val_poses, h->d_val_base, out_dec(h), 1, s));
+  EXM_CUDA(launch_sdf_grid(h->fp, h->d_val_poses, sc.T, h->d_grid, h->d_cell_start, h->d_cloud,
+                           h->d_val_dmin, s));
+  EXM_CUDA(launch_finalize(sc, h->d_val_dmin, h->d_val_base, h->d_upd, h->d_nominal, h->d_dyn,
+                           out_dec(h), out_dmin(h), out_nominal(h), out_uprev(h), 1, s));
+  launches += 3;
+  h->launches_per_step = launches;
+  return EXM_OK;
+}
+
+exm_status ensure_graph(exm_handle* h, int variant) {
+  if (h->exec[variant]) return EXM_OK;
+  cudaGraph_t g = nullptr;
+  EXM_CUDA(cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeThreadLocal));
+  exm_status st = enqueue_step(h, variant == 0, &h->graph_ev, h->stream, true);
+  cudaError_t ce = cudaStreamEndCapture(h->stream, &g);
+  if (st != EXM_OK) {
+    if (g) cudaGraphDestroy(g);
+    return st;
+  }
+  if (ce != cudaSuccess) return fail(EXM_ERR_CUDA, std::string("capture: ") + cudaGetErrorString(ce));
+  size_t nn = 0;
+  EXM_CUDA(cudaGraphGetNodes(g, nullptr, &nn));
+  std::vector<cudaGraphNode_t> nodes(nn);
+  EXM_CUDA(cudaGraphGetNodes(g, nodes.data(), &nn));
+  cudaGraphExec_t exec = nullptr;
+  EXM_CUDA(cudaGraphInstantiate(&exec, g, 0));
+  for (auto n : nodes) {
+    cudaGraphNodeType t;
+    EXM_CUDA(cudaGraphNodeGetType(n, &t));
+    if (t != cudaGraphNodeTypeEventRecord) continue;
+    cudaEvent_t e;
+    EXM_CUDA(cudaGraphEventRecordNodeGetEvent(n, &e));
+    if (e == h->graph_ev.a) h->ev_node[variant][0] = n;
+    if (e == h->graph_ev.b) h->ev_node[variant][1] = n;
+  }
+  cudaGraphDestroy(g);
+  h->exec[variant] = exec;
+  return EXM_OK;
+}
+
+exm_status launch_graph(exm_handle* h, int variant, const EventPair& ev) {
+  exm_status st = ensure_graph(h, variant);
+  if (st != EXM_OK) return st;
+  if (h->ev_node[variant][0]) {
+    EXM_CUDA(cudaGraphExecEventRecordNodeSetEvent(h->exec[variant], h->ev_node[variant][0], ev.a));
+    EXM_CUDA(cudaGraphExecEventRecordNodeSetEvent(h->exec[variant], h->ev_node[variant][1], ev.b));
+  }
+  EXM_CUDA(cudaGraphLaunch(h->exec[variant], h->stream));
+  return EXM_OK;
+}
+
+exm_status ensure_ring(exm_handle* h, int n) {
+  while (static_cast<int>(h->ring.size()) < n) {
+    EventPair p;
+    EXM_CUDA(cudaEventCreate(&p.a));
+    EXM_CUDA(cudaEventCreate(&p.b));
+    h->ring.push_back(p);
+  }
+  return EXM_OK;
+}
+
+exm_status check_cloud(const exm_handle* h, const double* pts, int32_t n) {
+  if (n < 0 || n > h->n_cap) return fail(EXM_ERR_INVALID_ARGUMENT, "point count exceeds obstacle-set capacity");
+  if (n > 0 && !pts) return fail(EXM_ERR_INVALID_ARGUMENT, "points pointer is null");
+  return EXM_OK;
+}
+
+exm_status check_guide(const exm_handle* h, const double* g, int32_t n) {
+  if (n < 1 || !g) return fail(EXM_ERR_INVALID_ARGUMENT, "guidance polyline is empty");
+  if (n > h->guide_cap) return fail(EXM_ERR_INVALID_ARGUMENT, "guidance polyline exceeds guide_cap");
+  return EXM_OK;
+}
+
+// Stage the per-step inputs into pinned memory and enqueue their H2D copies.
+exm_status upload_inputs(exm_handle* h, const double q0[3], const double* pts, const uint8_t* mask,
+                         int32_t n, const double* guide, int32_t ng, const double goal[3],
+                         const double* nominal, const double* u_prev, uint64_t cycle) {
+  exm_status st = check_cloud(h, pts, n);
+  if (st != EXM_OK) return st;
+  st = check_guide(h, guide, ng);
+  if (st != EXM_OK) return st;
+  if (!q0 || !goal || !nominal || !u_prev) return fail(EXM_ERR_INVALID_ARGUMENT, "null input pointer");
+  StepDyn& d = *h->h_dyn;
+  for (int i = 0; i < 3; ++i) {
+    d.q0[i] = q0[i];
+    d.goal[i] = goal[i];
+    d.u_prev[i] = i < h->D ? u_prev[i] : 0.0;
+  }
+  d.cycle = cycle;
+  d.n_points = n;
+  d.n_guide = ng;
+  d.use_mask = mask ? 1 : 0;
+  d.reserved = 0;
+  const size_t TD = static_cast<size_t>(h->T) * h->D;
+  std::memcpy(h->h_nominal, nominal, TD * sizeof(double));
+  std::memcpy(h->h_guide, guide, 2 * static_cast<size_t>(ng) * sizeof(double));
+  if (n > 0) std::memcpy(h->h_pts, pts, 2 * static_cast<size_t>(n) * sizeof(double));
+  if (mask && n > 0) std::memcpy(h->h_mask, mask, static_cast<size_t>(n));
+  cudaStream_t s = h->stream;
+  EXM_CUDA(cudaMemcpyAsync(h->d_dyn, h->h_dyn, sizeof(StepDyn), cudaMemcpyHostToDevice, s));
+  EXM_CUDA(cudaMemcpyAsync(h->d_nominal, h->h_nominal, TD * sizeof(double), cudaMemcpyHostToDevice, s));
+  EXM_CUDA(cudaMemcpyAsync(h->d_guide, h->h_guide, 2 * static_cast<size_t>(ng) * sizeof(double),
+                           cudaMemcpyHostToDevice, s));
+  if (n > 0)
+    EXM_CUDA(cudaMemcpyAsync(h->d_pts, h->h_pts, 2 * static_cast<size_t>(n) * sizeof(double),
+                             cudaMemcpyHostToDevice, s));
+  if (mask && n > 0)
+    EXM_CUDA(cudaMemcpyAsync(h->d_mask, h->h_mask, static_cast<size_t>(n), cudaMemcpyHostToDevice, s));
+  return EXM_OK;
+}
+
+exm_status upload_eps(exm_handle* h, const double* eps) {
+  const size_t row = static_cast<size_t>(h->T) * h->D;
+  EXM_CUDA(cudaMemcpyAsync(h->d_eps, eps + static_cast<size_t>(h->sc.r_offset) * row,
+                           static_cast<size_t>(h->sc.k_local) * row * sizeof(double),
+                           cudaMemcpyHostToDevice, h->stream));
+  return EXM_OK;
+}
+
+void unpack_decision(exm_handle* h, exm_decision* out, double* nominal_out, double* u_prev_out) {
+  const DecisionDev* d = reinterpret_cast<const DecisionDev*>(h->h_out);
+  const double* dmin = reinterpret_cast<const double*>(h->h_out + sizeof(DecisionDev));
+  const double* nom = dmin + h->T;
+  const double* up = nom + h->T * h->D;
+  if (out) {
+    for (int i = 0; i < 3; ++i) out->command[i] = d->command[i];
+    out->validated = d->validated;
+    out->argmin = d->argmin;
+    out->best_cost = d->best_cost;
+    out->weight_entropy = d->entropy;
+    out->nominal_cost = d->nominal_cost;
+    if (out->nominal_dmin) std::memcpy(out->nominal_dmin, dmin, sizeof(double) * h->T);
+  }
+  if (nominal_out) std::memcpy(nominal_out, nom, sizeof(double) * h->T * h->D);
+  if (u_prev_out)
+    for (int i = 0; i < h->D; ++i) u_prev_out[i] = up[i];
+}
+
+exm_status ensure_sdf_workspace(exm_handle* h, int P, int N, bool pairs) {
+  if (P > h->sb_poses_cap) {
+    cudaFree(h->sb_poses);
+    cudaFree(h->sb_keys);
+    cudaFree(h->sb_min);
+    EXM_CUDA(dalloc(&h->sb_poses, P));
+    EXM_CUDA(dalloc(&h->sb_keys, P));
+    EXM_CUDA(dalloc(&h->sb_min, P));
+    h->sb_poses_cap = P;
+  }
+  if (N > h->sb_points_cap) {
+    cudaFree(h->sb_pts64);
+    cudaFree(h->sb_pts);
+    cudaFree(h->sb_mask);
+    EXM_CUDA(dalloc(&h->sb_pts64, 2 * static_cast<size_t>(N)));
+    EXM_CUDA(dalloc(&h->sb_pts, N));
+    EXM_CUDA(dalloc(&h->sb_mask, N));
+    h->sb_points_cap = N;
+  }
+  const size_t np = static_cast<size_t>(P) * N;
+  if (pairs && np > h->sb_pairs_cap) {
+    cudaFree(h->sb_pairs);
+    EXM_CUDA(dalloc(&h->sb_pairs, np));
+    h->sb_pairs_cap = np;
+  }
+  return EXM_OK;
+}
+
+exm_status sdf_enqueue(exm_handle* h, bool pairs, const EventPair* ev) {
+  cudaStream_t s = h->stream;
+  EXM_CUDA(launch_fill_u32(h->sb_keys, 0xffffffffu, h->sb_P, s));
+  if (ev) EXM_CUDA(cudaEventRecord(ev->a, s));
+  EXM_CUDA(launch_sdf_pairs(h->fp, h->sb_poses, h->sb_P, h->sb_pts,
+                            h->sb_has_mask ? h->sb_mask : nullptr, h->sb_N,
+                            pairs ? h->sb_pairs : nullptr, h->sb_keys, s));
+  if (ev) EXM_CUDA(cudaEventRecord(ev->b, s));
+  EXM_CUDA(launch_min_keys_to_double(h->sb_keys, h->sb_P, h->sb_min, s));
+  return EXM_OK;
+}
+
+}  // namespace
+
+// =========================================================================== C ABI
+extern "C" {
+
+int32_t exm_abi_version(void) { return EXM_ABI_VERSION; }
+
+const char* exm_last_error(void) { return g_err.c_str(); }
+
+exm_status exm_create(const exm_footprint* footprint, const exm_model* model,
+                      const exm_limits* limits, const exm_params* params, int32_t n_cap,
+                      int32_t guide_cap, int32_t device, exm_handle** out) {
+  if (!out) return fail(EXM_ERR_INVALID_ARGUMENT, "out handle pointer is null");
+  *out = nullptr;
+  if (!model || !limits || !params) return fail(EXM_ERR_INVALID_ARGUMENT, "null argument");
+  FpDev fp;
+  exm_status st = build_footprint(footprint, &fp);
+  if (st != EXM_OK) return st;
+  const int D = model_dim(model->tag);
+  if (D == 0) return fail(EXM_ERR_INVALID_ARGUMENT, "unknown motion model");
+  if (model->tag == EXM_MODEL_ACKERMANN && model->wheelbase <= 0.0)
+    return fail(EXM_ERR_INVALID_ARGUMENT, "ackermann wheelbase must be positive");
+  st = check_params(params);
+  if (st != EXM_OK) return st;
+  if (n_cap < 0 || guide_cap < 1) return fail(EXM_ERR_INVALID_ARGUMENT, "bad capacity");
+
+  int dev = device;
+  if (dev < 0) EXM_CUDA(cudaGetDevice(&dev));
+  EXM_CUDA(cudaSetDevice(dev));
+  auto* h = new exm_handle();
+  h->device = dev;
+  h->fp = fp;
+  h->K = params->rollouts;
+  h->T = params->horizon;
+  h->D = D;
+  h->n_cap = n_cap;
+  h->guide_cap = guide_cap;
+  StepConst& sc = h->sc;
+  std::memset(&sc, 0, sizeof sc);
+  sc.K = h->K;
+  sc.T = h->T;
+  sc.D = D;
+  sc.tag = model->tag;
+  sc.dt = params->dt;
+  sc.lambda = params->lambda;
+  sc.d_safe = params->d_safe;
+  sc.w_coll = params->w_coll;
+  sc.w_rep = params->w_rep;
+  sc.w_inf = params->w_inf;
+  sc.w_goal_pos = params->w_goal_pos;
+  sc.w_goal_head = params->w_goal_head;
+  sc.w_xtrack = params->w_xtrack;
+  sc.w_progress = params->w_progress;
+  sc.w_ctrl = params->w_ctrl;
+  sc.wheelbase = model->wheelbase;
+  for (int i = 0; i < 3; ++i) {
+    sc.sigma[i] = params->sigma[i];
+    sc.vel_min[i] = limits->vel_min[i];
+    sc.vel_max[i] = limits->vel_max[i];
+    sc.acc_min[i] = limits->acc_min[i];
+    sc.acc_max[i] = limits->acc_max[i];
+  }
+  sc.steer_max = limits->steer_max;
+  sc.seed = params->seed;
+  set_shard(h);
+
+  auto cleanup_fail = [&](exm_status s) {
+    exm_destroy(h);
+    return s;
+  };
+#define EXM_CUDA_C(call)                                                                 \
+  do {                                                                                   \
+    cudaError_t e_ = (call);                                                             \
+    if (e_ != cudaSuccess)                                                               \
+      return cleanup_fail(fail(EXM_ERR_CUDA, std::string(#call) + ": " + cudaGetErrorString(e_))); \
+  } while (0)
+  EXM_CUDA_C(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
+  const size_t KT = static_cast<size_t>(h->K) * h->T;
+  const size_t TD = static_cast<size_t>(h->T) * D;
+  EXM_CUDA_C(dalloc(&h->d_dyn, 1));
+  EXM_CUDA_C(dalloc(&h->d_nominal, TD));
+  EXM_CUDA_C(dalloc(&h->d_guide, 2 * static_cast<size_t>(guide_cap)));
+  EXM_CUDA_C(dalloc(&h->d_pts, 2 * static_cast<size_t>(n_cap)));
+  EXM_CUDA_C(dalloc(&h->d_mask, static_cast<size_t>(n_cap)));
+  EXM_CUDA_C(dalloc(&h->d_tmp, static_cast<size_t>(n_cap)));
+  EXM_CUDA_C(dalloc(&h->d_cloud, static_cast<size_t>(n_cap)));
+  EXM_CUDA_C(dalloc(&h->d_cell_start, static_cast<size_t>(kGridMax) * kGridMax + 1));
+  EXM_CUDA_C(dalloc(&h->d_grid, 1));
+  EXM_CUDA_C(dalloc(&h->d_eps, KT * D));
+  EXM_CUDA_C(dalloc(&h->d_poses, KT));
+  EXM_CUDA_C(dalloc(&h->d_base, static_cast<size_t>(h->K)));
+  EXM_CUDA_C(dalloc(&h->d_dmin, KT));
+  const size_t nblocks_max = (static_cast<size_t>(h->K) + kBlockRollouts - 1) / kBlockRollouts + 8;
+  EXM_CUDA_C(dalloc(&h->d_partials, nblocks_max * partial_stride(h->T, D)));
+  EXM_CUDA_C(dalloc(&h->d_upd, TD));
+  EXM_CUDA_C(dalloc(&h->d_val_poses, static_cast<size_t>(h->T)));
+  EXM_CUDA_C(dalloc(&h->d_val_base, 1));
+  EXM_CUDA_C(dalloc(&h->d_val_dmin, static_cast<size_t>(h->T)));
+  h->out_bytes = sizeof(DecisionDev) + sizeof(double) * (h->T + TD + 3);
+  EXM_CUDA_C(dalloc(&h->d_out, h->out_bytes));
+  EXM_CUDA_C(cudaMemset(h->d_out, 0, h->out_bytes));
+  EXM_CUDA_C(halloc(&h->h_dyn, 1));
+  EXM_CUDA_C(halloc(&h->h_nominal, TD));
+  EXM_CUDA_C(halloc(&h->h_guide, 2 * static_cast<size_t>(guide_cap)));
+  EXM_CUDA_C(halloc(&h->h_pts, 2 * static_cast<size_t>(n_cap)));
+  EXM_CUDA_C(halloc(&h->h_mask, static_cast<size_t>(n_cap)));
+  EXM_CUDA_C(halloc(&h->h_out, h->out_bytes));
+  EXM_CUDA_C(cudaEventCreate(&h->graph_ev.a));
+  EXM_CUDA_C(cudaEventCreate(&h->graph_ev.b));
+  EXM_CUDA_C(cudaEventCreate(&h->step_ev.a));
+  EXM_CUDA_C(cudaEventCreate(&h->step_ev.b));
+#undef EXM_CUDA_C
+  *out = h;
+  return EXM_OK;
+}
+
+void exm_destroy(exm_handle* h) {
+  if (!h) return;
+  cudaSetDevice(h->device);
+  if (h->stream) cudaStreamSynchronize(h->stream);
+  destroy_graphs(h);
+  if (h->comm && g_nccl.destroy) g_nccl.destroy(h->comm);
+  void* dev[] = {h->d_dyn, h->d_nominal, h->d_guide, h->d_pts, h->d_mask, h->d_tmp, h->d_cloud,
+                 h->d_cell_start, h->d_grid, h->d_eps, h->d_poses, h->d_base, h->d_dmin,
+                 h->d_partials, h->d_upd, h->d_val_poses, h->d_val_base, h->d_val_dmin, h->d_out,
+                 h->d_controls, h->d_states, h->d_cost, h->d_unsafe, h->sb_poses, h->sb_pts64,
+                 h->sb_pts, h->sb_mask, h->sb_keys, h->sb_min, h->sb_pairs};
+  for (void* p : dev)
+    if (p) cudaFree(p);
+  void* host[] = {h->h_dyn, h->h_nominal, h->h_guide, h->h_pts, h->h_mask, h->h_out};
+  for (void* p : host)
+    if (p) cudaFreeHost(p);
+  for (auto& p : h->ring) {
+    cudaEventDestroy(p.a);
+    cudaEventDestroy(p.b);
+  }
+  EventPair* evs[] = {&h->graph_ev, &h->step_ev};
+  for (auto* p : evs) {
+    if (p->a) cudaEventDestroy(p->a);
+    if (p->b) cudaEventDestroy(p->b);
+  }
+  if (h->stream) cudaStreamDestroy(h->stream);
+  delete h;
+}
+
+exm_status exm_control_cycle(exm_handle* h, const double q0[3], const double* pts_xy,
+                             const uint8_t* mask, int32_t n_points, const double* guide_xy,
+                             int32_t n_guide, const double goal[3], double* nominal_inout,
+                             double* u_prev_inout, uint64_t cycle, const double* eps_or_null,
+                             exm_decision* out) {
+  if (!h) return fail(EXM_ERR_INVALID_ARGUMENT, "handle is null");
+  if (!nominal_inout || !u_prev_inout) return fail(EXM_ERR_INVALID_ARGUMENT, "null state pointer");
+  EXM_CUDA(cudaSetDevice(h->device));
+  exm_status st = upload_inputs(h, q0, pts_xy, mask, n_points, guide_xy, n_guide, goal,
+                                nominal_inout, u_prev_inout, cycle);
+  if (st != EXM_OK) return st;
+  if (eps_or_null) {
+    st = upload_eps(h, eps_or_null);
+    if (st != EXM_OK) return st;
+  }
+  st = launch_graph(h, eps_or_null ? 1 : 0, h->step_ev);
+  if (st != EXM_OK) return st;
+  EXM_CUDA(cudaMemcpyAsync(h->h_out, h->d_out, h->out_bytes, cudaMemcpyDeviceToHost, h->stream));
+  EXM_CUDA(cudaStreamSynchronize(h->stream));
+  h->last_steps = 1;
+  h->ring_used = 0;
+  h->last_pairs = static_cast<int64_t>(h->sc.k_local) * h->T * n_points;
+  unpack_decision(h, out, nominal_inout, u_prev_inout);
+  return EXM_OK;
+}
+
+exm_status exm_evaluate_rollouts(exm_handle* h, const double q0[3], const double* nominal,
+                                 const double* eps, const double* pts_xy, const uint8_t* mask,
+                                 int32_t n_points, const double* guide_xy, int32_t n_guide,
+                                 const double goal[3], const double* u_prev,
+                                 double* controls_out, double* states_out, double* dmin_out,
+                                 double* costs_out, uint8_t* unsafe_out) {
+  if (!h) return fail(EXM_ERR_INVALID_ARGUMENT, "handle is null");
+  if (h->world > 1) return fail(EXM_ERR_UNSUPPORTED, "evaluate_rollouts on a sharded handle");
+  if (!eps) return fail(EXM_ERR_INVALID_ARGUMENT, "perturbation array does not match K*T");
+  EXM_CUDA(cudaSetDevice(h->device));
+  exm_status st = upload_inputs(h, q0, pts_xy, mask, n_points, guide_xy, n_guide, goal, nominal,
+                                u_prev, 0);
+  if (st != EXM_OK) return st;
+  st = upload_eps(h, eps);
+  if (st != EXM_OK) return st;
+  const size_t KT = static_cast<size_t>(h->K) * h->T;
+  if (controls_out && !h->d_controls) EXM_CUDA(dalloc(&h->d_controls, KT * h->D));
+  if (states_out && !h->d_states) EXM_CUDA(dalloc(&h->d_states, static_cast<size_t>(h->K) * (h->T + 1) * 3));
+  if (!h->d_cost) EXM_CUDA(dalloc(&h->d_cost, static_cast<size_t>(h->K)));
+  if (!h->d_unsafe) EXM_CUDA(dalloc(&h->d_unsafe, static_cast<size_t>(h->K)));
+  cudaStream_t s = h->stream;
+  const StepConst& sc = h->sc;
+  EXM_CUDA(launch_cloud_prep(h->d_pts, h->d_mask, h->d_dyn, h->fp.radius, h->d_tmp, h->d_cloud,
+                             h->d_cell_start, h->d_grid, s));
+  EXM_CUDA(launch_rollout(sc, h->d_dyn, h->d_nominal, h->d_guide, h->guide_cap, h->d_eps,
+                          h->d_poses, h->d_base, controls_out ? h->d_controls : nullptr,
+                          states_out ? h->d_states : nullptr, s));
+  EXM_CUDA(launch_sdf_grid(h->fp, h->d_poses, static_cast<int>(KT), h->d_grid, h->d_cell_start,
+                           h->d_cloud, h->d_dmin, s));
+  EXM_CUDA(launch_block_partials(sc, h->d_base, h->d_dmin, h->d_eps, nullptr, h->d_cost,
+                                 h->d_unsafe, s));
+  if (controls_out)
+    EXM_CUDA(cudaMemcpyAsync(controls_out, h->d_controls, KT * h->D * sizeof(double), cudaMemcpyDeviceToHost, s));
+  if (states_out)
+    EXM_CUDA(cudaMemcpyAsync(states_out, h->d_states, static_cast<size_t>(h->K) * (h->T + 1) * 3 * sizeof(double),
+                             cudaMemcpyDeviceToHost, s));
+  std::vector<float> dmin_f;
+  if (dmin_out) {
+    dmin_f.resize(KT);
+    EXM_CUDA(cudaMemcpyAsync(dmin_f.data(), h->d_dmin, KT * sizeof(float), cudaMemcpyDeviceToHost, s));
+  }
+  if (costs_out)
+    EXM_CUDA(cudaMemcpyAsync(costs_out, h->d_cost, h->K * sizeof(double), cudaMemcpyDeviceToHost, s));
+  if (unsafe_out)
+    EXM_CUDA(cudaMemcpyAsync(unsafe_out, h->d_unsafe, h->K, cudaMemcpyDeviceToHost, s));
+  EXM_CUDA(cudaStreamSynchronize(s));
+  if (dmin_out)
+    for (size_t i = 0; i < KT; ++i) dmin_out[i] = static_cast<double>(dmin_f[i]);
+  return EXM_OK;
+}
+
+exm_status exm_sample_perturbations(exm_handle* h, uint64_t seed, uint64_t cycle, double* eps_out) {
+  if (!h || !eps_out) return fail(EXM_ERR_INVALID_ARGUMENT, "null argument");
+  if (h->world > 1) return fail(EXM_ERR_UNSUPPORTED, "sample_perturbations on a sharded handle");
+  EXM_CUDA(cudaSetDevice(h->device));
+  StepConst sc = h->sc;
+  sc.seed = seed;
+  h->h_dyn->cycle = cycle;
+  EXM_CUDA(cudaMemcpyAsync(h->d_dyn, h->h_dyn, sizeof(StepDyn), cudaMemcpyHostToDevice, h->stream));
+  EXM_CUDA(launch_noise(sc, h->d_dyn, h->d_eps, h->stream));
+  const size_t n = static_cast<size_t>(h->K) * h->T * h->D;
+  EXM_CUDA(cudaMemcpyAsync(eps_out, h->d_eps, n * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+  EXM_CUDA(cudaStreamSynchronize(h->stream));
+  return EXM_OK;
+}
+
+exm_status exm_validate_nominal(exm_handle* h, const double* nominal, const double q0[3],
+                                const double* pts_xy, const uint8_t* mask, int32_t n_points,
+                                const double* guide_xy, int32_t n_guide, const double goal[3],
+                                const double* u_prev, int32_t* valid_out, double* dmin_out,
+                                double* cost_out) {
+  if (!h) return fail(EXM_ERR_INVALID_ARGUMENT, "handle is null");
+  EXM_CUDA(cudaSetDevice(h->device));
+  exm_status st = upload_inputs(h, q0, pts_xy, mask, n_points, guide_xy, n_guide, goal, nominal,
+                                u_prev, 0);
+  if (st != EXM_OK) return st;
+  cudaStream_t s = h->stream;
+  const StepConst& sc = h->sc;
+  EXM_CUDA(launch_cloud_prep(h->d_pts, h->d_mask, h->d_dyn, h->fp.radius, h->d_tmp, h->d_cloud,
+                             h->d_cell_start, h->d_grid, s));
+  EXM_CUDA(launch_update(sc, nullptr, h->d_nominal, h->d_dyn, h->d_guide, h->guide_cap, h->d_upd,
+                         h->d_val_poses, h->d_val_base, out_dec(h), 0, s));
+  EXM_CUDA(launch_sdf_grid(h->fp, h->d_val_poses, sc.T, h->d_grid, h->d_cell_start, h->d_cloud,
+                           h->d_val_dmin, s));
+  EXM_CUDA(launch_finalize(sc, h->d_val_dmin, h->d_val_base, h->d_upd, h->d_nominal, h->d_dyn,
+                           out_dec(h), out_dmin(h), nullptr, nullptr, 0, s));
+  EXM_CUDA(cudaMemcpyAsync(h->h_out, h->d_out, h->out_bytes, cudaMemcpyDeviceToHost, s));
+  EXM_CUDA(cudaStreamSynchronize(s));
+  const DecisionDev* d = reinterpret_cast<const DecisionDev*>(h->h_out);
+  if (valid_out) *valid_out = d->validated;
+  if (cost_out) *cost_out = d->nominal_cost;
+  if (dmin_out) std::memcpy(dmin_out, h->h_out + sizeof(DecisionDev), sizeof(double) * h->T);
+  return EXM_OK;
+}
+
+exm_status exm_sdf_stage(exm_handle* h, const double* poses, int32_t n_poses,
+                         const double* pts_xy, const uint8_t* mask, int32_t n_points) {
+  if (!h) return fail(EXM_ERR_INVALID_ARGUMENT, "handle is null");
+  if (n_poses < 0 || n_points < 0 || (n_poses > 0 && !poses) || (n_points > 0 && !pts_xy))
+    return fail(EXM_ERR_INVALID_ARGUMENT, "bad pose/point arrays");
+  EXM_CUDA(cudaSetDevice(h->device));
+  exm_status st = ensure_sdf_workspace(h, std::max(n_poses, 1), std::max(n_points, 1), false);
+  if (st != EXM_OK) return st;
+  // Recentre poses and points at the poses' centroid in FP64, then round (Appendix B).
+  double cx = 0.0, cy = 0.0;
+  for (int p = 0; p < n_poses; ++p) {
+    cx += poses[3 * p];
+    cy += poses[3 * p + 1];
+  }
+  if (n_poses > 0) {
+    cx /= n_poses;
+    cy /= n_poses;
+  }
+  std::vector<float4> q(static_cast<size_t>(n_poses));
+  for (int p = 0; p < n_poses; ++p) {
+    const double th = poses[3 * p + 2];
+    q[p] = make_float4(static_cast<float>(poses[3 * p] - cx), static_cast<float>(poses[3 * p + 1] - cy),
+                       static_cast<float>(std::cos(th)), static_cast<float>(std::sin(th)));
+  }
+  cudaStream_t s = h->stream;
+  if (n_poses > 0)
+    EXM_CUDA(cudaMemcpyAsync(h->sb_poses, q.data(), q.size() * sizeof(float4), cudaMemcpyHostToDevice, s));
+  if (n_points > 0)
+    EXM_CUDA(cudaMemcpyAsync(h->sb_pts64, pts_xy, 2 * static_cast<size_t>(n_points) * sizeof(double),
+                             cudaMemcpyHostToDevice, s));
+  if (mask && n_points > 0)
+    EXM_CUDA(cudaMemcpyAsync(h->sb_mask, mask, static_cast<size_t>(n_points), cudaMemcpyHostToDevice, s));
+  EXM_CUDA(launch_recentre(h->sb_pts64, n_points, cx, cy, h->sb_pts, s));
+  EXM_CUDA(cudaStreamSynchronize(s));  // q is a stack vector
+  h->sb_P = n_poses;
+  h->sb_N = n_points;
+  h->sb_has_mask = mask ? 1 : 0;
+  return EXM_OK;
+}
+
+exm_status exm_sdf_run_resident(exm_handle* h, int32_t n_steps, int32_t want_pairs) {
+  if (!h) return fail(EXM_ERR_INVALID_ARGUMENT, "handle is null");
+  EXM_CUDA(cudaSetDevice(h->device));
+  exm_status st = ensure_sdf_workspace(h, std::max(h->sb_P, 1), std::max(h->sb_N, 1), want_pairs != 0);
+  if (st != EXM_OK) return st;
+  st = ensure_ring(h, h->ring_used + n_steps);
+  if (st != EXM_OK) return st;
+  for (int i = 0; i < n_steps; ++i) {
+    st = sdf_enqueue(h, want_pairs != 0, &h->ring[h->ring_used + i]);
+    if (st != EXM_OK) return st;
+  }
+  h->ring_used += n_steps;
+  h->last_steps = n_steps;
+  h->sb_last_pairs = want_pairs != 0;
+  h->launches_per_step = 3;
+  h->last_pairs = static_cast<int64_t>(h->sb_P) * h->sb_N;
+  return EXM_OK;
+}
+
+exm_status exm_sdf_read(exm_handle* h, float* per_pair, double* per_pose_min) {
+  if (!h) return fail(EXM_ERR_INVALID_ARGUMENT, "handle is null");
+  EXM_CUDA(cudaSetDevice(h->device));
+  cudaStream_t s = h->stream;
+  if (per_pair) {
+    if (!h->sb_last_pairs) return fail(EXM_ERR_INVALID_ARGUMENT, "per-pair output was not computed");
+    EXM_CUDA(cudaMemcpyAsync(per_pair, h->sb_pairs, static_cast<size_t>(h->sb_P) * h->sb_N * sizeof(float),
+                             cudaMemcpyDeviceToHost, s));
+  }
+  if (per_pose_min)
+    EXM_CUDA(cudaMemcpyAsync(per_pose_min, h->sb_min, static_cast<size_t>(h->sb_P) * sizeof(double),
+                             cudaMemcpyDeviceToHost, s));
+  EXM_CUDA(cudaStreamSynchronize(s));
+  return EXM_OK;
+}
+
+exm_status exm_sdf_batch(exm_handle* h, const double* poses, int32_t n_poses,
+                         const double* pts_xy, const uint8_t* mask, int32_t n_points,
+                         float* per_pair, double* per_pose_min) {
+  exm_status st = exm_sdf_stage(h, poses, n_poses, pts_xy, mask, n_points);
+  if (st != EXM_OK) return st;
+  st = exm_sdf_run_resident(h, 1, per_pair != nullptr);
+  if (st != EXM_OK) return st;
+  return exm_sdf_read(h, per_pair, per_pose_min);
+}
+
+exm_status exm_batch_signed_distance(exm_handle* h, const double* queries, int32_t n, double* out) {
+  if (!h || (n > 0 && (!queries || !out))) return fail(EXM_ERR_INVALID_ARGUMENT, "null argument");
+  if (n == 0) return EXM_OK;
+  const double identity[3] = {0.0, 0.0, 0.0};
+  std::vector<float> tmp(static_cast<size_t>(n));
+  exm_status st = exm_sdf_batch(h, identity, 1, queries, nullptr, n, tmp.data(), nullptr);
+  if (st != EXM_OK) return st;
+  for (int i = 0; i < n; ++i) out[i] = static_cast<double>(tmp[i]);
+  return EXM_OK;
+}
+
+exm_status exm_nccl_unique_id(uint8_t id_out[128]) {
+  if (!id_out) return fail(EXM_ERR_INVALID_ARGUMENT, "null id buffer");
+  if (!g_nccl.load()) return fail(EXM_ERR_NCCL, "libnccl.so.2 not loadable");
+  nccl_uid_t id;
+  const int rc = g_nccl.get_uid(&id);
+  if (rc != 0) return fail(EXM_ERR_NCCL, "ncclGetUniqueId failed");
+  std::memcpy(id_out, id.internal, 128);
+  return EXM_OK;
+}
+
+exm_status exm_attach_comm(exm_handle* h, int32_t rank, int32_t world, const uint8_t id[128]) {
+  if (!h) return fail(EXM_ERR_INVALID_ARGUMENT, "handle is null");
+  if (world < 1 || rank < 0 || rank >= world) return fail(EXM_ERR_INVALID_ARGUMENT, "bad rank/world");
+  if (h->K % (world * kBlockRollouts) != 0 && world > 1)
+    return fail(EXM_ERR_INVALID_ARGUMENT, "rollouts must be a multiple of 256 * world for sharding");
+  EXM_CUDA(cudaSetDevice(h->device));
+  EXM_CUDA(cudaStreamSynchronize(h->stream));
+  destroy_graphs(h);
+  if (h->comm && g_nccl.destroy) {
+    g_nccl.destroy(h->comm);
+    h->comm = nullptr;
+  }
+  h->rank = rank;
+  h->world = world;
+  if (world > 1) {
+    if (!id) return fail(EXM_ERR_INVALID_ARGUMENT, "null id");
+    if (!g_nccl.load()) return fail(EXM_ERR_NCCL, "libnccl.so.2 not loadable");
+    nccl_uid_t uid;
+    std::memcpy(uid.internal, id, 128);
+    const int rc = g_nccl.init_rank(&h->comm, world, uid, rank);
+    if (rc != 0) return fail(EXM_ERR_NCCL, "ncclCommInitRank failed");
+  }
+  set_shard(h);
+  return EXM_OK;
+}
+
+exm_status exm_stage_inputs(exm_handle* h, const double q0[3], const double* pts_xy,
+                            const uint8_t* mask, int32_t n_points, const double* guide_xy,
+                            int32_t n_guide, const double goal[3], const double* nominal,
+                            const double* u_prev, uint64_t cycle) {
+  if (!h) return fail(EXM_ERR_INVALID_ARGUMENT, "handle is null");
+  EXM_CUDA(cudaSetDevice(h->device));
+  exm_status st = upload_inputs(h, q0, pts_xy, mask, n_points, guide_xy, n_guide, goal, nominal,
+                                u_prev, cycle);
+  if (st != EXM_OK) return st;
+  EXM_CUDA(cudaStreamSynchronize(h->stream));
+  return EXM_OK;
+}
+
+exm_status exm_run_resident(exm_handle* h, int32_t n_steps) {
+  if (!h) return fail(EXM_ERR_INVALID_ARGUMENT, "handle is null");
+  EXM_CUDA(cudaSetDevice(h->device));
+  exm_status st = ensure_ring(h, h->ring_used + n_steps);
+  if (st != EXM_OK) return st;
+  for (int i = 0; i < n_steps; ++i) {
+    st = launch_graph(h, 0, h->ring[h->ring_used + i]);
+    if (st != EXM_OK) return st;
+  }
+  h->ring_used += n_steps;
+  h->last_steps = n_steps;
+  h->last_pairs = static_cast<int64_t>(h->sc.k_local) * h->T * h->h_dyn->n_points;
+  return EXM_OK;
+}
+
+exm_status exm_read_resident(exm_handle* h, double* nominal_out, double* u_prev_out, exm_decision* out) {
+  if (!h) return fail(EXM_ERR_INVALID_ARGUMENT, "handle is null");
+  EXM_CUDA(cudaSetDevice(h->device));
+  EXM_CUDA(cudaMemcpyAsync(h->h_out, h->d_out, h->out_bytes, cudaMemcpyDeviceToHost, h->stream));
+  EXM_CUDA(cudaStreamSynchronize(h->stream));
+  unpack_decision(h, out, nominal_out, u_prev_out);
+  return EXM_OK;
+}
+
+void* exm_stream(exm_handle* h) { return h ? static_cast<void*>(h->stream) : nullptr; }
+
+exm_status exm_step_stats(exm_handle* h, int32_t* launches_per_step, float* sdf_ms,
+                          int64_t* sdf_pairs) {
+  if (!h) return fail(EXM_ERR_INVALID_ARGUMENT, "handle is null");
+  EXM_CUDA(cudaSetDevice(h->device));
+  EXM_CUDA(cudaStreamSynchronize(h->stream));
+  float total = 0.0f;
+  int n = 0;
+  if (h->ring_used > 0) {
+    for (int i = 0; i < h->ring_used; ++i) {
+      float ms = 0.0f;
+      EXM_CUDA(cudaEventElapsedTime(&ms, h->ring[i].a, h->ring[i].b));
+      total += ms;
+      ++n;
+    }
+  } else if (h->last_steps > 0) {
+    EXM_CUDA(cudaEventElapsedTime(&total, h->step_ev.a, h->step_ev.b));
+    n = 1;
+  }
+  if (launches_per_step) *launches_per_step = h->launches_per_step;
+  if (sdf_ms) *sdf_ms = n ? total / n : 0.0f;
+  h->ring_used = 0;  // consumed: the next run starts a fresh accumulation
+  if (sdf_pairs) *sdf_pairs = h->last_pairs;
+  return EXM_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,107 @@
+// exm_common.cuh — structs shared by the host side (exm_abi.cu) and the kernels
+// (exm_kernels.cu) of libexm_b200.so. Nothing here crosses the public C ABI.
+#pragma once
+
+#include <cstdint>
+
+#include <cuda_runtime.h>
+
+namespace exm {
+
+constexpr int kMaxEdges = 64;        // polygon edges / cover boxes held in kernel parameters
+constexpr int kBlockRollouts = 256;  // rollouts per softmax partial (fixed: G-invariant)
+constexpr int kGridMax = 128;        // cloud grid cells per axis (<= 16384 cells, smem histogram)
+constexpr float kEmptyDistance = 1e6f;  // kEmptyMaskDistance (geometry.hpp:37)
+constexpr float kCullMargin = 1e-3f;    // conservative slack on every lower-bound cull (m)
+
+// FP32 footprint table, passed by value as a __grid_constant__ kernel parameter so the
+// inner loops read it from the constant bank (uniform datapath), never from memory.
+// Polygon edge b (prepare, geometry.cpp:236-247), recentring-free body frame:
+//   e[b] = {vx, vy, ex, ey, ex/|e|^2, ey/|e|^2, -(v.e)/|e|^2, vy+ey}
+// Box j (geometry.cpp:250-255): e[j] = {cx, cy, hx, hy, 0...}
+struct FpDev {
+  int kind;  // EXM_FOOTPRINT_*
+  int count;
+  float radius;  // PreparedFootprint::bounding_radius (max vertex norm, geometry.cpp:127-131)
+  float reserved;
+  float e[kMaxEdges][8];
+};
+
+// Uniform grid over the recentred valid cloud (written by the prep kernel).
+struct GridMeta {
+  float x0, y0, cs, inv_cs;
+  int gx, gy, n_valid, reserved;
+};
+
+// Per-step small inputs, uploaded with one copy (host API) or kept resident.
+struct StepDyn {
+  double q0[3];
+  double goal[3];
+  double u_prev[3];
+  uint64_t cycle;
+  int32_t n_points;
+  int32_t n_guide;
+  int32_t use_mask;
+  int32_t reserved;
+};
+
+// Model, limits and MPPI parameters (kernel parameter).
+struct StepConst {
+  int K, T, D, tag;
+  int k_local, r_offset;        // this rank's rollout shard [r_offset, r_offset + k_local)
+  int nblocks_local, block_offset, nblocks_total;
+  int reserved;
+  double dt, lambda, d_safe, w_coll, w_rep, w_inf;
+  double w_goal_pos, w_goal_head, w_xtrack, w_progress, w_ctrl, wheelbase;
+  double sigma[3];
+  double vel_min[3], vel_max[3], acc_min[3], acc_max[3];
+  double steer_max;
+  uint64_t seed;
+};
+
+struct DecisionDev {
+  double command[3];
+  int32_t validated;
+  int32_t argmin;
+  double best_cost;
+  double entropy;
+  double nominal_cost;
+  double reserved;
+};
+
+// Softmax partial of one block of kBlockRollouts rollouts:
+//   {beta_b, S_b = sum e, A_b = sum e (J - beta_b)/lambda, argmin_b, U_b[T*D] = sum e eps}
+inline __host__ __device__ int partial_stride(int T, int D) { return 4 + T * D; }
+
+// ---- kernel launchers (exm_kernels.cu) ---------------------------------------------------
+cudaError_t launch_noise(const StepConst& sc, const StepDyn* dyn, double* eps, cudaStream_t s);
+cudaError_t launch_cloud_prep(const double* pts, const uint8_t* mask, const StepDyn* dyn,
+                              float radius, float2* tmp, float2* cloud, int* cell_start,
+                              GridMeta* gm, cudaStream_t s);
+cudaError_t launch_rollout(const StepConst& sc, const StepDyn* dyn, const double* nominal,
+                           const double* guide, int guide_cap, const double* eps, float4* poses,
+                           double* base_cost, double* controls_out, double* states_out,
+                           cudaStream_t s);
+cudaError_t launch_sdf_grid(const FpDev& fp, const float4* poses, int n_poses,
+                            const GridMeta* gm, const int* cell_start, const float2* cloud,
+                            float* out, cudaStream_t s);
+cudaError_t launch_block_partials(const StepConst& sc, const double* base_cost,
+                                  const float* dmin, const double* eps, double* partials,
+                                  double* cost_out, uint8_t* unsafe_out, cudaStream_t s);
+cudaError_t launch_update(const StepConst& sc, const double* partials, const double* nominal,
+                          const StepDyn* dyn, const double* guide, int guide_cap, double* upd,
+                          float4* val_poses, double* val_base, DecisionDev* dec,
+                          int merge, cudaStream_t s);
+cudaError_t launch_finalize(const StepConst& sc, const float* val_dmin, const double* val_base,
+                            const double* upd, double* nominal, StepDyn* dyn, DecisionDev* dec,
+                            double* out_dmin, double* out_nominal, double* out_uprev,
+                            int commit, cudaStream_t s);
+cudaError_t launch_recentre(const double* pts, int n, double cx, double cy, float2* out,
+                            cudaStream_t s);
+cudaError_t launch_sdf_pairs(const FpDev& fp, const float4* poses, int n_poses,
+                             const float2* pts, const uint8_t* mask, int n_points,
+                             float* per_pair, unsigned* pose_min_key, cudaStream_t s);
+cudaError_t launch_min_keys_to_double(const unsigned* keys, int n, double* out, cudaStream_t s);
+cudaError_t launch_fill_u32(unsigned* p, unsigned v, int n, cudaStream_t s);
+
+}  // namespace exm

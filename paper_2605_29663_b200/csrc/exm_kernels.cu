@@ -1,0 +1,978 @@
+// exm_kernels.cu — sm_100a kernels of the EXACT-MPPI rollout + exact signed-distance path.
+//
+// Kernel map (reference function each one replaces, proj/...):
+//   k_noise          sample_perturbations / gaussian_at      controller.cpp:78-96, rng.hpp:12-39
+//   k_cloud_prep     ObstacleSet masking, recentring at q0,  geometry.cpp:357-375 (mask, layout)
+//                    uniform-grid binning for exact culling
+//   k_rollout        score_rollout minus the SDF             controller.cpp:138-174,
+//                    (clamp, Euler step, task/ctrl cost)      kinematics.cpp:75-117
+//   k_sdf_grid       min_signed_distance_at over K*T poses   geometry.cpp:357-375, :260-296
+//   k_block_partials obstacle cost, unsafe flag, augmented  controller.cpp:160-166, :310-318
+//                    cost, min-shifted softmax partials       controller.cpp:222-233, :320-328
+//   k_update         partial merge, weighted update,         controller.cpp:314-340
+//                    sequential clamp, validation rollout     controller.cpp:254-282
+//   k_finalize       validation cost, command, shift / hold  controller.cpp:342-364
+//   k_sdf_pairs      batch_signed_distance (every pair)      geometry.cpp:298-318
+//
+// Numerics: dynamics, costs and the softmax are FP64 (as the reference). The signed
+// distance inner loops are FP32 on coordinates recentred at q0 in FP64 before rounding
+// (SURVEY.md Appendix B).
+#include <cfloat>
+#include <cmath>
+#include <cstdint>
+
+#include "exm_common.cuh"
+
+#define EXM_FOOTPRINT_RECT_COVER 0
+#define EXM_FOOTPRINT_POLYGON 1
+#define EXM_MODEL_DIFF 0
+#define EXM_MODEL_ACKERMANN 1
+#define EXM_MODEL_OMNI 2
+#define EXM_MODEL_SPIN 3
+#define EXM_MODEL_PARALLEL 4
+
+namespace exm {
+namespace {
+
+constexpr double kPi = 3.14159265358979323846;
+constexpr unsigned kFull = 0xffffffffu;
+
+// ------------------------------------------------------------------ counter RNG (rng.hpp)
+__device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
+  x += 0x9E3779B97F4A7C15ull;
+  x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+  x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+  return x ^ (x >> 31);
+}
+__device__ __forceinline__ uint64_t hash_mix(uint64_t h, uint64_t v) {
+  return splitmix64(h ^ (v + 0x9E3779B97F4A7C15ull + (h << 6) + (h >> 2)));
+}
+__device__ __forceinline__ double unit_oc(uint64_t h) {  // (0, 1]
+  return static_cast<double>((h >> 11) + 1) * 0x1.0p-53;
+}
+
+// ------------------------------------------------------------------ FP64 scalar helpers
+// std::min / std::max / std::clamp with libstdc++'s comparison order.
+__device__ __forceinline__ double mn(double a, double b) { return (b < a) ? b : a; }
+__device__ __forceinline__ double mx(double a, double b) { return (a < b) ? b : a; }
+__device__ __forceinline__ double clampd(double v, double lo, double hi) {
+  return (v < lo) ? lo : (hi < v) ? hi : v;
+}
+__device__ __forceinline__ double wrap_angle(double a) {  // geometry.cpp:17-23
+  const double tau = 2.0 * kPi;
+  a = fmod(a, tau);
+  if (a <= -kPi) a += tau;
+  if (a > kPi) a -= tau;
+  return a;
+}
+
+// clamp_control, kinematics.cpp:99-117
+__device__ __forceinline__ void clamp_control(const StepConst& sc, const double* u,
+                                              const double* prev, double* out) {
+  for (int i = 0; i < sc.D; ++i) {
+    double lo = sc.vel_min[i], hi = sc.vel_max[i];
+    if (sc.tag == EXM_MODEL_ACKERMANN && i == 1) {
+      lo = mx(lo, -sc.steer_max);
+      hi = mn(hi, sc.steer_max);
+    }
+    const double v = clampd(u[i], lo, hi);
+    out[i] = clampd(v, prev[i] + sc.acc_min[i] * sc.dt, prev[i] + sc.acc_max[i] * sc.dt);
+  }
+}
+
+// derivative + step, kinematics.cpp:75-97 (cos/sin of the pre-step heading supplied)
+__device__ __forceinline__ void euler_step(const StepConst& sc, double q[3], const double* u,
+                                           double ct, double st) {
+  double fx = 0.0, fy = 0.0, fth = 0.0;
+  switch (sc.tag) {
+    case EXM_MODEL_DIFF: fx = u[0] * ct; fy = u[0] * st; fth = u[1]; break;
+    case EXM_MODEL_ACKERMANN: fx = u[0] * ct; fy = u[0] * st; fth = u[0] / sc.wheelbase * tan(u[1]); break;
+    case EXM_MODEL_OMNI: fx = u[0] * ct - u[1] * st; fy = u[0] * st + u[1] * ct; fth = u[2]; break;
+    case EXM_MODEL_SPIN: fth = u[0]; break;
+    case EXM_MODEL_PARALLEL: fx = -u[0] * st; fy = u[0] * ct; break;
+  }
+  q[0] = q[0] + fx * sc.dt;
+  q[1] = q[1] + fy * sc.dt;
+  q[2] = q[2] + fth * sc.dt;
+}
+
+// project_on_polyline + task_cost, controller.cpp:50-66, :103-118
+__device__ double task_cost(const StepConst& sc, const double q[3], const double* g, int ng,
+                            const double* goal, bool terminal) {
+  const double dx = q[0] - goal[0], dy = q[1] - goal[1];
+  double cost = sc.w_goal_pos * (dx * dx + dy * dy);
+  if (terminal) {
+    const double e = wrap_angle(q[2] - goal[2]);
+    cost += sc.w_goal_head * e * e;
+  }
+  double best_d, best_p = 0.0;
+  if (ng == 1) {
+    const double ax = q[0] - g[0], ay = q[1] - g[1];
+    best_d = sqrt(ax * ax + ay * ay);
+  } else {
+    best_d = HUGE_VAL;
+    double arc = 0.0;
+    for (int i = 0; i + 1 < ng; ++i) {
+      const double ax = g[2 * i], ay = g[2 * i + 1];
+      const double sx = g[2 * i + 2] - ax, sy = g[2 * i + 3] - ay;
+      const double len = sqrt(sx * sx + sy * sy);
+      double t = 0.0;
+      if (len > 0.0) t = clampd(((q[0] - ax) * sx + (q[1] - ay) * sy) / (len * len), 0.0, 1.0);
+      const double ex = q[0] - (ax + t * sx), ey = q[1] - (ay + t * sy);
+      const double d = sqrt(ex * ex + ey * ey);
+      if (d < best_d) {
+        best_d = d;
+        best_p = arc + t * len;
+      }
+      arc += len;
+    }
+  }
+  cost += sc.w_xtrack * best_d * best_d;
+  cost -= sc.w_progress * best_p;
+  return cost;
+}
+
+__device__ __forceinline__ double terminal_cost(const StepConst& sc, const double q[3],
+                                                const double* goal) {  // controller.cpp:120-126
+  const double dx = q[0] - goal[0], dy = q[1] - goal[1];
+  const double e = wrap_angle(q[2] - goal[2]);
+  return sc.w_goal_pos * (dx * dx + dy * dy) + sc.w_goal_head * e * e;
+}
+
+__device__ __forceinline__ double control_cost(const StepConst& sc, const double* u) {
+  double s = 0.0;
+  for (int i = 0; i < sc.D; ++i) s += u[i] * u[i];
+  return sc.w_ctrl * s;
+}
+
+__device__ __forceinline__ double obstacle_cost(const StepConst& sc, double d) {  // :98-101
+  const double m = mx(sc.d_safe - d, 0.0);
+  return sc.w_coll * (d < 0.0 ? 1.0 : 0.0) + sc.w_rep * m * m;
+}
+
+// One rollout of T steps (score_rollout without the SDF): emits recentred FP32 poses for the
+// SDF kernel and returns task + control + terminal cost. eps_row may be null (validation).
+__device__ double rollout_one(const StepConst& sc, const StepDyn& dyn, const double* nominal,
+                              const double* eps_row, const double* g, int ng,
+                              float4* poses_row, double* controls_row, double* states_row) {
+  const int T = sc.T, D = sc.D;
+  double prev[3] = {dyn.u_prev[0], dyn.u_prev[1], dyn.u_prev[2]};
+  double q[3] = {dyn.q0[0], dyn.q0[1], dyn.q0[2]};
+  double base = 0.0;
+  if (states_row) { states_row[0] = q[0]; states_row[1] = q[1]; states_row[2] = q[2]; }
+  for (int h = 0; h < T; ++h) {
+    double u[3] = {0.0, 0.0, 0.0}, uc[3] = {0.0, 0.0, 0.0};
+    for (int c = 0; c < D; ++c) u[c] = nominal[h * D + c] + (eps_row ? eps_row[h * D + c] : 0.0);
+    clamp_control(sc, u, prev, uc);
+    for (int c = 0; c < D; ++c) prev[c] = uc[c];
+    if (controls_row)
+      for (int c = 0; c < D; ++c) controls_row[h * D + c] = uc[c];
+    double st, ct;
+    sincos(q[2], &st, &ct);
+    poses_row[h] = make_float4(static_cast<float>(q[0] - dyn.q0[0]),
+                               static_cast<float>(q[1] - dyn.q0[1]), static_cast<float>(ct),
+                               static_cast<float>(st));
+    base += task_cost(sc, q, g, ng, dyn.goal, false);
+    base += control_cost(sc, uc);
+    euler_step(sc, q, uc, ct, st);
+    if (states_row) {
+      states_row[3 * (h + 1)] = q[0];
+      states_row[3 * (h + 1) + 1] = q[1];
+      states_row[3 * (h + 1) + 2] = q[2];
+    }
+  }
+  return base + terminal_cost(sc, q, dyn.goal);
+}
+
+// ------------------------------------------------------------------ FP32 signed distance
+// Polygon edge step (PreparedFootprint::sd polygon branch, geometry.cpp:273-292).
+//   t  = sat(p.e/|e|^2 - v.e/|e|^2)           2 FFMA (second .SAT)
+//   q  = v + t e - p;  d2 = |q|^2              2 FADD, 2 FFMA, FMUL, FFMA
+//   crossing (division-free): edge counts iff (vy<py) != (vy+ey<py) and
+//   x_cross - px = cross(v-p, e)/ey > 0; with r = v - p the sign bits give
+//   count = (sb(ry) ^ sb(y1-py)) & (sb(ry) ^ sb(cross)).
+__device__ __forceinline__ void poly_edge(const float* e, float px, float py, float& best2,
+                                          unsigned& par) {
+  const float t = __saturatef(fmaf(px, e[4], fmaf(py, e[5], e[6])));
+  const float rx = e[0] - px, ry = e[1] - py;
+  const float qx = fmaf(t, e[2], rx), qy = fmaf(t, e[3], ry);
+  best2 = fminf(best2, fmaf(qx, qx, qy * qy));
+  const float w2 = e[7] - py;
+  const float cr = fmaf(rx, e[3], -(ry * e[2]));
+  par ^= (__float_as_uint(ry) ^ __float_as_uint(w2)) & (__float_as_uint(ry) ^ __float_as_uint(cr));
+}
+
+template <int NB>
+__device__ __forceinline__ float sd_polygon(const FpDev& fp, float px, float py) {
+  float best2 = __int_as_float(0x7f800000);
+  unsigned par = 0u;
+  if constexpr (NB > 0) {
+#pragma unroll
+    for (int b = 0; b < NB; ++b) poly_edge(fp.e[b], px, py, best2, par);
+  } else {
+#pragma unroll 4
+    for (int b = 0; b < fp.count; ++b) poly_edge(fp.e[b], px, py, best2, par);
+  }
+  if (best2 < 1e-24f) return 0.0f;  // kBoundaryEpsilon rule (d < 1e-12 -> 0)
+  const float d = sqrtf(best2);
+  return (par >> 31) ? -d : d;
+}
+
+// Rectangle cover (geometry.cpp:261-272): min_j [sqrt(|max(a,0)|^2) + min(max(ax,ay),0)]
+// == (min_j max(ax,ay) <= 0) ? min_j max(ax,ay) : sqrt(min_j |max(a,0)|^2)  (sqrt monotone).
+__device__ __forceinline__ void rect_box(const float* e, float px, float py, float& m_in,
+                                         float& m_e2) {
+  const float ax = fabsf(px - e[0]) - e[2];
+  const float ay = fabsf(py - e[1]) - e[3];
+  const float ox = fmaxf(ax, 0.0f), oy = fmaxf(ay, 0.0f);
+  m_e2 = fminf(m_e2, fmaf(ox, ox, oy * oy));
+  m_in = fminf(m_in, fmaxf(ax, ay));
+}
+
+template <int NB>
+__device__ __forceinline__ float sd_rect(const FpDev& fp, float px, float py) {
+  float m_in = __int_as_float(0x7f800000), m_e2 = __int_as_float(0x7f800000);
+  if constexpr (NB > 0) {
+#pragma unroll
+    for (int j = 0; j < NB; ++j) rect_box(fp.e[j], px, py, m_in, m_e2);
+  } else {
+#pragma unroll 2
+    for (int j = 0; j < fp.count; ++j) rect_box(fp.e[j], px, py, m_in, m_e2);
+  }
+  return m_in <= 0.0f ? m_in : sqrtf(m_e2);
+}
+
+template <int KIND, int NB>
+__device__ __forceinline__ float sd_body(const FpDev& fp, float px, float py) {
+  if constexpr (KIND == EXM_FOOTPRINT_POLYGON) return sd_polygon<NB>(fp, px, py);
+  else return sd_rect<NB>(fp, px, py);
+}
+
+// Order-preserving float -> u32 key (for min via integer reductions / atomics).
+__device__ __forceinline__ unsigned fkey(float f) {
+  const unsigned u = __float_as_uint(f);
+  return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+__device__ __forceinline__ float unkey(unsigned k) {
+  return __uint_as_float((k & 0x80000000u) ? (k & 0x7fffffffu) : ~k);
+}
+
+// ------------------------------------------------------------------ kernels
+__global__ void k_noise(const StepConst sc, const StepDyn* __restrict__ dyn,
+                        double* __restrict__ eps) {
+  const int idx = blockIdx.x * blockDim.x + threadIdx.x;  // local (r, h)
+  if (idx >= sc.k_local * sc.T) return;
+  const int r = idx / sc.T, h = idx % sc.T;
+  const uint64_t rg = static_cast<uint64_t>(sc.r_offset + r);
+  const uint64_t k =
+      hash_mix(hash_mix(hash_mix(splitmix64(sc.seed), dyn->cycle), rg), static_cast<uint64_t>(h));
+  for (int c = 0; c < sc.D; ++c) {
+    const uint64_t kc = hash_mix(k, static_cast<uint64_t>(c));
+    const double u1 = unit_oc(hash_mix(kc, 0xD1B54A32D192ED03ull));
+    const double u2 = unit_oc(hash_mix(kc, 0x8CB92BA72F3D8DD7ull));
+    eps[static_cast<size_t>(idx) * sc.D + c] =
+        sc.sigma[c] * (sqrt(-2.0 * log(u1)) * cos(2.0 * kPi * u2));
+  }
+}
+
+// Single-CTA cloud preparation: mask compaction, FP64 recentring at q0 then FP32 rounding,
+// bounding box, uniform grid (cell >= cs_target, <= kGridMax per axis), counting sort.
+__global__ void __launch_bounds__(1024) k_cloud_prep(const double* __restrict__ pts,
+                                                     const uint8_t* __restrict__ mask,
+                                                     const StepDyn* __restrict__ dyn,
+                                                     float cs_target, float2* __restrict__ tmp,
+                                                     float2* __restrict__ cloud,
+                                                     int* __restrict__ cell_start,
+                                                     GridMeta* __restrict__ gm_out) {
+  extern __shared__ int hist[];  // kGridMax * kGridMax
+  __shared__ float red[4][32];
+  __shared__ int redc[32];
+  __shared__ int scan_tot[32];
+  __shared__ GridMeta gm;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int n = dyn->n_points;
+  const bool use_mask = dyn->use_mask != 0;
+  const double qx = dyn->q0[0], qy = dyn->q0[1];
+  const float nanf_ = __int_as_float(0x7fc00000);
+  float mnx = FLT_MAX, mxx = -FLT_MAX, mny = FLT_MAX, mxy = -FLT_MAX;
+  int cnt = 0;
+  const double2* p2 = reinterpret_cast<const double2*>(pts);
+  for (int i = tid; i < n; i += blockDim.x) {
+    const bool v = !use_mask || mask[i] != 0;
+    float2 p = make_float2(nanf_, nanf_);
+    if (v) {
+      const double2 w = p2[i];
+      p = make_float2(static_cast<float>(w.x - qx), static_cast<float>(w.y - qy));
+      mnx = fminf(mnx, p.x); mxx = fmaxf(mxx, p.x);
+      mny = fminf(mny, p.y); mxy = fmaxf(mxy, p.y);
+      ++cnt;
+    }
+    tmp[i] = p;
+  }
+  for (int o = 16; o; o >>= 1) {
+    mnx = fminf(mnx, __shfl_xor_sync(kFull, mnx, o));
+    mxx = fmaxf(mxx, __shfl_xor_sync(kFull, mxx, o));
+    mny = fminf(mny, __shfl_xor_sync(kFull, mny, o));
+    mxy = fmaxf(mxy, __shfl_xor_sync(kFull, mxy, o));
+    cnt += __shfl_xor_sync(kFull, cnt, o);
+  }
+  if (lane == 0) { red[0][warp] = mnx; red[1][warp] = mxx; red[2][warp] = mny; red[3][warp] = mxy; redc[warp] = cnt; }
+  __syncthreads();
+  if (tid == 0) {
+    const int nw = blockDim.x >> 5;
+    for (int w = 1; w < nw; ++w) {
+      mnx = fminf(mnx, red[0][w]); mxx = fmaxf(mxx, red[1][w]);
+      mny = fminf(mny, red[2][w]); mxy = fmaxf(mxy, red[3][w]);
+      cnt += redc[w];
+    }
+    GridMeta g;
+    g.n_valid = cnt;
+    g.reserved = 0;
+    if (cnt == 0) {
+      g.x0 = g.y0 = 0.0f; g.cs = 1.0f; g.inv_cs = 1.0f; g.gx = g.gy = 1;
+    } else {
+      const float ex = mxx - mnx, ey = mxy - mny;
+      float cs = fmaxf(cs_target, fmaxf(ex, ey) / static_cast<float>(kGridMax - 1) * 1.001f);
+      cs = fmaxf(cs, 1e-4f);
+      g.x0 = mnx; g.y0 = mny; g.cs = cs; g.inv_cs = 1.0f / cs;
+      g.gx = min(kGridMax, static_cast<int>(ex * g.inv_cs) + 1);
+      g.gy = min(kGridMax, static_cast<int>(ey * g.inv_cs) + 1);
+    }
+    gm = g;
+    *gm_out = g;
+  }
+  __syncthreads();
+  const int cells = gm.gx * gm.gy;
+  for (int c = tid; c < cells; c += blockDim.x) hist[c] = 0;
+  __syncthreads();
+  if (gm.n_valid > 0) {
+    for (int i = tid; i < n; i += blockDim.x) {
+      const float2 p = tmp[i];
+      if (p.x == p.x) {
+        const int ix = min(gm.gx - 1, max(0, static_cast<int>((p.x - gm.x0) * gm.inv_cs)));
+        const int iy = min(gm.gy - 1, max(0, static_cast<int>((p.y - gm.y0) * gm.inv_cs)));
+        atomicAdd(&hist[iy * gm.gx + ix], 1);
+      }
+    }
+  }
+  __syncthreads();
+  // exclusive scan: each thread owns a contiguous segment
+  const int seg = (cells + blockDim.x - 1) / blockDim.x;
+  const int c0 = min(cells, tid * seg), c1 = min(cells, c0 + seg);
+  int local = 0;
+  for (int c = c0; c < c1; ++c) local += hist[c];
+  int incl = local;
+  for (int o = 1; o < 32; o <<= 1) {
+    const int v = __shfl_up_sync(kFull, incl, o);
+    if (lane >= o) incl += v;
+  }
+  if (lane == 31) scan_tot[warp] = incl;
+  __syncthreads();
+  if (warp == 0) {
+    const int nw = blockDim.x >> 5;
+    int v = lane < nw ? scan_tot[lane] : 0;
+    int s = v;
+    for (int o = 1; o < 32; o <<= 1) {
+      const int u = __shfl_up_sync(kFull, s, o);
+      if (lane >= o) s += u;
+    }
+    if (lane < nw) scan_tot[lane] = s - v;  // exclusive warp offsets
+  }
+  __syncthreads();
+  int run = scan_tot[warp] + incl - local;
+  for (int c = c0; c < c1; ++c) {
+    const int h = hist[c];
+    cell_start[c] = run;
+    hist[c] = run;  // becomes the scatter cursor
+    run += h;
+  }
+  if (tid == 0) cell_start[cells] = gm.n_valid;
+  __syncthreads();
+  if (gm.n_valid > 0) {
+    for (int i = tid; i < n; i += blockDim.x) {
+      const float2 p = tmp[i];
+      if (p.x == p.x) {
+        const int ix = min(gm.gx - 1, max(0, static_cast<int>((p.x - gm.x0) * gm.inv_cs)));
+        const int iy = min(gm.gy - 1, max(0, static_cast<int>((p.y - gm.y0) * gm.inv_cs)));
+        const int slot = atomicAdd(&hist[iy * gm.gx + ix], 1);
+        cloud[slot] = p;
+      }
+    }
+  }
+}
+
+__global__ void k_rollout(const StepConst sc, const StepDyn* __restrict__ dynp,
+                          const double* __restrict__ nominal, const double* __restrict__ guide,
+                          const double* __restrict__ eps, float4* __restrict__ poses,
+                          double* __restrict__ base_cost, double* __restrict__ controls_out,
+                          double* __restrict__ states_out) {
+  extern __shared__ double sm[];
+  const StepDyn dyn = *dynp;
+  const int ng = dyn.n_guide;
+  double* g = sm;
+  double* nom = sm + 2 * ng;
+  for (int i = threadIdx.x; i < 2 * ng; i += blockDim.x) g[i] = guide[i];
+  for (int i = threadIdx.x; i < sc.T * sc.D; i += blockDim.x) nom[i] = nominal[i];
+  __syncthreads();
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= sc.k_local) return;
+  const size_t row = static_cast<size_t>(r) * sc.T;
+  base_cost[r] = rollout_one(sc, dyn, nom, eps + row * sc.D, g, ng, poses + row,
+                             controls_out ? controls_out + row * sc.D : nullptr,
+                             states_out ? states_out + static_cast<size_t>(r) * (sc.T + 1) * 3 : nullptr);
+}
+
+// Ring c (Chebyshev radius k >= 1) around (ci, cj): 8k cells, enumerated row/column-wise.
+__device__ __forceinline__ void ring_cell(int k, int t, int ci, int cj, int& i, int& j) {
+  if (k == 0) { i = ci; j = cj; return; }
+  const int row = 2 * k + 1;
+  if (t < row) { i = ci - k + t; j = cj + k; return; }
+  t -= row;
+  if (t < row) { i = ci - k + t; j = cj - k; return; }
+  t -= row;
+  const int col = 2 * k - 1;
+  if (t < col) { i = ci - k; j = cj - k + 1 + t; return; }
+  t -= col;
+  i = ci + k; j = cj - k + 1 + t;
+}
+
+// Exact per-pose min signed distance with exact culling (min_signed_distance_at semantics).
+// Thread <-> pose; a warp walks grid rings outward from its poses' centroid, nearest first,
+// and stops once no lane's lower bound |o - t| - R can beat that lane's running minimum
+// (the reference's own prune, geometry.cpp:368-369, applied to cells, then to points).
+template <int KIND, int NB>
+__global__ void __launch_bounds__(128) k_sdf_grid(const __grid_constant__ FpDev fp,
+                                                  const float4* __restrict__ poses, int n_poses,
+                                                  const GridMeta* __restrict__ gmp,
+                                                  const int* __restrict__ cell_start,
+                                                  const float2* __restrict__ cloud,
+                                                  float* __restrict__ out) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const bool active = i < n_poses;
+  const GridMeta gm = *gmp;
+  if (gm.n_valid == 0) {
+    if (active) out[i] = kEmptyDistance;
+    return;
+  }
+  const float4 q = active ? poses[i] : make_float4(0.f, 0.f, 1.f, 0.f);
+  float sx = active ? q.x : 0.f, sy = active ? q.y : 0.f;
+  int na = active ? 1 : 0;
+  for (int o = 16; o; o >>= 1) {
+    sx += __shfl_xor_sync(kFull, sx, o);
+    sy += __shfl_xor_sync(kFull, sy, o);
+    na += __shfl_xor_sync(kFull, na, o);
+  }
+  if (na == 0) return;
+  const float cx = sx / na, cy = sy / na;
+  const int ci = min(gm.gx - 1, max(0, static_cast<int>(floorf((cx - gm.x0) * gm.inv_cs))));
+  const int cj = min(gm.gy - 1, max(0, static_cast<int>(floorf((cy - gm.y0) * gm.inv_cs))));
+  const float R = fp.radius + kCullMargin;
+  float best = __int_as_float(0x7f800000);
+  const int kmax = max(max(ci, gm.gx - 1 - ci), max(cj, gm.gy - 1 - cj));
+  for (int k = 0; k <= kmax; ++k) {
+    if (k > 0) {
+      const float bx0 = gm.x0 + static_cast<float>(ci - k + 1) * gm.cs;
+      const float bx1 = gm.x0 + static_cast<float>(ci + k) * gm.cs;
+      const float by0 = gm.y0 + static_cast<float>(cj - k + 1) * gm.cs;
+      const float by1 = gm.y0 + static_cast<float>(cj + k) * gm.cs;
+      const float lb = fmaxf(fminf(fminf(q.x - bx0, bx1 - q.x), fminf(q.y - by0, by1 - q.y)), 0.f);
+      const bool need = active && lb < R + best;
+      if (!__any_sync(kFull, need)) break;
+    }
+    const int ncell = k == 0 ? 1 : 8 * k;
+    for (int t = 0; t < ncell; ++t) {
+      int ii, jj;
+      ring_cell(k, t, ci, cj, ii, jj);
+      if (ii < 0 || jj < 0 || ii >= gm.gx || jj >= gm.gy) continue;
+      const int c = jj * gm.gx + ii;
+      const int s = __ldg(cell_start + c), e = __ldg(cell_start + c + 1);
+      if (s == e) continue;
+      const float bx0 = gm.x0 + static_cast<float>(ii) * gm.cs, bx1 = bx0 + gm.cs;
+      const float by0 = gm.y0 + static_cast<float>(jj) * gm.cs, by1 = by0 + gm.cs;
+      const float gx_ = fmaxf(fmaxf(bx0 - q.x, q.x - bx1), 0.f);
+      const float gy_ = fmaxf(fmaxf(by0 - q.y, q.y - by1), 0.f);
+      const float lim = R + best;
+      const bool need = active && (gx_ * gx_ + gy_ * gy_ < lim * lim);
+      if (!__any_sync(kFull, need)) continue;
+      for (int p = s; p < e; ++p) {
+        const float2 o = __ldg(cloud + p);
+        if (need) {
+          const float dx = o.x - q.x, dy = o.y - q.y;
+          const float l2 = R + best;
+          if (dx * dx + dy * dy < l2 * l2) {
+            const float bx = fmaf(q.z, dx, q.w * dy);
+            const float by = fmaf(q.z, dy, -(q.w * dx));
+            best = fminf(best, sd_body<KIND, NB>(fp, bx, by));
+          }
+        }
+      }
+    }
+  }
+  if (active) out[i] = best;
+}
+
+// Obstacle cost, unsafe flag, augmented cost and the min-shifted softmax partial of one
+// block of kBlockRollouts rollouts (fixed tree => deterministic, independent of sharding).
+__global__ void __launch_bounds__(kBlockRollouts) k_block_partials(
+    const StepConst sc, const double* __restrict__ base_cost, const float* __restrict__ dmin,
+    const double* __restrict__ eps, double* __restrict__ partials, double* __restrict__ cost_out,
+    uint8_t* __restrict__ unsafe_out) {
+  __shared__ double s_e[kBlockRollouts];
+  __shared__ double s_v[kBlockRollouts / 32];
+  __shared__ double s_a[kBlockRollouts / 32];
+  __shared__ int s_i[kBlockRollouts / 32];
+  __shared__ double s_beta;
+  __shared__ int s_arg;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int r0 = blockIdx.x * kBlockRollouts;
+  const int r = r0 + tid;
+  const bool valid = r < sc.k_local;
+  double jt = HUGE_VAL;
+  if (valid) {
+    double obs = 0.0;
+    bool bad = false;
+    const float* drow = dmin + static_cast<size_t>(r) * sc.T;
+    for (int h = 0; h < sc.T; ++h) {
+      const double d = static_cast<double>(drow[h]);
+      bad = bad || (d < sc.d_safe);
+      obs += obstacle_cost(sc, d);
+    }
+    const double J = base_cost[r] + obs;
+    if (cost_out) cost_out[r] = J;
+    if (unsafe_out) unsafe_out[r] = bad ? 1 : 0;
+    jt = bad ? J + sc.w_inf : J;
+  }
+  if (!partials) return;
+  // argmin with first-index tie break (std::min_element)
+  double v = jt;
+  int vi = valid ? sc.r_offset + r : 0x7fffffff;
+  for (int o = 16; o; o >>= 1) {
+    const double ov = __shfl_xor_sync(kFull, v, o);
+    const int oi = __shfl_xor_sync(kFull, vi, o);
+    if (ov < v || (ov == v && oi < vi)) { v = ov; vi = oi; }
+  }
+  if (lane == 0) { s_v[warp] = v; s_i[warp] = vi; }
+  __syncthreads();
+  if (tid == 0) {
+    double b = s_v[0];
+    int bi = s_i[0];
+    for (int w = 1; w < kBlockRollouts / 32; ++w)
+      if (s_v[w] < b || (s_v[w] == b && s_i[w] < bi)) { b = s_v[w]; bi = s_i[w]; }
+    s_beta = b;
+    s_arg = bi;
+  }
+  __syncthreads();
+  const double beta = s_beta;
+  const double z = valid ? (jt - beta) / sc.lambda : 0.0;
+  const double e = valid ? exp(-z) : 0.0;
+  const double a = valid ? e * z : 0.0;
+  s_e[tid] = e;
+  double se = e, sa = a;
+  for (int o = 16; o; o >>= 1) {
+    se += __shfl_xor_sync(kFull, se, o);
+    sa += __shfl_xor_sync(kFull, sa, o);
+  }
+  if (lane == 0) { s_v[warp] = se; s_a[warp] = sa; }
+  __syncthreads();
+  const int stride = partial_stride(sc.T, sc.D);
+  double* out = partials + static_cast<size_t>(sc.block_offset + blockIdx.x) * stride;
+  if (tid == 0) {
+    double S = 0.0, A = 0.0;
+    for (int w = 0; w < kBlockRollouts / 32; ++w) { S += s_v[w]; A += s_a[w]; }
+    out[0] = beta;
+    out[1] = S;
+    out[2] = A;
+    out[3] = static_cast<double>(s_arg);
+  }
+  const int nv = min(kBlockRollouts, sc.k_local - r0);
+  const int TD = sc.T * sc.D;
+  const double* erow = eps + static_cast<size_t>(r0) * TD;
+  for (int o = tid; o < TD; o += blockDim.x) {
+    double acc = 0.0;
+    for (int j = 0; j < nv; ++j) acc += s_e[j] * erow[static_cast<size_t>(j) * TD + o];
+    out[4 + o] = acc;
+  }
+}
+
+// Merge all block partials in block order (every rank does this identically), apply the
+// weighted update, then the sequential clamp + validation rollout (one thread).
+__global__ void __launch_bounds__(256) k_update(const StepConst sc,
+                                                const double* __restrict__ partials,
+                                                const double* __restrict__ nominal,
+                                                const StepDyn* __restrict__ dynp,
+                                                const double* __restrict__ guide,
+                                                double* __restrict__ upd,
+                                                float4* __restrict__ val_poses,
+                                                double* __restrict__ val_base,
+                                                DecisionDev* __restrict__ dec, int merge) {
+  extern __shared__ double sf[];  // nblocks_total factors, then guide
+  __shared__ double s_beta, s_S;
+  const int tid = threadIdx.x;
+  const int nb = sc.nblocks_total;
+  const int stride = partial_stride(sc.T, sc.D);
+  const int TD = sc.T * sc.D;
+  const StepDyn dyn = *dynp;
+  double* g = sf + (merge ? nb : 0);
+  for (int i = tid; i < 2 * dyn.n_guide; i += blockDim.x) g[i] = guide[i];
+  if (merge) {
+    if (tid == 0) {
+      double beta = partials[0];
+      int arg = static_cast<int>(partials[3]);
+      for (int b = 1; b < nb; ++b) {
+        const double bb = partials[static_cast<size_t>(b) * stride];
+        if (bb < beta) { beta = bb; arg = static_cast<int>(partials[static_cast<size_t>(b) * stride + 3]); }
+      }
+      s_beta = beta;
+      dec->argmin = arg;
+      dec->best_cost = beta;
+    }
+    __syncthreads();
+    for (int b = tid; b < nb; b += blockDim.x)
+      sf[b] = exp(-(partials[static_cast<size_t>(b) * stride] - s_beta) / sc.lambda);
+    __syncthreads();
+    if (tid == 0) {
+      double S = 0.0, A = 0.0;
+      for (int b = 0; b < nb; ++b) {
+        const double* p = partials + static_cast<size_t>(b) * stride;
+        S += sf[b] * p[1];
+        A += sf[b] * (p[2] + p[1] * ((p[0] - s_beta) / sc.lambda));
+      }
+      s_S = S;
+      dec->entropy = A / S + log(S);
+    }
+    __syncthreads();
+    for (int o = tid; o < TD; o += blockDim.x) {
+      double U = 0.0;
+      for (int b = 0; b < nb; ++b) U += sf[b] * partials[static_cast<size_t>(b) * stride + 4 + o];
+      upd[o] = nominal[o] + U / s_S;
+    }
+  } else {
+    for (int o = tid; o < TD; o += blockDim.x) upd[o] = nominal[o];
+  }
+  __syncthreads();
+  if (tid == 0) {
+    // rollout_one clamps sequentially from u_prev and writes the clamped sequence back; the
+    // reference's second clamp inside validate_nominal is idempotent on it.
+    *val_base = rollout_one(sc, dyn, upd, nullptr, g, dyn.n_guide, val_poses, upd, nullptr);
+  }
+}
+
+__global__ void k_finalize(const StepConst sc, const float* __restrict__ val_dmin,
+                           const double* __restrict__ val_base, const double* __restrict__ upd,
+                           double* __restrict__ nominal, StepDyn* __restrict__ dyn,
+                           DecisionDev* __restrict__ dec, double* __restrict__ out_dmin,
+                           double* __restrict__ out_nominal, double* __restrict__ out_uprev,
+                           int commit) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  const int T = sc.T, D = sc.D;
+  double obs = 0.0;
+  int ok = 1;
+  for (int h = 0; h < T; ++h) {
+    const double d = static_cast<double>(val_dmin[h]);
+    if (out_dmin) out_dmin[h] = d;
+    if (d < sc.d_safe) ok = 0;
+    obs += obstacle_cost(sc, d);
+  }
+  dec->nominal_cost = *val_base + obs;
+  dec->validated = ok;
+  if (!commit) return;
+  double cmd[3] = {0.0, 0.0, 0.0};
+  if (ok) {
+    for (int c = 0; c < D; ++c) cmd[c] = upd[c];
+    for (int h = 0; h + 1 < T; ++h)
+      for (int c = 0; c < D; ++c) nominal[h * D + c] = upd[(h + 1) * D + c];
+    for (int c = 0; c < D; ++c) nominal[(T - 1) * D + c] = upd[(T - 1) * D + c];
+  } else {
+    for (int i = 0; i < T * D; ++i) nominal[i] = 0.0;
+  }
+  for (int c = 0; c < 3; ++c) {
+    dec->command[c] = cmd[c];
+    dyn->u_prev[c] = cmd[c];
+    if (out_uprev) out_uprev[c] = cmd[c];
+  }
+  if (out_nominal)
+    for (int i = 0; i < T * D; ++i) out_nominal[i] = nominal[i];
+  dyn->cycle += 1;
+}
+
+__global__ void k_recentre(const double* __restrict__ pts, int n, double cx, double cy,
+                           float2* __restrict__ out) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double2 w = reinterpret_cast<const double2*>(pts)[i];
+  out[i] = make_float2(static_cast<float>(w.x - cx), static_cast<float>(w.y - cy));
+}
+
+// ---- TMA bulk copy (cp.async.bulk global -> shared, mbarrier completion) -------------
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void tma_bulk_g2s(void* dst, const void* src, unsigned bytes,
+                                             uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tWAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+constexpr int kPairThreads = 256;
+constexpr int kPairPts = 2;           // points per thread (registers)
+constexpr int kPoseChunk = 1024;      // poses staged per TMA bulk copy (16 KB)
+
+// Every point-pose pair (batch_signed_distance semantics per pose). Thread <-> 2 points in
+// registers; pose tiles are staged into shared memory by one TMA bulk copy and broadcast.
+// Per-pair output per_pair[p*N + i] (coalesced); per-pose min via REDUX + smem atomics.
+template <int KIND, int NB>
+__global__ void __launch_bounds__(kPairThreads) k_sdf_pairs(
+    const __grid_constant__ FpDev fp, const float4* __restrict__ poses, int n_poses,
+    const float2* __restrict__ pts, const uint8_t* __restrict__ mask, int n_points,
+    float* __restrict__ per_pair, unsigned* __restrict__ pose_min_key) {
+  __shared__ __align__(128) float4 s_pose[kPoseChunk];
+  __shared__ unsigned s_min[kPoseChunk];
+  __shared__ __align__(8) uint64_t bar;
+  const int tid = threadIdx.x;
+  const int lane = tid & 31;
+  const int base = blockIdx.x * (kPairThreads * kPairPts);
+  float px[kPairPts], py[kPairPts];
+  bool ok[kPairPts];
+#pragma unroll
+  for (int k = 0; k < kPairPts; ++k) {
+    const int i = base + k * kPairThreads + tid;
+    ok[k] = i < n_points && (mask == nullptr || mask[i] != 0);
+    const float2 p = i < n_points ? pts[i] : make_float2(0.f, 0.f);
+    px[k] = p.x;
+    py[k] = p.y;
+  }
+  if (tid == 0) mbar_init(&bar, 1);
+  __syncthreads();
+  unsigned phase = 0;
+  for (int p0 = 0; p0 < n_poses; p0 += kPoseChunk) {
+    const int np = min(kPoseChunk, n_poses - p0);
+    if (tid == 0) {
+      const unsigned bytes = static_cast<unsigned>(np) * sizeof(float4);
+      mbar_expect_tx(&bar, bytes);
+      tma_bulk_g2s(s_pose, poses + p0, bytes, &bar);
+    }
+    for (int j = tid; j < np; j += kPairThreads) s_min[j] = 0xffffffffu;
+    mbar_wait(&bar, phase);
+    phase ^= 1u;
+    __syncthreads();
+    for (int j = 0; j < np; ++j) {
+      const float4 q = s_pose[j];
+      unsigned key = 0xffffffffu;
+#pragma unroll
+      for (int k = 0; k < kPairPts; ++k) {
+        const float dx = px[k] - q.x, dy = py[k] - q.y;
+        const float bx = fmaf(q.z, dx, q.w * dy);
+        const float by = fmaf(q.z, dy, -(q.w * dx));
+        float v = sd_body<KIND, NB>(fp, bx, by);
+        v = ok[k] ? v : __int_as_float(0x7f800000);
+        const int i = base + k * kPairThreads + tid;
+        if (per_pair && i < n_points) per_pair[static_cast<size_t>(p0 + j) * n_points + i] = v;
+        key = min(key, fkey(v));
+      }
+      if (pose_min_key) {
+        key = __reduce_min_sync(kFull, key);
+        if (lane == 0) atomicMin(&s_min[j], key);
+      }
+    }
+    __syncthreads();
+    if (pose_min_key)
+      for (int j = tid; j < np; j += kPairThreads) atomicMin(&pose_min_key[p0 + j], s_min[j]);
+    __syncthreads();
+  }
+}
+
+__global__ void k_keys_to_double(const unsigned* __restrict__ keys, int n,
+                                 double* __restrict__ out) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const float v = unkey(keys[i]);
+  out[i] = isinf(v) ? static_cast<double>(kEmptyDistance) : static_cast<double>(v);
+}
+
+__global__ void k_fill_u32(unsigned* p, unsigned v, int n) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) p[i] = v;
+}
+
+// ------------------------------------------------------------------ dispatch
+template <template <int, int> class Launch, typename... Args>
+cudaError_t dispatch_fp(const FpDev& fp, Args&&... args) {
+  if (fp.kind == EXM_FOOTPRINT_POLYGON) {
+    switch (fp.count) {
+      case 3: return Launch<EXM_FOOTPRINT_POLYGON, 3>::run(fp, args...);
+      case 4: return Launch<EXM_FOOTPRINT_POLYGON, 4>::run(fp, args...);
+      case 5: return Launch<EXM_FOOTPRINT_POLYGON, 5>::run(fp, args...);
+      case 6: return Launch<EXM_FOOTPRINT_POLYGON, 6>::run(fp, args...);
+      case 7: return Launch<EXM_FOOTPRINT_POLYGON, 7>::run(fp, args...);
+      case 8: return Launch<EXM_FOOTPRINT_POLYGON, 8>::run(fp, args...);
+      case 10: return Launch<EXM_FOOTPRINT_POLYGON, 10>::run(fp, args...);
+      case 12: return Launch<EXM_FOOTPRINT_POLYGON, 12>::run(fp, args...);
+      case 16: return Launch<EXM_FOOTPRINT_POLYGON, 16>::run(fp, args...);
+      case 32: return Launch<EXM_FOOTPRINT_POLYGON, 32>::run(fp, args...);
+      case 64: return Launch<EXM_FOOTPRINT_POLYGON, 64>::run(fp, args...);
+      default: return Launch<EXM_FOOTPRINT_POLYGON, 0>::run(fp, args...);
+    }
+  }
+  switch (fp.count) {
+    case 1: return Launch<EXM_FOOTPRINT_RECT_COVER, 1>::run(fp, args...);
+    case 2: return Launch<EXM_FOOTPRINT_RECT_COVER, 2>::run(fp, args...);
+    case 3: return Launch<EXM_FOOTPRINT_RECT_COVER, 3>::run(fp, args...);
+    case 4: return Launch<EXM_FOOTPRINT_RECT_COVER, 4>::run(fp, args...);
+    default: return Launch<EXM_FOOTPRINT_RECT_COVER, 0>::run(fp, args...);
+  }
+}
+
+template <int KIND, int NB>
+struct GridLaunch {
+  static cudaError_t run(const FpDev& fp, const float4* poses, int n_poses, const GridMeta* gm,
+                         const int* cell_start, const float2* cloud, float* out, cudaStream_t s) {
+    if (n_poses <= 0) return cudaSuccess;
+    const int threads = 128;
+    k_sdf_grid<KIND, NB><<<(n_poses + threads - 1) / threads, threads, 0, s>>>(
+        fp, poses, n_poses, gm, cell_start, cloud, out);
+    return cudaGetLastError();
+  }
+};
+
+template <int KIND, int NB>
+struct PairsLaunch {
+  static cudaError_t run(const FpDev& fp, const float4* poses, int n_poses, const float2* pts,
+                         const uint8_t* mask, int n_points, float* per_pair, unsigned* keys,
+                         cudaStream_t s) {
+    if (n_poses <= 0 || n_points <= 0) return cudaSuccess;
+    const int per_block = kPairThreads * kPairPts;
+    k_sdf_pairs<KIND, NB><<<(n_points + per_block - 1) / per_block, kPairThreads, 0, s>>>(
+        fp, poses, n_poses, pts, mask, n_points, per_pair, keys);
+    return cudaGetLastError();
+  }
+};
+
+}  // namespace
+
+// ------------------------------------------------------------------ launchers
+cudaError_t launch_noise(const StepConst& sc, const StepDyn* dyn, double* eps, cudaStream_t s) {
+  const int n = sc.k_local * sc.T;
+  if (n <= 0) return cudaSuccess;
+  k_noise<<<(n + 255) / 256, 256, 0, s>>>(sc, dyn, eps);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_cloud_prep(const double* pts, const uint8_t* mask, const StepDyn* dyn,
+                              float radius, float2* tmp, float2* cloud, int* cell_start,
+                              GridMeta* gm, cudaStream_t s) {
+  const int smem = kGridMax * kGridMax * static_cast<int>(sizeof(int));
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(k_cloud_prep, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
+  // Cells of half the bounding radius: a cull disc of radius R + d covers ~(2(R+d)/cs)^2 cells.
+  const float cs_target = fmaxf(0.5f * radius, 0.02f);
+  k_cloud_prep<<<1, 1024, smem, s>>>(pts, mask, dyn, cs_target, tmp, cloud, cell_start, gm);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_rollout(const StepConst& sc, const StepDyn* dyn, const double* nominal,
+                                const double* guide, int guide_cap, const double* eps,
+                                float4* poses, double* base_cost, double* controls_out,
+                                double* states_out, cudaStream_t s) {
+  const int threads = 128;
+  const size_t smem = sizeof(double) * (2 * static_cast<size_t>(guide_cap) + sc.T * sc.D);
+  if (smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(k_rollout, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(smem));
+    if (e != cudaSuccess) return e;
+  }
+  k_rollout<<<(sc.k_local + threads - 1) / threads, threads, smem, s>>>(
+      sc, dyn, nominal, guide, eps, poses, base_cost, controls_out, states_out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_sdf_grid(const FpDev& fp, const float4* poses, int n_poses,
+                            const GridMeta* gm, const int* cell_start, const float2* cloud,
+                            float* out, cudaStream_t s) {
+  return dispatch_fp<GridLaunch>(fp, poses, n_poses, gm, cell_start, cloud, out, s);
+}
+
+cudaError_t launch_block_partials(const StepConst& sc, const double* base_cost,
+                                  const float* dmin, const double* eps, double* partials,
+                                  double* cost_out, uint8_t* unsafe_out, cudaStream_t s) {
+  if (sc.nblocks_local <= 0) return cudaSuccess;
+  k_block_partials<<<sc.nblocks_local, kBlockRollouts, 0, s>>>(sc, base_cost, dmin, eps, partials,
+                                                              cost_out, unsafe_out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_update(const StepConst& sc, const double* partials, const double* nominal,
+                          const StepDyn* dyn, const double* guide, int guide_cap, double* upd,
+                          float4* val_poses, double* val_base, DecisionDev* dec, int merge,
+                          cudaStream_t s) {
+  const size_t smem = sizeof(double) * (static_cast<size_t>(merge ? sc.nblocks_total : 0) +
+                                        2 * static_cast<size_t>(guide_cap));
+  if (smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(k_update, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(smem));
+    if (e != cudaSuccess) return e;
+  }
+  k_update<<<1, 256, smem, s>>>(sc, partials, nominal, dyn, guide, upd, val_poses, val_base, dec,
+                                merge);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_finalize(const StepConst& sc, const float* val_dmin, const double* val_base,
+                            const double* upd, double* nominal, StepDyn* dyn, DecisionDev* dec,
+                            double* out_dmin, double* out_nominal, double* out_uprev,
+                            int commit, cudaStream_t s) {
+  k_finalize<<<1, 32, 0, s>>>(sc, val_dmin, val_base, upd, nominal, dyn, dec, out_dmin,
+                              out_nominal, out_uprev, commit);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_recentre(const double* pts, int n, double cx, double cy, float2* out,
+                            cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  k_recentre<<<(n + 255) / 256, 256, 0, s>>>(pts, n, cx, cy, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_sdf_pairs(const FpDev& fp, const float4* poses, int n_poses,
+                             const float2* pts, const uint8_t* mask, int n_points,
+                             float* per_pair, unsigned* pose_min_key, cudaStream_t s) {
+  return dispatch_fp<PairsLaunch>(fp, poses, n_poses, pts, mask, n_points, per_pair,
+                                  pose_min_key, s);
+}
+
+cudaError_t launch_min_keys_to_double(const unsigned* keys, int n, double* out, cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  k_keys_to_double<<<(n + 255) / 256, 256, 0, s>>>(keys, n, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_fill_u32(unsigned* p, unsigned v, int n, cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  k_fill_u32<<<(n + 255) / 256, 256, 0, s>>>(p, v, n);
+  return cudaGetLastError();
+}
+
+}  // namespace exm

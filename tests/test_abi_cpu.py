@@ -1,0 +1,69 @@
+"""CPU checks of the boundary: libexm_b200.so loads, exports every symbol include/exm_b200.h
+declares, validates inputs with the reference's messages before touching the device, and
+fails loudly (no CPU fallback) when no GPU is present."""
+import ctypes as C
+import os
+import re
+
+import pytest
+
+from paper_2605_29663_b200 import _abi
+from paper_2605_29663_b200 import workloads as W
+from paper_2605_29663_b200.api import Engine, FootprintSpec, MppiParams
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def header_functions():
+    txt = open(os.path.join(ROOT, "include", "exm_b200.h")).read()
+    txt = re.sub(r"/\*.*?\*/", "", txt, flags=re.S)
+    return sorted(set(re.findall(r"\b(exm_[a-z0-9_]+)\s*\(", txt)))
+
+
+def test_header_and_binding_agree():
+    assert header_functions() == sorted(_abi.SIGNATURES)
+
+
+def test_library_exports_every_symbol():
+    lib = _abi.load_library()
+    for name in header_functions():
+        assert hasattr(lib, name), name
+    assert lib.exm_abi_version() == 1
+
+
+def test_library_is_sm100a_only():
+    out = os.popen(f"cuobjdump --list-elf {_abi.LIB_PATH} 2>&1").read()
+    assert "sm_100a" in out and "sm_90" not in out
+
+
+def _create(fp, params=None, model=None):
+    wl = W.cfg1(K=8, T=4)
+    return Engine(model or wl.model, wl.limits, fp, params or wl.params, n_cap=16, guide_cap=4)
+
+
+def test_validation_messages_without_gpu():
+    with pytest.raises(ValueError, match="at least 3 vertices"):
+        _create(FootprintSpec.polygon([[0, 0], [1, 0]]))
+    with pytest.raises(ValueError, match="self-intersects"):
+        _create(FootprintSpec.polygon([[0, 0], [1, 1], [1, 0], [0, 1]]))
+    with pytest.raises(ValueError, match="zero-length"):
+        _create(FootprintSpec.polygon([[0, 0], [1, 0], [1, 0], [0, 1]]))
+    with pytest.raises(ValueError, match="strictly positive"):
+        _create(FootprintSpec.rect_cover([[0, 0]], [[0.0, 1.0]]))
+    with pytest.raises(ValueError, match="rollouts must be >= 1"):
+        _create(W.footprint("l_shape"), MppiParams(rollouts=0))
+    with pytest.raises(ValueError, match="lambda must be positive"):
+        _create(W.footprint("l_shape"), MppiParams(lambda_=0.0))
+    with pytest.raises(ValueError, match="sigma"):
+        _create(W.footprint("l_shape"), MppiParams(sigma=(0.0, 0.3, 0.3)))
+
+
+def test_no_cpu_fallback():
+    try:
+        import torch
+        if torch.cuda.is_available():
+            pytest.skip("GPU present")
+    except ImportError:
+        pass
+    with pytest.raises(_abi.ExmError, match="status 2"):
+        _create(W.footprint("l_shape"))
