@@ -262,6 +262,7 @@ struct exm_handle {
   unsigned char* h_out = nullptr;
   // graphs: [0] device noise, [1] injected noise
   cudaGraphExec_t exec[2] = {nullptr, nullptr};
+  cudaGraph_t graph[2] = {nullptr, nullptr};  // kept alive: exec node updates need its nodes
   cudaGraphNode_t ev_node[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};
   EventPair graph_ev;
   // per-step SDF timing ring (resident runs)
@@ -305,6 +306,11 @@ void destroy_graphs(exm_handle* h) {
     if (e) {
       cudaGraphExecDestroy(e);
       e = nullptr;
+    }
+  for (auto& g : h->graph)
+    if (g) {
+      cudaGraphDestroy(g);
+      g = nullptr;
     }
 }
 
@@ -376,7 +382,7 @@ exm_status ensure_graph(exm_handle* h, int variant) {
     if (e == h->graph_ev.a) h->ev_node[variant][0] = n;
     if (e == h->graph_ev.b) h->ev_node[variant][1] = n;
   }
-  cudaGraphDestroy(g);
+  h->graph[variant] = g;
   h->exec[variant] = exec;
   return EXM_OK;
 }
