@@ -166,7 +166,7 @@ exm_status build_footprint(const exm_footprint* fp, FpDev* out) {
       e[4] = static_cast<float>(ex * inv);
       e[5] = static_cast<float>(ey * inv);
       e[6] = static_cast<float>(-(vx * ex + vy * ey) * inv);
-      e[7] = static_cast<float>(vy + ey);
+      e[7] = static_cast<float>(-ex);
       radius = std::max(radius, std::sqrt(vx * vx + vy * vy));
     }
   } else if (fp->kind == EXM_FOOTPRINT_RECT_COVER) {
@@ -195,6 +195,22 @@ exm_status build_footprint(const exm_footprint* fp, FpDev* out) {
     return fail(EXM_ERR_INVALID_ARGUMENT, "unknown footprint kind");
   }
   out->radius = static_cast<float>(radius);
+  // body-frame AABB of all vertices (corners for a cover), widened by one FP32 ulp-ish margin
+  double bx0 = 1e300, bx1 = -1e300, by0 = 1e300, by1 = -1e300;
+  for (int i = 0; i < out->count; ++i) {
+    const float* e = out->e[i];
+    const double xs[2] = {out->kind == EXM_FOOTPRINT_POLYGON ? e[0] : e[0] - e[2],
+                          out->kind == EXM_FOOTPRINT_POLYGON ? e[0] : e[0] + e[2]};
+    const double ys[2] = {out->kind == EXM_FOOTPRINT_POLYGON ? e[1] : e[1] - e[3],
+                          out->kind == EXM_FOOTPRINT_POLYGON ? e[1] : e[1] + e[3]};
+    for (double v : xs) { bx0 = std::min(bx0, v); bx1 = std::max(bx1, v); }
+    for (double v : ys) { by0 = std::min(by0, v); by1 = std::max(by1, v); }
+  }
+  const double m = 1e-4 * (1.0 + radius);
+  out->aabb[0] = static_cast<float>(bx0 - m);
+  out->aabb[1] = static_cast<float>(bx1 + m);
+  out->aabb[2] = static_cast<float>(by0 - m);
+  out->aabb[3] = static_cast<float>(by1 + m);
   return EXM_OK;
 }
 

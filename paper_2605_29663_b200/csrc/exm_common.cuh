@@ -17,13 +17,14 @@ constexpr float kCullMargin = 1e-3f;    // conservative slack on every lower-bou
 // FP32 footprint table, passed by value as a __grid_constant__ kernel parameter so the
 // inner loops read it from the constant bank (uniform datapath), never from memory.
 // Polygon edge b (prepare, geometry.cpp:236-247), recentring-free body frame:
-//   e[b] = {vx, vy, ex, ey, ex/|e|^2, ey/|e|^2, -(v.e)/|e|^2, vy+ey}
+//   e[b] = {vx, vy, ex, ey, ex/|e|^2, ey/|e|^2, -(v.e)/|e|^2, -ex}
 // Box j (geometry.cpp:250-255): e[j] = {cx, cy, hx, hy, 0...}
 struct FpDev {
   int kind;  // EXM_FOOTPRINT_*
   int count;
   float radius;  // PreparedFootprint::bounding_radius (max vertex norm, geometry.cpp:127-131)
   float reserved;
+  float aabb[4];  // body-frame bounding box {xmin, xmax, ymin, ymax}
   float e[kMaxEdges][8];
 };
 

@@ -188,30 +188,37 @@ __device__ double rollout_one(const StepConst& sc, const StepDyn& dyn, const dou
 // Polygon edge step (PreparedFootprint::sd polygon branch, geometry.cpp:273-292).
 //   t  = sat(p.e/|e|^2 - v.e/|e|^2)           2 FFMA (second .SAT)
 //   q  = v + t e - p;  d2 = |q|^2              2 FADD, 2 FFMA, FMUL, FFMA
-//   crossing (division-free): edge counts iff (vy<py) != (vy+ey<py) and
-//   x_cross - px = cross(v-p, e)/ey > 0; with r = v - p the sign bits give
-//   count = (sb(ry) ^ sb(y1-py)) & (sb(ry) ^ sb(cross)).
-__device__ __forceinline__ void poly_edge(const float* e, float px, float py, float& best2,
-                                          unsigned& par) {
+//   crossing, division-free: with r = v - p, edge b counts iff (vy_b < py) != (vy_b+1 < py)
+//   and x_cross - px = cross(v - p, e)/ey > 0, i.e. in sign bits
+//   count = (sb(ry_b) ^ sb(ry_b+1)) & (sb(ry_b) ^ sb(rx ey - ry ex)).
+//   Vertex signs are shared by the two edges that meet there, so the straddle count over a
+//   closed polygon is always even (parity exact outside the footprint's y-range).
+__device__ __forceinline__ void poly_edge(const float* e, float px, float py, float& ry,
+                                          float ry_next, float& best2, unsigned& par) {
   const float t = __saturatef(fmaf(px, e[4], fmaf(py, e[5], e[6])));
-  const float rx = e[0] - px, ry = e[1] - py;
+  const float rx = e[0] - px;
   const float qx = fmaf(t, e[2], rx), qy = fmaf(t, e[3], ry);
   best2 = fminf(best2, fmaf(qx, qx, qy * qy));
-  const float w2 = e[7] - py;
-  const float cr = fmaf(rx, e[3], -(ry * e[2]));
-  par ^= (__float_as_uint(ry) ^ __float_as_uint(w2)) & (__float_as_uint(ry) ^ __float_as_uint(cr));
+  const float cr = fmaf(ry, e[7], rx * e[3]);  // e[7] = -ex
+  par ^= (__float_as_uint(ry) ^ __float_as_uint(ry_next)) & (__float_as_uint(ry) ^ __float_as_uint(cr));
+  ry = ry_next;
 }
 
 template <int NB>
 __device__ __forceinline__ float sd_polygon(const FpDev& fp, float px, float py) {
   float best2 = __int_as_float(0x7f800000);
   unsigned par = 0u;
+  const float ry0 = fp.e[0][1] - py;
+  float ry = ry0;
   if constexpr (NB > 0) {
 #pragma unroll
-    for (int b = 0; b < NB; ++b) poly_edge(fp.e[b], px, py, best2, par);
+    for (int b = 0; b < NB; ++b)
+      poly_edge(fp.e[b], px, py, ry, b + 1 < NB ? fp.e[b + 1][1] - py : ry0, best2, par);
   } else {
+    const int n = fp.count;
 #pragma unroll 4
-    for (int b = 0; b < fp.count; ++b) poly_edge(fp.e[b], px, py, best2, par);
+    for (int b = 0; b < n; ++b)
+      poly_edge(fp.e[b], px, py, ry, b + 1 < n ? fp.e[b + 1][1] - py : ry0, best2, par);
   }
   if (best2 < 1e-24f) return 0.0f;  // kBoundaryEpsilon rule (d < 1e-12 -> 0)
   const float d = sqrtf(best2);
@@ -801,6 +808,206 @@ __global__ void __launch_bounds__(kPairThreads) k_sdf_pairs(
   }
 }
 
+// ---- packed FP32x2 (sm_100 FFMA2/FADD2/FMUL2) helpers ---------------------------------
+typedef unsigned long long u64;
+__device__ __forceinline__ u64 pk(float a, float b) {
+  u64 r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+  return r;
+}
+__device__ __forceinline__ float lo(u64 v) {
+  float a, b;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(v));
+  return a;
+}
+__device__ __forceinline__ float hi(u64 v) {
+  float a, b;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(v));
+  return b;
+}
+__device__ __forceinline__ u64 bc(float x) { return pk(x, x); }
+__device__ __forceinline__ u64 fma2(u64 a, u64 b, u64 c) {
+  u64 r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+  return r;
+}
+__device__ __forceinline__ u64 mul2(u64 a, u64 b) {
+  u64 r;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+__device__ __forceinline__ u64 sub2(u64 a, u64 b) {
+  u64 r;
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+__device__ __forceinline__ unsigned sgn_lo(u64 v) { return __float_as_uint(lo(v)); }
+__device__ __forceinline__ unsigned sgn_hi(u64 v) { return __float_as_uint(hi(v)); }
+
+__device__ __forceinline__ float min3f(float a, float b, float c) {
+  float r;
+  asm("min.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));  // FMNMX3
+  return r;
+}
+
+// One polygon edge against two body-frame points packed in f32x2 lanes (same arithmetic as
+// poly_edge, two pairs per FFMA2/FADD2/FMUL2). Per pair: 8 FP32 ops for the distance, 2 for
+// the crossing product (CROSS), the clamp as scalar FFMA.SAT (no .sat form of FFMA2).
+// Returns the packed squared distances; the caller folds two edges per FMNMX3.
+template <bool CROSS>
+__device__ __forceinline__ u64 poly_edge2(const float* e, float vy_next, u64 X, u64 Y, u64& RY,
+                                          unsigned& pA, unsigned& pB) {
+  const u64 TP = fma2(Y, bc(e[5]), bc(e[6]));
+  const u64 Tt = pk(__saturatef(fmaf(lo(X), e[4], lo(TP))), __saturatef(fmaf(hi(X), e[4], hi(TP))));
+  const u64 RX = sub2(bc(e[0]), X);
+  const u64 QX = fma2(Tt, bc(e[2]), RX);
+  const u64 QY = fma2(Tt, bc(e[3]), RY);
+  const u64 D2 = fma2(QY, QY, mul2(QX, QX));
+  const u64 RYN = sub2(bc(vy_next), Y);
+  if constexpr (CROSS) {
+    const u64 CR = fma2(RY, bc(e[7]), mul2(RX, bc(e[3])));
+    pA ^= (sgn_lo(RY) ^ sgn_lo(RYN)) & (sgn_lo(RY) ^ sgn_lo(CR));
+    pB ^= (sgn_hi(RY) ^ sgn_hi(RYN)) & (sgn_hi(RY) ^ sgn_hi(CR));
+  }
+  RY = RYN;
+  return D2;
+}
+
+template <int NB, bool CROSS>
+__device__ __forceinline__ void poly_pairs4(const FpDev& fp, u64 X01, u64 Y01, u64 X23, u64 Y23,
+                                            float* b, unsigned* par) {
+  // Edge groups of kEdgeGroup with a rolled outer loop: the per-edge constants stay uniform
+  // (LDCU from the parameter bank at a uniform offset) while the code stays small enough for
+  // the instruction cache at B = 64.
+  constexpr int G = NB % 4 == 0 ? 4 : 2;
+  const float vy0 = fp.e[0][1];
+  u64 R01 = sub2(bc(vy0), Y01), R23 = sub2(bc(vy0), Y23);
+  constexpr int NFULL = (NB / G) * G;
+#pragma unroll 1
+  for (int g = 0; g < NFULL; g += G) {
+#pragma unroll
+    for (int j = 0; j < G; j += 2) {
+      const int e = g + j;
+      const float vy1 = fp.e[e + 1][1];
+      const float vy2 = e + 2 < NB ? fp.e[e + 2][1] : vy0;
+      const u64 a01 = poly_edge2<CROSS>(fp.e[e], vy1, X01, Y01, R01, par[0], par[1]);
+      const u64 a23 = poly_edge2<CROSS>(fp.e[e], vy1, X23, Y23, R23, par[2], par[3]);
+      const u64 c01 = poly_edge2<CROSS>(fp.e[e + 1], vy2, X01, Y01, R01, par[0], par[1]);
+      const u64 c23 = poly_edge2<CROSS>(fp.e[e + 1], vy2, X23, Y23, R23, par[2], par[3]);
+      b[0] = min3f(b[0], lo(a01), lo(c01));
+      b[1] = min3f(b[1], hi(a01), hi(c01));
+      b[2] = min3f(b[2], lo(a23), lo(c23));
+      b[3] = min3f(b[3], hi(a23), hi(c23));
+    }
+  }
+#pragma unroll
+  for (int e = NFULL; e < NB; ++e) {
+    const float vyn = e + 1 < NB ? fp.e[e + 1][1] : vy0;
+    const u64 a01 = poly_edge2<CROSS>(fp.e[e], vyn, X01, Y01, R01, par[0], par[1]);
+    const u64 a23 = poly_edge2<CROSS>(fp.e[e], vyn, X23, Y23, R23, par[2], par[3]);
+    b[0] = fminf(b[0], lo(a01));
+    b[1] = fminf(b[1], hi(a01));
+    b[2] = fminf(b[2], lo(a23));
+    b[3] = fminf(b[3], hi(a23));
+  }
+}
+
+constexpr int kPackPts = 4;  // points per thread (two f32x2 packs)
+
+// Every point-pose pair for a polygon footprint, packed: thread <-> 4 points held in
+// registers as two f32x2 packs, pose tiles staged into shared memory by one TMA bulk copy
+// and broadcast. The crossing-number pass runs only for (pose, warp) tiles where some point
+// lies inside the footprint's body-frame AABB: outside it no edge can count an odd number of
+// crossings, so skipping is exact.
+template <int NB>
+__global__ void __launch_bounds__(kPairThreads, 2) k_sdf_pairs_poly(
+    const __grid_constant__ FpDev fp, const float4* __restrict__ poses, int n_poses,
+    const float2* __restrict__ pts, const uint8_t* __restrict__ mask, int n_points,
+    float* __restrict__ per_pair, unsigned* __restrict__ pose_min_key) {
+  __shared__ __align__(128) float4 s_pose[kPoseChunk];
+  __shared__ unsigned s_min[kPoseChunk];
+  __shared__ __align__(8) uint64_t bar;
+  const int tid = threadIdx.x, lane = tid & 31;
+  const int base = blockIdx.x * (kPairThreads * kPackPts);
+  float px[kPackPts], py[kPackPts];
+  bool ok[kPackPts];
+#pragma unroll
+  for (int k = 0; k < kPackPts; ++k) {
+    const int i = base + k * kPairThreads + tid;
+    ok[k] = i < n_points && (mask == nullptr || mask[i] != 0);
+    const float2 p = i < n_points ? pts[i] : make_float2(0.f, 0.f);
+    px[k] = p.x;
+    py[k] = p.y;
+  }
+  const u64 PX01 = pk(px[0], px[1]), PY01 = pk(py[0], py[1]);
+  const u64 PX23 = pk(px[2], px[3]), PY23 = pk(py[2], py[3]);
+  const float ax0 = fp.aabb[0], ax1 = fp.aabb[1], ay0 = fp.aabb[2], ay1 = fp.aabb[3];
+  if (tid == 0) mbar_init(&bar, 1);
+  __syncthreads();
+  unsigned phase = 0;
+  for (int p0 = 0; p0 < n_poses; p0 += kPoseChunk) {
+    const int np = min(kPoseChunk, n_poses - p0);
+    if (tid == 0) {
+      const unsigned bytes = static_cast<unsigned>(np) * sizeof(float4);
+      mbar_expect_tx(&bar, bytes);
+      tma_bulk_g2s(s_pose, poses + p0, bytes, &bar);
+    }
+    for (int j = tid; j < np; j += kPairThreads) s_min[j] = 0xffffffffu;
+    mbar_wait(&bar, phase);
+    phase ^= 1u;
+    __syncthreads();
+    for (int j = 0; j < np; ++j) {
+      const float4 q = s_pose[j];
+      // body frame: b = R(theta)^T (o - t)
+      const u64 DX01 = sub2(PX01, bc(q.x)), DY01 = sub2(PY01, bc(q.y));
+      const u64 DX23 = sub2(PX23, bc(q.x)), DY23 = sub2(PY23, bc(q.y));
+      const float ns = -q.w;
+      const u64 X01 = fma2(DX01, bc(q.z), mul2(DY01, bc(q.w)));
+      const u64 Y01 = fma2(DY01, bc(q.z), mul2(DX01, bc(ns)));
+      const u64 X23 = fma2(DX23, bc(q.z), mul2(DY23, bc(q.w)));
+      const u64 Y23 = fma2(DY23, bc(q.z), mul2(DX23, bc(ns)));
+      const float bx[4] = {lo(X01), hi(X01), lo(X23), hi(X23)};
+      const float by[4] = {lo(Y01), hi(Y01), lo(Y23), hi(Y23)};
+      bool in = false;
+#pragma unroll
+      for (int k = 0; k < kPackPts; ++k)
+        in |= bx[k] >= ax0 && bx[k] <= ax1 && by[k] >= ay0 && by[k] <= ay1;
+      float b[4] = {__int_as_float(0x7f800000), __int_as_float(0x7f800000),
+                    __int_as_float(0x7f800000), __int_as_float(0x7f800000)};
+      unsigned par[4] = {0u, 0u, 0u, 0u};
+      if (__any_sync(kFull, in)) poly_pairs4<NB, true>(fp, X01, Y01, X23, Y23, b, par);
+      else poly_pairs4<NB, false>(fp, X01, Y01, X23, Y23, b, par);
+      unsigned key = 0xffffffffu;
+#pragma unroll
+      for (int k = 0; k < kPackPts; ++k) {
+        const float d2 = b[k] < 1e-24f ? 0.0f : b[k];
+        const bool inside = (par[k] >> 31) != 0;
+        if (per_pair) {
+          const int i = base + k * kPairThreads + tid;
+          float v = sqrtf(d2);
+          v = inside ? -v : v;
+          if (i < n_points) per_pair[static_cast<size_t>(p0 + j) * n_points + i] = ok[k] ? v : __int_as_float(0x7f800000);
+        }
+        // order by the signed square (same order as sd; one sqrt per pose below)
+        const float s2 = ok[k] ? (inside ? -d2 : d2) : __int_as_float(0x7f800000);
+        key = min(key, fkey(s2));
+      }
+      if (pose_min_key) {
+        key = __reduce_min_sync(kFull, key);
+        if (lane == 0) {
+          const float s2 = unkey(key);
+          const float d = isinf(s2) ? s2 : copysignf(sqrtf(fabsf(s2)), s2);
+          atomicMin(&s_min[j], fkey(d));
+        }
+      }
+    }
+    __syncthreads();
+    if (pose_min_key)
+      for (int j = tid; j < np; j += kPairThreads) atomicMin(&pose_min_key[p0 + j], s_min[j]);
+    __syncthreads();
+  }
+}
+
 __global__ void k_keys_to_double(const unsigned* __restrict__ keys, int n,
                                  double* __restrict__ out) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -860,9 +1067,15 @@ struct PairsLaunch {
                          const uint8_t* mask, int n_points, float* per_pair, unsigned* keys,
                          cudaStream_t s) {
     if (n_poses <= 0 || n_points <= 0) return cudaSuccess;
-    const int per_block = kPairThreads * kPairPts;
-    k_sdf_pairs<KIND, NB><<<(n_points + per_block - 1) / per_block, kPairThreads, 0, s>>>(
-        fp, poses, n_poses, pts, mask, n_points, per_pair, keys);
+    if constexpr (KIND == EXM_FOOTPRINT_POLYGON && NB > 0) {
+      const int per_block = kPairThreads * kPackPts;
+      k_sdf_pairs_poly<NB><<<(n_points + per_block - 1) / per_block, kPairThreads, 0, s>>>(
+          fp, poses, n_poses, pts, mask, n_points, per_pair, keys);
+    } else {
+      const int per_block = kPairThreads * kPairPts;
+      k_sdf_pairs<KIND, NB><<<(n_points + per_block - 1) / per_block, kPairThreads, 0, s>>>(
+          fp, poses, n_poses, pts, mask, n_points, per_pair, keys);
+    }
     return cudaGetLastError();
   }
 };
