@@ -254,11 +254,15 @@ struct exm_handle {
   GridMeta* d_grid = nullptr;
   double* d_eps = nullptr;
   float4* d_poses = nullptr;
+  double2* d_xy = nullptr;
+  double* d_stage = nullptr;
+  uint8_t* d_flags = nullptr;
   double* d_base = nullptr;
   float* d_dmin = nullptr;
   double* d_partials = nullptr;
   double* d_upd = nullptr;
   float4* d_val_poses = nullptr;
+  double2* d_val_xy = nullptr;
   double* d_val_base = nullptr;
   float* d_val_dmin = nullptr;
   // contiguous output block: DecisionDev | nominal_dmin[T] | nominal[T*D] | u_prev[3]
@@ -342,17 +346,19 @@ exm_status enqueue_step(exm_handle* h, bool draw_noise, const EventPair* ev, cud
   }
   EXM_CUDA(launch_cloud_prep(h->d_pts, h->d_mask, h->d_dyn, h->fp.radius, h->d_tmp, h->d_cloud,
                              h->d_cell_start, h->d_grid, s));
-  EXM_CUDA(launch_rollout(sc, h->d_dyn, h->d_nominal, h->d_guide, h->guide_cap, h->d_eps,
-                          h->d_poses, h->d_base, nullptr, nullptr, s));
+  EXM_CUDA(launch_rollout(sc, h->d_dyn, h->d_nominal, h->d_eps, h->d_poses, h->d_xy, h->d_base,
+                          nullptr, nullptr, s));
   if (ev) EXM_CUDA(capturing ? cudaEventRecordWithFlags(ev->a, s, cudaEventRecordExternal)
                              : cudaEventRecord(ev->a, s));
   EXM_CUDA(launch_sdf_grid(h->fp, h->d_poses, sc.k_local * sc.T, h->d_grid, h->d_cell_start,
                            h->d_cloud, h->d_dmin, s));
   if (ev) EXM_CUDA(capturing ? cudaEventRecordWithFlags(ev->b, s, cudaEventRecordExternal)
                              : cudaEventRecord(ev->b, s));
-  EXM_CUDA(launch_block_partials(sc, h->d_base, h->d_dmin, h->d_eps, h->d_partials, nullptr,
-                                 nullptr, s));
-  launches += 4;
+  EXM_CUDA(launch_stage_costs(sc, h->d_dyn, h->d_guide, h->guide_cap, h->d_xy, h->d_dmin,
+                              h->d_stage, h->d_flags, s));
+  EXM_CUDA(launch_block_partials(sc, h->d_base, h->d_stage, h->d_flags, h->d_eps, h->d_partials,
+                                 nullptr, nullptr, s));
+  launches += 5;
   if (h->world > 1) {
     const size_t count = static_cast<size_t>(sc.nblocks_local) * partial_stride(sc.T, sc.D);
     const int rc = g_nccl.allgather(h->d_partials + static_cast<size_t>(sc.block_offset) *
@@ -361,12 +367,13 @@ exm_status enqueue_step(exm_handle* h, bool draw_noise, const EventPair* ev, cud
     if (rc != 0)
       return fail(EXM_ERR_NCCL, std::string("ncclAllGather: ") + (g_nccl.errstr ? g_nccl.errstr(rc) : "error"));
   }
-  EXM_CUDA(launch_update(sc, h->d_partials, h->d_nominal, h->d_dyn, h->d_guide, h->guide_cap,
-                         h->d_upd, h->d_val_poses, h->d_val_base, out_dec(h), 1, s));
+  EXM_CUDA(launch_update(sc, h->d_partials, h->d_nominal, h->d_dyn, h->d_upd, h->d_val_poses,
+                         h->d_val_xy, h->d_val_base, out_dec(h), 1, s));
   EXM_CUDA(launch_sdf_grid(h->fp, h->d_val_poses, sc.T, h->d_grid, h->d_cell_start, h->d_cloud,
                            h->d_val_dmin, s));
-  EXM_CUDA(launch_finalize(sc, h->d_val_dmin, h->d_val_base, h->d_upd, h->d_nominal, h->d_dyn,
-                           out_dec(h), out_dmin(h), out_nominal(h), out_uprev(h), 1, s));
+  EXM_CUDA(launch_finalize(sc, h->d_val_dmin, h->d_val_xy, h->d_val_base, h->d_upd, h->d_guide,
+                           h->guide_cap, h->d_nominal, h->d_dyn, out_dec(h), out_dmin(h),
+                           out_nominal(h), out_uprev(h), 1, s));
   launches += 3;
   h->launches_per_step = launches;
   return EXM_OK;
@@ -631,12 +638,16 @@ exm_status exm_create(const exm_footprint* footprint, const exm_model* model,
   EXM_CUDA_C(dalloc(&h->d_grid, 1));
   EXM_CUDA_C(dalloc(&h->d_eps, KT * D));
   EXM_CUDA_C(dalloc(&h->d_poses, KT));
+  EXM_CUDA_C(dalloc(&h->d_xy, KT));
+  EXM_CUDA_C(dalloc(&h->d_stage, KT));
+  EXM_CUDA_C(dalloc(&h->d_flags, KT));
   EXM_CUDA_C(dalloc(&h->d_base, static_cast<size_t>(h->K)));
   EXM_CUDA_C(dalloc(&h->d_dmin, KT));
   const size_t nblocks_max = (static_cast<size_t>(h->K) + kBlockRollouts - 1) / kBlockRollouts + 8;
   EXM_CUDA_C(dalloc(&h->d_partials, nblocks_max * partial_stride(h->T, D)));
   EXM_CUDA_C(dalloc(&h->d_upd, TD));
   EXM_CUDA_C(dalloc(&h->d_val_poses, static_cast<size_t>(h->T)));
+  EXM_CUDA_C(dalloc(&h->d_val_xy, static_cast<size_t>(h->T)));
   EXM_CUDA_C(dalloc(&h->d_val_base, 1));
   EXM_CUDA_C(dalloc(&h->d_val_dmin, static_cast<size_t>(h->T)));
   h->out_bytes = sizeof(DecisionDev) + sizeof(double) * (h->T + TD + 3);
@@ -664,7 +675,8 @@ void exm_destroy(exm_handle* h) {
   destroy_graphs(h);
   if (h->comm && g_nccl.destroy) g_nccl.destroy(h->comm);
   void* dev[] = {h->d_dyn, h->d_nominal, h->d_guide, h->d_pts, h->d_mask, h->d_tmp, h->d_cloud,
-                 h->d_cell_start, h->d_grid, h->d_eps, h->d_poses, h->d_base, h->d_dmin,
+                 h->d_cell_start, h->d_grid, h->d_eps, h->d_poses, h->d_xy, h->d_stage,
+                 h->d_flags, h->d_val_xy, h->d_base, h->d_dmin,
                  h->d_partials, h->d_upd, h->d_val_poses, h->d_val_base, h->d_val_dmin, h->d_out,
                  h->d_controls, h->d_states, h->d_cost, h->d_unsafe, h->sb_poses, h->sb_pts64,
                  h->sb_pts, h->sb_mask, h->sb_keys, h->sb_min, h->sb_pairs};
@@ -736,13 +748,15 @@ exm_status exm_evaluate_rollouts(exm_handle* h, const double q0[3], const double
   const StepConst& sc = h->sc;
   EXM_CUDA(launch_cloud_prep(h->d_pts, h->d_mask, h->d_dyn, h->fp.radius, h->d_tmp, h->d_cloud,
                              h->d_cell_start, h->d_grid, s));
-  EXM_CUDA(launch_rollout(sc, h->d_dyn, h->d_nominal, h->d_guide, h->guide_cap, h->d_eps,
-                          h->d_poses, h->d_base, controls_out ? h->d_controls : nullptr,
+  EXM_CUDA(launch_rollout(sc, h->d_dyn, h->d_nominal, h->d_eps, h->d_poses, h->d_xy, h->d_base,
+                          controls_out ? h->d_controls : nullptr,
                           states_out ? h->d_states : nullptr, s));
   EXM_CUDA(launch_sdf_grid(h->fp, h->d_poses, static_cast<int>(KT), h->d_grid, h->d_cell_start,
                            h->d_cloud, h->d_dmin, s));
-  EXM_CUDA(launch_block_partials(sc, h->d_base, h->d_dmin, h->d_eps, nullptr, h->d_cost,
-                                 h->d_unsafe, s));
+  EXM_CUDA(launch_stage_costs(sc, h->d_dyn, h->d_guide, h->guide_cap, h->d_xy, h->d_dmin,
+                              h->d_stage, h->d_flags, s));
+  EXM_CUDA(launch_block_partials(sc, h->d_base, h->d_stage, h->d_flags, h->d_eps, nullptr,
+                                 h->d_cost, h->d_unsafe, s));
   if (controls_out)
     EXM_CUDA(cudaMemcpyAsync(controls_out, h->d_controls, KT * h->D * sizeof(double), cudaMemcpyDeviceToHost, s));
   if (states_out)
@@ -792,12 +806,13 @@ exm_status exm_validate_nominal(exm_handle* h, const double* nominal, const doub
   const StepConst& sc = h->sc;
   EXM_CUDA(launch_cloud_prep(h->d_pts, h->d_mask, h->d_dyn, h->fp.radius, h->d_tmp, h->d_cloud,
                              h->d_cell_start, h->d_grid, s));
-  EXM_CUDA(launch_update(sc, nullptr, h->d_nominal, h->d_dyn, h->d_guide, h->guide_cap, h->d_upd,
-                         h->d_val_poses, h->d_val_base, out_dec(h), 0, s));
+  EXM_CUDA(launch_update(sc, nullptr, h->d_nominal, h->d_dyn, h->d_upd, h->d_val_poses,
+                         h->d_val_xy, h->d_val_base, out_dec(h), 0, s));
   EXM_CUDA(launch_sdf_grid(h->fp, h->d_val_poses, sc.T, h->d_grid, h->d_cell_start, h->d_cloud,
                            h->d_val_dmin, s));
-  EXM_CUDA(launch_finalize(sc, h->d_val_dmin, h->d_val_base, h->d_upd, h->d_nominal, h->d_dyn,
-                           out_dec(h), out_dmin(h), nullptr, nullptr, 0, s));
+  EXM_CUDA(launch_finalize(sc, h->d_val_dmin, h->d_val_xy, h->d_val_base, h->d_upd, h->d_guide,
+                           h->guide_cap, h->d_nominal, h->d_dyn, out_dec(h), out_dmin(h), nullptr,
+                           nullptr, 0, s));
   EXM_CUDA(cudaMemcpyAsync(h->h_out, h->d_out, h->out_bytes, cudaMemcpyDeviceToHost, s));
   EXM_CUDA(cudaStreamSynchronize(s));
   const DecisionDev* d = reinterpret_cast<const DecisionDev*>(h->h_out);

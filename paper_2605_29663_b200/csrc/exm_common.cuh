@@ -80,23 +80,26 @@ cudaError_t launch_cloud_prep(const double* pts, const uint8_t* mask, const Step
                               float radius, float2* tmp, float2* cloud, int* cell_start,
                               GridMeta* gm, cudaStream_t s);
 cudaError_t launch_rollout(const StepConst& sc, const StepDyn* dyn, const double* nominal,
-                           const double* guide, int guide_cap, const double* eps, float4* poses,
-                           double* base_cost, double* controls_out, double* states_out,
-                           cudaStream_t s);
+                           const double* eps, float4* poses, double2* xy, double* base_cost,
+                           double* controls_out, double* states_out, cudaStream_t s);
 cudaError_t launch_sdf_grid(const FpDev& fp, const float4* poses, int n_poses,
                             const GridMeta* gm, const int* cell_start, const float2* cloud,
                             float* out, cudaStream_t s);
+cudaError_t launch_stage_costs(const StepConst& sc, const StepDyn* dyn, const double* guide,
+                               int guide_cap, const double2* xy, const float* dmin,
+                               double* stage, uint8_t* flags, cudaStream_t s);
 cudaError_t launch_block_partials(const StepConst& sc, const double* base_cost,
-                                  const float* dmin, const double* eps, double* partials,
-                                  double* cost_out, uint8_t* unsafe_out, cudaStream_t s);
+                                  const double* stage, const uint8_t* flags, const double* eps,
+                                  double* partials, double* cost_out, uint8_t* unsafe_out,
+                                  cudaStream_t s);
 cudaError_t launch_update(const StepConst& sc, const double* partials, const double* nominal,
-                          const StepDyn* dyn, const double* guide, int guide_cap, double* upd,
-                          float4* val_poses, double* val_base, DecisionDev* dec,
-                          int merge, cudaStream_t s);
-cudaError_t launch_finalize(const StepConst& sc, const float* val_dmin, const double* val_base,
-                            const double* upd, double* nominal, StepDyn* dyn, DecisionDev* dec,
-                            double* out_dmin, double* out_nominal, double* out_uprev,
-                            int commit, cudaStream_t s);
+                          const StepDyn* dyn, double* upd, float4* val_poses, double2* val_xy,
+                          double* val_base, DecisionDev* dec, int merge, cudaStream_t s);
+cudaError_t launch_finalize(const StepConst& sc, const float* val_dmin, const double2* val_xy,
+                            const double* val_base, const double* upd, const double* guide,
+                            int guide_cap, double* nominal, StepDyn* dyn, DecisionDev* dec,
+                            double* out_dmin, double* out_nominal, double* out_uprev, int commit,
+                            cudaStream_t s);
 cudaError_t launch_recentre(const double* pts, int n, double cx, double cy, float2* out,
                             cudaStream_t s);
 cudaError_t launch_sdf_pairs(const FpDev& fp, const float4* poses, int n_poses,

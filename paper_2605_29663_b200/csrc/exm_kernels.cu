@@ -51,6 +51,36 @@ __device__ __forceinline__ double unit_oc(uint64_t h) {  // (0, 1]
   return static_cast<double>((h >> 11) + 1) * 0x1.0p-53;
 }
 
+// ---- TMA bulk copy (cp.async.bulk global -> shared, mbarrier completion) -------------
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void tma_bulk_g2s(void* dst, const void* src, unsigned bytes,
+                                             uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tWAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
 // ------------------------------------------------------------------ FP64 scalar helpers
 // std::min / std::max / std::clamp with libstdc++'s comparison order.
 __device__ __forceinline__ double mn(double a, double b) { return (b < a) ? b : a; }
@@ -66,12 +96,19 @@ __device__ __forceinline__ double wrap_angle(double a) {  // geometry.cpp:17-23
   return a;
 }
 
-// clamp_control, kinematics.cpp:99-117
+template <int TAG>
+__host__ __device__ constexpr int model_dim() {  // kinematics.cpp:14-26
+  return (TAG == EXM_MODEL_DIFF || TAG == EXM_MODEL_ACKERMANN) ? 2 : (TAG == EXM_MODEL_OMNI ? 3 : 1);
+}
+
+// clamp_control, kinematics.cpp:99-117 (model known at compile time: everything in registers)
+template <int TAG>
 __device__ __forceinline__ void clamp_control(const StepConst& sc, const double* u,
                                               const double* prev, double* out) {
-  for (int i = 0; i < sc.D; ++i) {
+#pragma unroll
+  for (int i = 0; i < model_dim<TAG>(); ++i) {
     double lo = sc.vel_min[i], hi = sc.vel_max[i];
-    if (sc.tag == EXM_MODEL_ACKERMANN && i == 1) {
+    if (TAG == EXM_MODEL_ACKERMANN && i == 1) {
       lo = mx(lo, -sc.steer_max);
       hi = mn(hi, sc.steer_max);
     }
@@ -81,16 +118,15 @@ __device__ __forceinline__ void clamp_control(const StepConst& sc, const double*
 }
 
 // derivative + step, kinematics.cpp:75-97 (cos/sin of the pre-step heading supplied)
+template <int TAG>
 __device__ __forceinline__ void euler_step(const StepConst& sc, double q[3], const double* u,
                                            double ct, double st) {
   double fx = 0.0, fy = 0.0, fth = 0.0;
-  switch (sc.tag) {
-    case EXM_MODEL_DIFF: fx = u[0] * ct; fy = u[0] * st; fth = u[1]; break;
-    case EXM_MODEL_ACKERMANN: fx = u[0] * ct; fy = u[0] * st; fth = u[0] / sc.wheelbase * tan(u[1]); break;
-    case EXM_MODEL_OMNI: fx = u[0] * ct - u[1] * st; fy = u[0] * st + u[1] * ct; fth = u[2]; break;
-    case EXM_MODEL_SPIN: fth = u[0]; break;
-    case EXM_MODEL_PARALLEL: fx = -u[0] * st; fy = u[0] * ct; break;
-  }
+  if (TAG == EXM_MODEL_DIFF) { fx = u[0] * ct; fy = u[0] * st; fth = u[1]; }
+  if (TAG == EXM_MODEL_ACKERMANN) { fx = u[0] * ct; fy = u[0] * st; fth = u[0] / sc.wheelbase * tan(u[1]); }
+  if (TAG == EXM_MODEL_OMNI) { fx = u[0] * ct - u[1] * st; fy = u[0] * st + u[1] * ct; fth = u[2]; }
+  if (TAG == EXM_MODEL_SPIN) { fth = u[0]; }
+  if (TAG == EXM_MODEL_PARALLEL) { fx = -u[0] * st; fy = u[0] * ct; }
   q[0] = q[0] + fx * sc.dt;
   q[1] = q[1] + fy * sc.dt;
   q[2] = q[2] + fth * sc.dt;
@@ -139,9 +175,11 @@ __device__ __forceinline__ double terminal_cost(const StepConst& sc, const doubl
   return sc.w_goal_pos * (dx * dx + dy * dy) + sc.w_goal_head * e * e;
 }
 
+template <int TAG>
 __device__ __forceinline__ double control_cost(const StepConst& sc, const double* u) {
   double s = 0.0;
-  for (int i = 0; i < sc.D; ++i) s += u[i] * u[i];
+#pragma unroll
+  for (int i = 0; i < model_dim<TAG>(); ++i) s += u[i] * u[i];
   return sc.w_ctrl * s;
 }
 
@@ -150,31 +188,40 @@ __device__ __forceinline__ double obstacle_cost(const StepConst& sc, double d) {
   return sc.w_coll * (d < 0.0 ? 1.0 : 0.0) + sc.w_rep * m * m;
 }
 
-// One rollout of T steps (score_rollout without the SDF): emits recentred FP32 poses for the
-// SDF kernel and returns task + control + terminal cost. eps_row may be null (validation).
-__device__ double rollout_one(const StepConst& sc, const StepDyn& dyn, const double* nominal,
-                              const double* eps_row, const double* g, int ng,
-                              float4* poses_row, double* controls_row, double* states_row) {
-  const int T = sc.T, D = sc.D;
+// Serial part of one rollout (score_rollout, controller.cpp:151-169, minus the SDF and the
+// task cost): u = nominal + eps, sequential clamp from u_prev, Euler step. Emits the recentred
+// FP32 pose (x, y, cos, sin) and the FP64 position of every pre-step state; returns the
+// control cost summed over h plus the terminal goal cost. The per-step task cost is
+// independent across (r, h) and is computed in parallel by k_stage_costs.
+template <int TAG>
+__device__ double rollout_dyn(const StepConst& sc, const StepDyn& dyn, const double* nominal,
+                              const double* eps_row, float4* poses_row, double2* xy_row,
+                              double* controls_row, double* states_row) {
+  constexpr int D = model_dim<TAG>();
+  const int T = sc.T;
   double prev[3] = {dyn.u_prev[0], dyn.u_prev[1], dyn.u_prev[2]};
   double q[3] = {dyn.q0[0], dyn.q0[1], dyn.q0[2]};
+  const double qx0 = dyn.q0[0], qy0 = dyn.q0[1];
   double base = 0.0;
   if (states_row) { states_row[0] = q[0]; states_row[1] = q[1]; states_row[2] = q[2]; }
   for (int h = 0; h < T; ++h) {
     double u[3] = {0.0, 0.0, 0.0}, uc[3] = {0.0, 0.0, 0.0};
+#pragma unroll
     for (int c = 0; c < D; ++c) u[c] = nominal[h * D + c] + (eps_row ? eps_row[h * D + c] : 0.0);
-    clamp_control(sc, u, prev, uc);
+    clamp_control<TAG>(sc, u, prev, uc);
+#pragma unroll
     for (int c = 0; c < D; ++c) prev[c] = uc[c];
-    if (controls_row)
+    if (controls_row) {
+#pragma unroll
       for (int c = 0; c < D; ++c) controls_row[h * D + c] = uc[c];
+    }
     double st, ct;
     sincos(q[2], &st, &ct);
-    poses_row[h] = make_float4(static_cast<float>(q[0] - dyn.q0[0]),
-                               static_cast<float>(q[1] - dyn.q0[1]), static_cast<float>(ct),
-                               static_cast<float>(st));
-    base += task_cost(sc, q, g, ng, dyn.goal, false);
-    base += control_cost(sc, uc);
-    euler_step(sc, q, uc, ct, st);
+    poses_row[h] = make_float4(static_cast<float>(q[0] - qx0), static_cast<float>(q[1] - qy0),
+                               static_cast<float>(ct), static_cast<float>(st));
+    xy_row[h] = make_double2(q[0], q[1]);
+    base += control_cost<TAG>(sc, uc);
+    euler_step<TAG>(sc, q, uc, ct, st);
     if (states_row) {
       states_row[3 * (h + 1)] = q[0];
       states_row[3 * (h + 1) + 1] = q[1];
@@ -182,6 +229,14 @@ __device__ double rollout_one(const StepConst& sc, const StepDyn& dyn, const dou
     }
   }
   return base + terminal_cost(sc, q, dyn.goal);
+}
+
+// Running cost of one pre-step state: task_cost (controller.cpp:103-118, non-terminal) +
+// obstacle_cost (controller.cpp:98-101).
+__device__ __forceinline__ double stage_cost(const StepConst& sc, double2 xy, double d,
+                                             const double* g, int ng, const double* goal) {
+  const double q[3] = {xy.x, xy.y, 0.0};
+  return task_cost(sc, q, g, ng, goal, false) + obstacle_cost(sc, d);
 }
 
 // ------------------------------------------------------------------ FP32 signed distance
@@ -253,6 +308,17 @@ template <int KIND, int NB>
 __device__ __forceinline__ float sd_body(const FpDev& fp, float px, float py) {
   if constexpr (KIND == EXM_FOOTPRINT_POLYGON) return sd_polygon<NB>(fp, px, py);
   else return sd_rect<NB>(fp, px, py);
+}
+
+// Exact second-level cull on the body-frame point: the footprint lies inside its AABB, so an
+// exterior point's signed distance is at least its distance to the AABB. Points inside the
+// AABB (distance 0) may be inside the footprint and are always evaluated.
+__device__ __forceinline__ bool aabb_may_beat(const FpDev& fp, float bx, float by, float best) {
+  const float ax = fmaxf(fmaxf(fp.aabb[0] - bx, bx - fp.aabb[1]), 0.f);
+  const float ay = fmaxf(fmaxf(fp.aabb[2] - by, by - fp.aabb[3]), 0.f);
+  const float a2 = fmaf(ax, ax, ay * ay);
+  const float lim = best + kCullMargin;
+  return a2 == 0.f || (lim > 0.f && a2 < lim * lim);
 }
 
 // Order-preserving float -> u32 key (for min via integer reductions / atomics).
@@ -408,25 +474,63 @@ __global__ void __launch_bounds__(1024) k_cloud_prep(const double* __restrict__ 
   }
 }
 
+template <int TAG>
 __global__ void k_rollout(const StepConst sc, const StepDyn* __restrict__ dynp,
-                          const double* __restrict__ nominal, const double* __restrict__ guide,
-                          const double* __restrict__ eps, float4* __restrict__ poses,
+                          const double* __restrict__ nominal, const double* __restrict__ eps,
+                          float4* __restrict__ poses, double2* __restrict__ xy,
                           double* __restrict__ base_cost, double* __restrict__ controls_out,
                           double* __restrict__ states_out) {
-  extern __shared__ double sm[];
-  const StepDyn dyn = *dynp;
-  const int ng = dyn.n_guide;
-  double* g = sm;
-  double* nom = sm + 2 * ng;
-  for (int i = threadIdx.x; i < 2 * ng; i += blockDim.x) g[i] = guide[i];
-  for (int i = threadIdx.x; i < sc.T * sc.D; i += blockDim.x) nom[i] = nominal[i];
+  // One warp per CTA: only K threads exist, so spread them over SMs. The CTA's perturbation
+  // rows (one contiguous block) are staged into shared memory by a single TMA bulk copy, so
+  // the sequential h-loop never waits on global memory.
+  extern __shared__ __align__(16) double sm[];
+  __shared__ __align__(8) uint64_t bar;
+  const int TD = sc.T * sc.D;
+  double* nom = sm;
+  double* e_s = sm + ((TD + 1) & ~1);  // 16-byte aligned
+  const int r0 = blockIdx.x * blockDim.x;
+  const int nr = min(static_cast<int>(blockDim.x), sc.k_local - r0);
+  const double* src = eps + static_cast<size_t>(r0) * TD;
+  const unsigned bytes = static_cast<unsigned>(nr) * TD * sizeof(double);
+  const unsigned bulk = bytes & ~15u;
+  if (threadIdx.x == 0) {
+    mbar_init(&bar, 1);
+    if (bulk) {
+      mbar_expect_tx(&bar, bulk);
+      tma_bulk_g2s(e_s, src, bulk, &bar);
+    }
+    if (bytes != bulk) e_s[bulk / sizeof(double)] = src[bulk / sizeof(double)];
+  }
+  for (int i = threadIdx.x; i < TD; i += blockDim.x) nom[i] = nominal[i];
   __syncthreads();
-  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (bulk) mbar_wait(&bar, 0);
+  const StepDyn dyn = *dynp;
+  __syncthreads();
+  const int r = r0 + threadIdx.x;
   if (r >= sc.k_local) return;
   const size_t row = static_cast<size_t>(r) * sc.T;
-  base_cost[r] = rollout_one(sc, dyn, nom, eps + row * sc.D, g, ng, poses + row,
+  base_cost[r] = rollout_dyn<TAG>(sc, dyn, nom, e_s + threadIdx.x * TD, poses + row, xy + row,
                              controls_out ? controls_out + row * sc.D : nullptr,
                              states_out ? states_out + static_cast<size_t>(r) * (sc.T + 1) * 3 : nullptr);
+}
+
+// Task + obstacle cost and the unsafe flag of every (r, h), in parallel. Thread i = h*K + r
+// writes stage[h*K + r] (h-major, so the per-rollout sums in k_block_partials coalesce).
+__global__ void k_stage_costs(const StepConst sc, const StepDyn* __restrict__ dynp,
+                              const double* __restrict__ guide, const double2* __restrict__ xy,
+                              const float* __restrict__ dmin, double* __restrict__ stage,
+                              uint8_t* __restrict__ flags) {
+  extern __shared__ double g[];
+  const int ng = dynp->n_guide;
+  for (int i = threadIdx.x; i < 2 * ng; i += blockDim.x) g[i] = guide[i];
+  __syncthreads();
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= sc.k_local * sc.T) return;
+  const int h = i / sc.k_local, r = i % sc.k_local;
+  const size_t src = static_cast<size_t>(r) * sc.T + h;
+  const double d = static_cast<double>(dmin[src]);
+  stage[i] = stage_cost(sc, xy[src], d, g, ng, dynp->goal);
+  flags[i] = d < sc.d_safe ? 1 : 0;
 }
 
 // Ring c (Chebyshev radius k >= 1) around (ci, cj): 8k cells, enumerated row/column-wise.
@@ -509,7 +613,7 @@ __global__ void __launch_bounds__(128) k_sdf_grid(const __grid_constant__ FpDev 
           if (dx * dx + dy * dy < l2 * l2) {
             const float bx = fmaf(q.z, dx, q.w * dy);
             const float by = fmaf(q.z, dy, -(q.w * dx));
-            best = fminf(best, sd_body<KIND, NB>(fp, bx, by));
+            if (aabb_may_beat(fp, bx, by, best)) best = fminf(best, sd_body<KIND, NB>(fp, bx, by));
           }
         }
       }
@@ -518,12 +622,107 @@ __global__ void __launch_bounds__(128) k_sdf_grid(const __grid_constant__ FpDev 
   if (active) out[i] = best;
 }
 
-// Obstacle cost, unsafe flag, augmented cost and the min-shifted softmax partial of one
-// block of kBlockRollouts rollouts (fixed tree => deterministic, independent of sharding).
+// Warp <-> pose variant for few poses (the T validation poses). Per ring, the lanes first
+// claim cells that pass the box bound, then stride together over the concatenation of those
+// cells' points (a shuffle search maps a flat index to its cell), so the loads coalesce and
+// all lanes stay busy; the warp minimum after every chunk drives the exact termination.
+template <int KIND, int NB>
+__global__ void __launch_bounds__(128) k_sdf_grid_warp(const __grid_constant__ FpDev fp,
+                                                       const float4* __restrict__ poses, int n_poses,
+                                                       const GridMeta* __restrict__ gmp,
+                                                       const int* __restrict__ cell_start,
+                                                       const float2* __restrict__ cloud,
+                                                       float* __restrict__ out) {
+  const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (w >= n_poses) return;  // warp-uniform
+  const GridMeta gm = *gmp;
+  if (gm.n_valid == 0) {
+    if (lane == 0) out[w] = kEmptyDistance;
+    return;
+  }
+  const float4 q = poses[w];
+  const int ci = min(gm.gx - 1, max(0, static_cast<int>(floorf((q.x - gm.x0) * gm.inv_cs))));
+  const int cj = min(gm.gy - 1, max(0, static_cast<int>(floorf((q.y - gm.y0) * gm.inv_cs))));
+  const float R = fp.radius + kCullMargin;
+  float best = __int_as_float(0x7f800000);
+  const int kmax = max(max(ci, gm.gx - 1 - ci), max(cj, gm.gy - 1 - cj));
+  for (int k = 0; k <= kmax; ++k) {
+    if (k > 0) {
+      const float bx0 = gm.x0 + static_cast<float>(ci - k + 1) * gm.cs;
+      const float bx1 = gm.x0 + static_cast<float>(ci + k) * gm.cs;
+      const float by0 = gm.y0 + static_cast<float>(cj - k + 1) * gm.cs;
+      const float by1 = gm.y0 + static_cast<float>(cj + k) * gm.cs;
+      const float lb = fmaxf(fminf(fminf(q.x - bx0, bx1 - q.x), fminf(q.y - by0, by1 - q.y)), 0.f);
+      if (!(lb < R + best)) break;  // best is warp-uniform here
+    }
+    const int ncell = k == 0 ? 1 : 8 * k;
+    for (int t0 = 0; t0 < ncell; t0 += 32) {
+      const int t = t0 + lane;
+      int cnt = 0, st = 0;
+      if (t < ncell) {
+        int ii, jj;
+        ring_cell(k, t, ci, cj, ii, jj);
+        if (ii >= 0 && jj >= 0 && ii < gm.gx && jj < gm.gy) {
+          const int c = jj * gm.gx + ii;
+          const float bx0 = gm.x0 + static_cast<float>(ii) * gm.cs, bx1 = bx0 + gm.cs;
+          const float by0 = gm.y0 + static_cast<float>(jj) * gm.cs, by1 = by0 + gm.cs;
+          const float gx_ = fmaxf(fmaxf(bx0 - q.x, q.x - bx1), 0.f);
+          const float gy_ = fmaxf(fmaxf(by0 - q.y, q.y - by1), 0.f);
+          const float lim = R + best;
+          if (gx_ * gx_ + gy_ * gy_ < lim * lim) {
+            st = __ldg(cell_start + c);
+            cnt = __ldg(cell_start + c + 1) - st;
+          }
+        }
+      }
+      int incl = cnt;
+      for (int o = 1; o < 32; o <<= 1) {
+        const int v = __shfl_up_sync(kFull, incl, o);
+        if (lane >= o) incl += v;
+      }
+      const int total = __shfl_sync(kFull, incl, 31);
+      float mine = best;
+      for (int b = 0; b < total; b += 32) {
+        const int i = b + lane;
+        // owner = first lane whose inclusive prefix exceeds i
+        int lo = 0;
+        for (int step = 16; step; step >>= 1) {
+          const int probe = __shfl_sync(kFull, incl, lo + step - 1);
+          if (probe <= i) lo += step;
+        }
+        const int o_incl = __shfl_sync(kFull, incl, lo);
+        const int o_cnt = __shfl_sync(kFull, cnt, lo);
+        const int o_st = __shfl_sync(kFull, st, lo);
+        if (i < total) {
+          const float2 o = __ldg(cloud + o_st + (i - (o_incl - o_cnt)));
+          const float dx = o.x - q.x, dy = o.y - q.y;
+          const float l2 = R + mine;
+          if (dx * dx + dy * dy < l2 * l2) {
+            const float bx = fmaf(q.z, dx, q.w * dy);
+            const float by = fmaf(q.z, dy, -(q.w * dx));
+            if (aabb_may_beat(fp, bx, by, mine)) mine = fminf(mine, sd_body<KIND, NB>(fp, bx, by));
+          }
+        }
+      }
+      for (int o = 16; o; o >>= 1) mine = fminf(mine, __shfl_xor_sync(kFull, mine, o));
+      best = mine;
+    }
+  }
+  if (lane == 0) out[w] = best;
+}
+
+// Augmented cost and the min-shifted softmax partial of one block of kBlockRollouts rollouts
+// (fixed block size and fixed reduction trees: deterministic and independent of sharding).
+//   J_r = (ctrl + terminal)_r + sum_h stage[h][r]       controller.cpp:164-171
+//   Jt_r = J_r + w_inf * unsafe_r                       controller.cpp:310-312
+//   {beta_b, S_b, A_b, argmin_b, U_b[T*D]}              controller.cpp:222-233, :316-328
 __global__ void __launch_bounds__(kBlockRollouts) k_block_partials(
-    const StepConst sc, const double* __restrict__ base_cost, const float* __restrict__ dmin,
-    const double* __restrict__ eps, double* __restrict__ partials, double* __restrict__ cost_out,
+    const StepConst sc, const double* __restrict__ base_cost, const double* __restrict__ stage,
+    const uint8_t* __restrict__ flags, const double* __restrict__ eps,
+    double* __restrict__ partials, double* __restrict__ cost_out,
     uint8_t* __restrict__ unsafe_out) {
+  extern __shared__ double s_u[];  // [warps][T*D]
   __shared__ double s_e[kBlockRollouts];
   __shared__ double s_v[kBlockRollouts / 32];
   __shared__ double s_a[kBlockRollouts / 32];
@@ -531,20 +730,20 @@ __global__ void __launch_bounds__(kBlockRollouts) k_block_partials(
   __shared__ double s_beta;
   __shared__ int s_arg;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  constexpr int kWarps = kBlockRollouts / 32;
   const int r0 = blockIdx.x * kBlockRollouts;
   const int r = r0 + tid;
   const bool valid = r < sc.k_local;
+  const int K = sc.k_local;
   double jt = HUGE_VAL;
   if (valid) {
-    double obs = 0.0;
-    bool bad = false;
-    const float* drow = dmin + static_cast<size_t>(r) * sc.T;
+    double J = base_cost[r];
+    unsigned bad = 0;
+#pragma unroll 10
     for (int h = 0; h < sc.T; ++h) {
-      const double d = static_cast<double>(drow[h]);
-      bad = bad || (d < sc.d_safe);
-      obs += obstacle_cost(sc, d);
+      J += stage[static_cast<size_t>(h) * K + r];
+      bad |= flags[static_cast<size_t>(h) * K + r];
     }
-    const double J = base_cost[r] + obs;
     if (cost_out) cost_out[r] = J;
     if (unsafe_out) unsafe_out[r] = bad ? 1 : 0;
     jt = bad ? J + sc.w_inf : J;
@@ -563,7 +762,7 @@ __global__ void __launch_bounds__(kBlockRollouts) k_block_partials(
   if (tid == 0) {
     double b = s_v[0];
     int bi = s_i[0];
-    for (int w = 1; w < kBlockRollouts / 32; ++w)
+    for (int w = 1; w < kWarps; ++w)
       if (s_v[w] < b || (s_v[w] == b && s_i[w] < bi)) { b = s_v[w]; bi = s_i[w]; }
     s_beta = b;
     s_arg = bi;
@@ -585,42 +784,52 @@ __global__ void __launch_bounds__(kBlockRollouts) k_block_partials(
   double* out = partials + static_cast<size_t>(sc.block_offset + blockIdx.x) * stride;
   if (tid == 0) {
     double S = 0.0, A = 0.0;
-    for (int w = 0; w < kBlockRollouts / 32; ++w) { S += s_v[w]; A += s_a[w]; }
+    for (int w = 0; w < kWarps; ++w) { S += s_v[w]; A += s_a[w]; }
     out[0] = beta;
     out[1] = S;
     out[2] = A;
     out[3] = static_cast<double>(s_arg);
   }
-  const int nv = min(kBlockRollouts, sc.k_local - r0);
+  // U_b[o] = sum_r e_r eps[r][o]: warp w sums its 32 rollouts (lanes over o, coalesced rows),
+  // then the kWarps warp sums are added in warp order.
   const int TD = sc.T * sc.D;
-  const double* erow = eps + static_cast<size_t>(r0) * TD;
+  const int nv = min(kBlockRollouts, sc.k_local - r0);
+  const int j0 = warp * 32, j1 = min(nv, j0 + 32);
+  for (int o = lane; o < TD; o += 32) {
+    double acc = 0.0;
+#pragma unroll 8
+    for (int j = j0; j < j1; ++j) acc += s_e[j] * eps[static_cast<size_t>(r0 + j) * TD + o];
+    s_u[warp * TD + o] = acc;
+  }
+  __syncthreads();
   for (int o = tid; o < TD; o += blockDim.x) {
     double acc = 0.0;
-    for (int j = 0; j < nv; ++j) acc += s_e[j] * erow[static_cast<size_t>(j) * TD + o];
+    for (int w = 0; w < kWarps; ++w) acc += s_u[w * TD + o];
     out[4 + o] = acc;
   }
 }
 
 // Merge all block partials in block order (every rank does this identically), apply the
-// weighted update, then the sequential clamp + validation rollout (one thread).
+// weighted update u_h += U_h / S (controller.cpp:320-328), then one thread runs the sequential
+// clamp + validation dynamics (controller.cpp:331-340, :254-282).
+template <int TAG>
 __global__ void __launch_bounds__(256) k_update(const StepConst sc,
                                                 const double* __restrict__ partials,
                                                 const double* __restrict__ nominal,
                                                 const StepDyn* __restrict__ dynp,
-                                                const double* __restrict__ guide,
                                                 double* __restrict__ upd,
                                                 float4* __restrict__ val_poses,
+                                                double2* __restrict__ val_xy,
                                                 double* __restrict__ val_base,
                                                 DecisionDev* __restrict__ dec, int merge) {
-  extern __shared__ double sf[];  // nblocks_total factors, then guide
+  extern __shared__ double sm_u[];  // T*D updated controls, then nblocks_total factors
   __shared__ double s_beta, s_S;
   const int tid = threadIdx.x;
   const int nb = sc.nblocks_total;
   const int stride = partial_stride(sc.T, sc.D);
   const int TD = sc.T * sc.D;
-  const StepDyn dyn = *dynp;
-  double* g = sf + (merge ? nb : 0);
-  for (int i = tid; i < 2 * dyn.n_guide; i += blockDim.x) g[i] = guide[i];
+  double* s_upd = sm_u;
+  double* sf = sm_u + TD;
   if (merge) {
     if (tid == 0) {
       double beta = partials[0];
@@ -650,56 +859,69 @@ __global__ void __launch_bounds__(256) k_update(const StepConst sc,
     __syncthreads();
     for (int o = tid; o < TD; o += blockDim.x) {
       double U = 0.0;
+#pragma unroll 8
       for (int b = 0; b < nb; ++b) U += sf[b] * partials[static_cast<size_t>(b) * stride + 4 + o];
-      upd[o] = nominal[o] + U / s_S;
+      s_upd[o] = nominal[o] + U / s_S;
     }
   } else {
-    for (int o = tid; o < TD; o += blockDim.x) upd[o] = nominal[o];
+    for (int o = tid; o < TD; o += blockDim.x) s_upd[o] = nominal[o];
   }
   __syncthreads();
   if (tid == 0) {
-    // rollout_one clamps sequentially from u_prev and writes the clamped sequence back; the
+    // rollout_dyn clamps sequentially from u_prev and writes the clamped sequence back; the
     // reference's second clamp inside validate_nominal is idempotent on it.
-    *val_base = rollout_one(sc, dyn, upd, nullptr, g, dyn.n_guide, val_poses, upd, nullptr);
+    const StepDyn dyn = *dynp;
+    *val_base = rollout_dyn<TAG>(sc, dyn, s_upd, nullptr, val_poses, val_xy, s_upd, nullptr);
   }
+  __syncthreads();
+  for (int o = tid; o < TD; o += blockDim.x) upd[o] = s_upd[o];
 }
 
-__global__ void k_finalize(const StepConst sc, const float* __restrict__ val_dmin,
-                           const double* __restrict__ val_base, const double* __restrict__ upd,
-                           double* __restrict__ nominal, StepDyn* __restrict__ dyn,
-                           DecisionDev* __restrict__ dec, double* __restrict__ out_dmin,
-                           double* __restrict__ out_nominal, double* __restrict__ out_uprev,
-                           int commit) {
-  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+// Validation cost, validity, command and shift / zero-hold (controller.cpp:339-364).
+__global__ void __launch_bounds__(64) k_finalize(
+    const StepConst sc, const float* __restrict__ val_dmin, const double2* __restrict__ val_xy,
+    const double* __restrict__ val_base, const double* __restrict__ upd,
+    const double* __restrict__ guide, double* __restrict__ nominal, StepDyn* __restrict__ dyn,
+    DecisionDev* __restrict__ dec, double* __restrict__ out_dmin,
+    double* __restrict__ out_nominal, double* __restrict__ out_uprev, int commit) {
+  extern __shared__ double sm2[];  // guide (2*ng) then per-step costs (T)
+  __shared__ int s_ok;
+  const int tid = threadIdx.x;
   const int T = sc.T, D = sc.D;
-  double obs = 0.0;
-  int ok = 1;
-  for (int h = 0; h < T; ++h) {
+  const int ng = dyn->n_guide;
+  double* g = sm2;
+  double* c = sm2 + 2 * ng;
+  for (int i = tid; i < 2 * ng; i += blockDim.x) g[i] = guide[i];
+  if (tid == 0) s_ok = 1;
+  __syncthreads();
+  for (int h = tid; h < T; h += blockDim.x) {
     const double d = static_cast<double>(val_dmin[h]);
     if (out_dmin) out_dmin[h] = d;
-    if (d < sc.d_safe) ok = 0;
-    obs += obstacle_cost(sc, d);
+    if (d < sc.d_safe) atomicAnd(&s_ok, 0);
+    c[h] = stage_cost(sc, val_xy[h], d, g, ng, dyn->goal);
   }
-  dec->nominal_cost = *val_base + obs;
-  dec->validated = ok;
+  __syncthreads();
+  const int ok = s_ok;
+  if (tid == 0) {
+    double J = *val_base;
+    for (int h = 0; h < T; ++h) J += c[h];
+    dec->nominal_cost = J;
+    dec->validated = ok;
+  }
   if (!commit) return;
-  double cmd[3] = {0.0, 0.0, 0.0};
-  if (ok) {
-    for (int c = 0; c < D; ++c) cmd[c] = upd[c];
-    for (int h = 0; h + 1 < T; ++h)
-      for (int c = 0; c < D; ++c) nominal[h * D + c] = upd[(h + 1) * D + c];
-    for (int c = 0; c < D; ++c) nominal[(T - 1) * D + c] = upd[(T - 1) * D + c];
-  } else {
-    for (int i = 0; i < T * D; ++i) nominal[i] = 0.0;
+  for (int i = tid; i < T * D; i += blockDim.x) {
+    const int h = i / D;
+    const double v = ok ? upd[(h + 1 < T ? h + 1 : T - 1) * D + i % D] : 0.0;
+    nominal[i] = v;
+    if (out_nominal) out_nominal[i] = v;
   }
-  for (int c = 0; c < 3; ++c) {
-    dec->command[c] = cmd[c];
-    dyn->u_prev[c] = cmd[c];
-    if (out_uprev) out_uprev[c] = cmd[c];
+  if (tid < 3) {
+    const double cmd = (ok && tid < D) ? upd[tid] : 0.0;
+    dec->command[tid] = cmd;
+    dyn->u_prev[tid] = cmd;
+    if (out_uprev) out_uprev[tid] = cmd;
   }
-  if (out_nominal)
-    for (int i = 0; i < T * D; ++i) out_nominal[i] = nominal[i];
-  dyn->cycle += 1;
+  if (tid == 0) dyn->cycle += 1;
 }
 
 __global__ void k_recentre(const double* __restrict__ pts, int n, double cx, double cy,
@@ -708,36 +930,6 @@ __global__ void k_recentre(const double* __restrict__ pts, int n, double cx, dou
   if (i >= n) return;
   const double2 w = reinterpret_cast<const double2*>(pts)[i];
   out[i] = make_float2(static_cast<float>(w.x - cx), static_cast<float>(w.y - cy));
-}
-
-// ---- TMA bulk copy (cp.async.bulk global -> shared, mbarrier completion) -------------
-__device__ __forceinline__ unsigned smem_u32(const void* p) {
-  return static_cast<unsigned>(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
-  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
-               "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void tma_bulk_g2s(void* dst, const void* src, unsigned bytes,
-                                             uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-          smem_u32(dst)),
-      "l"(src), "r"(bytes), "r"(smem_u32(bar))
-      : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n\tWAIT_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
-      "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
-      "r"(parity)
-      : "memory");
 }
 
 constexpr int kPairThreads = 256;
@@ -1062,6 +1254,18 @@ struct GridLaunch {
 };
 
 template <int KIND, int NB>
+struct GridWarpLaunch {
+  static cudaError_t run(const FpDev& fp, const float4* poses, int n_poses, const GridMeta* gm,
+                         const int* cell_start, const float2* cloud, float* out, cudaStream_t s) {
+    if (n_poses <= 0) return cudaSuccess;
+    const int threads = 128, warps = threads / 32;
+    k_sdf_grid_warp<KIND, NB><<<(n_poses + warps - 1) / warps, threads, 0, s>>>(
+        fp, poses, n_poses, gm, cell_start, cloud, out);
+    return cudaGetLastError();
+  }
+};
+
+template <int KIND, int NB>
 struct PairsLaunch {
   static cudaError_t run(const FpDev& fp, const float4* poses, int n_poses, const float2* pts,
                          const uint8_t* mask, int n_points, float* per_pair, unsigned* keys,
@@ -1106,59 +1310,118 @@ cudaError_t launch_cloud_prep(const double* pts, const uint8_t* mask, const Step
   return cudaGetLastError();
 }
 
-cudaError_t launch_rollout(const StepConst& sc, const StepDyn* dyn, const double* nominal,
-                                const double* guide, int guide_cap, const double* eps,
-                                float4* poses, double* base_cost, double* controls_out,
-                                double* states_out, cudaStream_t s) {
-  const int threads = 128;
-  const size_t smem = sizeof(double) * (2 * static_cast<size_t>(guide_cap) + sc.T * sc.D);
+template <int TAG>
+cudaError_t rollout_tag(const StepConst& sc, const StepDyn* dyn, const double* nominal,
+                        const double* eps, float4* poses, double2* xy, double* base_cost,
+                        double* controls_out, double* states_out, cudaStream_t s) {
+  const int threads = 32;  // K threads only: one warp per CTA spreads them over all SMs
+  const size_t smem = sizeof(double) * (static_cast<size_t>(sc.T) * sc.D * (threads + 1) + 2);
   if (smem > 48 * 1024) {
-    cudaError_t e = cudaFuncSetAttribute(k_rollout, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaError_t e = cudaFuncSetAttribute(k_rollout<TAG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(smem));
     if (e != cudaSuccess) return e;
   }
-  k_rollout<<<(sc.k_local + threads - 1) / threads, threads, smem, s>>>(
-      sc, dyn, nominal, guide, eps, poses, base_cost, controls_out, states_out);
+  k_rollout<TAG><<<(sc.k_local + threads - 1) / threads, threads, smem, s>>>(
+      sc, dyn, nominal, eps, poses, xy, base_cost, controls_out, states_out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_rollout(const StepConst& sc, const StepDyn* dyn, const double* nominal,
+                           const double* eps, float4* poses, double2* xy, double* base_cost,
+                           double* controls_out, double* states_out, cudaStream_t s) {
+  switch (sc.tag) {
+    case EXM_MODEL_DIFF: return rollout_tag<EXM_MODEL_DIFF>(sc, dyn, nominal, eps, poses, xy, base_cost, controls_out, states_out, s);
+    case EXM_MODEL_ACKERMANN: return rollout_tag<EXM_MODEL_ACKERMANN>(sc, dyn, nominal, eps, poses, xy, base_cost, controls_out, states_out, s);
+    case EXM_MODEL_OMNI: return rollout_tag<EXM_MODEL_OMNI>(sc, dyn, nominal, eps, poses, xy, base_cost, controls_out, states_out, s);
+    case EXM_MODEL_SPIN: return rollout_tag<EXM_MODEL_SPIN>(sc, dyn, nominal, eps, poses, xy, base_cost, controls_out, states_out, s);
+    case EXM_MODEL_PARALLEL: return rollout_tag<EXM_MODEL_PARALLEL>(sc, dyn, nominal, eps, poses, xy, base_cost, controls_out, states_out, s);
+  }
+  return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_stage_costs(const StepConst& sc, const StepDyn* dyn, const double* guide,
+                               int guide_cap, const double2* xy, const float* dmin,
+                               double* stage, uint8_t* flags, cudaStream_t s) {
+  const int n = sc.k_local * sc.T;
+  if (n <= 0) return cudaSuccess;
+  const size_t smem = sizeof(double) * 2 * static_cast<size_t>(guide_cap);
+  if (smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(k_stage_costs, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(smem));
+    if (e != cudaSuccess) return e;
+  }
+  k_stage_costs<<<(n + 255) / 256, 256, smem, s>>>(sc, dyn, guide, xy, dmin, stage, flags);
   return cudaGetLastError();
 }
 
 cudaError_t launch_sdf_grid(const FpDev& fp, const float4* poses, int n_poses,
                             const GridMeta* gm, const int* cell_start, const float2* cloud,
                             float* out, cudaStream_t s) {
+  // Few poses (validation rollout, single queries): one warp per pose keeps all lanes busy.
+  if (n_poses <= 4096)
+    return dispatch_fp<GridWarpLaunch>(fp, poses, n_poses, gm, cell_start, cloud, out, s);
   return dispatch_fp<GridLaunch>(fp, poses, n_poses, gm, cell_start, cloud, out, s);
 }
 
 cudaError_t launch_block_partials(const StepConst& sc, const double* base_cost,
-                                  const float* dmin, const double* eps, double* partials,
-                                  double* cost_out, uint8_t* unsafe_out, cudaStream_t s) {
+                                  const double* stage, const uint8_t* flags, const double* eps,
+                                  double* partials, double* cost_out, uint8_t* unsafe_out,
+                                  cudaStream_t s) {
   if (sc.nblocks_local <= 0) return cudaSuccess;
-  k_block_partials<<<sc.nblocks_local, kBlockRollouts, 0, s>>>(sc, base_cost, dmin, eps, partials,
-                                                              cost_out, unsafe_out);
+  const size_t smem = sizeof(double) * (kBlockRollouts / 32) * static_cast<size_t>(sc.T) * sc.D;
+  if (smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(k_block_partials,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(smem));
+    if (e != cudaSuccess) return e;
+  }
+  k_block_partials<<<sc.nblocks_local, kBlockRollouts, smem, s>>>(
+      sc, base_cost, stage, flags, eps, partials, cost_out, unsafe_out);
+  return cudaGetLastError();
+}
+
+template <int TAG>
+cudaError_t update_tag(const StepConst& sc, const double* partials, const double* nominal,
+                       const StepDyn* dyn, double* upd, float4* val_poses, double2* val_xy,
+                       double* val_base, DecisionDev* dec, int merge, cudaStream_t s) {
+  const size_t smem = sizeof(double) * (static_cast<size_t>(sc.T) * sc.D +
+                                        static_cast<size_t>(merge ? sc.nblocks_total : 1));
+  if (smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(k_update<TAG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(smem));
+    if (e != cudaSuccess) return e;
+  }
+  k_update<TAG><<<1, 256, smem, s>>>(sc, partials, nominal, dyn, upd, val_poses, val_xy, val_base,
+                                     dec, merge);
   return cudaGetLastError();
 }
 
 cudaError_t launch_update(const StepConst& sc, const double* partials, const double* nominal,
-                          const StepDyn* dyn, const double* guide, int guide_cap, double* upd,
-                          float4* val_poses, double* val_base, DecisionDev* dec, int merge,
-                          cudaStream_t s) {
-  const size_t smem = sizeof(double) * (static_cast<size_t>(merge ? sc.nblocks_total : 0) +
-                                        2 * static_cast<size_t>(guide_cap));
+                          const StepDyn* dyn, double* upd, float4* val_poses, double2* val_xy,
+                          double* val_base, DecisionDev* dec, int merge, cudaStream_t s) {
+  switch (sc.tag) {
+    case EXM_MODEL_DIFF: return update_tag<EXM_MODEL_DIFF>(sc, partials, nominal, dyn, upd, val_poses, val_xy, val_base, dec, merge, s);
+    case EXM_MODEL_ACKERMANN: return update_tag<EXM_MODEL_ACKERMANN>(sc, partials, nominal, dyn, upd, val_poses, val_xy, val_base, dec, merge, s);
+    case EXM_MODEL_OMNI: return update_tag<EXM_MODEL_OMNI>(sc, partials, nominal, dyn, upd, val_poses, val_xy, val_base, dec, merge, s);
+    case EXM_MODEL_SPIN: return update_tag<EXM_MODEL_SPIN>(sc, partials, nominal, dyn, upd, val_poses, val_xy, val_base, dec, merge, s);
+    case EXM_MODEL_PARALLEL: return update_tag<EXM_MODEL_PARALLEL>(sc, partials, nominal, dyn, upd, val_poses, val_xy, val_base, dec, merge, s);
+  }
+  return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_finalize(const StepConst& sc, const float* val_dmin, const double2* val_xy,
+                            const double* val_base, const double* upd, const double* guide,
+                            int guide_cap, double* nominal, StepDyn* dyn, DecisionDev* dec,
+                            double* out_dmin, double* out_nominal, double* out_uprev, int commit,
+                            cudaStream_t s) {
+  const size_t smem = sizeof(double) * (2 * static_cast<size_t>(guide_cap) + sc.T);
   if (smem > 48 * 1024) {
-    cudaError_t e = cudaFuncSetAttribute(k_update, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaError_t e = cudaFuncSetAttribute(k_finalize, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(smem));
     if (e != cudaSuccess) return e;
   }
-  k_update<<<1, 256, smem, s>>>(sc, partials, nominal, dyn, guide, upd, val_poses, val_base, dec,
-                                merge);
-  return cudaGetLastError();
-}
-
-cudaError_t launch_finalize(const StepConst& sc, const float* val_dmin, const double* val_base,
-                            const double* upd, double* nominal, StepDyn* dyn, DecisionDev* dec,
-                            double* out_dmin, double* out_nominal, double* out_uprev,
-                            int commit, cudaStream_t s) {
-  k_finalize<<<1, 32, 0, s>>>(sc, val_dmin, val_base, upd, nominal, dyn, dec, out_dmin,
-                              out_nominal, out_uprev, commit);
+  k_finalize<<<1, 64, smem, s>>>(sc, val_dmin, val_xy, val_base, upd, guide, nominal, dyn, dec,
+                                 out_dmin, out_nominal, out_uprev, commit);
   return cudaGetLastError();
 }
 
