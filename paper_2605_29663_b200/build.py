@@ -44,6 +44,14 @@ def build_oracle(with_reference: bool | None = None) -> None:
         subprocess.run(["make", "-s", "-C", odir, "ref", f"REF_DIR={ref}"], check=True)
 
 
+def build_dropin() -> None:
+    """C++ link-time drop-in demo (needs the reference tree: dev container only)."""
+    ref = os.environ.get("REF_DIR", "/root/reference/proj")
+    if os.path.isdir(os.path.join(ref, "src")):
+        subprocess.run(["make", "-s", "-C", os.path.join(HERE, "host"), f"REF_DIR={ref}"], check=True)
+
+
 if __name__ == "__main__":
     build_library(force=True, verbose=True)
     build_oracle()
+    build_dropin()

@@ -12,6 +12,7 @@
 // handle, no user destructor), so device handles live in a process-wide cache keyed by the
 // controller configuration; the controller's own state (nominal_, u_prev_,
 // cycle_) stays in the object and crosses the ABI per call.
+#include <algorithm>
 #include <cmath>
 #include <cstring>
 #include <limits>
