@@ -186,7 +186,8 @@ def run_ours(args, world, rank, local):
     from paper_2605_29663_b200 import workloads as W
     from paper_2605_29663_b200.api import Engine
 
-    wl = W.cfg2()
+    wl = {"cfg1": W.cfg1, "cfg2": W.cfg2, "cfg3": W.cfg3, "cfg5": W.cfg5}[args.config]()
+    fp = wl.footprint
     K, T, N = wl.params.rollouts, wl.params.horizon, wl.n_points
     D = wl.model.control_dim()
     torch.cuda.set_device(local)
@@ -242,7 +243,6 @@ def run_ours(args, world, rank, local):
     h2d = 104 + 8 * T * D + 16 * wl.guidance.path.shape[0] + 16 * N + N
     d2h = 64 + 8 * (T + T * D + 3)
 
-    fp = wl.footprint
     F = ops_per_pair(fp)
     pairs = K // world * T * N
     peak, peak_src = fp32_peak_tflops(torch.cuda.get_device_properties(local).multi_processor_count)
@@ -260,8 +260,10 @@ def run_ours(args, world, rank, local):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
         "data": "synthetic",
-        "config": {"workload": wl.name, "K": K, "T": T, "N": N, "footprint": "l_shape_12 polygon (B=12)",
-                   "model": "diff", "parallelism": f"rollout-sharded x{world}",
+        "config": {"workload": wl.name, "K": K, "T": T, "N": N,
+                   "footprint": f"{wl.footprint.name} ({'polygon B' if fp.is_polygon() else 'cover R'}={fp.count()})",
+                   "model": ["diff", "ackermann", "omni", "spin", "parallel"][wl.model.tag],
+                   "parallelism": f"rollout-sharded x{world}",
                    "l2": "flushed (256 MiB write) before every timed step"},
         "sdf_evals_per_s": K * T * N / (ms * 1e-3),
         "e2e": {"value": 1.0 / e2e_s, "unit": "steps/s", "h2d_bytes_per_step": h2d,
@@ -269,7 +271,7 @@ def run_ours(args, world, rank, local):
         "gpu_launches": stats["launches_per_step"] * args.steps,
         "roofline": {"bound": "fp32", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                      "frac": achieved / peak, "traffic": traffic,
-                     "kernel": "k_sdf_grid (per-pose exact SDF min, exact culling)",
+                     "kernel": f"k_sdf_grid<{'POLYGON' if fp.is_polygon() else 'RECT'},{fp.count()}> (per-pose exact SDF min, exact culling)",
                      "sdf_kernel_ms": sdf_avg_ms,
                      "algorithmic": f"K*T*N pairs x {F} ops/pair (SURVEY §8(d), unpruned)",
                      "peak_source": peak_src},
@@ -322,6 +324,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-sdf-batch", action="store_true")
+    ap.add_argument("--config", default="cfg2", choices=["cfg1", "cfg2", "cfg3", "cfg5"],
+                    help="workload (the headline is cfg2; the others are reported separately)")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
     world, rank, local = dist_setup()

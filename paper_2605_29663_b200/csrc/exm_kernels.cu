@@ -547,10 +547,37 @@ __device__ __forceinline__ void ring_cell(int k, int t, int ci, int cj, int& i, 
   i = ci + k; j = cj - k + 1 + t;
 }
 
+// World-frame AABB of the footprint at pose q: the body-frame AABB (fp.aabb) rotated by theta
+// and re-boxed. Every footprint point lies inside it, so for any obstacle point o outside it
+// sd(o) >= dist(o, W) — an exact lower bound that is much tighter than |o - t| - R for
+// elongated or off-centre footprints (forklift, L).
+struct WBox {
+  float x0, x1, y0, y1;
+};
+__device__ __forceinline__ WBox world_box(const FpDev& fp, float4 q) {
+  const float cx = 0.5f * (fp.aabb[0] + fp.aabb[1]), cy = 0.5f * (fp.aabb[2] + fp.aabb[3]);
+  const float hx = 0.5f * (fp.aabb[1] - fp.aabb[0]), hy = 0.5f * (fp.aabb[3] - fp.aabb[2]);
+  const float ac = fabsf(q.z), as = fabsf(q.w);
+  const float wx = fmaf(ac, hx, as * hy) + kCullMargin, wy = fmaf(as, hx, ac * hy) + kCullMargin;
+  const float ox = q.x + fmaf(q.z, cx, -(q.w * cy)), oy = q.y + fmaf(q.w, cx, q.z * cy);
+  return {ox - wx, ox + wx, oy - wy, oy + wy};
+}
+// d2 = squared distance from W to the box [bx0,bx1]x[by0,by1] (0 if they overlap); may the box
+// contain a point that beats `best`?
+__device__ __forceinline__ bool box_may_beat(const WBox& w, float bx0, float bx1, float by0,
+                                             float by1, float best) {
+  const float gx = fmaxf(fmaxf(bx0 - w.x1, w.x0 - bx1), 0.f);
+  const float gy = fmaxf(fmaxf(by0 - w.y1, w.y0 - by1), 0.f);
+  const float d2 = fmaf(gx, gx, gy * gy);
+  const float lim = best + kCullMargin;
+  return d2 == 0.f || (lim > 0.f && d2 < lim * lim);
+}
+
 // Exact per-pose min signed distance with exact culling (min_signed_distance_at semantics).
-// Thread <-> pose; a warp walks grid rings outward from its poses' centroid, nearest first,
-// and stops once no lane's lower bound |o - t| - R can beat that lane's running minimum
-// (the reference's own prune, geometry.cpp:368-369, applied to cells, then to points).
+// Thread <-> pose; a warp walks grid rings outward from its poses' centroid, nearest first, and
+// stops once no lane's lower bound can beat that lane's running minimum. Lower bounds (all
+// exact): ring and cell via the world box W of the footprint, then per point the
+// distance to W and the distance to the body-frame AABB, then the exact polygon/cover SDF.
 template <int KIND, int NB>
 __global__ void __launch_bounds__(128) k_sdf_grid(const __grid_constant__ FpDev fp,
                                                   const float4* __restrict__ poses, int n_poses,
@@ -577,17 +604,21 @@ __global__ void __launch_bounds__(128) k_sdf_grid(const __grid_constant__ FpDev 
   const float cx = sx / na, cy = sy / na;
   const int ci = min(gm.gx - 1, max(0, static_cast<int>(floorf((cx - gm.x0) * gm.inv_cs))));
   const int cj = min(gm.gy - 1, max(0, static_cast<int>(floorf((cy - gm.y0) * gm.inv_cs))));
+  const WBox w = world_box(fp, q);
   const float R = fp.radius + kCullMargin;
   float best = __int_as_float(0x7f800000);
   const int kmax = max(max(ci, gm.gx - 1 - ci), max(cj, gm.gy - 1 - cj));
   for (int k = 0; k <= kmax; ++k) {
     if (k > 0) {
+      // every point of ring k or beyond lies outside the inner square S_{k-1}
       const float bx0 = gm.x0 + static_cast<float>(ci - k + 1) * gm.cs;
       const float bx1 = gm.x0 + static_cast<float>(ci + k) * gm.cs;
       const float by0 = gm.y0 + static_cast<float>(cj - k + 1) * gm.cs;
       const float by1 = gm.y0 + static_cast<float>(cj + k) * gm.cs;
-      const float lb = fmaxf(fminf(fminf(q.x - bx0, bx1 - q.x), fminf(q.y - by0, by1 - q.y)), 0.f);
-      const bool need = active && lb < R + best;
+      const float lbw = fminf(fminf(w.x0 - bx0, bx1 - w.x1), fminf(w.y0 - by0, by1 - w.y1));
+      const float lbc = fminf(fminf(q.x - bx0, bx1 - q.x), fminf(q.y - by0, by1 - q.y)) - R;
+      const float lb = fmaxf(fmaxf(lbw, lbc), 0.f);
+      const bool need = active && lb < best + kCullMargin;
       if (!__any_sync(kFull, need)) break;
     }
     const int ncell = k == 0 ? 1 : 8 * k;
@@ -603,17 +634,22 @@ __global__ void __launch_bounds__(128) k_sdf_grid(const __grid_constant__ FpDev 
       const float gx_ = fmaxf(fmaxf(bx0 - q.x, q.x - bx1), 0.f);
       const float gy_ = fmaxf(fmaxf(by0 - q.y, q.y - by1), 0.f);
       const float lim = R + best;
-      const bool need = active && (gx_ * gx_ + gy_ * gy_ < lim * lim);
+      const bool need = active && (gx_ * gx_ + gy_ * gy_ < lim * lim) &&
+                        box_may_beat(w, bx0, bx1, by0, by1, best);
       if (!__any_sync(kFull, need)) continue;
-      for (int p = s; p < e; ++p) {
-        const float2 o = __ldg(cloud + p);
-        if (need) {
-          const float dx = o.x - q.x, dy = o.y - q.y;
-          const float l2 = R + best;
-          if (dx * dx + dy * dy < l2 * l2) {
-            const float bx = fmaf(q.z, dx, q.w * dy);
-            const float by = fmaf(q.z, dy, -(q.w * dx));
-            if (aabb_may_beat(fp, bx, by, best)) best = fminf(best, sd_body<KIND, NB>(fp, bx, by));
+      const float2* cp = cloud + s;
+      const int n = e - s;
+      float l2 = lim * lim;
+      for (int p = 0; p < n; ++p) {
+        const float2 o = __ldg(cp + p);
+        const float dx = o.x - q.x, dy = o.y - q.y;
+        if (need && dx * dx + dy * dy < l2) {
+          const float bx = fmaf(q.z, dx, q.w * dy);
+          const float by = fmaf(q.z, dy, -(q.w * dx));
+          if (aabb_may_beat(fp, bx, by, best)) {
+            best = fminf(best, sd_body<KIND, NB>(fp, bx, by));
+            const float nl = R + best;
+            l2 = nl * nl;
           }
         }
       }
