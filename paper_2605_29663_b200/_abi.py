@@ -12,7 +12,7 @@ import os
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "lib", "libexm_b200.so")
+LIB_PATH = os.environ.get("EXM_LIB_PATH", os.path.join(HERE, "lib", "libexm_b200.so"))
 
 EXM_OK = 0
 EXM_ERR_INVALID_ARGUMENT = 1

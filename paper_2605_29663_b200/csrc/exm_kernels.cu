@@ -1107,10 +1107,13 @@ __device__ __forceinline__ void poly_pairs4(const FpDev& fp, u64 X01, u64 Y01, u
   // Edge groups of kEdgeGroup with a rolled outer loop: the per-edge constants stay uniform
   // (LDCU from the parameter bank at a uniform offset) while the code stays small enough for
   // the instruction cache at B = 64.
-  constexpr int G = NB % 4 == 0 ? 4 : 2;
+  // The distance-only pass (most pose-warps) is fully unrolled: every edge constant is an
+  // immediate constant-bank/uniform operand. The rarer crossing pass keeps a rolled outer loop
+  // so both together stay inside the instruction cache at B = 64.
+  constexpr int G = CROSS ? (NB % 4 == 0 ? 4 : 2) : (NB / 2) * 2;
   const float vy0 = fp.e[0][1];
   u64 R01 = sub2(bc(vy0), Y01), R23 = sub2(bc(vy0), Y23);
-  constexpr int NFULL = (NB / G) * G;
+  constexpr int NFULL = G > 0 ? (NB / G) * G : 0;
 #pragma unroll 1
   for (int g = 0; g < NFULL; g += G) {
 #pragma unroll
