@@ -100,6 +100,30 @@ class ClockSampler:
                 "samples": len(rows)}
 
 
+def ncu_profile(name: str) -> dict:
+    """Per-launch DRAM traffic and executed pipe utilisation of a kernel from the newest
+    committed `ncu --set full` summary (profiles/rNN_ncu_<name>.json, tools/ncu_summary.py)."""
+    import glob
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", f"r*_ncu_{name}.json")))
+    if not files:
+        return {}
+    try:
+        kern = next(iter(json.load(open(files[-1])).values()))[0]
+
+        def num(key):
+            v = kern.get(key, "")
+            x, _, unit = v.partition(" ")
+            scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(unit, 1)
+            return float(x.replace(",", "")) * scale
+        return {"traffic": num("dram__bytes_read.sum") + num("dram__bytes_write.sum"),
+                "executed": {"source": os.path.relpath(files[-1], ROOT),
+                             "fma_pipe_active_pct": num("sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active"),
+                             "alu_pipe_active_pct": num("sm__pipe_alu_cycles_active.avg.pct_of_peak_sustained_active"),
+                             "issue_active_pct": num("smsp__issue_active.avg.pct_of_peak_sustained_active")}}
+    except Exception:
+        return {}
+
+
 def dist_setup():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -248,13 +272,7 @@ def run_ours(args, world, rank, local):
     peak, peak_src = fp32_peak_tflops(torch.cuda.get_device_properties(local).multi_processor_count)
     sdf_avg_ms = stats["sdf_ms"]
     achieved = pairs * F / (sdf_avg_ms * 1e-3) / 1e12
-    traffic = None
-    prof = os.path.join(ROOT, "profiles", "r01_sdf_grid_dram_bytes.json")
-    if os.path.exists(prof):
-        try:
-            traffic = json.load(open(prof)).get("dram_bytes_per_launch")
-        except Exception:
-            traffic = None
+    prof = ncu_profile(f"sdf_grid_{args.config}")
     line = {
         "metric": "MPPI control steps/sec", "value": value, "unit": "steps/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
@@ -270,7 +288,8 @@ def run_ours(args, world, rank, local):
                 "d2h_bytes_per_step": d2h},
         "gpu_launches": stats["launches_per_step"] * args.steps,
         "roofline": {"bound": "fp32", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                     "frac": achieved / peak, "traffic": traffic,
+                     "frac": achieved / peak, "traffic": prof.get("traffic"),
+                     "executed": prof.get("executed"),
                      "kernel": f"k_sdf_grid<{'POLYGON' if fp.is_polygon() else 'RECT'},{fp.count()}> (per-pose exact SDF min, exact culling)",
                      "sdf_kernel_ms": sdf_avg_ms,
                      "algorithmic": f"K*T*N pairs x {F} ops/pair (SURVEY §8(d), unpruned)",
@@ -308,10 +327,12 @@ def bench_sdf_batch(args, torch, peak, peak_src):
     achieved = pairs * F / (ms * 1e-3) / 1e12
     eng.sdf_run_resident(1, True)
     st2 = eng.step_stats()
+    prof = ncu_profile("sdf_pairs_cfg4")
     return {"workload": "cfg4_star64_P1000_N1e6", "pairs": pairs, "kernel_ms_min_only": ms,
             "kernel_ms_with_pairs": st2["sdf_ms"], "sdf_evals_per_s": pairs / (ms * 1e-3),
             "roofline": {"bound": "fp32", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                          "frac": achieved / peak, "kernel": "k_sdf_pairs<POLYGON,64>",
+                         "traffic": prof.get("traffic"), "executed": prof.get("executed"),
                          "algorithmic": f"P*N pairs x {F} ops/pair (every pair evaluated)",
                          "peak_source": peak_src}}
 
