@@ -260,9 +260,12 @@ def run_ours(args, world, rank, local):
         eng.control_cycle_raw(wl.q0, obstacles, wl.guidance, nom, up, c)
     if world > 1:
         torch.distributed.barrier()
+    e2e_ms = []
     t0 = time.perf_counter()
     for c in range(args.steps):
+        t1 = time.perf_counter()
         eng.control_cycle_raw(wl.q0, obstacles, wl.guidance, nom, up, 1000 + c)
+        e2e_ms.append(1e3 * (time.perf_counter() - t1))
     e2e_s = allreduce_max((time.perf_counter() - t0) / args.steps, world)
     h2d = 104 + 8 * T * D + 16 * wl.guidance.path.shape[0] + 16 * N + N
     d2h = 64 + 8 * (T + T * D + 3)
@@ -277,6 +280,9 @@ def run_ours(args, world, rank, local):
         "metric": "MPPI control steps/sec", "value": value, "unit": "steps/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+        "dtype_note": "SDF kernels FP32 on q0-recentred coordinates; dynamics, costs, softmax FP64",
+        "ms_per_step_p50": float(np.percentile(step_ms, 50)),
+        "ms_per_step_p99": float(np.percentile(step_ms, 99)),
         "data": "synthetic",
         "config": {"workload": wl.name, "K": K, "T": T, "N": N,
                    "footprint": f"{wl.footprint.name} ({'polygon B' if fp.is_polygon() else 'cover R'}={fp.count()})",
@@ -285,7 +291,9 @@ def run_ours(args, world, rank, local):
                    "l2": "flushed (256 MiB write) before every timed step"},
         "sdf_evals_per_s": K * T * N / (ms * 1e-3),
         "e2e": {"value": 1.0 / e2e_s, "unit": "steps/s", "h2d_bytes_per_step": h2d,
-                "d2h_bytes_per_step": d2h},
+                "d2h_bytes_per_step": d2h, "ms_p50": float(np.percentile(e2e_ms, 50)),
+                "ms_p99": float(np.percentile(e2e_ms, 99)),
+                "path": "exm_control_cycle (C ABI): host cloud/state -> pinned -> H2D, graph, D2H decision"},
         "gpu_launches": stats["launches_per_step"] * args.steps,
         "roofline": {"bound": "fp32", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                      "frac": achieved / peak, "traffic": prof.get("traffic"),

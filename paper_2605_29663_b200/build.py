@@ -48,7 +48,8 @@ def build_dropin() -> None:
     """C++ link-time drop-in demo (needs the reference tree: dev container only)."""
     ref = os.environ.get("REF_DIR", "/root/reference/proj")
     if os.path.isdir(os.path.join(ref, "src")):
-        subprocess.run(["make", "-s", "-C", os.path.join(HERE, "host"), f"REF_DIR={ref}"], check=True)
+        subprocess.run(["make", "-s", "-C", os.path.join(HERE, "host"), f"REF_DIR={ref}", "all",
+                        "acceptance"], check=True)
 
 
 if __name__ == "__main__":

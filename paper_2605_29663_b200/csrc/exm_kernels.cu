@@ -117,20 +117,7 @@ __device__ __forceinline__ void clamp_control(const StepConst& sc, const double*
   }
 }
 
-// derivative + step, kinematics.cpp:75-97 (cos/sin of the pre-step heading supplied)
-template <int TAG>
-__device__ __forceinline__ void euler_step(const StepConst& sc, double q[3], const double* u,
-                                           double ct, double st) {
-  double fx = 0.0, fy = 0.0, fth = 0.0;
-  if (TAG == EXM_MODEL_DIFF) { fx = u[0] * ct; fy = u[0] * st; fth = u[1]; }
-  if (TAG == EXM_MODEL_ACKERMANN) { fx = u[0] * ct; fy = u[0] * st; fth = u[0] / sc.wheelbase * tan(u[1]); }
-  if (TAG == EXM_MODEL_OMNI) { fx = u[0] * ct - u[1] * st; fy = u[0] * st + u[1] * ct; fth = u[2]; }
-  if (TAG == EXM_MODEL_SPIN) { fth = u[0]; }
-  if (TAG == EXM_MODEL_PARALLEL) { fx = -u[0] * st; fy = u[0] * ct; }
-  q[0] = q[0] + fx * sc.dt;
-  q[1] = q[1] + fy * sc.dt;
-  q[2] = q[2] + fth * sc.dt;
-}
+// derivative + step (kinematics.cpp:75-97) are heading_rate / xy_rate below.
 
 // project_on_polyline + task_cost, controller.cpp:50-66, :103-118
 __device__ double task_cost(const StepConst& sc, const double q[3], const double* g, int ng,
@@ -193,6 +180,32 @@ __device__ __forceinline__ double obstacle_cost(const StepConst& sc, double d) {
 // FP32 pose (x, y, cos, sin) and the FP64 position of every pre-step state; returns the
 // control cost summed over h plus the terminal goal cost. The per-step task cost is
 // independent across (r, h) and is computed in parallel by k_stage_costs.
+//
+// In all five models the heading rate depends on u only (kinematics.cpp:75-92), so the long
+// FP64 sincos latency is taken off the serial chain: per chunk of kChunk steps the clamp and
+// heading recurrences run first, then the kChunk independent sincos, then the x/y updates —
+// the same operations on the same values as the reference's step-by-step order.
+template <int TAG>
+__device__ __forceinline__ double heading_rate(const StepConst& sc, const double* u) {
+  if (TAG == EXM_MODEL_DIFF) return u[1];
+  if (TAG == EXM_MODEL_ACKERMANN) return u[0] / sc.wheelbase * tan(u[1]);
+  if (TAG == EXM_MODEL_OMNI) return u[2];
+  if (TAG == EXM_MODEL_SPIN) return u[0];
+  return 0.0;
+}
+
+template <int TAG>
+__device__ __forceinline__ void xy_rate(const double* u, double ct, double st, double& fx,
+                                        double& fy) {
+  fx = 0.0;
+  fy = 0.0;
+  if (TAG == EXM_MODEL_DIFF || TAG == EXM_MODEL_ACKERMANN) { fx = u[0] * ct; fy = u[0] * st; }
+  if (TAG == EXM_MODEL_OMNI) { fx = u[0] * ct - u[1] * st; fy = u[0] * st + u[1] * ct; }
+  if (TAG == EXM_MODEL_PARALLEL) { fx = -u[0] * st; fy = u[0] * ct; }
+}
+
+constexpr int kChunk = 4;
+
 template <int TAG>
 __device__ double rollout_dyn(const StepConst& sc, const StepDyn& dyn, const double* nominal,
                               const double* eps_row, float4* poses_row, double2* xy_row,
@@ -200,35 +213,57 @@ __device__ double rollout_dyn(const StepConst& sc, const StepDyn& dyn, const dou
   constexpr int D = model_dim<TAG>();
   const int T = sc.T;
   double prev[3] = {dyn.u_prev[0], dyn.u_prev[1], dyn.u_prev[2]};
-  double q[3] = {dyn.q0[0], dyn.q0[1], dyn.q0[2]};
+  double x = dyn.q0[0], y = dyn.q0[1], th = dyn.q0[2];
   const double qx0 = dyn.q0[0], qy0 = dyn.q0[1];
   double base = 0.0;
-  if (states_row) { states_row[0] = q[0]; states_row[1] = q[1]; states_row[2] = q[2]; }
-  for (int h = 0; h < T; ++h) {
-    double u[3] = {0.0, 0.0, 0.0}, uc[3] = {0.0, 0.0, 0.0};
+  if (states_row) { states_row[0] = x; states_row[1] = y; states_row[2] = th; }
+  for (int h0 = 0; h0 < T; h0 += kChunk) {
+    double uc[kChunk][3], thj[kChunk], thn[kChunk];
 #pragma unroll
-    for (int c = 0; c < D; ++c) u[c] = nominal[h * D + c] + (eps_row ? eps_row[h * D + c] : 0.0);
-    clamp_control<TAG>(sc, u, prev, uc);
+    for (int j = 0; j < kChunk; ++j) {
+      const int h = h0 + j;
+      if (h < T) {
+        double u[3] = {0.0, 0.0, 0.0};
 #pragma unroll
-    for (int c = 0; c < D; ++c) prev[c] = uc[c];
-    if (controls_row) {
+        for (int c = 0; c < D; ++c) u[c] = nominal[h * D + c] + (eps_row ? eps_row[h * D + c] : 0.0);
+        clamp_control<TAG>(sc, u, prev, uc[j]);
 #pragma unroll
-      for (int c = 0; c < D; ++c) controls_row[h * D + c] = uc[c];
+        for (int c = 0; c < D; ++c) prev[c] = uc[j][c];
+        thj[j] = th;
+        th = th + heading_rate<TAG>(sc, uc[j]) * sc.dt;
+        thn[j] = th;
+      }
     }
-    double st, ct;
-    sincos(q[2], &st, &ct);
-    poses_row[h] = make_float4(static_cast<float>(q[0] - qx0), static_cast<float>(q[1] - qy0),
-                               static_cast<float>(ct), static_cast<float>(st));
-    xy_row[h] = make_double2(q[0], q[1]);
-    base += control_cost<TAG>(sc, uc);
-    euler_step<TAG>(sc, q, uc, ct, st);
-    if (states_row) {
-      states_row[3 * (h + 1)] = q[0];
-      states_row[3 * (h + 1) + 1] = q[1];
-      states_row[3 * (h + 1) + 2] = q[2];
+    double st[kChunk], ct[kChunk];
+#pragma unroll
+    for (int j = 0; j < kChunk; ++j)
+      if (h0 + j < T) sincos(thj[j], &st[j], &ct[j]);
+#pragma unroll
+    for (int j = 0; j < kChunk; ++j) {
+      const int h = h0 + j;
+      if (h < T) {
+        if (controls_row) {
+#pragma unroll
+          for (int c = 0; c < D; ++c) controls_row[h * D + c] = uc[j][c];
+        }
+        poses_row[h] = make_float4(static_cast<float>(x - qx0), static_cast<float>(y - qy0),
+                                   static_cast<float>(ct[j]), static_cast<float>(st[j]));
+        xy_row[h] = make_double2(x, y);
+        base += control_cost<TAG>(sc, uc[j]);
+        double fx, fy;
+        xy_rate<TAG>(uc[j], ct[j], st[j], fx, fy);
+        x = x + fx * sc.dt;
+        y = y + fy * sc.dt;
+        if (states_row) {
+          states_row[3 * (h + 1)] = x;
+          states_row[3 * (h + 1) + 1] = y;
+          states_row[3 * (h + 1) + 2] = thn[j];
+        }
+      }
     }
   }
-  return base + terminal_cost(sc, q, dyn.goal);
+  const double qT[3] = {x, y, th};
+  return base + terminal_cost(sc, qT, dyn.goal);
 }
 
 // Running cost of one pre-step state: task_cost (controller.cpp:103-118, non-terminal) +
