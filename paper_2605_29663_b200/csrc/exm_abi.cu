@@ -236,6 +236,8 @@ struct EventPair {
 struct exm_handle {
   int device = 0;
   cudaStream_t stream = nullptr;
+  cudaStream_t side = nullptr;  // parallel graph branch (cloud preparation)
+  cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
   FpDev fp{};
   StepConst sc{};
   int K = 0, T = 0, D = 0, n_cap = 0, guide_cap = 0;
@@ -340,14 +342,20 @@ exm_status enqueue_step(exm_handle* h, bool draw_noise, const EventPair* ev, cud
                         bool capturing) {
   const StepConst& sc = h->sc;
   int launches = 0;
+  // Fork: the cloud preparation (single CTA) runs on a side stream concurrently with the
+  // noise + rollout branch; the graph captures both branches and the join before the SDF.
+  EXM_CUDA(cudaEventRecord(h->fork_ev, s));
+  EXM_CUDA(cudaStreamWaitEvent(h->side, h->fork_ev, 0));
+  EXM_CUDA(launch_cloud_prep(h->d_pts, h->d_mask, h->d_dyn, h->fp.radius, h->d_tmp, h->d_cloud,
+                             h->d_cell_start, h->d_grid, h->side));
+  EXM_CUDA(cudaEventRecord(h->join_ev, h->side));
   if (draw_noise) {
     EXM_CUDA(launch_noise(sc, h->d_dyn, h->d_eps, s));
     ++launches;
   }
-  EXM_CUDA(launch_cloud_prep(h->d_pts, h->d_mask, h->d_dyn, h->fp.radius, h->d_tmp, h->d_cloud,
-                             h->d_cell_start, h->d_grid, s));
   EXM_CUDA(launch_rollout(sc, h->d_dyn, h->d_nominal, h->d_eps, h->d_poses, h->d_xy, h->d_base,
                           nullptr, nullptr, s));
+  EXM_CUDA(cudaStreamWaitEvent(s, h->join_ev, 0));
   if (ev) EXM_CUDA(capturing ? cudaEventRecordWithFlags(ev->a, s, cudaEventRecordExternal)
                              : cudaEventRecord(ev->a, s));
   EXM_CUDA(launch_sdf_grid(h->fp, h->d_poses, sc.k_local * sc.T, h->d_grid, h->d_cell_start,
@@ -625,6 +633,9 @@ exm_status exm_create(const exm_footprint* footprint, const exm_model* model,
       return cleanup_fail(fail(EXM_ERR_CUDA, std::string(#call) + ": " + cudaGetErrorString(e_))); \
   } while (0)
   EXM_CUDA_C(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
+  EXM_CUDA_C(cudaStreamCreateWithFlags(&h->side, cudaStreamNonBlocking));
+  EXM_CUDA_C(cudaEventCreateWithFlags(&h->fork_ev, cudaEventDisableTiming));
+  EXM_CUDA_C(cudaEventCreateWithFlags(&h->join_ev, cudaEventDisableTiming));
   const size_t KT = static_cast<size_t>(h->K) * h->T;
   const size_t TD = static_cast<size_t>(h->T) * D;
   EXM_CUDA_C(dalloc(&h->d_dyn, 1));
@@ -694,6 +705,9 @@ void exm_destroy(exm_handle* h) {
     if (p->a) cudaEventDestroy(p->a);
     if (p->b) cudaEventDestroy(p->b);
   }
+  if (h->fork_ev) cudaEventDestroy(h->fork_ev);
+  if (h->join_ev) cudaEventDestroy(h->join_ev);
+  if (h->side) cudaStreamDestroy(h->side);
   if (h->stream) cudaStreamDestroy(h->stream);
   delete h;
 }

@@ -205,6 +205,7 @@ __device__ __forceinline__ void xy_rate(const double* u, double ct, double st, d
 }
 
 constexpr int kChunk = 4;
+constexpr int kPartialThreads = 1024;  // 32 warps: 8 rollouts per warp in the U sums
 
 template <int TAG>
 __device__ double rollout_dyn(const StepConst& sc, const StepDyn& dyn, const double* nominal,
@@ -788,12 +789,12 @@ __global__ void __launch_bounds__(128) k_sdf_grid_warp(const __grid_constant__ F
 //   J_r = (ctrl + terminal)_r + sum_h stage[h][r]       controller.cpp:164-171
 //   Jt_r = J_r + w_inf * unsafe_r                       controller.cpp:310-312
 //   {beta_b, S_b, A_b, argmin_b, U_b[T*D]}              controller.cpp:222-233, :316-328
-__global__ void __launch_bounds__(kBlockRollouts) k_block_partials(
+__global__ void __launch_bounds__(kPartialThreads) k_block_partials(
     const StepConst sc, const double* __restrict__ base_cost, const double* __restrict__ stage,
     const uint8_t* __restrict__ flags, const double* __restrict__ eps,
     double* __restrict__ partials, double* __restrict__ cost_out,
     uint8_t* __restrict__ unsafe_out) {
-  extern __shared__ double s_u[];  // [warps][T*D]
+  extern __shared__ double s_u[];  // [kPartialThreads/32][T*D]
   __shared__ double s_e[kBlockRollouts];
   __shared__ double s_v[kBlockRollouts / 32];
   __shared__ double s_a[kBlockRollouts / 32];
@@ -801,10 +802,11 @@ __global__ void __launch_bounds__(kBlockRollouts) k_block_partials(
   __shared__ double s_beta;
   __shared__ int s_arg;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  constexpr int kWarps = kBlockRollouts / 32;
+  constexpr int kWarps = kBlockRollouts / 32;  // warps owning one rollout per lane
   const int r0 = blockIdx.x * kBlockRollouts;
   const int r = r0 + tid;
-  const bool valid = r < sc.k_local;
+  const bool owner = tid < kBlockRollouts;
+  const bool valid = owner && r < sc.k_local;
   const int K = sc.k_local;
   double jt = HUGE_VAL;
   if (valid) {
@@ -828,7 +830,7 @@ __global__ void __launch_bounds__(kBlockRollouts) k_block_partials(
     const int oi = __shfl_xor_sync(kFull, vi, o);
     if (ov < v || (ov == v && oi < vi)) { v = ov; vi = oi; }
   }
-  if (lane == 0) { s_v[warp] = v; s_i[warp] = vi; }
+  if (lane == 0 && owner) { s_v[warp] = v; s_i[warp] = vi; }
   __syncthreads();
   if (tid == 0) {
     double b = s_v[0];
@@ -843,13 +845,14 @@ __global__ void __launch_bounds__(kBlockRollouts) k_block_partials(
   const double z = valid ? (jt - beta) / sc.lambda : 0.0;
   const double e = valid ? exp(-z) : 0.0;
   const double a = valid ? e * z : 0.0;
-  s_e[tid] = e;
+  if (owner) s_e[tid] = e;
   double se = e, sa = a;
   for (int o = 16; o; o >>= 1) {
     se += __shfl_xor_sync(kFull, se, o);
     sa += __shfl_xor_sync(kFull, sa, o);
   }
-  if (lane == 0) { s_v[warp] = se; s_a[warp] = sa; }
+  __syncthreads();  // s_v/s_a reuse: the argmin values were consumed by thread 0 above
+  if (lane == 0 && owner) { s_v[warp] = se; s_a[warp] = sa; }
   __syncthreads();
   const int stride = partial_stride(sc.T, sc.D);
   double* out = partials + static_cast<size_t>(sc.block_offset + blockIdx.x) * stride;
@@ -861,21 +864,23 @@ __global__ void __launch_bounds__(kBlockRollouts) k_block_partials(
     out[2] = A;
     out[3] = static_cast<double>(s_arg);
   }
-  // U_b[o] = sum_r e_r eps[r][o]: warp w sums its 32 rollouts (lanes over o, coalesced rows),
-  // then the kWarps warp sums are added in warp order.
+  // U_b[o] = sum_r e_r eps[r][o]: each of the kPartialThreads/32 warps sums its slice of
+  // rollouts (lanes over o, coalesced rows), then the warp sums are added in warp order.
+  constexpr int kUWarps = kPartialThreads / 32;
+  constexpr int kPerWarp = kBlockRollouts / kUWarps;
   const int TD = sc.T * sc.D;
   const int nv = min(kBlockRollouts, sc.k_local - r0);
-  const int j0 = warp * 32, j1 = min(nv, j0 + 32);
+  const int j0 = warp * kPerWarp, j1 = min(nv, j0 + kPerWarp);
   for (int o = lane; o < TD; o += 32) {
     double acc = 0.0;
-#pragma unroll 8
+#pragma unroll
     for (int j = j0; j < j1; ++j) acc += s_e[j] * eps[static_cast<size_t>(r0 + j) * TD + o];
     s_u[warp * TD + o] = acc;
   }
   __syncthreads();
   for (int o = tid; o < TD; o += blockDim.x) {
     double acc = 0.0;
-    for (int w = 0; w < kWarps; ++w) acc += s_u[w * TD + o];
+    for (int w = 0; w < kUWarps; ++w) acc += s_u[w * TD + o];
     out[4 + o] = acc;
   }
 }
@@ -1442,14 +1447,14 @@ cudaError_t launch_block_partials(const StepConst& sc, const double* base_cost,
                                   double* partials, double* cost_out, uint8_t* unsafe_out,
                                   cudaStream_t s) {
   if (sc.nblocks_local <= 0) return cudaSuccess;
-  const size_t smem = sizeof(double) * (kBlockRollouts / 32) * static_cast<size_t>(sc.T) * sc.D;
+  const size_t smem = sizeof(double) * (kPartialThreads / 32) * static_cast<size_t>(sc.T) * sc.D;
   if (smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(k_block_partials,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(smem));
     if (e != cudaSuccess) return e;
   }
-  k_block_partials<<<sc.nblocks_local, kBlockRollouts, smem, s>>>(
+  k_block_partials<<<sc.nblocks_local, kPartialThreads, smem, s>>>(
       sc, base_cost, stage, flags, eps, partials, cost_out, unsafe_out);
   return cudaGetLastError();
 }
