@@ -276,6 +276,8 @@ struct exm_handle {
   double* d_cost = nullptr;
   uint8_t* d_unsafe = nullptr;
   // pinned staging
+  unsigned char* d_in_block = nullptr;  // d_dyn | d_nominal | d_guide | d_pts | d_mask
+  unsigned char* h_in_block = nullptr;  // pinned mirror, same layout
   StepDyn* h_dyn = nullptr;
   double* h_nominal = nullptr;
   double* h_guide = nullptr;
@@ -477,13 +479,12 @@ exm_status upload_inputs(exm_handle* h, const double q0[3], const double* pts, c
   if (n > 0) std::memcpy(h->h_pts, pts, 2 * static_cast<size_t>(n) * sizeof(double));
   if (mask && n > 0) std::memcpy(h->h_mask, mask, static_cast<size_t>(n));
   cudaStream_t s = h->stream;
-  EXM_CUDA(cudaMemcpyAsync(h->d_dyn, h->h_dyn, sizeof(StepDyn), cudaMemcpyHostToDevice, s));
-  EXM_CUDA(cudaMemcpyAsync(h->d_nominal, h->h_nominal, TD * sizeof(double), cudaMemcpyHostToDevice, s));
-  EXM_CUDA(cudaMemcpyAsync(h->d_guide, h->h_guide, 2 * static_cast<size_t>(ng) * sizeof(double),
-                           cudaMemcpyHostToDevice, s));
-  if (n > 0)
-    EXM_CUDA(cudaMemcpyAsync(h->d_pts, h->h_pts, 2 * static_cast<size_t>(n) * sizeof(double),
-                             cudaMemcpyHostToDevice, s));
+  // dyn | nominal | guide | points share one allocation (same layout pinned and on device):
+  // one H2D copy for all of them, a second one for the mask.
+  const size_t head = static_cast<size_t>(reinterpret_cast<unsigned char*>(h->h_pts) -
+                                          reinterpret_cast<unsigned char*>(h->h_dyn)) +
+                      2 * static_cast<size_t>(n) * sizeof(double);
+  EXM_CUDA(cudaMemcpyAsync(h->d_dyn, h->h_dyn, head, cudaMemcpyHostToDevice, s));
   if (mask && n > 0)
     EXM_CUDA(cudaMemcpyAsync(h->d_mask, h->h_mask, static_cast<size_t>(n), cudaMemcpyHostToDevice, s));
   return EXM_OK;
@@ -638,11 +639,30 @@ exm_status exm_create(const exm_footprint* footprint, const exm_model* model,
   EXM_CUDA_C(cudaEventCreateWithFlags(&h->join_ev, cudaEventDisableTiming));
   const size_t KT = static_cast<size_t>(h->K) * h->T;
   const size_t TD = static_cast<size_t>(h->T) * D;
-  EXM_CUDA_C(dalloc(&h->d_dyn, 1));
-  EXM_CUDA_C(dalloc(&h->d_nominal, TD));
-  EXM_CUDA_C(dalloc(&h->d_guide, 2 * static_cast<size_t>(guide_cap)));
-  EXM_CUDA_C(dalloc(&h->d_pts, 2 * static_cast<size_t>(n_cap)));
-  EXM_CUDA_C(dalloc(&h->d_mask, static_cast<size_t>(n_cap)));
+  {
+    auto al = [](size_t b) { return (b + 255) & ~static_cast<size_t>(255); };
+    const size_t o_nom = al(sizeof(StepDyn));
+    const size_t o_guide = o_nom + al(TD * sizeof(double));
+    const size_t o_pts = o_guide + al(2 * static_cast<size_t>(guide_cap) * sizeof(double));
+    const size_t o_mask = o_pts + al(2 * static_cast<size_t>(n_cap) * sizeof(double));
+    const size_t total = o_mask + al(static_cast<size_t>(n_cap) + 1);
+    unsigned char* d = nullptr;
+    unsigned char* hh = nullptr;
+    EXM_CUDA_C(dalloc(&d, total));
+    EXM_CUDA_C(halloc(&hh, total));
+    h->d_in_block = d;
+    h->h_in_block = hh;
+    h->d_dyn = reinterpret_cast<StepDyn*>(d);
+    h->d_nominal = reinterpret_cast<double*>(d + o_nom);
+    h->d_guide = reinterpret_cast<double*>(d + o_guide);
+    h->d_pts = reinterpret_cast<double*>(d + o_pts);
+    h->d_mask = d + o_mask;
+    h->h_dyn = reinterpret_cast<StepDyn*>(hh);
+    h->h_nominal = reinterpret_cast<double*>(hh + o_nom);
+    h->h_guide = reinterpret_cast<double*>(hh + o_guide);
+    h->h_pts = reinterpret_cast<double*>(hh + o_pts);
+    h->h_mask = hh + o_mask;
+  }
   EXM_CUDA_C(dalloc(&h->d_tmp, static_cast<size_t>(n_cap)));
   EXM_CUDA_C(dalloc(&h->d_cloud, static_cast<size_t>(n_cap)));
   EXM_CUDA_C(dalloc(&h->d_cell_start, static_cast<size_t>(kGridMax) * kGridMax + 1));
@@ -664,11 +684,6 @@ exm_status exm_create(const exm_footprint* footprint, const exm_model* model,
   h->out_bytes = sizeof(DecisionDev) + sizeof(double) * (h->T + TD + 3);
   EXM_CUDA_C(dalloc(&h->d_out, h->out_bytes));
   EXM_CUDA_C(cudaMemset(h->d_out, 0, h->out_bytes));
-  EXM_CUDA_C(halloc(&h->h_dyn, 1));
-  EXM_CUDA_C(halloc(&h->h_nominal, TD));
-  EXM_CUDA_C(halloc(&h->h_guide, 2 * static_cast<size_t>(guide_cap)));
-  EXM_CUDA_C(halloc(&h->h_pts, 2 * static_cast<size_t>(n_cap)));
-  EXM_CUDA_C(halloc(&h->h_mask, static_cast<size_t>(n_cap)));
   EXM_CUDA_C(halloc(&h->h_out, h->out_bytes));
   EXM_CUDA_C(cudaEventCreate(&h->graph_ev.a));
   EXM_CUDA_C(cudaEventCreate(&h->graph_ev.b));
@@ -685,7 +700,7 @@ void exm_destroy(exm_handle* h) {
   if (h->stream) cudaStreamSynchronize(h->stream);
   destroy_graphs(h);
   if (h->comm && g_nccl.destroy) g_nccl.destroy(h->comm);
-  void* dev[] = {h->d_dyn, h->d_nominal, h->d_guide, h->d_pts, h->d_mask, h->d_tmp, h->d_cloud,
+  void* dev[] = {h->d_in_block, h->d_tmp, h->d_cloud,
                  h->d_cell_start, h->d_grid, h->d_eps, h->d_poses, h->d_xy, h->d_stage,
                  h->d_flags, h->d_val_xy, h->d_base, h->d_dmin,
                  h->d_partials, h->d_upd, h->d_val_poses, h->d_val_base, h->d_val_dmin, h->d_out,
@@ -693,7 +708,7 @@ void exm_destroy(exm_handle* h) {
                  h->sb_pts, h->sb_mask, h->sb_keys, h->sb_min, h->sb_pairs};
   for (void* p : dev)
     if (p) cudaFree(p);
-  void* host[] = {h->h_dyn, h->h_nominal, h->h_guide, h->h_pts, h->h_mask, h->h_out};
+  void* host[] = {h->h_in_block, h->h_out};
   for (void* p : host)
     if (p) cudaFreeHost(p);
   for (auto& p : h->ring) {
