@@ -199,6 +199,27 @@ exm_status exm_sdf_read(exm_handle* h, float* per_pair, double* per_pose_min);
 exm_status exm_batch_signed_distance(exm_handle* h, const double* queries, int32_t n,
                                      double* out);
 
+/* ---- hybrid mode families ---------------------------------------------
+ * Replaces the per-mode loop of HybridController::hybrid_cycle (hybrid.cpp:103-111): n_modes
+ * MPPI families that share the footprint, the cloud and the guidance, each with its own
+ * model and limits (modes[m], limits[m]) and the seed params.seed ^ (0x9E3779B97F4A7C15*(m+1))
+ * (hybrid.cpp:89). One call runs every family's MPPI step in one CUDA graph: one cloud
+ * preparation, one SDF launch over all n_modes*K*T poses, per-family noise/rollout and
+ * softmax/update/validation chains on parallel graph branches. Mode selection (switch
+ * penalty, cooldown, projection, deadzone; hybrid.cpp:113-155) stays with the caller.
+ * nominals_inout: n_modes blocks of T*3 doubles (family m uses its first T*dim_m);
+ * u_prev_inout: n_modes*3; out: n_modes decisions. */
+typedef struct exm_hybrid exm_hybrid;
+exm_status exm_hybrid_create(const exm_footprint* footprint, const exm_model* models,
+                             const exm_limits* limits, int32_t n_modes,
+                             const exm_params* params, int32_t n_cap, int32_t guide_cap,
+                             int32_t device, exm_hybrid** out);
+void exm_hybrid_destroy(exm_hybrid* hy);
+exm_status exm_hybrid_cycle(exm_hybrid* hy, const double q0[3], const double* pts_xy,
+                            const uint8_t* mask, int32_t n_points, const double* guide_xy,
+                            int32_t n_guide, const double goal[3], double* nominals_inout,
+                            double* u_prev_inout, uint64_t cycle, exm_decision* out);
+
 /* ---- multi-GPU (one process per GPU) ----------------------------------------------
  * The reference's only parallelism is a std::thread fork-join over rollouts
  * (controller.cpp:207-218). Here rollouts are sharded over ranks; rank 0 creates the id,

@@ -17,6 +17,7 @@
 
 #include "exactmppi/controller.hpp"
 #include "exactmppi/geometry.hpp"
+#include "exactmppi/hybrid.hpp"
 #include "exactmppi/kinematics.hpp"
 #include "exm_b200.h"
 
@@ -293,6 +294,54 @@ int32_t ref_controller_reset(void* cp) {
   return guard([&] {
     c->controller = std::make_unique<MppiController>(c->model, c->limits, c->spec, c->params,
                                                      c->threads);
+  });
+}
+
+// ---- HybridController (hybrid.hpp:51-69) over the reference's own MppiControllers ----
+struct RefHybrid {
+  std::unique_ptr<HybridController> hc;
+  std::vector<HybridMode> modes;
+};
+
+void* ref_hybrid_create(const exm_footprint* fp, const exm_model* models, const exm_limits* limits,
+                        int32_t n_modes, const exm_params* p, const double hp[6], int32_t threads) {
+  RefHybrid* out = nullptr;
+  int st = guard([&] {
+    auto h = std::make_unique<RefHybrid>();
+    for (int m = 0; m < n_modes; ++m)
+      h->modes.push_back({"m" + std::to_string(m), to_model(&models[m]), to_limits(&limits[m])});
+    HybridParams hpar;
+    hpar.lambda_switch = hp[0];
+    hpar.tau_cool_max = static_cast<int>(hp[1]);
+    hpar.v_min = hp[2];
+    hpar.omega_min = hp[3];
+    hpar.noise_deadzone_v = hp[4];
+    hpar.noise_deadzone_omega = hp[5];
+    h->hc = std::make_unique<HybridController>(h->modes, to_spec(fp), to_params(p), hpar,
+                                               threads < 1 ? 1 : threads);
+    out = h.release();
+  });
+  return st == EXM_OK ? out : nullptr;
+}
+
+void ref_hybrid_destroy(void* h) { delete static_cast<RefHybrid*>(h); }
+
+// command[3], mode_index, validated, mode_costs[n_modes], and the selected mode's diagnostics.
+int32_t ref_hybrid_cycle(void* hp, const double q0[3], const double* pts, const uint8_t* mask,
+                         int32_t n, const double* guide, int32_t n_guide, const double goal[3],
+                         double* command, int32_t* mode_index, int32_t* validated,
+                         double* mode_costs, double* diag /* best, entropy, nominal_cost */) {
+  auto* h = static_cast<RefHybrid*>(hp);
+  return guard([&] {
+    auto d = h->hc->hybrid_cycle({q0[0], q0[1], q0[2]}, to_cloud(pts, mask, n),
+                                 to_guidance(guide, n_guide, goal));
+    for (int k = 0; k < 3; ++k) command[k] = k < d.command.dim ? d.command[k] : 0.0;
+    *mode_index = d.mode_index;
+    *validated = d.validated ? 1 : 0;
+    for (std::size_t m = 0; m < d.mode_costs.size(); ++m) mode_costs[m] = d.mode_costs[m];
+    diag[0] = d.diagnostics.best_cost;
+    diag[1] = d.diagnostics.weight_entropy;
+    diag[2] = d.diagnostics.nominal_cost;
   });
 }
 

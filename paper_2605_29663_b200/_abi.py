@@ -67,6 +67,13 @@ class ExmHandle(C.Structure):
 
 _Hp = C.POINTER(ExmHandle)
 
+
+class ExmHybrid(C.Structure):
+    pass
+
+
+_HYp = C.POINTER(ExmHybrid)
+
 # name -> (restype, argtypes); every entry point declared in include/exm_b200.h
 SIGNATURES = {
     "exm_abi_version": (C.c_int32, []),
@@ -87,6 +94,12 @@ SIGNATURES = {
     "exm_sdf_run_resident": (C.c_int32, [_Hp, C.c_int32, C.c_int32]),
     "exm_sdf_read": (C.c_int32, [_Hp, _fp, _dp]),
     "exm_batch_signed_distance": (C.c_int32, [_Hp, _dp, C.c_int32, _dp]),
+    "exm_hybrid_create": (C.c_int32, [C.POINTER(ExmFootprint), C.POINTER(ExmModel),
+                                      C.POINTER(ExmLimits), C.c_int32, C.POINTER(ExmParams),
+                                      C.c_int32, C.c_int32, C.c_int32, C.POINTER(_HYp)]),
+    "exm_hybrid_destroy": (None, [_HYp]),
+    "exm_hybrid_cycle": (C.c_int32, [_HYp, _dp, _dp, _u8p, C.c_int32, _dp, C.c_int32, _dp, _dp,
+                                     _dp, C.c_uint64, C.POINTER(ExmDecision)]),
     "exm_nccl_unique_id": (C.c_int32, [C.POINTER(C.c_uint8)]),
     "exm_attach_comm": (C.c_int32, [_Hp, C.c_int32, C.c_int32, C.POINTER(C.c_uint8)]),
     "exm_stage_inputs": (C.c_int32, [_Hp, _dp, _dp, _u8p, C.c_int32, _dp, C.c_int32, _dp, _dp,

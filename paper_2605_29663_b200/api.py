@@ -562,3 +562,182 @@ def wrap_angle(a: float) -> float:  # geometry.cpp:17-23
     if a > math.pi:
         a -= tau
     return a
+
+
+# ------------------------------------------------------------------------------ hybrid modes
+@dataclass
+class HybridParams:
+    """HybridParams (hybrid.hpp:12-21)."""
+    lambda_switch: float = 5.0
+    tau_cool_max: int = 10
+    v_min: float = 0.05
+    omega_min: float = 0.05
+    noise_deadzone_v: float = 0.01
+    noise_deadzone_omega: float = 0.01
+
+    def validate(self):  # hybrid.cpp:9-16
+        if self.lambda_switch < 0.0:
+            raise ValueError("hybrid: lambda_switch must be >= 0")
+        if self.tau_cool_max < 0:
+            raise ValueError("hybrid: tau_cool_max must be >= 0")
+        if self.noise_deadzone_v < 0.0 or self.noise_deadzone_v >= self.v_min:
+            raise ValueError("hybrid: noise_deadzone_v must lie in [0, v_min)")
+        if self.noise_deadzone_omega < 0.0 or self.noise_deadzone_omega >= self.omega_min:
+            raise ValueError("hybrid: noise_deadzone_omega must lie in [0, omega_min)")
+
+
+@dataclass
+class HybridMode:
+    name: str
+    model: MotionModel
+    limits: KinematicLimits
+
+
+@dataclass
+class HybridDecision:
+    command: np.ndarray
+    mode_index: int
+    mode_name: str
+    validated: bool
+    mode_costs: list
+    diagnostics: ControlDecision
+
+
+def project_to_mode(u_raw: np.ndarray, mode: MotionModel) -> np.ndarray:
+    """hybrid.cpp:18-57: zero every inadmissible component; same-dim inputs pass through."""
+    u_raw = np.asarray(u_raw, np.float64).reshape(-1)
+    if u_raw.size == mode.control_dim():
+        return u_raw.copy()
+    vx = vy = om = 0.0
+    if u_raw.size == 3:
+        vx, vy, om = u_raw
+    elif u_raw.size == 2:
+        vx, om = u_raw
+    elif u_raw.size == 1:
+        vx = u_raw[0]
+    out = np.zeros(mode.control_dim())
+    if mode.tag == _abi.MODEL_DIFF:
+        out[:] = (vx, om)
+    elif mode.tag == _abi.MODEL_ACKERMANN:
+        out[0] = vx
+    elif mode.tag == _abi.MODEL_OMNI:
+        out[:] = (vx, vy, om)
+    elif mode.tag == _abi.MODEL_SPIN:
+        out[0] = om
+    else:
+        out[0] = vy
+    return out
+
+
+def deadzone_correct(u: np.ndarray, mode: MotionModel, hp: HybridParams) -> np.ndarray:
+    """hybrid.cpp:59-78."""
+    out = np.asarray(u, np.float64).copy()
+    if mode.tag == _abi.MODEL_SPIN:
+        w = out[0]
+        if hp.noise_deadzone_omega < abs(w) < hp.omega_min:
+            out[0] = math.copysign(hp.omega_min, w)
+        return out
+    lin = 2 if mode.tag == _abi.MODEL_OMNI else 1
+    mag = math.sqrt(sum(out[i] * out[i] for i in range(lin)))
+    if hp.noise_deadzone_v < mag < hp.v_min:
+        scale = hp.v_min / mag
+        for i in range(lin):
+            out[i] *= scale
+    return out
+
+
+class HybridController:
+    """HybridController (hybrid.hpp:51-69, hybrid.cpp:80-156) with all mode families stepped in
+    ONE device call (exm_hybrid_cycle: one cloud preparation, one SDF launch over every
+    family's poses, parallel per-family chains). Selection logic stays on the host."""
+
+    def __init__(self, modes, footprint: FootprintSpec, params: MppiParams,
+                 hybrid_params: HybridParams, threads: int = 1, n_cap: int = 1024,
+                 guide_cap: int = 64, device: int = 0):
+        del threads
+        if not modes:
+            raise ValueError("hybrid: at least one active mode required")
+        hybrid_params.validate()
+        self.modes, self.hp, self.params = list(modes), hybrid_params, params
+        self.M, self.T = len(self.modes), params.horizon
+        self.lib = _abi.load_library()
+        fp, keep = footprint._c()
+        self._keep = keep
+        models = (_abi.ExmModel * self.M)(*[m.model._c() for m in self.modes])
+        limits = (_abi.ExmLimits * self.M)(*[m.limits._c() for m in self.modes])
+        p = params._c()
+        h = C.POINTER(_abi.ExmHybrid)()
+        check(self.lib.exm_hybrid_create(C.byref(fp), models, limits, self.M, C.byref(p),
+                                         int(n_cap), int(guide_cap), int(device), C.byref(h)))
+        self.h = h
+        self.n_cap = int(n_cap)
+        self.nominals = np.zeros(self.M * self.T * 3)
+        self.u_prev = np.zeros(self.M * 3)
+        self.cycle = 0
+        self.m_prev = 0
+        self.tau_cool = 0
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.lib.exm_hybrid_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def family_cycles(self, q0, obstacles: ObstacleSet, guidance: Guidance):
+        """One device call: every family's MppiController::control_cycle."""
+        pts, mask = obstacles.points, obstacles.mask
+        if pts.shape[0] > self.n_cap:
+            raise ValueError("point count exceeds obstacle-set capacity")
+        dm = [np.empty(self.T) for _ in range(self.M)]
+        decs = (_abi.ExmDecision * self.M)()
+        for m in range(self.M):
+            decs[m].nominal_dmin = dptr(dm[m])
+        q = np.ascontiguousarray(np.asarray(q0, np.float64).reshape(3))
+        check(self.lib.exm_hybrid_cycle(self.h, dptr(q), dptr(pts), u8ptr(mask), pts.shape[0],
+                                        dptr(guidance.path), guidance.path.shape[0],
+                                        dptr(guidance.goal), dptr(self.nominals),
+                                        dptr(self.u_prev), self.cycle, decs))
+        self.cycle += 1
+        out = []
+        for m, mode in enumerate(self.modes):
+            d, D = decs[m], mode.model.control_dim()
+            nom = self.nominals[m * self.T * 3: m * self.T * 3 + self.T * D].reshape(self.T, D)
+            out.append(ControlDecision(np.array(d.command[:D]), bool(d.validated), nom.copy(),
+                                       d.best_cost, d.weight_entropy, d.nominal_cost, dm[m],
+                                       d.argmin))
+        return out
+
+    def hybrid_cycle(self, q0, obstacles: ObstacleSet, guidance: Guidance) -> HybridDecision:
+        decisions = self.family_cycles(q0, obstacles, guidance)
+        costs = [math.inf] * self.M
+        for m, d in enumerate(decisions):  # hybrid.cpp:103-111
+            if d.validated:
+                costs[m] = d.nominal_cost + (self.hp.lambda_switch if m != self.m_prev else 0.0)
+        if not any(math.isfinite(c) for c in costs):  # safe stop, hybrid.cpp:113-123
+            mp = self.modes[self.m_prev]
+            return HybridDecision(np.zeros(mp.model.control_dim()), self.m_prev, mp.name, False,
+                                  costs, decisions[self.m_prev])
+        best, best_cost = self.m_prev, costs[self.m_prev]  # ties toward m_prev, then order
+        for m in range(self.M):
+            if costs[m] < best_cost:
+                best, best_cost = m, costs[m]
+        if self.tau_cool > 0 and best != self.m_prev:  # blocked switch
+            best = self.m_prev
+        self.tau_cool = self.hp.tau_cool_max if best != self.m_prev else max(self.tau_cool - 1, 0)
+        sel = decisions[best]
+        raw = sel.command
+        cmd = deadzone_correct(project_to_mode(raw, self.modes[best].model),
+                               self.modes[best].model, self.hp)
+        for m in range(self.M):  # re-anchor the unselected families (hybrid.cpp:149-152)
+            if m == best:
+                continue
+            a = project_to_mode(raw, self.modes[m].model)
+            self.u_prev[3 * m: 3 * m + 3] = 0.0
+            self.u_prev[3 * m: 3 * m + a.size] = a
+        self.m_prev = best
+        return HybridDecision(cmd, best, self.modes[best].name, sel.validated, costs, sel)

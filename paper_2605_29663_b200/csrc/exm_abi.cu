@@ -307,6 +307,8 @@ struct exm_handle {
   int sb_P = 0, sb_N = 0, sb_has_mask = 0, sb_last_pairs = 0;
   int launches_per_step = 0;
   int64_t last_pairs = 0;
+  // hybrid families share the pose / d_min arrays and family 0's cloud grid
+  bool borrowed_poses = false, borrowed_cloud = false;
 };
 
 namespace {
@@ -338,37 +340,36 @@ void destroy_graphs(exm_handle* h) {
     }
 }
 
-// The control step: [noise] -> cloud prep -> rollout -> SDF -> block partials ->
-// [all-gather] -> merge/update/validation rollout -> validation SDF -> finalize.
-exm_status enqueue_step(exm_handle* h, bool draw_noise, const EventPair* ev, cudaStream_t s,
-                        bool capturing) {
-  const StepConst& sc = h->sc;
-  int launches = 0;
-  // Fork: the cloud preparation (single CTA) runs on a side stream concurrently with the
-  // noise + rollout branch; the graph captures both branches and the join before the SDF.
-  EXM_CUDA(cudaEventRecord(h->fork_ev, s));
-  EXM_CUDA(cudaStreamWaitEvent(h->side, h->fork_ev, 0));
+// Phases of one control step (all stream-ordered, capturable):
+//   prep  : cloud preparation (mask, recentre, grid)                 -> d_cloud, d_grid
+//   pre   : [noise] -> rollout                                       -> d_poses, d_xy, d_base
+//   sdf   : per-pose exact SDF over the step's K*T poses             -> d_dmin
+//   post  : stage costs -> block partials -> [all-gather] -> merge/update/validation
+//           dynamics -> validation SDF -> finalize                    -> d_out, state
+exm_status enqueue_prep(exm_handle* h, cudaStream_t s) {
   EXM_CUDA(launch_cloud_prep(h->d_pts, h->d_mask, h->d_dyn, h->fp.radius, h->d_tmp, h->d_cloud,
-                             h->d_cell_start, h->d_grid, h->side));
-  EXM_CUDA(cudaEventRecord(h->join_ev, h->side));
+                             h->d_cell_start, h->d_grid, s));
+  return EXM_OK;
+}
+
+exm_status enqueue_pre(exm_handle* h, bool draw_noise, cudaStream_t s, int* launches) {
+  const StepConst& sc = h->sc;
   if (draw_noise) {
     EXM_CUDA(launch_noise(sc, h->d_dyn, h->d_eps, s));
-    ++launches;
+    ++*launches;
   }
   EXM_CUDA(launch_rollout(sc, h->d_dyn, h->d_nominal, h->d_eps, h->d_poses, h->d_xy, h->d_base,
                           nullptr, nullptr, s));
-  EXM_CUDA(cudaStreamWaitEvent(s, h->join_ev, 0));
-  if (ev) EXM_CUDA(capturing ? cudaEventRecordWithFlags(ev->a, s, cudaEventRecordExternal)
-                             : cudaEventRecord(ev->a, s));
-  EXM_CUDA(launch_sdf_grid(h->fp, h->d_poses, sc.k_local * sc.T, h->d_grid, h->d_cell_start,
-                           h->d_cloud, h->d_dmin, s));
-  if (ev) EXM_CUDA(capturing ? cudaEventRecordWithFlags(ev->b, s, cudaEventRecordExternal)
-                             : cudaEventRecord(ev->b, s));
+  ++*launches;
+  return EXM_OK;
+}
+
+exm_status enqueue_post(exm_handle* h, cudaStream_t s, int* launches) {
+  const StepConst& sc = h->sc;
   EXM_CUDA(launch_stage_costs(sc, h->d_dyn, h->d_guide, h->guide_cap, h->d_xy, h->d_dmin,
                               h->d_stage, h->d_flags, s));
   EXM_CUDA(launch_block_partials(sc, h->d_base, h->d_stage, h->d_flags, h->d_eps, h->d_partials,
                                  nullptr, nullptr, s));
-  launches += 5;
   if (h->world > 1) {
     const size_t count = static_cast<size_t>(sc.nblocks_local) * partial_stride(sc.T, sc.D);
     const int rc = g_nccl.allgather(h->d_partials + static_cast<size_t>(sc.block_offset) *
@@ -384,7 +385,36 @@ exm_status enqueue_step(exm_handle* h, bool draw_noise, const EventPair* ev, cud
   EXM_CUDA(launch_finalize(sc, h->d_val_dmin, h->d_val_xy, h->d_val_base, h->d_upd, h->d_guide,
                            h->guide_cap, h->d_nominal, h->d_dyn, out_dec(h), out_dmin(h),
                            out_nominal(h), out_uprev(h), 1, s));
-  launches += 3;
+  *launches += 6;
+  return EXM_OK;
+}
+
+exm_status record_ev(cudaEvent_t e, cudaStream_t s, bool capturing) {
+  EXM_CUDA(capturing ? cudaEventRecordWithFlags(e, s, cudaEventRecordExternal)
+                     : cudaEventRecord(e, s));
+  return EXM_OK;
+}
+
+// The control step. The cloud preparation (single CTA) runs on a side stream concurrently
+// with the noise + rollout branch; the graph captures both branches and their join.
+exm_status enqueue_step(exm_handle* h, bool draw_noise, const EventPair* ev, cudaStream_t s,
+                        bool capturing) {
+  const StepConst& sc = h->sc;
+  int launches = 0;
+  exm_status st;
+  EXM_CUDA(cudaEventRecord(h->fork_ev, s));
+  EXM_CUDA(cudaStreamWaitEvent(h->side, h->fork_ev, 0));
+  if ((st = enqueue_prep(h, h->side)) != EXM_OK) return st;
+  ++launches;
+  EXM_CUDA(cudaEventRecord(h->join_ev, h->side));
+  if ((st = enqueue_pre(h, draw_noise, s, &launches)) != EXM_OK) return st;
+  EXM_CUDA(cudaStreamWaitEvent(s, h->join_ev, 0));
+  if (ev && (st = record_ev(ev->a, s, capturing)) != EXM_OK) return st;
+  EXM_CUDA(launch_sdf_grid(h->fp, h->d_poses, sc.k_local * sc.T, h->d_grid, h->d_cell_start,
+                           h->d_cloud, h->d_dmin, s));
+  ++launches;
+  if (ev && (st = record_ev(ev->b, s, capturing)) != EXM_OK) return st;
+  if ((st = enqueue_post(h, s, &launches)) != EXM_OK) return st;
   h->launches_per_step = launches;
   return EXM_OK;
 }
@@ -700,6 +730,8 @@ void exm_destroy(exm_handle* h) {
   if (h->stream) cudaStreamSynchronize(h->stream);
   destroy_graphs(h);
   if (h->comm && g_nccl.destroy) g_nccl.destroy(h->comm);
+  if (h->borrowed_poses) h->d_poses = nullptr, h->d_dmin = nullptr;
+  if (h->borrowed_cloud) h->d_cloud = nullptr, h->d_cell_start = nullptr, h->d_grid = nullptr;
   void* dev[] = {h->d_in_block, h->d_tmp, h->d_cloud,
                  h->d_cell_start, h->d_grid, h->d_eps, h->d_poses, h->d_xy, h->d_stage,
                  h->d_flags, h->d_val_xy, h->d_base, h->d_dmin,
@@ -1044,6 +1076,189 @@ exm_status exm_step_stats(exm_handle* h, int32_t* launches_per_step, float* sdf_
   if (sdf_ms) *sdf_ms = n ? total / n : 0.0f;
   h->ring_used = 0;  // consumed: the next run starts a fresh accumulation
   if (sdf_pairs) *sdf_pairs = h->last_pairs;
+  return EXM_OK;
+}
+
+}  // extern "C"
+
+// =========================================================================== hybrid families
+struct exm_hybrid {
+  int M = 0, K = 0, T = 0, device = 0;
+  std::vector<exm_handle*> fam;
+  float4* poses_all = nullptr;  // [m][r][h]
+  float* dmin_all = nullptr;
+  cudaEvent_t fork = nullptr, prep_done = nullptr, sdf_done = nullptr;
+  std::vector<cudaEvent_t> pre_done, fin;
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t exec = nullptr;
+};
+
+namespace {
+
+// One graph: cloud prep (family 0) || per-family noise+rollout -> one SDF over all families'
+// poses -> per-family post chains in parallel -> join.
+exm_status hybrid_enqueue(exm_hybrid* hy, cudaStream_t s0) {
+  exm_handle* f0 = hy->fam[0];
+  exm_status st;
+  int launches = 0;
+  EXM_CUDA(cudaEventRecord(hy->fork, s0));
+  EXM_CUDA(cudaStreamWaitEvent(f0->side, hy->fork, 0));
+  if ((st = enqueue_prep(f0, f0->side)) != EXM_OK) return st;
+  EXM_CUDA(cudaEventRecord(hy->prep_done, f0->side));
+  for (int m = 0; m < hy->M; ++m) {
+    cudaStream_t sm = m == 0 ? s0 : hy->fam[m]->stream;
+    if (m) EXM_CUDA(cudaStreamWaitEvent(sm, hy->fork, 0));
+    if ((st = enqueue_pre(hy->fam[m], true, sm, &launches)) != EXM_OK) return st;
+    EXM_CUDA(cudaEventRecord(hy->pre_done[m], sm));
+  }
+  for (int m = 1; m < hy->M; ++m) EXM_CUDA(cudaStreamWaitEvent(s0, hy->pre_done[m], 0));
+  EXM_CUDA(cudaStreamWaitEvent(s0, hy->prep_done, 0));
+  EXM_CUDA(launch_sdf_grid(f0->fp, hy->poses_all, hy->M * hy->K * hy->T, f0->d_grid,
+                           f0->d_cell_start, f0->d_cloud, hy->dmin_all, s0));
+  EXM_CUDA(cudaEventRecord(hy->sdf_done, s0));
+  for (int m = 0; m < hy->M; ++m) {
+    cudaStream_t sm = m == 0 ? s0 : hy->fam[m]->stream;
+    if (m) EXM_CUDA(cudaStreamWaitEvent(sm, hy->sdf_done, 0));
+    if ((st = enqueue_post(hy->fam[m], sm, &launches)) != EXM_OK) return st;
+    EXM_CUDA(cudaEventRecord(hy->fin[m], sm));
+  }
+  for (int m = 1; m < hy->M; ++m) EXM_CUDA(cudaStreamWaitEvent(s0, hy->fin[m], 0));
+  return EXM_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+void exm_hybrid_destroy(exm_hybrid* hy) {
+  if (!hy) return;
+  cudaSetDevice(hy->device);
+  if (!hy->fam.empty() && hy->fam[0]) cudaStreamSynchronize(hy->fam[0]->stream);
+  if (hy->exec) cudaGraphExecDestroy(hy->exec);
+  if (hy->graph) cudaGraphDestroy(hy->graph);
+  cudaEvent_t evs[] = {hy->fork, hy->prep_done, hy->sdf_done};
+  for (auto e : evs)
+    if (e) cudaEventDestroy(e);
+  for (auto e : hy->pre_done) cudaEventDestroy(e);
+  for (auto e : hy->fin) cudaEventDestroy(e);
+  for (exm_handle* h : hy->fam) exm_destroy(h);  // families free only what they own
+  if (hy->poses_all) cudaFree(hy->poses_all);
+  if (hy->dmin_all) cudaFree(hy->dmin_all);
+  delete hy;
+}
+
+exm_status exm_hybrid_create(const exm_footprint* footprint, const exm_model* models,
+                             const exm_limits* limits, int32_t n_modes,
+                             const exm_params* params, int32_t n_cap, int32_t guide_cap,
+                             int32_t device, exm_hybrid** out) {
+  if (!out) return fail(EXM_ERR_INVALID_ARGUMENT, "out handle pointer is null");
+  *out = nullptr;
+  if (n_modes < 1 || !models || !limits || !params)
+    return fail(EXM_ERR_INVALID_ARGUMENT, "hybrid: at least one active mode required");
+  auto* hy = new exm_hybrid();
+  hy->M = n_modes;
+  hy->K = params->rollouts;
+  hy->T = params->horizon;
+  for (int m = 0; m < n_modes; ++m) {
+    exm_params p = *params;
+    p.seed = params->seed ^ (0x9E3779B97F4A7C15ull * static_cast<uint64_t>(m + 1));  // hybrid.cpp:89
+    exm_handle* h = nullptr;
+    exm_status st = exm_create(footprint, &models[m], &limits[m], &p, m == 0 ? n_cap : 0,
+                               guide_cap, device, &h);
+    if (st != EXM_OK) {
+      exm_hybrid_destroy(hy);
+      return st;
+    }
+    hy->fam.push_back(h);
+  }
+  exm_handle* f0 = hy->fam[0];
+  hy->device = f0->device;
+  auto bail = [&](exm_status s) {
+    exm_hybrid_destroy(hy);
+    return s;
+  };
+  const size_t KT = static_cast<size_t>(hy->K) * hy->T;
+  cudaError_t ce;
+  if ((ce = dalloc(&hy->poses_all, KT * n_modes)) != cudaSuccess ||
+      (ce = dalloc(&hy->dmin_all, KT * n_modes)) != cudaSuccess)
+    return bail(fail(EXM_ERR_CUDA, std::string("hybrid alloc: ") + cudaGetErrorString(ce)));
+  for (int m = 0; m < n_modes; ++m) {
+    exm_handle* h = hy->fam[m];
+    cudaFree(h->d_poses);
+    cudaFree(h->d_dmin);
+    h->d_poses = hy->poses_all + m * KT;
+    h->d_dmin = hy->dmin_all + m * KT;
+    h->borrowed_poses = true;
+    if (m > 0) {
+      cudaFree(h->d_cloud);
+      cudaFree(h->d_cell_start);
+      cudaFree(h->d_grid);
+      h->d_cloud = f0->d_cloud;
+      h->d_cell_start = f0->d_cell_start;
+      h->d_grid = f0->d_grid;
+      h->borrowed_cloud = true;
+    }
+  }
+  cudaEvent_t* evs[] = {&hy->fork, &hy->prep_done, &hy->sdf_done};
+  for (auto e : evs)
+    if ((ce = cudaEventCreateWithFlags(e, cudaEventDisableTiming)) != cudaSuccess)
+      return bail(fail(EXM_ERR_CUDA, cudaGetErrorString(ce)));
+  hy->pre_done.resize(n_modes);
+  hy->fin.resize(n_modes);
+  for (int m = 0; m < n_modes; ++m) {
+    cudaEventCreateWithFlags(&hy->pre_done[m], cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&hy->fin[m], cudaEventDisableTiming);
+  }
+  *out = hy;
+  return EXM_OK;
+}
+
+exm_status exm_hybrid_cycle(exm_hybrid* hy, const double q0[3], const double* pts_xy,
+                            const uint8_t* mask, int32_t n_points, const double* guide_xy,
+                            int32_t n_guide, const double goal[3], double* nominals_inout,
+                            double* u_prev_inout, uint64_t cycle, exm_decision* out) {
+  if (!hy) return fail(EXM_ERR_INVALID_ARGUMENT, "hybrid handle is null");
+  if (!nominals_inout || !u_prev_inout) return fail(EXM_ERR_INVALID_ARGUMENT, "null state pointer");
+  EXM_CUDA(cudaSetDevice(hy->device));
+  exm_handle* f0 = hy->fam[0];
+  cudaStream_t s0 = f0->stream;
+  const size_t stride = static_cast<size_t>(hy->T) * 3;
+  for (int m = 0; m < hy->M; ++m) {
+    exm_handle* h = hy->fam[m];
+    // only family 0 prepares the cloud; the others upload just their state and the guidance
+    exm_status st = upload_inputs(h, q0, m == 0 ? pts_xy : nullptr, m == 0 ? mask : nullptr,
+                                  m == 0 ? n_points : 0, guide_xy, n_guide, goal,
+                                  nominals_inout + m * stride, u_prev_inout + 3 * m, cycle);
+    if (st != EXM_OK) return st;
+    if (m) {  // family m's copies were issued on its own stream: order them before the graph
+      EXM_CUDA(cudaEventRecord(hy->pre_done[m], h->stream));
+      EXM_CUDA(cudaStreamWaitEvent(s0, hy->pre_done[m], 0));
+    }
+  }
+  if (!hy->exec) {
+    cudaGraph_t g = nullptr;
+    EXM_CUDA(cudaStreamBeginCapture(s0, cudaStreamCaptureModeThreadLocal));
+    exm_status st = hybrid_enqueue(hy, s0);
+    cudaError_t ce = cudaStreamEndCapture(s0, &g);
+    if (st != EXM_OK) {
+      if (g) cudaGraphDestroy(g);
+      return st;
+    }
+    if (ce != cudaSuccess) return fail(EXM_ERR_CUDA, std::string("capture: ") + cudaGetErrorString(ce));
+    EXM_CUDA(cudaGraphInstantiate(&hy->exec, g, 0));
+    hy->graph = g;
+  }
+  EXM_CUDA(cudaGraphLaunch(hy->exec, s0));
+  for (int m = 0; m < hy->M; ++m)
+    EXM_CUDA(cudaMemcpyAsync(hy->fam[m]->h_out, hy->fam[m]->d_out, hy->fam[m]->out_bytes,
+                             cudaMemcpyDeviceToHost, s0));
+  EXM_CUDA(cudaStreamSynchronize(s0));
+  for (int m = 0; m < hy->M; ++m) {
+    exm_handle* h = hy->fam[m];
+    h->last_steps = 1;
+    h->ring_used = 0;
+    unpack_decision(h, out ? out + m : nullptr, nominals_inout + m * stride, u_prev_inout + 3 * m);
+  }
   return EXM_OK;
 }
 

@@ -295,4 +295,33 @@ def cfg5(K: int = 65536, T: int = 80, N: int = 50_000, cycle: int = 0) -> Worklo
                     "omni L (B=6), K=65536, T=80, N=50000, moving discs + gap walls")
 
 
+# trap_hybrid.json: the three mode families, the obstacles and the hybrid block.
+TRAP_OBSTACLES = [
+    [[-5.0, 0.8], [5.0, 0.8], [5.0, 1.1], [-5.0, 1.1]],
+    [[-5.0, -1.15], [2.0, -1.15], [2.0, -0.5], [-5.0, -0.5]],
+    [[3.25, -1.15], [5.0, -1.15], [5.0, -0.5], [3.25, -0.5]],
+    [[1.7, -1.45], [3.55, -1.45], [3.55, -1.15], [1.7, -1.15]],
+]
+
+
+def trap_hybrid(K: int = 384, T: int = 25, N: int = 400):
+    """The trap_hybrid fixture as a hybrid workload: (footprint, modes, params, hybrid params,
+    q0, cloud, guidance). Cloud: N boundary samples of the four trap obstacles."""
+    from .api import HybridMode, HybridParams
+    fp = FootprintSpec.rect_cover([[0.0, 0.0]], [[0.5, 0.25]], "hybrid-box")
+    modes = [
+        HybridMode("ackermann", MotionModel.ackermann(0.5), KinematicLimits.from_json(TRAP_ACK_LIMITS)),
+        HybridMode("parallel", MotionModel.parallel(), KinematicLimits.from_json(
+            {"acc_max": [1.5], "acc_min": [-1.5], "steer_max": 1e9, "vel_max": [0.5], "vel_min": [-0.5]})),
+        HybridMode("spin", MotionModel.spin(), KinematicLimits.from_json(
+            {"acc_max": [4.0], "acc_min": [-4.0], "steer_max": 1e9, "vel_max": [1.0], "vel_min": [-1.0]})),
+    ]
+    params = MppiParams.from_json(TRAP_MPPI, rollouts=K, horizon=T, seed=1)
+    hp = HybridParams(lambda_switch=3.0, tau_cool_max=5, v_min=0.05, omega_min=0.05,
+                      noise_deadzone_v=0.01, noise_deadzone_omega=0.01)
+    return (fp, modes, params, hp, np.array([2.625, -0.825, 0.0]),
+            sample_boundaries(TRAP_OBSTACLES, N),
+            Guidance([[2.625, -0.825], [2.625, 0.15], [-3.0, 0.0]], [-3.0, 0.0, 0.0]))
+
+
 CONFIGS = {"cfg1": cfg1, "cfg2": cfg2, "cfg3": cfg3, "cfg5": cfg5}

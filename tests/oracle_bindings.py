@@ -356,3 +356,52 @@ def oracle_weights(costs, lam):
     w = np.empty_like(costs)
     oracle_lib().exo_weights_from_costs(_p(costs), costs.size, lam, _p(w))
     return w
+
+
+class ReferenceHybrid:
+    """The reference's HybridController (hybrid.cpp) over its own MppiControllers (oracle/_ref)."""
+
+    def __init__(self, footprint, modes, params, hp, threads=1):
+        L = ref_lib()
+        if not hasattr(L, "_hy_ready"):
+            L.ref_hybrid_create.restype = C.c_void_p
+            L.ref_hybrid_create.argtypes = [C.POINTER(ExmFootprint), C.POINTER(ExmModel),
+                                            C.POINTER(ExmLimits), C.c_int32, C.POINTER(ExmParams),
+                                            _dp, C.c_int32]
+            L.ref_hybrid_destroy.argtypes = [C.c_void_p]
+            L.ref_hybrid_cycle.restype = C.c_int32
+            L.ref_hybrid_cycle.argtypes = [C.c_void_p, _dp, _dp, _u8p, C.c_int32, _dp, C.c_int32,
+                                           _dp, _dp, C.POINTER(C.c_int32), C.POINTER(C.c_int32),
+                                           _dp, _dp]
+            L._hy_ready = True
+        self.L, self.M = L, len(modes)
+        fp, self._keep = footprint._c()
+        models = (ExmModel * self.M)(*[m.model._c() for m in modes])
+        limits = (ExmLimits * self.M)(*[m.limits._c() for m in modes])
+        p = params._c()
+        h = np.array([hp.lambda_switch, hp.tau_cool_max, hp.v_min, hp.omega_min,
+                      hp.noise_deadzone_v, hp.noise_deadzone_omega], np.float64)
+        self.ctx = L.ref_hybrid_create(C.byref(fp), models, limits, self.M, C.byref(p), _p(h),
+                                       int(threads))
+        if not self.ctx:
+            raise ValueError(L.ref_last_error().decode())
+
+    def __del__(self):
+        try:
+            self.L.ref_hybrid_destroy(self.ctx)
+        except Exception:
+            pass
+
+    def hybrid_cycle(self, q0, pts, mask, guidance):
+        pts = _c(pts).reshape(-1, 2)
+        cmd = np.zeros(3)
+        mi, val = C.c_int32(), C.c_int32()
+        costs = np.zeros(self.M)
+        diag = np.zeros(3)
+        rc = self.L.ref_hybrid_cycle(self.ctx, _p(_c(q0)), _p(pts), _m(mask), pts.shape[0],
+                                     _p(guidance.path), guidance.path.shape[0], _p(guidance.goal),
+                                     _p(cmd), C.byref(mi), C.byref(val), _p(costs), _p(diag))
+        if rc:
+            raise ValueError(self.L.ref_last_error().decode())
+        return dict(command=cmd, mode_index=mi.value, validated=bool(val.value), mode_costs=costs,
+                    best_cost=diag[0], weight_entropy=diag[1], nominal_cost=diag[2])
