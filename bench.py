@@ -260,11 +260,17 @@ def run_ours(args, world, rank, local):
         eng.control_cycle_raw(wl.q0, obstacles, wl.guidance, nom, up, c)
     if world > 1:
         torch.distributed.barrier()
+    # config 5 has moving obstacles: the cloud is regenerated every cycle (quasi-static within
+    # the horizon) — cycle through 8 pre-generated snapshots so every e2e step
+    # uploads a different cloud.
+    clouds = [obstacles]
+    if args.config == "cfg5":
+        clouds = [W.cfg5(cycle=10 * j).obstacles() for j in range(8)]
     e2e_ms = []
     t0 = time.perf_counter()
     for c in range(args.steps):
         t1 = time.perf_counter()
-        eng.control_cycle_raw(wl.q0, obstacles, wl.guidance, nom, up, 1000 + c)
+        eng.control_cycle_raw(wl.q0, clouds[c % len(clouds)], wl.guidance, nom, up, 1000 + c)
         e2e_ms.append(1e3 * (time.perf_counter() - t1))
     e2e_s = allreduce_max((time.perf_counter() - t0) / args.steps, world)
     h2d = 104 + 8 * T * D + 16 * wl.guidance.path.shape[0] + 16 * N + N
@@ -311,6 +317,8 @@ def run_ours(args, world, rank, local):
         line["cpu_baseline"] = {k: base[k] for k in ("value", "unit", "cores", "kind", "sample")}
     if rank == 0 and not args.no_sdf_batch:
         line["sdf_batch"] = bench_sdf_batch(args, torch, peak, peak_src)
+    if rank == 0 and not args.no_sdf_batch:
+        line["hybrid"] = bench_hybrid(args, torch)
     if rank == 0:
         print(json.dumps(line), flush=True)
 
@@ -343,6 +351,41 @@ def bench_sdf_batch(args, torch, peak, peak_src):
                          "traffic": prof.get("traffic"), "executed": prof.get("executed"),
                          "algorithmic": f"P*N pairs x {F} ops/pair (every pair evaluated)",
                          "peak_source": peak_src}}
+
+
+def bench_hybrid(args, torch):
+    """the three trap_hybrid mode families (Ackermann, parallel, spin; hybrid-box,
+    K=384, T=25) stepped in one device call vs one exm_control_cycle per family (wall clock per
+    hybrid step, host API both ways, selection on the host excluded)."""
+    from paper_2605_29663_b200 import workloads as W
+    from paper_2605_29663_b200.api import Engine, HybridController, ObstacleSet
+    fp, modes, params, hp, q0, cloud, g = W.trap_hybrid()
+    obst = ObstacleSet(cloud, np.ones(cloud.shape[0], np.uint8))
+    hc = HybridController(modes, fp, params, hp, n_cap=cloud.shape[0], guide_cap=8)
+    singles = []
+    for m, mode in enumerate(modes):
+        p = W.MppiParams(**{**params.__dict__})
+        p.seed = params.seed ^ ((0x9E3779B97F4A7C15 * (m + 1)) & 0xFFFFFFFFFFFFFFFF)
+        e = Engine(mode.model, mode.limits, fp, p, n_cap=cloud.shape[0], guide_cap=8)
+        singles.append((e, np.zeros(params.horizon * mode.model.control_dim()), np.zeros(3)))
+    n = max(20, args.steps // 2)
+    for _ in range(5):
+        hc.family_cycles(q0, obst, g)
+    t0 = time.perf_counter()
+    for _ in range(n):
+        hc.family_cycles(q0, obst, g)
+    batched = (time.perf_counter() - t0) / n
+    for c in range(5):
+        for e, nom, up in singles:
+            e.control_cycle_raw(q0, obst, g, nom, up, c)
+    t0 = time.perf_counter()
+    for c in range(n):
+        for e, nom, up in singles:
+            e.control_cycle_raw(q0, obst, g, nom, up, c)
+    seq = (time.perf_counter() - t0) / n
+    return {"workload": "trap_hybrid 3 families (ackermann/parallel/spin), K=384, T=25, N=400",
+            "batched_ms_per_step": 1e3 * batched, "per_family_calls_ms_per_step": 1e3 * seq,
+            "speedup": seq / batched}
 
 
 def main():
