@@ -10,6 +10,7 @@
 #include <dlfcn.h>
 
 #include <algorithm>
+#include <array>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -120,6 +121,89 @@ bool segments_cross(const std::vector<double>& x, const std::vector<double>& y, 
          (o3 == 0 && within(cx, cy, dx, dy, ax, ay)) || (o4 == 0 && within(cx, cy, dx, dy, bx, by));
 }
 
+// Bounding box {x0, x1, y0, y1} of the part of polygon (x, y) inside the slab
+// lo <= coord < hi along `axis` (Sutherland-Hodgman clip against two half-planes); empty ->
+// x0 > x1.
+std::array<double, 4> clipped_box(const std::vector<double>& x, const std::vector<double>& y,
+                                  int axis, double lo, double hi) {
+  std::vector<std::array<double, 2>> poly;
+  for (size_t i = 0; i < x.size(); ++i) poly.push_back({x[i], y[i]});
+  auto clip = [&](double bound, bool keep_above) {
+    std::vector<std::array<double, 2>> out;
+    const size_t n = poly.size();
+    for (size_t i = 0; i < n; ++i) {
+      const auto& a = poly[i];
+      const auto& b = poly[(i + 1) % n];
+      const bool ina = keep_above ? a[axis] >= bound : a[axis] <= bound;
+      const bool inb = keep_above ? b[axis] >= bound : b[axis] <= bound;
+      if (ina) out.push_back(a);
+      if (ina != inb) {
+        const double t = (bound - a[axis]) / (b[axis] - a[axis]);
+        out.push_back({a[0] + t * (b[0] - a[0]), a[1] + t * (b[1] - a[1])});
+      }
+    }
+    poly = out;
+  };
+  clip(lo, true);
+  if (!poly.empty()) clip(hi, false);
+  std::array<double, 4> bb = {1e300, -1e300, 1e300, -1e300};
+  for (const auto& v : poly) {
+    bb[0] = std::min(bb[0], v[0]);
+    bb[1] = std::max(bb[1], v[0]);
+    bb[2] = std::min(bb[2], v[1]);
+    bb[3] = std::max(bb[3], v[1]);
+  }
+  return bb;
+}
+
+// Greedy cover of a polygon by <= max_boxes axis-aligned boxes: repeatedly split the largest
+// box at the vertex coordinate (either axis) that minimises the summed area of the two
+// clipped halves. Exact (zero slack) for rectilinear polygons whose cuts it finds.
+std::vector<std::array<double, 4>> cover_boxes(const std::vector<double>& x,
+                                               const std::vector<double>& y, int max_boxes) {
+  auto area = [](const std::array<double, 4>& b) {
+    return b[0] > b[1] ? 0.0 : (b[1] - b[0]) * (b[3] - b[2]);
+  };
+  std::vector<std::array<double, 4>> boxes = {clipped_box(x, y, 0, -1e300, 1e300)};
+  while (static_cast<int>(boxes.size()) < max_boxes) {
+    size_t big = 0;
+    for (size_t j = 1; j < boxes.size(); ++j)
+      if (area(boxes[j]) > area(boxes[big])) big = j;
+    const auto b = boxes[big];
+    double best_gain = 1e-9 * area(b), best_cut = 0.0;
+    int best_axis = -1;
+    std::array<double, 4> best_lo{}, best_hi{};
+    for (int axis = 0; axis < 2; ++axis) {
+      const std::vector<double>& c = axis == 0 ? x : y;
+      for (double cut : c) {
+        if (cut <= (axis == 0 ? b[0] : b[2]) || cut >= (axis == 0 ? b[1] : b[3])) continue;
+        const double lo0 = axis == 0 ? b[0] : b[2], hi1 = axis == 0 ? b[1] : b[3];
+        auto lo = clipped_box(x, y, axis, lo0, cut);
+        auto hi = clipped_box(x, y, axis, cut, hi1);
+        // restrict to the current box on the other axis
+        const int o = axis == 0 ? 2 : 0;
+        for (auto* q : {&lo, &hi}) {
+          (*q)[o] = std::max((*q)[o], b[o]);
+          (*q)[o + 1] = std::min((*q)[o + 1], b[o + 1]);
+        }
+        const double gain = area(b) - area(lo) - area(hi);
+        if (gain > best_gain) {
+          best_gain = gain;
+          best_cut = cut;
+          best_axis = axis;
+          best_lo = lo;
+          best_hi = hi;
+        }
+      }
+    }
+    (void)best_cut;
+    if (best_axis < 0) break;
+    boxes[big] = best_lo;
+    boxes.push_back(best_hi);
+  }
+  return boxes;
+}
+
 exm_status build_footprint(const exm_footprint* fp, FpDev* out) {
   std::memset(out, 0, sizeof *out);
   if (!fp) return fail(EXM_ERR_INVALID_ARGUMENT, "footprint is null");
@@ -211,6 +295,22 @@ exm_status build_footprint(const exm_footprint* fp, FpDev* out) {
   out->aabb[1] = static_cast<float>(bx1 + m);
   out->aabb[2] = static_cast<float>(by0 - m);
   out->aabb[3] = static_cast<float>(by1 + m);
+  if (out->kind == EXM_FOOTPRINT_POLYGON) {
+    std::vector<double> px(out->count), py(out->count);
+    for (int i = 0; i < out->count; ++i) {
+      px[i] = out->e[i][0];
+      py[i] = out->e[i][1];
+    }
+    const auto boxes = cover_boxes(px, py, kMaxCover);
+    out->ncover = static_cast<int>(boxes.size());
+    for (int j = 0; j < kMaxCover; ++j) {  // unused slots repeat box 0 (the kernel unrolls)
+      const auto& bj = boxes[static_cast<size_t>(j) < boxes.size() ? j : 0];
+      out->cover[j][0] = static_cast<float>(0.5 * (bj[0] + bj[1]));
+      out->cover[j][1] = static_cast<float>(0.5 * (bj[2] + bj[3]));
+      out->cover[j][2] = static_cast<float>(0.5 * (bj[1] - bj[0]) + m);
+      out->cover[j][3] = static_cast<float>(0.5 * (bj[3] - bj[2]) + m);
+    }
+  }
   return EXM_OK;
 }
 

@@ -9,6 +9,7 @@
 namespace exm {
 
 constexpr int kMaxEdges = 64;        // polygon edges / cover boxes held in kernel parameters
+constexpr int kMaxCover = 3;         // boxes of the polygon cull cover
 constexpr int kBlockRollouts = 256;  // rollouts per softmax partial (fixed: G-invariant)
 constexpr int kGridMax = 128;        // cloud grid cells per axis (<= 16384 cells, smem histogram)
 constexpr float kEmptyDistance = 1e6f;  // kEmptyMaskDistance (geometry.hpp:37)
@@ -25,6 +26,12 @@ struct FpDev {
   float radius;  // PreparedFootprint::bounding_radius (max vertex norm, geometry.cpp:127-131)
   float reserved;
   float aabb[4];  // body-frame bounding box {xmin, xmax, ymin, ymax}
+  // Polygons: <= kMaxCover axis-aligned boxes {cx, cy, hx, hy} whose union contains the
+  // polygon (exact for rectilinear shapes such as the L): an exterior point's signed distance
+  // is at least its distance to that union, a tighter cull bound than the AABB.
+  int ncover;
+  int reserved2;
+  float cover[kMaxCover][4];
   float e[kMaxEdges][8];
 };
 

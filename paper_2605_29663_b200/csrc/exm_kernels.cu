@@ -205,6 +205,7 @@ __device__ __forceinline__ void xy_rate(const double* u, double ct, double st, d
 }
 
 constexpr int kChunk = 4;
+constexpr float kPtsPerCell = 32.0f;
 constexpr int kPartialThreads = 1024;  // 32 warps: 8 rollouts per warp in the U sums
 
 template <int TAG>
@@ -357,6 +358,21 @@ __device__ __forceinline__ bool aabb_may_beat(const FpDev& fp, float bx, float b
   return a2 == 0.f || (lim > 0.f && a2 < lim * lim);
 }
 
+// Polygon cover bound: the union of the kMaxCover cover boxes (unused slots repeat box 0)
+// contains the polygon, so an exterior point's signed distance is at least its distance to the
+// nearest box (0 inside a box: evaluate). Subsumes the AABB bound.
+__device__ __forceinline__ bool cover_may_beat(const FpDev& fp, float bx, float by, float best) {
+  float d2 = __int_as_float(0x7f800000);
+#pragma unroll
+  for (int j = 0; j < kMaxCover; ++j) {
+    const float ax = fmaxf(fabsf(bx - fp.cover[j][0]) - fp.cover[j][2], 0.f);
+    const float ay = fmaxf(fabsf(by - fp.cover[j][1]) - fp.cover[j][3], 0.f);
+    d2 = fminf(d2, fmaf(ax, ax, ay * ay));
+  }
+  const float lim = best + kCullMargin;
+  return d2 == 0.f || (lim > 0.f && d2 < lim * lim);
+}
+
 // Order-preserving float -> u32 key (for min via integer reductions / atomics).
 __device__ __forceinline__ unsigned fkey(float f) {
   const unsigned u = __float_as_uint(f);
@@ -441,7 +457,11 @@ __global__ void __launch_bounds__(1024) k_cloud_prep(const double* __restrict__ 
       g.x0 = g.y0 = 0.0f; g.cs = 1.0f; g.inv_cs = 1.0f; g.gx = g.gy = 1;
     } else {
       const float ex = mxx - mnx, ey = mxy - mny;
-      float cs = fmaxf(cs_target, fmaxf(ex, ey) / static_cast<float>(kGridMax - 1) * 1.001f);
+      // Cell edge: about kPtsPerCell points per cell on average, between R/4 and R/2 (dense
+      // boundary clouds get finer cells, sparse ones coarser), at most kGridMax per axis.
+      const float dens = sqrtf(kPtsPerCell * fmaxf(ex * ey, 1e-6f) / static_cast<float>(cnt));
+      float cs = fminf(fmaxf(dens, 0.5f * cs_target), cs_target);
+      cs = fmaxf(cs, fmaxf(ex, ey) / static_cast<float>(kGridMax - 1) * 1.001f);
       cs = fmaxf(cs, 1e-4f);
       g.x0 = mnx; g.y0 = mny; g.cs = cs; g.inv_cs = 1.0f / cs;
       g.gx = min(kGridMax, static_cast<int>(ex * g.inv_cs) + 1);
@@ -682,7 +702,10 @@ __global__ void __launch_bounds__(128) k_sdf_grid(const __grid_constant__ FpDev 
         if (need && dx * dx + dy * dy < l2) {
           const float bx = fmaf(q.z, dx, q.w * dy);
           const float by = fmaf(q.z, dy, -(q.w * dx));
-          if (aabb_may_beat(fp, bx, by, best)) {
+          // the cover bound pays for itself only when the exact polygon SDF is expensive
+          if ((KIND == EXM_FOOTPRINT_POLYGON && (NB == 0 || NB >= 8))
+                  ? cover_may_beat(fp, bx, by, best)
+                  : aabb_may_beat(fp, bx, by, best)) {
             best = fminf(best, sd_body<KIND, NB>(fp, bx, by));
             const float nl = R + best;
             l2 = nl * nl;
