@@ -249,6 +249,7 @@ def run_ours(args, world, rank, local):
         torch.cuda.synchronize()
         step_ms = [a.elapsed_time(b) for a, b in evs]
     stats = eng.step_stats()  # SDF kernel mean over exactly the timed steps
+    tested, evaluated = eng.cull_stats()  # pairs that reached a point test / the exact SDF
     ms_local = float(np.mean(step_ms))
     ms = allreduce_max(ms_local, world)
     value = 1e3 / ms
@@ -281,6 +282,8 @@ def run_ours(args, world, rank, local):
     peak, peak_src = fp32_peak_tflops(torch.cuda.get_device_properties(local).multi_processor_count)
     sdf_avg_ms = stats["sdf_ms"]
     achieved = pairs * F / (sdf_avg_ms * 1e-3) / 1e12
+    # executed work: 6 ops per point test (2 sub, mul, fma, compare) + F per exact SDF
+    executed_tf = (6.0 * tested + F * evaluated) / (sdf_avg_ms * 1e-3) / 1e12
     prof = ncu_profile(f"sdf_grid_{args.config}")
     line = {
         "metric": "MPPI control steps/sec", "value": value, "unit": "steps/s", "n_gpus": world,
@@ -303,7 +306,11 @@ def run_ours(args, world, rank, local):
         "gpu_launches": stats["launches_per_step"] * args.steps,
         "roofline": {"bound": "fp32", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                      "frac": achieved / peak, "traffic": prof.get("traffic"),
-                     "executed": prof.get("executed"),
+                     "executed": {**(prof.get("executed") or {}),
+                                  "pairs_point_tested": tested, "pairs_exact_sdf": evaluated,
+                                  "culled_fraction": 1.0 - evaluated / pairs,
+                                  "achieved_executed_tflops": executed_tf,
+                                  "frac_executed": executed_tf / peak},
                      "kernel": f"k_sdf_grid<{'POLYGON' if fp.is_polygon() else 'RECT'},{fp.count()}> (per-pose exact SDF min, exact culling)",
                      "sdf_kernel_ms": sdf_avg_ms,
                      "algorithmic": f"K*T*N pairs x {F} ops/pair (SURVEY §8(d), unpruned)",

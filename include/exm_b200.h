@@ -249,6 +249,11 @@ void* exm_stream(exm_handle* h);
 exm_status exm_step_stats(exm_handle* h, int32_t* launches_per_step, float* sdf_ms,
                           int64_t* sdf_pairs);
 
+/* Culling statistics of the last resident step's pose set: re-runs the SDF kernel once with
+ * counters (profiling only; not on the step path): point-pose pairs that reached a point test,
+ * and pairs that reached the exact signed-distance evaluation. */
+exm_status exm_sdf_cull_stats(exm_handle* h, int64_t* points_tested, int64_t* sdf_evaluated);
+
 #ifdef __cplusplus
 }
 #endif

@@ -463,6 +463,13 @@ class Engine:
         check(self.lib.exm_sdf_read(self.h, fptr(pairs), dptr(mins)))
         return mins, pairs
 
+    def cull_stats(self):
+        """(pairs that reached a point test, pairs that reached the exact SDF) for the last
+        resident step's poses (re-runs the SDF once with counters)."""
+        a, b = C.c_int64(), C.c_int64()
+        check(self.lib.exm_sdf_cull_stats(self.h, C.byref(a), C.byref(b)))
+        return a.value, b.value
+
     def stream_ptr(self) -> int:
         return int(self.lib.exm_stream(self.h) or 0)
 

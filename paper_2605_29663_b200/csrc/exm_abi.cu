@@ -1154,6 +1154,26 @@ exm_status exm_read_resident(exm_handle* h, double* nominal_out, double* u_prev_
 
 void* exm_stream(exm_handle* h) { return h ? static_cast<void*>(h->stream) : nullptr; }
 
+exm_status exm_sdf_cull_stats(exm_handle* h, int64_t* points_tested, int64_t* sdf_evaluated) {
+  if (!h) return fail(EXM_ERR_INVALID_ARGUMENT, "handle is null");
+  EXM_CUDA(cudaSetDevice(h->device));
+  unsigned long long* d = nullptr;
+  EXM_CUDA(dalloc(&d, 2));
+  unsigned long long hv[2] = {0, 0};
+  cudaStream_t s = h->stream;
+  cudaError_t e = cudaMemsetAsync(d, 0, 2 * sizeof(unsigned long long), s);
+  if (e == cudaSuccess)
+    e = launch_sdf_grid_stats(h->fp, h->d_poses, h->sc.k_local * h->T, h->d_grid, h->d_cell_start,
+                              h->d_cloud, h->d_dmin, d, s);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(hv, d, sizeof hv, cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  cudaFree(d);
+  if (e != cudaSuccess) return fail(EXM_ERR_CUDA, std::string("cull stats: ") + cudaGetErrorString(e));
+  if (points_tested) *points_tested = static_cast<int64_t>(hv[0]);
+  if (sdf_evaluated) *sdf_evaluated = static_cast<int64_t>(hv[1]);
+  return EXM_OK;
+}
+
 exm_status exm_step_stats(exm_handle* h, int32_t* launches_per_step, float* sdf_ms,
                           int64_t* sdf_pairs) {
   if (!h) return fail(EXM_ERR_INVALID_ARGUMENT, "handle is null");

@@ -92,6 +92,9 @@ cudaError_t launch_rollout(const StepConst& sc, const StepDyn* dyn, const double
 cudaError_t launch_sdf_grid(const FpDev& fp, const float4* poses, int n_poses,
                             const GridMeta* gm, const int* cell_start, const float2* cloud,
                             float* out, cudaStream_t s);
+cudaError_t launch_sdf_grid_stats(const FpDev& fp, const float4* poses, int n_poses,
+                                  const GridMeta* gm, const int* cell_start, const float2* cloud,
+                                  float* out, unsigned long long* stats, cudaStream_t s);
 cudaError_t launch_stage_costs(const StepConst& sc, const StepDyn* dyn, const double* guide,
                                int guide_cap, const double2* xy, const float* dmin,
                                double* stage, uint8_t* flags, cudaStream_t s);

@@ -634,13 +634,17 @@ __device__ __forceinline__ bool box_may_beat(const WBox& w, float bx0, float bx1
 // stops once no lane's lower bound can beat that lane's running minimum. Lower bounds (all
 // exact): ring and cell via the world box W of the footprint, then per point the
 // distance to W and the distance to the body-frame AABB, then the exact polygon/cover SDF.
-template <int KIND, int NB>
+// STATS (profiling builds of the launch only): count the point tests and exact SDF
+// evaluations the culls let through, for the executed-work roofline.
+template <int KIND, int NB, bool STATS = false>
 __global__ void __launch_bounds__(128) k_sdf_grid(const __grid_constant__ FpDev fp,
                                                   const float4* __restrict__ poses, int n_poses,
                                                   const GridMeta* __restrict__ gmp,
                                                   const int* __restrict__ cell_start,
                                                   const float2* __restrict__ cloud,
-                                                  float* __restrict__ out) {
+                                                  float* __restrict__ out,
+                                                  unsigned long long* __restrict__ stats = nullptr) {
+  unsigned long long n_test = 0, n_eval = 0;
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   const bool active = i < n_poses;
   const GridMeta gm = *gmp;
@@ -699,6 +703,7 @@ __global__ void __launch_bounds__(128) k_sdf_grid(const __grid_constant__ FpDev 
       for (int p = 0; p < n; ++p) {
         const float2 o = __ldg(cp + p);
         const float dx = o.x - q.x, dy = o.y - q.y;
+        if (STATS && need) ++n_test;
         if (need && dx * dx + dy * dy < l2) {
           const float bx = fmaf(q.z, dx, q.w * dy);
           const float by = fmaf(q.z, dy, -(q.w * dx));
@@ -706,6 +711,7 @@ __global__ void __launch_bounds__(128) k_sdf_grid(const __grid_constant__ FpDev 
           if ((KIND == EXM_FOOTPRINT_POLYGON && (NB == 0 || NB >= 8))
                   ? cover_may_beat(fp, bx, by, best)
                   : aabb_may_beat(fp, bx, by, best)) {
+            if (STATS) ++n_eval;
             best = fminf(best, sd_body<KIND, NB>(fp, bx, by));
             const float nl = R + best;
             l2 = nl * nl;
@@ -715,6 +721,10 @@ __global__ void __launch_bounds__(128) k_sdf_grid(const __grid_constant__ FpDev 
     }
   }
   if (active) out[i] = best;
+  if (STATS) {
+    atomicAdd(stats, n_test);
+    atomicAdd(stats + 1, n_eval);
+  }
 }
 
 // Warp <-> pose variant for few poses (the T validation poses). Per ring, the lanes first
@@ -1356,6 +1366,19 @@ struct GridLaunch {
 };
 
 template <int KIND, int NB>
+struct GridStatsLaunch {
+  static cudaError_t run(const FpDev& fp, const float4* poses, int n_poses, const GridMeta* gm,
+                         const int* cell_start, const float2* cloud, float* out,
+                         unsigned long long* stats, cudaStream_t s) {
+    if (n_poses <= 0) return cudaSuccess;
+    const int threads = 128;
+    k_sdf_grid<KIND, NB, true><<<(n_poses + threads - 1) / threads, threads, 0, s>>>(
+        fp, poses, n_poses, gm, cell_start, cloud, out, stats);
+    return cudaGetLastError();
+  }
+};
+
+template <int KIND, int NB>
 struct GridWarpLaunch {
   static cudaError_t run(const FpDev& fp, const float4* poses, int n_poses, const GridMeta* gm,
                          const int* cell_start, const float2* cloud, float* out, cudaStream_t s) {
@@ -1439,6 +1462,12 @@ cudaError_t launch_rollout(const StepConst& sc, const StepDyn* dyn, const double
     case EXM_MODEL_PARALLEL: return rollout_tag<EXM_MODEL_PARALLEL>(sc, dyn, nominal, eps, poses, xy, base_cost, controls_out, states_out, s);
   }
   return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_sdf_grid_stats(const FpDev& fp, const float4* poses, int n_poses,
+                                  const GridMeta* gm, const int* cell_start, const float2* cloud,
+                                  float* out, unsigned long long* stats, cudaStream_t s) {
+  return dispatch_fp<GridStatsLaunch>(fp, poses, n_poses, gm, cell_start, cloud, out, stats, s);
 }
 
 cudaError_t launch_stage_costs(const StepConst& sc, const StepDyn* dyn, const double* guide,
