@@ -42,8 +42,20 @@ def ops_per_pair(fp) -> int:
 
 
 def fp32_peak_tflops(sm_count: int = 148) -> tuple[float, str]:
-    """FP32 SIMT peak = 2 flops/FMA x 128 lanes x SMs x max SM clock. MEASURED_PEAKS.json holds
-    only HBM and bf16 peaks, so this is derived from its measured sm_max_mhz (1965 MHz)."""
+    """FP32 SIMT peak. MEASURED_PEAKS.json holds only HBM and bf16 peaks, so the FP32 number is
+    measured on this pool's B200 by tools/fp32_peak.cu (independent packed FFMA2 chains on all
+    SMs; committed as profiles/r01_fp32_peak.json). Fallback: 2 flops/FMA x 128 lanes x SMs x
+    sm_max_mhz of MEASURED_PEAKS.json."""
+    import glob
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_fp32_peak.json")))
+    if files:
+        try:
+            d = json.load(open(files[-1]))
+            return float(d["fp32_ffma2_tflops"]), (
+                f"measured: {os.path.relpath(files[-1], ROOT)} (tools/fp32_peak.cu, FFMA2 chains, "
+                f"{d['sms']} SMs; nominal {d['nominal_tflops_at_max_clock']} at {d['max_clock_mhz']} MHz)")
+        except Exception:
+            pass
     mhz = 1965.0
     src = "derived: 256 ops/SM/clk x %d SMs x sm_max_mhz" % sm_count
     try:
