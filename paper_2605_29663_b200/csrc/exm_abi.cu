@@ -170,7 +170,7 @@ std::vector<std::array<double, 4>> cover_boxes(const std::vector<double>& x,
     for (size_t j = 1; j < boxes.size(); ++j)
       if (area(boxes[j]) > area(boxes[big])) big = j;
     const auto b = boxes[big];
-    double best_gain = 1e-9 * area(b), best_cut = 0.0;
+    double best_gain = 1e-9 * area(b);
     int best_axis = -1;
     std::array<double, 4> best_lo{}, best_hi{};
     for (int axis = 0; axis < 2; ++axis) {
@@ -189,14 +189,12 @@ std::vector<std::array<double, 4>> cover_boxes(const std::vector<double>& x,
         const double gain = area(b) - area(lo) - area(hi);
         if (gain > best_gain) {
           best_gain = gain;
-          best_cut = cut;
           best_axis = axis;
           best_lo = lo;
           best_hi = hi;
         }
       }
     }
-    (void)best_cut;
     if (best_axis < 0) break;
     boxes[big] = best_lo;
     boxes.push_back(best_hi);

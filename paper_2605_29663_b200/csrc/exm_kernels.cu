@@ -204,68 +204,94 @@ __device__ __forceinline__ void xy_rate(const double* u, double ct, double st, d
   if (TAG == EXM_MODEL_PARALLEL) { fx = -u[0] * st; fy = u[0] * ct; }
 }
 
-constexpr int kChunk = 4;
+constexpr int kRolloutWarps = 4;  // rollouts (warps) per CTA in k_rollout
 constexpr float kPtsPerCell = 32.0f;
 constexpr int kPartialThreads = 1024;  // 32 warps: 8 rollouts per warp in the U sums
 
+// Serial part of one rollout (score_rollout, controller.cpp:151-169, minus the SDF and the task
+// cost, which k_stage_costs computes in parallel over (r, h)), spread over one warp:
+//   1. lanes stage u = nominal + eps (coalesced)
+//   2. lane 0 runs the two serial recurrences that really are serial: the sequential clamp
+//      (kinematics.cpp:99-117) and the heading integration — cheap scalar FP64
+//   3. lanes take the FP64 sincos of every pre-step heading (the long-latency part) in parallel
+//   4. lane 0 integrates x, y and the control cost in the reference's step order
+//   5. lanes write poses / positions / controls / states (coalesced)
+// scratch: per-warp shared memory of rollout_warp_scratch(T, D) doubles. Returns the control
+// cost sum + terminal goal cost in lane 0.
+__host__ __device__ constexpr int rollout_warp_scratch(int T, int D) { return T * (D + 5); }
+
 template <int TAG>
-__device__ double rollout_dyn(const StepConst& sc, const StepDyn& dyn, const double* nominal,
-                              const double* eps_row, float4* poses_row, double2* xy_row,
-                              double* controls_row, double* states_row) {
+__device__ double rollout_warp(const StepConst& sc, const StepDyn& dyn, const double* nominal,
+                               const double* eps_row, float4* poses_row, double2* xy_row,
+                               double* controls_row, double* states_row, double* scratch) {
   constexpr int D = model_dim<TAG>();
-  const int T = sc.T;
-  double prev[3] = {dyn.u_prev[0], dyn.u_prev[1], dyn.u_prev[2]};
-  double x = dyn.q0[0], y = dyn.q0[1], th = dyn.q0[2];
-  const double qx0 = dyn.q0[0], qy0 = dyn.q0[1];
-  double base = 0.0;
-  if (states_row) { states_row[0] = x; states_row[1] = y; states_row[2] = th; }
-  for (int h0 = 0; h0 < T; h0 += kChunk) {
-    double uc[kChunk][3], thj[kChunk], thn[kChunk];
+  const int T = sc.T, lane = threadIdx.x & 31;
+  double* s_u = scratch;          // T*D controls (clamped in place)
+  double* s_th = s_u + T * D;     // T pre-step headings
+  double* s_c = s_th + T;         // T cos
+  double* s_s = s_c + T;          // T sin
+  double* s_x = s_s + T;          // T pre-step x
+  double* s_y = s_x + T;          // T pre-step y  (s_x..s_y: 2T; total T*(D+5))
+  for (int i = lane; i < T * D; i += 32) s_u[i] = nominal[i] + (eps_row ? eps_row[i] : 0.0);
+  __syncwarp();
+  double thT = 0.0;
+  if (lane == 0) {
+    double prev[3] = {dyn.u_prev[0], dyn.u_prev[1], dyn.u_prev[2]};
+    double th = dyn.q0[2];
+    for (int h = 0; h < T; ++h) {
+      double u[3] = {0.0, 0.0, 0.0}, uc[3] = {0.0, 0.0, 0.0};
 #pragma unroll
-    for (int j = 0; j < kChunk; ++j) {
-      const int h = h0 + j;
-      if (h < T) {
-        double u[3] = {0.0, 0.0, 0.0};
+      for (int c = 0; c < D; ++c) u[c] = s_u[h * D + c];
+      clamp_control<TAG>(sc, u, prev, uc);
 #pragma unroll
-        for (int c = 0; c < D; ++c) u[c] = nominal[h * D + c] + (eps_row ? eps_row[h * D + c] : 0.0);
-        clamp_control<TAG>(sc, u, prev, uc[j]);
-#pragma unroll
-        for (int c = 0; c < D; ++c) prev[c] = uc[j][c];
-        thj[j] = th;
-        th = th + heading_rate<TAG>(sc, uc[j]) * sc.dt;
-        thn[j] = th;
-      }
+      for (int c = 0; c < D; ++c) prev[c] = s_u[h * D + c] = uc[c];
+      s_th[h] = th;
+      th = th + heading_rate<TAG>(sc, uc) * sc.dt;
     }
-    double st[kChunk], ct[kChunk];
+    thT = th;
+  }
+  __syncwarp();
+  for (int h = lane; h < T; h += 32) sincos(s_th[h], &s_s[h], &s_c[h]);
+  __syncwarp();
+  double base = 0.0;
+  if (lane == 0) {
+    double x = dyn.q0[0], y = dyn.q0[1];
+    for (int h = 0; h < T; ++h) {
+      s_x[h] = x;
+      s_y[h] = y;
+      double uc[3] = {0.0, 0.0, 0.0};
 #pragma unroll
-    for (int j = 0; j < kChunk; ++j)
-      if (h0 + j < T) sincos(thj[j], &st[j], &ct[j]);
-#pragma unroll
-    for (int j = 0; j < kChunk; ++j) {
-      const int h = h0 + j;
-      if (h < T) {
-        if (controls_row) {
-#pragma unroll
-          for (int c = 0; c < D; ++c) controls_row[h * D + c] = uc[j][c];
-        }
-        poses_row[h] = make_float4(static_cast<float>(x - qx0), static_cast<float>(y - qy0),
-                                   static_cast<float>(ct[j]), static_cast<float>(st[j]));
-        xy_row[h] = make_double2(x, y);
-        base += control_cost<TAG>(sc, uc[j]);
-        double fx, fy;
-        xy_rate<TAG>(uc[j], ct[j], st[j], fx, fy);
-        x = x + fx * sc.dt;
-        y = y + fy * sc.dt;
-        if (states_row) {
-          states_row[3 * (h + 1)] = x;
-          states_row[3 * (h + 1) + 1] = y;
-          states_row[3 * (h + 1) + 2] = thn[j];
-        }
-      }
+      for (int c = 0; c < D; ++c) uc[c] = s_u[h * D + c];
+      base += control_cost<TAG>(sc, uc);
+      double fx, fy;
+      xy_rate<TAG>(uc, s_c[h], s_s[h], fx, fy);
+      x = x + fx * sc.dt;
+      y = y + fy * sc.dt;
+    }
+    const double qT[3] = {x, y, thT};
+    base += terminal_cost(sc, qT, dyn.goal);
+    if (states_row) {
+      states_row[3 * T] = x;
+      states_row[3 * T + 1] = y;
+      states_row[3 * T + 2] = thT;
     }
   }
-  const double qT[3] = {x, y, th};
-  return base + terminal_cost(sc, qT, dyn.goal);
+  __syncwarp();
+  const double qx0 = dyn.q0[0], qy0 = dyn.q0[1];
+  for (int h = lane; h < T; h += 32) {
+    poses_row[h] = make_float4(static_cast<float>(s_x[h] - qx0), static_cast<float>(s_y[h] - qy0),
+                               static_cast<float>(s_c[h]), static_cast<float>(s_s[h]));
+    xy_row[h] = make_double2(s_x[h], s_y[h]);
+    if (states_row) {
+      states_row[3 * h] = s_x[h];
+      states_row[3 * h + 1] = s_y[h];
+      states_row[3 * h + 2] = s_th[h];
+    }
+  }
+  if (controls_row)
+    for (int i = lane; i < T * D; i += 32) controls_row[i] = s_u[i];
+  __syncwarp();
+  return base;
 }
 
 // Running cost of one pre-step state: task_cost (controller.cpp:103-118, non-terminal) +
@@ -531,43 +557,29 @@ __global__ void __launch_bounds__(1024) k_cloud_prep(const double* __restrict__ 
 }
 
 template <int TAG>
-__global__ void k_rollout(const StepConst sc, const StepDyn* __restrict__ dynp,
-                          const double* __restrict__ nominal, const double* __restrict__ eps,
-                          float4* __restrict__ poses, double2* __restrict__ xy,
-                          double* __restrict__ base_cost, double* __restrict__ controls_out,
-                          double* __restrict__ states_out) {
-  // One warp per CTA: only K threads exist, so spread them over SMs. The CTA's perturbation
-  // rows (one contiguous block) are staged into shared memory by a single TMA bulk copy, so
-  // the sequential h-loop never waits on global memory.
-  extern __shared__ __align__(16) double sm[];
-  __shared__ __align__(8) uint64_t bar;
+__global__ void __launch_bounds__(kRolloutWarps * 32) k_rollout(
+    const StepConst sc, const StepDyn* __restrict__ dynp, const double* __restrict__ nominal,
+    const double* __restrict__ eps, float4* __restrict__ poses, double2* __restrict__ xy,
+    double* __restrict__ base_cost, double* __restrict__ controls_out,
+    double* __restrict__ states_out) {
+  // One warp per rollout (rollout_warp): the serial recurrences stay on one lane, the FP64
+  // transcendentals and all memory traffic are spread over the warp.
+  extern __shared__ double sm[];
   const int TD = sc.T * sc.D;
   double* nom = sm;
-  double* e_s = sm + ((TD + 1) & ~1);  // 16-byte aligned
-  const int r0 = blockIdx.x * blockDim.x;
-  const int nr = min(static_cast<int>(blockDim.x), sc.k_local - r0);
-  const double* src = eps + static_cast<size_t>(r0) * TD;
-  const unsigned bytes = static_cast<unsigned>(nr) * TD * sizeof(double);
-  const unsigned bulk = bytes & ~15u;
-  if (threadIdx.x == 0) {
-    mbar_init(&bar, 1);
-    if (bulk) {
-      mbar_expect_tx(&bar, bulk);
-      tma_bulk_g2s(e_s, src, bulk, &bar);
-    }
-    if (bytes != bulk) e_s[bulk / sizeof(double)] = src[bulk / sizeof(double)];
-  }
+  const int warp = threadIdx.x >> 5;
+  double* scratch = sm + TD + warp * rollout_warp_scratch(sc.T, sc.D);
   for (int i = threadIdx.x; i < TD; i += blockDim.x) nom[i] = nominal[i];
-  __syncthreads();
-  if (bulk) mbar_wait(&bar, 0);
   const StepDyn dyn = *dynp;
   __syncthreads();
-  const int r = r0 + threadIdx.x;
-  if (r >= sc.k_local) return;
+  const int r = blockIdx.x * kRolloutWarps + warp;
+  if (r >= sc.k_local) return;  // warp-uniform
   const size_t row = static_cast<size_t>(r) * sc.T;
-  base_cost[r] = rollout_dyn<TAG>(sc, dyn, nom, e_s + threadIdx.x * TD, poses + row, xy + row,
-                             controls_out ? controls_out + row * sc.D : nullptr,
-                             states_out ? states_out + static_cast<size_t>(r) * (sc.T + 1) * 3 : nullptr);
+  const double b = rollout_warp<TAG>(sc, dyn, nom, eps + row * sc.D, poses + row, xy + row,
+                                     controls_out ? controls_out + row * sc.D : nullptr,
+                                     states_out ? states_out + static_cast<size_t>(r) * (sc.T + 1) * 3 : nullptr,
+                                     scratch);
+  if ((threadIdx.x & 31) == 0) base_cost[r] = b;
 }
 
 // Task + obstacle cost and the unsafe flag of every (r, h), in parallel. Thread i = h*K + r
@@ -976,14 +988,14 @@ __global__ void __launch_bounds__(256) k_update(const StepConst sc,
     for (int o = tid; o < TD; o += blockDim.x) s_upd[o] = nominal[o];
   }
   __syncthreads();
-  if (tid == 0) {
-    // rollout_dyn clamps sequentially from u_prev and writes the clamped sequence back; the
+  if (tid < 32) {
+    // warp 0 clamps sequentially from u_prev and writes the clamped sequence back; the
     // reference's second clamp inside validate_nominal is idempotent on it.
     const StepDyn dyn = *dynp;
-    *val_base = rollout_dyn<TAG>(sc, dyn, s_upd, nullptr, val_poses, val_xy, s_upd, nullptr);
+    const double b = rollout_warp<TAG>(sc, dyn, s_upd, nullptr, val_poses, val_xy, upd, nullptr,
+                                       sf + (merge ? nb : 0));
+    if (tid == 0) *val_base = b;
   }
-  __syncthreads();
-  for (int o = tid; o < TD; o += blockDim.x) upd[o] = s_upd[o];
 }
 
 // Validation cost, validity, command and shift / zero-hold (controller.cpp:339-364).
@@ -1119,11 +1131,13 @@ __device__ __forceinline__ u64 pk(float a, float b) {
 __device__ __forceinline__ float lo(u64 v) {
   float a, b;
   asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(v));
+  (void)b;
   return a;
 }
 __device__ __forceinline__ float hi(u64 v) {
   float a, b;
   asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(v));
+  (void)a;
   return b;
 }
 __device__ __forceinline__ u64 bc(float x) { return pk(x, x); }
@@ -1439,14 +1453,15 @@ template <int TAG>
 cudaError_t rollout_tag(const StepConst& sc, const StepDyn* dyn, const double* nominal,
                         const double* eps, float4* poses, double2* xy, double* base_cost,
                         double* controls_out, double* states_out, cudaStream_t s) {
-  const int threads = 32;  // K threads only: one warp per CTA spreads them over all SMs
-  const size_t smem = sizeof(double) * (static_cast<size_t>(sc.T) * sc.D * (threads + 1) + 2);
+  const int threads = kRolloutWarps * 32;
+  const size_t smem = sizeof(double) * (static_cast<size_t>(sc.T) * sc.D +
+                                        kRolloutWarps * static_cast<size_t>(rollout_warp_scratch(sc.T, sc.D)));
   if (smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(k_rollout<TAG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(smem));
     if (e != cudaSuccess) return e;
   }
-  k_rollout<TAG><<<(sc.k_local + threads - 1) / threads, threads, smem, s>>>(
+  k_rollout<TAG><<<(sc.k_local + kRolloutWarps - 1) / kRolloutWarps, threads, smem, s>>>(
       sc, dyn, nominal, eps, poses, xy, base_cost, controls_out, states_out);
   return cudaGetLastError();
 }
@@ -1516,7 +1531,8 @@ cudaError_t update_tag(const StepConst& sc, const double* partials, const double
                        const StepDyn* dyn, double* upd, float4* val_poses, double2* val_xy,
                        double* val_base, DecisionDev* dec, int merge, cudaStream_t s) {
   const size_t smem = sizeof(double) * (static_cast<size_t>(sc.T) * sc.D +
-                                        static_cast<size_t>(merge ? sc.nblocks_total : 1));
+                                        static_cast<size_t>(merge ? sc.nblocks_total : 0) +
+                                        rollout_warp_scratch(sc.T, sc.D));
   if (smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(k_update<TAG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(smem));
