@@ -89,6 +89,29 @@ cudaError_t halloc(T** p, size_t count) {
   return cudaMallocHost(reinterpret_cast<void**>(p), count * sizeof(T));
 }
 
+// One device block for the cloud structure of a handle (CloudGrid views, 16-byte aligned).
+cudaError_t alloc_cloud_grid(int n_cap, void** block, CloudGrid* g) {
+  const size_t n = static_cast<size_t>(n_cap > 0 ? n_cap : 1), cap = cloud_capacity(n_cap);
+  const size_t cells = static_cast<size_t>(kGridMax) * kGridMax + 1;
+  auto up = [](size_t b) { return (b + 15) & ~static_cast<size_t>(15); };
+  const size_t o_raw = up(n * sizeof(float2)), o_cloud = o_raw + up(n * sizeof(float2));
+  const size_t o_chunk = o_cloud + up(cap * sizeof(float2));
+  const size_t o_rs = o_chunk + up((cap / kChunk + 1) * sizeof(float4));
+  const size_t o_cs = o_rs + up(cells * sizeof(int)), o_gm = o_cs + up(cells * sizeof(int));
+  char* d = nullptr;
+  cudaError_t e = cudaMalloc(reinterpret_cast<void**>(&d), o_gm + sizeof(GridMeta));
+  if (e != cudaSuccess) return e;
+  *block = d;
+  g->tmp = reinterpret_cast<float2*>(d);
+  g->raw = reinterpret_cast<float2*>(d + o_raw);
+  g->cloud = reinterpret_cast<float2*>(d + o_cloud);
+  g->chunk = reinterpret_cast<float4*>(d + o_chunk);
+  g->raw_start = reinterpret_cast<int*>(d + o_rs);
+  g->cell_start = reinterpret_cast<int*>(d + o_cs);
+  g->gm = reinterpret_cast<GridMeta*>(d + o_gm);
+  return cudaSuccess;
+}
+
 int model_dim(int tag) {  // kinematics.cpp:14-26
   switch (tag) {
     case EXM_MODEL_DIFF:
@@ -293,6 +316,25 @@ exm_status build_footprint(const exm_footprint* fp, FpDev* out) {
   out->aabb[1] = static_cast<float>(bx1 + m);
   out->aabb[2] = static_cast<float>(by0 - m);
   out->aabb[3] = static_cast<float>(by1 + m);
+  if (out->kind == EXM_FOOTPRINT_RECT_COVER) {
+    // the cover union is the footprint itself when it has <= kMaxCover boxes, else the AABB
+    const bool own = out->count <= kMaxCover;
+    out->ncover = own ? out->count : 1;
+    for (int j = 0; j < kMaxCover; ++j) {  // unused slots repeat box 0 (the kernel unrolls)
+      const float* e = out->e[own && j < out->count ? j : 0];
+      if (own) {
+        out->cover[j][0] = e[0];
+        out->cover[j][1] = e[1];
+        out->cover[j][2] = static_cast<float>(e[2] + m);
+        out->cover[j][3] = static_cast<float>(e[3] + m);
+      } else {
+        out->cover[j][0] = 0.5f * (out->aabb[0] + out->aabb[1]);
+        out->cover[j][1] = 0.5f * (out->aabb[2] + out->aabb[3]);
+        out->cover[j][2] = 0.5f * (out->aabb[1] - out->aabb[0]);
+        out->cover[j][3] = 0.5f * (out->aabb[3] - out->aabb[2]);
+      }
+    }
+  }
   if (out->kind == EXM_FOOTPRINT_POLYGON) {
     std::vector<double> px(out->count), py(out->count);
     for (int i = 0; i < out->count; ++i) {
@@ -348,10 +390,8 @@ struct exm_handle {
   double* d_guide = nullptr;
   double* d_pts = nullptr;
   uint8_t* d_mask = nullptr;
-  float2* d_tmp = nullptr;
-  float2* d_cloud = nullptr;
-  int* d_cell_start = nullptr;
-  GridMeta* d_grid = nullptr;
+  CloudGrid grid;                 // per-step cloud structure (views into d_grid_block)
+  void* d_grid_block = nullptr;
   double* d_eps = nullptr;
   float4* d_poses = nullptr;
   double2* d_xy = nullptr;
@@ -439,14 +479,13 @@ void destroy_graphs(exm_handle* h) {
 }
 
 // Phases of one control step (all stream-ordered, capturable):
-//   prep  : cloud preparation (mask, recentre, grid)                 -> d_cloud, d_grid
+//   prep  : cloud preparation (mask, recentre, grid, in-cell sort, chunk boxes) -> grid
 //   pre   : [noise] -> rollout                                       -> d_poses, d_xy, d_base
 //   sdf   : per-pose exact SDF over the step's K*T poses             -> d_dmin
 //   post  : stage costs -> block partials -> [all-gather] -> merge/update/validation
 //           dynamics -> validation SDF -> finalize                    -> d_out, state
 exm_status enqueue_prep(exm_handle* h, cudaStream_t s) {
-  EXM_CUDA(launch_cloud_prep(h->d_pts, h->d_mask, h->d_dyn, h->fp.radius, h->d_tmp, h->d_cloud,
-                             h->d_cell_start, h->d_grid, s));
+  EXM_CUDA(launch_cloud_prep(h->d_pts, h->d_mask, h->d_dyn, h->fp.radius, h->grid, s));
   return EXM_OK;
 }
 
@@ -478,7 +517,7 @@ exm_status enqueue_post(exm_handle* h, cudaStream_t s, int* launches) {
   }
   EXM_CUDA(launch_update(sc, h->d_partials, h->d_nominal, h->d_dyn, h->d_upd, h->d_val_poses,
                          h->d_val_xy, h->d_val_base, out_dec(h), 1, s));
-  EXM_CUDA(launch_sdf_grid(h->fp, h->d_val_poses, sc.T, h->d_grid, h->d_cell_start, h->d_cloud,
+  EXM_CUDA(launch_sdf_grid(h->fp, h->d_val_poses, sc.T, h->grid,
                            h->d_val_dmin, s));
   EXM_CUDA(launch_finalize(sc, h->d_val_dmin, h->d_val_xy, h->d_val_base, h->d_upd, h->d_guide,
                            h->guide_cap, h->d_nominal, h->d_dyn, out_dec(h), out_dmin(h),
@@ -508,8 +547,7 @@ exm_status enqueue_step(exm_handle* h, bool draw_noise, const EventPair* ev, cud
   if ((st = enqueue_pre(h, draw_noise, s, &launches)) != EXM_OK) return st;
   EXM_CUDA(cudaStreamWaitEvent(s, h->join_ev, 0));
   if (ev && (st = record_ev(ev->a, s, capturing)) != EXM_OK) return st;
-  EXM_CUDA(launch_sdf_grid(h->fp, h->d_poses, sc.k_local * sc.T, h->d_grid, h->d_cell_start,
-                           h->d_cloud, h->d_dmin, s));
+  EXM_CUDA(launch_sdf_grid(h->fp, h->d_poses, sc.k_local * sc.T, h->grid, h->d_dmin, s));
   ++launches;
   if (ev && (st = record_ev(ev->b, s, capturing)) != EXM_OK) return st;
   if ((st = enqueue_post(h, s, &launches)) != EXM_OK) return st;
@@ -791,10 +829,7 @@ exm_status exm_create(const exm_footprint* footprint, const exm_model* model,
     h->h_pts = reinterpret_cast<double*>(hh + o_pts);
     h->h_mask = hh + o_mask;
   }
-  EXM_CUDA_C(dalloc(&h->d_tmp, static_cast<size_t>(n_cap)));
-  EXM_CUDA_C(dalloc(&h->d_cloud, static_cast<size_t>(n_cap)));
-  EXM_CUDA_C(dalloc(&h->d_cell_start, static_cast<size_t>(kGridMax) * kGridMax + 1));
-  EXM_CUDA_C(dalloc(&h->d_grid, 1));
+  EXM_CUDA_C(alloc_cloud_grid(n_cap, &h->d_grid_block, &h->grid));
   EXM_CUDA_C(dalloc(&h->d_eps, KT * D));
   EXM_CUDA_C(dalloc(&h->d_poses, KT));
   EXM_CUDA_C(dalloc(&h->d_xy, KT));
@@ -829,9 +864,7 @@ void exm_destroy(exm_handle* h) {
   destroy_graphs(h);
   if (h->comm && g_nccl.destroy) g_nccl.destroy(h->comm);
   if (h->borrowed_poses) h->d_poses = nullptr, h->d_dmin = nullptr;
-  if (h->borrowed_cloud) h->d_cloud = nullptr, h->d_cell_start = nullptr, h->d_grid = nullptr;
-  void* dev[] = {h->d_in_block, h->d_tmp, h->d_cloud,
-                 h->d_cell_start, h->d_grid, h->d_eps, h->d_poses, h->d_xy, h->d_stage,
+  void* dev[] = {h->d_in_block, h->d_grid_block, h->d_eps, h->d_poses, h->d_xy, h->d_stage,
                  h->d_flags, h->d_val_xy, h->d_base, h->d_dmin,
                  h->d_partials, h->d_upd, h->d_val_poses, h->d_val_base, h->d_val_dmin, h->d_out,
                  h->d_controls, h->d_states, h->d_cost, h->d_unsafe, h->sb_poses, h->sb_pts64,
@@ -905,13 +938,11 @@ exm_status exm_evaluate_rollouts(exm_handle* h, const double q0[3], const double
   if (!h->d_unsafe) EXM_CUDA(dalloc(&h->d_unsafe, static_cast<size_t>(h->K)));
   cudaStream_t s = h->stream;
   const StepConst& sc = h->sc;
-  EXM_CUDA(launch_cloud_prep(h->d_pts, h->d_mask, h->d_dyn, h->fp.radius, h->d_tmp, h->d_cloud,
-                             h->d_cell_start, h->d_grid, s));
+  EXM_CUDA(launch_cloud_prep(h->d_pts, h->d_mask, h->d_dyn, h->fp.radius, h->grid, s));
   EXM_CUDA(launch_rollout(sc, h->d_dyn, h->d_nominal, h->d_eps, h->d_poses, h->d_xy, h->d_base,
                           controls_out ? h->d_controls : nullptr,
                           states_out ? h->d_states : nullptr, s));
-  EXM_CUDA(launch_sdf_grid(h->fp, h->d_poses, static_cast<int>(KT), h->d_grid, h->d_cell_start,
-                           h->d_cloud, h->d_dmin, s));
+  EXM_CUDA(launch_sdf_grid(h->fp, h->d_poses, static_cast<int>(KT), h->grid, h->d_dmin, s));
   EXM_CUDA(launch_stage_costs(sc, h->d_dyn, h->d_guide, h->guide_cap, h->d_xy, h->d_dmin,
                               h->d_stage, h->d_flags, s));
   EXM_CUDA(launch_block_partials(sc, h->d_base, h->d_stage, h->d_flags, h->d_eps, nullptr,
@@ -963,11 +994,10 @@ exm_status exm_validate_nominal(exm_handle* h, const double* nominal, const doub
   if (st != EXM_OK) return st;
   cudaStream_t s = h->stream;
   const StepConst& sc = h->sc;
-  EXM_CUDA(launch_cloud_prep(h->d_pts, h->d_mask, h->d_dyn, h->fp.radius, h->d_tmp, h->d_cloud,
-                             h->d_cell_start, h->d_grid, s));
+  EXM_CUDA(launch_cloud_prep(h->d_pts, h->d_mask, h->d_dyn, h->fp.radius, h->grid, s));
   EXM_CUDA(launch_update(sc, nullptr, h->d_nominal, h->d_dyn, h->d_upd, h->d_val_poses,
                          h->d_val_xy, h->d_val_base, out_dec(h), 0, s));
-  EXM_CUDA(launch_sdf_grid(h->fp, h->d_val_poses, sc.T, h->d_grid, h->d_cell_start, h->d_cloud,
+  EXM_CUDA(launch_sdf_grid(h->fp, h->d_val_poses, sc.T, h->grid,
                            h->d_val_dmin, s));
   EXM_CUDA(launch_finalize(sc, h->d_val_dmin, h->d_val_xy, h->d_val_base, h->d_upd, h->d_guide,
                            h->guide_cap, h->d_nominal, h->d_dyn, out_dec(h), out_dmin(h), nullptr,
@@ -1161,8 +1191,7 @@ exm_status exm_sdf_cull_stats(exm_handle* h, int64_t* points_tested, int64_t* sd
   cudaStream_t s = h->stream;
   cudaError_t e = cudaMemsetAsync(d, 0, 2 * sizeof(unsigned long long), s);
   if (e == cudaSuccess)
-    e = launch_sdf_grid_stats(h->fp, h->d_poses, h->sc.k_local * h->T, h->d_grid, h->d_cell_start,
-                              h->d_cloud, h->d_dmin, d, s);
+    e = launch_sdf_grid_stats(h->fp, h->d_poses, h->sc.k_local * h->T, h->grid, h->d_dmin, d, s);
   if (e == cudaSuccess) e = cudaMemcpyAsync(hv, d, sizeof hv, cudaMemcpyDeviceToHost, s);
   if (e == cudaSuccess) e = cudaStreamSynchronize(s);
   cudaFree(d);
@@ -1231,8 +1260,8 @@ exm_status hybrid_enqueue(exm_hybrid* hy, cudaStream_t s0) {
   }
   for (int m = 1; m < hy->M; ++m) EXM_CUDA(cudaStreamWaitEvent(s0, hy->pre_done[m], 0));
   EXM_CUDA(cudaStreamWaitEvent(s0, hy->prep_done, 0));
-  EXM_CUDA(launch_sdf_grid(f0->fp, hy->poses_all, hy->M * hy->K * hy->T, f0->d_grid,
-                           f0->d_cell_start, f0->d_cloud, hy->dmin_all, s0));
+  EXM_CUDA(launch_sdf_grid(f0->fp, hy->poses_all, hy->M * hy->K * hy->T, f0->grid, hy->dmin_all,
+                           s0));
   EXM_CUDA(cudaEventRecord(hy->sdf_done, s0));
   for (int m = 0; m < hy->M; ++m) {
     cudaStream_t sm = m == 0 ? s0 : hy->fam[m]->stream;
@@ -1308,12 +1337,9 @@ exm_status exm_hybrid_create(const exm_footprint* footprint, const exm_model* mo
     h->d_dmin = hy->dmin_all + m * KT;
     h->borrowed_poses = true;
     if (m > 0) {
-      cudaFree(h->d_cloud);
-      cudaFree(h->d_cell_start);
-      cudaFree(h->d_grid);
-      h->d_cloud = f0->d_cloud;
-      h->d_cell_start = f0->d_cell_start;
-      h->d_grid = f0->d_grid;
+      cudaFree(h->d_grid_block);
+      h->d_grid_block = nullptr;
+      h->grid = f0->grid;
       h->borrowed_cloud = true;
     }
   }

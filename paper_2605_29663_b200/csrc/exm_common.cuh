@@ -14,6 +14,8 @@ constexpr int kBlockRollouts = 256;  // rollouts per softmax partial (fixed: G-i
 constexpr int kGridMax = 128;        // cloud grid cells per axis (<= 16384 cells, smem histogram)
 constexpr float kEmptyDistance = 1e6f;  // kEmptyMaskDistance (geometry.hpp:37)
 constexpr float kCullMargin = 1e-3f;    // conservative slack on every lower-bound cull (m)
+constexpr int kChunk = 8;               // cloud points per chunk (one bounding box each)
+constexpr int kSubCells = 16;           // per-axis sub-cells of the in-cell Morton order
 
 // FP32 footprint table, passed by value as a __grid_constant__ kernel parameter so the
 // inner loops read it from the constant bank (uniform datapath), never from memory.
@@ -26,9 +28,10 @@ struct FpDev {
   float radius;  // PreparedFootprint::bounding_radius (max vertex norm, geometry.cpp:127-131)
   float reserved;
   float aabb[4];  // body-frame bounding box {xmin, xmax, ymin, ymax}
-  // Polygons: <= kMaxCover axis-aligned boxes {cx, cy, hx, hy} whose union contains the
-  // polygon (exact for rectilinear shapes such as the L): an exterior point's signed distance
-  // is at least its distance to that union, a tighter cull bound than the AABB.
+  // <= kMaxCover axis-aligned boxes {cx, cy, hx, hy} whose union contains the footprint
+  // (polygons: exact for rectilinear shapes such as the L; rectangle covers of <= kMaxCover
+  // boxes: the boxes themselves; otherwise the AABB): an exterior point's signed distance is
+  // at least its distance to that union, a tighter cull bound than the AABB.
   int ncover;
   int reserved2;
   float cover[kMaxCover][4];
@@ -40,6 +43,25 @@ struct GridMeta {
   float x0, y0, cs, inv_cs;
   int gx, gy, n_valid, reserved;
 };
+
+// Device cloud structure of one control step (HBM, rebuilt every cycle by launch_cloud_prep):
+//   cloud[cell_start[c] .. cell_start[c+1])  cell c's points, Morton-ordered on a kSubCells^2
+//       sub-grid, padded with NaN to a multiple of kChunk (NaN never passes a distance test)
+//   chunk[i]  bounding box {cx, cy, hx, hy} of cloud[kChunk*i .. kChunk*i + kChunk)
+// tmp / raw / raw_start are the prep kernels' scratch (compacted points, cell-sorted points).
+struct CloudGrid {
+  float2* tmp = nullptr;
+  float2* raw = nullptr;
+  int* raw_start = nullptr;
+  float2* cloud = nullptr;
+  float4* chunk = nullptr;
+  int* cell_start = nullptr;
+  GridMeta* gm = nullptr;
+};
+// Padded cloud capacity for n_cap points: every nonempty cell adds at most kChunk - 1 pads.
+inline size_t cloud_capacity(int n_cap) {
+  return static_cast<size_t>(n_cap) + static_cast<size_t>(kChunk - 1) * kGridMax * kGridMax + kChunk;
+}
 
 // Per-step small inputs, uploaded with one copy (host API) or kept resident.
 struct StepDyn {
@@ -84,17 +106,15 @@ inline __host__ __device__ int partial_stride(int T, int D) { return 4 + T * D; 
 // ---- kernel launchers (exm_kernels.cu) ---------------------------------------------------
 cudaError_t launch_noise(const StepConst& sc, const StepDyn* dyn, double* eps, cudaStream_t s);
 cudaError_t launch_cloud_prep(const double* pts, const uint8_t* mask, const StepDyn* dyn,
-                              float radius, float2* tmp, float2* cloud, int* cell_start,
-                              GridMeta* gm, cudaStream_t s);
+                              float radius, const CloudGrid& g, cudaStream_t s);
 cudaError_t launch_rollout(const StepConst& sc, const StepDyn* dyn, const double* nominal,
                            const double* eps, float4* poses, double2* xy, double* base_cost,
                            double* controls_out, double* states_out, cudaStream_t s);
 cudaError_t launch_sdf_grid(const FpDev& fp, const float4* poses, int n_poses,
-                            const GridMeta* gm, const int* cell_start, const float2* cloud,
-                            float* out, cudaStream_t s);
+                            const CloudGrid& g, float* out, cudaStream_t s);
 cudaError_t launch_sdf_grid_stats(const FpDev& fp, const float4* poses, int n_poses,
-                                  const GridMeta* gm, const int* cell_start, const float2* cloud,
-                                  float* out, unsigned long long* stats, cudaStream_t s);
+                                  const CloudGrid& g, float* out, unsigned long long* stats,
+                                  cudaStream_t s);
 cudaError_t launch_stage_costs(const StepConst& sc, const StepDyn* dyn, const double* guide,
                                int guide_cap, const double2* xy, const float* dmin,
                                double* stage, uint8_t* flags, cudaStream_t s);

@@ -181,10 +181,9 @@ __device__ __forceinline__ double obstacle_cost(const StepConst& sc, double d) {
 // control cost summed over h plus the terminal goal cost. The per-step task cost is
 // independent across (r, h) and is computed in parallel by k_stage_costs.
 //
-// In all five models the heading rate depends on u only (kinematics.cpp:75-92), so the long
-// FP64 sincos latency is taken off the serial chain: per chunk of kChunk steps the clamp and
-// heading recurrences run first, then the kChunk independent sincos, then the x/y updates —
-// the same operations on the same values as the reference's step-by-step order.
+// In all five models the heading rate depends on u only (kinematics.cpp:75-92), so the FP64
+// sincos of every heading can be taken off the serial chain (rollout_warp below) — the same
+// operations on the same values as the reference's step-by-step order.
 template <int TAG>
 __device__ __forceinline__ double heading_rate(const StepConst& sc, const double* u) {
   if (TAG == EXM_MODEL_DIFF) return u[1];
@@ -399,6 +398,26 @@ __device__ __forceinline__ bool cover_may_beat(const FpDev& fp, float bx, float 
   return d2 == 0.f || (lim > 0.f && d2 < lim * lim);
 }
 
+// Chunk bound: the chunk's points lie in the world box {cx +- hx, cy +- hy}; in the body frame
+// of pose q that box lies inside the box centred at R(theta)^T (c - t) with half extents
+// (|cos| hx + |sin| hy, |sin| hx + |cos| hy). No point of the chunk is nearer to the footprint
+// than that box is to the cover union (0 if they overlap: evaluate).
+__device__ __forceinline__ bool chunk_may_beat(const FpDev& fp, float4 q, float4 b, float best) {
+  const float dx = b.x - q.x, dy = b.y - q.y;
+  const float bx = fmaf(q.z, dx, q.w * dy), by = fmaf(q.z, dy, -(q.w * dx));
+  const float ac = fabsf(q.z), as = fabsf(q.w);
+  const float ex = fmaf(ac, b.z, as * b.w), ey = fmaf(as, b.z, ac * b.w);
+  float d2 = __int_as_float(0x7f800000);
+#pragma unroll
+  for (int j = 0; j < kMaxCover; ++j) {
+    const float ax = fmaxf(fabsf(bx - fp.cover[j][0]) - (fp.cover[j][2] + ex), 0.f);
+    const float ay = fmaxf(fabsf(by - fp.cover[j][1]) - (fp.cover[j][3] + ey), 0.f);
+    d2 = fminf(d2, fmaf(ax, ax, ay * ay));
+  }
+  const float lim = best + kCullMargin;
+  return d2 == 0.f || (lim > 0.f && d2 < lim * lim);
+}
+
 // Order-preserving float -> u32 key (for min via integer reductions / atomics).
 __device__ __forceinline__ unsigned fkey(float f) {
   const unsigned u = __float_as_uint(f);
@@ -432,13 +451,14 @@ __global__ void __launch_bounds__(1024) k_cloud_prep(const double* __restrict__ 
                                                      const uint8_t* __restrict__ mask,
                                                      const StepDyn* __restrict__ dyn,
                                                      float cs_target, float2* __restrict__ tmp,
-                                                     float2* __restrict__ cloud,
+                                                     float2* __restrict__ raw,
+                                                     int* __restrict__ raw_start,
                                                      int* __restrict__ cell_start,
                                                      GridMeta* __restrict__ gm_out) {
   extern __shared__ int hist[];  // kGridMax * kGridMax
   __shared__ float red[4][32];
   __shared__ int redc[32];
-  __shared__ int scan_tot[32];
+  __shared__ long long scan_tot[32];
   __shared__ GridMeta gm;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int n = dyn->n_points;
@@ -511,37 +531,45 @@ __global__ void __launch_bounds__(1024) k_cloud_prep(const double* __restrict__ 
     }
   }
   __syncthreads();
-  // exclusive scan: each thread owns a contiguous segment
+  // Exclusive scans of the cell counts (raw_start) and of the counts padded to whole chunks
+  // (cell_start), as one 64-bit scan {padded:raw}; each thread owns a contiguous segment.
   const int seg = (cells + blockDim.x - 1) / blockDim.x;
   const int c0 = min(cells, tid * seg), c1 = min(cells, c0 + seg);
-  int local = 0;
-  for (int c = c0; c < c1; ++c) local += hist[c];
-  int incl = local;
+  auto both = [](int h) {
+    return (static_cast<long long>((h + kChunk - 1) & ~(kChunk - 1)) << 32) | static_cast<long long>(h);
+  };
+  long long local = 0;
+  for (int c = c0; c < c1; ++c) local += both(hist[c]);
+  long long incl = local;
   for (int o = 1; o < 32; o <<= 1) {
-    const int v = __shfl_up_sync(kFull, incl, o);
+    const long long v = __shfl_up_sync(kFull, incl, o);
     if (lane >= o) incl += v;
   }
   if (lane == 31) scan_tot[warp] = incl;
   __syncthreads();
   if (warp == 0) {
     const int nw = blockDim.x >> 5;
-    int v = lane < nw ? scan_tot[lane] : 0;
-    int s = v;
+    const long long v = lane < nw ? scan_tot[lane] : 0;
+    long long sc = v;
     for (int o = 1; o < 32; o <<= 1) {
-      const int u = __shfl_up_sync(kFull, s, o);
-      if (lane >= o) s += u;
+      const long long u = __shfl_up_sync(kFull, sc, o);
+      if (lane >= o) sc += u;
     }
-    if (lane < nw) scan_tot[lane] = s - v;  // exclusive warp offsets
+    if (lane < nw) scan_tot[lane] = sc - v;  // exclusive warp offsets
   }
   __syncthreads();
-  int run = scan_tot[warp] + incl - local;
+  long long run = scan_tot[warp] + incl - local;
   for (int c = c0; c < c1; ++c) {
     const int h = hist[c];
-    cell_start[c] = run;
-    hist[c] = run;  // becomes the scatter cursor
-    run += h;
+    raw_start[c] = static_cast<int>(run & 0xffffffffll);
+    cell_start[c] = static_cast<int>(run >> 32);
+    hist[c] = static_cast<int>(run & 0xffffffffll);  // becomes the scatter cursor
+    run += both(h);
   }
-  if (tid == 0) cell_start[cells] = gm.n_valid;
+  if (c0 < c1 && c1 == cells) {
+    raw_start[cells] = static_cast<int>(run & 0xffffffffll);
+    cell_start[cells] = static_cast<int>(run >> 32);
+  }
   __syncthreads();
   if (gm.n_valid > 0) {
     for (int i = tid; i < n; i += blockDim.x) {
@@ -550,9 +578,86 @@ __global__ void __launch_bounds__(1024) k_cloud_prep(const double* __restrict__ 
         const int ix = min(gm.gx - 1, max(0, static_cast<int>((p.x - gm.x0) * gm.inv_cs)));
         const int iy = min(gm.gy - 1, max(0, static_cast<int>((p.y - gm.y0) * gm.inv_cs)));
         const int slot = atomicAdd(&hist[iy * gm.gx + ix], 1);
-        cloud[slot] = p;
+        raw[slot] = p;
       }
     }
+  }
+}
+
+// Morton index of a point on the kSubCells x kSubCells sub-grid of its cell.
+__device__ __forceinline__ int sub_key(float2 p, float ox, float oy, float sub) {
+  const int sx = min(kSubCells - 1, max(0, static_cast<int>((p.x - ox) * sub)));
+  const int sy = min(kSubCells - 1, max(0, static_cast<int>((p.y - oy) * sub)));
+  auto spread = [](int v) {
+    v = (v | (v << 2)) & 0x33;
+    return (v | (v << 1)) & 0x55;
+  };
+  return spread(sx) | (spread(sy) << 1);
+}
+
+// Second prep pass, one warp per nonempty cell: counting sort of the cell's points by their
+// sub-grid Morton index (so every kChunk consecutive points are close together), NaN pads up
+// to a whole chunk, and the chunk bounding boxes.
+constexpr int kSortWarps = 8;
+__global__ void __launch_bounds__(kSortWarps * 32) k_cell_sort(
+    const float2* __restrict__ raw, const int* __restrict__ raw_start,
+    const int* __restrict__ cell_start, const GridMeta* __restrict__ gmp,
+    float2* __restrict__ cloud, float4* __restrict__ chunk) {
+  constexpr int kKeys = kSubCells * kSubCells;
+  __shared__ int s_hist[kSortWarps][kKeys];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  int* hist = s_hist[wid];
+  const GridMeta gm = *gmp;
+  const int cells = gm.n_valid > 0 ? gm.gx * gm.gy : 0;
+  const float sub = gm.inv_cs * static_cast<float>(kSubCells);
+  const float2 pad = make_float2(__int_as_float(0x7fc00000), __int_as_float(0x7fc00000));
+  for (int c = blockIdx.x * kSortWarps + wid; c < cells; c += gridDim.x * kSortWarps) {
+    const int rs = raw_start[c], n = raw_start[c + 1] - rs;
+    if (n == 0) continue;  // warp-uniform
+    const int ps = cell_start[c];
+    const float ox = gm.x0 + static_cast<float>(c % gm.gx) * gm.cs;
+    const float oy = gm.y0 + static_cast<float>(c / gm.gx) * gm.cs;
+    for (int b = lane; b < kKeys; b += 32) hist[b] = 0;
+    __syncwarp();
+    for (int i = lane; i < n; i += 32) atomicAdd(&hist[sub_key(raw[rs + i], ox, oy, sub)], 1);
+    __syncwarp();
+    constexpr int kPer = kKeys / 32;
+    int v[kPer], loc = 0;
+#pragma unroll
+    for (int k = 0; k < kPer; ++k) loc += (v[k] = hist[lane * kPer + k]);
+    int incl = loc;
+    for (int o = 1; o < 32; o <<= 1) {
+      const int u = __shfl_up_sync(kFull, incl, o);
+      if (lane >= o) incl += u;
+    }
+    int run = incl - loc;
+#pragma unroll
+    for (int k = 0; k < kPer; ++k) {
+      hist[lane * kPer + k] = run;
+      run += v[k];
+    }
+    __syncwarp();
+    for (int i = lane; i < n; i += 32) {
+      const float2 p = raw[rs + i];
+      cloud[ps + atomicAdd(&hist[sub_key(p, ox, oy, sub)], 1)] = p;
+    }
+    const int np = (n + kChunk - 1) & ~(kChunk - 1);
+    if (n + lane < np) cloud[ps + n + lane] = pad;
+    __syncwarp();  // orders the warp's global stores before the L2 reads below
+    for (int j = lane; j < np / kChunk; j += 32) {
+      float x0 = FLT_MAX, x1 = -FLT_MAX, y0 = FLT_MAX, y1 = -FLT_MAX;
+#pragma unroll
+      for (int k = 0; k < kChunk; ++k) {
+        const float2 p = __ldcg(cloud + ps + j * kChunk + k);
+        if (p.x == p.x) {
+          x0 = fminf(x0, p.x); x1 = fmaxf(x1, p.x);
+          y0 = fminf(y0, p.y); y1 = fmaxf(y1, p.y);
+        }
+      }
+      chunk[ps / kChunk + j] =
+          make_float4(0.5f * (x0 + x1), 0.5f * (y0 + y1), 0.5f * (x1 - x0), 0.5f * (y1 - y0));
+    }
+    __syncwarp();
   }
 }
 
@@ -648,12 +753,13 @@ __device__ __forceinline__ bool box_may_beat(const WBox& w, float bx0, float bx1
 // distance to W and the distance to the body-frame AABB, then the exact polygon/cover SDF.
 // STATS (profiling builds of the launch only): count the point tests and exact SDF
 // evaluations the culls let through, for the executed-work roofline.
-template <int KIND, int NB, bool STATS = false>
+template <int KIND, int NB, bool STATS = false, bool CHUNKS = true>
 __global__ void __launch_bounds__(128) k_sdf_grid(const __grid_constant__ FpDev fp,
                                                   const float4* __restrict__ poses, int n_poses,
                                                   const GridMeta* __restrict__ gmp,
                                                   const int* __restrict__ cell_start,
                                                   const float2* __restrict__ cloud,
+                                                  const float4* __restrict__ chunk,
                                                   float* __restrict__ out,
                                                   unsigned long long* __restrict__ stats = nullptr) {
   unsigned long long n_test = 0, n_eval = 0;
@@ -709,24 +815,33 @@ __global__ void __launch_bounds__(128) k_sdf_grid(const __grid_constant__ FpDev 
       const bool need = active && (gx_ * gx_ + gy_ * gy_ < lim * lim) &&
                         box_may_beat(w, bx0, bx1, by0, by1, best);
       if (!__any_sync(kFull, need)) continue;
-      const float2* cp = cloud + s;
-      const int n = e - s;
       float l2 = lim * lim;
-      for (int p = 0; p < n; ++p) {
-        const float2 o = __ldg(cp + p);
-        const float dx = o.x - q.x, dy = o.y - q.y;
-        if (STATS && need) ++n_test;
-        if (need && dx * dx + dy * dy < l2) {
-          const float bx = fmaf(q.z, dx, q.w * dy);
-          const float by = fmaf(q.z, dy, -(q.w * dx));
-          // the cover bound pays for itself only when the exact polygon SDF is expensive
-          if ((KIND == EXM_FOOTPRINT_POLYGON && (NB == 0 || NB >= 8))
-                  ? cover_may_beat(fp, bx, by, best)
-                  : aabb_may_beat(fp, bx, by, best)) {
-            if (STATS) ++n_eval;
-            best = fminf(best, sd_body<KIND, NB>(fp, bx, by));
-            const float nl = R + best;
-            l2 = nl * nl;
+      // chunks of kChunk Morton-ordered points: one body-frame box bound per chunk, then the
+      // per-point bounds and the exact SDF for the points of the chunks some lane still needs
+      for (int ch = s / kChunk; ch < e / kChunk; ++ch) {
+        bool cneed = need;
+        if (CHUNKS) {
+          cneed = need && chunk_may_beat(fp, q, __ldg(chunk + ch), best);
+          if (!__any_sync(kFull, cneed)) continue;
+        }
+        const float2* cp = cloud + ch * kChunk;
+#pragma unroll 1
+        for (int p = 0; p < kChunk; ++p) {
+          const float2 o = __ldg(cp + p);
+          const float dx = o.x - q.x, dy = o.y - q.y;
+          if (STATS && cneed) ++n_test;
+          if (cneed && dx * dx + dy * dy < l2) {  // false for the NaN pads
+            const float bx = fmaf(q.z, dx, q.w * dy);
+            const float by = fmaf(q.z, dy, -(q.w * dx));
+            // the cover bound pays for itself only when the exact polygon SDF is expensive
+            if ((KIND == EXM_FOOTPRINT_POLYGON && (NB == 0 || NB >= 8))
+                    ? cover_may_beat(fp, bx, by, best)
+                    : aabb_may_beat(fp, bx, by, best)) {
+              if (STATS) ++n_eval;
+              best = fminf(best, sd_body<KIND, NB>(fp, bx, by));
+              const float nl = R + best;
+              l2 = nl * nl;
+            }
           }
         }
       }
@@ -1129,16 +1244,10 @@ __device__ __forceinline__ u64 pk(float a, float b) {
   return r;
 }
 __device__ __forceinline__ float lo(u64 v) {
-  float a, b;
-  asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(v));
-  (void)b;
-  return a;
+  return __uint_as_float(static_cast<unsigned>(v));
 }
 __device__ __forceinline__ float hi(u64 v) {
-  float a, b;
-  asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(v));
-  (void)a;
-  return b;
+  return __uint_as_float(static_cast<unsigned>(v >> 32));
 }
 __device__ __forceinline__ u64 bc(float x) { return pk(x, x); }
 __device__ __forceinline__ u64 fma2(u64 a, u64 b, u64 c) {
@@ -1367,39 +1476,52 @@ cudaError_t dispatch_fp(const FpDev& fp, Args&&... args) {
   }
 }
 
+// EXM_GRID_CHUNKS=0 disables the chunk bound (A/B measurements only; same results).
+inline bool grid_chunks() {
+  static const bool on = !(getenv("EXM_GRID_CHUNKS") && atoi(getenv("EXM_GRID_CHUNKS")) == 0);
+  return on;
+}
+
 template <int KIND, int NB>
 struct GridLaunch {
-  static cudaError_t run(const FpDev& fp, const float4* poses, int n_poses, const GridMeta* gm,
-                         const int* cell_start, const float2* cloud, float* out, cudaStream_t s) {
+  static cudaError_t run(const FpDev& fp, const float4* poses, int n_poses, const CloudGrid& g,
+                         float* out, cudaStream_t s) {
     if (n_poses <= 0) return cudaSuccess;
-    const int threads = 128;
-    k_sdf_grid<KIND, NB><<<(n_poses + threads - 1) / threads, threads, 0, s>>>(
-        fp, poses, n_poses, gm, cell_start, cloud, out);
+    const int threads = 128, blocks = (n_poses + threads - 1) / threads;
+    if (grid_chunks())
+      k_sdf_grid<KIND, NB><<<blocks, threads, 0, s>>>(fp, poses, n_poses, g.gm, g.cell_start,
+                                                      g.cloud, g.chunk, out);
+    else
+      k_sdf_grid<KIND, NB, false, false><<<blocks, threads, 0, s>>>(
+          fp, poses, n_poses, g.gm, g.cell_start, g.cloud, g.chunk, out);
     return cudaGetLastError();
   }
 };
 
 template <int KIND, int NB>
 struct GridStatsLaunch {
-  static cudaError_t run(const FpDev& fp, const float4* poses, int n_poses, const GridMeta* gm,
-                         const int* cell_start, const float2* cloud, float* out,
-                         unsigned long long* stats, cudaStream_t s) {
+  static cudaError_t run(const FpDev& fp, const float4* poses, int n_poses, const CloudGrid& g,
+                         float* out, unsigned long long* stats, cudaStream_t s) {
     if (n_poses <= 0) return cudaSuccess;
-    const int threads = 128;
-    k_sdf_grid<KIND, NB, true><<<(n_poses + threads - 1) / threads, threads, 0, s>>>(
-        fp, poses, n_poses, gm, cell_start, cloud, out, stats);
+    const int threads = 128, blocks = (n_poses + threads - 1) / threads;
+    if (grid_chunks())
+      k_sdf_grid<KIND, NB, true><<<blocks, threads, 0, s>>>(fp, poses, n_poses, g.gm,
+                                                            g.cell_start, g.cloud, g.chunk, out, stats);
+    else
+      k_sdf_grid<KIND, NB, true, false><<<blocks, threads, 0, s>>>(
+          fp, poses, n_poses, g.gm, g.cell_start, g.cloud, g.chunk, out, stats);
     return cudaGetLastError();
   }
 };
 
 template <int KIND, int NB>
 struct GridWarpLaunch {
-  static cudaError_t run(const FpDev& fp, const float4* poses, int n_poses, const GridMeta* gm,
-                         const int* cell_start, const float2* cloud, float* out, cudaStream_t s) {
+  static cudaError_t run(const FpDev& fp, const float4* poses, int n_poses, const CloudGrid& g,
+                         float* out, cudaStream_t s) {
     if (n_poses <= 0) return cudaSuccess;
     const int threads = 128, warps = threads / 32;
     k_sdf_grid_warp<KIND, NB><<<(n_poses + warps - 1) / warps, threads, 0, s>>>(
-        fp, poses, n_poses, gm, cell_start, cloud, out);
+        fp, poses, n_poses, g.gm, g.cell_start, g.cloud, out);
     return cudaGetLastError();
   }
 };
@@ -1434,8 +1556,7 @@ cudaError_t launch_noise(const StepConst& sc, const StepDyn* dyn, double* eps, c
 }
 
 cudaError_t launch_cloud_prep(const double* pts, const uint8_t* mask, const StepDyn* dyn,
-                              float radius, float2* tmp, float2* cloud, int* cell_start,
-                              GridMeta* gm, cudaStream_t s) {
+                              float radius, const CloudGrid& g, cudaStream_t s) {
   const int smem = kGridMax * kGridMax * static_cast<int>(sizeof(int));
   static bool attr_set = false;
   if (!attr_set) {
@@ -1445,7 +1566,15 @@ cudaError_t launch_cloud_prep(const double* pts, const uint8_t* mask, const Step
   }
   // Cells of half the bounding radius: a cull disc of radius R + d covers ~(2(R+d)/cs)^2 cells.
   const float cs_target = fmaxf(0.5f * radius, 0.02f);
-  k_cloud_prep<<<1, 1024, smem, s>>>(pts, mask, dyn, cs_target, tmp, cloud, cell_start, gm);
+  k_cloud_prep<<<1, 1024, smem, s>>>(pts, mask, dyn, cs_target, g.tmp, g.raw, g.raw_start,
+                                     g.cell_start, g.gm);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  int dev = 0, n_sm = 148;
+  if (cudaGetDevice(&dev) == cudaSuccess)
+    cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
+  k_cell_sort<<<2 * n_sm, kSortWarps * 32, 0, s>>>(g.raw, g.raw_start, g.cell_start, g.gm, g.cloud,
+                                                   g.chunk);
   return cudaGetLastError();
 }
 
@@ -1480,9 +1609,9 @@ cudaError_t launch_rollout(const StepConst& sc, const StepDyn* dyn, const double
 }
 
 cudaError_t launch_sdf_grid_stats(const FpDev& fp, const float4* poses, int n_poses,
-                                  const GridMeta* gm, const int* cell_start, const float2* cloud,
-                                  float* out, unsigned long long* stats, cudaStream_t s) {
-  return dispatch_fp<GridStatsLaunch>(fp, poses, n_poses, gm, cell_start, cloud, out, stats, s);
+                                  const CloudGrid& g, float* out, unsigned long long* stats,
+                                  cudaStream_t s) {
+  return dispatch_fp<GridStatsLaunch>(fp, poses, n_poses, g, out, stats, s);
 }
 
 cudaError_t launch_stage_costs(const StepConst& sc, const StepDyn* dyn, const double* guide,
@@ -1501,12 +1630,10 @@ cudaError_t launch_stage_costs(const StepConst& sc, const StepDyn* dyn, const do
 }
 
 cudaError_t launch_sdf_grid(const FpDev& fp, const float4* poses, int n_poses,
-                            const GridMeta* gm, const int* cell_start, const float2* cloud,
-                            float* out, cudaStream_t s) {
+                            const CloudGrid& g, float* out, cudaStream_t s) {
   // Few poses (validation rollout, single queries): one warp per pose keeps all lanes busy.
-  if (n_poses <= 4096)
-    return dispatch_fp<GridWarpLaunch>(fp, poses, n_poses, gm, cell_start, cloud, out, s);
-  return dispatch_fp<GridLaunch>(fp, poses, n_poses, gm, cell_start, cloud, out, s);
+  if (n_poses <= 4096) return dispatch_fp<GridWarpLaunch>(fp, poses, n_poses, g, out, s);
+  return dispatch_fp<GridLaunch>(fp, poses, n_poses, g, out, s);
 }
 
 cudaError_t launch_block_partials(const StepConst& sc, const double* base_cost,
