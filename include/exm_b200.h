@@ -254,6 +254,14 @@ exm_status exm_step_stats(exm_handle* h, int32_t* launches_per_step, float* sdf_
  * and pairs that reached the exact signed-distance evaluation. */
 exm_status exm_sdf_cull_stats(exm_handle* h, int64_t* points_tested, int64_t* sdf_evaluated);
 
+/* Diagnostics (host only, no GPU needed): validates a footprint exactly as exm_create does and
+ * returns the body-frame cull geometry the SDF kernels bound with: the bounding box
+ * {xmin, xmax, ymin, ymax} (aabb_out[4]) and n_out <= 3 axis-aligned boxes
+ * {cx, cy, hx, hy} whose union contains the footprint (boxes_out[12]). No reference
+ * counterpart: PreparedFootprint (geometry.hpp:127-136) keeps only bounding_radius. */
+exm_status exm_footprint_cull_boxes(const exm_footprint* fp, float* aabb_out, float* boxes_out,
+                                    int32_t* n_out);
+
 #ifdef __cplusplus
 }
 #endif

@@ -95,6 +95,17 @@ class FootprintSpec:
                                dptr(cols[2]), dptr(cols[3]))
         return fp, cols
 
+    def cull_boxes(self):
+        """(aabb[4], boxes[n, 4] as {cx, cy, hx, hy}): the body-frame cull geometry of the SDF
+        kernels (exm_footprint_cull_boxes; host-only, validates like exm_create)."""
+        fp, keep = self._c()
+        aabb = np.zeros(4, np.float32)
+        boxes = np.zeros(12, np.float32)
+        n = C.c_int32()
+        check(_abi.load_library().exm_footprint_cull_boxes(C.byref(fp), fptr(aabb), fptr(boxes),
+                                                           C.byref(n)))
+        return aabb, boxes.reshape(3, 4)[: n.value]
+
 
 @dataclass
 class MotionModel:

@@ -98,8 +98,11 @@ cudaError_t alloc_cloud_grid(int n_cap, void** block, CloudGrid* g) {
   const size_t o_chunk = o_cloud + up(cap * sizeof(float2));
   const size_t o_rs = o_chunk + up((cap / kChunk + 1) * sizeof(float4));
   const size_t o_cs = o_rs + up(cells * sizeof(int)), o_gm = o_cs + up(cells * sizeof(int));
+  const size_t o_ds = o_gm + up(sizeof(GridMeta));
   char* d = nullptr;
-  cudaError_t e = cudaMalloc(reinterpret_cast<void**>(&d), o_gm + sizeof(GridMeta));
+  cudaError_t e = cudaMalloc(reinterpret_cast<void**>(&d), o_ds + 2 * sizeof(float));
+  if (e != cudaSuccess) return e;
+  e = cudaMemset(d + o_ds, 0, 2 * sizeof(float));
   if (e != cudaSuccess) return e;
   *block = d;
   g->tmp = reinterpret_cast<float2*>(d);
@@ -109,6 +112,7 @@ cudaError_t alloc_cloud_grid(int n_cap, void** block, CloudGrid* g) {
   g->raw_start = reinterpret_cast<int*>(d + o_rs);
   g->cell_start = reinterpret_cast<int*>(d + o_cs);
   g->gm = reinterpret_cast<GridMeta*>(d + o_gm);
+  g->dstat = reinterpret_cast<float*>(d + o_ds);
   return cudaSuccess;
 }
 
@@ -179,30 +183,70 @@ std::array<double, 4> clipped_box(const std::vector<double>& x, const std::vecto
   return bb;
 }
 
+// Does the union of boxes {x0, x1, y0, y1} cover segment a-b? (Liang-Barsky parameter
+// intervals of the segment inside each box, merged over [0, 1].)
+bool segment_covered(double ax, double ay, double bx, double by,
+                     const std::vector<std::array<double, 4>>& boxes) {
+  std::vector<std::pair<double, double>> iv;
+  for (const auto& q : boxes) {
+    double t0 = 0.0, t1 = 1.0;
+    const double d[2] = {bx - ax, by - ay}, p0[2] = {ax, ay};
+    bool ok = true;
+    for (int k = 0; k < 2 && ok; ++k) {
+      const double lo = q[2 * k], hi = q[2 * k + 1];
+      if (d[k] == 0.0) {
+        ok = p0[k] >= lo && p0[k] <= hi;
+      } else {
+        double u = (lo - p0[k]) / d[k], v = (hi - p0[k]) / d[k];
+        if (u > v) std::swap(u, v);
+        t0 = std::max(t0, u);
+        t1 = std::min(t1, v);
+        ok = t0 <= t1;
+      }
+    }
+    if (ok) iv.push_back({t0, t1});
+  }
+  std::sort(iv.begin(), iv.end());
+  double reach = 0.0;
+  for (const auto& [u, v] : iv) {
+    if (u > reach + 1e-12) return false;
+    reach = std::max(reach, v);
+  }
+  return reach >= 1.0 - 1e-12;
+}
+
 // Greedy cover of a polygon by <= max_boxes axis-aligned boxes: repeatedly split the largest
-// box at the vertex coordinate (either axis) that minimises the summed area of the two
-// clipped halves. Exact (zero slack) for rectilinear polygons whose cuts it finds.
+// box at the vertex coordinate (either axis) that minimises the summed area of the two halves,
+// each half being the bounding box of the polygon strictly on its side of the cut (a boundary
+// edge lying on the cut line would otherwise stretch both halves), extended back to the cut.
+// Exact (zero slack) for rectilinear polygons such as the L. The result is checked: if some
+// edge is not covered by the union the cover falls back to the bounding box.
 std::vector<std::array<double, 4>> cover_boxes(const std::vector<double>& x,
                                                const std::vector<double>& y, int max_boxes) {
   auto area = [](const std::array<double, 4>& b) {
     return b[0] > b[1] ? 0.0 : (b[1] - b[0]) * (b[3] - b[2]);
   };
-  std::vector<std::array<double, 4>> boxes = {clipped_box(x, y, 0, -1e300, 1e300)};
+  const std::array<double, 4> whole = clipped_box(x, y, 0, -1e300, 1e300);
+  const double eps = 1e-9 * (1.0 + std::max(whole[1] - whole[0], whole[3] - whole[2]));
+  std::vector<std::array<double, 4>> boxes = {whole};
   while (static_cast<int>(boxes.size()) < max_boxes) {
     size_t big = 0;
     for (size_t j = 1; j < boxes.size(); ++j)
       if (area(boxes[j]) > area(boxes[big])) big = j;
     const auto b = boxes[big];
-    double best_gain = 1e-9 * area(b);
+    double best_gain = 1e-6 * area(b);
     int best_axis = -1;
     std::array<double, 4> best_lo{}, best_hi{};
     for (int axis = 0; axis < 2; ++axis) {
       const std::vector<double>& c = axis == 0 ? x : y;
+      const double lo0 = axis == 0 ? b[0] : b[2], hi1 = axis == 0 ? b[1] : b[3];
       for (double cut : c) {
-        if (cut <= (axis == 0 ? b[0] : b[2]) || cut >= (axis == 0 ? b[1] : b[3])) continue;
-        const double lo0 = axis == 0 ? b[0] : b[2], hi1 = axis == 0 ? b[1] : b[3];
-        auto lo = clipped_box(x, y, axis, lo0, cut);
-        auto hi = clipped_box(x, y, axis, cut, hi1);
+        if (cut <= lo0 + 2 * eps || cut >= hi1 - 2 * eps) continue;
+        auto lo = clipped_box(x, y, axis, lo0, cut - eps);
+        auto hi = clipped_box(x, y, axis, cut + eps, hi1);
+        if (lo[0] > lo[1] || hi[0] > hi[1]) continue;
+        lo[2 * axis + 1] = cut;
+        hi[2 * axis] = cut;
         // restrict to the current box on the other axis
         const int o = axis == 0 ? 2 : 0;
         for (auto* q : {&lo, &hi}) {
@@ -222,6 +266,12 @@ std::vector<std::array<double, 4>> cover_boxes(const std::vector<double>& x,
     boxes[big] = best_lo;
     boxes.push_back(best_hi);
   }
+  // safety net: every polygon edge must lie in the union (slack eps on each box)
+  std::vector<std::array<double, 4>> grown = boxes;
+  for (auto& q : grown) q = {q[0] - 4 * eps, q[1] + 4 * eps, q[2] - 4 * eps, q[3] + 4 * eps};
+  const size_t n = x.size();
+  for (size_t i = 0; i < n; ++i)
+    if (!segment_covered(x[i], y[i], x[(i + 1) % n], y[(i + 1) % n], grown)) return {whole};
   return boxes;
 }
 
@@ -504,7 +554,7 @@ exm_status enqueue_pre(exm_handle* h, bool draw_noise, cudaStream_t s, int* laun
 exm_status enqueue_post(exm_handle* h, cudaStream_t s, int* launches) {
   const StepConst& sc = h->sc;
   EXM_CUDA(launch_stage_costs(sc, h->d_dyn, h->d_guide, h->guide_cap, h->d_xy, h->d_dmin,
-                              h->d_stage, h->d_flags, s));
+                              h->d_stage, h->d_flags, h->grid.dstat, s));
   EXM_CUDA(launch_block_partials(sc, h->d_base, h->d_stage, h->d_flags, h->d_eps, h->d_partials,
                                  nullptr, nullptr, s));
   if (h->world > 1) {
@@ -944,7 +994,7 @@ exm_status exm_evaluate_rollouts(exm_handle* h, const double q0[3], const double
                           states_out ? h->d_states : nullptr, s));
   EXM_CUDA(launch_sdf_grid(h->fp, h->d_poses, static_cast<int>(KT), h->grid, h->d_dmin, s));
   EXM_CUDA(launch_stage_costs(sc, h->d_dyn, h->d_guide, h->guide_cap, h->d_xy, h->d_dmin,
-                              h->d_stage, h->d_flags, s));
+                              h->d_stage, h->d_flags, h->grid.dstat, s));
   EXM_CUDA(launch_block_partials(sc, h->d_base, h->d_stage, h->d_flags, h->d_eps, nullptr,
                                  h->d_cost, h->d_unsafe, s));
   if (controls_out)
@@ -1181,6 +1231,20 @@ exm_status exm_read_resident(exm_handle* h, double* nominal_out, double* u_prev_
 }
 
 void* exm_stream(exm_handle* h) { return h ? static_cast<void*>(h->stream) : nullptr; }
+
+exm_status exm_footprint_cull_boxes(const exm_footprint* fp, float* aabb_out, float* boxes_out,
+                                    int32_t* n_out) {
+  FpDev d;
+  const exm_status st = build_footprint(fp, &d);
+  if (st != EXM_OK) return st;
+  if (aabb_out)
+    for (int k = 0; k < 4; ++k) aabb_out[k] = d.aabb[k];
+  if (boxes_out)
+    for (int j = 0; j < kMaxCover; ++j)
+      for (int k = 0; k < 4; ++k) boxes_out[4 * j + k] = d.cover[j][k];
+  if (n_out) *n_out = d.ncover;
+  return EXM_OK;
+}
 
 exm_status exm_sdf_cull_stats(exm_handle* h, int64_t* points_tested, int64_t* sdf_evaluated) {
   if (!h) return fail(EXM_ERR_INVALID_ARGUMENT, "handle is null");

@@ -57,6 +57,9 @@ struct CloudGrid {
   float4* chunk = nullptr;
   int* cell_start = nullptr;
   GridMeta* gm = nullptr;
+  // {sum of clamped per-pose minima, count} accumulated by the stage-cost kernel and consumed
+  // (then reset) by the next step's prep kernel: sizes the cells for the searches to come
+  float* dstat = nullptr;
 };
 // Padded cloud capacity for n_cap points: every nonempty cell adds at most kChunk - 1 pads.
 inline size_t cloud_capacity(int n_cap) {
@@ -117,7 +120,7 @@ cudaError_t launch_sdf_grid_stats(const FpDev& fp, const float4* poses, int n_po
                                   cudaStream_t s);
 cudaError_t launch_stage_costs(const StepConst& sc, const StepDyn* dyn, const double* guide,
                                int guide_cap, const double2* xy, const float* dmin,
-                               double* stage, uint8_t* flags, cudaStream_t s);
+                               double* stage, uint8_t* flags, float* dstat, cudaStream_t s);
 cudaError_t launch_block_partials(const StepConst& sc, const double* base_cost,
                                   const double* stage, const uint8_t* flags, const double* eps,
                                   double* partials, double* cost_out, uint8_t* unsafe_out,

@@ -205,6 +205,12 @@ __device__ __forceinline__ void xy_rate(const double* u, double ct, double st, d
 
 constexpr int kRolloutWarps = 4;  // rollouts (warps) per CTA in k_rollout
 constexpr float kPtsPerCell = 32.0f;
+constexpr float kCellMaxR = 0.5f;        // cell edge <= kCellMaxR * R ...
+constexpr float kCellSearchFrac = 0.385f;  // ... or <= this fraction of R + mean d_min
+constexpr float kDstatClamp = 16.0f;       // d_min clamp in that mean (empty clouds: 1e6)
+// Below this many poses one thread per pose leaves most SMs idle (< ~16 warps each): use one
+// warp per pose instead.
+constexpr int kWarpPerPoseMax = 65536;
 constexpr int kPartialThreads = 1024;  // 32 warps: 8 rollouts per warp in the U sums
 
 // Serial part of one rollout (score_rollout, controller.cpp:151-169, minus the SDF and the task
@@ -375,12 +381,16 @@ __device__ __forceinline__ float sd_body(const FpDev& fp, float px, float py) {
 // Exact second-level cull on the body-frame point: the footprint lies inside its AABB, so an
 // exterior point's signed distance is at least its distance to the AABB. Points inside the
 // AABB (distance 0) may be inside the footprint and are always evaluated.
+// Interior bound (p inside the AABB): the footprint lies inside its AABB, so p is no deeper
+// in the footprint than in the AABB: sd(p) >= max(xmin - x, x - xmax, ymin - y, y - ymax).
+// Culls interior points once a negative minimum is known (footprint overlapping obstacles).
 __device__ __forceinline__ bool aabb_may_beat(const FpDev& fp, float bx, float by, float best) {
-  const float ax = fmaxf(fmaxf(fp.aabb[0] - bx, bx - fp.aabb[1]), 0.f);
-  const float ay = fmaxf(fmaxf(fp.aabb[2] - by, by - fp.aabb[3]), 0.f);
+  const float dx = fmaxf(fp.aabb[0] - bx, bx - fp.aabb[1]);
+  const float dy = fmaxf(fp.aabb[2] - by, by - fp.aabb[3]);
+  const float ax = fmaxf(dx, 0.f), ay = fmaxf(dy, 0.f);
   const float a2 = fmaf(ax, ax, ay * ay);
   const float lim = best + kCullMargin;
-  return a2 == 0.f || (lim > 0.f && a2 < lim * lim);
+  return a2 == 0.f ? fmaxf(dx, dy) < lim : (lim > 0.f && a2 < lim * lim);
 }
 
 // Polygon cover bound: the union of the kMaxCover cover boxes (unused slots repeat box 0)
@@ -395,7 +405,9 @@ __device__ __forceinline__ bool cover_may_beat(const FpDev& fp, float bx, float 
     d2 = fminf(d2, fmaf(ax, ax, ay * ay));
   }
   const float lim = best + kCullMargin;
-  return d2 == 0.f || (lim > 0.f && d2 < lim * lim);
+  if (d2 == 0.f)  // inside the cover: the AABB interior bound (aabb_may_beat)
+    return fmaxf(fmaxf(fp.aabb[0] - bx, bx - fp.aabb[1]), fmaxf(fp.aabb[2] - by, by - fp.aabb[3])) < lim;
+  return lim > 0.f && d2 < lim * lim;
 }
 
 // Chunk bound: the chunk's points lie in the world box {cx +- hx, cy +- hy}; in the body frame
@@ -415,7 +427,12 @@ __device__ __forceinline__ bool chunk_may_beat(const FpDev& fp, float4 q, float4
     d2 = fminf(d2, fmaf(ax, ax, ay * ay));
   }
   const float lim = best + kCullMargin;
-  return d2 == 0.f || (lim > 0.f && d2 < lim * lim);
+  if (d2 == 0.f) {  // touches the cover: every point is at least as shallow as the AABB allows
+    const float lx = fmaxf(fp.aabb[0] - (bx + ex), (bx - ex) - fp.aabb[1]);
+    const float ly = fmaxf(fp.aabb[2] - (by + ey), (by - ey) - fp.aabb[3]);
+    return fmaxf(lx, ly) < lim;
+  }
+  return lim > 0.f && d2 < lim * lim;
 }
 
 // Order-preserving float -> u32 key (for min via integer reductions / atomics).
@@ -450,7 +467,9 @@ __global__ void k_noise(const StepConst sc, const StepDyn* __restrict__ dyn,
 __global__ void __launch_bounds__(1024) k_cloud_prep(const double* __restrict__ pts,
                                                      const uint8_t* __restrict__ mask,
                                                      const StepDyn* __restrict__ dyn,
-                                                     float cs_target, float2* __restrict__ tmp,
+                                                     float cs_lo, float cs_hi, float pts_per_cell,
+                                                     float radius, float* __restrict__ dstat,
+                                                     float2* __restrict__ tmp,
                                                      float2* __restrict__ raw,
                                                      int* __restrict__ raw_start,
                                                      int* __restrict__ cell_start,
@@ -503,10 +522,14 @@ __global__ void __launch_bounds__(1024) k_cloud_prep(const double* __restrict__ 
       g.x0 = g.y0 = 0.0f; g.cs = 1.0f; g.inv_cs = 1.0f; g.gx = g.gy = 1;
     } else {
       const float ex = mxx - mnx, ey = mxy - mny;
-      // Cell edge: about kPtsPerCell points per cell on average, between R/4 and R/2 (dense
+      // Cell edge: about pts_per_cell points per cell on average, within [cs_lo, cs_hi] (dense
       // boundary clouds get finer cells, sparse ones coarser), at most kGridMax per axis.
-      const float dens = sqrtf(kPtsPerCell * fmaxf(ex * ey, 1e-6f) / static_cast<float>(cnt));
-      float cs = fminf(fmaxf(dens, 0.5f * cs_target), cs_target);
+      const float dens = sqrtf(pts_per_cell * fmaxf(ex * ey, 1e-6f) / static_cast<float>(cnt));
+      // upper bound: a fixed fraction of the expected search radius R + mean(d_min) of the
+      // previous step when there is one (far obstacles: coarse cells, few rings), else cs_hi
+      float hi = cs_hi;
+      if (dstat[1] > 0.f) hi = fmaxf(cs_hi, kCellSearchFrac * (radius + dstat[0] / dstat[1]));
+      float cs = fminf(fmaxf(dens, cs_lo), hi);
       cs = fmaxf(cs, fmaxf(ex, ey) / static_cast<float>(kGridMax - 1) * 1.001f);
       cs = fmaxf(cs, 1e-4f);
       g.x0 = mnx; g.y0 = mny; g.cs = cs; g.inv_cs = 1.0f / cs;
@@ -515,6 +538,8 @@ __global__ void __launch_bounds__(1024) k_cloud_prep(const double* __restrict__ 
     }
     gm = g;
     *gm_out = g;
+    dstat[0] = 0.f;  // consumed: the stage costs of this step accumulate the next statistic
+    dstat[1] = 0.f;
   }
   __syncthreads();
   const int cells = gm.gx * gm.gy;
@@ -692,18 +717,47 @@ __global__ void __launch_bounds__(kRolloutWarps * 32) k_rollout(
 __global__ void k_stage_costs(const StepConst sc, const StepDyn* __restrict__ dynp,
                               const double* __restrict__ guide, const double2* __restrict__ xy,
                               const float* __restrict__ dmin, double* __restrict__ stage,
-                              uint8_t* __restrict__ flags) {
+                              uint8_t* __restrict__ flags, float* __restrict__ dstat) {
   extern __shared__ double g[];
   const int ng = dynp->n_guide;
   for (int i = threadIdx.x; i < 2 * ng; i += blockDim.x) g[i] = guide[i];
   __syncthreads();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= sc.k_local * sc.T) return;
-  const int h = i / sc.k_local, r = i % sc.k_local;
-  const size_t src = static_cast<size_t>(r) * sc.T + h;
-  const double d = static_cast<double>(dmin[src]);
-  stage[i] = stage_cost(sc, xy[src], d, g, ng, dynp->goal);
-  flags[i] = d < sc.d_safe ? 1 : 0;
+  const bool live = i < sc.k_local * sc.T;
+  float dc = 0.f;
+  if (live) {
+    const int h = i / sc.k_local, r = i % sc.k_local;
+    const size_t src = static_cast<size_t>(r) * sc.T + h;
+    const double d = static_cast<double>(dmin[src]);
+    stage[i] = stage_cost(sc, xy[src], d, g, ng, dynp->goal);
+    flags[i] = d < sc.d_safe ? 1 : 0;
+    dc = fminf(fmaxf(dmin[src], 0.f), kDstatClamp);
+  }
+  // search-radius statistic for the next step's cell size (k_cloud_prep): one atomic pair
+  // per block
+  __shared__ float red[2][8];
+  float cnt = live ? 1.f : 0.f;
+  for (int o = 16; o; o >>= 1) {
+    dc += __shfl_xor_sync(kFull, dc, o);
+    cnt += __shfl_xor_sync(kFull, cnt, o);
+  }
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (lane == 0) {
+    red[0][warp] = dc;
+    red[1][warp] = cnt;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float a = 0.f, b = 0.f;
+    for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) {
+      a += red[0][w];
+      b += red[1][w];
+    }
+    if (b > 0.f) {
+      atomicAdd(dstat, a);
+      atomicAdd(dstat + 1, b);
+    }
+  }
 }
 
 // Ring c (Chebyshev radius k >= 1) around (ci, cj): 8k cells, enumerated row/column-wise.
@@ -833,8 +887,9 @@ __global__ void __launch_bounds__(128) k_sdf_grid(const __grid_constant__ FpDev 
           if (cneed && dx * dx + dy * dy < l2) {  // false for the NaN pads
             const float bx = fmaf(q.z, dx, q.w * dy);
             const float by = fmaf(q.z, dy, -(q.w * dx));
-            // the cover bound pays for itself only when the exact polygon SDF is expensive
-            if ((KIND == EXM_FOOTPRINT_POLYGON && (NB == 0 || NB >= 8))
+            // polygons: the cover bound (exact for rectilinear shapes: the L's notch is culled);
+            // rectangle covers: the AABB pre-test (the exact SDF costs about as much as a cover)
+            if (KIND == EXM_FOOTPRINT_POLYGON
                     ? cover_may_beat(fp, bx, by, best)
                     : aabb_may_beat(fp, bx, by, best)) {
               if (STATS) ++n_eval;
@@ -1564,10 +1619,13 @@ cudaError_t launch_cloud_prep(const double* pts, const uint8_t* mask, const Step
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
-  // Cells of half the bounding radius: a cull disc of radius R + d covers ~(2(R+d)/cs)^2 cells.
-  const float cs_target = fmaxf(0.5f * radius, 0.02f);
-  k_cloud_prep<<<1, 1024, smem, s>>>(pts, mask, dyn, cs_target, g.tmp, g.raw, g.raw_start,
-                                     g.cell_start, g.gm);
+  // Cells sized for about kPtsPerCell points, between R/4 and kCellMaxR * R: a cull disc of
+  // radius R + d covers ~(2(R+d)/cs)^2 cells; the chunk bounds cull inside a cell.
+  static const float ppc = getenv("EXM_PTS_PER_CELL") ? atof(getenv("EXM_PTS_PER_CELL")) : kPtsPerCell;
+  static const float cmax = getenv("EXM_CELL_MAX_R") ? atof(getenv("EXM_CELL_MAX_R")) : kCellMaxR;
+  const float r = fmaxf(radius, 0.04f);
+  k_cloud_prep<<<1, 1024, smem, s>>>(pts, mask, dyn, 0.25f * r, cmax * r, ppc, r, g.dstat, g.tmp,
+                                     g.raw, g.raw_start, g.cell_start, g.gm);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   int dev = 0, n_sm = 148;
@@ -1616,7 +1674,7 @@ cudaError_t launch_sdf_grid_stats(const FpDev& fp, const float4* poses, int n_po
 
 cudaError_t launch_stage_costs(const StepConst& sc, const StepDyn* dyn, const double* guide,
                                int guide_cap, const double2* xy, const float* dmin,
-                               double* stage, uint8_t* flags, cudaStream_t s) {
+                               double* stage, uint8_t* flags, float* dstat, cudaStream_t s) {
   const int n = sc.k_local * sc.T;
   if (n <= 0) return cudaSuccess;
   const size_t smem = sizeof(double) * 2 * static_cast<size_t>(guide_cap);
@@ -1625,14 +1683,15 @@ cudaError_t launch_stage_costs(const StepConst& sc, const StepDyn* dyn, const do
                                          static_cast<int>(smem));
     if (e != cudaSuccess) return e;
   }
-  k_stage_costs<<<(n + 255) / 256, 256, smem, s>>>(sc, dyn, guide, xy, dmin, stage, flags);
+  k_stage_costs<<<(n + 255) / 256, 256, smem, s>>>(sc, dyn, guide, xy, dmin, stage, flags, dstat);
   return cudaGetLastError();
 }
 
 cudaError_t launch_sdf_grid(const FpDev& fp, const float4* poses, int n_poses,
                             const CloudGrid& g, float* out, cudaStream_t s) {
   // Few poses (validation rollout, single queries): one warp per pose keeps all lanes busy.
-  if (n_poses <= 4096) return dispatch_fp<GridWarpLaunch>(fp, poses, n_poses, g, out, s);
+  static const int warp_max = getenv("EXM_WARP_MAX") ? atoi(getenv("EXM_WARP_MAX")) : kWarpPerPoseMax;
+  if (n_poses <= warp_max) return dispatch_fp<GridWarpLaunch>(fp, poses, n_poses, g, out, s);
   return dispatch_fp<GridLaunch>(fp, poses, n_poses, g, out, s);
 }
 
