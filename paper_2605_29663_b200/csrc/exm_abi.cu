@@ -386,6 +386,13 @@ exm_status build_footprint(const exm_footprint* fp, FpDev* out) {
     }
   }
   if (out->kind == EXM_FOOTPRINT_POLYGON) {
+    for (int b = 0; b < out->count + (out->count & 1); ++b) {
+      float z[8] = {out->e[0][0], out->e[0][1], 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+      const float* e = b < out->count ? out->e[b] : z;
+      for (int k = 0; k < 8; ++k) out->ep[b / 2][k][b & 1] = e[k];
+    }
+  }
+  if (out->kind == EXM_FOOTPRINT_POLYGON) {
     std::vector<double> px(out->count), py(out->count);
     for (int i = 0; i < out->count; ++i) {
       px[i] = out->e[i][0];

@@ -13,7 +13,7 @@ constexpr int kMaxCover = 3;         // boxes of the polygon cull cover
 constexpr int kBlockRollouts = 256;  // rollouts per softmax partial (fixed: G-invariant)
 constexpr int kGridMax = 128;        // cloud grid cells per axis (<= 16384 cells, smem histogram)
 constexpr float kEmptyDistance = 1e6f;  // kEmptyMaskDistance (geometry.hpp:37)
-constexpr float kCullMargin = 1e-3f;    // conservative slack on every lower-bound cull (m)
+constexpr float kCullMargin = 1e-4f;    // base slack on every lower-bound cull (m)
 constexpr int kChunk = 8;               // cloud points per chunk (one bounding box each)
 constexpr int kSubCells = 16;           // per-axis sub-cells of the in-cell Morton order
 
@@ -36,12 +36,16 @@ struct FpDev {
   int reserved2;
   float cover[kMaxCover][4];
   float e[kMaxEdges][8];
+  // polygon edges in pairs for the f32x2 path: ep[j][k] = {e[2j][k], e[2j+1][k]}; an odd
+  // count is padded with the zero-length edge {v0x, v0y, 0...}
+  alignas(8) float ep[kMaxEdges / 2][8][2];
 };
 
 // Uniform grid over the recentred valid cloud (written by the prep kernel).
 struct GridMeta {
   float x0, y0, cs, inv_cs;
-  int gx, gy, n_valid, reserved;
+  int gx, gy, n_valid;
+  float margin;  // cull slack (m): kCullMargin + rounding allowance for the cloud's extent
 };
 
 // Device cloud structure of one control step (HBM, rebuilt every cycle by launch_cloud_prep):

@@ -20,6 +20,8 @@
 #include <cfloat>
 #include <cmath>
 #include <cstdint>
+#include <cstdlib>
+#include <cstring>
 
 #include "exm_common.cuh"
 
@@ -307,6 +309,44 @@ __device__ __forceinline__ double stage_cost(const StepConst& sc, double2 xy, do
   return task_cost(sc, q, g, ng, goal, false) + obstacle_cost(sc, d);
 }
 
+// ---- packed FP32x2 (sm_100 FFMA2/FADD2/FMUL2) helpers ---------------------------------
+typedef unsigned long long u64;
+__device__ __forceinline__ u64 pk(float a, float b) {
+  u64 r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+  return r;
+}
+__device__ __forceinline__ float lo(u64 v) {
+  return __uint_as_float(static_cast<unsigned>(v));
+}
+__device__ __forceinline__ float hi(u64 v) {
+  return __uint_as_float(static_cast<unsigned>(v >> 32));
+}
+__device__ __forceinline__ u64 bc(float x) { return pk(x, x); }
+__device__ __forceinline__ u64 fma2(u64 a, u64 b, u64 c) {
+  u64 r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+  return r;
+}
+__device__ __forceinline__ u64 mul2(u64 a, u64 b) {
+  u64 r;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+__device__ __forceinline__ u64 sub2(u64 a, u64 b) {
+  u64 r;
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+__device__ __forceinline__ unsigned sgn_lo(u64 v) { return __float_as_uint(lo(v)); }
+__device__ __forceinline__ unsigned sgn_hi(u64 v) { return __float_as_uint(hi(v)); }
+
+__device__ __forceinline__ float min3f(float a, float b, float c) {
+  float r;
+  asm("min.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));  // FMNMX3
+  return r;
+}
+
 // ------------------------------------------------------------------ FP32 signed distance
 // Polygon edge step (PreparedFootprint::sd polygon branch, geometry.cpp:273-292).
 //   t  = sat(p.e/|e|^2 - v.e/|e|^2)           2 FFMA (second .SAT)
@@ -325,6 +365,41 @@ __device__ __forceinline__ void poly_edge(const float* e, float px, float py, fl
   const float cr = fmaf(ry, e[7], rx * e[3]);  // e[7] = -ex
   par ^= (__float_as_uint(ry) ^ __float_as_uint(ry_next)) & (__float_as_uint(ry) ^ __float_as_uint(cr));
   ry = ry_next;
+}
+
+// The same polygon SDF with two edges per f32x2 operation (FFMA2/FADD2/FMUL2): edge pair j
+// is fp.ep[j] (field k of edges 2j, 2j+1 adjacent; an odd count is padded with a zero-length
+// edge at vertex 0, which neither straddles nor changes the minimum). Every lane performs the
+// scalar poly_edge arithmetic in the same order, so the result is bit-identical.
+__device__ __forceinline__ u64 ldp(const float (&a)[2]) { return *reinterpret_cast<const u64*>(a); }
+
+template <int NB>
+__device__ __forceinline__ float sd_polygon_x2(const FpDev& fp, float px, float py) {
+  constexpr int NP = (NB + 1) / 2;
+  const u64 PX = bc(px), PY = bc(py);
+  const u64 RY0 = sub2(ldp(fp.ep[0][1]), PY);
+  u64 RY = RY0;
+  float best2 = __int_as_float(0x7f800000);
+  unsigned par = 0u;
+#pragma unroll
+  for (int j = 0; j < NP; ++j) {
+    const u64 RYn = j + 1 < NP ? sub2(ldp(fp.ep[j + 1][1]), PY) : RY0;
+    const u64 TP = fma2(PY, ldp(fp.ep[j][5]), ldp(fp.ep[j][6]));
+    const u64 T = pk(__saturatef(fmaf(px, fp.ep[j][4][0], lo(TP))),
+                     __saturatef(fmaf(px, fp.ep[j][4][1], hi(TP))));
+    const u64 RX = sub2(ldp(fp.ep[j][0]), PX);
+    const u64 QX = fma2(T, ldp(fp.ep[j][2]), RX);
+    const u64 QY = fma2(T, ldp(fp.ep[j][3]), RY);
+    const u64 D2 = fma2(QX, QX, mul2(QY, QY));
+    best2 = min3f(best2, lo(D2), hi(D2));
+    const u64 CR = fma2(RY, ldp(fp.ep[j][7]), mul2(RX, ldp(fp.ep[j][3])));
+    const unsigned a0 = sgn_lo(RY), a1 = sgn_hi(RY), a2 = sgn_lo(RYn);
+    par ^= ((a0 ^ a1) & (a0 ^ sgn_lo(CR))) ^ ((a1 ^ a2) & (a1 ^ sgn_hi(CR)));
+    RY = RYn;
+  }
+  if (best2 < 1e-24f) return 0.0f;  // kBoundaryEpsilon rule (d < 1e-12 -> 0)
+  const float d = sqrtf(best2);
+  return (par >> 31) ? -d : d;
 }
 
 template <int NB>
@@ -374,7 +449,8 @@ __device__ __forceinline__ float sd_rect(const FpDev& fp, float px, float py) {
 
 template <int KIND, int NB>
 __device__ __forceinline__ float sd_body(const FpDev& fp, float px, float py) {
-  if constexpr (KIND == EXM_FOOTPRINT_POLYGON) return sd_polygon<NB>(fp, px, py);
+  if constexpr (KIND == EXM_FOOTPRINT_POLYGON && NB > 0) return sd_polygon_x2<NB>(fp, px, py);
+  else if constexpr (KIND == EXM_FOOTPRINT_POLYGON) return sd_polygon<NB>(fp, px, py);
   else return sd_rect<NB>(fp, px, py);
 }
 
@@ -384,19 +460,21 @@ __device__ __forceinline__ float sd_body(const FpDev& fp, float px, float py) {
 // Interior bound (p inside the AABB): the footprint lies inside its AABB, so p is no deeper
 // in the footprint than in the AABB: sd(p) >= max(xmin - x, x - xmax, ymin - y, y - ymax).
 // Culls interior points once a negative minimum is known (footprint overlapping obstacles).
-__device__ __forceinline__ bool aabb_may_beat(const FpDev& fp, float bx, float by, float best) {
+__device__ __forceinline__ bool aabb_may_beat(const FpDev& fp, float bx, float by, float best,
+                                              float mg) {
   const float dx = fmaxf(fp.aabb[0] - bx, bx - fp.aabb[1]);
   const float dy = fmaxf(fp.aabb[2] - by, by - fp.aabb[3]);
   const float ax = fmaxf(dx, 0.f), ay = fmaxf(dy, 0.f);
   const float a2 = fmaf(ax, ax, ay * ay);
-  const float lim = best + kCullMargin;
+  const float lim = best + mg;
   return a2 == 0.f ? fmaxf(dx, dy) < lim : (lim > 0.f && a2 < lim * lim);
 }
 
 // Polygon cover bound: the union of the kMaxCover cover boxes (unused slots repeat box 0)
 // contains the polygon, so an exterior point's signed distance is at least its distance to the
 // nearest box (0 inside a box: evaluate). Subsumes the AABB bound.
-__device__ __forceinline__ bool cover_may_beat(const FpDev& fp, float bx, float by, float best) {
+__device__ __forceinline__ bool cover_may_beat(const FpDev& fp, float bx, float by, float best,
+                                               float mg) {
   float d2 = __int_as_float(0x7f800000);
 #pragma unroll
   for (int j = 0; j < kMaxCover; ++j) {
@@ -404,7 +482,7 @@ __device__ __forceinline__ bool cover_may_beat(const FpDev& fp, float bx, float 
     const float ay = fmaxf(fabsf(by - fp.cover[j][1]) - fp.cover[j][3], 0.f);
     d2 = fminf(d2, fmaf(ax, ax, ay * ay));
   }
-  const float lim = best + kCullMargin;
+  const float lim = best + mg;
   if (d2 == 0.f)  // inside the cover: the AABB interior bound (aabb_may_beat)
     return fmaxf(fmaxf(fp.aabb[0] - bx, bx - fp.aabb[1]), fmaxf(fp.aabb[2] - by, by - fp.aabb[3])) < lim;
   return lim > 0.f && d2 < lim * lim;
@@ -414,7 +492,8 @@ __device__ __forceinline__ bool cover_may_beat(const FpDev& fp, float bx, float 
 // of pose q that box lies inside the box centred at R(theta)^T (c - t) with half extents
 // (|cos| hx + |sin| hy, |sin| hx + |cos| hy). No point of the chunk is nearer to the footprint
 // than that box is to the cover union (0 if they overlap: evaluate).
-__device__ __forceinline__ bool chunk_may_beat(const FpDev& fp, float4 q, float4 b, float best) {
+__device__ __forceinline__ bool chunk_may_beat(const FpDev& fp, float4 q, float4 b, float best,
+                                               float mg) {
   const float dx = b.x - q.x, dy = b.y - q.y;
   const float bx = fmaf(q.z, dx, q.w * dy), by = fmaf(q.z, dy, -(q.w * dx));
   const float ac = fabsf(q.z), as = fabsf(q.w);
@@ -426,7 +505,7 @@ __device__ __forceinline__ bool chunk_may_beat(const FpDev& fp, float4 q, float4
     const float ay = fmaxf(fabsf(by - fp.cover[j][1]) - (fp.cover[j][3] + ey), 0.f);
     d2 = fminf(d2, fmaf(ax, ax, ay * ay));
   }
-  const float lim = best + kCullMargin;
+  const float lim = best + mg;
   if (d2 == 0.f) {  // touches the cover: every point is at least as shallow as the AABB allows
     const float lx = fmaxf(fp.aabb[0] - (bx + ex), (bx - ex) - fp.aabb[1]);
     const float ly = fmaxf(fp.aabb[2] - (by + ey), (by - ey) - fp.aabb[3]);
@@ -517,10 +596,12 @@ __global__ void __launch_bounds__(1024) k_cloud_prep(const double* __restrict__ 
     }
     GridMeta g;
     g.n_valid = cnt;
-    g.reserved = 0;
+    g.margin = kCullMargin;
     if (cnt == 0) {
       g.x0 = g.y0 = 0.0f; g.cs = 1.0f; g.inv_cs = 1.0f; g.gx = g.gy = 1;
     } else {
+      // cull slack: covers the FP32 rounding of every bound (coordinates recentred at q0)
+      g.margin += 5e-7f * fmaxf(fmaxf(fabsf(mnx), fabsf(mxx)), fmaxf(fabsf(mny), fabsf(mxy)));
       const float ex = mxx - mnx, ey = mxy - mny;
       // Cell edge: about pts_per_cell points per cell on average, within [cs_lo, cs_hi] (dense
       // boundary clouds get finer cells, sparse ones coarser), at most kGridMax per axis.
@@ -781,22 +862,22 @@ __device__ __forceinline__ void ring_cell(int k, int t, int ci, int cj, int& i, 
 struct WBox {
   float x0, x1, y0, y1;
 };
-__device__ __forceinline__ WBox world_box(const FpDev& fp, float4 q) {
+__device__ __forceinline__ WBox world_box(const FpDev& fp, float4 q, float mg) {
   const float cx = 0.5f * (fp.aabb[0] + fp.aabb[1]), cy = 0.5f * (fp.aabb[2] + fp.aabb[3]);
   const float hx = 0.5f * (fp.aabb[1] - fp.aabb[0]), hy = 0.5f * (fp.aabb[3] - fp.aabb[2]);
   const float ac = fabsf(q.z), as = fabsf(q.w);
-  const float wx = fmaf(ac, hx, as * hy) + kCullMargin, wy = fmaf(as, hx, ac * hy) + kCullMargin;
+  const float wx = fmaf(ac, hx, as * hy) + mg, wy = fmaf(as, hx, ac * hy) + mg;
   const float ox = q.x + fmaf(q.z, cx, -(q.w * cy)), oy = q.y + fmaf(q.w, cx, q.z * cy);
   return {ox - wx, ox + wx, oy - wy, oy + wy};
 }
 // d2 = squared distance from W to the box [bx0,bx1]x[by0,by1] (0 if they overlap); may the box
 // contain a point that beats `best`?
 __device__ __forceinline__ bool box_may_beat(const WBox& w, float bx0, float bx1, float by0,
-                                             float by1, float best) {
+                                             float by1, float best, float mg) {
   const float gx = fmaxf(fmaxf(bx0 - w.x1, w.x0 - bx1), 0.f);
   const float gy = fmaxf(fmaxf(by0 - w.y1, w.y0 - by1), 0.f);
   const float d2 = fmaf(gx, gx, gy * gy);
-  const float lim = best + kCullMargin;
+  const float lim = best + mg;
   return d2 == 0.f || (lim > 0.f && d2 < lim * lim);
 }
 
@@ -807,7 +888,11 @@ __device__ __forceinline__ bool box_may_beat(const WBox& w, float bx0, float bx1
 // distance to W and the distance to the body-frame AABB, then the exact polygon/cover SDF.
 // STATS (profiling builds of the launch only): count the point tests and exact SDF
 // evaluations the culls let through, for the executed-work roofline.
-template <int KIND, int NB, bool STATS = false, bool CHUNKS = true>
+// MODE: kGridFull (every bound), kGridNoChunk (no chunk bound: A/B only), kGridBrute (no bound
+// at all: every valid point is evaluated, the same arithmetic without culling — the reference
+// the exactness tests compare the culled minimum with, bit for bit).
+constexpr int kGridNoChunk = 0, kGridFull = 1, kGridBrute = 2;
+template <int KIND, int NB, bool STATS = false, int MODE = kGridFull>
 __global__ void __launch_bounds__(128) k_sdf_grid(const __grid_constant__ FpDev fp,
                                                   const float4* __restrict__ poses, int n_poses,
                                                   const GridMeta* __restrict__ gmp,
@@ -836,8 +921,9 @@ __global__ void __launch_bounds__(128) k_sdf_grid(const __grid_constant__ FpDev 
   const float cx = sx / na, cy = sy / na;
   const int ci = min(gm.gx - 1, max(0, static_cast<int>(floorf((cx - gm.x0) * gm.inv_cs))));
   const int cj = min(gm.gy - 1, max(0, static_cast<int>(floorf((cy - gm.y0) * gm.inv_cs))));
-  const WBox w = world_box(fp, q);
-  const float R = fp.radius + kCullMargin;
+  const float mg = gm.margin;
+  const WBox w = world_box(fp, q, mg);
+  const float R = fp.radius + mg;
   float best = __int_as_float(0x7f800000);
   const int kmax = max(max(ci, gm.gx - 1 - ci), max(cj, gm.gy - 1 - cj));
   for (int k = 0; k <= kmax; ++k) {
@@ -847,10 +933,12 @@ __global__ void __launch_bounds__(128) k_sdf_grid(const __grid_constant__ FpDev 
       const float bx1 = gm.x0 + static_cast<float>(ci + k) * gm.cs;
       const float by0 = gm.y0 + static_cast<float>(cj - k + 1) * gm.cs;
       const float by1 = gm.y0 + static_cast<float>(cj + k) * gm.cs;
+      // lbc: sd >= |o - t| - R holds inside the footprint too (|p| + depth <= R), so it bounds
+      // negative minima; lbw (distance from W to the outside of S) only when W lies inside S
       const float lbw = fminf(fminf(w.x0 - bx0, bx1 - w.x1), fminf(w.y0 - by0, by1 - w.y1));
       const float lbc = fminf(fminf(q.x - bx0, bx1 - q.x), fminf(q.y - by0, by1 - q.y)) - R;
-      const float lb = fmaxf(fmaxf(lbw, lbc), 0.f);
-      const bool need = active && lb < best + kCullMargin;
+      const float lb = lbw > 0.f ? fmaxf(lbw, lbc) : lbc;
+      const bool need = active && (MODE == kGridBrute || lb < best + mg);
       if (!__any_sync(kFull, need)) break;
     }
     const int ncell = k == 0 ? 1 : 8 * k;
@@ -866,16 +954,16 @@ __global__ void __launch_bounds__(128) k_sdf_grid(const __grid_constant__ FpDev 
       const float gx_ = fmaxf(fmaxf(bx0 - q.x, q.x - bx1), 0.f);
       const float gy_ = fmaxf(fmaxf(by0 - q.y, q.y - by1), 0.f);
       const float lim = R + best;
-      const bool need = active && (gx_ * gx_ + gy_ * gy_ < lim * lim) &&
-                        box_may_beat(w, bx0, bx1, by0, by1, best);
+      const bool need = active && (MODE == kGridBrute || ((gx_ * gx_ + gy_ * gy_ < lim * lim) &&
+                                   box_may_beat(w, bx0, bx1, by0, by1, best, mg)));
       if (!__any_sync(kFull, need)) continue;
       float l2 = lim * lim;
       // chunks of kChunk Morton-ordered points: one body-frame box bound per chunk, then the
       // per-point bounds and the exact SDF for the points of the chunks some lane still needs
       for (int ch = s / kChunk; ch < e / kChunk; ++ch) {
         bool cneed = need;
-        if (CHUNKS) {
-          cneed = need && chunk_may_beat(fp, q, __ldg(chunk + ch), best);
+        if (MODE == kGridFull) {
+          cneed = need && chunk_may_beat(fp, q, __ldg(chunk + ch), best, mg);
           if (!__any_sync(kFull, cneed)) continue;
         }
         const float2* cp = cloud + ch * kChunk;
@@ -884,14 +972,14 @@ __global__ void __launch_bounds__(128) k_sdf_grid(const __grid_constant__ FpDev 
           const float2 o = __ldg(cp + p);
           const float dx = o.x - q.x, dy = o.y - q.y;
           if (STATS && cneed) ++n_test;
-          if (cneed && dx * dx + dy * dy < l2) {  // false for the NaN pads
+          if (cneed && (MODE == kGridBrute ? o.x == o.x : dx * dx + dy * dy < l2)) {  // NaN pads
             const float bx = fmaf(q.z, dx, q.w * dy);
             const float by = fmaf(q.z, dy, -(q.w * dx));
             // polygons: the cover bound (exact for rectilinear shapes: the L's notch is culled);
             // rectangle covers: the AABB pre-test (the exact SDF costs about as much as a cover)
-            if (KIND == EXM_FOOTPRINT_POLYGON
-                    ? cover_may_beat(fp, bx, by, best)
-                    : aabb_may_beat(fp, bx, by, best)) {
+            if (MODE == kGridBrute ||
+                (KIND == EXM_FOOTPRINT_POLYGON ? cover_may_beat(fp, bx, by, best, mg)
+                                               : aabb_may_beat(fp, bx, by, best, mg))) {
               if (STATS) ++n_eval;
               best = fminf(best, sd_body<KIND, NB>(fp, bx, by));
               const float nl = R + best;
@@ -931,7 +1019,8 @@ __global__ void __launch_bounds__(128) k_sdf_grid_warp(const __grid_constant__ F
   const float4 q = poses[w];
   const int ci = min(gm.gx - 1, max(0, static_cast<int>(floorf((q.x - gm.x0) * gm.inv_cs))));
   const int cj = min(gm.gy - 1, max(0, static_cast<int>(floorf((q.y - gm.y0) * gm.inv_cs))));
-  const float R = fp.radius + kCullMargin;
+  const float mg = gm.margin;
+  const float R = fp.radius + mg;
   float best = __int_as_float(0x7f800000);
   const int kmax = max(max(ci, gm.gx - 1 - ci), max(cj, gm.gy - 1 - cj));
   for (int k = 0; k <= kmax; ++k) {
@@ -988,7 +1077,7 @@ __global__ void __launch_bounds__(128) k_sdf_grid_warp(const __grid_constant__ F
           if (dx * dx + dy * dy < l2 * l2) {
             const float bx = fmaf(q.z, dx, q.w * dy);
             const float by = fmaf(q.z, dy, -(q.w * dx));
-            if (aabb_may_beat(fp, bx, by, mine)) mine = fminf(mine, sd_body<KIND, NB>(fp, bx, by));
+            if (aabb_may_beat(fp, bx, by, mine, mg)) mine = fminf(mine, sd_body<KIND, NB>(fp, bx, by));
           }
         }
       }
@@ -1291,44 +1380,6 @@ __global__ void __launch_bounds__(kPairThreads) k_sdf_pairs(
   }
 }
 
-// ---- packed FP32x2 (sm_100 FFMA2/FADD2/FMUL2) helpers ---------------------------------
-typedef unsigned long long u64;
-__device__ __forceinline__ u64 pk(float a, float b) {
-  u64 r;
-  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
-  return r;
-}
-__device__ __forceinline__ float lo(u64 v) {
-  return __uint_as_float(static_cast<unsigned>(v));
-}
-__device__ __forceinline__ float hi(u64 v) {
-  return __uint_as_float(static_cast<unsigned>(v >> 32));
-}
-__device__ __forceinline__ u64 bc(float x) { return pk(x, x); }
-__device__ __forceinline__ u64 fma2(u64 a, u64 b, u64 c) {
-  u64 r;
-  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
-  return r;
-}
-__device__ __forceinline__ u64 mul2(u64 a, u64 b) {
-  u64 r;
-  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
-  return r;
-}
-__device__ __forceinline__ u64 sub2(u64 a, u64 b) {
-  u64 r;
-  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
-  return r;
-}
-__device__ __forceinline__ unsigned sgn_lo(u64 v) { return __float_as_uint(lo(v)); }
-__device__ __forceinline__ unsigned sgn_hi(u64 v) { return __float_as_uint(hi(v)); }
-
-__device__ __forceinline__ float min3f(float a, float b, float c) {
-  float r;
-  asm("min.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));  // FMNMX3
-  return r;
-}
-
 // One polygon edge against two body-frame points packed in f32x2 lanes (same arithmetic as
 // poly_edge, two pairs per FFMA2/FADD2/FMUL2). Per pair: 8 FP32 ops for the distance, 2 for
 // the crossing product (CROSS), the clamp as scalar FFMA.SAT (no .sat form of FFMA2).
@@ -1531,10 +1582,12 @@ cudaError_t dispatch_fp(const FpDev& fp, Args&&... args) {
   }
 }
 
-// EXM_GRID_CHUNKS=0 disables the chunk bound (A/B measurements only; same results).
-inline bool grid_chunks() {
-  static const bool on = !(getenv("EXM_GRID_CHUNKS") && atoi(getenv("EXM_GRID_CHUNKS")) == 0);
-  return on;
+// EXM_GRID_MODE (tests and A/B measurements; read at every launch, so at graph capture):
+//   "brute" every valid point evaluated (exactness reference), "nochunk" no chunk bound,
+//   "thread" / "warp" force the thread- or warp-per-pose kernel. Default: automatic.
+inline const char* grid_mode() {
+  const char* m = getenv("EXM_GRID_MODE");
+  return m ? m : "";
 }
 
 template <int KIND, int NB>
@@ -1543,12 +1596,16 @@ struct GridLaunch {
                          float* out, cudaStream_t s) {
     if (n_poses <= 0) return cudaSuccess;
     const int threads = 128, blocks = (n_poses + threads - 1) / threads;
-    if (grid_chunks())
+    const char* m = grid_mode();
+    if (!strcmp(m, "brute"))
+      k_sdf_grid<KIND, NB, false, kGridBrute><<<blocks, threads, 0, s>>>(
+          fp, poses, n_poses, g.gm, g.cell_start, g.cloud, g.chunk, out);
+    else if (!strcmp(m, "nochunk"))
+      k_sdf_grid<KIND, NB, false, kGridNoChunk><<<blocks, threads, 0, s>>>(
+          fp, poses, n_poses, g.gm, g.cell_start, g.cloud, g.chunk, out);
+    else
       k_sdf_grid<KIND, NB><<<blocks, threads, 0, s>>>(fp, poses, n_poses, g.gm, g.cell_start,
                                                       g.cloud, g.chunk, out);
-    else
-      k_sdf_grid<KIND, NB, false, false><<<blocks, threads, 0, s>>>(
-          fp, poses, n_poses, g.gm, g.cell_start, g.cloud, g.chunk, out);
     return cudaGetLastError();
   }
 };
@@ -1559,12 +1616,12 @@ struct GridStatsLaunch {
                          float* out, unsigned long long* stats, cudaStream_t s) {
     if (n_poses <= 0) return cudaSuccess;
     const int threads = 128, blocks = (n_poses + threads - 1) / threads;
-    if (grid_chunks())
+    if (!strcmp(grid_mode(), "nochunk"))
+      k_sdf_grid<KIND, NB, true, kGridNoChunk><<<blocks, threads, 0, s>>>(
+          fp, poses, n_poses, g.gm, g.cell_start, g.cloud, g.chunk, out, stats);
+    else
       k_sdf_grid<KIND, NB, true><<<blocks, threads, 0, s>>>(fp, poses, n_poses, g.gm,
                                                             g.cell_start, g.cloud, g.chunk, out, stats);
-    else
-      k_sdf_grid<KIND, NB, true, false><<<blocks, threads, 0, s>>>(
-          fp, poses, n_poses, g.gm, g.cell_start, g.cloud, g.chunk, out, stats);
     return cudaGetLastError();
   }
 };
@@ -1621,10 +1678,8 @@ cudaError_t launch_cloud_prep(const double* pts, const uint8_t* mask, const Step
   }
   // Cells sized for about kPtsPerCell points, between R/4 and kCellMaxR * R: a cull disc of
   // radius R + d covers ~(2(R+d)/cs)^2 cells; the chunk bounds cull inside a cell.
-  static const float ppc = getenv("EXM_PTS_PER_CELL") ? atof(getenv("EXM_PTS_PER_CELL")) : kPtsPerCell;
-  static const float cmax = getenv("EXM_CELL_MAX_R") ? atof(getenv("EXM_CELL_MAX_R")) : kCellMaxR;
   const float r = fmaxf(radius, 0.04f);
-  k_cloud_prep<<<1, 1024, smem, s>>>(pts, mask, dyn, 0.25f * r, cmax * r, ppc, r, g.dstat, g.tmp,
+  k_cloud_prep<<<1, 1024, smem, s>>>(pts, mask, dyn, 0.25f * r, kCellMaxR * r, kPtsPerCell, r, g.dstat, g.tmp,
                                      g.raw, g.raw_start, g.cell_start, g.gm);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
@@ -1690,8 +1745,10 @@ cudaError_t launch_stage_costs(const StepConst& sc, const StepDyn* dyn, const do
 cudaError_t launch_sdf_grid(const FpDev& fp, const float4* poses, int n_poses,
                             const CloudGrid& g, float* out, cudaStream_t s) {
   // Few poses (validation rollout, single queries): one warp per pose keeps all lanes busy.
-  static const int warp_max = getenv("EXM_WARP_MAX") ? atoi(getenv("EXM_WARP_MAX")) : kWarpPerPoseMax;
-  if (n_poses <= warp_max) return dispatch_fp<GridWarpLaunch>(fp, poses, n_poses, g, out, s);
+  const char* m = grid_mode();
+  const bool warp = !strcmp(m, "warp") ||
+                    (n_poses <= kWarpPerPoseMax && strcmp(m, "thread") && strcmp(m, "brute"));
+  if (warp) return dispatch_fp<GridWarpLaunch>(fp, poses, n_poses, g, out, s);
   return dispatch_fp<GridLaunch>(fp, poses, n_poses, g, out, s);
 }
 
