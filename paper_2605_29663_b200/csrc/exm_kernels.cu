@@ -977,7 +977,8 @@ __global__ void __launch_bounds__(128) k_sdf_grid(const __grid_constant__ FpDev 
             const float by = fmaf(q.z, dy, -(q.w * dx));
             // polygons: the cover bound (exact for rectilinear shapes: the L's notch is culled);
             // rectangle covers: the AABB pre-test (the exact SDF costs about as much as a cover)
-            if (MODE == kGridBrute ||
+            // (rectangle covers of <= 3 boxes: the exact SDF is hardly dearer than a bound)
+            if (MODE == kGridBrute || (KIND != EXM_FOOTPRINT_POLYGON && NB > 0 && NB <= 3) ||
                 (KIND == EXM_FOOTPRINT_POLYGON ? cover_may_beat(fp, bx, by, best, mg)
                                                : aabb_may_beat(fp, bx, by, best, mg))) {
               if (STATS) ++n_eval;
