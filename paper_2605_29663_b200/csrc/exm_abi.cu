@@ -560,10 +560,10 @@ exm_status enqueue_pre(exm_handle* h, bool draw_noise, cudaStream_t s, int* laun
 
 exm_status enqueue_post(exm_handle* h, cudaStream_t s, int* launches) {
   const StepConst& sc = h->sc;
-  EXM_CUDA(launch_stage_costs(sc, h->d_dyn, h->d_guide, h->guide_cap, h->d_xy, h->d_dmin,
-                              h->d_stage, h->d_flags, h->grid.dstat, s));
-  EXM_CUDA(launch_block_partials(sc, h->d_base, h->d_stage, h->d_flags, h->d_eps, h->d_partials,
-                                 nullptr, nullptr, s));
+  // per-rollout cost / unsafe flag in the first K entries of d_stage / d_flags
+  EXM_CUDA(launch_rollout_costs(sc, h->d_dyn, h->d_guide, h->guide_cap, h->d_base, h->d_xy,
+                                h->d_dmin, h->d_stage, h->d_flags, h->grid.dstat, s));
+  EXM_CUDA(launch_block_partials(sc, h->d_stage, h->d_flags, h->d_eps, h->d_partials, s));
   if (h->world > 1) {
     const size_t count = static_cast<size_t>(sc.nblocks_local) * partial_stride(sc.T, sc.D);
     const int rc = g_nccl.allgather(h->d_partials + static_cast<size_t>(sc.block_offset) *
@@ -1000,10 +1000,8 @@ exm_status exm_evaluate_rollouts(exm_handle* h, const double q0[3], const double
                           controls_out ? h->d_controls : nullptr,
                           states_out ? h->d_states : nullptr, s));
   EXM_CUDA(launch_sdf_grid(h->fp, h->d_poses, static_cast<int>(KT), h->grid, h->d_dmin, s));
-  EXM_CUDA(launch_stage_costs(sc, h->d_dyn, h->d_guide, h->guide_cap, h->d_xy, h->d_dmin,
-                              h->d_stage, h->d_flags, h->grid.dstat, s));
-  EXM_CUDA(launch_block_partials(sc, h->d_base, h->d_stage, h->d_flags, h->d_eps, nullptr,
-                                 h->d_cost, h->d_unsafe, s));
+  EXM_CUDA(launch_rollout_costs(sc, h->d_dyn, h->d_guide, h->guide_cap, h->d_base, h->d_xy,
+                                h->d_dmin, h->d_cost, h->d_unsafe, h->grid.dstat, s));
   if (controls_out)
     EXM_CUDA(cudaMemcpyAsync(controls_out, h->d_controls, KT * h->D * sizeof(double), cudaMemcpyDeviceToHost, s));
   if (states_out)

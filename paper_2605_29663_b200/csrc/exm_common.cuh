@@ -122,13 +122,12 @@ cudaError_t launch_sdf_grid(const FpDev& fp, const float4* poses, int n_poses,
 cudaError_t launch_sdf_grid_stats(const FpDev& fp, const float4* poses, int n_poses,
                                   const CloudGrid& g, float* out, unsigned long long* stats,
                                   cudaStream_t s);
-cudaError_t launch_stage_costs(const StepConst& sc, const StepDyn* dyn, const double* guide,
-                               int guide_cap, const double2* xy, const float* dmin,
-                               double* stage, uint8_t* flags, float* dstat, cudaStream_t s);
-cudaError_t launch_block_partials(const StepConst& sc, const double* base_cost,
-                                  const double* stage, const uint8_t* flags, const double* eps,
-                                  double* partials, double* cost_out, uint8_t* unsafe_out,
-                                  cudaStream_t s);
+cudaError_t launch_rollout_costs(const StepConst& sc, const StepDyn* dyn, const double* guide,
+                                 int guide_cap, const double* base_cost, const double2* xy,
+                                 const float* dmin, double* cost, uint8_t* unsafe, float* dstat,
+                                 cudaStream_t s);
+cudaError_t launch_block_partials(const StepConst& sc, const double* cost, const uint8_t* unsafe,
+                                  const double* eps, double* partials, cudaStream_t s);
 cudaError_t launch_update(const StepConst& sc, const double* partials, const double* nominal,
                           const StepDyn* dyn, double* upd, float4* val_poses, double2* val_xy,
                           double* val_base, DecisionDev* dec, int merge, cudaStream_t s);

@@ -793,50 +793,61 @@ __global__ void __launch_bounds__(kRolloutWarps * 32) k_rollout(
   if ((threadIdx.x & 31) == 0) base_cost[r] = b;
 }
 
-// Task + obstacle cost and the unsafe flag of every (r, h), in parallel. Thread i = h*K + r
-// writes stage[h*K + r] (h-major, so the per-rollout sums in k_block_partials coalesce).
-__global__ void k_stage_costs(const StepConst sc, const StepDyn* __restrict__ dynp,
-                              const double* __restrict__ guide, const double2* __restrict__ xy,
-                              const float* __restrict__ dmin, double* __restrict__ stage,
-                              uint8_t* __restrict__ flags, float* __restrict__ dstat) {
+// Rollout cost J_r and unsafe flag chi_r (score_rollout, controller.cpp:151-171), one warp per
+// rollout: lanes take the task + obstacle cost (controller.cpp:98-118) of the pre-step states
+// h = lane, lane + 32, ...; a fixed xor-butterfly sums them (deterministic, ~1e-16 relative to
+// the reference's sequential order) and adds the control + terminal part from k_rollout.
+// Also accumulates the search-radius statistic of the next step's cell size (k_cloud_prep).
+constexpr int kCostWarps = 8;
+__global__ void __launch_bounds__(kCostWarps * 32) k_rollout_costs(
+    const StepConst sc, const StepDyn* __restrict__ dynp, const double* __restrict__ guide,
+    const double* __restrict__ base_cost, const double2* __restrict__ xy,
+    const float* __restrict__ dmin, double* __restrict__ cost, uint8_t* __restrict__ unsafe,
+    float* __restrict__ dstat) {
   extern __shared__ double g[];
+  __shared__ float red[2][kCostWarps];
   const int ng = dynp->n_guide;
   for (int i = threadIdx.x; i < 2 * ng; i += blockDim.x) g[i] = guide[i];
   __syncthreads();
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  const bool live = i < sc.k_local * sc.T;
-  float dc = 0.f;
-  if (live) {
-    const int h = i / sc.k_local, r = i % sc.k_local;
-    const size_t src = static_cast<size_t>(r) * sc.T + h;
-    const double d = static_cast<double>(dmin[src]);
-    stage[i] = stage_cost(sc, xy[src], d, g, ng, dynp->goal);
-    flags[i] = d < sc.d_safe ? 1 : 0;
-    dc = fminf(fmaxf(dmin[src], 0.f), kDstatClamp);
-  }
-  // search-radius statistic for the next step's cell size (k_cloud_prep): one atomic pair
-  // per block
-  __shared__ float red[2][8];
-  float cnt = live ? 1.f : 0.f;
-  for (int o = 16; o; o >>= 1) {
-    dc += __shfl_xor_sync(kFull, dc, o);
-    cnt += __shfl_xor_sync(kFull, cnt, o);
-  }
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int r = blockIdx.x * kCostWarps + warp;
+  const bool live = r < sc.k_local;  // warp-uniform
+  double J = 0.0;
+  float dc = 0.f;
+  bool bad = false;
+  if (live) {
+    const size_t row = static_cast<size_t>(r) * sc.T;
+    for (int h = lane; h < sc.T; h += 32) {
+      const float df = dmin[row + h];
+      const double d = static_cast<double>(df);
+      J += stage_cost(sc, xy[row + h], d, g, ng, dynp->goal);
+      bad |= d < sc.d_safe;
+      dc += fminf(fmaxf(df, 0.f), kDstatClamp);
+    }
+  }
+  for (int o = 16; o; o >>= 1) {
+    J += __shfl_xor_sync(kFull, J, o);
+    dc += __shfl_xor_sync(kFull, dc, o);
+  }
+  bad = __any_sync(kFull, bad);
   if (lane == 0) {
-    red[0][warp] = dc;
-    red[1][warp] = cnt;
+    if (live) {
+      cost[r] = base_cost[r] + J;
+      unsafe[r] = bad ? 1 : 0;
+    }
+    red[0][warp] = live ? dc : 0.f;
+    red[1][warp] = live ? static_cast<float>(sc.T) : 0.f;
   }
   __syncthreads();
-  if (threadIdx.x == 0) {
-    float a = 0.f, b = 0.f;
-    for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) {
+  if (threadIdx.x == 0) {  // one atomic pair per block
+    float a = 0.f, c = 0.f;
+    for (int w = 0; w < kCostWarps; ++w) {
       a += red[0][w];
-      b += red[1][w];
+      c += red[1][w];
     }
-    if (b > 0.f) {
+    if (c > 0.f) {
       atomicAdd(dstat, a);
-      atomicAdd(dstat + 1, b);
+      atomicAdd(dstat + 1, c);
     }
   }
 }
@@ -1091,14 +1102,11 @@ __global__ void __launch_bounds__(128) k_sdf_grid_warp(const __grid_constant__ F
 
 // Augmented cost and the min-shifted softmax partial of one block of kBlockRollouts rollouts
 // (fixed block size and fixed reduction trees: deterministic and independent of sharding).
-//   J_r = (ctrl + terminal)_r + sum_h stage[h][r]       controller.cpp:164-171
 //   Jt_r = J_r + w_inf * unsafe_r                       controller.cpp:310-312
 //   {beta_b, S_b, A_b, argmin_b, U_b[T*D]}              controller.cpp:222-233, :316-328
 __global__ void __launch_bounds__(kPartialThreads) k_block_partials(
-    const StepConst sc, const double* __restrict__ base_cost, const double* __restrict__ stage,
-    const uint8_t* __restrict__ flags, const double* __restrict__ eps,
-    double* __restrict__ partials, double* __restrict__ cost_out,
-    uint8_t* __restrict__ unsafe_out) {
+    const StepConst sc, const double* __restrict__ cost, const uint8_t* __restrict__ unsafe,
+    const double* __restrict__ eps, double* __restrict__ partials) {
   extern __shared__ double s_u[];  // [kPartialThreads/32][T*D]
   __shared__ double s_e[kBlockRollouts];
   __shared__ double s_v[kBlockRollouts / 32];
@@ -1112,21 +1120,8 @@ __global__ void __launch_bounds__(kPartialThreads) k_block_partials(
   const int r = r0 + tid;
   const bool owner = tid < kBlockRollouts;
   const bool valid = owner && r < sc.k_local;
-  const int K = sc.k_local;
   double jt = HUGE_VAL;
-  if (valid) {
-    double J = base_cost[r];
-    unsigned bad = 0;
-#pragma unroll 10
-    for (int h = 0; h < sc.T; ++h) {
-      J += stage[static_cast<size_t>(h) * K + r];
-      bad |= flags[static_cast<size_t>(h) * K + r];
-    }
-    if (cost_out) cost_out[r] = J;
-    if (unsafe_out) unsafe_out[r] = bad ? 1 : 0;
-    jt = bad ? J + sc.w_inf : J;
-  }
-  if (!partials) return;
+  if (valid) jt = unsafe[r] ? cost[r] + sc.w_inf : cost[r];
   // argmin with first-index tie break (std::min_element)
   double v = jt;
   int vi = valid ? sc.r_offset + r : 0x7fffffff;
@@ -1728,18 +1723,19 @@ cudaError_t launch_sdf_grid_stats(const FpDev& fp, const float4* poses, int n_po
   return dispatch_fp<GridStatsLaunch>(fp, poses, n_poses, g, out, stats, s);
 }
 
-cudaError_t launch_stage_costs(const StepConst& sc, const StepDyn* dyn, const double* guide,
-                               int guide_cap, const double2* xy, const float* dmin,
-                               double* stage, uint8_t* flags, float* dstat, cudaStream_t s) {
-  const int n = sc.k_local * sc.T;
-  if (n <= 0) return cudaSuccess;
+cudaError_t launch_rollout_costs(const StepConst& sc, const StepDyn* dyn, const double* guide,
+                                 int guide_cap, const double* base_cost, const double2* xy,
+                                 const float* dmin, double* cost, uint8_t* unsafe, float* dstat,
+                                 cudaStream_t s) {
+  if (sc.k_local <= 0) return cudaSuccess;
   const size_t smem = sizeof(double) * 2 * static_cast<size_t>(guide_cap);
   if (smem > 48 * 1024) {
-    cudaError_t e = cudaFuncSetAttribute(k_stage_costs, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaError_t e = cudaFuncSetAttribute(k_rollout_costs, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(smem));
     if (e != cudaSuccess) return e;
   }
-  k_stage_costs<<<(n + 255) / 256, 256, smem, s>>>(sc, dyn, guide, xy, dmin, stage, flags, dstat);
+  k_rollout_costs<<<(sc.k_local + kCostWarps - 1) / kCostWarps, kCostWarps * 32, smem, s>>>(
+      sc, dyn, guide, base_cost, xy, dmin, cost, unsafe, dstat);
   return cudaGetLastError();
 }
 
@@ -1753,10 +1749,8 @@ cudaError_t launch_sdf_grid(const FpDev& fp, const float4* poses, int n_poses,
   return dispatch_fp<GridLaunch>(fp, poses, n_poses, g, out, s);
 }
 
-cudaError_t launch_block_partials(const StepConst& sc, const double* base_cost,
-                                  const double* stage, const uint8_t* flags, const double* eps,
-                                  double* partials, double* cost_out, uint8_t* unsafe_out,
-                                  cudaStream_t s) {
+cudaError_t launch_block_partials(const StepConst& sc, const double* cost, const uint8_t* unsafe,
+                                  const double* eps, double* partials, cudaStream_t s) {
   if (sc.nblocks_local <= 0) return cudaSuccess;
   const size_t smem = sizeof(double) * (kPartialThreads / 32) * static_cast<size_t>(sc.T) * sc.D;
   if (smem > 48 * 1024) {
@@ -1765,8 +1759,7 @@ cudaError_t launch_block_partials(const StepConst& sc, const double* base_cost,
                                          static_cast<int>(smem));
     if (e != cudaSuccess) return e;
   }
-  k_block_partials<<<sc.nblocks_local, kPartialThreads, smem, s>>>(
-      sc, base_cost, stage, flags, eps, partials, cost_out, unsafe_out);
+  k_block_partials<<<sc.nblocks_local, kPartialThreads, smem, s>>>(sc, cost, unsafe, eps, partials);
   return cudaGetLastError();
 }
 
