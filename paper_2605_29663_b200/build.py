@@ -8,9 +8,13 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "lib", "libexm_b200.so")
-SOURCES = ["exm_kernels.cu", "exm_abi.cu"]
+SOURCES = ["exm_kernels.cu", "exm_dynamics.cu", "exm_abi.cu"]
+HEADERS = ["exm_common.cuh", "exm_device.cuh"]
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo", "-O3", "-std=c++17",
-              "-Xcompiler", "-fPIC", "-Xcompiler", "-Wall", "-shared"]
+              "-Xcompiler", "-fPIC", "-Xcompiler", "-Wall"]
+# Per-unit flags: the FP64 dynamics round every product and sum separately, as the reference's
+# x86-64 build does (no FMA contraction); the FP32 signed-distance kernels fuse explicitly.
+UNIT_FLAGS = {"exm_dynamics.cu": ["-fmad=false"]}
 
 
 def _stale(target: str, deps) -> bool:
@@ -21,11 +25,22 @@ def _stale(target: str, deps) -> bool:
 
 
 def build_library(force: bool = False, verbose: bool = False) -> str:
-    deps = [os.path.join(CSRC, s) for s in SOURCES] + [
-        os.path.join(CSRC, "exm_common.cuh"), os.path.join(ROOT, "include", "exm_b200.h")]
+    deps = [os.path.join(CSRC, s) for s in SOURCES + HEADERS] + [
+        os.path.join(ROOT, "include", "exm_b200.h")]
     if force or _stale(LIB, deps):
-        os.makedirs(os.path.dirname(LIB), exist_ok=True)
-        cmd = ["nvcc", *NVCC_FLAGS, "-o", LIB, *[os.path.join(CSRC, s) for s in SOURCES], "-ldl"]
+        objdir = os.path.join(os.path.dirname(LIB), "obj")
+        os.makedirs(objdir, exist_ok=True)
+        objs = []
+        for src in SOURCES:
+            obj = os.path.join(objdir, src.replace(".cu", ".o"))
+            cmd = ["nvcc", *NVCC_FLAGS, *UNIT_FLAGS.get(src, []), "-c", "-o", obj,
+                   os.path.join(CSRC, src)]
+            if verbose:
+                print(" ".join(cmd))
+            subprocess.run(cmd, check=True)
+            objs.append(obj)
+        cmd = ["nvcc", "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", LIB, *objs,
+               "-ldl"]
         if verbose:
             print(" ".join(cmd))
         subprocess.run(cmd, check=True)

@@ -452,8 +452,7 @@ struct exm_handle {
   double* d_eps = nullptr;
   float4* d_poses = nullptr;
   double2* d_xy = nullptr;
-  double* d_stage = nullptr;
-  uint8_t* d_flags = nullptr;
+  double* d_ctrl = nullptr;       // control cost per (r, h)
   double* d_base = nullptr;
   float* d_dmin = nullptr;
   double* d_partials = nullptr;
@@ -548,22 +547,17 @@ exm_status enqueue_prep(exm_handle* h, cudaStream_t s) {
 
 exm_status enqueue_pre(exm_handle* h, bool draw_noise, cudaStream_t s, int* launches) {
   const StepConst& sc = h->sc;
-  if (draw_noise) {
-    EXM_CUDA(launch_noise(sc, h->d_dyn, h->d_eps, s));
-    ++*launches;
-  }
-  EXM_CUDA(launch_rollout(sc, h->d_dyn, h->d_nominal, h->d_eps, h->d_poses, h->d_xy, h->d_base,
-                          nullptr, nullptr, s));
+  EXM_CUDA(launch_rollout(sc, h->d_dyn, h->d_nominal, h->d_eps, draw_noise ? 1 : 0, h->d_poses,
+                          h->d_xy, h->d_base, h->d_ctrl, nullptr, nullptr, s));
   ++*launches;
   return EXM_OK;
 }
 
 exm_status enqueue_post(exm_handle* h, cudaStream_t s, int* launches) {
   const StepConst& sc = h->sc;
-  // per-rollout cost / unsafe flag in the first K entries of d_stage / d_flags
-  EXM_CUDA(launch_rollout_costs(sc, h->d_dyn, h->d_guide, h->guide_cap, h->d_base, h->d_xy,
-                                h->d_dmin, h->d_stage, h->d_flags, h->grid.dstat, s));
-  EXM_CUDA(launch_block_partials(sc, h->d_stage, h->d_flags, h->d_eps, h->d_partials, s));
+  EXM_CUDA(launch_rollout_costs(sc, h->d_dyn, h->d_guide, h->guide_cap, h->d_base, h->d_ctrl,
+                                h->d_xy, h->d_dmin, h->d_cost, h->d_unsafe, h->grid.dstat, s));
+  EXM_CUDA(launch_block_partials(sc, h->d_cost, h->d_unsafe, h->d_eps, h->d_partials, s));
   if (h->world > 1) {
     const size_t count = static_cast<size_t>(sc.nblocks_local) * partial_stride(sc.T, sc.D);
     const int rc = g_nccl.allgather(h->d_partials + static_cast<size_t>(sc.block_offset) *
@@ -890,8 +884,9 @@ exm_status exm_create(const exm_footprint* footprint, const exm_model* model,
   EXM_CUDA_C(dalloc(&h->d_eps, KT * D));
   EXM_CUDA_C(dalloc(&h->d_poses, KT));
   EXM_CUDA_C(dalloc(&h->d_xy, KT));
-  EXM_CUDA_C(dalloc(&h->d_stage, KT));
-  EXM_CUDA_C(dalloc(&h->d_flags, KT));
+  EXM_CUDA_C(dalloc(&h->d_ctrl, KT));
+  EXM_CUDA_C(dalloc(&h->d_cost, static_cast<size_t>(h->K)));
+  EXM_CUDA_C(dalloc(&h->d_unsafe, static_cast<size_t>(h->K)));
   EXM_CUDA_C(dalloc(&h->d_base, static_cast<size_t>(h->K)));
   EXM_CUDA_C(dalloc(&h->d_dmin, KT));
   const size_t nblocks_max = (static_cast<size_t>(h->K) + kBlockRollouts - 1) / kBlockRollouts + 8;
@@ -899,7 +894,7 @@ exm_status exm_create(const exm_footprint* footprint, const exm_model* model,
   EXM_CUDA_C(dalloc(&h->d_upd, TD));
   EXM_CUDA_C(dalloc(&h->d_val_poses, static_cast<size_t>(h->T)));
   EXM_CUDA_C(dalloc(&h->d_val_xy, static_cast<size_t>(h->T)));
-  EXM_CUDA_C(dalloc(&h->d_val_base, 1));
+  EXM_CUDA_C(dalloc(&h->d_val_base, static_cast<size_t>(h->T) + 1));
   EXM_CUDA_C(dalloc(&h->d_val_dmin, static_cast<size_t>(h->T)));
   h->out_bytes = sizeof(DecisionDev) + sizeof(double) * (h->T + TD + 3);
   EXM_CUDA_C(dalloc(&h->d_out, h->out_bytes));
@@ -921,8 +916,8 @@ void exm_destroy(exm_handle* h) {
   destroy_graphs(h);
   if (h->comm && g_nccl.destroy) g_nccl.destroy(h->comm);
   if (h->borrowed_poses) h->d_poses = nullptr, h->d_dmin = nullptr;
-  void* dev[] = {h->d_in_block, h->d_grid_block, h->d_eps, h->d_poses, h->d_xy, h->d_stage,
-                 h->d_flags, h->d_val_xy, h->d_base, h->d_dmin,
+  void* dev[] = {h->d_in_block, h->d_grid_block, h->d_eps, h->d_poses, h->d_xy, h->d_ctrl,
+                 h->d_val_xy, h->d_base, h->d_dmin,
                  h->d_partials, h->d_upd, h->d_val_poses, h->d_val_base, h->d_val_dmin, h->d_out,
                  h->d_controls, h->d_states, h->d_cost, h->d_unsafe, h->sb_poses, h->sb_pts64,
                  h->sb_pts, h->sb_mask, h->sb_keys, h->sb_min, h->sb_pairs};
@@ -991,17 +986,15 @@ exm_status exm_evaluate_rollouts(exm_handle* h, const double q0[3], const double
   const size_t KT = static_cast<size_t>(h->K) * h->T;
   if (controls_out && !h->d_controls) EXM_CUDA(dalloc(&h->d_controls, KT * h->D));
   if (states_out && !h->d_states) EXM_CUDA(dalloc(&h->d_states, static_cast<size_t>(h->K) * (h->T + 1) * 3));
-  if (!h->d_cost) EXM_CUDA(dalloc(&h->d_cost, static_cast<size_t>(h->K)));
-  if (!h->d_unsafe) EXM_CUDA(dalloc(&h->d_unsafe, static_cast<size_t>(h->K)));
   cudaStream_t s = h->stream;
   const StepConst& sc = h->sc;
   EXM_CUDA(launch_cloud_prep(h->d_pts, h->d_mask, h->d_dyn, h->fp.radius, h->grid, s));
-  EXM_CUDA(launch_rollout(sc, h->d_dyn, h->d_nominal, h->d_eps, h->d_poses, h->d_xy, h->d_base,
-                          controls_out ? h->d_controls : nullptr,
+  EXM_CUDA(launch_rollout(sc, h->d_dyn, h->d_nominal, h->d_eps, 0, h->d_poses, h->d_xy, h->d_base,
+                          h->d_ctrl, controls_out ? h->d_controls : nullptr,
                           states_out ? h->d_states : nullptr, s));
   EXM_CUDA(launch_sdf_grid(h->fp, h->d_poses, static_cast<int>(KT), h->grid, h->d_dmin, s));
-  EXM_CUDA(launch_rollout_costs(sc, h->d_dyn, h->d_guide, h->guide_cap, h->d_base, h->d_xy,
-                                h->d_dmin, h->d_cost, h->d_unsafe, h->grid.dstat, s));
+  EXM_CUDA(launch_rollout_costs(sc, h->d_dyn, h->d_guide, h->guide_cap, h->d_base, h->d_ctrl,
+                                h->d_xy, h->d_dmin, h->d_cost, h->d_unsafe, h->grid.dstat, s));
   if (controls_out)
     EXM_CUDA(cudaMemcpyAsync(controls_out, h->d_controls, KT * h->D * sizeof(double), cudaMemcpyDeviceToHost, s));
   if (states_out)

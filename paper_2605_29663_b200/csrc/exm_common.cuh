@@ -114,20 +114,24 @@ inline __host__ __device__ int partial_stride(int T, int D) { return 4 + T * D; 
 cudaError_t launch_noise(const StepConst& sc, const StepDyn* dyn, double* eps, cudaStream_t s);
 cudaError_t launch_cloud_prep(const double* pts, const uint8_t* mask, const StepDyn* dyn,
                               float radius, const CloudGrid& g, cudaStream_t s);
+// draw != 0: the rollout kernel draws the device noise into eps; else eps is read (injected).
+// base_cost: terminal goal cost per rollout; ctrl_cost: control cost per (r, h).
 cudaError_t launch_rollout(const StepConst& sc, const StepDyn* dyn, const double* nominal,
-                           const double* eps, float4* poses, double2* xy, double* base_cost,
-                           double* controls_out, double* states_out, cudaStream_t s);
+                           double* eps, int draw, float4* poses, double2* xy, double* base_cost,
+                           double* ctrl_cost, double* controls_out, double* states_out,
+                           cudaStream_t s);
 cudaError_t launch_sdf_grid(const FpDev& fp, const float4* poses, int n_poses,
                             const CloudGrid& g, float* out, cudaStream_t s);
 cudaError_t launch_sdf_grid_stats(const FpDev& fp, const float4* poses, int n_poses,
                                   const CloudGrid& g, float* out, unsigned long long* stats,
                                   cudaStream_t s);
 cudaError_t launch_rollout_costs(const StepConst& sc, const StepDyn* dyn, const double* guide,
-                                 int guide_cap, const double* base_cost, const double2* xy,
-                                 const float* dmin, double* cost, uint8_t* unsafe, float* dstat,
-                                 cudaStream_t s);
+                                 int guide_cap, const double* base_cost, const double* ctrl_cost,
+                                 const double2* xy, const float* dmin, double* cost,
+                                 uint8_t* unsafe, float* dstat, cudaStream_t s);
 cudaError_t launch_block_partials(const StepConst& sc, const double* cost, const uint8_t* unsafe,
                                   const double* eps, double* partials, cudaStream_t s);
+// val_base: T + 1 doubles {terminal cost, control cost of every step} of the validation rollout
 cudaError_t launch_update(const StepConst& sc, const double* partials, const double* nominal,
                           const StepDyn* dyn, double* upd, float4* val_poses, double2* val_xy,
                           double* val_base, DecisionDev* dec, int merge, cudaStream_t s);

@@ -1,57 +1,20 @@
-// exm_kernels.cu — sm_100a kernels of the EXACT-MPPI rollout + exact signed-distance path.
+// exm_kernels.cu — sm_100a kernels of the cloud preparation and the exact signed distance.
 //
 // Kernel map (reference function each one replaces, proj/...):
-//   k_noise          sample_perturbations / gaussian_at      controller.cpp:78-96, rng.hpp:12-39
 //   k_cloud_prep     ObstacleSet masking, recentring at q0,  geometry.cpp:357-375 (mask, layout)
 //                    uniform-grid binning for exact culling
-//   k_rollout        score_rollout minus the SDF             controller.cpp:138-174,
-//                    (clamp, Euler step, task/ctrl cost)      kinematics.cpp:75-117
+//   k_cell_sort      in-cell Morton order, chunk boxes       (cull structure, no counterpart)
 //   k_sdf_grid       min_signed_distance_at over K*T poses   geometry.cpp:357-375, :260-296
-//   k_block_partials obstacle cost, unsafe flag, augmented  controller.cpp:160-166, :310-318
-//                    cost, min-shifted softmax partials       controller.cpp:222-233, :320-328
-//   k_update         partial merge, weighted update,         controller.cpp:314-340
-//                    sequential clamp, validation rollout     controller.cpp:254-282
-//   k_finalize       validation cost, command, shift / hold  controller.cpp:342-364
+//   k_sdf_grid_warp  the same, one warp per pose (few poses)
 //   k_sdf_pairs      batch_signed_distance (every pair)      geometry.cpp:298-318
+// The FP64 dynamics / cost / softmax kernels are in exm_dynamics.cu.
 //
-// Numerics: dynamics, costs and the softmax are FP64 (as the reference). The signed
-// distance inner loops are FP32 on coordinates recentred at q0 in FP64 before rounding
-// (SURVEY.md Appendix B).
-#include <cfloat>
-#include <cmath>
-#include <cstdint>
-#include <cstdlib>
-#include <cstring>
-
-#include "exm_common.cuh"
-
-#define EXM_FOOTPRINT_RECT_COVER 0
-#define EXM_FOOTPRINT_POLYGON 1
-#define EXM_MODEL_DIFF 0
-#define EXM_MODEL_ACKERMANN 1
-#define EXM_MODEL_OMNI 2
-#define EXM_MODEL_SPIN 3
-#define EXM_MODEL_PARALLEL 4
+// Numerics: the signed distance inner loops are FP32 on coordinates recentred at q0 in FP64
+// before rounding.
+#include "exm_device.cuh"
 
 namespace exm {
 namespace {
-
-constexpr double kPi = 3.14159265358979323846;
-constexpr unsigned kFull = 0xffffffffu;
-
-// ------------------------------------------------------------------ counter RNG (rng.hpp)
-__device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
-  x += 0x9E3779B97F4A7C15ull;
-  x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
-  x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
-  return x ^ (x >> 31);
-}
-__device__ __forceinline__ uint64_t hash_mix(uint64_t h, uint64_t v) {
-  return splitmix64(h ^ (v + 0x9E3779B97F4A7C15ull + (h << 6) + (h >> 2)));
-}
-__device__ __forceinline__ double unit_oc(uint64_t h) {  // (0, 1]
-  return static_cast<double>((h >> 11) + 1) * 0x1.0p-53;
-}
 
 // ---- TMA bulk copy (cp.async.bulk global -> shared, mbarrier completion) -------------
 __device__ __forceinline__ unsigned smem_u32(const void* p) {
@@ -81,232 +44,6 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
       "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
       "r"(parity)
       : "memory");
-}
-
-// ------------------------------------------------------------------ FP64 scalar helpers
-// std::min / std::max / std::clamp with libstdc++'s comparison order.
-__device__ __forceinline__ double mn(double a, double b) { return (b < a) ? b : a; }
-__device__ __forceinline__ double mx(double a, double b) { return (a < b) ? b : a; }
-__device__ __forceinline__ double clampd(double v, double lo, double hi) {
-  return (v < lo) ? lo : (hi < v) ? hi : v;
-}
-__device__ __forceinline__ double wrap_angle(double a) {  // geometry.cpp:17-23
-  const double tau = 2.0 * kPi;
-  a = fmod(a, tau);
-  if (a <= -kPi) a += tau;
-  if (a > kPi) a -= tau;
-  return a;
-}
-
-template <int TAG>
-__host__ __device__ constexpr int model_dim() {  // kinematics.cpp:14-26
-  return (TAG == EXM_MODEL_DIFF || TAG == EXM_MODEL_ACKERMANN) ? 2 : (TAG == EXM_MODEL_OMNI ? 3 : 1);
-}
-
-// clamp_control, kinematics.cpp:99-117 (model known at compile time: everything in registers)
-template <int TAG>
-__device__ __forceinline__ void clamp_control(const StepConst& sc, const double* u,
-                                              const double* prev, double* out) {
-#pragma unroll
-  for (int i = 0; i < model_dim<TAG>(); ++i) {
-    double lo = sc.vel_min[i], hi = sc.vel_max[i];
-    if (TAG == EXM_MODEL_ACKERMANN && i == 1) {
-      lo = mx(lo, -sc.steer_max);
-      hi = mn(hi, sc.steer_max);
-    }
-    const double v = clampd(u[i], lo, hi);
-    out[i] = clampd(v, prev[i] + sc.acc_min[i] * sc.dt, prev[i] + sc.acc_max[i] * sc.dt);
-  }
-}
-
-// derivative + step (kinematics.cpp:75-97) are heading_rate / xy_rate below.
-
-// project_on_polyline + task_cost, controller.cpp:50-66, :103-118
-__device__ double task_cost(const StepConst& sc, const double q[3], const double* g, int ng,
-                            const double* goal, bool terminal) {
-  const double dx = q[0] - goal[0], dy = q[1] - goal[1];
-  double cost = sc.w_goal_pos * (dx * dx + dy * dy);
-  if (terminal) {
-    const double e = wrap_angle(q[2] - goal[2]);
-    cost += sc.w_goal_head * e * e;
-  }
-  double best_d, best_p = 0.0;
-  if (ng == 1) {
-    const double ax = q[0] - g[0], ay = q[1] - g[1];
-    best_d = sqrt(ax * ax + ay * ay);
-  } else {
-    best_d = HUGE_VAL;
-    double arc = 0.0;
-    for (int i = 0; i + 1 < ng; ++i) {
-      const double ax = g[2 * i], ay = g[2 * i + 1];
-      const double sx = g[2 * i + 2] - ax, sy = g[2 * i + 3] - ay;
-      const double len = sqrt(sx * sx + sy * sy);
-      double t = 0.0;
-      if (len > 0.0) t = clampd(((q[0] - ax) * sx + (q[1] - ay) * sy) / (len * len), 0.0, 1.0);
-      const double ex = q[0] - (ax + t * sx), ey = q[1] - (ay + t * sy);
-      const double d = sqrt(ex * ex + ey * ey);
-      if (d < best_d) {
-        best_d = d;
-        best_p = arc + t * len;
-      }
-      arc += len;
-    }
-  }
-  cost += sc.w_xtrack * best_d * best_d;
-  cost -= sc.w_progress * best_p;
-  return cost;
-}
-
-__device__ __forceinline__ double terminal_cost(const StepConst& sc, const double q[3],
-                                                const double* goal) {  // controller.cpp:120-126
-  const double dx = q[0] - goal[0], dy = q[1] - goal[1];
-  const double e = wrap_angle(q[2] - goal[2]);
-  return sc.w_goal_pos * (dx * dx + dy * dy) + sc.w_goal_head * e * e;
-}
-
-template <int TAG>
-__device__ __forceinline__ double control_cost(const StepConst& sc, const double* u) {
-  double s = 0.0;
-#pragma unroll
-  for (int i = 0; i < model_dim<TAG>(); ++i) s += u[i] * u[i];
-  return sc.w_ctrl * s;
-}
-
-__device__ __forceinline__ double obstacle_cost(const StepConst& sc, double d) {  // :98-101
-  const double m = mx(sc.d_safe - d, 0.0);
-  return sc.w_coll * (d < 0.0 ? 1.0 : 0.0) + sc.w_rep * m * m;
-}
-
-// Serial part of one rollout (score_rollout, controller.cpp:151-169, minus the SDF and the
-// task cost): u = nominal + eps, sequential clamp from u_prev, Euler step. Emits the recentred
-// FP32 pose (x, y, cos, sin) and the FP64 position of every pre-step state; returns the
-// control cost summed over h plus the terminal goal cost. The per-step task cost is
-// independent across (r, h) and is computed in parallel by k_stage_costs.
-//
-// In all five models the heading rate depends on u only (kinematics.cpp:75-92), so the FP64
-// sincos of every heading can be taken off the serial chain (rollout_warp below) — the same
-// operations on the same values as the reference's step-by-step order.
-template <int TAG>
-__device__ __forceinline__ double heading_rate(const StepConst& sc, const double* u) {
-  if (TAG == EXM_MODEL_DIFF) return u[1];
-  if (TAG == EXM_MODEL_ACKERMANN) return u[0] / sc.wheelbase * tan(u[1]);
-  if (TAG == EXM_MODEL_OMNI) return u[2];
-  if (TAG == EXM_MODEL_SPIN) return u[0];
-  return 0.0;
-}
-
-template <int TAG>
-__device__ __forceinline__ void xy_rate(const double* u, double ct, double st, double& fx,
-                                        double& fy) {
-  fx = 0.0;
-  fy = 0.0;
-  if (TAG == EXM_MODEL_DIFF || TAG == EXM_MODEL_ACKERMANN) { fx = u[0] * ct; fy = u[0] * st; }
-  if (TAG == EXM_MODEL_OMNI) { fx = u[0] * ct - u[1] * st; fy = u[0] * st + u[1] * ct; }
-  if (TAG == EXM_MODEL_PARALLEL) { fx = -u[0] * st; fy = u[0] * ct; }
-}
-
-constexpr int kRolloutWarps = 4;  // rollouts (warps) per CTA in k_rollout
-constexpr float kPtsPerCell = 32.0f;
-constexpr float kCellMaxR = 0.5f;        // cell edge <= kCellMaxR * R ...
-constexpr float kCellSearchFrac = 0.385f;  // ... or <= this fraction of R + mean d_min
-constexpr float kDstatClamp = 16.0f;       // d_min clamp in that mean (empty clouds: 1e6)
-// Below this many poses one thread per pose leaves most SMs idle (< ~16 warps each): use one
-// warp per pose instead.
-constexpr int kWarpPerPoseMax = 65536;
-constexpr int kPartialThreads = 1024;  // 32 warps: 8 rollouts per warp in the U sums
-
-// Serial part of one rollout (score_rollout, controller.cpp:151-169, minus the SDF and the task
-// cost, which k_stage_costs computes in parallel over (r, h)), spread over one warp:
-//   1. lanes stage u = nominal + eps (coalesced)
-//   2. lane 0 runs the two serial recurrences that really are serial: the sequential clamp
-//      (kinematics.cpp:99-117) and the heading integration — cheap scalar FP64
-//   3. lanes take the FP64 sincos of every pre-step heading (the long-latency part) in parallel
-//   4. lane 0 integrates x, y and the control cost in the reference's step order
-//   5. lanes write poses / positions / controls / states (coalesced)
-// scratch: per-warp shared memory of rollout_warp_scratch(T, D) doubles. Returns the control
-// cost sum + terminal goal cost in lane 0.
-__host__ __device__ constexpr int rollout_warp_scratch(int T, int D) { return T * (D + 5); }
-
-template <int TAG>
-__device__ double rollout_warp(const StepConst& sc, const StepDyn& dyn, const double* nominal,
-                               const double* eps_row, float4* poses_row, double2* xy_row,
-                               double* controls_row, double* states_row, double* scratch) {
-  constexpr int D = model_dim<TAG>();
-  const int T = sc.T, lane = threadIdx.x & 31;
-  double* s_u = scratch;          // T*D controls (clamped in place)
-  double* s_th = s_u + T * D;     // T pre-step headings
-  double* s_c = s_th + T;         // T cos
-  double* s_s = s_c + T;          // T sin
-  double* s_x = s_s + T;          // T pre-step x
-  double* s_y = s_x + T;          // T pre-step y  (s_x..s_y: 2T; total T*(D+5))
-  for (int i = lane; i < T * D; i += 32) s_u[i] = nominal[i] + (eps_row ? eps_row[i] : 0.0);
-  __syncwarp();
-  double thT = 0.0;
-  if (lane == 0) {
-    double prev[3] = {dyn.u_prev[0], dyn.u_prev[1], dyn.u_prev[2]};
-    double th = dyn.q0[2];
-    for (int h = 0; h < T; ++h) {
-      double u[3] = {0.0, 0.0, 0.0}, uc[3] = {0.0, 0.0, 0.0};
-#pragma unroll
-      for (int c = 0; c < D; ++c) u[c] = s_u[h * D + c];
-      clamp_control<TAG>(sc, u, prev, uc);
-#pragma unroll
-      for (int c = 0; c < D; ++c) prev[c] = s_u[h * D + c] = uc[c];
-      s_th[h] = th;
-      th = th + heading_rate<TAG>(sc, uc) * sc.dt;
-    }
-    thT = th;
-  }
-  __syncwarp();
-  for (int h = lane; h < T; h += 32) sincos(s_th[h], &s_s[h], &s_c[h]);
-  __syncwarp();
-  double base = 0.0;
-  if (lane == 0) {
-    double x = dyn.q0[0], y = dyn.q0[1];
-    for (int h = 0; h < T; ++h) {
-      s_x[h] = x;
-      s_y[h] = y;
-      double uc[3] = {0.0, 0.0, 0.0};
-#pragma unroll
-      for (int c = 0; c < D; ++c) uc[c] = s_u[h * D + c];
-      base += control_cost<TAG>(sc, uc);
-      double fx, fy;
-      xy_rate<TAG>(uc, s_c[h], s_s[h], fx, fy);
-      x = x + fx * sc.dt;
-      y = y + fy * sc.dt;
-    }
-    const double qT[3] = {x, y, thT};
-    base += terminal_cost(sc, qT, dyn.goal);
-    if (states_row) {
-      states_row[3 * T] = x;
-      states_row[3 * T + 1] = y;
-      states_row[3 * T + 2] = thT;
-    }
-  }
-  __syncwarp();
-  const double qx0 = dyn.q0[0], qy0 = dyn.q0[1];
-  for (int h = lane; h < T; h += 32) {
-    poses_row[h] = make_float4(static_cast<float>(s_x[h] - qx0), static_cast<float>(s_y[h] - qy0),
-                               static_cast<float>(s_c[h]), static_cast<float>(s_s[h]));
-    xy_row[h] = make_double2(s_x[h], s_y[h]);
-    if (states_row) {
-      states_row[3 * h] = s_x[h];
-      states_row[3 * h + 1] = s_y[h];
-      states_row[3 * h + 2] = s_th[h];
-    }
-  }
-  if (controls_row)
-    for (int i = lane; i < T * D; i += 32) controls_row[i] = s_u[i];
-  __syncwarp();
-  return base;
-}
-
-// Running cost of one pre-step state: task_cost (controller.cpp:103-118, non-terminal) +
-// obstacle_cost (controller.cpp:98-101).
-__device__ __forceinline__ double stage_cost(const StepConst& sc, double2 xy, double d,
-                                             const double* g, int ng, const double* goal) {
-  const double q[3] = {xy.x, xy.y, 0.0};
-  return task_cost(sc, q, g, ng, goal, false) + obstacle_cost(sc, d);
 }
 
 // ---- packed FP32x2 (sm_100 FFMA2/FADD2/FMUL2) helpers ---------------------------------
@@ -524,23 +261,12 @@ __device__ __forceinline__ float unkey(unsigned k) {
 }
 
 // ------------------------------------------------------------------ kernels
-__global__ void k_noise(const StepConst sc, const StepDyn* __restrict__ dyn,
-                        double* __restrict__ eps) {
-  const int idx = blockIdx.x * blockDim.x + threadIdx.x;  // local (r, h)
-  if (idx >= sc.k_local * sc.T) return;
-  const int r = idx / sc.T, h = idx % sc.T;
-  const uint64_t rg = static_cast<uint64_t>(sc.r_offset + r);
-  const uint64_t k =
-      hash_mix(hash_mix(hash_mix(splitmix64(sc.seed), dyn->cycle), rg), static_cast<uint64_t>(h));
-  for (int c = 0; c < sc.D; ++c) {
-    const uint64_t kc = hash_mix(k, static_cast<uint64_t>(c));
-    const double u1 = unit_oc(hash_mix(kc, 0xD1B54A32D192ED03ull));
-    const double u2 = unit_oc(hash_mix(kc, 0x8CB92BA72F3D8DD7ull));
-    eps[static_cast<size_t>(idx) * sc.D + c] =
-        sc.sigma[c] * (sqrt(-2.0 * log(u1)) * cos(2.0 * kPi * u2));
-  }
-}
-
+constexpr float kPtsPerCell = 32.0f;
+constexpr float kCellMaxR = 0.5f;        // cell edge <= kCellMaxR * R ...
+constexpr float kCellSearchFrac = 0.385f;  // ... or <= this fraction of R + mean d_min
+// Below this many poses one thread per pose leaves most SMs idle (< ~16 warps each): use one
+// warp per pose instead.
+constexpr int kWarpPerPoseMax = 65536;
 // Single-CTA cloud preparation: mask compaction, FP64 recentring at q0 then FP32 rounding,
 // bounding box, uniform grid (cell >= cs_target, <= kGridMax per axis), counting sort.
 __global__ void __launch_bounds__(1024) k_cloud_prep(const double* __restrict__ pts,
@@ -764,91 +490,6 @@ __global__ void __launch_bounds__(kSortWarps * 32) k_cell_sort(
           make_float4(0.5f * (x0 + x1), 0.5f * (y0 + y1), 0.5f * (x1 - x0), 0.5f * (y1 - y0));
     }
     __syncwarp();
-  }
-}
-
-template <int TAG>
-__global__ void __launch_bounds__(kRolloutWarps * 32) k_rollout(
-    const StepConst sc, const StepDyn* __restrict__ dynp, const double* __restrict__ nominal,
-    const double* __restrict__ eps, float4* __restrict__ poses, double2* __restrict__ xy,
-    double* __restrict__ base_cost, double* __restrict__ controls_out,
-    double* __restrict__ states_out) {
-  // One warp per rollout (rollout_warp): the serial recurrences stay on one lane, the FP64
-  // transcendentals and all memory traffic are spread over the warp.
-  extern __shared__ double sm[];
-  const int TD = sc.T * sc.D;
-  double* nom = sm;
-  const int warp = threadIdx.x >> 5;
-  double* scratch = sm + TD + warp * rollout_warp_scratch(sc.T, sc.D);
-  for (int i = threadIdx.x; i < TD; i += blockDim.x) nom[i] = nominal[i];
-  const StepDyn dyn = *dynp;
-  __syncthreads();
-  const int r = blockIdx.x * kRolloutWarps + warp;
-  if (r >= sc.k_local) return;  // warp-uniform
-  const size_t row = static_cast<size_t>(r) * sc.T;
-  const double b = rollout_warp<TAG>(sc, dyn, nom, eps + row * sc.D, poses + row, xy + row,
-                                     controls_out ? controls_out + row * sc.D : nullptr,
-                                     states_out ? states_out + static_cast<size_t>(r) * (sc.T + 1) * 3 : nullptr,
-                                     scratch);
-  if ((threadIdx.x & 31) == 0) base_cost[r] = b;
-}
-
-// Rollout cost J_r and unsafe flag chi_r (score_rollout, controller.cpp:151-171), one warp per
-// rollout: lanes take the task + obstacle cost (controller.cpp:98-118) of the pre-step states
-// h = lane, lane + 32, ...; a fixed xor-butterfly sums them (deterministic, ~1e-16 relative to
-// the reference's sequential order) and adds the control + terminal part from k_rollout.
-// Also accumulates the search-radius statistic of the next step's cell size (k_cloud_prep).
-constexpr int kCostWarps = 8;
-__global__ void __launch_bounds__(kCostWarps * 32) k_rollout_costs(
-    const StepConst sc, const StepDyn* __restrict__ dynp, const double* __restrict__ guide,
-    const double* __restrict__ base_cost, const double2* __restrict__ xy,
-    const float* __restrict__ dmin, double* __restrict__ cost, uint8_t* __restrict__ unsafe,
-    float* __restrict__ dstat) {
-  extern __shared__ double g[];
-  __shared__ float red[2][kCostWarps];
-  const int ng = dynp->n_guide;
-  for (int i = threadIdx.x; i < 2 * ng; i += blockDim.x) g[i] = guide[i];
-  __syncthreads();
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int r = blockIdx.x * kCostWarps + warp;
-  const bool live = r < sc.k_local;  // warp-uniform
-  double J = 0.0;
-  float dc = 0.f;
-  bool bad = false;
-  if (live) {
-    const size_t row = static_cast<size_t>(r) * sc.T;
-    for (int h = lane; h < sc.T; h += 32) {
-      const float df = dmin[row + h];
-      const double d = static_cast<double>(df);
-      J += stage_cost(sc, xy[row + h], d, g, ng, dynp->goal);
-      bad |= d < sc.d_safe;
-      dc += fminf(fmaxf(df, 0.f), kDstatClamp);
-    }
-  }
-  for (int o = 16; o; o >>= 1) {
-    J += __shfl_xor_sync(kFull, J, o);
-    dc += __shfl_xor_sync(kFull, dc, o);
-  }
-  bad = __any_sync(kFull, bad);
-  if (lane == 0) {
-    if (live) {
-      cost[r] = base_cost[r] + J;
-      unsafe[r] = bad ? 1 : 0;
-    }
-    red[0][warp] = live ? dc : 0.f;
-    red[1][warp] = live ? static_cast<float>(sc.T) : 0.f;
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {  // one atomic pair per block
-    float a = 0.f, c = 0.f;
-    for (int w = 0; w < kCostWarps; ++w) {
-      a += red[0][w];
-      c += red[1][w];
-    }
-    if (c > 0.f) {
-      atomicAdd(dstat, a);
-      atomicAdd(dstat + 1, c);
-    }
   }
 }
 
@@ -1098,206 +739,6 @@ __global__ void __launch_bounds__(128) k_sdf_grid_warp(const __grid_constant__ F
     }
   }
   if (lane == 0) out[w] = best;
-}
-
-// Augmented cost and the min-shifted softmax partial of one block of kBlockRollouts rollouts
-// (fixed block size and fixed reduction trees: deterministic and independent of sharding).
-//   Jt_r = J_r + w_inf * unsafe_r                       controller.cpp:310-312
-//   {beta_b, S_b, A_b, argmin_b, U_b[T*D]}              controller.cpp:222-233, :316-328
-__global__ void __launch_bounds__(kPartialThreads) k_block_partials(
-    const StepConst sc, const double* __restrict__ cost, const uint8_t* __restrict__ unsafe,
-    const double* __restrict__ eps, double* __restrict__ partials) {
-  extern __shared__ double s_u[];  // [kPartialThreads/32][T*D]
-  __shared__ double s_e[kBlockRollouts];
-  __shared__ double s_v[kBlockRollouts / 32];
-  __shared__ double s_a[kBlockRollouts / 32];
-  __shared__ int s_i[kBlockRollouts / 32];
-  __shared__ double s_beta;
-  __shared__ int s_arg;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  constexpr int kWarps = kBlockRollouts / 32;  // warps owning one rollout per lane
-  const int r0 = blockIdx.x * kBlockRollouts;
-  const int r = r0 + tid;
-  const bool owner = tid < kBlockRollouts;
-  const bool valid = owner && r < sc.k_local;
-  double jt = HUGE_VAL;
-  if (valid) jt = unsafe[r] ? cost[r] + sc.w_inf : cost[r];
-  // argmin with first-index tie break (std::min_element)
-  double v = jt;
-  int vi = valid ? sc.r_offset + r : 0x7fffffff;
-  for (int o = 16; o; o >>= 1) {
-    const double ov = __shfl_xor_sync(kFull, v, o);
-    const int oi = __shfl_xor_sync(kFull, vi, o);
-    if (ov < v || (ov == v && oi < vi)) { v = ov; vi = oi; }
-  }
-  if (lane == 0 && owner) { s_v[warp] = v; s_i[warp] = vi; }
-  __syncthreads();
-  if (tid == 0) {
-    double b = s_v[0];
-    int bi = s_i[0];
-    for (int w = 1; w < kWarps; ++w)
-      if (s_v[w] < b || (s_v[w] == b && s_i[w] < bi)) { b = s_v[w]; bi = s_i[w]; }
-    s_beta = b;
-    s_arg = bi;
-  }
-  __syncthreads();
-  const double beta = s_beta;
-  const double z = valid ? (jt - beta) / sc.lambda : 0.0;
-  const double e = valid ? exp(-z) : 0.0;
-  const double a = valid ? e * z : 0.0;
-  if (owner) s_e[tid] = e;
-  double se = e, sa = a;
-  for (int o = 16; o; o >>= 1) {
-    se += __shfl_xor_sync(kFull, se, o);
-    sa += __shfl_xor_sync(kFull, sa, o);
-  }
-  __syncthreads();  // s_v/s_a reuse: the argmin values were consumed by thread 0 above
-  if (lane == 0 && owner) { s_v[warp] = se; s_a[warp] = sa; }
-  __syncthreads();
-  const int stride = partial_stride(sc.T, sc.D);
-  double* out = partials + static_cast<size_t>(sc.block_offset + blockIdx.x) * stride;
-  if (tid == 0) {
-    double S = 0.0, A = 0.0;
-    for (int w = 0; w < kWarps; ++w) { S += s_v[w]; A += s_a[w]; }
-    out[0] = beta;
-    out[1] = S;
-    out[2] = A;
-    out[3] = static_cast<double>(s_arg);
-  }
-  // U_b[o] = sum_r e_r eps[r][o]: each of the kPartialThreads/32 warps sums its slice of
-  // rollouts (lanes over o, coalesced rows), then the warp sums are added in warp order.
-  constexpr int kUWarps = kPartialThreads / 32;
-  constexpr int kPerWarp = kBlockRollouts / kUWarps;
-  const int TD = sc.T * sc.D;
-  const int nv = min(kBlockRollouts, sc.k_local - r0);
-  const int j0 = warp * kPerWarp, j1 = min(nv, j0 + kPerWarp);
-  for (int o = lane; o < TD; o += 32) {
-    double acc = 0.0;
-#pragma unroll
-    for (int j = j0; j < j1; ++j) acc += s_e[j] * eps[static_cast<size_t>(r0 + j) * TD + o];
-    s_u[warp * TD + o] = acc;
-  }
-  __syncthreads();
-  for (int o = tid; o < TD; o += blockDim.x) {
-    double acc = 0.0;
-    for (int w = 0; w < kUWarps; ++w) acc += s_u[w * TD + o];
-    out[4 + o] = acc;
-  }
-}
-
-// Merge all block partials in block order (every rank does this identically), apply the
-// weighted update u_h += U_h / S (controller.cpp:320-328), then one thread runs the sequential
-// clamp + validation dynamics (controller.cpp:331-340, :254-282).
-template <int TAG>
-__global__ void __launch_bounds__(256) k_update(const StepConst sc,
-                                                const double* __restrict__ partials,
-                                                const double* __restrict__ nominal,
-                                                const StepDyn* __restrict__ dynp,
-                                                double* __restrict__ upd,
-                                                float4* __restrict__ val_poses,
-                                                double2* __restrict__ val_xy,
-                                                double* __restrict__ val_base,
-                                                DecisionDev* __restrict__ dec, int merge) {
-  extern __shared__ double sm_u[];  // T*D updated controls, then nblocks_total factors
-  __shared__ double s_beta, s_S;
-  const int tid = threadIdx.x;
-  const int nb = sc.nblocks_total;
-  const int stride = partial_stride(sc.T, sc.D);
-  const int TD = sc.T * sc.D;
-  double* s_upd = sm_u;
-  double* sf = sm_u + TD;
-  if (merge) {
-    if (tid == 0) {
-      double beta = partials[0];
-      int arg = static_cast<int>(partials[3]);
-      for (int b = 1; b < nb; ++b) {
-        const double bb = partials[static_cast<size_t>(b) * stride];
-        if (bb < beta) { beta = bb; arg = static_cast<int>(partials[static_cast<size_t>(b) * stride + 3]); }
-      }
-      s_beta = beta;
-      dec->argmin = arg;
-      dec->best_cost = beta;
-    }
-    __syncthreads();
-    for (int b = tid; b < nb; b += blockDim.x)
-      sf[b] = exp(-(partials[static_cast<size_t>(b) * stride] - s_beta) / sc.lambda);
-    __syncthreads();
-    if (tid == 0) {
-      double S = 0.0, A = 0.0;
-      for (int b = 0; b < nb; ++b) {
-        const double* p = partials + static_cast<size_t>(b) * stride;
-        S += sf[b] * p[1];
-        A += sf[b] * (p[2] + p[1] * ((p[0] - s_beta) / sc.lambda));
-      }
-      s_S = S;
-      dec->entropy = A / S + log(S);
-    }
-    __syncthreads();
-    for (int o = tid; o < TD; o += blockDim.x) {
-      double U = 0.0;
-#pragma unroll 8
-      for (int b = 0; b < nb; ++b) U += sf[b] * partials[static_cast<size_t>(b) * stride + 4 + o];
-      s_upd[o] = nominal[o] + U / s_S;
-    }
-  } else {
-    for (int o = tid; o < TD; o += blockDim.x) s_upd[o] = nominal[o];
-  }
-  __syncthreads();
-  if (tid < 32) {
-    // warp 0 clamps sequentially from u_prev and writes the clamped sequence back; the
-    // reference's second clamp inside validate_nominal is idempotent on it.
-    const StepDyn dyn = *dynp;
-    const double b = rollout_warp<TAG>(sc, dyn, s_upd, nullptr, val_poses, val_xy, upd, nullptr,
-                                       sf + (merge ? nb : 0));
-    if (tid == 0) *val_base = b;
-  }
-}
-
-// Validation cost, validity, command and shift / zero-hold (controller.cpp:339-364).
-__global__ void __launch_bounds__(64) k_finalize(
-    const StepConst sc, const float* __restrict__ val_dmin, const double2* __restrict__ val_xy,
-    const double* __restrict__ val_base, const double* __restrict__ upd,
-    const double* __restrict__ guide, double* __restrict__ nominal, StepDyn* __restrict__ dyn,
-    DecisionDev* __restrict__ dec, double* __restrict__ out_dmin,
-    double* __restrict__ out_nominal, double* __restrict__ out_uprev, int commit) {
-  extern __shared__ double sm2[];  // guide (2*ng) then per-step costs (T)
-  __shared__ int s_ok;
-  const int tid = threadIdx.x;
-  const int T = sc.T, D = sc.D;
-  const int ng = dyn->n_guide;
-  double* g = sm2;
-  double* c = sm2 + 2 * ng;
-  for (int i = tid; i < 2 * ng; i += blockDim.x) g[i] = guide[i];
-  if (tid == 0) s_ok = 1;
-  __syncthreads();
-  for (int h = tid; h < T; h += blockDim.x) {
-    const double d = static_cast<double>(val_dmin[h]);
-    if (out_dmin) out_dmin[h] = d;
-    if (d < sc.d_safe) atomicAnd(&s_ok, 0);
-    c[h] = stage_cost(sc, val_xy[h], d, g, ng, dyn->goal);
-  }
-  __syncthreads();
-  const int ok = s_ok;
-  if (tid == 0) {
-    double J = *val_base;
-    for (int h = 0; h < T; ++h) J += c[h];
-    dec->nominal_cost = J;
-    dec->validated = ok;
-  }
-  if (!commit) return;
-  for (int i = tid; i < T * D; i += blockDim.x) {
-    const int h = i / D;
-    const double v = ok ? upd[(h + 1 < T ? h + 1 : T - 1) * D + i % D] : 0.0;
-    nominal[i] = v;
-    if (out_nominal) out_nominal[i] = v;
-  }
-  if (tid < 3) {
-    const double cmd = (ok && tid < D) ? upd[tid] : 0.0;
-    dec->command[tid] = cmd;
-    dyn->u_prev[tid] = cmd;
-    if (out_uprev) out_uprev[tid] = cmd;
-  }
-  if (tid == 0) dyn->cycle += 1;
 }
 
 __global__ void k_recentre(const double* __restrict__ pts, int n, double cx, double cy,
@@ -1656,13 +1097,6 @@ struct PairsLaunch {
 }  // namespace
 
 // ------------------------------------------------------------------ launchers
-cudaError_t launch_noise(const StepConst& sc, const StepDyn* dyn, double* eps, cudaStream_t s) {
-  const int n = sc.k_local * sc.T;
-  if (n <= 0) return cudaSuccess;
-  k_noise<<<(n + 255) / 256, 256, 0, s>>>(sc, dyn, eps);
-  return cudaGetLastError();
-}
-
 cudaError_t launch_cloud_prep(const double* pts, const uint8_t* mask, const StepDyn* dyn,
                               float radius, const CloudGrid& g, cudaStream_t s) {
   const int smem = kGridMax * kGridMax * static_cast<int>(sizeof(int));
@@ -1687,56 +1121,10 @@ cudaError_t launch_cloud_prep(const double* pts, const uint8_t* mask, const Step
   return cudaGetLastError();
 }
 
-template <int TAG>
-cudaError_t rollout_tag(const StepConst& sc, const StepDyn* dyn, const double* nominal,
-                        const double* eps, float4* poses, double2* xy, double* base_cost,
-                        double* controls_out, double* states_out, cudaStream_t s) {
-  const int threads = kRolloutWarps * 32;
-  const size_t smem = sizeof(double) * (static_cast<size_t>(sc.T) * sc.D +
-                                        kRolloutWarps * static_cast<size_t>(rollout_warp_scratch(sc.T, sc.D)));
-  if (smem > 48 * 1024) {
-    cudaError_t e = cudaFuncSetAttribute(k_rollout<TAG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(smem));
-    if (e != cudaSuccess) return e;
-  }
-  k_rollout<TAG><<<(sc.k_local + kRolloutWarps - 1) / kRolloutWarps, threads, smem, s>>>(
-      sc, dyn, nominal, eps, poses, xy, base_cost, controls_out, states_out);
-  return cudaGetLastError();
-}
-
-cudaError_t launch_rollout(const StepConst& sc, const StepDyn* dyn, const double* nominal,
-                           const double* eps, float4* poses, double2* xy, double* base_cost,
-                           double* controls_out, double* states_out, cudaStream_t s) {
-  switch (sc.tag) {
-    case EXM_MODEL_DIFF: return rollout_tag<EXM_MODEL_DIFF>(sc, dyn, nominal, eps, poses, xy, base_cost, controls_out, states_out, s);
-    case EXM_MODEL_ACKERMANN: return rollout_tag<EXM_MODEL_ACKERMANN>(sc, dyn, nominal, eps, poses, xy, base_cost, controls_out, states_out, s);
-    case EXM_MODEL_OMNI: return rollout_tag<EXM_MODEL_OMNI>(sc, dyn, nominal, eps, poses, xy, base_cost, controls_out, states_out, s);
-    case EXM_MODEL_SPIN: return rollout_tag<EXM_MODEL_SPIN>(sc, dyn, nominal, eps, poses, xy, base_cost, controls_out, states_out, s);
-    case EXM_MODEL_PARALLEL: return rollout_tag<EXM_MODEL_PARALLEL>(sc, dyn, nominal, eps, poses, xy, base_cost, controls_out, states_out, s);
-  }
-  return cudaErrorInvalidValue;
-}
-
 cudaError_t launch_sdf_grid_stats(const FpDev& fp, const float4* poses, int n_poses,
                                   const CloudGrid& g, float* out, unsigned long long* stats,
                                   cudaStream_t s) {
   return dispatch_fp<GridStatsLaunch>(fp, poses, n_poses, g, out, stats, s);
-}
-
-cudaError_t launch_rollout_costs(const StepConst& sc, const StepDyn* dyn, const double* guide,
-                                 int guide_cap, const double* base_cost, const double2* xy,
-                                 const float* dmin, double* cost, uint8_t* unsafe, float* dstat,
-                                 cudaStream_t s) {
-  if (sc.k_local <= 0) return cudaSuccess;
-  const size_t smem = sizeof(double) * 2 * static_cast<size_t>(guide_cap);
-  if (smem > 48 * 1024) {
-    cudaError_t e = cudaFuncSetAttribute(k_rollout_costs, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(smem));
-    if (e != cudaSuccess) return e;
-  }
-  k_rollout_costs<<<(sc.k_local + kCostWarps - 1) / kCostWarps, kCostWarps * 32, smem, s>>>(
-      sc, dyn, guide, base_cost, xy, dmin, cost, unsafe, dstat);
-  return cudaGetLastError();
 }
 
 cudaError_t launch_sdf_grid(const FpDev& fp, const float4* poses, int n_poses,
@@ -1747,66 +1135,6 @@ cudaError_t launch_sdf_grid(const FpDev& fp, const float4* poses, int n_poses,
                     (n_poses <= kWarpPerPoseMax && strcmp(m, "thread") && strcmp(m, "brute"));
   if (warp) return dispatch_fp<GridWarpLaunch>(fp, poses, n_poses, g, out, s);
   return dispatch_fp<GridLaunch>(fp, poses, n_poses, g, out, s);
-}
-
-cudaError_t launch_block_partials(const StepConst& sc, const double* cost, const uint8_t* unsafe,
-                                  const double* eps, double* partials, cudaStream_t s) {
-  if (sc.nblocks_local <= 0) return cudaSuccess;
-  const size_t smem = sizeof(double) * (kPartialThreads / 32) * static_cast<size_t>(sc.T) * sc.D;
-  if (smem > 48 * 1024) {
-    cudaError_t e = cudaFuncSetAttribute(k_block_partials,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(smem));
-    if (e != cudaSuccess) return e;
-  }
-  k_block_partials<<<sc.nblocks_local, kPartialThreads, smem, s>>>(sc, cost, unsafe, eps, partials);
-  return cudaGetLastError();
-}
-
-template <int TAG>
-cudaError_t update_tag(const StepConst& sc, const double* partials, const double* nominal,
-                       const StepDyn* dyn, double* upd, float4* val_poses, double2* val_xy,
-                       double* val_base, DecisionDev* dec, int merge, cudaStream_t s) {
-  const size_t smem = sizeof(double) * (static_cast<size_t>(sc.T) * sc.D +
-                                        static_cast<size_t>(merge ? sc.nblocks_total : 0) +
-                                        rollout_warp_scratch(sc.T, sc.D));
-  if (smem > 48 * 1024) {
-    cudaError_t e = cudaFuncSetAttribute(k_update<TAG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(smem));
-    if (e != cudaSuccess) return e;
-  }
-  k_update<TAG><<<1, 256, smem, s>>>(sc, partials, nominal, dyn, upd, val_poses, val_xy, val_base,
-                                     dec, merge);
-  return cudaGetLastError();
-}
-
-cudaError_t launch_update(const StepConst& sc, const double* partials, const double* nominal,
-                          const StepDyn* dyn, double* upd, float4* val_poses, double2* val_xy,
-                          double* val_base, DecisionDev* dec, int merge, cudaStream_t s) {
-  switch (sc.tag) {
-    case EXM_MODEL_DIFF: return update_tag<EXM_MODEL_DIFF>(sc, partials, nominal, dyn, upd, val_poses, val_xy, val_base, dec, merge, s);
-    case EXM_MODEL_ACKERMANN: return update_tag<EXM_MODEL_ACKERMANN>(sc, partials, nominal, dyn, upd, val_poses, val_xy, val_base, dec, merge, s);
-    case EXM_MODEL_OMNI: return update_tag<EXM_MODEL_OMNI>(sc, partials, nominal, dyn, upd, val_poses, val_xy, val_base, dec, merge, s);
-    case EXM_MODEL_SPIN: return update_tag<EXM_MODEL_SPIN>(sc, partials, nominal, dyn, upd, val_poses, val_xy, val_base, dec, merge, s);
-    case EXM_MODEL_PARALLEL: return update_tag<EXM_MODEL_PARALLEL>(sc, partials, nominal, dyn, upd, val_poses, val_xy, val_base, dec, merge, s);
-  }
-  return cudaErrorInvalidValue;
-}
-
-cudaError_t launch_finalize(const StepConst& sc, const float* val_dmin, const double2* val_xy,
-                            const double* val_base, const double* upd, const double* guide,
-                            int guide_cap, double* nominal, StepDyn* dyn, DecisionDev* dec,
-                            double* out_dmin, double* out_nominal, double* out_uprev, int commit,
-                            cudaStream_t s) {
-  const size_t smem = sizeof(double) * (2 * static_cast<size_t>(guide_cap) + sc.T);
-  if (smem > 48 * 1024) {
-    cudaError_t e = cudaFuncSetAttribute(k_finalize, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(smem));
-    if (e != cudaSuccess) return e;
-  }
-  k_finalize<<<1, 64, smem, s>>>(sc, val_dmin, val_xy, val_base, upd, guide, nominal, dyn, dec,
-                                 out_dmin, out_nominal, out_uprev, commit);
-  return cudaGetLastError();
 }
 
 cudaError_t launch_recentre(const double* pts, int n, double cx, double cy, float2* out,
