@@ -458,36 +458,44 @@ __global__ void __launch_bounds__(256) k_update(const StepConst sc,
                                                 double2* __restrict__ val_xy,
                                                 double* __restrict__ val_base,
                                                 DecisionDev* __restrict__ dec, int merge) {
-  extern __shared__ double sm_u[];  // T*D updated controls, then nblocks_total factors
+  extern __shared__ double sm_u[];  // T*D updated controls, nb factors, nb betas; then scratch
   __shared__ double s_beta, s_S;
-  const int tid = threadIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31;
   const int nb = sc.nblocks_total;
   const int stride = partial_stride(sc.T, sc.D);
   const int TD = sc.T * sc.D;
   double* s_upd = sm_u;
   double* sf = sm_u + TD;
   if (merge) {
-    if (tid == 0) {
-      double beta = partials[0];
-      int arg = static_cast<int>(partials[3]);
-      for (int b = 1; b < nb; ++b) {
-        const double bb = partials[static_cast<size_t>(b) * stride];
-        if (bb < beta) { beta = bb; arg = static_cast<int>(partials[static_cast<size_t>(b) * stride + 3]); }
+    double* sb = sf + nb;
+    for (int b = tid; b < nb; b += blockDim.x) sb[b] = partials[static_cast<size_t>(b) * stride];
+    __syncthreads();
+    if (tid < 32) {  // beta = min_b beta_b, first block on ties (blocks are in rollout order)
+      double v = HUGE_VAL;
+      int vi = 0x7fffffff;
+      for (int b = lane; b < nb; b += 32)
+        if (sb[b] < v) { v = sb[b]; vi = b; }
+      for (int o = 16; o; o >>= 1) {
+        const double ov = __shfl_xor_sync(kFull, v, o);
+        const int oi = __shfl_xor_sync(kFull, vi, o);
+        if (ov < v || (ov == v && oi < vi)) { v = ov; vi = oi; }
       }
-      s_beta = beta;
-      dec->argmin = arg;
-      dec->best_cost = beta;
+      if (tid == 0) {
+        s_beta = v;
+        dec->argmin = static_cast<int>(partials[static_cast<size_t>(vi) * stride + 3]);
+        dec->best_cost = v;
+      }
     }
     __syncthreads();
-    for (int b = tid; b < nb; b += blockDim.x)
-      sf[b] = exp(-(partials[static_cast<size_t>(b) * stride] - s_beta) / sc.lambda);
+    for (int b = tid; b < nb; b += blockDim.x) sf[b] = exp(-(sb[b] - s_beta) / sc.lambda);
     __syncthreads();
-    if (tid == 0) {
+    if (tid == 0) {  // block order: deterministic, independent of the GPU count
       double S = 0.0, A = 0.0;
+#pragma unroll 8
       for (int b = 0; b < nb; ++b) {
         const double* p = partials + static_cast<size_t>(b) * stride;
         S += sf[b] * p[1];
-        A += sf[b] * (p[2] + p[1] * ((p[0] - s_beta) / sc.lambda));
+        A += sf[b] * (p[2] + p[1] * ((sb[b] - s_beta) / sc.lambda));
       }
       s_S = S;
       dec->entropy = A / S + log(S);
@@ -509,7 +517,7 @@ __global__ void __launch_bounds__(256) k_update(const StepConst sc,
     const StepDyn dyn = *dynp;
     const double b = rollout_warp<TAG>(sc, dyn, s_upd, nullptr, nullptr, 0ull, val_poses, val_xy,
                                        upd, nullptr, val_base + 1,
-                                       sf + (merge ? nb : 0));
+                                       sf + (merge ? 2 * nb : 0));
     if (tid == 0) *val_base = b;
   }
 }
@@ -646,7 +654,7 @@ cudaError_t update_tag(const StepConst& sc, const double* partials, const double
                        const StepDyn* dyn, double* upd, float4* val_poses, double2* val_xy,
                        double* val_base, DecisionDev* dec, int merge, cudaStream_t s) {
   const size_t smem = sizeof(double) * (static_cast<size_t>(sc.T) * sc.D +
-                                        static_cast<size_t>(merge ? sc.nblocks_total : 0) +
+                                        static_cast<size_t>(merge ? 2 * sc.nblocks_total : 0) +
                                         rollout_warp_scratch(sc.T, sc.D));
   if (smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(k_update<TAG>, cudaFuncAttributeMaxDynamicSharedMemorySize,

@@ -267,6 +267,7 @@ constexpr float kCellSearchFrac = 0.385f;  // ... or <= this fraction of R + mea
 // Below this many poses one thread per pose leaves most SMs idle (< ~16 warps each): use one
 // warp per pose instead.
 constexpr int kWarpPerPoseMax = 65536;
+constexpr int kCtaPerPoseMax = 1024;  // ... and below this, a CTA of 8 warps per pose
 // Single-CTA cloud preparation: mask compaction, FP64 recentring at q0 then FP32 rounding,
 // bounding box, uniform grid (cell >= cs_target, <= kGridMax per axis), counting sort.
 __global__ void __launch_bounds__(1024) k_cloud_prep(const double* __restrict__ pts,
@@ -650,20 +651,23 @@ __global__ void __launch_bounds__(128) k_sdf_grid(const __grid_constant__ FpDev 
   }
 }
 
-// Warp <-> pose variant for few poses (the T validation poses). Per ring, the lanes first
-// claim cells that pass the box bound, then stride together over the concatenation of those
-// cells' points (a shuffle search maps a flat index to its cell), so the loads coalesce and
-// all lanes stay busy; the warp minimum after every chunk drives the exact termination.
-template <int KIND, int NB>
-__global__ void __launch_bounds__(128) k_sdf_grid_warp(const __grid_constant__ FpDev fp,
-                                                       const float4* __restrict__ poses, int n_poses,
-                                                       const GridMeta* __restrict__ gmp,
-                                                       const int* __restrict__ cell_start,
-                                                       const float2* __restrict__ cloud,
-                                                       float* __restrict__ out) {
-  const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+// Warp(s) <-> pose variant for few poses (the T validation poses, small rollout sets). Per ring,
+// the lanes first claim cells that pass the box bound, then the W warps of the pose stride
+// together over the concatenation of those cells' points (a shuffle search maps a flat index to
+// its cell), so the loads coalesce and all lanes stay busy; the minimum over the pose's warps
+// after every chunk drives the exact termination. W == 1: four poses per 128-thread CTA;
+// W > 1: one pose per CTA of W warps.
+template <int KIND, int NB, int W = 1>
+__global__ void __launch_bounds__(W == 1 ? 128 : 32 * W) k_sdf_grid_warp(
+    const __grid_constant__ FpDev fp, const float4* __restrict__ poses, int n_poses,
+    const GridMeta* __restrict__ gmp, const int* __restrict__ cell_start,
+    const float2* __restrict__ cloud, float* __restrict__ out) {
+  __shared__ float s_best[W];
   const int lane = threadIdx.x & 31;
-  if (w >= n_poses) return;  // warp-uniform
+  const int wid = W == 1 ? 0 : static_cast<int>(threadIdx.x >> 5);
+  const int w = W == 1 ? static_cast<int>((blockIdx.x * blockDim.x + threadIdx.x) >> 5)
+                       : static_cast<int>(blockIdx.x);
+  if (w >= n_poses) return;  // uniform over the pose's warps
   const GridMeta gm = *gmp;
   if (gm.n_valid == 0) {
     if (lane == 0) out[w] = kEmptyDistance;
@@ -712,7 +716,7 @@ __global__ void __launch_bounds__(128) k_sdf_grid_warp(const __grid_constant__ F
       }
       const int total = __shfl_sync(kFull, incl, 31);
       float mine = best;
-      for (int b = 0; b < total; b += 32) {
+      for (int b = wid * 32; b < total; b += 32 * W) {
         const int i = b + lane;
         // owner = first lane whose inclusive prefix exceeds i
         int lo = 0;
@@ -730,15 +734,28 @@ __global__ void __launch_bounds__(128) k_sdf_grid_warp(const __grid_constant__ F
           if (dx * dx + dy * dy < l2 * l2) {
             const float bx = fmaf(q.z, dx, q.w * dy);
             const float by = fmaf(q.z, dy, -(q.w * dx));
-            if (aabb_may_beat(fp, bx, by, mine, mg)) mine = fminf(mine, sd_body<KIND, NB>(fp, bx, by));
+            if ((KIND != EXM_FOOTPRINT_POLYGON && NB > 0 && NB <= 3) ||
+                (KIND == EXM_FOOTPRINT_POLYGON ? cover_may_beat(fp, bx, by, mine, mg)
+                                               : aabb_may_beat(fp, bx, by, mine, mg)))
+              mine = fminf(mine, sd_body<KIND, NB>(fp, bx, by));
           }
         }
       }
       for (int o = 16; o; o >>= 1) mine = fminf(mine, __shfl_xor_sync(kFull, mine, o));
-      best = mine;
+      if constexpr (W == 1) {
+        best = mine;
+      } else {
+        if (lane == 0) s_best[wid] = mine;
+        __syncthreads();
+        float m = s_best[0];
+#pragma unroll
+        for (int j = 1; j < W; ++j) m = fminf(m, s_best[j]);
+        best = m;
+        __syncthreads();
+      }
     }
   }
-  if (lane == 0) out[w] = best;
+  if (lane == 0 && wid == 0) out[w] = best;
 }
 
 __global__ void k_recentre(const double* __restrict__ pts, int n, double cx, double cy,
@@ -1021,7 +1038,8 @@ cudaError_t dispatch_fp(const FpDev& fp, Args&&... args) {
 
 // EXM_GRID_MODE (tests and A/B measurements; read at every launch, so at graph capture):
 //   "brute" every valid point evaluated (exactness reference), "nochunk" no chunk bound,
-//   "thread" / "warp" force the thread- or warp-per-pose kernel. Default: automatic.
+//   "thread" / "warp" / "cta" force one thread, one warp or one 8-warp CTA per pose.
+//   Default: automatic.
 inline const char* grid_mode() {
   const char* m = getenv("EXM_GRID_MODE");
   return m ? m : "";
@@ -1068,9 +1086,14 @@ struct GridWarpLaunch {
   static cudaError_t run(const FpDev& fp, const float4* poses, int n_poses, const CloudGrid& g,
                          float* out, cudaStream_t s) {
     if (n_poses <= 0) return cudaSuccess;
-    const int threads = 128, warps = threads / 32;
-    k_sdf_grid_warp<KIND, NB><<<(n_poses + warps - 1) / warps, threads, 0, s>>>(
-        fp, poses, n_poses, g.gm, g.cell_start, g.cloud, out);
+    if (n_poses <= kCtaPerPoseMax || !strcmp(grid_mode(), "cta")) {  // few poses: 8 warps each
+      k_sdf_grid_warp<KIND, NB, 8><<<n_poses, 256, 0, s>>>(fp, poses, n_poses, g.gm, g.cell_start,
+                                                           g.cloud, out);
+    } else {
+      const int threads = 128, warps = threads / 32;
+      k_sdf_grid_warp<KIND, NB><<<(n_poses + warps - 1) / warps, threads, 0, s>>>(
+          fp, poses, n_poses, g.gm, g.cell_start, g.cloud, out);
+    }
     return cudaGetLastError();
   }
 };
@@ -1131,7 +1154,7 @@ cudaError_t launch_sdf_grid(const FpDev& fp, const float4* poses, int n_poses,
                             const CloudGrid& g, float* out, cudaStream_t s) {
   // Few poses (validation rollout, single queries): one warp per pose keeps all lanes busy.
   const char* m = grid_mode();
-  const bool warp = !strcmp(m, "warp") ||
+  const bool warp = !strcmp(m, "warp") || !strcmp(m, "cta") ||
                     (n_poses <= kWarpPerPoseMax && strcmp(m, "thread") && strcmp(m, "brute"));
   if (warp) return dispatch_fp<GridWarpLaunch>(fp, poses, n_poses, g, out, s);
   return dispatch_fp<GridLaunch>(fp, poses, n_poses, g, out, s);

@@ -57,7 +57,7 @@ def _dmin(wl, mode):
 
 
 @pytest.mark.parametrize("case", list(CASES))
-@pytest.mark.parametrize("mode", ["thread", "warp", "nochunk"])
+@pytest.mark.parametrize("mode", ["thread", "warp", "cta", "nochunk"])
 def test_culled_minimum_is_bitwise_brute_force(case, mode):
     wl = CASES[case]()
     want = _dmin(wl, "brute")
