@@ -16,6 +16,21 @@
 // every FP64 product and sum is rounded where the reference rounds it.
 #include "exm_device.cuh"
 
+#ifdef EXM_TIMING  // phase timestamps of k_update (diagnostic builds only)
+__device__ long long g_probe[16];
+#define EXM_PROBE(i) \
+  do {                \
+    if (threadIdx.x == 0) g_probe[i] = clock64(); \
+  } while (0)
+extern "C" int exm_debug_probes(long long* out) {
+  return static_cast<int>(cudaMemcpyFromSymbol(out, g_probe, sizeof(g_probe)));
+}
+#else
+#define EXM_PROBE(i) \
+  do {               \
+  } while (0)
+#endif
+
 namespace exm {
 namespace {
 
@@ -162,24 +177,30 @@ __device__ double rollout_warp(const StepConst& sc, const StepDyn& dyn, const do
     } else if (eps_in) {
       e = eps_in[i];
     }
-    s_u[i] = __dadd_rn(nominal[i], e);
-  }
-  __syncwarp();
-  if (lane < D) {
-    double lo = sc.vel_min[lane], hi = sc.vel_max[lane];
-    if (TAG == EXM_MODEL_ACKERMANN && lane == 1) {
+    // the velocity clamp of kinematics.cpp:105-112 does not depend on the previous control:
+    // applied here in parallel, only the rate clamp (:113) stays in the serial chain
+    const int c = i % D;
+    double lo = sc.vel_min[c], hi = sc.vel_max[c];
+    if (TAG == EXM_MODEL_ACKERMANN && c == 1) {
       lo = mx(lo, -sc.steer_max);
       hi = mn(hi, sc.steer_max);
     }
+    s_u[i] = clampd(__dadd_rn(nominal[i], e), lo, hi);
+  }
+  __syncwarp();
+  EXM_PROBE(4);
+  if (lane < D) {
     const double amin = __dmul_rn(sc.acc_min[lane], sc.dt), amax = __dmul_rn(sc.acc_max[lane], sc.dt);
     double prev = dyn.u_prev[lane];
+#pragma unroll 5
     for (int h = 0; h < T; ++h) {
-      const double v = clampd(s_u[h * D + lane], lo, hi);
+      const double v = s_u[h * D + lane];
       prev = clampd(v, __dadd_rn(prev, amin), __dadd_rn(prev, amax));
       s_u[h * D + lane] = prev;
     }
   }
   __syncwarp();
+  EXM_PROBE(5);
   for (int h = lane; h < T; h += 32) {
     double uc[3] = {0.0, 0.0, 0.0};
 #pragma unroll
@@ -190,6 +211,7 @@ __device__ double rollout_warp(const StepConst& sc, const StepDyn& dyn, const do
   __syncwarp();
   if (lane == 0) {
     double th = dyn.q0[2];
+#pragma unroll 5
     for (int h = 0; h < T; ++h) {
       const double inc = s_th[h];
       s_th[h] = th;
@@ -198,6 +220,7 @@ __device__ double rollout_warp(const StepConst& sc, const StepDyn& dyn, const do
     s_c[0] = th;  // theta_T, parked until the sincos pass reads s_th
   }
   __syncwarp();
+  EXM_PROBE(6);
   const double thT = s_c[0];
   __syncwarp();
   for (int h = lane; h < T; h += 32) {
@@ -214,10 +237,12 @@ __device__ double rollout_warp(const StepConst& sc, const StepDyn& dyn, const do
     s_y[h] = __dmul_rn(fy, sc.dt);
   }
   __syncwarp();
+  EXM_PROBE(7);
   double endp = 0.0;
   if (lane < 2) {
     double* chain = lane == 0 ? s_x : s_y;
     double v = dyn.q0[lane];
+#pragma unroll 5
     for (int h = 0; h < T; ++h) {
       const double inc = chain[h];
       chain[h] = v;
@@ -225,6 +250,7 @@ __device__ double rollout_warp(const StepConst& sc, const StepDyn& dyn, const do
     }
     endp = v;
   }
+  EXM_PROBE(8);
   const double xT = __shfl_sync(kFull, endp, 0), yT = __shfl_sync(kFull, endp, 1);
   const double qT[3] = {xT, yT, thT};
   const double base = terminal_cost(sc, qT, dyn.goal);
@@ -466,9 +492,19 @@ __global__ void __launch_bounds__(256) k_update(const StepConst sc,
   const int TD = sc.T * sc.D;
   double* s_upd = sm_u;
   double* sf = sm_u + TD;
+  EXM_PROBE(0);
   if (merge) {
-    double* sb = sf + nb;
-    for (int b = tid; b < nb; b += blockDim.x) sb[b] = partials[static_cast<size_t>(b) * stride];
+    double* sb = sf + nb;      // beta_b, then z_b = (beta_b - beta) / lambda
+    double* sS = sb + nb;      // S_b
+    double* sA = sS + nb;      // A_b
+    double* sg = sA + nb;      // argmin_b
+    for (int b = tid; b < nb; b += blockDim.x) {
+      const double* p = partials + static_cast<size_t>(b) * stride;
+      sb[b] = p[0];
+      sS[b] = p[1];
+      sA[b] = p[2];
+      sg[b] = p[3];
+    }
     __syncthreads();
     if (tid < 32) {  // beta = min_b beta_b, first block on ties (blocks are in rollout order)
       double v = HUGE_VAL;
@@ -482,43 +518,59 @@ __global__ void __launch_bounds__(256) k_update(const StepConst sc,
       }
       if (tid == 0) {
         s_beta = v;
-        dec->argmin = static_cast<int>(partials[static_cast<size_t>(vi) * stride + 3]);
+        dec->argmin = static_cast<int>(sg[vi]);
         dec->best_cost = v;
       }
     }
     __syncthreads();
-    for (int b = tid; b < nb; b += blockDim.x) sf[b] = exp(-(sb[b] - s_beta) / sc.lambda);
+    EXM_PROBE(1);
+    for (int b = tid; b < nb; b += blockDim.x) {
+      const double z = (sb[b] - s_beta) / sc.lambda;
+      sb[b] = z;
+      sf[b] = exp(-z);
+    }
     __syncthreads();
     if (tid == 0) {  // block order: deterministic, independent of the GPU count
       double S = 0.0, A = 0.0;
-#pragma unroll 8
       for (int b = 0; b < nb; ++b) {
-        const double* p = partials + static_cast<size_t>(b) * stride;
-        S += sf[b] * p[1];
-        A += sf[b] * (p[2] + p[1] * ((sb[b] - s_beta) / sc.lambda));
+        S += sf[b] * sS[b];
+        A += sf[b] * (sA[b] + sS[b] * sb[b]);
       }
       s_S = S;
       dec->entropy = A / S + log(S);
     }
+    // U_o = sum_b f_b U_b[o] needs only the factors: overlaps thread 0's S / A sums
+    double U[4] = {0.0, 0.0, 0.0, 0.0};
+    for (int k = 0, o = tid; k < 4 && o < TD; ++k, o += blockDim.x) {
+#pragma unroll 16
+      for (int b = 0; b < nb; ++b) U[k] += sf[b] * partials[static_cast<size_t>(b) * stride + 4 + o];
+    }
     __syncthreads();
-    for (int o = tid; o < TD; o += blockDim.x) {
-      double U = 0.0;
-#pragma unroll 8
-      for (int b = 0; b < nb; ++b) U += sf[b] * partials[static_cast<size_t>(b) * stride + 4 + o];
-      s_upd[o] = nominal[o] + U / s_S;
+    EXM_PROBE(2);
+    for (int k = 0, o = tid; o < TD; ++k, o += blockDim.x) {
+      double u = 0.0;
+      if (k < 4) {
+        u = U[k];
+      } else {  // T * D > 4 * blockDim: the remaining outputs
+#pragma unroll 16
+        for (int b = 0; b < nb; ++b) u += sf[b] * partials[static_cast<size_t>(b) * stride + 4 + o];
+      }
+      s_upd[o] = nominal[o] + u / s_S;
     }
   } else {
     for (int o = tid; o < TD; o += blockDim.x) s_upd[o] = nominal[o];
   }
   __syncthreads();
+  EXM_PROBE(3);
   if (tid < 32) {
     // warp 0 clamps sequentially from u_prev and writes the clamped sequence back; the
     // reference's second clamp inside validate_nominal is idempotent on it.
     const StepDyn dyn = *dynp;
     const double b = rollout_warp<TAG>(sc, dyn, s_upd, nullptr, nullptr, 0ull, val_poses, val_xy,
                                        upd, nullptr, val_base + 1,
-                                       sf + (merge ? 2 * nb : 0));
+                                       sf + (merge ? 5 * nb : 0));
     if (tid == 0) *val_base = b;
+    EXM_PROBE(9);
   }
 }
 
@@ -654,7 +706,7 @@ cudaError_t update_tag(const StepConst& sc, const double* partials, const double
                        const StepDyn* dyn, double* upd, float4* val_poses, double2* val_xy,
                        double* val_base, DecisionDev* dec, int merge, cudaStream_t s) {
   const size_t smem = sizeof(double) * (static_cast<size_t>(sc.T) * sc.D +
-                                        static_cast<size_t>(merge ? 2 * sc.nblocks_total : 0) +
+                                        static_cast<size_t>(merge ? 5 * sc.nblocks_total : 0) +
                                         rollout_warp_scratch(sc.T, sc.D));
   if (smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(k_update<TAG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
