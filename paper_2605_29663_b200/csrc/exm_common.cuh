@@ -3,6 +3,8 @@
 #pragma once
 
 #include <cstdint>
+#include <cstdlib>
+#include <utility>
 
 #include <cuda_runtime.h>
 
@@ -109,6 +111,30 @@ struct DecisionDev {
 // Softmax partial of one block of kBlockRollouts rollouts:
 //   {beta_b, S_b = sum e, A_b = sum e (J - beta_b)/lambda, argmin_b, U_b[T*D] = sum e eps}
 inline __host__ __device__ int partial_stride(int T, int D) { return 4 + T * D; }
+
+// Kernel launch with programmatic dependent launch (PDL) allowed: the next kernel in the stream
+// (or graph) may be scheduled while this one drains, and waits in pdl_wait() (griddepcontrol
+// .wait, the first statement of every kernel) for the predecessor's completion and memory
+// flush, so launch latency overlaps the previous kernel's tail. EXM_PDL=0 disables it.
+inline bool pdl_enabled() {
+  static const bool on = !(std::getenv("EXM_PDL") && std::getenv("EXM_PDL")[0] == '0');
+  return on;
+}
+template <typename... KArgs, typename... Args>
+cudaError_t launch_k(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                     Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
 
 // ---- kernel launchers (exm_kernels.cu) ---------------------------------------------------
 cudaError_t launch_noise(const StepConst& sc, const StepDyn* dyn, double* eps, cudaStream_t s);

@@ -22,6 +22,15 @@
 namespace exm {
 namespace {
 
+// First statement of every kernel: with programmatic dependent launch (launch_k) wait for the
+// predecessor grid's completion and memory flush; a no-op for a normally launched kernel.
+// Then let the dependent grid launch right away: its CTAs take free SM slots and park in their
+// own wait, so the launch latency overlaps this grid's execution.
+__device__ __forceinline__ void pdl_wait() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" :::);
+}
+
 constexpr double kPi = 3.14159265358979323846;
 constexpr unsigned kFull = 0xffffffffu;
 

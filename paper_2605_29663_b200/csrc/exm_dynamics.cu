@@ -280,6 +280,7 @@ __device__ double rollout_warp(const StepConst& sc, const StepDyn& dyn, const do
 
 __global__ void k_noise(const StepConst sc, const StepDyn* __restrict__ dyn,
                         double* __restrict__ eps) {
+  pdl_wait();
   const int idx = blockIdx.x * blockDim.x + threadIdx.x;  // local (r, h)
   if (idx >= sc.k_local * sc.T) return;
   const int r = idx / sc.T, h = idx % sc.T;
@@ -293,6 +294,7 @@ __global__ void __launch_bounds__(kRolloutWarps * 32) k_rollout(
     double* __restrict__ eps, int draw, float4* __restrict__ poses, double2* __restrict__ xy,
     double* __restrict__ base_cost, double* __restrict__ ctrl_cost,
     double* __restrict__ controls_out, double* __restrict__ states_out) {
+  pdl_wait();
   // One warp per rollout (rollout_warp). draw: the perturbations are drawn here (device noise,
   // written to eps for the softmax update); else eps holds injected perturbations.
   extern __shared__ double sm[];
@@ -329,6 +331,7 @@ __global__ void __launch_bounds__(kCostWarps * 32) k_rollout_costs(
     const double* __restrict__ base_cost, const double* __restrict__ ctrl_cost,
     const double2* __restrict__ xy, const float* __restrict__ dmin, double* __restrict__ cost,
     uint8_t* __restrict__ unsafe, float* __restrict__ dstat) {
+  pdl_wait();
   extern __shared__ double g[];  // guide (2*ng), then per warp: task[T], obst[T]
   __shared__ float red[2][kCostWarps];
   const int ng = dynp->n_guide, T = sc.T;
@@ -393,6 +396,7 @@ __global__ void __launch_bounds__(kCostWarps * 32) k_rollout_costs(
 __global__ void __launch_bounds__(kPartialThreads) k_block_partials(
     const StepConst sc, const double* __restrict__ cost, const uint8_t* __restrict__ unsafe,
     const double* __restrict__ eps, double* __restrict__ partials) {
+  pdl_wait();
   extern __shared__ double s_u[];  // [kPartialThreads/32][T*D]
   __shared__ double s_e[kBlockRollouts];
   __shared__ double s_v[kBlockRollouts / 32];
@@ -484,6 +488,7 @@ __global__ void __launch_bounds__(256) k_update(const StepConst sc,
                                                 double2* __restrict__ val_xy,
                                                 double* __restrict__ val_base,
                                                 DecisionDev* __restrict__ dec, int merge) {
+  pdl_wait();
   extern __shared__ double sm_u[];  // T*D updated controls, nb factors, nb betas; then scratch
   __shared__ double s_beta, s_S;
   const int tid = threadIdx.x, lane = tid & 31;
@@ -581,6 +586,7 @@ __global__ void __launch_bounds__(64) k_finalize(
     const double* __restrict__ guide, double* __restrict__ nominal, StepDyn* __restrict__ dyn,
     DecisionDev* __restrict__ dec, double* __restrict__ out_dmin,
     double* __restrict__ out_nominal, double* __restrict__ out_uprev, int commit) {
+  pdl_wait();
   extern __shared__ double sm2[];  // guide (2*ng) then per-step task (T) and obstacle (T) costs
   __shared__ int s_ok;
   const int tid = threadIdx.x;
@@ -634,7 +640,7 @@ __global__ void __launch_bounds__(64) k_finalize(
 cudaError_t launch_noise(const StepConst& sc, const StepDyn* dyn, double* eps, cudaStream_t s) {
   const int n = sc.k_local * sc.T;
   if (n <= 0) return cudaSuccess;
-  k_noise<<<(n + 255) / 256, 256, 0, s>>>(sc, dyn, eps);
+  { if (const cudaError_t le = launch_k(k_noise, (n + 255) / 256, 256, 0, s, sc, dyn, eps); le != cudaSuccess) return le; }
   return cudaGetLastError();
 }
 
@@ -651,8 +657,8 @@ cudaError_t rollout_tag(const StepConst& sc, const StepDyn* dyn, const double* n
                                          static_cast<int>(smem));
     if (e != cudaSuccess) return e;
   }
-  k_rollout<TAG><<<(sc.k_local + kRolloutWarps - 1) / kRolloutWarps, threads, smem, s>>>(
-      sc, dyn, nominal, eps, draw, poses, xy, base_cost, ctrl_cost, controls_out, states_out);
+  { if (const cudaError_t le = launch_k(k_rollout<TAG>, (sc.k_local + kRolloutWarps - 1) / kRolloutWarps, threads, smem, s, 
+      sc, dyn, nominal, eps, draw, poses, xy, base_cost, ctrl_cost, controls_out, states_out); le != cudaSuccess) return le; }
   return cudaGetLastError();
 }
 
@@ -682,8 +688,8 @@ cudaError_t launch_rollout_costs(const StepConst& sc, const StepDyn* dyn, const 
                                          static_cast<int>(smem));
     if (e != cudaSuccess) return e;
   }
-  k_rollout_costs<<<(sc.k_local + kCostWarps - 1) / kCostWarps, kCostWarps * 32, smem, s>>>(
-      sc, dyn, guide, base_cost, ctrl_cost, xy, dmin, cost, unsafe, dstat);
+  { if (const cudaError_t le = launch_k(k_rollout_costs, (sc.k_local + kCostWarps - 1) / kCostWarps, kCostWarps * 32, smem, s, 
+      sc, dyn, guide, base_cost, ctrl_cost, xy, dmin, cost, unsafe, dstat); le != cudaSuccess) return le; }
   return cudaGetLastError();
 }
 
@@ -697,7 +703,7 @@ cudaError_t launch_block_partials(const StepConst& sc, const double* cost, const
                                          static_cast<int>(smem));
     if (e != cudaSuccess) return e;
   }
-  k_block_partials<<<sc.nblocks_local, kPartialThreads, smem, s>>>(sc, cost, unsafe, eps, partials);
+  { if (const cudaError_t le = launch_k(k_block_partials, sc.nblocks_local, kPartialThreads, smem, s, sc, cost, unsafe, eps, partials); le != cudaSuccess) return le; }
   return cudaGetLastError();
 }
 
@@ -713,8 +719,8 @@ cudaError_t update_tag(const StepConst& sc, const double* partials, const double
                                          static_cast<int>(smem));
     if (e != cudaSuccess) return e;
   }
-  k_update<TAG><<<1, 256, smem, s>>>(sc, partials, nominal, dyn, upd, val_poses, val_xy, val_base,
-                                     dec, merge);
+  { if (const cudaError_t le = launch_k(k_update<TAG>, 1, 256, smem, s, sc, partials, nominal, dyn, upd, val_poses, val_xy, val_base,
+                                     dec, merge); le != cudaSuccess) return le; }
   return cudaGetLastError();
 }
 
@@ -742,8 +748,8 @@ cudaError_t launch_finalize(const StepConst& sc, const float* val_dmin, const do
                                          static_cast<int>(smem));
     if (e != cudaSuccess) return e;
   }
-  k_finalize<<<1, 64, smem, s>>>(sc, val_dmin, val_xy, val_base, upd, guide, nominal, dyn, dec,
-                                 out_dmin, out_nominal, out_uprev, commit);
+  { if (const cudaError_t le = launch_k(k_finalize, 1, 64, smem, s, sc, val_dmin, val_xy, val_base, upd, guide, nominal, dyn, dec,
+                                 out_dmin, out_nominal, out_uprev, commit); le != cudaSuccess) return le; }
   return cudaGetLastError();
 }
 

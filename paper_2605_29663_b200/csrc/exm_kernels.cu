@@ -280,6 +280,7 @@ __global__ void __launch_bounds__(1024) k_cloud_prep(const double* __restrict__ 
                                                      int* __restrict__ raw_start,
                                                      int* __restrict__ cell_start,
                                                      GridMeta* __restrict__ gm_out) {
+  pdl_wait();
   extern __shared__ int hist[];  // kGridMax * kGridMax
   __shared__ float red[4][32];
   __shared__ int redc[32];
@@ -436,6 +437,7 @@ __global__ void __launch_bounds__(kSortWarps * 32) k_cell_sort(
     const float2* __restrict__ raw, const int* __restrict__ raw_start,
     const int* __restrict__ cell_start, const GridMeta* __restrict__ gmp,
     float2* __restrict__ cloud, float4* __restrict__ chunk) {
+  pdl_wait();
   constexpr int kKeys = kSubCells * kSubCells;
   __shared__ int s_hist[kSortWarps][kKeys];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -554,6 +556,7 @@ __global__ void __launch_bounds__(128) k_sdf_grid(const __grid_constant__ FpDev 
                                                   const float4* __restrict__ chunk,
                                                   float* __restrict__ out,
                                                   unsigned long long* __restrict__ stats = nullptr) {
+  pdl_wait();
   unsigned long long n_test = 0, n_eval = 0;
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   const bool active = i < n_poses;
@@ -662,6 +665,7 @@ __global__ void __launch_bounds__(W == 1 ? 128 : 32 * W) k_sdf_grid_warp(
     const __grid_constant__ FpDev fp, const float4* __restrict__ poses, int n_poses,
     const GridMeta* __restrict__ gmp, const int* __restrict__ cell_start,
     const float2* __restrict__ cloud, float* __restrict__ out) {
+  pdl_wait();
   __shared__ float s_best[W];
   const int lane = threadIdx.x & 31;
   const int wid = W == 1 ? 0 : static_cast<int>(threadIdx.x >> 5);
@@ -760,6 +764,7 @@ __global__ void __launch_bounds__(W == 1 ? 128 : 32 * W) k_sdf_grid_warp(
 
 __global__ void k_recentre(const double* __restrict__ pts, int n, double cx, double cy,
                            float2* __restrict__ out) {
+  pdl_wait();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   const double2 w = reinterpret_cast<const double2*>(pts)[i];
@@ -778,6 +783,7 @@ __global__ void __launch_bounds__(kPairThreads) k_sdf_pairs(
     const __grid_constant__ FpDev fp, const float4* __restrict__ poses, int n_poses,
     const float2* __restrict__ pts, const uint8_t* __restrict__ mask, int n_points,
     float* __restrict__ per_pair, unsigned* __restrict__ pose_min_key) {
+  pdl_wait();
   __shared__ __align__(128) float4 s_pose[kPoseChunk];
   __shared__ unsigned s_min[kPoseChunk];
   __shared__ __align__(8) uint64_t bar;
@@ -911,6 +917,7 @@ __global__ void __launch_bounds__(kPairThreads, 2) k_sdf_pairs_poly(
     const __grid_constant__ FpDev fp, const float4* __restrict__ poses, int n_poses,
     const float2* __restrict__ pts, const uint8_t* __restrict__ mask, int n_points,
     float* __restrict__ per_pair, unsigned* __restrict__ pose_min_key) {
+  pdl_wait();
   __shared__ __align__(128) float4 s_pose[kPoseChunk];
   __shared__ unsigned s_min[kPoseChunk];
   __shared__ __align__(8) uint64_t bar;
@@ -997,6 +1004,7 @@ __global__ void __launch_bounds__(kPairThreads, 2) k_sdf_pairs_poly(
 
 __global__ void k_keys_to_double(const unsigned* __restrict__ keys, int n,
                                  double* __restrict__ out) {
+  pdl_wait();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   const float v = unkey(keys[i]);
@@ -1004,6 +1012,7 @@ __global__ void k_keys_to_double(const unsigned* __restrict__ keys, int n,
 }
 
 __global__ void k_fill_u32(unsigned* p, unsigned v, int n) {
+  pdl_wait();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) p[i] = v;
 }
@@ -1053,14 +1062,14 @@ struct GridLaunch {
     const int threads = 128, blocks = (n_poses + threads - 1) / threads;
     const char* m = grid_mode();
     if (!strcmp(m, "brute"))
-      k_sdf_grid<KIND, NB, false, kGridBrute><<<blocks, threads, 0, s>>>(
-          fp, poses, n_poses, g.gm, g.cell_start, g.cloud, g.chunk, out);
+      { if (const cudaError_t le = launch_k(k_sdf_grid<KIND, NB, false, kGridBrute>, blocks, threads, 0, s, 
+          fp, poses, n_poses, g.gm, g.cell_start, g.cloud, g.chunk, out, nullptr); le != cudaSuccess) return le; }
     else if (!strcmp(m, "nochunk"))
-      k_sdf_grid<KIND, NB, false, kGridNoChunk><<<blocks, threads, 0, s>>>(
-          fp, poses, n_poses, g.gm, g.cell_start, g.cloud, g.chunk, out);
+      { if (const cudaError_t le = launch_k(k_sdf_grid<KIND, NB, false, kGridNoChunk>, blocks, threads, 0, s, 
+          fp, poses, n_poses, g.gm, g.cell_start, g.cloud, g.chunk, out, nullptr); le != cudaSuccess) return le; }
     else
-      k_sdf_grid<KIND, NB><<<blocks, threads, 0, s>>>(fp, poses, n_poses, g.gm, g.cell_start,
-                                                      g.cloud, g.chunk, out);
+      { if (const cudaError_t le = launch_k(k_sdf_grid<KIND, NB>, blocks, threads, 0, s, fp, poses, n_poses, g.gm, g.cell_start,
+                                                      g.cloud, g.chunk, out, nullptr); le != cudaSuccess) return le; }
     return cudaGetLastError();
   }
 };
@@ -1072,11 +1081,11 @@ struct GridStatsLaunch {
     if (n_poses <= 0) return cudaSuccess;
     const int threads = 128, blocks = (n_poses + threads - 1) / threads;
     if (!strcmp(grid_mode(), "nochunk"))
-      k_sdf_grid<KIND, NB, true, kGridNoChunk><<<blocks, threads, 0, s>>>(
-          fp, poses, n_poses, g.gm, g.cell_start, g.cloud, g.chunk, out, stats);
+      { if (const cudaError_t le = launch_k(k_sdf_grid<KIND, NB, true, kGridNoChunk>, blocks, threads, 0, s, 
+          fp, poses, n_poses, g.gm, g.cell_start, g.cloud, g.chunk, out, stats); le != cudaSuccess) return le; }
     else
-      k_sdf_grid<KIND, NB, true><<<blocks, threads, 0, s>>>(fp, poses, n_poses, g.gm,
-                                                            g.cell_start, g.cloud, g.chunk, out, stats);
+      { if (const cudaError_t le = launch_k(k_sdf_grid<KIND, NB, true>, blocks, threads, 0, s, fp, poses, n_poses, g.gm,
+                                                            g.cell_start, g.cloud, g.chunk, out, stats); le != cudaSuccess) return le; }
     return cudaGetLastError();
   }
 };
@@ -1087,12 +1096,12 @@ struct GridWarpLaunch {
                          float* out, cudaStream_t s) {
     if (n_poses <= 0) return cudaSuccess;
     if (n_poses <= kCtaPerPoseMax || !strcmp(grid_mode(), "cta")) {  // few poses: 8 warps each
-      k_sdf_grid_warp<KIND, NB, 8><<<n_poses, 256, 0, s>>>(fp, poses, n_poses, g.gm, g.cell_start,
-                                                           g.cloud, out);
+      { if (const cudaError_t le = launch_k(k_sdf_grid_warp<KIND, NB, 8>, n_poses, 256, 0, s, fp, poses, n_poses, g.gm, g.cell_start,
+                                                           g.cloud, out); le != cudaSuccess) return le; }
     } else {
       const int threads = 128, warps = threads / 32;
-      k_sdf_grid_warp<KIND, NB><<<(n_poses + warps - 1) / warps, threads, 0, s>>>(
-          fp, poses, n_poses, g.gm, g.cell_start, g.cloud, out);
+      { if (const cudaError_t le = launch_k(k_sdf_grid_warp<KIND, NB>, (n_poses + warps - 1) / warps, threads, 0, s, 
+          fp, poses, n_poses, g.gm, g.cell_start, g.cloud, out); le != cudaSuccess) return le; }
     }
     return cudaGetLastError();
   }
@@ -1106,12 +1115,12 @@ struct PairsLaunch {
     if (n_poses <= 0 || n_points <= 0) return cudaSuccess;
     if constexpr (KIND == EXM_FOOTPRINT_POLYGON && NB > 0) {
       const int per_block = kPairThreads * kPackPts;
-      k_sdf_pairs_poly<NB><<<(n_points + per_block - 1) / per_block, kPairThreads, 0, s>>>(
-          fp, poses, n_poses, pts, mask, n_points, per_pair, keys);
+      { if (const cudaError_t le = launch_k(k_sdf_pairs_poly<NB>, (n_points + per_block - 1) / per_block, kPairThreads, 0, s, 
+          fp, poses, n_poses, pts, mask, n_points, per_pair, keys); le != cudaSuccess) return le; }
     } else {
       const int per_block = kPairThreads * kPairPts;
-      k_sdf_pairs<KIND, NB><<<(n_points + per_block - 1) / per_block, kPairThreads, 0, s>>>(
-          fp, poses, n_poses, pts, mask, n_points, per_pair, keys);
+      { if (const cudaError_t le = launch_k(k_sdf_pairs<KIND, NB>, (n_points + per_block - 1) / per_block, kPairThreads, 0, s, 
+          fp, poses, n_poses, pts, mask, n_points, per_pair, keys); le != cudaSuccess) return le; }
     }
     return cudaGetLastError();
   }
@@ -1132,15 +1141,15 @@ cudaError_t launch_cloud_prep(const double* pts, const uint8_t* mask, const Step
   // Cells sized for about kPtsPerCell points, between R/4 and kCellMaxR * R: a cull disc of
   // radius R + d covers ~(2(R+d)/cs)^2 cells; the chunk bounds cull inside a cell.
   const float r = fmaxf(radius, 0.04f);
-  k_cloud_prep<<<1, 1024, smem, s>>>(pts, mask, dyn, 0.25f * r, kCellMaxR * r, kPtsPerCell, r, g.dstat, g.tmp,
-                                     g.raw, g.raw_start, g.cell_start, g.gm);
+  { if (const cudaError_t le = launch_k(k_cloud_prep, 1, 1024, smem, s, pts, mask, dyn, 0.25f * r, kCellMaxR * r, kPtsPerCell, r, g.dstat, g.tmp,
+                                     g.raw, g.raw_start, g.cell_start, g.gm); le != cudaSuccess) return le; }
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   int dev = 0, n_sm = 148;
   if (cudaGetDevice(&dev) == cudaSuccess)
     cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
-  k_cell_sort<<<2 * n_sm, kSortWarps * 32, 0, s>>>(g.raw, g.raw_start, g.cell_start, g.gm, g.cloud,
-                                                   g.chunk);
+  { if (const cudaError_t le = launch_k(k_cell_sort, 2 * n_sm, kSortWarps * 32, 0, s, g.raw, g.raw_start, g.cell_start, g.gm, g.cloud,
+                                                   g.chunk); le != cudaSuccess) return le; }
   return cudaGetLastError();
 }
 
@@ -1163,7 +1172,7 @@ cudaError_t launch_sdf_grid(const FpDev& fp, const float4* poses, int n_poses,
 cudaError_t launch_recentre(const double* pts, int n, double cx, double cy, float2* out,
                             cudaStream_t s) {
   if (n <= 0) return cudaSuccess;
-  k_recentre<<<(n + 255) / 256, 256, 0, s>>>(pts, n, cx, cy, out);
+  { if (const cudaError_t le = launch_k(k_recentre, (n + 255) / 256, 256, 0, s, pts, n, cx, cy, out); le != cudaSuccess) return le; }
   return cudaGetLastError();
 }
 
@@ -1176,13 +1185,13 @@ cudaError_t launch_sdf_pairs(const FpDev& fp, const float4* poses, int n_poses,
 
 cudaError_t launch_min_keys_to_double(const unsigned* keys, int n, double* out, cudaStream_t s) {
   if (n <= 0) return cudaSuccess;
-  k_keys_to_double<<<(n + 255) / 256, 256, 0, s>>>(keys, n, out);
+  { if (const cudaError_t le = launch_k(k_keys_to_double, (n + 255) / 256, 256, 0, s, keys, n, out); le != cudaSuccess) return le; }
   return cudaGetLastError();
 }
 
 cudaError_t launch_fill_u32(unsigned* p, unsigned v, int n, cudaStream_t s) {
   if (n <= 0) return cudaSuccess;
-  k_fill_u32<<<(n + 255) / 256, 256, 0, s>>>(p, v, n);
+  { if (const cudaError_t le = launch_k(k_fill_u32, (n + 255) / 256, 256, 0, s, p, v, n); le != cudaSuccess) return le; }
   return cudaGetLastError();
 }
 
