@@ -254,6 +254,15 @@ exm_status exm_step_stats(exm_handle* h, int32_t* launches_per_step, float* sdf_
  * and pairs that reached the exact signed-distance evaluation. */
 exm_status exm_sdf_cull_stats(exm_handle* h, int64_t* points_tested, int64_t* sdf_evaluated);
 
+/* Per-step hints for the culled signed distance (T floats, +inf = none): the rollout SDF first
+ * prunes every point whose lower bound reaches cap[h], then re-runs without cap the poses it
+ * left unresolved, so results are exact for any caps; good caps (a little above the step's
+ * minima) only save work; caps below the minima cost a second pass. Caps persist in the handle
+ * until set again (EXM_AUTO_CAPS=1: every committed step derives them from its own per-step
+ * d_min mean + 3 sigma). No reference counterpart (an optimisation of min_signed_distance_at,
+ * geometry.cpp:357-375). */
+exm_status exm_set_sdf_caps(exm_handle* h, const float* caps);
+
 /* Diagnostics (host only, no GPU needed): validates a footprint exactly as exm_create does and
  * returns the body-frame cull geometry the SDF kernels bound with: the bounding box
  * {xmin, xmax, ymin, ymax} (aabb_out[4]) and n_out <= 3 axis-aligned boxes

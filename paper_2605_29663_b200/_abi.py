@@ -108,6 +108,7 @@ SIGNATURES = {
     "exm_read_resident": (C.c_int32, [_Hp, _dp, _dp, C.POINTER(ExmDecision)]),
     "exm_stream": (C.c_void_p, [_Hp]),
     "exm_sdf_cull_stats": (C.c_int32, [_Hp, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
+    "exm_set_sdf_caps": (C.c_int32, [_Hp, C.POINTER(C.c_float)]),
     "exm_footprint_cull_boxes": (C.c_int32, [C.POINTER(ExmFootprint), C.POINTER(C.c_float),
                                              C.POINTER(C.c_float), C.POINTER(C.c_int32)]),
     "exm_step_stats": (C.c_int32, [_Hp, C.POINTER(C.c_int32), C.POINTER(C.c_float),

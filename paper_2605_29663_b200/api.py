@@ -474,6 +474,12 @@ class Engine:
         check(self.lib.exm_sdf_read(self.h, fptr(pairs), dptr(mins)))
         return mins, pairs
 
+    def set_sdf_caps(self, caps):
+        """Per-step cap hints of the culled SDF (exm_set_sdf_caps; exact for any values)."""
+        c = np.ascontiguousarray(np.broadcast_to(np.asarray(caps, np.float32),
+                                                 (self.params.horizon,)))
+        check(self.lib.exm_set_sdf_caps(self.h, fptr(c)))
+
     def cull_stats(self):
         """(pairs that reached a point test, pairs that reached the exact SDF) for the last
         resident step's poses (re-runs the SDF once with counters)."""

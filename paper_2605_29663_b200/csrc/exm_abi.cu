@@ -13,6 +13,7 @@
 #include <array>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -453,6 +454,8 @@ struct exm_handle {
   float4* d_poses = nullptr;
   double2* d_xy = nullptr;
   double* d_ctrl = nullptr;       // control cost per (r, h)
+  float* d_hstat = nullptr;       // per-step d_min statistic {sum[T], sum of squares[T], count}
+  float* d_cap = nullptr;         // per-step SDF caps for the next step (T; +inf: none)
   double* d_base = nullptr;
   float* d_dmin = nullptr;
   double* d_partials = nullptr;
@@ -553,10 +556,19 @@ exm_status enqueue_pre(exm_handle* h, bool draw_noise, cudaStream_t s, int* laun
   return EXM_OK;
 }
 
+bool auto_caps() {
+  static const bool on = std::getenv("EXM_AUTO_CAPS") && std::getenv("EXM_AUTO_CAPS")[0] == '1';
+  return on;
+}
+
 exm_status enqueue_post(exm_handle* h, cudaStream_t s, int* launches) {
   const StepConst& sc = h->sc;
+  // automatic per-step caps (d_min statistic -> k_finalize) measured slower than none on the
+  // benchmark configs (fallback passes): off unless EXM_AUTO_CAPS=1; exm_set_sdf_caps still works
+  float* hstat = auto_caps() ? h->d_hstat : nullptr;
   EXM_CUDA(launch_rollout_costs(sc, h->d_dyn, h->d_guide, h->guide_cap, h->d_base, h->d_ctrl,
-                                h->d_xy, h->d_dmin, h->d_cost, h->d_unsafe, h->grid.dstat, s));
+                                h->d_xy, h->d_dmin, h->d_cost, h->d_unsafe, h->grid.dstat,
+                                hstat, s));
   EXM_CUDA(launch_block_partials(sc, h->d_cost, h->d_unsafe, h->d_eps, h->d_partials, s));
   if (h->world > 1) {
     const size_t count = static_cast<size_t>(sc.nblocks_local) * partial_stride(sc.T, sc.D);
@@ -572,7 +584,7 @@ exm_status enqueue_post(exm_handle* h, cudaStream_t s, int* launches) {
                            h->d_val_dmin, s));
   EXM_CUDA(launch_finalize(sc, h->d_val_dmin, h->d_val_xy, h->d_val_base, h->d_upd, h->d_guide,
                            h->guide_cap, h->d_nominal, h->d_dyn, out_dec(h), out_dmin(h),
-                           out_nominal(h), out_uprev(h), 1, s));
+                           out_nominal(h), out_uprev(h), 1, hstat, h->d_cap, h->fp.radius, s));
   *launches += 6;
   return EXM_OK;
 }
@@ -598,7 +610,9 @@ exm_status enqueue_step(exm_handle* h, bool draw_noise, const EventPair* ev, cud
   if ((st = enqueue_pre(h, draw_noise, s, &launches)) != EXM_OK) return st;
   EXM_CUDA(cudaStreamWaitEvent(s, h->join_ev, 0));
   if (ev && (st = record_ev(ev->a, s, capturing)) != EXM_OK) return st;
-  EXM_CUDA(launch_sdf_grid(h->fp, h->d_poses, sc.k_local * sc.T, h->grid, h->d_dmin, s));
+  // capped by the previous step's per-step statistic (hybrid batches: one SDF over all families)
+  EXM_CUDA(launch_sdf_grid_capped(h->fp, h->d_poses, sc.k_local * sc.T, h->grid, h->d_cap, sc.T,
+                                  h->d_dmin, s));
   ++launches;
   if (ev && (st = record_ev(ev->b, s, capturing)) != EXM_OK) return st;
   if ((st = enqueue_post(h, s, &launches)) != EXM_OK) return st;
@@ -885,6 +899,13 @@ exm_status exm_create(const exm_footprint* footprint, const exm_model* model,
   EXM_CUDA_C(dalloc(&h->d_poses, KT));
   EXM_CUDA_C(dalloc(&h->d_xy, KT));
   EXM_CUDA_C(dalloc(&h->d_ctrl, KT));
+  EXM_CUDA_C(dalloc(&h->d_hstat, 2 * static_cast<size_t>(h->T) + 1));
+  EXM_CUDA_C(cudaMemset(h->d_hstat, 0, (2 * static_cast<size_t>(h->T) + 1) * sizeof(float)));
+  EXM_CUDA_C(dalloc(&h->d_cap, static_cast<size_t>(h->T)));
+  {
+    const std::vector<float> inf(static_cast<size_t>(h->T), HUGE_VALF);
+    EXM_CUDA_C(cudaMemcpy(h->d_cap, inf.data(), inf.size() * sizeof(float), cudaMemcpyHostToDevice));
+  }
   EXM_CUDA_C(dalloc(&h->d_cost, static_cast<size_t>(h->K)));
   EXM_CUDA_C(dalloc(&h->d_unsafe, static_cast<size_t>(h->K)));
   EXM_CUDA_C(dalloc(&h->d_base, static_cast<size_t>(h->K)));
@@ -917,7 +938,7 @@ void exm_destroy(exm_handle* h) {
   if (h->comm && g_nccl.destroy) g_nccl.destroy(h->comm);
   if (h->borrowed_poses) h->d_poses = nullptr, h->d_dmin = nullptr;
   void* dev[] = {h->d_in_block, h->d_grid_block, h->d_eps, h->d_poses, h->d_xy, h->d_ctrl,
-                 h->d_val_xy, h->d_base, h->d_dmin,
+                 h->d_hstat, h->d_cap, h->d_val_xy, h->d_base, h->d_dmin,
                  h->d_partials, h->d_upd, h->d_val_poses, h->d_val_base, h->d_val_dmin, h->d_out,
                  h->d_controls, h->d_states, h->d_cost, h->d_unsafe, h->sb_poses, h->sb_pts64,
                  h->sb_pts, h->sb_mask, h->sb_keys, h->sb_min, h->sb_pairs};
@@ -992,9 +1013,11 @@ exm_status exm_evaluate_rollouts(exm_handle* h, const double q0[3], const double
   EXM_CUDA(launch_rollout(sc, h->d_dyn, h->d_nominal, h->d_eps, 0, h->d_poses, h->d_xy, h->d_base,
                           h->d_ctrl, controls_out ? h->d_controls : nullptr,
                           states_out ? h->d_states : nullptr, s));
-  EXM_CUDA(launch_sdf_grid(h->fp, h->d_poses, static_cast<int>(KT), h->grid, h->d_dmin, s));
+  EXM_CUDA(launch_sdf_grid_capped(h->fp, h->d_poses, static_cast<int>(KT), h->grid, h->d_cap,
+                                  h->T, h->d_dmin, s));
   EXM_CUDA(launch_rollout_costs(sc, h->d_dyn, h->d_guide, h->guide_cap, h->d_base, h->d_ctrl,
-                                h->d_xy, h->d_dmin, h->d_cost, h->d_unsafe, h->grid.dstat, s));
+                                h->d_xy, h->d_dmin, h->d_cost, h->d_unsafe, h->grid.dstat,
+                                nullptr, s));
   if (controls_out)
     EXM_CUDA(cudaMemcpyAsync(controls_out, h->d_controls, KT * h->D * sizeof(double), cudaMemcpyDeviceToHost, s));
   if (states_out)
@@ -1049,7 +1072,7 @@ exm_status exm_validate_nominal(exm_handle* h, const double* nominal, const doub
                            h->d_val_dmin, s));
   EXM_CUDA(launch_finalize(sc, h->d_val_dmin, h->d_val_xy, h->d_val_base, h->d_upd, h->d_guide,
                            h->guide_cap, h->d_nominal, h->d_dyn, out_dec(h), out_dmin(h), nullptr,
-                           nullptr, 0, s));
+                           nullptr, 0, nullptr, nullptr, h->fp.radius, s));
   EXM_CUDA(cudaMemcpyAsync(h->h_out, h->d_out, h->out_bytes, cudaMemcpyDeviceToHost, s));
   EXM_CUDA(cudaStreamSynchronize(s));
   const DecisionDev* d = reinterpret_cast<const DecisionDev*>(h->h_out);
@@ -1230,6 +1253,14 @@ exm_status exm_read_resident(exm_handle* h, double* nominal_out, double* u_prev_
 
 void* exm_stream(exm_handle* h) { return h ? static_cast<void*>(h->stream) : nullptr; }
 
+exm_status exm_set_sdf_caps(exm_handle* h, const float* caps) {
+  if (!h || !caps) return fail(EXM_ERR_INVALID_ARGUMENT, "null argument");
+  EXM_CUDA(cudaSetDevice(h->device));
+  EXM_CUDA(cudaMemcpyAsync(h->d_cap, caps, sizeof(float) * h->T, cudaMemcpyHostToDevice, h->stream));
+  EXM_CUDA(cudaStreamSynchronize(h->stream));
+  return EXM_OK;
+}
+
 exm_status exm_footprint_cull_boxes(const exm_footprint* fp, float* aabb_out, float* boxes_out,
                                     int32_t* n_out) {
   FpDev d;
@@ -1253,7 +1284,8 @@ exm_status exm_sdf_cull_stats(exm_handle* h, int64_t* points_tested, int64_t* sd
   cudaStream_t s = h->stream;
   cudaError_t e = cudaMemsetAsync(d, 0, 2 * sizeof(unsigned long long), s);
   if (e == cudaSuccess)
-    e = launch_sdf_grid_stats(h->fp, h->d_poses, h->sc.k_local * h->T, h->grid, h->d_dmin, d, s);
+    e = launch_sdf_grid_stats(h->fp, h->d_poses, h->sc.k_local * h->T, h->grid, h->d_cap, h->T,
+                              h->d_dmin, d, s);
   if (e == cudaSuccess) e = cudaMemcpyAsync(hv, d, sizeof hv, cudaMemcpyDeviceToHost, s);
   if (e == cudaSuccess) e = cudaStreamSynchronize(s);
   cudaFree(d);

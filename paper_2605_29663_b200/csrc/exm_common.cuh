@@ -148,24 +148,31 @@ cudaError_t launch_rollout(const StepConst& sc, const StepDyn* dyn, const double
                            cudaStream_t s);
 cudaError_t launch_sdf_grid(const FpDev& fp, const float4* poses, int n_poses,
                             const CloudGrid& g, float* out, cudaStream_t s);
+// cap (optional, T floats): a guess of each step's minimum distance; the kernel stays exact
+// for any cap (capped pass, then an uncapped pass for the poses it did not resolve).
+cudaError_t launch_sdf_grid_capped(const FpDev& fp, const float4* poses, int n_poses,
+                                   const CloudGrid& g, const float* cap, int T, float* out,
+                                   cudaStream_t s);
 cudaError_t launch_sdf_grid_stats(const FpDev& fp, const float4* poses, int n_poses,
-                                  const CloudGrid& g, float* out, unsigned long long* stats,
-                                  cudaStream_t s);
+                                  const CloudGrid& g, const float* cap, int T, float* out,
+                                  unsigned long long* stats, cudaStream_t s);
 cudaError_t launch_rollout_costs(const StepConst& sc, const StepDyn* dyn, const double* guide,
                                  int guide_cap, const double* base_cost, const double* ctrl_cost,
                                  const double2* xy, const float* dmin, double* cost,
-                                 uint8_t* unsafe, float* dstat, cudaStream_t s);
+                                 uint8_t* unsafe, float* dstat, float* hstat, cudaStream_t s);
 cudaError_t launch_block_partials(const StepConst& sc, const double* cost, const uint8_t* unsafe,
                                   const double* eps, double* partials, cudaStream_t s);
 // val_base: T + 1 doubles {terminal cost, control cost of every step} of the validation rollout
 cudaError_t launch_update(const StepConst& sc, const double* partials, const double* nominal,
                           const StepDyn* dyn, double* upd, float4* val_poses, double2* val_xy,
                           double* val_base, DecisionDev* dec, int merge, cudaStream_t s);
+// hstat ({sum d, sum d^2} per step + count, from k_rollout_costs) -> cap: the next step's
+// per-step SDF caps (both optional; commit steps only).
 cudaError_t launch_finalize(const StepConst& sc, const float* val_dmin, const double2* val_xy,
                             const double* val_base, const double* upd, const double* guide,
                             int guide_cap, double* nominal, StepDyn* dyn, DecisionDev* dec,
                             double* out_dmin, double* out_nominal, double* out_uprev, int commit,
-                            cudaStream_t s);
+                            float* hstat, float* cap, float radius, cudaStream_t s);
 cudaError_t launch_recentre(const double* pts, int n, double cx, double cy, float2* out,
                             cudaStream_t s);
 cudaError_t launch_sdf_pairs(const FpDev& fp, const float4* poses, int n_poses,

@@ -140,6 +140,9 @@ __device__ __forceinline__ double noise_at(const StepConst& sc, uint64_t row_key
 
 constexpr int kRolloutWarps = 4;  // rollouts (warps) per CTA in k_rollout
 constexpr float kDstatClamp = 16.0f;       // d_min clamp in that mean (empty clouds: 1e6)
+constexpr int kHstatEvery = 4;             // rollout blocks sampled for the per-step statistic
+constexpr float kCapSigma = 3.0f;          // cap = mean + kCapSigma * std (+ kCapSlack * R)
+constexpr float kCapSlack = 0.02f;
 constexpr int kPartialThreads = 1024;  // 32 warps: 8 rollouts per warp in the U sums
 
 // The serial part of one rollout (score_rollout, controller.cpp:151-169, minus the SDF and the
@@ -330,12 +333,17 @@ __global__ void __launch_bounds__(kCostWarps * 32) k_rollout_costs(
     const StepConst sc, const StepDyn* __restrict__ dynp, const double* __restrict__ guide,
     const double* __restrict__ base_cost, const double* __restrict__ ctrl_cost,
     const double2* __restrict__ xy, const float* __restrict__ dmin, double* __restrict__ cost,
-    uint8_t* __restrict__ unsafe, float* __restrict__ dstat) {
+    uint8_t* __restrict__ unsafe, float* __restrict__ dstat, float* __restrict__ hstat) {
   pdl_wait();
-  extern __shared__ double g[];  // guide (2*ng), then per warp: task[T], obst[T]
+  extern __shared__ double g[];  // guide (2*ng), per warp: task[T], obst[T]; then 2T floats
   __shared__ float red[2][kCostWarps];
   const int ng = dynp->n_guide, T = sc.T;
+  float* sh = reinterpret_cast<float*>(g + 2 * ng + kCostWarps * 2 * T);
+  // every kHstatEvery-th block samples the per-step d_min statistic (k_finalize -> caps)
+  const bool sampled = hstat != nullptr && blockIdx.x % kHstatEvery == 0;
   for (int i = threadIdx.x; i < 2 * ng; i += blockDim.x) g[i] = guide[i];
+  if (sampled)
+    for (int i = threadIdx.x; i < 2 * T; i += blockDim.x) sh[i] = 0.f;
   __syncthreads();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   double* s_t = g + 2 * ng + warp * 2 * T;
@@ -355,6 +363,11 @@ __global__ void __launch_bounds__(kCostWarps * 32) k_rollout_costs(
       s_o[h] = obstacle_cost(sc, d);
       bad |= d < sc.d_safe;
       dc += fminf(fmaxf(df, 0.f), kDstatClamp);
+      if (sampled) {
+        const float dv = fminf(df, kDstatClamp);
+        atomicAdd(&sh[h], dv);
+        atomicAdd(&sh[T + h], dv * dv);
+      }
     }
     __syncwarp();
     if (lane == 0) {
@@ -376,6 +389,14 @@ __global__ void __launch_bounds__(kCostWarps * 32) k_rollout_costs(
     red[1][warp] = live ? static_cast<float>(T) : 0.f;
   }
   __syncthreads();
+  if (sampled) {
+    for (int i = threadIdx.x; i < 2 * T; i += blockDim.x) atomicAdd(&hstat[i], sh[i]);
+    if (threadIdx.x == 0) {
+      int n = 0;
+      for (int w = 0; w < kCostWarps; ++w) n += blockIdx.x * kCostWarps + w < sc.k_local;
+      atomicAdd(&hstat[2 * T], static_cast<float>(n));
+    }
+  }
   if (threadIdx.x == 0) {  // one atomic pair per block
     float a = 0.f, c = 0.f;
     for (int w = 0; w < kCostWarps; ++w) {
@@ -585,7 +606,8 @@ __global__ void __launch_bounds__(64) k_finalize(
     const double* __restrict__ val_base, const double* __restrict__ upd,
     const double* __restrict__ guide, double* __restrict__ nominal, StepDyn* __restrict__ dyn,
     DecisionDev* __restrict__ dec, double* __restrict__ out_dmin,
-    double* __restrict__ out_nominal, double* __restrict__ out_uprev, int commit) {
+    double* __restrict__ out_nominal, double* __restrict__ out_uprev, int commit,
+    float* __restrict__ hstat, float* __restrict__ cap, float radius) {
   pdl_wait();
   extern __shared__ double sm2[];  // guide (2*ng) then per-step task (T) and obstacle (T) costs
   __shared__ int s_ok;
@@ -619,6 +641,23 @@ __global__ void __launch_bounds__(64) k_finalize(
     dec->validated = ok;
   }
   if (!commit) return;
+  if (hstat != nullptr) {
+    // next step's per-step caps for k_sdf_grid: that step's nominal is this one shifted by one,
+    // so its step h looks like this step's h + 1 (a guess only: the SDF is exact for any cap)
+    const float n = hstat[2 * T];
+    for (int h = tid; h < T; h += blockDim.x) {
+      const int src = h + 1 < T ? h + 1 : T - 1;
+      float c = __int_as_float(0x7f800000);
+      if (n > 0.f) {
+        const float m = hstat[src] / n;
+        const float v = fmaxf(hstat[T + src] / n - m * m, 0.f);
+        c = m + kCapSigma * sqrtf(v) + kCapSlack * radius;
+      }
+      cap[h] = c;
+    }
+    __syncthreads();
+    for (int i = tid; i <= 2 * T; i += blockDim.x) hstat[i] = 0.f;
+  }
   for (int i = tid; i < T * D; i += blockDim.x) {
     const int h = i / D;
     const double v = ok ? upd[(h + 1 < T ? h + 1 : T - 1) * D + i % D] : 0.0;
@@ -679,17 +718,17 @@ cudaError_t launch_rollout(const StepConst& sc, const StepDyn* dyn, const double
 cudaError_t launch_rollout_costs(const StepConst& sc, const StepDyn* dyn, const double* guide,
                                  int guide_cap, const double* base_cost, const double* ctrl_cost,
                                  const double2* xy, const float* dmin, double* cost,
-                                 uint8_t* unsafe, float* dstat, cudaStream_t s) {
+                                 uint8_t* unsafe, float* dstat, float* hstat, cudaStream_t s) {
   if (sc.k_local <= 0) return cudaSuccess;
-  const size_t smem = sizeof(double) * 2 * (static_cast<size_t>(guide_cap) +
-                                            static_cast<size_t>(kCostWarps) * sc.T);
+  const size_t smem = sizeof(double) * (2 * (static_cast<size_t>(guide_cap) +
+                                             static_cast<size_t>(kCostWarps) * sc.T) + sc.T);
   if (smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(k_rollout_costs, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(smem));
     if (e != cudaSuccess) return e;
   }
   { if (const cudaError_t le = launch_k(k_rollout_costs, (sc.k_local + kCostWarps - 1) / kCostWarps, kCostWarps * 32, smem, s, 
-      sc, dyn, guide, base_cost, ctrl_cost, xy, dmin, cost, unsafe, dstat); le != cudaSuccess) return le; }
+      sc, dyn, guide, base_cost, ctrl_cost, xy, dmin, cost, unsafe, dstat, hstat); le != cudaSuccess) return le; }
   return cudaGetLastError();
 }
 
@@ -741,7 +780,7 @@ cudaError_t launch_finalize(const StepConst& sc, const float* val_dmin, const do
                             const double* val_base, const double* upd, const double* guide,
                             int guide_cap, double* nominal, StepDyn* dyn, DecisionDev* dec,
                             double* out_dmin, double* out_nominal, double* out_uprev, int commit,
-                            cudaStream_t s) {
+                            float* hstat, float* cap, float radius, cudaStream_t s) {
   const size_t smem = sizeof(double) * (2 * static_cast<size_t>(guide_cap) + 2 * sc.T);
   if (smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(k_finalize, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -749,7 +788,7 @@ cudaError_t launch_finalize(const StepConst& sc, const float* val_dmin, const do
     if (e != cudaSuccess) return e;
   }
   { if (const cudaError_t le = launch_k(k_finalize, 1, 64, smem, s, sc, val_dmin, val_xy, val_base, upd, guide, nominal, dyn, dec,
-                                 out_dmin, out_nominal, out_uprev, commit); le != cudaSuccess) return le; }
+                                 out_dmin, out_nominal, out_uprev, commit, hstat, cap, radius); le != cudaSuccess) return le; }
   return cudaGetLastError();
 }
 

@@ -554,6 +554,7 @@ __global__ void __launch_bounds__(128) k_sdf_grid(const __grid_constant__ FpDev 
                                                   const int* __restrict__ cell_start,
                                                   const float2* __restrict__ cloud,
                                                   const float4* __restrict__ chunk,
+                                                  const float* __restrict__ cap, int T,
                                                   float* __restrict__ out,
                                                   unsigned long long* __restrict__ stats = nullptr) {
   pdl_wait();
@@ -580,8 +581,21 @@ __global__ void __launch_bounds__(128) k_sdf_grid(const __grid_constant__ FpDev 
   const float mg = gm.margin;
   const WBox w = world_box(fp, q, mg);
   const float R = fp.radius + mg;
-  float best = __int_as_float(0x7f800000);
   const int kmax = max(max(ci, gm.gx - 1 - ci), max(cj, gm.gy - 1 - cj));
+  // Capped first pass: cap[h] is a guess of step h's minimum (from the previous control step).
+  // Bounds at or above the cap are pruned as if a point at distance cap had been evaluated, so a
+  // pose whose true minimum m* lies below the cap still gets m* exactly (no point with sd = m*
+  // is ever pruned: its bound is <= m* < best); poses left at the cap rerun uncapped (pass 1).
+  const float kInf = __int_as_float(0x7f800000);
+  const float capv = (cap != nullptr && active && MODE != kGridBrute) ? cap[i % T] : kInf;
+  float best = capv;
+  bool todo = active;
+  for (int pass = 0; pass < 2; ++pass) {
+  if (pass == 1) {
+    todo = active && !(best < capv);
+    if (!__any_sync(kFull, todo)) break;
+    if (todo) best = kInf;
+  }
   for (int k = 0; k <= kmax; ++k) {
     if (k > 0) {
       // every point of ring k or beyond lies outside the inner square S_{k-1}
@@ -594,7 +608,7 @@ __global__ void __launch_bounds__(128) k_sdf_grid(const __grid_constant__ FpDev 
       const float lbw = fminf(fminf(w.x0 - bx0, bx1 - w.x1), fminf(w.y0 - by0, by1 - w.y1));
       const float lbc = fminf(fminf(q.x - bx0, bx1 - q.x), fminf(q.y - by0, by1 - q.y)) - R;
       const float lb = lbw > 0.f ? fmaxf(lbw, lbc) : lbc;
-      const bool need = active && (MODE == kGridBrute || lb < best + mg);
+      const bool need = todo && (MODE == kGridBrute || lb < best + mg);
       if (!__any_sync(kFull, need)) break;
     }
     const int ncell = k == 0 ? 1 : 8 * k;
@@ -610,7 +624,7 @@ __global__ void __launch_bounds__(128) k_sdf_grid(const __grid_constant__ FpDev 
       const float gx_ = fmaxf(fmaxf(bx0 - q.x, q.x - bx1), 0.f);
       const float gy_ = fmaxf(fmaxf(by0 - q.y, q.y - by1), 0.f);
       const float lim = R + best;
-      const bool need = active && (MODE == kGridBrute || ((gx_ * gx_ + gy_ * gy_ < lim * lim) &&
+      const bool need = todo && (MODE == kGridBrute || ((gx_ * gx_ + gy_ * gy_ < lim * lim) &&
                                    box_may_beat(w, bx0, bx1, by0, by1, best, mg)));
       if (!__any_sync(kFull, need)) continue;
       float l2 = lim * lim;
@@ -647,6 +661,7 @@ __global__ void __launch_bounds__(128) k_sdf_grid(const __grid_constant__ FpDev 
       }
     }
   }
+  }  // pass
   if (active) out[i] = best;
   if (STATS) {
     atomicAdd(stats, n_test);
@@ -1057,19 +1072,19 @@ inline const char* grid_mode() {
 template <int KIND, int NB>
 struct GridLaunch {
   static cudaError_t run(const FpDev& fp, const float4* poses, int n_poses, const CloudGrid& g,
-                         float* out, cudaStream_t s) {
+                         const float* cap, int T, float* out, cudaStream_t s) {
     if (n_poses <= 0) return cudaSuccess;
     const int threads = 128, blocks = (n_poses + threads - 1) / threads;
     const char* m = grid_mode();
     if (!strcmp(m, "brute"))
       { if (const cudaError_t le = launch_k(k_sdf_grid<KIND, NB, false, kGridBrute>, blocks, threads, 0, s, 
-          fp, poses, n_poses, g.gm, g.cell_start, g.cloud, g.chunk, out, nullptr); le != cudaSuccess) return le; }
+          fp, poses, n_poses, g.gm, g.cell_start, g.cloud, g.chunk, cap, T, out, nullptr); le != cudaSuccess) return le; }
     else if (!strcmp(m, "nochunk"))
       { if (const cudaError_t le = launch_k(k_sdf_grid<KIND, NB, false, kGridNoChunk>, blocks, threads, 0, s, 
-          fp, poses, n_poses, g.gm, g.cell_start, g.cloud, g.chunk, out, nullptr); le != cudaSuccess) return le; }
+          fp, poses, n_poses, g.gm, g.cell_start, g.cloud, g.chunk, cap, T, out, nullptr); le != cudaSuccess) return le; }
     else
       { if (const cudaError_t le = launch_k(k_sdf_grid<KIND, NB>, blocks, threads, 0, s, fp, poses, n_poses, g.gm, g.cell_start,
-                                                      g.cloud, g.chunk, out, nullptr); le != cudaSuccess) return le; }
+                                                      g.cloud, g.chunk, cap, T, out, nullptr); le != cudaSuccess) return le; }
     return cudaGetLastError();
   }
 };
@@ -1077,15 +1092,17 @@ struct GridLaunch {
 template <int KIND, int NB>
 struct GridStatsLaunch {
   static cudaError_t run(const FpDev& fp, const float4* poses, int n_poses, const CloudGrid& g,
-                         float* out, unsigned long long* stats, cudaStream_t s) {
+                         const float* cap, int T, float* out, unsigned long long* stats,
+                         cudaStream_t s) {
     if (n_poses <= 0) return cudaSuccess;
     const int threads = 128, blocks = (n_poses + threads - 1) / threads;
+    if (!strcmp(grid_mode(), "nocap")) cap = nullptr;
     if (!strcmp(grid_mode(), "nochunk"))
       { if (const cudaError_t le = launch_k(k_sdf_grid<KIND, NB, true, kGridNoChunk>, blocks, threads, 0, s, 
-          fp, poses, n_poses, g.gm, g.cell_start, g.cloud, g.chunk, out, stats); le != cudaSuccess) return le; }
+          fp, poses, n_poses, g.gm, g.cell_start, g.cloud, g.chunk, cap, T, out, stats); le != cudaSuccess) return le; }
     else
       { if (const cudaError_t le = launch_k(k_sdf_grid<KIND, NB, true>, blocks, threads, 0, s, fp, poses, n_poses, g.gm,
-                                                            g.cell_start, g.cloud, g.chunk, out, stats); le != cudaSuccess) return le; }
+                                                            g.cell_start, g.cloud, g.chunk, cap, T, out, stats); le != cudaSuccess) return le; }
     return cudaGetLastError();
   }
 };
@@ -1154,19 +1171,26 @@ cudaError_t launch_cloud_prep(const double* pts, const uint8_t* mask, const Step
 }
 
 cudaError_t launch_sdf_grid_stats(const FpDev& fp, const float4* poses, int n_poses,
-                                  const CloudGrid& g, float* out, unsigned long long* stats,
-                                  cudaStream_t s) {
-  return dispatch_fp<GridStatsLaunch>(fp, poses, n_poses, g, out, stats, s);
+                                  const CloudGrid& g, const float* cap, int T, float* out,
+                                  unsigned long long* stats, cudaStream_t s) {
+  return dispatch_fp<GridStatsLaunch>(fp, poses, n_poses, g, cap, T, out, stats, s);
 }
 
-cudaError_t launch_sdf_grid(const FpDev& fp, const float4* poses, int n_poses,
-                            const CloudGrid& g, float* out, cudaStream_t s) {
+cudaError_t launch_sdf_grid_capped(const FpDev& fp, const float4* poses, int n_poses,
+                                   const CloudGrid& g, const float* cap, int T, float* out,
+                                   cudaStream_t s) {
   // Few poses (validation rollout, single queries): one warp per pose keeps all lanes busy.
   const char* m = grid_mode();
   const bool warp = !strcmp(m, "warp") || !strcmp(m, "cta") ||
                     (n_poses <= kWarpPerPoseMax && strcmp(m, "thread") && strcmp(m, "brute"));
   if (warp) return dispatch_fp<GridWarpLaunch>(fp, poses, n_poses, g, out, s);
-  return dispatch_fp<GridLaunch>(fp, poses, n_poses, g, out, s);
+  if (!strcmp(m, "nocap")) cap = nullptr;
+  return dispatch_fp<GridLaunch>(fp, poses, n_poses, g, cap, T, out, s);
+}
+
+cudaError_t launch_sdf_grid(const FpDev& fp, const float4* poses, int n_poses,
+                            const CloudGrid& g, float* out, cudaStream_t s) {
+  return launch_sdf_grid_capped(fp, poses, n_poses, g, nullptr, 1, out, s);
 }
 
 cudaError_t launch_recentre(const double* pts, int n, double cx, double cy, float2* out,

@@ -35,11 +35,13 @@ CASES = {
 }
 
 
-def _dmin(wl, mode):
+def _dmin(wl, mode, caps=None):
     old = os.environ.get("EXM_GRID_MODE")
     os.environ["EXM_GRID_MODE"] = mode
     try:
         eng = Engine(wl.model, wl.limits, wl.footprint, wl.params, n_cap=wl.n_points, guide_cap=8)
+        if caps is not None:
+            eng.set_sdf_caps(caps)
         nom, up = wl.zero_state()
         eps = eng.sample_perturbations(wl.params.seed, 0)
         # a few cycles' worth of distinct pose sets: nominal offsets
@@ -65,3 +67,17 @@ def test_culled_minimum_is_bitwise_brute_force(case, mode):
     assert got.shape == want.shape
     bad = np.flatnonzero(got != want)
     assert bad.size == 0, f"{bad.size} poses differ, e.g. {bad[:5]}: {got[bad[:5]]} vs {want[bad[:5]]}"
+
+
+@pytest.mark.parametrize("case", ["cfg2_L12", "cfg3_forklift", "cfg5_L6_overlap"])
+def test_capped_minimum_is_bitwise_brute_force(case):
+    """Caps (per-step hints) only prune: caps far below, around and above the true minima, and
+    a per-step mix, all give the brute-force minima bit for bit."""
+    wl = CASES[case]()
+    want = _dmin(wl, "brute")
+    T = wl.params.horizon
+    per_step = np.quantile(want.reshape(-1, T), 0.5, axis=0).astype(np.float32)  # half resolve
+    for caps in (-1.0, 0.05, 0.3, 5.0, per_step):
+        got = _dmin(wl, "thread", caps)
+        bad = np.flatnonzero(got != want)
+        assert bad.size == 0, (caps, bad.size)
