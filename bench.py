@@ -338,6 +338,7 @@ def run_ours(args, world, rank, local):
         line["sdf_batch"] = bench_sdf_batch(args, torch, peak, peak_src)
     if rank == 0 and not args.no_sdf_batch:
         line["hybrid"] = bench_hybrid(args, torch)
+        line["sense"] = bench_sense(args, world == 1 and not args.no_cpu_baseline)
     if rank == 0:
         print(json.dumps(line), flush=True)
 
@@ -405,6 +406,51 @@ def bench_hybrid(args, torch):
     return {"workload": "trap_hybrid 3 families (ackermann/parallel/spin), K=384, T=25, N=400",
             "batched_ms_per_step": 1e3 * batched, "per_family_calls_ms_per_step": 1e3 * seq,
             "speedup": seq / batched}
+
+
+def bench_sense(args, with_cpu):
+    """sense() (world.cpp:182-243) for the config-5 world (omni_gap walls + 64
+    discs displaced along their trails, the cycle-10 positions) seen from q0, range 10 m, budget
+    720: exm_sense (host API: host obstacles in, host ObstacleSet out) vs the reference's own
+    sense() from oracle/_ref on one host core (the reference is single-threaded here)."""
+    import math as _m
+    from paper_2605_29663_b200 import workloads as W
+    from paper_2605_29663_b200.api import Engine, WorldObstacle
+    obs = [WorldObstacle.polygon(p) for p in W.OMNI_WALLS]
+    t = 1.0
+    for k in range(64):
+        ax, ay = W.uniform_range(9, k, 0, -8.0, 8.0), W.uniform_range(9, k, 1, -8.0, 8.0)
+        bx, by = W.uniform_range(9, k, 2, -8.0, 8.0), W.uniform_range(9, k, 3, -8.0, 8.0)
+        r = W.uniform_range(9, k, 4, 0.2, 0.5)
+        v = W.uniform_range(9, k, 5, 0.0, 0.2)
+        L = _m.hypot(bx - ax, by - ay)
+        sarc = (v * t) % (2 * L) if L > 0 else 0.0
+        sarc = sarc if sarc <= L else 2 * L - sarc
+        f = sarc / L if L > 0 else 0.0
+        obs.append(WorldObstacle.disc((ax, ay), r, (f * (bx - ax), f * (by - ay))))
+    wl = W.cfg1(K=32, T=4)
+    eng = Engine(wl.model, wl.limits, wl.footprint, wl.params, n_cap=16, guide_cap=4)
+    robot = np.array([-4.0, 0.0, 0.0])
+    for _ in range(3):
+        cloud = eng.sense(obs, robot, 10.0, 720, 7, 0)
+    n = max(20, args.steps // 4)
+    t0 = time.perf_counter()
+    for c in range(n):
+        cloud = eng.sense(obs, robot, 10.0, 720, 7, c)
+    gpu = (time.perf_counter() - t0) / n
+    out = {"workload": "cfg5 world: 2 walls + 64 moving discs, range 10 m, budget 720",
+           "visible_points": int(cloud.mask.sum()), "exm_sense_ms": 1e3 * gpu}
+    if with_cpu:
+        sys.path.insert(0, ROOT)
+        from tests.oracle_bindings import reference_available, reference_sense
+        if reference_available():
+            reference_sense(obs, robot, 10.0, 720, 7, 0)
+            t0 = time.perf_counter()
+            for c in range(n):
+                reference_sense(obs, robot, 10.0, 720, 7, c)
+            cpu = (time.perf_counter() - t0) / n
+            out.update({"reference_sense_ms": 1e3 * cpu, "cores": 1, "speedup": cpu / gpu})
+    return out
 
 
 def main():

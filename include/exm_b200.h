@@ -254,6 +254,29 @@ exm_status exm_step_stats(exm_handle* h, int32_t* launches_per_step, float* sdf_
  * and pairs that reached the exact signed-distance evaluation. */
 exm_status exm_sdf_cull_stats(exm_handle* h, int64_t* points_tested, int64_t* sdf_evaluated);
 
+/* ---- sensing (world.cpp:182-243) ---------------------------------------- */
+enum { EXM_OBSTACLE_POLYGON = 0, EXM_OBSTACLE_DISC = 1 };
+/* One scenario obstacle (world.hpp Obstacle): a polygon as PolygonFootprint stores it (CCW
+ * vertices) or a disc {centre x[0], y[0]; radius}, displaced by its current trail offset
+ * (obstacle_offset, world.cpp:159-164). */
+typedef struct exm_world_obstacle {
+  int32_t kind;
+  int32_t count; /* polygon vertices (disc: 1) */
+  const double* x;
+  const double* y;
+  double radius;
+  double offset[2];
+} exm_world_obstacle;
+
+/* sense(scenario, state, robot, sample_key) (world.cpp:182-243) on the device: boundary
+ * samples every 0.05 m, nearest sample per 720 angular bins within `range`, exact line of
+ * sight, seeded partial Fisher-Yates downsample to `budget` (scenario seed), padded to
+ * `budget` (ObstacleSet::padded: (1e9, 1e9), mask 0). Outputs pts_out[2*budget],
+ * mask_out[budget], *n_valid. Errors: budget < 1 ("sensor budget must be >= 1"). */
+exm_status exm_sense(exm_handle* h, const exm_world_obstacle* obstacles, int32_t n_obstacles,
+                     const double robot[3], double range, int32_t budget, uint64_t seed,
+                     uint64_t sample_key, double* pts_out, uint8_t* mask_out, int32_t* n_valid);
+
 /* Per-step hints for the culled signed distance (T floats, +inf = none): the rollout SDF first
  * prunes every point whose lower bound reaches cap[h], then re-runs without cap the poses it
  * left unresolved, so results are exact for any caps; good caps (a little above the step's

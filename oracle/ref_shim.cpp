@@ -9,6 +9,7 @@
 //   PreparedFootprint::sd, batch_signed_distance, min_signed_distance_at
 //   sample_perturbations, evaluate_rollouts, weights_from_costs, validate_nominal
 //   MppiController::control_cycle                              (controller.hpp)
+//   sense                                                      (world.hpp)
 #include <cstring>
 #include <exception>
 #include <memory>
@@ -19,6 +20,7 @@
 #include "exactmppi/geometry.hpp"
 #include "exactmppi/hybrid.hpp"
 #include "exactmppi/kinematics.hpp"
+#include "exactmppi/world.hpp"
 #include "exm_b200.h"
 
 using namespace exactmppi;
@@ -346,3 +348,42 @@ int32_t ref_hybrid_cycle(void* hp, const double q0[3], const double* pts, const 
 }
 
 }  // extern "C"
+
+// sense(scenario, state, robot, key) with the given obstacles displaced by their offsets
+// (geometry translated here, no trail motion: the reference then adds a zero offset).
+extern "C" int ref_sense(const exm_world_obstacle* obs, int n, const double robot[3], double range,
+                         int budget, uint64_t seed, uint64_t sample_key, double* pts_out,
+                         uint8_t* mask_out, int* n_valid) {
+  try {
+    Scenario sc;
+    sc.sensor.range = range;
+    sc.sensor.budget = budget;
+    sc.seed = seed;
+    for (int i = 0; i < n; ++i) {
+      const exm_world_obstacle& o = obs[i];
+      Obstacle ob;
+      if (o.kind == EXM_OBSTACLE_DISC) {
+        ob.shape = Disc{{o.x[0] + o.offset[0], o.y[0] + o.offset[1]}, o.radius};
+      } else {
+        std::vector<Point2> v;
+        for (int k = 0; k < o.count; ++k) v.push_back({o.x[k] + o.offset[0], o.y[k] + o.offset[1]});
+        ob.shape = PolygonFootprint::make(v);
+      }
+      sc.obstacles.push_back(std::move(ob));
+    }
+    const WorldState st = WorldState::initial(sc);
+    const ObstacleSet set = sense(sc, st, Pose2{robot[0], robot[1], robot[2]}, sample_key);
+    int nv = 0;
+    for (std::size_t i = 0; i < set.points.size(); ++i) {
+      pts_out[2 * i] = set.points[i].x;
+      pts_out[2 * i + 1] = set.points[i].y;
+      mask_out[i] = set.mask[i];
+      nv += set.mask[i] != 0;
+    }
+    *n_valid = nv;
+    return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return 1;
+  }
+}

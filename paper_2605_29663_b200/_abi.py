@@ -31,6 +31,14 @@ _u8p = C.POINTER(C.c_uint8)
 _fp = C.POINTER(C.c_float)
 
 
+class ExmWorldObstacle(C.Structure):
+    _fields_ = [("kind", C.c_int32), ("count", C.c_int32), ("x", C.POINTER(C.c_double)),
+                ("y", C.POINTER(C.c_double)), ("radius", C.c_double), ("offset", C.c_double * 2)]
+
+
+OBSTACLE_POLYGON, OBSTACLE_DISC = 0, 1
+
+
 class ExmFootprint(C.Structure):
     _fields_ = [("kind", C.c_int32), ("count", C.c_int32), ("x", _dp), ("y", _dp),
                 ("hx", _dp), ("hy", _dp)]
@@ -109,6 +117,9 @@ SIGNATURES = {
     "exm_stream": (C.c_void_p, [_Hp]),
     "exm_sdf_cull_stats": (C.c_int32, [_Hp, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
     "exm_set_sdf_caps": (C.c_int32, [_Hp, C.POINTER(C.c_float)]),
+    "exm_sense": (C.c_int32, [_Hp, C.POINTER(ExmWorldObstacle), C.c_int32, _dp, C.c_double,
+                              C.c_int32, C.c_uint64, C.c_uint64, _dp, _u8p,
+                              C.POINTER(C.c_int32)]),
     "exm_footprint_cull_boxes": (C.c_int32, [C.POINTER(ExmFootprint), C.POINTER(C.c_float),
                                              C.POINTER(C.c_float), C.POINTER(C.c_int32)]),
     "exm_step_stats": (C.c_int32, [_Hp, C.POINTER(C.c_int32), C.POINTER(C.c_float),

@@ -37,6 +37,49 @@ K_PADDED_COORDINATE = 1e9    # geometry.hpp:35
 
 # ------------------------------------------------------------------------------ types
 @dataclass
+class WorldObstacle:
+    """A scenario obstacle for sensing (world.hpp Obstacle): a polygon (vertices, CCW as
+    PolygonFootprint stores them; CW input is reversed like PolygonFootprint::make) or a disc
+    (center, radius), displaced by its current trail offset (obstacle_offset, world.cpp:159-164)."""
+    vertices: np.ndarray | None = None
+    center: Sequence[float] | None = None
+    radius: float = 0.0
+    offset: Sequence[float] = (0.0, 0.0)
+
+    @staticmethod
+    def polygon(vertices, offset=(0.0, 0.0)) -> "WorldObstacle":
+        v = np.ascontiguousarray(np.asarray(vertices, np.float64).reshape(-1, 2))
+        area2 = float(np.sum(v[:, 0] * np.roll(v[:, 1], -1) - v[:, 1] * np.roll(v[:, 0], -1)))
+        if area2 < 0.0:
+            v = np.ascontiguousarray(v[::-1])
+        return WorldObstacle(vertices=v, offset=tuple(offset))
+
+    @staticmethod
+    def disc(center, radius, offset=(0.0, 0.0)) -> "WorldObstacle":
+        return WorldObstacle(center=tuple(center), radius=float(radius), offset=tuple(offset))
+
+    def _c(self):
+        if self.vertices is not None:
+            x = np.ascontiguousarray(self.vertices[:, 0])
+            y = np.ascontiguousarray(self.vertices[:, 1])
+            o = _abi.ExmWorldObstacle(_abi.OBSTACLE_POLYGON, x.size, dptr(x), dptr(y), 0.0,
+                                      (C.c_double * 2)(*self.offset))
+        else:
+            x = np.array([self.center[0]], np.float64)
+            y = np.array([self.center[1]], np.float64)
+            o = _abi.ExmWorldObstacle(_abi.OBSTACLE_DISC, 1, dptr(x), dptr(y), self.radius,
+                                      (C.c_double * 2)(*self.offset))
+        return o, (x, y)
+
+
+def world_obstacles_c(obstacles):
+    """ctypes array of exm_world_obstacle plus the buffers it points into."""
+    items = [o._c() for o in obstacles]
+    arr = (_abi.ExmWorldObstacle * max(len(items), 1))(*[it[0] for it in items])
+    return arr, [it[1] for it in items]
+
+
+@dataclass
 class FootprintSpec:
     """Exactly one of a simple polygon (CCW, validated by the library) or a rectangle cover."""
     kind: int
@@ -473,6 +516,20 @@ class Engine:
         pairs = np.empty((P, N), np.float32) if per_pair else None
         check(self.lib.exm_sdf_read(self.h, fptr(pairs), dptr(mins)))
         return mins, pairs
+
+    def sense(self, obstacles, robot, sensor_range: float, budget: int, seed: int,
+              sample_key: int):
+        """sense(scenario, state, robot, sample_key) on the device (exm_sense,
+        world.cpp:182-243) -> ObstacleSet padded to `budget` (points (budget, 2), mask)."""
+        arr, keep = world_obstacles_c(obstacles)
+        pts = np.empty((budget, 2))
+        mask = np.empty(budget, np.uint8)
+        n = C.c_int32()
+        check(self.lib.exm_sense(self.h, arr, len(obstacles), dptr(self._vec3(robot)),
+                                 float(sensor_range), int(budget), int(seed), int(sample_key),
+                                 dptr(pts), u8ptr(mask), C.byref(n)))
+        del keep
+        return ObstacleSet(pts, mask)
 
     def set_sdf_caps(self, caps):
         """Per-step cap hints of the culled SDF (exm_set_sdf_caps; exact for any values)."""

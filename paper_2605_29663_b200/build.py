@@ -8,13 +8,13 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "lib", "libexm_b200.so")
-SOURCES = ["exm_kernels.cu", "exm_dynamics.cu", "exm_abi.cu"]
+SOURCES = ["exm_kernels.cu", "exm_dynamics.cu", "exm_world.cu", "exm_abi.cu"]
 HEADERS = ["exm_common.cuh", "exm_device.cuh"]
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo", "-O3", "-std=c++17",
               "-Xcompiler", "-fPIC", "-Xcompiler", "-Wall"]
 # Per-unit flags: the FP64 dynamics round every product and sum separately, as the reference's
 # x86-64 build does (no FMA contraction); the FP32 signed-distance kernels fuse explicitly.
-UNIT_FLAGS = {"exm_dynamics.cu": ["-fmad=false"]}
+UNIT_FLAGS = {"exm_dynamics.cu": ["-fmad=false"], "exm_world.cu": ["-fmad=false"]}
 
 
 def _stale(target: str, deps) -> bool:

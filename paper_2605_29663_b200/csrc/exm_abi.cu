@@ -75,6 +75,7 @@ struct NcclApi {
   }
 };
 NcclApi g_nccl;
+constexpr double kPiHost = 3.14159265358979323846;  // std::numbers::pi
 
 template <class T>
 cudaError_t dalloc(T** p, size_t count) {
@@ -454,6 +455,8 @@ struct exm_handle {
   float4* d_poses = nullptr;
   double2* d_xy = nullptr;
   double* d_ctrl = nullptr;       // control cost per (r, h)
+  void* d_sense = nullptr;        // exm_sense workspace (segments, obstacles, output)
+  size_t sense_bytes = 0;
   float* d_hstat = nullptr;       // per-step d_min statistic {sum[T], sum of squares[T], count}
   float* d_cap = nullptr;         // per-step SDF caps for the next step (T; +inf: none)
   double* d_base = nullptr;
@@ -938,7 +941,7 @@ void exm_destroy(exm_handle* h) {
   if (h->comm && g_nccl.destroy) g_nccl.destroy(h->comm);
   if (h->borrowed_poses) h->d_poses = nullptr, h->d_dmin = nullptr;
   void* dev[] = {h->d_in_block, h->d_grid_block, h->d_eps, h->d_poses, h->d_xy, h->d_ctrl,
-                 h->d_hstat, h->d_cap, h->d_val_xy, h->d_base, h->d_dmin,
+                 h->d_hstat, h->d_cap, h->d_sense, h->d_val_xy, h->d_base, h->d_dmin,
                  h->d_partials, h->d_upd, h->d_val_poses, h->d_val_base, h->d_val_dmin, h->d_out,
                  h->d_controls, h->d_states, h->d_cost, h->d_unsafe, h->sb_poses, h->sb_pts64,
                  h->sb_pts, h->sb_mask, h->sb_keys, h->sb_min, h->sb_pairs};
@@ -1252,6 +1255,107 @@ exm_status exm_read_resident(exm_handle* h, double* nominal_out, double* u_prev_
 }
 
 void* exm_stream(exm_handle* h) { return h ? static_cast<void*>(h->stream) : nullptr; }
+
+// Sensing: segment table in the reference's sampling order (world.cpp:39-65) built on the
+// host with the reference's arithmetic, then one device kernel (exm_world.cu).
+exm_status exm_sense(exm_handle* h, const exm_world_obstacle* obstacles, int32_t n_obstacles,
+                     const double robot[3], double range, int32_t budget, uint64_t seed,
+                     uint64_t sample_key, double* pts_out, uint8_t* mask_out, int32_t* n_valid) {
+  if (!h || !robot || !pts_out || !mask_out || (n_obstacles > 0 && !obstacles))
+    return fail(EXM_ERR_INVALID_ARGUMENT, "null argument");
+  if (budget < 1) return fail(EXM_ERR_INVALID_ARGUMENT, "sensor budget must be >= 1");
+  constexpr double kSpacing = 0.05;  // kBoundarySpacing, world.cpp:15
+  std::vector<SenseSeg> seg;
+  std::vector<SenseObs> obs(static_cast<size_t>(n_obstacles));
+  std::vector<double2> verts;
+  int total = 0;
+  for (int i = 0; i < n_obstacles; ++i) {
+    const exm_world_obstacle& o = obstacles[i];
+    const double ox = o.offset[0], oy = o.offset[1];
+    SenseObs& so = obs[static_cast<size_t>(i)];
+    so = {};
+    so.ox = ox;
+    so.oy = oy;
+    if (o.kind == EXM_OBSTACLE_POLYGON) {
+      if (o.count < 3 || !o.x || !o.y) return fail(EXM_ERR_INVALID_ARGUMENT, "obstacle polygon needs at least 3 vertices");
+      so.kind = 0;
+      so.count = o.count;
+      so.first = static_cast<int>(verts.size());
+      for (int v = 0; v < o.count; ++v) verts.push_back(make_double2(o.x[v], o.y[v]));
+      for (int v = 0; v < o.count; ++v) {
+        const int w = v + 1 == o.count ? 0 : v + 1;
+        SenseSeg g = {};
+        g.kind = 0;
+        g.obs = i;
+        g.ax = o.x[v] + ox;
+        g.ay = o.y[v] + oy;
+        g.bx = o.x[w] + ox;
+        g.by = o.y[w] + oy;
+        const double ex = g.bx - g.ax, ey = g.by - g.ay;
+        const double len = std::sqrt(ex * ex + ey * ey);
+        g.steps = std::max(1, static_cast<int>(std::ceil(len / kSpacing)));
+        g.start = total;
+        total += g.steps;
+        seg.push_back(g);
+      }
+    } else if (o.kind == EXM_OBSTACLE_DISC) {
+      if (!o.x || !o.y || !(o.radius >= 0.0)) return fail(EXM_ERR_INVALID_ARGUMENT, "bad disc obstacle");
+      so.kind = 1;
+      so.cx = o.x[0];
+      so.cy = o.y[0];
+      so.r = o.radius;
+      SenseSeg g = {};
+      g.kind = 1;
+      g.obs = i;
+      g.ax = o.x[0];
+      g.ay = o.y[0];
+      g.bx = ox;
+      g.by = oy;
+      g.r = o.radius;
+      const double circumference = 2.0 * kPiHost * o.radius;
+      g.steps = std::max(8, static_cast<int>(std::ceil(circumference / kSpacing)));
+      g.start = total;
+      total += g.steps;
+      seg.push_back(g);
+    } else {
+      return fail(EXM_ERR_INVALID_ARGUMENT, "unknown obstacle kind");
+    }
+  }
+  EXM_CUDA(cudaSetDevice(h->device));
+  cudaStream_t s = h->stream;
+  auto up = [](size_t b) { return (b + 255) & ~static_cast<size_t>(255); };  // region alignment
+  const size_t b_seg = up(std::max<size_t>(seg.size(), 1) * sizeof(SenseSeg));
+  const size_t b_obs = up(std::max<size_t>(obs.size(), 1) * sizeof(SenseObs));
+  const size_t b_ver = up(std::max<size_t>(verts.size(), 1) * sizeof(double2));
+  const size_t b_out = static_cast<size_t>(budget) * (2 * sizeof(double) + 1) + 16;
+  const size_t need = b_seg + b_obs + b_ver + b_out + 64;
+  if (need > h->sense_bytes) {
+    if (h->d_sense) cudaFree(h->d_sense);
+    h->d_sense = nullptr;
+    h->sense_bytes = 0;
+    EXM_CUDA(cudaMalloc(&h->d_sense, need));
+    h->sense_bytes = need;
+  }
+  char* d = static_cast<char*>(h->d_sense);
+  SenseSeg* d_seg = reinterpret_cast<SenseSeg*>(d);
+  SenseObs* d_obs = reinterpret_cast<SenseObs*>(d + b_seg);
+  double2* d_ver = reinterpret_cast<double2*>(d + b_seg + b_obs);
+  double* d_pts = reinterpret_cast<double*>(d + b_seg + b_obs + b_ver);
+  int* d_n = reinterpret_cast<int*>(d_pts + 2 * static_cast<size_t>(budget));
+  uint8_t* d_mask = reinterpret_cast<uint8_t*>(d_n + 4);
+  if (!seg.empty()) EXM_CUDA(cudaMemcpyAsync(d_seg, seg.data(), seg.size() * sizeof(SenseSeg), cudaMemcpyHostToDevice, s));
+  if (!obs.empty()) EXM_CUDA(cudaMemcpyAsync(d_obs, obs.data(), obs.size() * sizeof(SenseObs), cudaMemcpyHostToDevice, s));
+  if (!verts.empty()) EXM_CUDA(cudaMemcpyAsync(d_ver, verts.data(), verts.size() * sizeof(double2), cudaMemcpyHostToDevice, s));
+  EXM_CUDA(launch_sense(d_seg, static_cast<int>(seg.size()), total, d_obs, n_obstacles, d_ver,
+                        robot[0], robot[1], range, budget, seed, sample_key, d_pts, d_mask, d_n, s));
+  int n_host = 0;
+  EXM_CUDA(cudaMemcpyAsync(pts_out, d_pts, 2 * static_cast<size_t>(budget) * sizeof(double), cudaMemcpyDeviceToHost, s));
+  EXM_CUDA(cudaMemcpyAsync(mask_out, d_mask, static_cast<size_t>(budget), cudaMemcpyDeviceToHost, s));
+  EXM_CUDA(cudaMemcpyAsync(&n_host, d_n, sizeof(int), cudaMemcpyDeviceToHost, s));
+  EXM_CUDA(cudaStreamSynchronize(s));
+  if (n_valid) *n_valid = n_host;
+  return EXM_OK;
+}
 
 exm_status exm_set_sdf_caps(exm_handle* h, const float* caps) {
   if (!h || !caps) return fail(EXM_ERR_INVALID_ARGUMENT, "null argument");

@@ -72,6 +72,23 @@ inline size_t cloud_capacity(int n_cap) {
   return static_cast<size_t>(n_cap) + static_cast<size_t>(kChunk - 1) * kGridMax * kGridMax + kChunk;
 }
 
+// Sensing (exm_world.cu): boundary-sample segments in the reference's sampling order and the
+// obstacles for the line-of-sight test (world.cpp:39-65, :167-179). Built on the host.
+struct SenseSeg {
+  int kind;   // 0 polygon edge a -> b (vertices + offset), 1 disc (centre a, offset b, radius r)
+  int steps;  // samples on this segment
+  int start;  // global index of its first sample
+  int obs;
+  double ax, ay, bx, by, r;
+};
+struct SenseObs {
+  int kind;  // 0 polygon (verts[first .. first + count)), 1 disc
+  int count;
+  int first;
+  int reserved;
+  double cx, cy, ox, oy, r;  // disc centre, offset, radius
+};
+
 // Per-step small inputs, uploaded with one copy (host API) or kept resident.
 struct StepDyn {
   double q0[3];
@@ -178,6 +195,10 @@ cudaError_t launch_recentre(const double* pts, int n, double cx, double cy, floa
 cudaError_t launch_sdf_pairs(const FpDev& fp, const float4* poses, int n_poses,
                              const float2* pts, const uint8_t* mask, int n_points,
                              float* per_pair, unsigned* pose_min_key, cudaStream_t s);
+cudaError_t launch_sense(const SenseSeg* seg, int nseg, int n_samples, const SenseObs* obs,
+                         int n_obs, const double2* verts, double rx, double ry, double range,
+                         int budget, uint64_t seed, uint64_t sample_key, double* pts_out,
+                         uint8_t* mask_out, int* n_out, cudaStream_t s);
 cudaError_t launch_min_keys_to_double(const unsigned* keys, int n, double* out, cudaStream_t s);
 cudaError_t launch_fill_u32(unsigned* p, unsigned v, int n, cudaStream_t s);
 

@@ -405,3 +405,20 @@ class ReferenceHybrid:
             raise ValueError(self.L.ref_last_error().decode())
         return dict(command=cmd, mode_index=mi.value, validated=bool(val.value), mode_costs=costs,
                     best_cost=diag[0], weight_entropy=diag[1], nominal_cost=diag[2])
+
+
+def reference_sense(obstacles, robot, sensor_range, budget, seed, sample_key):
+    """The reference's sense() (world.cpp:182-243) through oracle/_ref (ref_sense)."""
+    from paper_2605_29663_b200.api import world_obstacles_c
+    L = ref_lib()
+    arr, keep = world_obstacles_c(obstacles)
+    pts = np.empty((budget, 2))
+    mask = np.empty(budget, np.uint8)
+    n = C.c_int32()
+    rc = L.ref_sense(arr, len(obstacles), _p(_c(robot)), C.c_double(sensor_range), budget,
+                     C.c_uint64(seed), C.c_uint64(sample_key), _p(pts),
+                     mask.ctypes.data_as(_u8p), C.byref(n))
+    del keep
+    if rc:
+        raise ValueError(L.ref_last_error().decode())
+    return pts, mask, n.value
