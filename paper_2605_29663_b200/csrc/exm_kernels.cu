@@ -13,6 +13,21 @@
 // before rounding.
 #include "exm_device.cuh"
 
+#ifdef EXM_TIMING  // phase timestamps of k_cloud_prep (diagnostic builds only)
+__device__ long long g_probe_prep[16];
+#define EXM_PROBE_P(i) \
+  do {                 \
+    if (threadIdx.x == 0) g_probe_prep[i] = clock64(); \
+  } while (0)
+extern "C" int exm_debug_probes_prep(long long* out) {
+  return static_cast<int>(cudaMemcpyFromSymbol(out, g_probe_prep, sizeof(g_probe_prep)));
+}
+#else
+#define EXM_PROBE_P(i) \
+  do {                 \
+  } while (0)
+#endif
+
 namespace exm {
 namespace {
 
@@ -262,6 +277,7 @@ __device__ __forceinline__ float unkey(unsigned k) {
 
 // ------------------------------------------------------------------ kernels
 constexpr float kPtsPerCell = 32.0f;
+constexpr int kPrepCache = 12;  // cloud points per k_cloud_prep thread kept in registers
 constexpr float kCellMaxR = 0.5f;        // cell edge <= kCellMaxR * R ...
 constexpr float kCellSearchFrac = 0.385f;  // ... or <= this fraction of R + mean d_min
 // Below this many poses one thread per pose leaves most SMs idle (< ~16 warps each): use one
@@ -293,19 +309,32 @@ __global__ void __launch_bounds__(1024) k_cloud_prep(const double* __restrict__ 
   const float nanf_ = __int_as_float(0x7fc00000);
   float mnx = FLT_MAX, mxx = -FLT_MAX, mny = FLT_MAX, mxy = -FLT_MAX;
   int cnt = 0;
+  EXM_PROBE_P(0);
+  // The first kPrepCache * blockDim points stay in registers across the three passes (bbox,
+  // histogram, scatter); the rest (large clouds) go through `tmp`.
   const double2* p2 = reinterpret_cast<const double2*>(pts);
-  for (int i = tid; i < n; i += blockDim.x) {
+  float2 pc[kPrepCache];
+  int pcell[kPrepCache];
+  auto load = [&](int i) {
+    const double2 w = p2[i];  // unconditional: independent of the mask load
     const bool v = !use_mask || mask[i] != 0;
     float2 p = make_float2(nanf_, nanf_);
     if (v) {
-      const double2 w = p2[i];
       p = make_float2(static_cast<float>(w.x - qx), static_cast<float>(w.y - qy));
       mnx = fminf(mnx, p.x); mxx = fmaxf(mxx, p.x);
       mny = fminf(mny, p.y); mxy = fmaxf(mxy, p.y);
       ++cnt;
     }
-    tmp[i] = p;
+    return p;
+  };
+#pragma unroll
+  for (int j = 0; j < kPrepCache; ++j) {
+    const int i = tid + j * static_cast<int>(blockDim.x);
+    pc[j] = i < n ? load(i) : make_float2(nanf_, nanf_);
   }
+  const int n_cached = kPrepCache * static_cast<int>(blockDim.x);
+#pragma unroll 4
+  for (int i = n_cached + tid; i < n; i += blockDim.x) tmp[i] = load(i);
   for (int o = 16; o; o >>= 1) {
     mnx = fminf(mnx, __shfl_xor_sync(kFull, mnx, o));
     mxx = fmaxf(mxx, __shfl_xor_sync(kFull, mxx, o));
@@ -313,15 +342,25 @@ __global__ void __launch_bounds__(1024) k_cloud_prep(const double* __restrict__ 
     mxy = fmaxf(mxy, __shfl_xor_sync(kFull, mxy, o));
     cnt += __shfl_xor_sync(kFull, cnt, o);
   }
+  EXM_PROBE_P(1);
   if (lane == 0) { red[0][warp] = mnx; red[1][warp] = mxx; red[2][warp] = mny; red[3][warp] = mxy; redc[warp] = cnt; }
   __syncthreads();
-  if (tid == 0) {
+  if (warp == 0) {
     const int nw = blockDim.x >> 5;
-    for (int w = 1; w < nw; ++w) {
-      mnx = fminf(mnx, red[0][w]); mxx = fmaxf(mxx, red[1][w]);
-      mny = fminf(mny, red[2][w]); mxy = fmaxf(mxy, red[3][w]);
-      cnt += redc[w];
+    mnx = lane < nw ? red[0][lane] : FLT_MAX;
+    mxx = lane < nw ? red[1][lane] : -FLT_MAX;
+    mny = lane < nw ? red[2][lane] : FLT_MAX;
+    mxy = lane < nw ? red[3][lane] : -FLT_MAX;
+    cnt = lane < nw ? redc[lane] : 0;
+    for (int o = 16; o; o >>= 1) {
+      mnx = fminf(mnx, __shfl_xor_sync(kFull, mnx, o));
+      mxx = fmaxf(mxx, __shfl_xor_sync(kFull, mxx, o));
+      mny = fminf(mny, __shfl_xor_sync(kFull, mny, o));
+      mxy = fmaxf(mxy, __shfl_xor_sync(kFull, mxy, o));
+      cnt += __shfl_xor_sync(kFull, cnt, o);
     }
+  }
+  if (tid == 0) {
     GridMeta g;
     g.n_valid = cnt;
     g.margin = kCullMargin;
@@ -351,20 +390,29 @@ __global__ void __launch_bounds__(1024) k_cloud_prep(const double* __restrict__ 
     dstat[1] = 0.f;
   }
   __syncthreads();
+  EXM_PROBE_P(2);
   const int cells = gm.gx * gm.gy;
   for (int c = tid; c < cells; c += blockDim.x) hist[c] = 0;
   __syncthreads();
+  auto cell_of = [&](float2 p) {
+    const int ix = min(gm.gx - 1, max(0, static_cast<int>((p.x - gm.x0) * gm.inv_cs)));
+    const int iy = min(gm.gy - 1, max(0, static_cast<int>((p.y - gm.y0) * gm.inv_cs)));
+    return iy * gm.gx + ix;
+  };
   if (gm.n_valid > 0) {
-    for (int i = tid; i < n; i += blockDim.x) {
+#pragma unroll
+    for (int j = 0; j < kPrepCache; ++j) {
+      pcell[j] = pc[j].x == pc[j].x ? cell_of(pc[j]) : -1;
+      if (pcell[j] >= 0) atomicAdd(&hist[pcell[j]], 1);
+    }
+#pragma unroll 4
+    for (int i = n_cached + tid; i < n; i += blockDim.x) {
       const float2 p = tmp[i];
-      if (p.x == p.x) {
-        const int ix = min(gm.gx - 1, max(0, static_cast<int>((p.x - gm.x0) * gm.inv_cs)));
-        const int iy = min(gm.gy - 1, max(0, static_cast<int>((p.y - gm.y0) * gm.inv_cs)));
-        atomicAdd(&hist[iy * gm.gx + ix], 1);
-      }
+      if (p.x == p.x) atomicAdd(&hist[cell_of(p)], 1);
     }
   }
   __syncthreads();
+  EXM_PROBE_P(3);
   // Exclusive scans of the cell counts (raw_start) and of the counts padded to whole chunks
   // (cell_start), as one 64-bit scan {padded:raw}; each thread owns a contiguous segment.
   const int seg = (cells + blockDim.x - 1) / blockDim.x;
@@ -405,17 +453,19 @@ __global__ void __launch_bounds__(1024) k_cloud_prep(const double* __restrict__ 
     cell_start[cells] = static_cast<int>(run >> 32);
   }
   __syncthreads();
+  EXM_PROBE_P(4);
   if (gm.n_valid > 0) {
-    for (int i = tid; i < n; i += blockDim.x) {
+#pragma unroll
+    for (int j = 0; j < kPrepCache; ++j)
+      if (pcell[j] >= 0) raw[atomicAdd(&hist[pcell[j]], 1)] = pc[j];
+#pragma unroll 4
+    for (int i = n_cached + tid; i < n; i += blockDim.x) {
       const float2 p = tmp[i];
-      if (p.x == p.x) {
-        const int ix = min(gm.gx - 1, max(0, static_cast<int>((p.x - gm.x0) * gm.inv_cs)));
-        const int iy = min(gm.gy - 1, max(0, static_cast<int>((p.y - gm.y0) * gm.inv_cs)));
-        const int slot = atomicAdd(&hist[iy * gm.gx + ix], 1);
-        raw[slot] = p;
-      }
+      if (p.x == p.x) raw[atomicAdd(&hist[cell_of(p)], 1)] = p;
     }
   }
+  __syncthreads();
+  EXM_PROBE_P(5);
 }
 
 // Morton index of a point on the kSubCells x kSubCells sub-grid of its cell.
