@@ -25,25 +25,32 @@ def _stale(target: str, deps) -> bool:
 
 
 def build_library(force: bool = False, verbose: bool = False) -> str:
-    deps = [os.path.join(CSRC, s) for s in SOURCES + HEADERS] + [
-        os.path.join(ROOT, "include", "exm_b200.h")]
-    if force or _stale(LIB, deps):
-        objdir = os.path.join(os.path.dirname(LIB), "obj")
-        os.makedirs(objdir, exist_ok=True)
-        objs = []
-        for src in SOURCES:
-            obj = os.path.join(objdir, src.replace(".cu", ".o"))
-            cmd = ["nvcc", *NVCC_FLAGS, *UNIT_FLAGS.get(src, []), "-c", "-o", obj,
-                   os.path.join(CSRC, src)]
-            if verbose:
-                print(" ".join(cmd))
-            subprocess.run(cmd, check=True)
-            objs.append(obj)
-        cmd = ["nvcc", "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", LIB, *objs,
-               "-ldl"]
+    """Compile the stale objects (source or a shared header newer than the object) in
+    parallel, then link when any object changed."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    common = [os.path.join(CSRC, h) for h in HEADERS] + [os.path.join(ROOT, "include", "exm_b200.h")]
+    objdir = os.path.join(os.path.dirname(LIB), "obj")
+    os.makedirs(objdir, exist_ok=True)
+    jobs, objs = [], []
+    for src in SOURCES:
+        obj = os.path.join(objdir, src.replace(".cu", ".o"))
+        objs.append(obj)
+        if force or _stale(obj, [os.path.join(CSRC, src), *common]):
+            jobs.append(["nvcc", *NVCC_FLAGS, *UNIT_FLAGS.get(src, []), "-c", "-o", obj,
+                         os.path.join(CSRC, src)])
+
+    def run(cmd):
         if verbose:
-            print(" ".join(cmd))
+            print(" ".join(cmd), flush=True)
         subprocess.run(cmd, check=True)
+
+    if jobs:
+        with ThreadPoolExecutor(max_workers=len(jobs)) as ex:
+            list(ex.map(run, jobs))
+    if force or jobs or _stale(LIB, objs):
+        run(["nvcc", "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", LIB, *objs,
+             "-ldl"])
     return LIB
 
 

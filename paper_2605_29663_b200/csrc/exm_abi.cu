@@ -402,13 +402,29 @@ exm_status build_footprint(const exm_footprint* fp, FpDev* out) {
     }
     const auto boxes = cover_boxes(px, py, kMaxCover);
     out->ncover = static_cast<int>(boxes.size());
+    // The cut-line boxes have disjoint interiors and contain the polygon, so they tile it
+    // exactly iff their areas sum to the polygon's area (rectilinear shapes: the L).
+    double box_area = 0.0, poly2 = 0.0;
+    for (const auto& bj : boxes) box_area += (bj[1] - bj[0]) * (bj[3] - bj[2]);
+    for (int i = 0; i < out->count; ++i) {
+      const int k = (i + 1) % out->count;
+      poly2 += px[i] * py[k] - py[i] * px[k];
+    }
+    const double poly_area = 0.5 * std::fabs(poly2);
+    out->cover_exact = std::fabs(box_area - poly_area) <= 1e-9 * std::max(poly_area, 1e-12) ? 1 : 0;
+    out->cover_slack = static_cast<float>(m);
     for (int j = 0; j < kMaxCover; ++j) {  // unused slots repeat box 0 (the kernel unrolls)
       const auto& bj = boxes[static_cast<size_t>(j) < boxes.size() ? j : 0];
       out->cover[j][0] = static_cast<float>(0.5 * (bj[0] + bj[1]));
       out->cover[j][1] = static_cast<float>(0.5 * (bj[2] + bj[3]));
       out->cover[j][2] = static_cast<float>(0.5 * (bj[1] - bj[0]) + m);
       out->cover[j][3] = static_cast<float>(0.5 * (bj[3] - bj[2]) + m);
+      out->cbox[j][0] = out->cover[j][0];
+      out->cbox[j][1] = out->cover[j][1];
+      out->cbox[j][2] = static_cast<float>(0.5 * (bj[1] - bj[0]));
+      out->cbox[j][3] = static_cast<float>(0.5 * (bj[3] - bj[2]));
     }
+    if (const char* ev = std::getenv("EXM_COVER_EXACT"); ev && ev[0] == '0') out->cover_exact = 0;
   }
   return EXM_OK;
 }

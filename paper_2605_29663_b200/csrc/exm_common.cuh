@@ -35,8 +35,14 @@ struct FpDev {
   // boxes: the boxes themselves; otherwise the AABB): an exterior point's signed distance is
   // at least its distance to that union, a tighter cull bound than the AABB.
   int ncover;
-  int reserved2;
-  float cover[kMaxCover][4];
+  // polygons whose cover boxes tile them exactly (rectilinear: the L): outside the slackened
+  // cover (every max(|b - c| - h) > cover_slack) the signed distance IS the distance to the
+  // unslackened boxes cbox, so the exact value costs one box pass instead of the edge loop
+  int cover_exact;
+  float cover[kMaxCover][4];  // {cx, cy, hx + slack, hy + slack}
+  float cbox[kMaxCover][4];   // {cx, cy, hx, hy} (cover_exact only)
+  float cover_slack;
+  float reserved3;
   float e[kMaxEdges][8];
   // polygon edges in pairs for the f32x2 path: ep[j][k] = {e[2j][k], e[2j+1][k]}; an odd
   // count is padded with the zero-length edge {v0x, v0y, 0...}

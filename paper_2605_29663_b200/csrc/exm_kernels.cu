@@ -240,6 +240,64 @@ __device__ __forceinline__ bool cover_may_beat(const FpDev& fp, float bx, float 
   return lim > 0.f && d2 < lim * lim;
 }
 
+// Exact-cover polygons (fp.cover_exact: rectilinear footprints tiled by their <= 3 cover boxes,
+// the L): a point outside the slackened cover (every box: max(|b - c| - h) > slack, so it is
+// exterior with a margin far above FP32 rounding) has signed distance = distance to the union
+// of the unslackened tiles; returns that squared distance. Other points (inside or within the
+// slack of the footprint) take the edge loop. Value function of the grid kernels:
+//   v(p) = exterior ? sqrt(d2_tiles) : sd_polygon(p)
+// (differs from the edge loop by FP32 rounding only; culled and brute-force modes share it).
+__device__ __forceinline__ bool tiles_exterior_d2(const FpDev& fp, float bx, float by, float& d2) {
+  float d2u = __int_as_float(0x7f800000), inm = __int_as_float(0x7f800000);
+#pragma unroll
+  for (int j = 0; j < kMaxCover; ++j) {
+    const float ax = fabsf(bx - fp.cbox[j][0]) - fp.cbox[j][2];
+    const float ay = fabsf(by - fp.cbox[j][1]) - fp.cbox[j][3];
+    const float ox = fmaxf(ax, 0.f), oy = fmaxf(ay, 0.f);
+    d2u = fminf(d2u, fmaf(ox, ox, oy * oy));
+    inm = fminf(inm, fmaxf(ax, ay));
+  }
+  d2 = d2u;
+  return inm > fp.cover_slack;
+}
+
+// One body-frame candidate point of the grid kernels: lower-bound tests, then the value v(p);
+// returns the new running minimum. BRUTE: no bound at all (every point valued, same arithmetic).
+template <int KIND, int NB, bool BRUTE>
+__device__ __forceinline__ float grid_point(const FpDev& fp, float bx, float by, float best,
+                                            float mg, bool& evaluated) {
+  evaluated = false;
+  if constexpr (KIND == EXM_FOOTPRINT_POLYGON) {
+    if (fp.cover_exact) {
+      float d2;
+      const float lim = best + mg;
+      if (tiles_exterior_d2(fp, bx, by, d2)) {
+        if (BRUTE || (lim > 0.f && d2 < lim * lim)) {
+          evaluated = true;
+          best = fminf(best, sqrtf(d2));
+        }
+        return best;
+      }
+      // inside (or at the rim of) the cover: the AABB interior bound, then the edge loop
+      if (BRUTE || fmaxf(fmaxf(fp.aabb[0] - bx, bx - fp.aabb[1]), fmaxf(fp.aabb[2] - by, by - fp.aabb[3])) < lim) {
+        evaluated = true;
+        best = fminf(best, sd_body<KIND, NB>(fp, bx, by));
+      }
+      return best;
+    }
+  }
+  // polygons: the cover bound (exact for rectilinear shapes: the L's notch is culled);
+  // rectangle covers of <= 3 boxes: the exact SDF is hardly dearer than a bound; larger
+  // covers: the AABB pre-test
+  if (BRUTE || (KIND != EXM_FOOTPRINT_POLYGON && NB > 0 && NB <= 3) ||
+      (KIND == EXM_FOOTPRINT_POLYGON ? cover_may_beat(fp, bx, by, best, mg)
+                                     : aabb_may_beat(fp, bx, by, best, mg))) {
+    evaluated = true;
+    best = fminf(best, sd_body<KIND, NB>(fp, bx, by));
+  }
+  return best;
+}
+
 // Chunk bound: the chunk's points lie in the world box {cx +- hx, cy +- hy}; in the body frame
 // of pose q that box lies inside the box centred at R(theta)^T (c - t) with half extents
 // (|cos| hx + |sin| hy, |sin| hx + |cos| hy). No point of the chunk is nearer to the footprint
@@ -695,14 +753,10 @@ __global__ void __launch_bounds__(128) k_sdf_grid(const __grid_constant__ FpDev 
           if (cneed && (MODE == kGridBrute ? o.x == o.x : dx * dx + dy * dy < l2)) {  // NaN pads
             const float bx = fmaf(q.z, dx, q.w * dy);
             const float by = fmaf(q.z, dy, -(q.w * dx));
-            // polygons: the cover bound (exact for rectilinear shapes: the L's notch is culled);
-            // rectangle covers: the AABB pre-test (the exact SDF costs about as much as a cover)
-            // (rectangle covers of <= 3 boxes: the exact SDF is hardly dearer than a bound)
-            if (MODE == kGridBrute || (KIND != EXM_FOOTPRINT_POLYGON && NB > 0 && NB <= 3) ||
-                (KIND == EXM_FOOTPRINT_POLYGON ? cover_may_beat(fp, bx, by, best, mg)
-                                               : aabb_may_beat(fp, bx, by, best, mg))) {
+            bool ev;
+            best = grid_point<KIND, NB, MODE == kGridBrute>(fp, bx, by, best, mg, ev);
+            if (ev) {
               if (STATS) ++n_eval;
-              best = fminf(best, sd_body<KIND, NB>(fp, bx, by));
               const float nl = R + best;
               l2 = nl * nl;
             }
@@ -803,10 +857,8 @@ __global__ void __launch_bounds__(W == 1 ? 128 : 32 * W) k_sdf_grid_warp(
           if (dx * dx + dy * dy < l2 * l2) {
             const float bx = fmaf(q.z, dx, q.w * dy);
             const float by = fmaf(q.z, dy, -(q.w * dx));
-            if ((KIND != EXM_FOOTPRINT_POLYGON && NB > 0 && NB <= 3) ||
-                (KIND == EXM_FOOTPRINT_POLYGON ? cover_may_beat(fp, bx, by, mine, mg)
-                                               : aabb_may_beat(fp, bx, by, mine, mg)))
-              mine = fminf(mine, sd_body<KIND, NB>(fp, bx, by));
+            bool ev;
+            mine = grid_point<KIND, NB, false>(fp, bx, by, mine, mg, ev);
           }
         }
       }
