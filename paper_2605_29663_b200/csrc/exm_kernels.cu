@@ -287,7 +287,8 @@ __device__ __forceinline__ float grid_point(const FpDev& fp, float bx, float by,
     }
   }
   // polygons: the cover bound (exact for rectilinear shapes: the L's notch is culled);
-  // rectangle covers of <= 3 boxes: the exact SDF is hardly dearer than a bound; larger
+  // rectangle covers of <= 3 boxes: the exact SDF is hardly dearer than a bound (skipping its
+  // sqrt behind a squared-distance test measured slower: the branch diverges); larger
   // covers: the AABB pre-test
   if (BRUTE || (KIND != EXM_FOOTPRINT_POLYGON && NB > 0 && NB <= 3) ||
       (KIND == EXM_FOOTPRINT_POLYGON ? cover_may_beat(fp, bx, by, best, mg)
