@@ -143,7 +143,6 @@ constexpr float kDstatClamp = 16.0f;       // d_min clamp in that mean (empty cl
 constexpr int kHstatEvery = 4;             // rollout blocks sampled for the per-step statistic
 constexpr float kCapSigma = 3.0f;          // cap = mean + kCapSigma * std (+ kCapSlack * R)
 constexpr float kCapSlack = 0.02f;
-constexpr int kPartialThreads = 1024;  // 32 warps: 8 rollouts per warp in the U sums
 
 // The serial part of one rollout (score_rollout, controller.cpp:151-169, minus the SDF and the
 // task cost, which k_rollout_costs computes in parallel over h), spread over one warp. Only
@@ -328,17 +327,17 @@ __global__ void __launch_bounds__(kRolloutWarps * 32) k_rollout(
 // in exactly the reference's order (with k_rollout's control and terminal costs), so J_r is
 // the reference's value for the same d_min. Also accumulates the search-radius statistic of
 // the next step's cell size (k_cloud_prep).
-constexpr int kCostWarps = 8;
+constexpr int kCostWarps = 16;
 __global__ void __launch_bounds__(kCostWarps * 32) k_rollout_costs(
     const StepConst sc, const StepDyn* __restrict__ dynp, const double* __restrict__ guide,
     const double* __restrict__ base_cost, const double* __restrict__ ctrl_cost,
     const double2* __restrict__ xy, const float* __restrict__ dmin, double* __restrict__ cost,
     uint8_t* __restrict__ unsafe, float* __restrict__ dstat, float* __restrict__ hstat) {
   pdl_wait();
-  extern __shared__ double g[];  // guide (2*ng), per warp: task[T], obst[T]; then 2T floats
+  extern __shared__ double g[];  // guide (2*ng), per warp: task[T], obst[T], ctrl[T]; then 2T floats
   __shared__ float red[2][kCostWarps];
   const int ng = dynp->n_guide, T = sc.T;
-  float* sh = reinterpret_cast<float*>(g + 2 * ng + kCostWarps * 2 * T);
+  float* sh = reinterpret_cast<float*>(g + 2 * ng + kCostWarps * 3 * T);
   // every kHstatEvery-th block samples the per-step d_min statistic (k_finalize -> caps)
   const bool sampled = hstat != nullptr && blockIdx.x % kHstatEvery == 0;
   for (int i = threadIdx.x; i < 2 * ng; i += blockDim.x) g[i] = guide[i];
@@ -346,8 +345,9 @@ __global__ void __launch_bounds__(kCostWarps * 32) k_rollout_costs(
     for (int i = threadIdx.x; i < 2 * T; i += blockDim.x) sh[i] = 0.f;
   __syncthreads();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  double* s_t = g + 2 * ng + warp * 2 * T;
+  double* s_t = g + 2 * ng + warp * 3 * T;
   double* s_o = s_t + T;
+  double* s_c = s_o + T;
   const int r = blockIdx.x * kCostWarps + warp;
   const bool live = r < sc.k_local;  // warp-uniform
   float dc = 0.f;
@@ -361,6 +361,7 @@ __global__ void __launch_bounds__(kCostWarps * 32) k_rollout_costs(
       const double q[3] = {p.x, p.y, 0.0};
       s_t[h] = task_cost(sc, q, g, ng, dynp->goal, false);
       s_o[h] = obstacle_cost(sc, d);
+      s_c[h] = ctrl_cost[row + h];  // staged: the serial sum below reads shared memory only
       bad |= d < sc.d_safe;
       dc += fminf(fmaxf(df, 0.f), kDstatClamp);
       if (sampled) {
@@ -368,17 +369,6 @@ __global__ void __launch_bounds__(kCostWarps * 32) k_rollout_costs(
         atomicAdd(&sh[h], dv);
         atomicAdd(&sh[T + h], dv * dv);
       }
-    }
-    __syncwarp();
-    if (lane == 0) {
-      const double* cc = ctrl_cost + row;
-      double J = 0.0;
-      for (int h = 0; h < T; ++h) {
-        J += s_t[h];
-        J += cc[h];
-        J += s_o[h];
-      }
-      cost[r] = J + base_cost[r];
     }
   }
   for (int o = 16; o; o >>= 1) dc += __shfl_xor_sync(kFull, dc, o);
@@ -389,6 +379,23 @@ __global__ void __launch_bounds__(kCostWarps * 32) k_rollout_costs(
     red[1][warp] = live ? static_cast<float>(T) : 0.f;
   }
   __syncthreads();
+  // J_r in the reference's order, one lane of warp 0 per rollout of the CTA (the serial sums of
+  // the kCostWarps rollouts run side by side instead of on one lane of every warp)
+  if (warp == 0 && lane < kCostWarps) {
+    const int rr = blockIdx.x * kCostWarps + lane;
+    if (rr < sc.k_local) {
+      const double* t_ = g + 2 * ng + lane * 3 * T;
+      const double jb = base_cost[rr];
+      double J = 0.0;
+#pragma unroll 10
+      for (int h = 0; h < T; ++h) {
+        J += t_[h];
+        J += t_[2 * T + h];
+        J += t_[T + h];
+      }
+      cost[rr] = J + jb;
+    }
+  }
   if (sampled) {
     for (int i = threadIdx.x; i < 2 * T; i += blockDim.x) atomicAdd(&hstat[i], sh[i]);
     if (threadIdx.x == 0) {
@@ -414,34 +421,53 @@ __global__ void __launch_bounds__(kCostWarps * 32) k_rollout_costs(
 // (fixed block size and fixed reduction trees: deterministic and independent of sharding).
 //   Jt_r = J_r + w_inf * unsafe_r                       controller.cpp:310-312
 //   {beta_b, S_b, A_b, argmin_b, U_b[T*D]}              controller.cpp:222-233, :316-328
-__global__ void __launch_bounds__(kPartialThreads) k_block_partials(
+// Grid (block, column group): every CTA recomputes the block's beta and weights (256 exps) and
+// sums one group of kPartCols columns (h, c) of U_b, one column per lane, the 8 warps over
+// interleaved rollouts, then the warp sums in warp order; column group 0 also writes the header.
+// The eps rows are read by blocks x column groups CTAs instead of one CTA per block.
+constexpr int kPartCols = 32;
+__global__ void __launch_bounds__(kBlockRollouts) k_block_partials(
     const StepConst sc, const double* __restrict__ cost, const uint8_t* __restrict__ unsafe,
     const double* __restrict__ eps, double* __restrict__ partials) {
   pdl_wait();
-  extern __shared__ double s_u[];  // [kPartialThreads/32][T*D]
+  constexpr int kWarps = kBlockRollouts / 32;
   __shared__ double s_e[kBlockRollouts];
-  __shared__ double s_v[kBlockRollouts / 32];
-  __shared__ double s_a[kBlockRollouts / 32];
-  __shared__ int s_i[kBlockRollouts / 32];
+  __shared__ double s_v[kWarps];
+  __shared__ double s_a[kWarps];
+  __shared__ int s_i[kWarps];
+  __shared__ double s_u[kWarps][kPartCols];
   __shared__ double s_beta;
   __shared__ int s_arg;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  constexpr int kWarps = kBlockRollouts / 32;  // warps owning one rollout per lane
   const int r0 = blockIdx.x * kBlockRollouts;
   const int r = r0 + tid;
-  const bool owner = tid < kBlockRollouts;
-  const bool valid = owner && r < sc.k_local;
+  const bool valid = r < sc.k_local;
+  const int TD = sc.T * sc.D;
+  const int o = blockIdx.y * kPartCols + lane;
+  const int nv = min(kBlockRollouts, sc.k_local - r0);
+  // this lane's column of rows warp, warp + 8, ... fetched first: the loads do not depend on
+  // the weights, so their latency overlaps the argmin / exp phase
+  constexpr int kRows = kBlockRollouts / kWarps;
+  double ev[kRows];
+  {
+    const double* col = eps + static_cast<size_t>(r0) * TD + o;
+#pragma unroll
+    for (int k = 0; k < kRows; ++k) {
+      const int j = warp + k * kWarps;
+      ev[k] = (o < TD && j < nv) ? col[static_cast<size_t>(j) * TD] : 0.0;
+    }
+  }
   double jt = HUGE_VAL;
   if (valid) jt = unsafe[r] ? cost[r] + sc.w_inf : cost[r];
   // argmin with first-index tie break (std::min_element)
   double v = jt;
   int vi = valid ? sc.r_offset + r : 0x7fffffff;
-  for (int o = 16; o; o >>= 1) {
-    const double ov = __shfl_xor_sync(kFull, v, o);
-    const int oi = __shfl_xor_sync(kFull, vi, o);
+  for (int k = 16; k; k >>= 1) {
+    const double ov = __shfl_xor_sync(kFull, v, k);
+    const int oi = __shfl_xor_sync(kFull, vi, k);
     if (ov < v || (ov == v && oi < vi)) { v = ov; vi = oi; }
   }
-  if (lane == 0 && owner) { s_v[warp] = v; s_i[warp] = vi; }
+  if (lane == 0) { s_v[warp] = v; s_i[warp] = vi; }
   __syncthreads();
   if (tid == 0) {
     double b = s_v[0];
@@ -455,44 +481,42 @@ __global__ void __launch_bounds__(kPartialThreads) k_block_partials(
   const double beta = s_beta;
   const double z = valid ? (jt - beta) / sc.lambda : 0.0;
   const double e = valid ? exp(-z) : 0.0;
-  const double a = valid ? e * z : 0.0;
-  if (owner) s_e[tid] = e;
-  double se = e, sa = a;
-  for (int o = 16; o; o >>= 1) {
-    se += __shfl_xor_sync(kFull, se, o);
-    sa += __shfl_xor_sync(kFull, sa, o);
-  }
-  __syncthreads();  // s_v/s_a reuse: the argmin values were consumed by thread 0 above
-  if (lane == 0 && owner) { s_v[warp] = se; s_a[warp] = sa; }
-  __syncthreads();
+  s_e[tid] = e;
   const int stride = partial_stride(sc.T, sc.D);
   double* out = partials + static_cast<size_t>(sc.block_offset + blockIdx.x) * stride;
-  if (tid == 0) {
-    double S = 0.0, A = 0.0;
-    for (int w = 0; w < kWarps; ++w) { S += s_v[w]; A += s_a[w]; }
-    out[0] = beta;
-    out[1] = S;
-    out[2] = A;
-    out[3] = static_cast<double>(s_arg);
+  if (blockIdx.y == 0) {
+    const double a = valid ? e * z : 0.0;
+    double se = e, sa = a;
+    for (int k = 16; k; k >>= 1) {
+      se += __shfl_xor_sync(kFull, se, k);
+      sa += __shfl_xor_sync(kFull, sa, k);
+    }
+    __syncthreads();  // s_v reuse: the argmin values were consumed by thread 0 above
+    if (lane == 0) { s_v[warp] = se; s_a[warp] = sa; }
+    __syncthreads();
+    if (tid == 0) {
+      double S = 0.0, A = 0.0;
+      for (int w = 0; w < kWarps; ++w) { S += s_v[w]; A += s_a[w]; }
+      out[0] = beta;
+      out[1] = S;
+      out[2] = A;
+      out[3] = static_cast<double>(s_arg);
+    }
+  } else {
+    __syncthreads();
   }
-  // U_b[o] = sum_r e_r eps[r][o]: each of the kPartialThreads/32 warps sums its slice of
-  // rollouts (lanes over o, coalesced rows), then the warp sums are added in warp order.
-  constexpr int kUWarps = kPartialThreads / 32;
-  constexpr int kPerWarp = kBlockRollouts / kUWarps;
-  const int TD = sc.T * sc.D;
-  const int nv = min(kBlockRollouts, sc.k_local - r0);
-  const int j0 = warp * kPerWarp, j1 = min(nv, j0 + kPerWarp);
-  for (int o = lane; o < TD; o += 32) {
-    double acc = 0.0;
+  // U_b[o] = sum_r e_r eps[r][o]: warp w sums rollouts w, w + 8, ... (rows coalesced over the
+  // lanes' columns), then the warp sums are added in warp order
+  double acc = 0.0;
 #pragma unroll
-    for (int j = j0; j < j1; ++j) acc += s_e[j] * eps[static_cast<size_t>(r0 + j) * TD + o];
-    s_u[warp * TD + o] = acc;
-  }
+  for (int k = 0; k < kRows; ++k) acc += s_e[warp + k * kWarps] * ev[k];  // e = 0 past nv
+  s_u[warp][lane] = acc;
   __syncthreads();
-  for (int o = tid; o < TD; o += blockDim.x) {
-    double acc = 0.0;
-    for (int w = 0; w < kUWarps; ++w) acc += s_u[w * TD + o];
-    out[4 + o] = acc;
+  if (warp == 0 && o < TD) {
+    double u = 0.0;
+#pragma unroll
+    for (int w = 0; w < kWarps; ++w) u += s_u[w][lane];
+    out[4 + o] = u;
   }
 }
 
@@ -617,6 +641,7 @@ __global__ void __launch_bounds__(64) k_finalize(
   double* g = sm2;
   double* c_t = sm2 + 2 * ng;
   double* c_o = c_t + T;
+  double* c_c = c_o + T;  // val_base = {terminal, ctrl[T]}, staged
   for (int i = tid; i < 2 * ng; i += blockDim.x) g[i] = guide[i];
   if (tid == 0) s_ok = 1;
   __syncthreads();
@@ -627,17 +652,20 @@ __global__ void __launch_bounds__(64) k_finalize(
     const double q[3] = {val_xy[h].x, val_xy[h].y, 0.0};
     c_t[h] = task_cost(sc, q, g, ng, dyn->goal, false);
     c_o[h] = obstacle_cost(sc, d);
+    c_c[h] = val_base[1 + h];
   }
   __syncthreads();
   const int ok = s_ok;
-  if (tid == 0) {  // validate_nominal's order (controller.cpp:268-279); val_base = {terminal, ctrl[T]}
+  if (tid == 0) {  // validate_nominal's order (controller.cpp:268-279)
+    const double jb = val_base[0];
     double J = 0.0;
+#pragma unroll 10
     for (int h = 0; h < T; ++h) {
       J += c_t[h];
-      J += val_base[1 + h];
+      J += c_c[h];
       J += c_o[h];
     }
-    dec->nominal_cost = J + val_base[0];
+    dec->nominal_cost = J + jb;
     dec->validated = ok;
   }
   if (!commit) return;
@@ -720,8 +748,8 @@ cudaError_t launch_rollout_costs(const StepConst& sc, const StepDyn* dyn, const 
                                  const double2* xy, const float* dmin, double* cost,
                                  uint8_t* unsafe, float* dstat, float* hstat, cudaStream_t s) {
   if (sc.k_local <= 0) return cudaSuccess;
-  const size_t smem = sizeof(double) * (2 * (static_cast<size_t>(guide_cap) +
-                                             static_cast<size_t>(kCostWarps) * sc.T) + sc.T);
+  const size_t smem = sizeof(double) * (2 * static_cast<size_t>(guide_cap) +
+                                        3 * static_cast<size_t>(kCostWarps) * sc.T + sc.T);
   if (smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(k_rollout_costs, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(smem));
@@ -735,14 +763,8 @@ cudaError_t launch_rollout_costs(const StepConst& sc, const StepDyn* dyn, const 
 cudaError_t launch_block_partials(const StepConst& sc, const double* cost, const uint8_t* unsafe,
                                   const double* eps, double* partials, cudaStream_t s) {
   if (sc.nblocks_local <= 0) return cudaSuccess;
-  const size_t smem = sizeof(double) * (kPartialThreads / 32) * static_cast<size_t>(sc.T) * sc.D;
-  if (smem > 48 * 1024) {
-    cudaError_t e = cudaFuncSetAttribute(k_block_partials,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(smem));
-    if (e != cudaSuccess) return e;
-  }
-  { if (const cudaError_t le = launch_k(k_block_partials, sc.nblocks_local, kPartialThreads, smem, s, sc, cost, unsafe, eps, partials); le != cudaSuccess) return le; }
+  const dim3 grid(sc.nblocks_local, (sc.T * sc.D + kPartCols - 1) / kPartCols);
+  { if (const cudaError_t le = launch_k(k_block_partials, grid, kBlockRollouts, 0, s, sc, cost, unsafe, eps, partials); le != cudaSuccess) return le; }
   return cudaGetLastError();
 }
 
@@ -781,7 +803,7 @@ cudaError_t launch_finalize(const StepConst& sc, const float* val_dmin, const do
                             int guide_cap, double* nominal, StepDyn* dyn, DecisionDev* dec,
                             double* out_dmin, double* out_nominal, double* out_uprev, int commit,
                             float* hstat, float* cap, float radius, cudaStream_t s) {
-  const size_t smem = sizeof(double) * (2 * static_cast<size_t>(guide_cap) + 2 * sc.T);
+  const size_t smem = sizeof(double) * (2 * static_cast<size_t>(guide_cap) + 3 * sc.T);
   if (smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(k_finalize, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(smem));
