@@ -668,7 +668,7 @@ __global__ void __launch_bounds__(128) k_sdf_grid(const __grid_constant__ FpDev 
                                                   unsigned long long* __restrict__ stats = nullptr) {
   pdl_wait();
   unsigned long long n_test = 0, n_eval = 0;
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x, lane = threadIdx.x & 31;
   const bool active = i < n_poses;
   const GridMeta gm = *gmp;
   if (gm.n_valid == 0) {
@@ -721,13 +721,25 @@ __global__ void __launch_bounds__(128) k_sdf_grid(const __grid_constant__ FpDev 
       if (!__any_sync(kFull, need)) break;
     }
     const int ncell = k == 0 ? 1 : 8 * k;
-    for (int t = 0; t < ncell; ++t) {
-      int ii, jj;
-      ring_cell(k, t, ci, cj, ii, jj);
-      if (ii < 0 || jj < 0 || ii >= gm.gx || jj >= gm.gy) continue;
-      const int c = jj * gm.gx + ii;
-      const int s = __ldg(cell_start + c), e = __ldg(cell_start + c + 1);
-      if (s == e) continue;
+    // The warp enumerates the ring 32 cells at a time, one cell per lane (position, range,
+    // CSR bounds: the cell_start loads of the 32 cells are in flight together), and then
+    // visits only the in-range nonempty ones, in ring order, with the cell's data shuffled in.
+    for (int t0 = 0; t0 < ncell; t0 += 32) {
+      int c_i = 0, c_j = 0, c_s = 0, c_e = 0;
+      if (t0 + lane < ncell) {
+        ring_cell(k, t0 + lane, ci, cj, c_i, c_j);
+        if (c_i >= 0 && c_j >= 0 && c_i < gm.gx && c_j < gm.gy) {
+          const int c = c_j * gm.gx + c_i;
+          c_s = __ldg(cell_start + c);
+          c_e = __ldg(cell_start + c + 1);
+        }
+      }
+      unsigned cells = __ballot_sync(kFull, c_s != c_e);
+    while (cells) {
+      const int src = __ffs(cells) - 1;
+      cells &= cells - 1;
+      const int ii = __shfl_sync(kFull, c_i, src), jj = __shfl_sync(kFull, c_j, src);
+      const int s = __shfl_sync(kFull, c_s, src), e = __shfl_sync(kFull, c_e, src);
       const float bx0 = gm.x0 + static_cast<float>(ii) * gm.cs, bx1 = bx0 + gm.cs;
       const float by0 = gm.y0 + static_cast<float>(jj) * gm.cs, by1 = by0 + gm.cs;
       const float gx_ = fmaxf(fmaxf(bx0 - q.x, q.x - bx1), 0.f);
@@ -764,7 +776,8 @@ __global__ void __launch_bounds__(128) k_sdf_grid(const __grid_constant__ FpDev 
           }
         }
       }
-    }
+    }  // cells of this group
+    }  // groups of 32 ring cells
   }
   }  // pass
   if (active) out[i] = best;
