@@ -102,9 +102,10 @@ cudaError_t alloc_cloud_grid(int n_cap, void** block, CloudGrid* g) {
   const size_t o_cs = o_rs + up(cells * sizeof(int)), o_gm = o_cs + up(cells * sizeof(int));
   const size_t o_ds = o_gm + up(sizeof(GridMeta));
   char* d = nullptr;
-  cudaError_t e = cudaMalloc(reinterpret_cast<void**>(&d), o_ds + 2 * sizeof(float));
+  const size_t o_wk = o_ds + up(2 * sizeof(float));
+  cudaError_t e = cudaMalloc(reinterpret_cast<void**>(&d), o_wk + 2 * sizeof(unsigned));
   if (e != cudaSuccess) return e;
-  e = cudaMemset(d + o_ds, 0, 2 * sizeof(float));
+  e = cudaMemset(d + o_ds, 0, o_wk + 2 * sizeof(unsigned) - o_ds);
   if (e != cudaSuccess) return e;
   *block = d;
   g->tmp = reinterpret_cast<float2*>(d);
@@ -115,6 +116,7 @@ cudaError_t alloc_cloud_grid(int n_cap, void** block, CloudGrid* g) {
   g->cell_start = reinterpret_cast<int*>(d + o_cs);
   g->gm = reinterpret_cast<GridMeta*>(d + o_gm);
   g->dstat = reinterpret_cast<float*>(d + o_ds);
+  g->work = reinterpret_cast<unsigned*>(d + o_wk);
   return cudaSuccess;
 }
 

@@ -72,6 +72,8 @@ struct CloudGrid {
   // {sum of clamped per-pose minima, count} accumulated by the stage-cost kernel and consumed
   // (then reset) by the next step's prep kernel: sizes the cells for the searches to come
   float* dstat = nullptr;
+  // {next pose, finished warps} of the persistent k_sdf_grid (zero between launches)
+  unsigned* work = nullptr;
 };
 // Padded cloud capacity for n_cap points: every nonempty cell adds at most kChunk - 1 pads.
 inline size_t cloud_capacity(int n_cap) {
