@@ -179,3 +179,15 @@ def u8ptr(a: np.ndarray | None):
         return None
     assert a.dtype == np.uint8 and a.flags.c_contiguous
     return a.ctypes.data_as(_u8p)
+
+
+def fast_control_cycle(lib):
+    """exm_control_cycle bound a second time with void* pointer arguments: callers pass cached
+    integer addresses (Engine.control_cycle_raw), which skips ctypes' per-call pointer-object
+    construction (several microseconds per argument on the host)."""
+    fn = C.CDLL(lib._name)["exm_control_cycle"]
+    v = C.c_void_p
+    fn.restype = C.c_int32
+    fn.argtypes = [v, v, v, v, C.c_int32, v, C.c_int32, v, v, v, C.c_uint64, v, v]
+    return fn
+

@@ -357,6 +357,31 @@ class Engine:
         check(self.lib.exm_create(C.byref(fp), C.byref(m), C.byref(l), C.byref(p), self.n_cap,
                                   self.guide_cap, int(device), C.byref(h)))
         self.h = h
+        # lean host path of control_cycle_raw: fixed-address scratch and cached addresses
+        self._cc = _abi.fast_control_cycle(self.lib)
+        self._hv = C.cast(h, C.c_void_p).value
+        self._q0buf = np.zeros(3)
+        self._dminbuf = np.zeros(int(params.horizon))
+        self._dec = _abi.ExmDecision()
+        self._dec.nominal_dmin = dptr(self._dminbuf)
+        self._decp = C.addressof(self._dec)
+        self._addrs: dict = {}
+
+    def _addr(self, a, dtype=np.float64):
+        """Address of a C-contiguous array of `dtype`, cached per array object (the cache holds
+        a reference, so an id cannot be reused while its entry lives)."""
+        if a is None:
+            return None
+        ent = self._addrs.get(id(a))
+        if ent is not None and ent[0] is a:
+            return ent[1]
+        if a.dtype != dtype or not a.flags.c_contiguous:
+            raise ValueError("array must be C-contiguous " + np.dtype(dtype).name)
+        if len(self._addrs) >= 64:
+            self._addrs.clear()
+        addr = a.ctypes.data
+        self._addrs[id(a)] = (a, addr)
+        return addr
 
     def close(self):
         if getattr(self, "h", None):
@@ -440,19 +465,19 @@ class Engine:
         """One MPPI step with explicit controller state (nominal and u_prev updated in place)."""
         T = self.params.horizon
         pts, mask = self._cloud(obstacles)
-        dmin = np.empty(T)
-        dec = _abi.ExmDecision()
-        dec.nominal_dmin = dptr(dmin)
+        self._q0buf[:] = q0
         eps_arr = None
         if eps is not None:
             eps_arr = np.ascontiguousarray(np.asarray(eps, np.float64))
-        check(self.lib.exm_control_cycle(
-            self.h, dptr(self._vec3(q0)), dptr(pts), u8ptr(mask), pts.shape[0],
-            dptr(guidance.path), guidance.path.shape[0], dptr(guidance.goal), dptr(nominal),
-            dptr(u_prev), int(cycle), dptr(eps_arr), C.byref(dec)))
+        A = self._addr
+        check(self._cc(self._hv, A(self._q0buf), A(pts), A(mask, np.uint8), pts.shape[0],
+                       A(guidance.path), guidance.path.shape[0], A(guidance.goal), A(nominal),
+                       A(u_prev), int(cycle), A(eps_arr), self._decp))
+        dec = self._dec
         return ControlDecision(np.array(dec.command[: self.dim]), bool(dec.validated),
                                nominal.reshape(T, self.dim).copy(), dec.best_cost,
-                               dec.weight_entropy, dec.nominal_cost, dmin, dec.argmin)
+                               dec.weight_entropy, dec.nominal_cost, self._dminbuf.copy(),
+                               dec.argmin)
 
     def batch_signed_distance(self, queries) -> np.ndarray:
         q = np.ascontiguousarray(np.asarray(queries, np.float64).reshape(-1, 2))
