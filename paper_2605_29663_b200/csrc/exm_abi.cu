@@ -453,8 +453,9 @@ struct EventPair {
 struct exm_handle {
   int device = 0;
   cudaStream_t stream = nullptr;
-  cudaStream_t side = nullptr;  // parallel graph branch (cloud preparation)
-  cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
+  cudaStream_t side = nullptr;  // parallel graph branch (cloud preparation, noise pregeneration)
+  cudaEvent_t fork_ev = nullptr, join_ev = nullptr, pg_fork = nullptr, pg_join = nullptr;
+  uint64_t* d_nstate = nullptr;  // StepConst::nstate
   FpDev fp{};
   StepConst sc{};
   int K = 0, T = 0, D = 0, n_cap = 0, guide_cap = 0;
@@ -582,7 +583,13 @@ bool auto_caps() {
   return on;
 }
 
-exm_status enqueue_post(exm_handle* h, cudaStream_t s, int* launches) {
+// EXM_PREGEN=0: no noise pregeneration (every rollout draws its own noise)
+bool pregen_enabled() {
+  static const bool on = !(std::getenv("EXM_PREGEN") && std::getenv("EXM_PREGEN")[0] == '0');
+  return on;
+}
+
+exm_status enqueue_post(exm_handle* h, cudaStream_t s, int* launches, bool pregen = false) {
   const StepConst& sc = h->sc;
   // automatic per-step caps (d_min statistic -> k_finalize) measured slower than none on the
   // benchmark configs (fallback passes): off unless EXM_AUTO_CAPS=1; exm_set_sdf_caps still works
@@ -591,6 +598,13 @@ exm_status enqueue_post(exm_handle* h, cudaStream_t s, int* launches) {
                                 h->d_xy, h->d_dmin, h->d_cost, h->d_unsafe, h->grid.dstat,
                                 hstat, s));
   EXM_CUDA(launch_block_partials(sc, h->d_cost, h->d_unsafe, h->d_eps, h->d_partials, s));
+  if (pregen) {  // the next cycle's noise on the side branch, overlapping the serial tail
+    EXM_CUDA(cudaEventRecord(h->pg_fork, s));
+    EXM_CUDA(cudaStreamWaitEvent(h->side, h->pg_fork, 0));
+    EXM_CUDA(launch_noise_pregen(sc, h->d_eps, h->side));
+    EXM_CUDA(cudaEventRecord(h->pg_join, h->side));
+    ++*launches;
+  }
   if (h->world > 1) {
     const size_t count = static_cast<size_t>(sc.nblocks_local) * partial_stride(sc.T, sc.D);
     const int rc = g_nccl.allgather(h->d_partials + static_cast<size_t>(sc.block_offset) *
@@ -636,7 +650,9 @@ exm_status enqueue_step(exm_handle* h, bool draw_noise, const EventPair* ev, cud
                                   h->d_dmin, s));
   ++launches;
   if (ev && (st = record_ev(ev->b, s, capturing)) != EXM_OK) return st;
-  if ((st = enqueue_post(h, s, &launches)) != EXM_OK) return st;
+  const bool pregen = draw_noise && h->sc.nstate != nullptr && pregen_enabled();
+  if ((st = enqueue_post(h, s, &launches, pregen)) != EXM_OK) return st;
+  if (pregen) EXM_CUDA(cudaStreamWaitEvent(s, h->pg_join, 0));
   h->launches_per_step = launches;
   return EXM_OK;
 }
@@ -742,7 +758,14 @@ exm_status upload_inputs(exm_handle* h, const double q0[3], const double* pts, c
   return EXM_OK;
 }
 
+// eps is about to hold noise that is not the handle's pregenerated cycle: forget the mark
+exm_status invalidate_pregen(exm_handle* h) {
+  if (h->d_nstate) EXM_CUDA(cudaMemsetAsync(h->d_nstate + 1, 0xff, sizeof(uint64_t), h->stream));
+  return EXM_OK;
+}
+
 exm_status upload_eps(exm_handle* h, const double* eps) {
+  if (const exm_status st = invalidate_pregen(h); st != EXM_OK) return st;
   const size_t row = static_cast<size_t>(h->T) * h->D;
   EXM_CUDA(cudaMemcpyAsync(h->d_eps, eps + static_cast<size_t>(h->sc.r_offset) * row,
                            static_cast<size_t>(h->sc.k_local) * row * sizeof(double),
@@ -889,6 +912,8 @@ exm_status exm_create(const exm_footprint* footprint, const exm_model* model,
   EXM_CUDA_C(cudaStreamCreateWithFlags(&h->side, cudaStreamNonBlocking));
   EXM_CUDA_C(cudaEventCreateWithFlags(&h->fork_ev, cudaEventDisableTiming));
   EXM_CUDA_C(cudaEventCreateWithFlags(&h->join_ev, cudaEventDisableTiming));
+  EXM_CUDA_C(cudaEventCreateWithFlags(&h->pg_fork, cudaEventDisableTiming));
+  EXM_CUDA_C(cudaEventCreateWithFlags(&h->pg_join, cudaEventDisableTiming));
   const size_t KT = static_cast<size_t>(h->K) * h->T;
   const size_t TD = static_cast<size_t>(h->T) * D;
   {
@@ -917,6 +942,9 @@ exm_status exm_create(const exm_footprint* footprint, const exm_model* model,
   }
   EXM_CUDA_C(alloc_cloud_grid(n_cap, &h->d_grid_block, &h->grid));
   EXM_CUDA_C(dalloc(&h->d_eps, KT * D));
+  EXM_CUDA_C(dalloc(&h->d_nstate, 2));
+  EXM_CUDA_C(cudaMemset(h->d_nstate, 0xff, 2 * sizeof(uint64_t)));
+  h->sc.nstate = h->d_nstate;
   EXM_CUDA_C(dalloc(&h->d_poses, KT));
   EXM_CUDA_C(dalloc(&h->d_xy, KT));
   EXM_CUDA_C(dalloc(&h->d_ctrl, KT));
@@ -962,7 +990,7 @@ void exm_destroy(exm_handle* h) {
                  h->d_hstat, h->d_cap, h->d_sense, h->d_val_xy, h->d_base, h->d_dmin,
                  h->d_partials, h->d_upd, h->d_val_poses, h->d_val_base, h->d_val_dmin, h->d_out,
                  h->d_controls, h->d_states, h->d_cost, h->d_unsafe, h->sb_poses, h->sb_pts64,
-                 h->sb_pts, h->sb_mask, h->sb_keys, h->sb_min, h->sb_pairs};
+                 h->sb_pts, h->sb_mask, h->sb_keys, h->sb_min, h->sb_pairs, h->d_nstate};
   for (void* p : dev)
     if (p) cudaFree(p);
   void* host[] = {h->h_in_block, h->h_out};
@@ -979,6 +1007,8 @@ void exm_destroy(exm_handle* h) {
   }
   if (h->fork_ev) cudaEventDestroy(h->fork_ev);
   if (h->join_ev) cudaEventDestroy(h->join_ev);
+  if (h->pg_fork) cudaEventDestroy(h->pg_fork);
+  if (h->pg_join) cudaEventDestroy(h->pg_join);
   if (h->side) cudaStreamDestroy(h->side);
   if (h->stream) cudaStreamDestroy(h->stream);
   delete h;
@@ -1067,6 +1097,7 @@ exm_status exm_sample_perturbations(exm_handle* h, uint64_t seed, uint64_t cycle
   sc.seed = seed;
   h->h_dyn->cycle = cycle;
   EXM_CUDA(cudaMemcpyAsync(h->d_dyn, h->h_dyn, sizeof(StepDyn), cudaMemcpyHostToDevice, h->stream));
+  if (const exm_status st = invalidate_pregen(h); st != EXM_OK) return st;
   EXM_CUDA(launch_noise(sc, h->d_dyn, h->d_eps, h->stream));
   const size_t n = static_cast<size_t>(h->K) * h->T * h->D;
   EXM_CUDA(cudaMemcpyAsync(eps_out, h->d_eps, n * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
@@ -1232,7 +1263,7 @@ exm_status exm_attach_comm(exm_handle* h, int32_t rank, int32_t world, const uin
     if (rc != 0) return fail(EXM_ERR_NCCL, "ncclCommInitRank failed");
   }
   set_shard(h);
-  return EXM_OK;
+  return invalidate_pregen(h);  // the shard (and so the noise rows eps holds) changed
 }
 
 exm_status exm_stage_inputs(exm_handle* h, const double q0[3], const double* pts_xy,

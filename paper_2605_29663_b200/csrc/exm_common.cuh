@@ -121,6 +121,9 @@ struct StepConst {
   double vel_min[3], vel_max[3], acc_min[3], acc_max[3];
   double steer_max;
   uint64_t seed;
+  // device noise state {cycle of the last drawing rollout, cycle whose noise eps holds
+  // (pregenerated by k_noise_pregen; ~0 = none)}; nullptr: always draw in the rollout
+  uint64_t* nstate;
 };
 
 struct DecisionDev {
@@ -163,6 +166,8 @@ cudaError_t launch_k(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t sme
 
 // ---- kernel launchers (exm_kernels.cu) ---------------------------------------------------
 cudaError_t launch_noise(const StepConst& sc, const StepDyn* dyn, double* eps, cudaStream_t s);
+// The next cycle's device noise (cycle sc.nstate[0] + 1) into eps, marked in sc.nstate[1]
+cudaError_t launch_noise_pregen(const StepConst& sc, double* eps, cudaStream_t s);
 cudaError_t launch_cloud_prep(const double* pts, const uint8_t* mask, const StepDyn* dyn,
                               float radius, const CloudGrid& g, cudaStream_t s);
 // draw != 0: the rollout kernel draws the device noise into eps; else eps is read (injected).

@@ -290,6 +290,21 @@ __global__ void k_noise(const StepConst sc, const StepDyn* __restrict__ dyn,
   for (int c = 0; c < sc.D; ++c) eps[static_cast<size_t>(idx) * sc.D + c] = noise_at(sc, key, h, c);
 }
 
+// The next control step's device noise, generated in the idle tail of this step (after the
+// softmax partials, the last reader of eps): cycle = the cycle this step's rollout drew + 1.
+// The next rollout finds sc.nstate[1] == its cycle and reads eps instead of drawing (a
+// different cycle, e.g. a caller restarting the sequence, simply draws). One thread per (r, h).
+__global__ void k_noise_pregen(const StepConst sc, double* __restrict__ eps) {
+  pdl_wait();
+  const uint64_t cycle = sc.nstate[0] + 1;
+  if (blockIdx.x == 0 && threadIdx.x == 0) sc.nstate[1] = cycle;  // read by the next graph
+  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= sc.k_local * sc.T) return;
+  const int r = idx / sc.T, h = idx - r * sc.T;
+  const uint64_t key = noise_row_key(sc, cycle, r);
+  for (int c = 0; c < sc.D; ++c) eps[static_cast<size_t>(idx) * sc.D + c] = noise_at(sc, key, h, c);
+}
+
 template <int TAG>
 __global__ void __launch_bounds__(kRolloutWarps * 32) k_rollout(
     const StepConst sc, const StepDyn* __restrict__ dynp, const double* __restrict__ nominal,
@@ -306,18 +321,196 @@ __global__ void __launch_bounds__(kRolloutWarps * 32) k_rollout(
   double* scratch = sm + TD + warp * rollout_warp_scratch(sc.T, sc.D);
   for (int i = threadIdx.x; i < TD; i += blockDim.x) nom[i] = nominal[i];
   const StepDyn dyn = *dynp;
+  const bool gen = draw && !(sc.nstate && sc.nstate[1] == dyn.cycle);  // else pregenerated
+  if (draw && sc.nstate && blockIdx.x == 0 && threadIdx.x == 0) sc.nstate[0] = dyn.cycle;
   __syncthreads();
   const int r = blockIdx.x * kRolloutWarps + warp;
   if (r >= sc.k_local) return;  // warp-uniform
   const size_t row = static_cast<size_t>(r) * sc.T;
   double* eps_row = eps + row * sc.D;
   const double b = rollout_warp<TAG>(
-      sc, dyn, nom, draw ? nullptr : eps_row, draw ? eps_row : nullptr,
-      draw ? noise_row_key(sc, dyn.cycle, r) : 0ull, poses + row, xy + row,
+      sc, dyn, nom, gen ? nullptr : eps_row, gen ? eps_row : nullptr,
+      gen ? noise_row_key(sc, dyn.cycle, r) : 0ull, poses + row, xy + row,
       controls_out ? controls_out + row * sc.D : nullptr,
       states_out ? states_out + static_cast<size_t>(r) * (sc.T + 1) * 3 : nullptr, ctrl_cost + row,
       scratch);
   if ((threadIdx.x & 31) == 0) base_cost[r] = b;
+}
+
+// The same rollouts as k_rollout with the recurrences on one LANE per rollout: a CTA of
+// kLaneThreads threads takes R rollouts; the parallel work (noise, velocity clamp, heading
+// rates, control costs, sin/cos, xy rates, stores) is spread over all (r, h, c) items, and each
+// serial recurrence (rate clamp per component, heading, x, y) runs on R lanes side by side,
+// so a chain instruction serves R rollouts instead of one. Every value is produced by the
+// same single-rounded FP64 operations in the same order as rollout_warp (bit-identical).
+// Shared memory ([item][R + 1] rows: conflict-free lanes over r):
+//   u[T*D], a[T] (heading increments -> pre-step headings), x[T], y[T] doubles, cs[T] float2
+constexpr int kLaneThreads = 256;
+__host__ __device__ constexpr size_t rollout_lanes_smem(int T, int D, int R) {
+  return sizeof(double) * (static_cast<size_t>(T) * (D + 3) * (R + 1) + static_cast<size_t>(T) * D +
+                           3 * R) +
+         sizeof(uint64_t) * R + sizeof(float2) * static_cast<size_t>(T) * (R + 1);
+}
+
+template <int TAG, int R>
+__global__ void __launch_bounds__(1024) k_rollout_lanes(
+    const StepConst sc, const StepDyn* __restrict__ dynp, const double* __restrict__ nominal,
+    double* __restrict__ eps, int draw, float4* __restrict__ poses, double2* __restrict__ xy,
+    double* __restrict__ base_cost, double* __restrict__ ctrl_cost,
+    double* __restrict__ controls_out, double* __restrict__ states_out) {
+  pdl_wait();
+  constexpr int D = model_dim<TAG>();
+  constexpr int P = R + 1;
+  const int T = sc.T, TD = T * D, tid = threadIdx.x, nthr = blockDim.x;
+  extern __shared__ double smd[];
+  double* s_u = smd;                          // [TD][P]
+  double* s_a = s_u + static_cast<size_t>(TD) * P;  // [T][P]
+  double* s_x = s_a + static_cast<size_t>(T) * P;
+  double* s_y = s_x + static_cast<size_t>(T) * P;
+  double* s_nom = s_y + static_cast<size_t>(T) * P;  // [TD]
+  double* s_end = s_nom + TD;                 // [3][R]: x_T, y_T, theta_T
+  uint64_t* s_key = reinterpret_cast<uint64_t*>(s_end + 3 * R);
+  float2* s_cs = reinterpret_cast<float2*>(s_key + R);  // [T][P]
+  const int r0 = blockIdx.x * R;
+  const int nr = min(R, sc.k_local - r0);
+  if (nr <= 0) return;
+  const StepDyn dyn = *dynp;
+  // eps already holds this cycle's noise when the previous step pregenerated it
+  const bool gen = draw && !(sc.nstate && sc.nstate[1] == dyn.cycle);
+  if (draw && sc.nstate && blockIdx.x == 0 && tid == 0) sc.nstate[0] = dyn.cycle;
+  for (int i = tid; i < TD; i += nthr) s_nom[i] = nominal[i];
+  if (gen && tid < R) s_key[tid] = noise_row_key(sc, dyn.cycle, r0 + tid);
+  __syncthreads();
+  // 1. u = clamp_velocity(nominal + eps); eps drawn here (device noise) or loaded, kPre
+  //    loads per thread in flight together (the rows come from HBM)
+  constexpr int kPre = 8;
+  double* erow = eps + static_cast<size_t>(r0) * TD;
+  const int n_items = nr * TD;
+  for (int base = tid; base < n_items; base += nthr * kPre) {
+    double ev[kPre];
+#pragma unroll
+    for (int k = 0; k < kPre; ++k) {
+      const int idx = base + k * nthr;
+      ev[k] = (!gen && idx < n_items) ? erow[idx] : 0.0;
+    }
+#pragma unroll
+    for (int k = 0; k < kPre; ++k) {
+      const int idx = base + k * nthr;
+      if (idx >= n_items) break;
+      const int r = idx / TD, o = idx - r * TD, c = o % D;
+      double e = ev[k];
+      if (gen) {
+        e = noise_at(sc, s_key[r], o / D, c);
+        erow[idx] = e;
+      }
+      double lo = sc.vel_min[c], hi = sc.vel_max[c];
+      if (TAG == EXM_MODEL_ACKERMANN && c == 1) {
+        lo = mx(lo, -sc.steer_max);
+        hi = mn(hi, sc.steer_max);
+      }
+      s_u[o * P + r] = clampd(__dadd_rn(s_nom[o], e), lo, hi);
+    }
+  }
+  __syncthreads();
+  // 2. rate clamp, one lane per (component, rollout) (kinematics.cpp:113)
+  if (tid < D * R) {
+    const int r = tid % R, c = tid / R;
+    if (r < nr) {
+      const double amin = __dmul_rn(sc.acc_min[c], sc.dt), amax = __dmul_rn(sc.acc_max[c], sc.dt);
+      double prev = dyn.u_prev[c];
+      double* col = s_u + c * P + r;
+#pragma unroll 5
+      for (int h = 0; h < T; ++h) {
+        prev = clampd(col[h * D * P], __dadd_rn(prev, amin), __dadd_rn(prev, amax));
+        col[h * D * P] = prev;
+      }
+    }
+  }
+  __syncthreads();
+  // 3. heading increments and control costs
+  for (int idx = tid; idx < nr * T; idx += nthr) {
+    const int r = idx / T, h = idx - r * T;
+    double uc[3] = {0.0, 0.0, 0.0};
+#pragma unroll
+    for (int c = 0; c < D; ++c) uc[c] = s_u[(h * D + c) * P + r];
+    s_a[h * P + r] = __dmul_rn(heading_rate<TAG>(sc, uc), sc.dt);
+    ctrl_cost[static_cast<size_t>(r0) * T + idx] = control_cost<TAG>(sc, uc);
+  }
+  __syncthreads();
+  // 4. heading chain
+  if (tid < nr) {
+    double th = dyn.q0[2];
+#pragma unroll 5
+    for (int h = 0; h < T; ++h) {
+      const double inc = s_a[h * P + tid];
+      s_a[h * P + tid] = th;
+      th = __dadd_rn(th, inc);
+    }
+    s_end[2 * R + tid] = th;
+  }
+  __syncthreads();
+  // 5. sin / cos of every pre-step heading, xy increments
+  for (int idx = tid; idx < nr * T; idx += nthr) {
+    const int r = idx / T, h = idx - r * T;
+    double st, ct;
+    sincos(s_a[h * P + r], &st, &ct);
+    s_cs[h * P + r] = make_float2(static_cast<float>(ct), static_cast<float>(st));
+    double uc[3] = {0.0, 0.0, 0.0};
+#pragma unroll
+    for (int c = 0; c < D; ++c) uc[c] = s_u[(h * D + c) * P + r];
+    double fx, fy;
+    xy_rate<TAG>(uc, ct, st, fx, fy);
+    s_x[h * P + r] = __dmul_rn(fx, sc.dt);
+    s_y[h * P + r] = __dmul_rn(fy, sc.dt);
+  }
+  __syncthreads();
+  // 6. x and y chains, one lane each per rollout
+  if (tid < 2 * R) {
+    const int r = tid % R, k = tid / R;
+    if (r < nr) {
+      double* chain = (k == 0 ? s_x : s_y) + r;
+      double v = dyn.q0[k];
+#pragma unroll 5
+      for (int h = 0; h < T; ++h) {
+        const double inc = chain[h * P];
+        chain[h * P] = v;
+        v = __dadd_rn(v, inc);
+      }
+      s_end[k * R + r] = v;
+    }
+  }
+  __syncthreads();
+  // 7. stores (rows of consecutive h: coalesced) and the terminal cost
+  const double qx0 = dyn.q0[0], qy0 = dyn.q0[1];
+  for (int idx = tid; idx < nr * T; idx += nthr) {
+    const int r = idx / T, h = idx - r * T;
+    const double x = s_x[h * P + r], y = s_y[h * P + r];
+    const float2 cs = s_cs[h * P + r];
+    const size_t g = static_cast<size_t>(r0) * T + idx;
+    poses[g] = make_float4(static_cast<float>(x - qx0), static_cast<float>(y - qy0), cs.x, cs.y);
+    xy[g] = make_double2(x, y);
+    if (states_out) {
+      double* srow = states_out + static_cast<size_t>(r0 + r) * (T + 1) * 3;
+      srow[3 * h] = x;
+      srow[3 * h + 1] = y;
+      srow[3 * h + 2] = s_a[h * P + r];
+    }
+  }
+  if (controls_out)
+    for (int idx = tid; idx < nr * TD; idx += nthr) {
+      const int r = idx / TD, o = idx - r * TD;
+      controls_out[static_cast<size_t>(r0) * TD + idx] = s_u[o * P + r];
+    }
+  if (tid < nr) {
+    const double qT[3] = {s_end[tid], s_end[R + tid], s_end[2 * R + tid]};
+    base_cost[r0 + tid] = terminal_cost(sc, qT, dyn.goal);
+    if (states_out) {
+      double* srow = states_out + static_cast<size_t>(r0 + tid) * (T + 1) * 3;
+      srow[3 * T] = qT[0];
+      srow[3 * T + 1] = qT[1];
+      srow[3 * T + 2] = qT[2];
+    }
+  }
 }
 
 // Rollout cost J_r and unsafe flag chi_r (score_rollout, controller.cpp:151-171), one warp per
@@ -711,11 +904,64 @@ cudaError_t launch_noise(const StepConst& sc, const StepDyn* dyn, double* eps, c
   return cudaGetLastError();
 }
 
+template <int TAG, int R>
+cudaError_t rollout_lanes_launch(const StepConst& sc, const StepDyn* dyn, const double* nominal,
+                                 double* eps, int draw, float4* poses, double2* xy,
+                                 double* base_cost, double* ctrl_cost, double* controls_out,
+                                 double* states_out, size_t smem, cudaStream_t s) {
+  static size_t attr = 0;
+  if (smem > 48 * 1024 && smem > attr) {
+    cudaError_t e = cudaFuncSetAttribute(k_rollout_lanes<TAG, R>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(smem));
+    if (e != cudaSuccess) return e;
+    attr = smem;
+  }
+  static const int threads = getenv("EXM_LANE_THREADS") ? atoi(getenv("EXM_LANE_THREADS")) : kLaneThreads;
+  if (const cudaError_t le = launch_k(k_rollout_lanes<TAG, R>, (sc.k_local + R - 1) / R,
+                                      threads, smem, s, sc, dyn, nominal, eps, draw, poses,
+                                      xy, base_cost, ctrl_cost, controls_out, states_out);
+      le != cudaSuccess)
+    return le;
+  return cudaGetLastError();
+}
+
+// EXM_ROLLOUT=warp: the warp-per-rollout kernel (A/B); default: lanes per rollout when the
+// CTA's shared memory fits (32 rollouts per CTA, else 16), warp per rollout otherwise.
+inline bool rollout_warp_mode() {
+  static const bool on = getenv("EXM_ROLLOUT") && !strcmp(getenv("EXM_ROLLOUT"), "warp");
+  return on;
+}
+
+cudaError_t launch_noise_pregen(const StepConst& sc, double* eps, cudaStream_t s) {
+  const int n = sc.k_local * sc.T;
+  if (n <= 0 || sc.nstate == nullptr) return cudaSuccess;
+  { if (const cudaError_t le = launch_k(k_noise_pregen, (n + 255) / 256, 256, 0, s, sc, eps); le != cudaSuccess) return le; }
+  return cudaGetLastError();
+}
+
 template <int TAG>
 cudaError_t rollout_tag(const StepConst& sc, const StepDyn* dyn, const double* nominal,
                         double* eps, int draw, float4* poses, double2* xy, double* base_cost,
                         double* ctrl_cost, double* controls_out, double* states_out,
                         cudaStream_t s) {
+  if (!rollout_warp_mode()) {
+    constexpr int D = model_dim<TAG>();
+    const size_t s32 = rollout_lanes_smem(sc.T, D, 32), s16 = rollout_lanes_smem(sc.T, D, 16);
+    // 8 rollouts per CTA: ~28 resident warps per SM hide the eps loads (cold L2) as well as
+    // the warp-per-rollout kernel does, with a quarter of its instructions
+    static const int want_r = getenv("EXM_LANE_R") ? atoi(getenv("EXM_LANE_R")) : 8;
+    if (want_r == 8)
+      return rollout_lanes_launch<TAG, 8>(sc, dyn, nominal, eps, draw, poses, xy, base_cost,
+                                          ctrl_cost, controls_out, states_out,
+                                          rollout_lanes_smem(sc.T, D, 8), s);
+    if (want_r == 32 && s32 <= 100 * 1024)
+      return rollout_lanes_launch<TAG, 32>(sc, dyn, nominal, eps, draw, poses, xy, base_cost,
+                                           ctrl_cost, controls_out, states_out, s32, s);
+    if (s16 <= 200 * 1024)
+      return rollout_lanes_launch<TAG, 16>(sc, dyn, nominal, eps, draw, poses, xy, base_cost,
+                                           ctrl_cost, controls_out, states_out, s16, s);
+  }
   const int threads = kRolloutWarps * 32;
   const size_t smem = sizeof(double) * (static_cast<size_t>(sc.T) * sc.D +
                                         kRolloutWarps * static_cast<size_t>(rollout_warp_scratch(sc.T, sc.D)));

@@ -1256,7 +1256,8 @@ template <int KIND, int NB, bool STATS, int MODE>
 cudaError_t launch_grid_kernel(const FpDev& fp, const float4* poses, int n_poses,
                                const CloudGrid& g, const float* cap, int T, float* out,
                                unsigned long long* stats, cudaStream_t s) {
-  const int threads = 128, blocks = (n_poses + threads - 1) / threads;
+  static const int threads = getenv("EXM_SDF_THREADS") ? atoi(getenv("EXM_SDF_THREADS")) : 128;
+  const int blocks = (n_poses + threads - 1) / threads;
   auto k = k_sdf_grid<KIND, NB, STATS, MODE>;
   // persistent only for many waves (cfg5: ~30): at one to three waves the hardware block
   // scheduler balances as well and the static mapping keeps neighbouring poses in one CTA

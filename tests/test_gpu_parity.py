@@ -258,3 +258,23 @@ def test_full_size_cfg2_sampled_parity():
     aug = r.costs + wl.params.w_inf * r.unsafe
     assert d.argmin == int(np.argmin(aug))
     assert abs(d.best_cost - aug.min()) <= 1e-9 * max(1.0, abs(aug.min()))
+
+
+def test_pregenerated_noise_is_the_drawn_noise():
+    """The next cycle's noise is generated in the tail of each step (k_noise_pregen) and used
+    by the next rollout when its cycle matches: consecutive device-noise cycles, a jump in the
+    cycle sequence (no pregenerated match) and a repeat after injected noise must all equal the
+    same cycles run with that cycle's noise injected (exm_sample_perturbations), bit for bit."""
+    wl = W.cfg2(K=512, T=16, N=2000)
+    eng, _ = engine_and_oracle(wl)
+    ref, _ = engine_and_oracle(wl)
+    nom, up = wl.zero_state()
+    nom_r, up_r = wl.zero_state()
+    for cyc in [0, 1, 2, 3, 9, 10, 10, 11]:
+        d = eng.control_cycle_raw(wl.q0, wl.obstacles(), wl.guidance, nom, up, cyc)
+        eps = ref.sample_perturbations(wl.params.seed, cyc)
+        r = ref.control_cycle_raw(wl.q0, wl.obstacles(), wl.guidance, nom_r, up_r, cyc, eps)
+        assert np.array_equal(d.command, r.command), cyc
+        assert np.array_equal(nom, nom_r), cyc
+        assert d.argmin == r.argmin and d.best_cost == r.best_cost, cyc
+        assert d.weight_entropy == r.weight_entropy, cyc
