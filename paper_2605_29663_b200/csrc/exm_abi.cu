@@ -11,6 +11,7 @@
 
 #include <algorithm>
 #include <array>
+#include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -456,6 +457,8 @@ struct exm_handle {
   cudaStream_t side = nullptr;  // parallel graph branch (cloud preparation, noise pregeneration)
   cudaEvent_t fork_ev = nullptr, join_ev = nullptr, pg_fork = nullptr, pg_join = nullptr;
   uint64_t* d_nstate = nullptr;  // StepConst::nstate
+  double host_us[4] = {0.0, 0.0, 0.0, 0.0};  // EXM_HOST_TIMING
+  int64_t host_calls = 0;
   FpDev fp{};
   StepConst sc{};
   int K = 0, T = 0, D = 0, n_cap = 0, guide_cap = 0;
@@ -512,6 +515,7 @@ struct exm_handle {
   std::vector<EventPair> ring;
   int ring_used = 0;
   EventPair step_ev;
+  EventPair ev_set[2];  // events the exec's SDF event nodes currently record
   int last_steps = 0;
   // SDF batch workspace (grown on demand)
   int sb_poses_cap = 0, sb_points_cap = 0;
@@ -685,15 +689,19 @@ exm_status ensure_graph(exm_handle* h, int variant) {
   }
   h->graph[variant] = g;
   h->exec[variant] = exec;
+  h->ev_set[variant] = h->graph_ev;  // as captured
   return EXM_OK;
 }
 
 exm_status launch_graph(exm_handle* h, int variant, const EventPair& ev) {
   exm_status st = ensure_graph(h, variant);
   if (st != EXM_OK) return st;
-  if (h->ev_node[variant][0]) {
+  // retarget the SDF-bracketing event nodes only when the events change (benchmark rings);
+  // repeated exm_control_cycle calls reuse step_ev and skip the two exec-node updates
+  if (h->ev_node[variant][0] && (h->ev_set[variant].a != ev.a || h->ev_set[variant].b != ev.b)) {
     EXM_CUDA(cudaGraphExecEventRecordNodeSetEvent(h->exec[variant], h->ev_node[variant][0], ev.a));
     EXM_CUDA(cudaGraphExecEventRecordNodeSetEvent(h->exec[variant], h->ev_node[variant][1], ev.b));
+    h->ev_set[variant] = ev;
   }
   EXM_CUDA(cudaGraphLaunch(h->exec[variant], h->stream));
   return EXM_OK;
@@ -719,6 +727,29 @@ exm_status check_guide(const exm_handle* h, const double* g, int32_t n) {
   if (n < 1 || !g) return fail(EXM_ERR_INVALID_ARGUMENT, "guidance polyline is empty");
   if (n > h->guide_cap) return fail(EXM_ERR_INVALID_ARGUMENT, "guidance polyline exceeds guide_cap");
   return EXM_OK;
+}
+
+// EXM_HOST_TIMING=1: per-phase host wall time of exm_control_cycle (stage+enqueue H2D,
+// graph launch + D2H enqueue, wait, unpack), accumulated per handle, printed by exm_destroy.
+bool host_timing() {
+  static const bool on = std::getenv("EXM_HOST_TIMING") && std::getenv("EXM_HOST_TIMING")[0] == '1';
+  return on;
+}
+struct HostTimer {
+  exm_handle* h;
+  std::chrono::steady_clock::time_point t0;
+  explicit HostTimer(exm_handle* hh) : h(hh) {
+    if (host_timing()) t0 = std::chrono::steady_clock::now();
+  }
+  void mark(int phase);
+};
+
+void HostTimer::mark(int phase) {
+  if (!host_timing()) return;
+  const auto t = std::chrono::steady_clock::now();
+  h->host_us[phase] += std::chrono::duration<double, std::micro>(t - t0).count();
+  t0 = t;
+  if (phase == 3) ++h->host_calls;
 }
 
 // Stage the per-step inputs into pinned memory and enqueue their H2D copies.
@@ -981,6 +1012,11 @@ exm_status exm_create(const exm_footprint* footprint, const exm_model* model,
 
 void exm_destroy(exm_handle* h) {
   if (!h) return;
+  if (host_timing() && h->host_calls > 0)
+    std::fprintf(stderr, "[exm host] %lld calls, us/call: stage+H2D %.1f launch %.1f wait %.1f unpack %.1f\n",
+                 static_cast<long long>(h->host_calls), h->host_us[0] / h->host_calls,
+                 h->host_us[1] / h->host_calls, h->host_us[2] / h->host_calls,
+                 h->host_us[3] / h->host_calls);
   cudaSetDevice(h->device);
   if (h->stream) cudaStreamSynchronize(h->stream);
   destroy_graphs(h);
@@ -1021,6 +1057,7 @@ exm_status exm_control_cycle(exm_handle* h, const double q0[3], const double* pt
                              exm_decision* out) {
   if (!h) return fail(EXM_ERR_INVALID_ARGUMENT, "handle is null");
   if (!nominal_inout || !u_prev_inout) return fail(EXM_ERR_INVALID_ARGUMENT, "null state pointer");
+  HostTimer ht(h);
   EXM_CUDA(cudaSetDevice(h->device));
   exm_status st = upload_inputs(h, q0, pts_xy, mask, n_points, guide_xy, n_guide, goal,
                                 nominal_inout, u_prev_inout, cycle);
@@ -1029,14 +1066,18 @@ exm_status exm_control_cycle(exm_handle* h, const double q0[3], const double* pt
     st = upload_eps(h, eps_or_null);
     if (st != EXM_OK) return st;
   }
+  ht.mark(0);
   st = launch_graph(h, eps_or_null ? 1 : 0, h->step_ev);
   if (st != EXM_OK) return st;
   EXM_CUDA(cudaMemcpyAsync(h->h_out, h->d_out, h->out_bytes, cudaMemcpyDeviceToHost, h->stream));
+  ht.mark(1);
   EXM_CUDA(cudaStreamSynchronize(h->stream));
+  ht.mark(2);
   h->last_steps = 1;
   h->ring_used = 0;
   h->last_pairs = static_cast<int64_t>(h->sc.k_local) * h->T * n_points;
   unpack_decision(h, out, nominal_inout, u_prev_inout);
+  ht.mark(3);
   return EXM_OK;
 }
 
