@@ -14,10 +14,15 @@ tail -1 "$out/pytest_gpu.log"
 python tools/ncu_targets.py step 5 > /dev/null 2>&1 && \
   ncu --metrics gpu__time_duration.sum --clock-control none --csv \
       --log-file "$out/launches_step_cfg2.csv" python tools/ncu_targets.py step 5 > /dev/null 2>&1
-python tools/ncu_targets.py step 3 > /dev/null 2>&1 && \
+# the same with warm caches (no flush between kernels): the in-step durations
+python tools/ncu_targets.py step 20 > /dev/null 2>&1 && \
+  ncu --metrics gpu__time_duration.sum --clock-control none --cache-control none --csv \
+      --log-file "$out/launches_step_cfg2_warm.csv" python tools/ncu_targets.py step 20 > /dev/null 2>&1
+# a steady-state step (the 25th: the nominal has converged, as in the bench's timed steps)
+python tools/ncu_targets.py step 26 > /dev/null 2>&1 && \
   ncu --set full --clock-control none --import-source on --kernel-name-base mangled \
-      -k regex:"10k_sdf_gridI" -s 1 -c 1 -f -o "$out/ncu_sdf_grid_cfg2" \
-      python tools/ncu_targets.py step 3 > /dev/null 2>&1 && \
+      -k regex:"10k_sdf_gridI" -s 25 -c 1 -f -o "$out/ncu_sdf_grid_cfg2" \
+      python tools/ncu_targets.py step 26 > /dev/null 2>&1 && \
   python tools/ncu_summary.py "$out/ncu_sdf_grid_cfg2.ncu-rep" > "profiles/${tag}_ncu_sdf_grid_cfg2.json"
 python tools/ncu_targets.py pairs 2 > /dev/null 2>&1 && \
   ncu --set full --clock-control none --import-source on --kernel-name-base mangled \
