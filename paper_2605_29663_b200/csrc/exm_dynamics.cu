@@ -520,7 +520,7 @@ __global__ void __launch_bounds__(1024) k_rollout_lanes(
 // in exactly the reference's order (with k_rollout's control and terminal costs), so J_r is
 // the reference's value for the same d_min. Also accumulates the search-radius statistic of
 // the next step's cell size (k_cloud_prep).
-constexpr int kCostWarps = 16;
+template <int kCostWarps>
 __global__ void __launch_bounds__(kCostWarps * 32) k_rollout_costs(
     const StepConst sc, const StepDyn* __restrict__ dynp, const double* __restrict__ guide,
     const double* __restrict__ base_cost, const double* __restrict__ ctrl_cost,
@@ -973,10 +973,10 @@ cudaError_t rollout_tag(const StepConst& sc, const StepDyn* dyn, const double* n
     // 8 rollouts per CTA: ~28 resident warps per SM hide the eps loads (cold L2) as well as
     // the warp-per-rollout kernel does, with a quarter of its instructions
     static const int want_r = getenv("EXM_LANE_R") ? atoi(getenv("EXM_LANE_R")) : 8;
-    if (want_r == 8)
+    const size_t s8 = rollout_lanes_smem(sc.T, D, 8);
+    if (want_r == 8 && s8 <= 200 * 1024)
       return rollout_lanes_launch<TAG, 8>(sc, dyn, nominal, eps, draw, poses, xy, base_cost,
-                                          ctrl_cost, controls_out, states_out,
-                                          rollout_lanes_smem(sc.T, D, 8), s);
+                                          ctrl_cost, controls_out, states_out, s8, s);
     if (want_r == 32 && s32 <= 100 * 1024)
       return rollout_lanes_launch<TAG, 32>(sc, dyn, nominal, eps, draw, poses, xy, base_cost,
                                            ctrl_cost, controls_out, states_out, s32, s);
@@ -1011,21 +1011,40 @@ cudaError_t launch_rollout(const StepConst& sc, const StepDyn* dyn, const double
   return cudaErrorInvalidValue;
 }
 
+template <int W>
+cudaError_t rollout_costs_launch(const StepConst& sc, const StepDyn* dyn, const double* guide,
+                                 int guide_cap, const double* base_cost, const double* ctrl_cost,
+                                 const double2* xy, const float* dmin, double* cost,
+                                 uint8_t* unsafe, float* dstat, float* hstat, size_t smem,
+                                 cudaStream_t s) {
+  if (smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(k_rollout_costs<W>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(smem));
+    if (e != cudaSuccess) return e;
+  }
+  { if (const cudaError_t le = launch_k(k_rollout_costs<W>, (sc.k_local + W - 1) / W, W * 32, smem, s,
+      sc, dyn, guide, base_cost, ctrl_cost, xy, dmin, cost, unsafe, dstat, hstat); le != cudaSuccess) return le; }
+  return cudaGetLastError();
+}
+
 cudaError_t launch_rollout_costs(const StepConst& sc, const StepDyn* dyn, const double* guide,
                                  int guide_cap, const double* base_cost, const double* ctrl_cost,
                                  const double2* xy, const float* dmin, double* cost,
                                  uint8_t* unsafe, float* dstat, float* hstat, cudaStream_t s) {
   if (sc.k_local <= 0) return cudaSuccess;
-  const size_t smem = sizeof(double) * (2 * static_cast<size_t>(guide_cap) +
-                                        3 * static_cast<size_t>(kCostWarps) * sc.T + sc.T);
-  if (smem > 48 * 1024) {
-    cudaError_t e = cudaFuncSetAttribute(k_rollout_costs, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(smem));
-    if (e != cudaSuccess) return e;
-  }
-  { if (const cudaError_t le = launch_k(k_rollout_costs, (sc.k_local + kCostWarps - 1) / kCostWarps, kCostWarps * 32, smem, s, 
-      sc, dyn, guide, base_cost, ctrl_cost, xy, dmin, cost, unsafe, dstat, hstat); le != cudaSuccess) return le; }
-  return cudaGetLastError();
+  // 16 rollouts per CTA; long horizons (per-warp stage arrays beyond ~200 KB) use fewer
+  auto smem_for = [&](int w) {
+    return sizeof(double) * (2 * static_cast<size_t>(guide_cap) + 3 * static_cast<size_t>(w) * sc.T +
+                             sc.T);
+  };
+  if (smem_for(16) <= 200 * 1024)
+    return rollout_costs_launch<16>(sc, dyn, guide, guide_cap, base_cost, ctrl_cost, xy, dmin, cost,
+                                    unsafe, dstat, hstat, smem_for(16), s);
+  if (smem_for(4) <= 200 * 1024)
+    return rollout_costs_launch<4>(sc, dyn, guide, guide_cap, base_cost, ctrl_cost, xy, dmin, cost,
+                                   unsafe, dstat, hstat, smem_for(4), s);
+  return rollout_costs_launch<1>(sc, dyn, guide, guide_cap, base_cost, ctrl_cost, xy, dmin, cost,
+                                 unsafe, dstat, hstat, smem_for(1), s);
 }
 
 cudaError_t launch_block_partials(const StepConst& sc, const double* cost, const uint8_t* unsafe,

@@ -37,6 +37,10 @@ CASES = {
 
 def _dmin(wl, mode, caps=None):
     old = os.environ.get("EXM_GRID_MODE")
+    old_p = os.environ.pop("EXM_SDF_PERSIST", None)
+    if mode == "persist":  # thread per pose, persistent warps with the work counter
+        mode = "thread"
+        os.environ["EXM_SDF_PERSIST"] = "1"
     os.environ["EXM_GRID_MODE"] = mode
     try:
         eng = Engine(wl.model, wl.limits, wl.footprint, wl.params, n_cap=wl.n_points, guide_cap=8)
@@ -52,6 +56,9 @@ def _dmin(wl, mode, caps=None):
         eng.close()
         return np.concatenate([o.reshape(-1) for o in out])
     finally:
+        os.environ.pop("EXM_SDF_PERSIST", None)
+        if old_p is not None:
+            os.environ["EXM_SDF_PERSIST"] = old_p
         if old is None:
             del os.environ["EXM_GRID_MODE"]
         else:
@@ -59,7 +66,7 @@ def _dmin(wl, mode, caps=None):
 
 
 @pytest.mark.parametrize("case", list(CASES))
-@pytest.mark.parametrize("mode", ["thread", "warp", "cta", "nochunk"])
+@pytest.mark.parametrize("mode", ["thread", "warp", "cta", "nochunk", "persist"])
 def test_culled_minimum_is_bitwise_brute_force(case, mode):
     wl = CASES[case]()
     want = _dmin(wl, "brute")

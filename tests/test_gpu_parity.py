@@ -96,6 +96,8 @@ SMALL = {
     "cfg2": lambda: W.cfg2(K=512, T=20, N=3000),
     "cfg3": lambda: W.cfg3(K=256, T=20, N=4000),
     "cfg5": lambda: W.cfg5(K=256, T=16, N=4000),
+    # a horizon whose lane-per-rollout tiles exceed shared memory: the warp-per-rollout kernel
+    "cfg5_long": lambda: W.cfg5(K=64, T=600, N=2000),
 }
 
 
