@@ -570,7 +570,7 @@ void destroy_graphs(exm_handle* h) {
 //   post  : stage costs -> block partials -> [all-gather] -> merge/update/validation
 //           dynamics -> validation SDF -> finalize                    -> d_out, state
 exm_status enqueue_prep(exm_handle* h, cudaStream_t s) {
-  EXM_CUDA(launch_cloud_prep(h->d_pts, h->d_mask, h->d_dyn, h->fp.radius, h->grid, s));
+  EXM_CUDA(launch_cloud_prep(h->d_pts, h->d_mask, h->d_dyn, h->fp.radius, h->grid, h->n_cap, s));
   return EXM_OK;
 }
 
@@ -1101,7 +1101,7 @@ exm_status exm_evaluate_rollouts(exm_handle* h, const double q0[3], const double
   if (states_out && !h->d_states) EXM_CUDA(dalloc(&h->d_states, static_cast<size_t>(h->K) * (h->T + 1) * 3));
   cudaStream_t s = h->stream;
   const StepConst& sc = h->sc;
-  EXM_CUDA(launch_cloud_prep(h->d_pts, h->d_mask, h->d_dyn, h->fp.radius, h->grid, s));
+  EXM_CUDA(launch_cloud_prep(h->d_pts, h->d_mask, h->d_dyn, h->fp.radius, h->grid, h->n_cap, s));
   EXM_CUDA(launch_rollout(sc, h->d_dyn, h->d_nominal, h->d_eps, 0, h->d_poses, h->d_xy, h->d_base,
                           h->d_ctrl, controls_out ? h->d_controls : nullptr,
                           states_out ? h->d_states : nullptr, s));
@@ -1158,7 +1158,7 @@ exm_status exm_validate_nominal(exm_handle* h, const double* nominal, const doub
   if (st != EXM_OK) return st;
   cudaStream_t s = h->stream;
   const StepConst& sc = h->sc;
-  EXM_CUDA(launch_cloud_prep(h->d_pts, h->d_mask, h->d_dyn, h->fp.radius, h->grid, s));
+  EXM_CUDA(launch_cloud_prep(h->d_pts, h->d_mask, h->d_dyn, h->fp.radius, h->grid, h->n_cap, s));
   EXM_CUDA(launch_update(sc, nullptr, h->d_nominal, h->d_dyn, h->d_upd, h->d_val_poses,
                          h->d_val_xy, h->d_val_base, out_dec(h), 0, s));
   EXM_CUDA(launch_sdf_grid(h->fp, h->d_val_poses, sc.T, h->grid,

@@ -169,7 +169,7 @@ cudaError_t launch_noise(const StepConst& sc, const StepDyn* dyn, double* eps, c
 // The next cycle's device noise (cycle sc.nstate[0] + 1) into eps, marked in sc.nstate[1]
 cudaError_t launch_noise_pregen(const StepConst& sc, double* eps, cudaStream_t s);
 cudaError_t launch_cloud_prep(const double* pts, const uint8_t* mask, const StepDyn* dyn,
-                              float radius, const CloudGrid& g, cudaStream_t s);
+                              float radius, const CloudGrid& g, int n_cap, cudaStream_t s);
 // draw != 0: the rollout kernel draws the device noise into eps; else eps is read (injected).
 // base_cost: terminal goal cost per rollout; ctrl_cost: control cost per (r, h).
 cudaError_t launch_rollout(const StepConst& sc, const StepDyn* dyn, const double* nominal,
