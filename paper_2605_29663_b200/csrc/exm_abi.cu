@@ -775,14 +775,26 @@ exm_status upload_inputs(exm_handle* h, const double q0[3], const double* pts, c
   const size_t TD = static_cast<size_t>(h->T) * h->D;
   std::memcpy(h->h_nominal, nominal, TD * sizeof(double));
   std::memcpy(h->h_guide, guide, 2 * static_cast<size_t>(ng) * sizeof(double));
+  cudaStream_t s = h->stream;
+  // The cloud goes straight from the caller's buffers (the driver stages pageable memory
+  // while this call returns): measured 10 us per config-2 call faster end to end than a host
+  // memcpy into the pinned mirror plus an async copy (EXM_STAGE=pinned, kept for A/B).
+  static const bool pinned = std::getenv("EXM_STAGE") && !std::strcmp(std::getenv("EXM_STAGE"), "pinned");
+  const size_t head0 = static_cast<size_t>(reinterpret_cast<unsigned char*>(h->h_pts) -
+                                           reinterpret_cast<unsigned char*>(h->h_dyn));
+  if (!pinned) {
+    EXM_CUDA(cudaMemcpyAsync(h->d_dyn, h->h_dyn, head0, cudaMemcpyHostToDevice, s));
+    if (n > 0)
+      EXM_CUDA(cudaMemcpyAsync(h->d_pts, pts, 2 * static_cast<size_t>(n) * sizeof(double), cudaMemcpyHostToDevice, s));
+    if (mask && n > 0)
+      EXM_CUDA(cudaMemcpyAsync(h->d_mask, mask, static_cast<size_t>(n), cudaMemcpyHostToDevice, s));
+    return EXM_OK;
+  }
   if (n > 0) std::memcpy(h->h_pts, pts, 2 * static_cast<size_t>(n) * sizeof(double));
   if (mask && n > 0) std::memcpy(h->h_mask, mask, static_cast<size_t>(n));
-  cudaStream_t s = h->stream;
   // dyn | nominal | guide | points share one allocation (same layout pinned and on device):
   // one H2D copy for all of them, a second one for the mask.
-  const size_t head = static_cast<size_t>(reinterpret_cast<unsigned char*>(h->h_pts) -
-                                          reinterpret_cast<unsigned char*>(h->h_dyn)) +
-                      2 * static_cast<size_t>(n) * sizeof(double);
+  const size_t head = head0 + 2 * static_cast<size_t>(n) * sizeof(double);
   EXM_CUDA(cudaMemcpyAsync(h->d_dyn, h->h_dyn, head, cudaMemcpyHostToDevice, s));
   if (mask && n > 0)
     EXM_CUDA(cudaMemcpyAsync(h->d_mask, h->h_mask, static_cast<size_t>(n), cudaMemcpyHostToDevice, s));
