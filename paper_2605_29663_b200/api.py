@@ -361,6 +361,7 @@ class Engine:
         self._cc = _abi.fast_control_cycle(self.lib)
         self._hv = C.cast(h, C.c_void_p).value
         self._q0buf = np.zeros(3)
+        self._q0addr = self._q0buf.ctypes.data
         self._dminbuf = np.zeros(int(params.horizon))
         self._dec = _abi.ExmDecision()
         self._dec.nominal_dmin = dptr(self._dminbuf)
@@ -463,21 +464,30 @@ class Engine:
     def control_cycle_raw(self, q0, obstacles, guidance: Guidance, nominal: np.ndarray,
                           u_prev: np.ndarray, cycle: int, eps=None) -> ControlDecision:
         """One MPPI step with explicit controller state (nominal and u_prev updated in place)."""
-        T = self.params.horizon
-        pts, mask = self._cloud(obstacles)
-        self._q0buf[:] = q0
+        if isinstance(obstacles, ObstacleSet) and obstacles.points.shape[0] <= self.n_cap:
+            pts, mask = obstacles.points, obstacles.mask  # validated at ObstacleSet creation
+        else:
+            pts, mask = self._cloud(obstacles)
+        q = self._q0buf
+        q[0], q[1], q[2] = q0[0], q0[1], q0[2]
         eps_arr = None
         if eps is not None:
             eps_arr = np.ascontiguousarray(np.asarray(eps, np.float64))
         A = self._addr
-        check(self._cc(self._hv, A(self._q0buf), A(pts), A(mask, np.uint8), pts.shape[0],
-                       A(guidance.path), guidance.path.shape[0], A(guidance.goal), A(nominal),
-                       A(u_prev), int(cycle), A(eps_arr), self._decp))
+        rc = self._cc(self._hv, self._q0addr, A(pts), A(mask, np.uint8), pts.shape[0],
+                      A(guidance.path), guidance.path.shape[0], A(guidance.goal), A(nominal),
+                      A(u_prev), int(cycle), A(eps_arr), self._decp)
+        if rc:
+            check(rc)
         dec = self._dec
-        return ControlDecision(np.array(dec.command[: self.dim]), bool(dec.validated),
-                               nominal.reshape(T, self.dim).copy(), dec.best_cost,
-                               dec.weight_entropy, dec.nominal_cost, self._dminbuf.copy(),
-                               dec.argmin)
+        D = self.dim
+        cmd = np.empty(D)
+        c = dec.command
+        for i in range(D):
+            cmd[i] = c[i]
+        return ControlDecision(cmd, bool(dec.validated), nominal.reshape(-1, D).copy(),
+                               dec.best_cost, dec.weight_entropy, dec.nominal_cost,
+                               self._dminbuf.copy(), dec.argmin)
 
     def batch_signed_distance(self, queries) -> np.ndarray:
         q = np.ascontiguousarray(np.asarray(queries, np.float64).reshape(-1, 2))
