@@ -16,7 +16,8 @@ constexpr int kBlockRollouts = 256;  // rollouts per softmax partial (fixed: G-i
 constexpr int kGridMax = 128;        // cloud grid cells per axis (<= 16384 cells, smem histogram)
 constexpr float kEmptyDistance = 1e6f;  // kEmptyMaskDistance (geometry.hpp:37)
 constexpr float kCullMargin = 1e-4f;    // base slack on every lower-bound cull (m)
-constexpr int kChunk = 8;               // cloud points per chunk (one bounding box each)
+// cloud points per chunk (one bounding box each): 8 or 16, chosen per handle (GridMeta::chunk)
+constexpr int kChunkMax = 16;
 constexpr int kSubCells = 16;           // per-axis sub-cells of the in-cell Morton order
 
 // FP32 footprint table, passed by value as a __grid_constant__ kernel parameter so the
@@ -54,12 +55,15 @@ struct GridMeta {
   float x0, y0, cs, inv_cs;
   int gx, gy, n_valid;
   float margin;  // cull slack (m): kCullMargin + rounding allowance for the cloud's extent
+  int chunk;     // points per chunk (8 or 16)
+  int reserved;
 };
 
 // Device cloud structure of one control step (HBM, rebuilt every cycle by launch_cloud_prep):
 //   cloud[cell_start[c] .. cell_start[c+1])  cell c's points, Morton-ordered on a kSubCells^2
-//       sub-grid, padded with NaN to a multiple of kChunk (NaN never passes a distance test)
-//   chunk[i]  bounding box {cx, cy, hx, hy} of cloud[kChunk*i .. kChunk*i + kChunk)
+//       sub-grid, padded with NaN to a multiple of the chunk size C = GridMeta::chunk (NaN never
+//       passes a distance test)
+//   chunk[i]  bounding box {cx, cy, hx, hy} of cloud[C*i .. C*i + C)
 // tmp / raw / raw_start are the prep kernels' scratch (compacted points, cell-sorted points).
 struct CloudGrid {
   float2* tmp = nullptr;
@@ -75,9 +79,9 @@ struct CloudGrid {
   // {next pose, finished warps} of the persistent k_sdf_grid (zero between launches)
   unsigned* work = nullptr;
 };
-// Padded cloud capacity for n_cap points: every nonempty cell adds at most kChunk - 1 pads.
+// Padded cloud capacity for n_cap points: every nonempty cell adds at most kChunkMax - 1 pads.
 inline size_t cloud_capacity(int n_cap) {
-  return static_cast<size_t>(n_cap) + static_cast<size_t>(kChunk - 1) * kGridMax * kGridMax + kChunk;
+  return static_cast<size_t>(n_cap) + static_cast<size_t>(kChunkMax - 1) * kGridMax * kGridMax + kChunkMax;
 }
 
 // Sensing (exm_world.cu): boundary-sample segments in the reference's sampling order and the
@@ -168,8 +172,11 @@ cudaError_t launch_k(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t sme
 cudaError_t launch_noise(const StepConst& sc, const StepDyn* dyn, double* eps, cudaStream_t s);
 // The next cycle's device noise (cycle sc.nstate[0] + 1) into eps, marked in sc.nstate[1]
 cudaError_t launch_noise_pregen(const StepConst& sc, double* eps, cudaStream_t s);
+// chunk: points per cull chunk (8 for small clouds; 16 for clouds of >= 16k points, whose long
+// walls make a chunk test per 8 points the larger cost)
 cudaError_t launch_cloud_prep(const double* pts, const uint8_t* mask, const StepDyn* dyn,
                               float radius, const CloudGrid& g, int n_cap, cudaStream_t s);
+int chunk_for_capacity(int n_cap);
 // draw != 0: the rollout kernel draws the device noise into eps; else eps is read (injected).
 // base_cost: terminal goal cost per rollout; ctrl_cost: control cost per (r, h).
 cudaError_t launch_rollout(const StepConst& sc, const StepDyn* dyn, const double* nominal,

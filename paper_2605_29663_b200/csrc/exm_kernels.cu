@@ -350,9 +350,11 @@ constexpr int kCtaPerPoseMax = 1024;  // ... and below this, a CTA of 8 warps pe
 __device__ __forceinline__ GridMeta make_gridmeta(float mnx, float mxx, float mny, float mxy,
                                                   int cnt, float cs_lo, float cs_hi,
                                                   float pts_per_cell, float radius, float ds0,
-                                                  float ds1) {
+                                                  float ds1, int chunk) {
   GridMeta g;
   g.n_valid = cnt;
+  g.chunk = chunk;
+  g.reserved = 0;
   g.margin = kCullMargin;
   if (cnt == 0) {
     g.x0 = g.y0 = 0.0f; g.cs = 1.0f; g.inv_cs = 1.0f; g.gx = g.gy = 1;
@@ -383,7 +385,7 @@ __global__ void __launch_bounds__(1024) k_cloud_prep(const double* __restrict__ 
                                                      const uint8_t* __restrict__ mask,
                                                      const StepDyn* __restrict__ dyn,
                                                      float cs_lo, float cs_hi, float pts_per_cell,
-                                                     float radius, float* __restrict__ dstat,
+                                                     float radius, int chunk, float* __restrict__ dstat,
                                                      float2* __restrict__ tmp,
                                                      float2* __restrict__ raw,
                                                      int* __restrict__ raw_start,
@@ -455,7 +457,7 @@ __global__ void __launch_bounds__(1024) k_cloud_prep(const double* __restrict__ 
   }
   if (tid == 0) {
     const GridMeta g = make_gridmeta(mnx, mxx, mny, mxy, cnt, cs_lo, cs_hi, pts_per_cell, radius,
-                                     dstat[0], dstat[1]);
+                                     dstat[0], dstat[1], chunk);
     gm = g;
     *gm_out = g;
     dstat[0] = 0.f;  // consumed: the stage costs of this step accumulate the next statistic
@@ -489,8 +491,8 @@ __global__ void __launch_bounds__(1024) k_cloud_prep(const double* __restrict__ 
   // (cell_start), as one 64-bit scan {padded:raw}; each thread owns a contiguous segment.
   const int seg = (cells + blockDim.x - 1) / blockDim.x;
   const int c0 = min(cells, tid * seg), c1 = min(cells, c0 + seg);
-  auto both = [](int h) {
-    return (static_cast<long long>((h + kChunk - 1) & ~(kChunk - 1)) << 32) | static_cast<long long>(h);
+  auto both = [chunk](int h) {
+    return (static_cast<long long>((h + chunk - 1) & ~(chunk - 1)) << 32) | static_cast<long long>(h);
   };
   long long local = 0;
   for (int c = c0; c < c1; ++c) local += both(hist[c]);
@@ -552,7 +554,7 @@ __device__ __forceinline__ int sub_key(float2 p, float ox, float oy, float sub) 
 }
 
 // One nonempty cell, one warp: counting sort of the cell's points by their sub-grid Morton index
-// (so every kChunk consecutive points are close together), NaN pads up to a whole chunk, and the
+// (so every chunk of consecutive points is compact), NaN pads up to a whole chunk, and the
 // chunk bounding boxes. hist: kSubCells^2 ints of this warp's shared memory.
 __device__ __forceinline__ void sort_cell(int c, int lane, int* hist, const float2* __restrict__ raw,
                                           const int* __restrict__ raw_start,
@@ -590,27 +592,28 @@ __device__ __forceinline__ void sort_cell(int c, int lane, int* hist, const floa
     const float2 p = raw[rs + i];
     cloud[ps + atomicAdd(&hist[sub_key(p, ox, oy, sub)], 1)] = p;
   }
-  const int np = (n + kChunk - 1) & ~(kChunk - 1);
+  const int C = gm.chunk;
+  const int np = (n + C - 1) & ~(C - 1);
   if (n + lane < np) cloud[ps + n + lane] = pad;
   __syncwarp();  // orders the warp's global stores before the L2 reads below
-  for (int j = lane; j < np / kChunk; j += 32) {
+  for (int j = lane; j < np / C; j += 32) {
     float x0 = FLT_MAX, x1 = -FLT_MAX, y0 = FLT_MAX, y1 = -FLT_MAX;
-#pragma unroll
-    for (int k = 0; k < kChunk; ++k) {
-      const float2 p = __ldcg(cloud + ps + j * kChunk + k);
+#pragma unroll 8
+    for (int k = 0; k < C; ++k) {
+      const float2 p = __ldcg(cloud + ps + j * C + k);
       if (p.x == p.x) {
         x0 = fminf(x0, p.x); x1 = fmaxf(x1, p.x);
         y0 = fminf(y0, p.y); y1 = fmaxf(y1, p.y);
       }
     }
-    chunk[ps / kChunk + j] =
+    chunk[ps / C + j] =
         make_float4(0.5f * (x0 + x1), 0.5f * (y0 + y1), 0.5f * (x1 - x0), 0.5f * (y1 - y0));
   }
   __syncwarp();
 }
 
 // Second prep pass, one warp per nonempty cell: counting sort of the cell's points by their
-// sub-grid Morton index (so every kChunk consecutive points are close together), NaN pads up
+// sub-grid Morton index (so every chunk of consecutive points is compact), NaN pads up
 // to a whole chunk, and the chunk bounding boxes.
 constexpr int kSortWarps = 8;
 __global__ void __launch_bounds__(kSortWarps * 32) k_cell_sort(
@@ -768,17 +771,18 @@ __device__ __forceinline__ void sdf_grid_warp(const FpDev& fp, const float4* __r
                                    box_may_beat(w, bx0, bx1, by0, by1, best, mg)));
       if (!__any_sync(kFull, need)) continue;
       float l2 = lim * lim;
-      // chunks of kChunk Morton-ordered points: one body-frame box bound per chunk, then the
+      // chunks of gm.chunk Morton-ordered points: one body-frame box bound per chunk, then the
       // per-point bounds and the exact SDF for the points of the chunks some lane still needs
-      for (int ch = s / kChunk; ch < e / kChunk; ++ch) {
+      const int csh = gm.chunk == 16 ? 4 : 3;
+      for (int ch = s >> csh; ch < e >> csh; ++ch) {
         bool cneed = need;
         if (MODE == kGridFull) {
           cneed = need && chunk_may_beat(fp, q, __ldg(chunk + ch), best, mg);
           if (!__any_sync(kFull, cneed)) continue;
         }
-        const float2* cp = cloud + ch * kChunk;
+        const float2* cp = cloud + (ch << csh);
 #pragma unroll 1
-        for (int p = 0; p < kChunk; ++p) {
+        for (int p = 0; p < gm.chunk; ++p) {
           const float2 o = __ldg(cp + p);
           const float dx = o.x - q.x, dy = o.y - q.y;
           if (STATS && cneed) ++n_test;
@@ -1361,12 +1365,20 @@ struct PairsLaunch {
 }  // namespace
 
 // ------------------------------------------------------------------ launchers
+// Chunk size per handle (EXM_CHUNK=8/16 overrides): 16-point chunks measured 10 % faster on the
+// 20k / 50k-point aisle and moving-disc clouds (configs 3, 5), 6 % slower on config 2's 10k
+// clutter points.
+int chunk_for_capacity(int n_cap) {
+  static const int forced = getenv("EXM_CHUNK") ? atoi(getenv("EXM_CHUNK")) : 0;
+  if (forced == 8 || forced == 16) return forced;
+  return n_cap >= 16384 ? 16 : 8;
+}
+
 cudaError_t launch_cloud_prep(const double* pts, const uint8_t* mask, const StepDyn* dyn,
                               float radius, const CloudGrid& g, int n_cap, cudaStream_t s) {
   // (A one-cluster version — 8 CTAs meeting through distributed shared memory, cell sort fused —
   // measured 20.9 us against 13.6 + 5.9 us for config 2: the cluster barriers cost what the
   // parallel load saves at 10k points. The single CTA stays.)
-  (void)n_cap;
   const int smem = kGridMax * kGridMax * static_cast<int>(sizeof(int));
   static bool attr_set = false;
   if (!attr_set) {
@@ -1377,7 +1389,7 @@ cudaError_t launch_cloud_prep(const double* pts, const uint8_t* mask, const Step
   // Cells sized for about kPtsPerCell points, between R/4 and kCellMaxR * R: a cull disc of
   // radius R + d covers ~(2(R+d)/cs)^2 cells; the chunk bounds cull inside a cell.
   const float r = fmaxf(radius, 0.04f);
-  { if (const cudaError_t le = launch_k(k_cloud_prep, 1, 1024, smem, s, pts, mask, dyn, 0.25f * r, kCellMaxR * r, kPtsPerCell, r, g.dstat, g.tmp,
+  { if (const cudaError_t le = launch_k(k_cloud_prep, 1, 1024, smem, s, pts, mask, dyn, 0.25f * r, kCellMaxR * r, kPtsPerCell, r, chunk_for_capacity(n_cap), g.dstat, g.tmp,
                                      g.raw, g.raw_start, g.cell_start, g.gm); le != cudaSuccess) return le; }
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
