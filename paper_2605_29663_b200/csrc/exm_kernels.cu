@@ -1389,7 +1389,11 @@ cudaError_t launch_cloud_prep(const double* pts, const uint8_t* mask, const Step
   // Cells sized for about kPtsPerCell points, between R/4 and kCellMaxR * R: a cull disc of
   // radius R + d covers ~(2(R+d)/cs)^2 cells; the chunk bounds cull inside a cell.
   const float r = fmaxf(radius, 0.04f);
-  { if (const cudaError_t le = launch_k(k_cloud_prep, 1, 1024, smem, s, pts, mask, dyn, 0.25f * r, kCellMaxR * r, kPtsPerCell, r, chunk_for_capacity(n_cap), g.dstat, g.tmp,
+  // (EXM_PTS_PER_CELL / EXM_CELL_MINR / EXM_CELL_MAXR: tuning overrides for A/B runs)
+  static const float ppc = getenv("EXM_PTS_PER_CELL") ? static_cast<float>(atof(getenv("EXM_PTS_PER_CELL"))) : kPtsPerCell;
+  static const float cmin = getenv("EXM_CELL_MINR") ? static_cast<float>(atof(getenv("EXM_CELL_MINR"))) : 0.25f;
+  static const float cmax = getenv("EXM_CELL_MAXR") ? static_cast<float>(atof(getenv("EXM_CELL_MAXR"))) : kCellMaxR;
+  { if (const cudaError_t le = launch_k(k_cloud_prep, 1, 1024, smem, s, pts, mask, dyn, cmin * r, cmax * r, ppc, r, chunk_for_capacity(n_cap), g.dstat, g.tmp,
                                      g.raw, g.raw_start, g.cell_start, g.gm); le != cudaSuccess) return le; }
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
