@@ -343,7 +343,9 @@ constexpr float kCellMaxR = 0.5f;        // cell edge <= kCellMaxR * R ...
 constexpr float kCellSearchFrac = 0.385f;  // ... or <= this fraction of R + mean d_min
 // Below this many poses one thread per pose leaves most SMs idle (< ~16 warps each): use one
 // warp per pose instead.
-constexpr int kWarpPerPoseMax = 65536;
+// (measured on config 2's cloud: 25.6k poses warp 45 us / thread 64 us, 51.2k poses warp 76 us
+// / thread 65 us; config 1's 30.7k poses warp 68 us / thread 114 us)
+constexpr int kWarpPerPoseMax = 40000;
 constexpr int kCtaPerPoseMax = 1024;  // ... and below this, a CTA of 8 warps per pose
 // Grid of the recentred valid cloud: bounding box, cell edge from the point density and the
 // previous step's search radius, cull margin (shared by both preparation kernels).
