@@ -310,7 +310,8 @@ def run_ours(args, world, rank, local):
                    "model": ["diff", "ackermann", "omni", "spin", "parallel"][wl.model.tag],
                    "parallelism": f"rollout-sharded x{world}",
                    "l2": "flushed (256 MiB write) before every timed step"},
-        "sdf_evals_per_s": K * T * N / (ms * 1e-3),
+        "sdf_evals_per_s": K * T * N / (ms * 1e-3),  # point-pose pairs per second of MPPI step
+        "sdf_kernel_evals_per_s": pairs * world / (sdf_avg_ms * 1e-3),  # ... of the SDF kernel
         "e2e": {"value": 1.0 / e2e_s, "unit": "steps/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "ms_p50": float(np.percentile(e2e_ms, 50)),
                 "ms_p99": float(np.percentile(e2e_ms, 99)),
