@@ -741,16 +741,6 @@ __global__ void __launch_bounds__(256) k_update(const StepConst sc,
     double* sS = sb + nb;      // S_b
     double* sA = sS + nb;      // A_b
     double* sg = sA + nb;      // argmin_b
-    // every global load of the merge is issued up front: the headers, and (nb <= kPreBlocks)
-    // this thread's U column of every block, so one memory latency covers the whole merge
-    constexpr int kPreBlocks = 32;
-    const bool pre = nb <= kPreBlocks && TD <= static_cast<int>(blockDim.x);
-    double ucol[kPreBlocks];
-    if (pre) {
-#pragma unroll
-      for (int b = 0; b < kPreBlocks; ++b)
-        ucol[b] = (b < nb && tid < TD) ? partials[static_cast<size_t>(b) * stride + 4 + tid] : 0.0;
-    }
     for (int b = tid; b < nb; b += blockDim.x) {
       const double* p = partials + static_cast<size_t>(b) * stride;
       sb[b] = p[0];
@@ -783,32 +773,20 @@ __global__ void __launch_bounds__(256) k_update(const StepConst sc,
       sf[b] = exp(-z);
     }
     __syncthreads();
-    if (tid < 32) {  // S, A: lane-strided partial sums in block order, then a fixed xor tree
+    if (tid == 0) {  // block order: deterministic, independent of the GPU count
       double S = 0.0, A = 0.0;
-      for (int b = lane; b < nb; b += 32) {
+      for (int b = 0; b < nb; ++b) {
         S += sf[b] * sS[b];
         A += sf[b] * (sA[b] + sS[b] * sb[b]);
       }
-      for (int o = 16; o; o >>= 1) {
-        S += __shfl_xor_sync(kFull, S, o);
-        A += __shfl_xor_sync(kFull, A, o);
-      }
-      if (tid == 0) {
-        s_S = S;
-        dec->entropy = A / S + log(S);
-      }
+      s_S = S;
+      dec->entropy = A / S + log(S);
     }
-    // U_o = sum_b f_b U_b[o] needs only the factors: overlaps the S / A sums
+    // U_o = sum_b f_b U_b[o] needs only the factors: overlaps thread 0's S / A sums
     double U[4] = {0.0, 0.0, 0.0, 0.0};
-    if (pre) {
-#pragma unroll
-      for (int b = 0; b < kPreBlocks; ++b)
-        if (b < nb) U[0] += sf[b] * ucol[b];
-    } else {
-      for (int k = 0, o = tid; k < 4 && o < TD; ++k, o += blockDim.x) {
+    for (int k = 0, o = tid; k < 4 && o < TD; ++k, o += blockDim.x) {
 #pragma unroll 16
-        for (int b = 0; b < nb; ++b) U[k] += sf[b] * partials[static_cast<size_t>(b) * stride + 4 + o];
-      }
+      for (int b = 0; b < nb; ++b) U[k] += sf[b] * partials[static_cast<size_t>(b) * stride + 4 + o];
     }
     __syncthreads();
     EXM_PROBE(2);
