@@ -13,7 +13,7 @@ namespace exm {
 constexpr int kMaxEdges = 64;        // polygon edges / cover boxes held in kernel parameters
 constexpr int kMaxCover = 3;         // boxes of the polygon cull cover
 constexpr int kBlockRollouts = 256;  // rollouts per softmax partial (fixed: G-invariant)
-constexpr int kGridMax = 128;        // cloud grid cells per axis (<= 16384 cells, smem histogram)
+constexpr int kGridMax = 181;        // cloud grid cells per axis (<= 32761 cells, 131 KB smem histogram)
 constexpr float kEmptyDistance = 1e6f;  // kEmptyMaskDistance (geometry.hpp:37)
 constexpr float kCullMargin = 1e-4f;    // base slack on every lower-bound cull (m)
 // cloud points per chunk (one bounding box each): 8 or 16, chosen per handle (GridMeta::chunk)

@@ -337,8 +337,10 @@ __device__ __forceinline__ float unkey(unsigned k) {
 }
 
 // ------------------------------------------------------------------ kernels
-constexpr float kPtsPerCell = 32.0f;
+constexpr float kPtsPerCell = 16.0f;  // swept 8-64 (tools/cfg5_snapshots.py): cfg2/cfg3 flat over 16-32, cfg5 snapshots -3 % at 16
 constexpr int kPrepCache = 12;  // cloud points per k_cloud_prep thread kept in registers
+constexpr float kCellMinR = 0.18f;       // cell edge >= kCellMinR * R (swept 0.12-0.25: cfg3 1.99 -> 1.88 ms,
+                                          // cfg5 snapshots -1 %, cfg1/cfg2 flat; cfg3 is alignment-sensitive)
 constexpr float kCellMaxR = 0.5f;        // cell edge <= kCellMaxR * R ...
 constexpr float kCellSearchFrac = 0.385f;  // ... or <= this fraction of R + mean d_min
 // Below this many poses one thread per pose leaves most SMs idle (< ~16 warps each): use one
@@ -1393,7 +1395,7 @@ cudaError_t launch_cloud_prep(const double* pts, const uint8_t* mask, const Step
   const float r = fmaxf(radius, 0.04f);
   // (EXM_PTS_PER_CELL / EXM_CELL_MINR / EXM_CELL_MAXR: tuning overrides for A/B runs)
   static const float ppc = getenv("EXM_PTS_PER_CELL") ? static_cast<float>(atof(getenv("EXM_PTS_PER_CELL"))) : kPtsPerCell;
-  static const float cmin = getenv("EXM_CELL_MINR") ? static_cast<float>(atof(getenv("EXM_CELL_MINR"))) : 0.25f;
+  static const float cmin = getenv("EXM_CELL_MINR") ? static_cast<float>(atof(getenv("EXM_CELL_MINR"))) : kCellMinR;
   static const float cmax = getenv("EXM_CELL_MAXR") ? static_cast<float>(atof(getenv("EXM_CELL_MAXR"))) : kCellMaxR;
   { if (const cudaError_t le = launch_k(k_cloud_prep, 1, 1024, smem, s, pts, mask, dyn, cmin * r, cmax * r, ppc, r, chunk_for_capacity(n_cap), g.dstat, g.tmp,
                                      g.raw, g.raw_start, g.cell_start, g.gm); le != cudaSuccess) return le; }
