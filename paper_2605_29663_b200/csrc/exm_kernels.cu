@@ -354,7 +354,7 @@ constexpr int kCtaPerPoseMax = 1024;  // ... and below this, a CTA of 8 warps pe
 __device__ __forceinline__ GridMeta make_gridmeta(float mnx, float mxx, float mny, float mxy,
                                                   int cnt, float cs_lo, float cs_hi,
                                                   float pts_per_cell, float radius, float ds0,
-                                                  float ds1, int chunk) {
+                                                  float ds1, int chunk, float search_lo) {
   GridMeta g;
   g.n_valid = cnt;
   g.chunk = chunk;
@@ -375,6 +375,9 @@ __device__ __forceinline__ GridMeta make_gridmeta(float mnx, float mxx, float mn
   float hi = cs_hi;
   if (ds1 > 0.f) hi = fmaxf(cs_hi, kCellSearchFrac * (radius + ds0 / ds1));
   float cs = fminf(fmaxf(dens, cs_lo), hi);
+  // far obstacles (large mean d_min): the search covers more rings; search_lo > 0 floors the
+  // cell edge at that fraction of the expected search radius
+  if (ds1 > 0.f && search_lo > 0.f) cs = fmaxf(cs, search_lo * (radius + ds0 / ds1));
   cs = fmaxf(cs, fmaxf(ex, ey) / static_cast<float>(kGridMax - 1) * 1.001f);
   cs = fmaxf(cs, 1e-4f);
   g.x0 = mnx; g.y0 = mny; g.cs = cs; g.inv_cs = 1.0f / cs;
@@ -389,7 +392,8 @@ __global__ void __launch_bounds__(1024) k_cloud_prep(const double* __restrict__ 
                                                      const uint8_t* __restrict__ mask,
                                                      const StepDyn* __restrict__ dyn,
                                                      float cs_lo, float cs_hi, float pts_per_cell,
-                                                     float radius, int chunk, float* __restrict__ dstat,
+                                                     float radius, int chunk, float search_lo,
+                                                     float* __restrict__ dstat,
                                                      float2* __restrict__ tmp,
                                                      float2* __restrict__ raw,
                                                      int* __restrict__ raw_start,
@@ -461,7 +465,7 @@ __global__ void __launch_bounds__(1024) k_cloud_prep(const double* __restrict__ 
   }
   if (tid == 0) {
     const GridMeta g = make_gridmeta(mnx, mxx, mny, mxy, cnt, cs_lo, cs_hi, pts_per_cell, radius,
-                                     dstat[0], dstat[1], chunk);
+                                     dstat[0], dstat[1], chunk, search_lo);
     gm = g;
     *gm_out = g;
     dstat[0] = 0.f;  // consumed: the stage costs of this step accumulate the next statistic
@@ -1396,8 +1400,9 @@ cudaError_t launch_cloud_prep(const double* pts, const uint8_t* mask, const Step
   // (EXM_PTS_PER_CELL / EXM_CELL_MINR / EXM_CELL_MAXR: tuning overrides for A/B runs)
   static const float ppc = getenv("EXM_PTS_PER_CELL") ? static_cast<float>(atof(getenv("EXM_PTS_PER_CELL"))) : kPtsPerCell;
   static const float cmin = getenv("EXM_CELL_MINR") ? static_cast<float>(atof(getenv("EXM_CELL_MINR"))) : kCellMinR;
+  static const float slo = getenv("EXM_CELL_SEARCH_LO") ? static_cast<float>(atof(getenv("EXM_CELL_SEARCH_LO"))) : 0.0f;
   static const float cmax = getenv("EXM_CELL_MAXR") ? static_cast<float>(atof(getenv("EXM_CELL_MAXR"))) : kCellMaxR;
-  { if (const cudaError_t le = launch_k(k_cloud_prep, 1, 1024, smem, s, pts, mask, dyn, cmin * r, cmax * r, ppc, r, chunk_for_capacity(n_cap), g.dstat, g.tmp,
+  { if (const cudaError_t le = launch_k(k_cloud_prep, 1, 1024, smem, s, pts, mask, dyn, cmin * r, cmax * r, ppc, r, chunk_for_capacity(n_cap), slo, g.dstat, g.tmp,
                                      g.raw, g.raw_start, g.cell_start, g.gm); le != cudaSuccess) return le; }
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
