@@ -23,7 +23,17 @@ def _nonagon() -> FootprintSpec:
     return FootprintSpec.polygon(np.stack([r * np.cos(a), r * np.sin(a)], 1), "nonagon")
 
 
+def _wide_scene():
+    """Config 2's clutter plus 2,000 points on a ring 90 m out: a 180 m extent, so the grid's
+    per-axis cell cap (kGridMax) binds and the cells are far coarser than the density asks."""
+    wl = W.cfg2(K=2048, T=40, N=10_000)
+    a = 2 * math.pi * np.arange(2000) / 2000
+    ring = wl.q0[:2] + 90.0 * np.stack([np.cos(a), np.sin(a)], 1)
+    return dataclasses.replace(wl, cloud=np.concatenate([wl.cloud, ring]))
+
+
 CASES = {
+    "cfg2_wide_capped_grid": _wide_scene,
     "cfg2_star64": lambda: dataclasses.replace(W.cfg2(K=2048, T=40, N=10_000),
                                                footprint=W.star64_footprint()),
     "cfg2_nonagon": lambda: dataclasses.replace(W.cfg2(K=2048, T=40, N=10_000),
