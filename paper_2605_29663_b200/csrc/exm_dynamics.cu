@@ -50,19 +50,30 @@ __device__ double task_cost(const StepConst& sc, const double q[3], const double
     const double ax = q[0] - g[0], ay = q[1] - g[1];
     best_d = sqrt(ax * ax + ay * ay);
   } else {
+    // Same values as the reference loop with fewer FP64 sqrt/div sequences: the quotient is
+    // formed only when it is not clamped (num <= 0 -> t = 0, num >= len^2 -> t = 1 exactly, the
+    // division being monotonic), and sqrt(e.e) only when e.e is below the best so far (sqrt is
+    // monotonic, so e.e >= best_a implies d >= best_d and the reference keeps its best).
     best_d = HUGE_VAL;
-    double arc = 0.0;
+    double best_a = HUGE_VAL, arc = 0.0;
     for (int i = 0; i + 1 < ng; ++i) {
       const double ax = g[2 * i], ay = g[2 * i + 1];
       const double sx = g[2 * i + 2] - ax, sy = g[2 * i + 3] - ay;
       const double len = sqrt(sx * sx + sy * sy);
       double t = 0.0;
-      if (len > 0.0) t = clampd(((q[0] - ax) * sx + (q[1] - ay) * sy) / (len * len), 0.0, 1.0);
+      if (len > 0.0) {
+        const double num = (q[0] - ax) * sx + (q[1] - ay) * sy, den = len * len;
+        t = num <= 0.0 ? 0.0 : num >= den ? 1.0 : clampd(num / den, 0.0, 1.0);
+      }
       const double ex = q[0] - (ax + t * sx), ey = q[1] - (ay + t * sy);
-      const double d = sqrt(ex * ex + ey * ey);
-      if (d < best_d) {
-        best_d = d;
-        best_p = arc + t * len;
+      const double a = ex * ex + ey * ey;
+      if (a < best_a) {
+        const double d = sqrt(a);
+        if (d < best_d) {
+          best_d = d;
+          best_a = a;
+          best_p = arc + t * len;
+        }
       }
       arc += len;
     }
