@@ -280,3 +280,39 @@ def test_pregenerated_noise_is_the_drawn_noise():
         assert np.array_equal(nom, nom_r), cyc
         assert d.argmin == r.argmin and d.best_cost == r.best_cost, cyc
         assert d.weight_entropy == r.weight_entropy, cyc
+
+
+def _guidance_cases(q0, goal):
+    x, y = float(q0[0]), float(q0[1])
+    a, b = [x - 1.0, y + 0.3], [x + 4.0, y + 0.3]
+    return {
+        # segment 2 repeats segment 0 exactly: equal distances, the first segment's progress wins
+        "repeated_segment": [a, b, a, b],
+        "zero_length_segments": [a, a, [x + 1.0, y], [x + 1.0, y], b],
+        "vertex_at_start_pose": [[x - 2.0, y], [x, y], [x + 2.0, y + 2.0]],
+        "single_point": [[x + 3.0, y - 1.0]],
+        "doubled_back": [a, b, a],
+    }
+
+
+@pytest.mark.parametrize("case", ["repeated_segment", "zero_length_segments",
+                                  "vertex_at_start_pose", "single_point", "doubled_back"])
+def test_task_cost_polyline_edge_cases(case):
+    """Polyline projection (controller.cpp:50-66) in the rollout costs: zero-length segments,
+    exact ties between segments (first segment kept), a single guide point."""
+    wl = W.cfg1(K=256, T=16)
+    path = _guidance_cases(wl.q0, wl.guidance.goal)[case]
+    wl.guidance = Guidance(np.asarray(path, np.float64), wl.guidance.goal)
+    eng, orc = engine_and_oracle(wl)
+    D = wl.model.control_dim()
+    eps = orc.sample_perturbations(3, 0)
+    nom = 0.3 * np.ones(wl.params.horizon * D)
+    up = np.zeros(3)
+    got = eng.evaluate_rollouts(wl.q0, nom, eps, wl.obstacles(), wl.guidance, up)
+    want = orc.evaluate_rollouts(wl.q0, nom, eps, wl.cloud, None, wl.guidance, up)
+    ok = ~degenerate_rows(want["d_min"], wl.params.d_safe)
+    rel = np.abs(got.costs - want["costs"]) / np.maximum(np.abs(want["costs"]), 1.0)
+    assert ok.any() and np.max(rel[ok]) <= 1e-5
+    g = eng.validate_nominal(nom, wl.q0, wl.obstacles(), wl.guidance, up)
+    o = orc.validate_nominal(nom, wl.q0, wl.cloud, None, wl.guidance, up)
+    assert g[0] == o[0] and abs(g[2] - o[2]) <= 1e-5 * max(1.0, abs(o[2]))
