@@ -1026,6 +1026,14 @@ cudaError_t launch_rollout_costs(const StepConst& sc, const StepDyn* dyn, const 
     return sizeof(double) * (2 * static_cast<size_t>(guide_cap) + 3 * static_cast<size_t>(w) * sc.T +
                              sc.T);
   };
+  // EXM_COST_WARPS=8|4: rollouts per CTA override for A/B runs
+  static const int want_w = getenv("EXM_COST_WARPS") ? atoi(getenv("EXM_COST_WARPS")) : 16;
+  if (want_w == 8 && smem_for(8) <= 200 * 1024)
+    return rollout_costs_launch<8>(sc, dyn, guide, guide_cap, base_cost, ctrl_cost, xy, dmin, cost,
+                                   unsafe, dstat, hstat, smem_for(8), s);
+  if (want_w == 4 && smem_for(4) <= 200 * 1024)
+    return rollout_costs_launch<4>(sc, dyn, guide, guide_cap, base_cost, ctrl_cost, xy, dmin, cost,
+                                   unsafe, dstat, hstat, smem_for(4), s);
   if (smem_for(16) <= 200 * 1024)
     return rollout_costs_launch<16>(sc, dyn, guide, guide_cap, base_cost, ctrl_cost, xy, dmin, cost,
                                     unsafe, dstat, hstat, smem_for(16), s);
