@@ -12,9 +12,16 @@ scaling) with one NCCL all-gather of the softmax partials per step.
          HBM; L2 is flushed (256 MiB write) before every timed step, outside the events.
   e2e    the same step through the C ABI with host buffers (cloud, state in; decision,
          nominal out), host<->device copies inside the timed region (wall clock).
+  roofline  the SDF kernel (k_sdf_grid) on EXECUTED FP32 work: its work counters
+         (exm_sdf_work_stats) charged at each unit's FP32 op count, divided by the
+         kernel's mean device time in the timed steps and by the measured FP32 peak. The
+         unpruned algorithmic work (K*T*N pairs x F ops) over the executed work is reported as
+         `culling_factor`.
 
 `--impl reference` times the reference's own CPU implementation (MppiController::control_cycle
-of the unmodified reference built into oracle/_ref) on this host's cores.
+of the unmodified reference built into oracle/_ref) on this host's cores at the same config:
+full K, a fresh controller per step, all host threads (plus a threads=1 sample and the
+config-4 batch_signed_distance evals/s of the same build).
 """
 from __future__ import annotations
 
@@ -39,6 +46,45 @@ F_RECT = lambda R: 9 + 16 * R   # noqa: E731
 
 def ops_per_pair(fp) -> int:
     return F_POLY(fp.count()) if fp.is_polygon() else F_RECT(fp.count())
+
+
+def cover_is_exact(fp) -> bool:
+    """The polygon's cull cover tiles it exactly (rectilinear: the L), as exm_create decides."""
+    if not fp.is_polygon():
+        return False
+    _, boxes = fp.cull_boxes()
+    m = 1e-4 * (1.0 + fp.bounding_radius())  # slack added to the cull boxes (exm_abi.cu)
+    area = float(np.sum((2 * (boxes[:, 2] - m)) * (2 * (boxes[:, 3] - m))))
+    x, y = fp.a[:, 0], fp.a[:, 1]
+    poly = 0.5 * abs(float(np.dot(x, np.roll(y, -1)) - np.dot(y, np.roll(x, -1))))
+    return abs(area - poly) <= 1e-4 * poly
+
+
+def executed_ops(counts: dict, fp) -> tuple[float, dict]:
+    """FP32 ops executed by k_sdf_grid: each counted unit (exm_sdf_work_stats) at its op count,
+    FMA = 2, as written in csrc/exm_kernels.cu (DESIGN.md §4 derives each figure):
+      ring step 27 per lane (x32, counted per warp), cell bound 33, chunk bound 63, point circle
+      test 6, body-frame transform 6, exact-cover tile test 44, tile value 7, cover/AABB bound
+      8 (exact cover: interior AABB test) / 41 (polygon cover) / 15 (rect AABB), edge or box
+      loop F - 8 (the reference-literal pair cost without its transform) + 2."""
+    F = ops_per_pair(fp)
+    bound = 8 if cover_is_exact(fp) else (41 if fp.is_polygon() else 15)
+    per = {"ring_steps": 27 * 32, "cell_tests": 33, "chunk_tests": 63, "point_tests": 6,
+           "point_iters_warp": 0, "transforms": 6, "tile_tests": 44, "tile_values": 7,
+           "bound_tests": bound, "edge_loops": F - 8 + 2}
+    parts = {k: counts[k] * per[k] for k in per}
+    return float(sum(parts.values())), per
+
+
+def bench_config(wl, world: int) -> dict:
+    """The config dict both arms print (the driver compares them)."""
+    fp = wl.footprint
+    return {"workload": wl.name, "K": wl.params.rollouts, "T": wl.params.horizon,
+            "N": wl.n_points,
+            "footprint": f"{fp.name} ({'polygon B' if fp.is_polygon() else 'cover R'}={fp.count()})",
+            "model": ["diff", "ackermann", "omni", "spin", "parallel"][wl.model.tag],
+            "parallelism": f"K sharded over {world} GPU(s) (reference arm: host threads)",
+            "l2": "GPU arm: flushed (256 MiB write) before every timed device step"}
 
 
 def fp32_peak_tflops(sm_count: int = 148) -> tuple[float, str]:
@@ -148,19 +194,6 @@ def dist_setup():
     return world, rank, local
 
 
-def pinned_obstacles(o):
-    """The same ObstacleSet with its points / mask copied into page-locked host memory (the numpy
-    views keep the pinned tensors alive)."""
-    import torch
-    pts = torch.empty(o.points.shape, dtype=torch.float64, pin_memory=True)
-    mask = torch.empty(o.mask.shape, dtype=torch.uint8, pin_memory=True)
-    pts.numpy()[...] = o.points
-    mask.numpy()[...] = o.mask
-    p = type(o)(pts.numpy(), mask.numpy())
-    assert p.points.ctypes.data == pts.data_ptr() and p.mask.ctypes.data == mask.data_ptr()
-    return p
-
-
 def allreduce_max(x: float, world: int) -> float:
     if world == 1:
         return x
@@ -171,62 +204,124 @@ def allreduce_max(x: float, world: int) -> float:
     return float(t.item())
 
 
-def cpu_reference_sample(wl, seconds: float = 12.0, k_sample: int = 512):
-    """The reference's own control_cycle (oracle/_ref: unmodified sources, all host threads) on
-    a K-subsample of the workload, extrapolated linearly in K (the step is K-parallel)."""
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def reference_steps(wl, threads: int, n_steps: int, warmup: int = 0, min_seconds: float = 0.0,
+                    max_seconds: float = 1e9):
+    """Wall times of MppiController::control_cycle of the unmodified reference (oracle/_ref) at
+    the FULL workload (K, T, N as configured), a fresh controller (zero nominal, cycle 0) per
+    step, built outside the timed call. Falls back to the C restatement when
+    the reference build is absent (kind "port", one thread)."""
     from tests import oracle_bindings as ob
-    import copy
-    p = copy.deepcopy(wl.params)
-    p.rollouts = min(k_sample, wl.params.rollouts)
-    threads = os.cpu_count() or 1
     if ob.reference_available():
-        ref = ob.Reference(wl.footprint, wl.model, wl.limits, p, threads=threads)
+        ref = ob.Reference(wl.footprint, wl.model, wl.limits, wl.params, threads=threads)
         ref.set_cloud(wl.cloud)
         kind = "reference"
-        step = lambda: ref.controller_cycle(wl.q0, None, None, wl.guidance, use_stored_cloud=True)  # noqa
-    else:  # C restatement, single-threaded
-        orc = ob.Oracle(wl.footprint, wl.model, wl.limits, p)
-        nom, up = wl.zero_state()
-        threads = 1
-        kind = "port"
-        cyc = [0]
 
         def step():
-            orc.control_cycle(wl.q0, wl.cloud, None, wl.guidance, nom, up, cyc[0])
-            cyc[0] += 1
-    times = []
-    t_end = time.perf_counter() + seconds
-    while time.perf_counter() < t_end or len(times) < 2:
-        t0 = time.perf_counter()
+            ref.reset()  # fresh controller, untimed
+            t0 = time.perf_counter()
+            ref.controller_cycle(wl.q0, None, None, wl.guidance, use_stored_cloud=True)
+            return time.perf_counter() - t0
+    else:
+        orc = ob.Oracle(wl.footprint, wl.model, wl.limits, wl.params)
+        threads, kind = 1, "port"
+
+        def step():
+            nom, up = wl.zero_state()
+            t0 = time.perf_counter()
+            orc.control_cycle(wl.q0, wl.cloud, None, wl.guidance, nom, up, 0)
+            return time.perf_counter() - t0
+    for _ in range(warmup):
         step()
-        times.append(time.perf_counter() - t0)
-        if len(times) >= 50:
+    times = []
+    t_end = time.perf_counter() + min_seconds
+    t_cap = time.perf_counter() + max_seconds
+    while len(times) < n_steps or time.perf_counter() < t_end:
+        times.append(step())
+        if time.perf_counter() > t_cap and len(times) >= 1:
             break
-    t_sample = statistics.median(times)
-    t_full = t_sample * wl.params.rollouts / p.rollouts
-    return {"value": 1.0 / t_full, "unit": "steps/s", "cores": threads, "kind": kind,
-            "sample": (f"{len(times)} MppiController::control_cycle calls at K={p.rollouts} of "
-                       f"{wl.params.rollouts} (T={p.horizon}, N={wl.n_points}), median "
-                       f"{t_sample * 1e3:.1f} ms, extrapolated linearly in K"),
-            "sec_per_step": t_full}
+    return times, threads, kind
+
+
+def cpu_reference_sample(wl, seconds: float = 10.0):
+    """cpu_baseline of the GPU arm: the reference's full-K control_cycle on all host threads for
+    about `seconds` (at least 3 steps)."""
+    threads = os.cpu_count() or 1
+    times, threads, kind = reference_steps(wl, threads, 3, warmup=1, min_seconds=seconds)
+    t = statistics.median(times)
+    return {"value": 1.0 / t, "unit": "steps/s", "cores": threads, "kind": kind,
+            "sample": (f"{len(times)} MppiController::control_cycle calls at the full workload "
+                       f"(K={wl.params.rollouts}, T={wl.params.horizon}, N={wl.n_points}), fresh "
+                       f"controller each, median {t * 1e3:.1f} ms, {threads} threads, "
+                       f"CPU {cpu_model()}"),
+            "sec_per_step": t}
+
+
+def reference_sdf_evals(threads: int, trials: int = 5):
+    """Config 4 on the reference's batch_signed_distance (the scaling_benchmark protocol,
+    bench.cpp:67-113: 3 warm-ups, then timed trials): 64-vertex star, 10^6 body-frame queries
+    (benchmark_queries, 50 m region, seed 1), evals/s."""
+    from paper_2605_29663_b200 import workloads as W
+    from tests import oracle_bindings as ob
+    if not ob.reference_available():
+        return None
+    wl = W.cfg1(K=8, T=2)
+    fp, _, pts = W.cfg4(P=1)
+    ref = ob.Reference(fp, wl.model, wl.limits, wl.params, threads=threads)
+    for _ in range(3):
+        ref.batch_signed_distance(pts, threads)
+    ts = []
+    for _ in range(trials):
+        t0 = time.perf_counter()
+        ref.batch_signed_distance(pts, threads)
+        ts.append(time.perf_counter() - t0)
+    t = statistics.median(ts)
+    return {"workload": "cfg4 star64, batch_signed_distance of 10^6 queries", "threads": threads,
+            "median_ms": 1e3 * t, "evals_per_s": pts.shape[0] / t,
+            "seconds_for_1e9_pairs": 1e9 / (pts.shape[0] / t)}
 
 
 def run_reference(args, world, rank):
+    """The reference arm: the reference's own CPU control_cycle at the GPU arm's config."""
     from paper_2605_29663_b200 import workloads as W
     if rank != 0:
         return
-    wl = W.cfg2()
-    base = cpu_reference_sample(wl, seconds=max(6.0, min(30.0, 0.05 * (args.steps + args.warmup))))
-    v = base["value"]
+    wl = {"cfg1": W.cfg1, "cfg2": W.cfg2, "cfg3": W.cfg3, "cfg5": W.cfg5}[args.config]()
+    nproc = os.cpu_count() or 1
+    times, threads, kind = reference_steps(wl, nproc, args.steps, warmup=args.warmup)
+    ms = 1e3 * statistics.mean(times)
+    v = 1e3 / ms
+    # threads = 1 (BASELINE.md §3): >= 5 steps, or 1 when a step exceeds 10 s
+    t1, _, _ = reference_steps(wl, 1, 1)
+    if t1[0] < 10.0:
+        more, _, _ = reference_steps(wl, 1, 4, max_seconds=60.0)
+        t1 += more
+    K, T, N = wl.params.rollouts, wl.params.horizon, wl.n_points
     line = {"metric": "MPPI control steps/sec", "value": v, "unit": "steps/s", "n_gpus": args.gpus,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 / v,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+            "ms_per_step_p50": 1e3 * statistics.median(times),
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic", "impl": "reference",
-            "config": {"workload": wl.name, "K": wl.params.rollouts, "T": wl.params.horizon,
-                       "N": wl.n_points, "footprint": "l_shape_12 polygon (B=12)", "model": "diff"},
-            "cpu_baseline": {k: base[k] for k in ("value", "unit", "cores", "kind", "sample")},
+            "config": bench_config(wl, world),
+            "cpu_baseline": {"value": v, "unit": "steps/s", "cores": threads, "kind": kind,
+                             "sample": (f"{len(times)} full-size MppiController::control_cycle "
+                                        f"calls (K={K}, T={T}, N={N}), a fresh controller each, "
+                                        f"{threads} threads, CPU {cpu_model()}")},
+            "cpu_threads1": {"steps": len(t1), "ms_per_step_median": 1e3 * statistics.median(t1),
+                             "steps_per_s": 1.0 / statistics.median(t1)},
+            "cpu_model": cpu_model(), "nproc": nproc,
             "e2e": {"value": v, "unit": "steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-            "sdf_evals_per_s": wl.params.rollouts * wl.params.horizon * wl.n_points * v}
+            "sdf_evals_per_s": K * T * N * v,
+            "sdf_batch_cfg4": reference_sdf_evals(nproc)}
     print(json.dumps(line), flush=True)
 
 
@@ -274,7 +369,8 @@ def run_ours(args, world, rank, local):
         torch.cuda.synchronize()
         step_ms = [a.elapsed_time(b) for a, b in evs]
     stats = eng.step_stats()  # SDF kernel mean over exactly the timed steps
-    tested, evaluated = eng.cull_stats()  # pairs that reached a point test / the exact SDF
+    path, vpath = eng.last_sdf_path()
+    counts = eng.sdf_work_stats()  # the last timed step's pose set, counters on
     ms_local = float(np.mean(step_ms))
     ms = allreduce_max(ms_local, world)
     value = 1e3 / ms
@@ -292,13 +388,6 @@ def run_ours(args, world, rank, local):
     clouds = [obstacles]
     if args.config == "cfg5":
         clouds = [W.cfg5(cycle=10 * j).obstacles() for j in range(8)]
-    if os.environ.get("EXM_BENCH_ONE_CLOUD") == "1":  # diagnostic: cfg5 without the snapshots
-        clouds = [obstacles]
-    # EXM_BENCH_PINNED=1: the caller's cloud buffers in page-locked memory, so the H2D copies are
-    # direct DMA. Measured 2 % slower end to end on config 2 than plain numpy buffers (the
-    # driver's staging of 170 KB is cheaper than the pinned-source DMA setup), equal on config 5.
-    if os.environ.get("EXM_BENCH_PINNED") == "1":
-        clouds = [pinned_obstacles(o) for o in clouds]
     e2e_ms = []
     t0 = time.perf_counter()
     for c in range(args.steps):
@@ -313,9 +402,9 @@ def run_ours(args, world, rank, local):
     pairs = K // world * T * N
     peak, peak_src = fp32_peak_tflops(torch.cuda.get_device_properties(local).multi_processor_count)
     sdf_avg_ms = stats["sdf_ms"]
-    achieved = pairs * F / (sdf_avg_ms * 1e-3) / 1e12
-    # executed work: 6 ops per point test (2 sub, mul, fma, compare) + F per exact SDF
-    executed_tf = (6.0 * tested + F * evaluated) / (sdf_avg_ms * 1e-3) / 1e12
+    ex_ops, per_unit = executed_ops(counts, fp)
+    achieved = ex_ops / (sdf_avg_ms * 1e-3) / 1e12
+    algorithmic = pairs * F
     prof = ncu_profile(f"sdf_grid_{args.config}")
     line = {
         "metric": "MPPI control steps/sec", "value": value, "unit": "steps/s", "n_gpus": world,
@@ -325,28 +414,30 @@ def run_ours(args, world, rank, local):
         "ms_per_step_p50": float(np.percentile(step_ms, 50)),
         "ms_per_step_p99": float(np.percentile(step_ms, 99)),
         "data": "synthetic",
-        "config": {"workload": wl.name, "K": K, "T": T, "N": N,
-                   "footprint": f"{wl.footprint.name} ({'polygon B' if fp.is_polygon() else 'cover R'}={fp.count()})",
-                   "model": ["diff", "ackermann", "omni", "spin", "parallel"][wl.model.tag],
-                   "parallelism": f"rollout-sharded x{world}",
-                   "l2": "flushed (256 MiB write) before every timed step"},
+        "config": bench_config(wl, world),
         "sdf_evals_per_s": K * T * N / (ms * 1e-3),  # point-pose pairs per second of MPPI step
         "sdf_kernel_evals_per_s": pairs * world / (sdf_avg_ms * 1e-3),  # ... of the SDF kernel
         "e2e": {"value": 1.0 / e2e_s, "unit": "steps/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "ms_p50": float(np.percentile(e2e_ms, 50)),
                 "ms_p99": float(np.percentile(e2e_ms, 99)),
-                "path": "exm_control_cycle (C ABI): host cloud/state -> pinned -> H2D, graph, D2H decision"},
+                "path": ("Engine.control_cycle_raw -> exm_control_cycle (C ABI): q0/goal/nominal/"
+                         "u_prev/guidance via the handle's pinned mirror, the cloud and mask "
+                         "copied from the caller's pageable numpy buffers (driver-staged), one "
+                         "graph launch, one D2H of the decision + nominal")},
         "gpu_launches": stats["launches_per_step"] * args.steps,
         "roofline": {"bound": "fp32", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                      "frac": achieved / peak, "traffic": prof.get("traffic"),
-                     "executed": {**(prof.get("executed") or {}),
-                                  "pairs_point_tested": tested, "pairs_exact_sdf": evaluated,
-                                  "culled_fraction": 1.0 - evaluated / pairs,
-                                  "achieved_executed_tflops": executed_tf,
-                                  "frac_executed": executed_tf / peak},
                      "kernel": f"k_sdf_grid<{'POLYGON' if fp.is_polygon() else 'RECT'},{fp.count()}> (per-pose exact SDF min, exact culling)",
                      "sdf_kernel_ms": sdf_avg_ms,
-                     "algorithmic": f"K*T*N pairs x {F} ops/pair (SURVEY §8(d), unpruned)",
+                     "work": "EXECUTED FP32 ops: exm_sdf_work_stats counters x per-unit op counts (DESIGN.md §4)",
+                     "executed_ops_per_launch": ex_ops,
+                     "counters": counts, "ops_per_unit": per_unit,
+                     "lane_efficiency_point_loop": (counts["point_tests"] / (32.0 * counts["point_iters_warp"])
+                                                    if counts["point_iters_warp"] else None),
+                     "algorithmic_ops_unpruned": algorithmic,
+                     "culling_factor": algorithmic / ex_ops if ex_ops else None,
+                     "ncu": prof.get("executed"),
+                     "sdf_path": path,
                      "peak_source": peak_src},
         "clocks": clk.summary(),
         "decision": {"validated": dec.validated, "argmin": dec.argmin,

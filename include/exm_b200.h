@@ -23,8 +23,9 @@
  * dim is MotionModel::control_dim() (kinematics.cpp:14-26): diff/ackermann 2, omni 3,
  * spin/parallel 1.
  *
- * Threading mirrors MppiController (controller.hpp:138-139): one handle is not safe for
- * concurrent use; distinct handles may be used from distinct threads.
+ * Threading: the reference's MppiController is "sendable between threads, not concurrently
+ * shared" (controller.hpp:138-139). Here every call on a handle holds that handle's lock, so
+ * concurrent calls on one handle are safe and serialise; distinct handles run concurrently.
  */
 #ifndef EXM_B200_H
 #define EXM_B200_H
@@ -35,7 +36,7 @@
 extern "C" {
 #endif
 
-#define EXM_ABI_VERSION 1
+#define EXM_ABI_VERSION 2
 
 typedef int32_t exm_status;
 enum {
@@ -222,10 +223,28 @@ exm_status exm_hybrid_cycle(exm_hybrid* hy, const double q0[3], const double* pt
 
 /* ---- multi-GPU (one process per GPU) ----------------------------------------------
  * The reference's only parallelism is a std::thread fork-join over rollouts
- * (controller.cpp:207-218). Here rollouts are sharded over ranks; rank 0 creates the id,
- * the caller broadcasts it (e.g. torch.distributed), every rank attaches. */
+ * (controller.cpp:207-218). Here rollouts are sharded over ranks in fixed 256-rollout blocks
+ * (rank g of G owns rollouts [g*K/G, (g+1)*K/G); K must be a multiple of 256*G); rank 0 creates
+ * the id, the caller broadcasts it (e.g. torch.distributed), every rank attaches. With a
+ * communicator attached (any world >= 1, a 1-rank one included) every control step issues one
+ * in-place ncclAllGather of the softmax block partials inside its CUDA graph; every rank merges
+ * them in block order and returns the same decision, bit-identical for every G.
+ * exm_attach_comm(h, 0, 1, NULL) detaches (unsharded, no collective). */
 exm_status exm_nccl_unique_id(uint8_t id_out[128]);
 exm_status exm_attach_comm(exm_handle* h, int32_t rank, int32_t world, const uint8_t id[128]);
+
+/* Sharding without a communicator, for several shard handles on ONE device (tests, and
+ * emulating G ranks on one GPU): exm_set_shard(h, g, G) makes h own rank g's rollouts;
+ * exm_sharded_cycle then runs one control step on all G shard handles (shards[g] of rank g,
+ * same configuration, same device), exchanging the block partials between them with one
+ * device-to-device copy per block where the ranks' all-gather would run. Per-shard state:
+ * nominals_inout[g*T*dim ...], u_prevs_inout[3*g ...], out[g]. exm_set_shard(h, 0, 1) undoes. */
+exm_status exm_set_shard(exm_handle* h, int32_t rank, int32_t world);
+exm_status exm_sharded_cycle(exm_handle* const* shards, int32_t n_shards, const double q0[3],
+                             const double* pts_xy, const uint8_t* mask, int32_t n_points,
+                             const double* guide_xy, int32_t n_guide, const double goal[3],
+                             double* nominals_inout, double* u_prevs_inout, uint64_t cycle,
+                             const double* eps_or_null, exm_decision* out);
 
 /* ---- resident-input stepping (benchmark / serving loop) -----------------------------
  * Stage the inputs of a control step once (host -> device), then run n_steps control
@@ -253,6 +272,45 @@ exm_status exm_step_stats(exm_handle* h, int32_t* launches_per_step, float* sdf_
  * counters (profiling only; not on the step path): point-pose pairs that reached a point test,
  * and pairs that reached the exact signed-distance evaluation. */
 exm_status exm_sdf_cull_stats(exm_handle* h, int64_t* points_tested, int64_t* sdf_evaluated);
+
+/* ---- options and diagnostics ------------------------------------------------------------ */
+enum {
+  EXM_OPT_SDF_MODE = 1,    /* EXM_SDF_* below (tests / A/B only; default EXM_SDF_AUTO) */
+  EXM_OPT_AUTO_CAPS = 2,   /* 1: derive per-step SDF caps from each step's own d_min statistic */
+  EXM_OPT_PREGEN = 3,      /* 0: no next-cycle noise pregeneration (default 1) */
+  EXM_OPT_HOST_TIMING = 4, /* 1: accumulate exm_control_cycle host phases (exm_host_timing) */
+  EXM_OPT_HOST_THREADS = 5 /* host threads converting batch_signed_distance queries (default:
+                              min(8, hardware threads)); the reference's `threads` argument */
+};
+/* Signed-distance kernel selection: automatic, or (tests) every bound disabled, no chunk
+ * bound, a forced thread / warp / 8-warp-CTA per pose kernel, persistent warps, caps ignored. */
+enum {
+  EXM_SDF_AUTO = 0, EXM_SDF_BRUTE = 1, EXM_SDF_NOCHUNK = 2, EXM_SDF_THREAD = 3,
+  EXM_SDF_WARP = 4, EXM_SDF_CTA = 5, EXM_SDF_PERSIST = 6, EXM_SDF_NOCAP = 7
+};
+/* Set a handle option. Captured step graphs are rebuilt on the next step. */
+exm_status exm_set_option(exm_handle* h, int32_t option, int32_t value);
+/* EXM_OPT_HOST_TIMING: mean host microseconds per exm_control_cycle call in each phase
+ * {stage + H2D enqueue, graph launch + D2H enqueue, wait, unpack} and the call count. */
+exm_status exm_host_timing(exm_handle* h, double us_per_call[4], int64_t* calls);
+
+/* Which signed-distance kernel the last rollout / validation launch ran. */
+typedef struct exm_sdf_path {
+  int32_t kernel;     /* 0 thread per pose, 1 warp per pose, 2 8-warp CTA per pose */
+  int32_t chunk;      /* points per cull chunk of the cloud layout (8 or 16) */
+  int32_t persistent; /* 1: persistent warps with a work counter */
+  int32_t ctas, threads;
+  int32_t hmajor;     /* 1: a warp's lanes take consecutive rollouts at one horizon step */
+} exm_sdf_path;
+exm_status exm_last_sdf_path(exm_handle* h, exm_sdf_path* rollout, exm_sdf_path* validation);
+
+/* Work counters of the rollout signed distance over the last step's poses (re-runs the kernel
+ * once with counters; profiling only): counts[EXM_SDF_NCOUNT] = {ring steps (per warp),
+ * cell bound tests, chunk bound tests, point circle tests, point-loop iterations (per warp),
+ * body-frame transforms, exact-cover tile tests, tile distances taken, cover/AABB bound tests,
+ * edge-loop (polygon) or box-loop (cover) signed distances}; per lane unless noted. */
+#define EXM_SDF_NCOUNT 10
+exm_status exm_sdf_work_stats(exm_handle* h, int64_t* counts);
 
 /* ---- sensing (world.cpp:182-243) ---------------------------------------- */
 enum { EXM_OBSTACLE_POLYGON = 0, EXM_OBSTACLE_DISC = 1 };

@@ -69,6 +69,20 @@ class ExmDecision(C.Structure):
                 ("nominal_cost", C.c_double), ("nominal_dmin", _dp)]
 
 
+class ExmSdfPath(C.Structure):
+    _fields_ = [("kernel", C.c_int32), ("chunk", C.c_int32), ("persistent", C.c_int32),
+                ("ctas", C.c_int32), ("threads", C.c_int32), ("hmajor", C.c_int32)]
+
+
+# exm_set_option options and EXM_SDF_* modes (include/exm_b200.h)
+OPT_SDF_MODE, OPT_AUTO_CAPS, OPT_PREGEN, OPT_HOST_TIMING, OPT_HOST_THREADS = 1, 2, 3, 4, 5
+SDF_MODES = {"auto": 0, "brute": 1, "nochunk": 2, "thread": 3, "warp": 4, "cta": 5,
+             "persist": 6, "nocap": 7}
+SDF_NCOUNT = 10
+SDF_COUNTERS = ("ring_steps", "cell_tests", "chunk_tests", "point_tests", "point_iters_warp",
+                "transforms", "tile_tests", "tile_values", "bound_tests", "edge_loops")
+
+
 class ExmHandle(C.Structure):
     pass
 
@@ -124,6 +138,14 @@ SIGNATURES = {
                                              C.POINTER(C.c_float), C.POINTER(C.c_int32)]),
     "exm_step_stats": (C.c_int32, [_Hp, C.POINTER(C.c_int32), C.POINTER(C.c_float),
                                    C.POINTER(C.c_int64)]),
+    "exm_set_shard": (C.c_int32, [_Hp, C.c_int32, C.c_int32]),
+    "exm_sharded_cycle": (C.c_int32, [C.POINTER(_Hp), C.c_int32, _dp, _dp, _u8p, C.c_int32, _dp,
+                                      C.c_int32, _dp, _dp, _dp, C.c_uint64, _dp,
+                                      C.POINTER(ExmDecision)]),
+    "exm_set_option": (C.c_int32, [_Hp, C.c_int32, C.c_int32]),
+    "exm_host_timing": (C.c_int32, [_Hp, _dp, C.POINTER(C.c_int64)]),
+    "exm_last_sdf_path": (C.c_int32, [_Hp, C.POINTER(ExmSdfPath), C.POINTER(ExmSdfPath)]),
+    "exm_sdf_work_stats": (C.c_int32, [_Hp, C.POINTER(C.c_int64)]),
 }
 
 _lib = None

@@ -293,6 +293,8 @@ class ObstacleSet:
     def __post_init__(self):
         self.points = np.ascontiguousarray(np.asarray(self.points, dtype=np.float64).reshape(-1, 2))
         self.mask = np.ascontiguousarray(np.asarray(self.mask, dtype=np.uint8).reshape(-1))
+        if self.mask.size != self.points.shape[0]:
+            raise ValueError("obstacle mask length must equal the number of points")
 
     @staticmethod
     def padded(valid_points, capacity: int) -> "ObstacleSet":
@@ -368,9 +370,11 @@ class Engine:
         self._decp = C.addressof(self._dec)
         self._addrs: dict = {}
 
-    def _addr(self, a, dtype=np.float64):
+    def _addr(self, a, dtype=np.float64, min_size: int = 0, size: int = -1):
         """Address of a C-contiguous array of `dtype`, cached per array object (the cache holds
-        a reference, so an id cannot be reused while its entry lives)."""
+        a reference, so an id cannot be reused while its entry lives and the array cannot be
+        resized in place). Sizes are checked on a cache miss. Only long-lived arrays (state,
+        guidance, obstacle buffers) go through here."""
         if a is None:
             return None
         ent = self._addrs.get(id(a))
@@ -378,7 +382,10 @@ class Engine:
             return ent[1]
         if a.dtype != dtype or not a.flags.c_contiguous:
             raise ValueError("array must be C-contiguous " + np.dtype(dtype).name)
-        if len(self._addrs) >= 64:
+        if a.size < min_size or (size >= 0 and a.size != size):
+            raise ValueError(f"array has {a.size} elements, expected "
+                             f"{size if size >= 0 else f'at least {min_size}'}")
+        if len(self._addrs) >= 16:
             self._addrs.clear()
         addr = a.ctypes.data
         self._addrs[id(a)] = (a, addr)
@@ -470,13 +477,17 @@ class Engine:
             pts, mask = self._cloud(obstacles)
         q = self._q0buf
         q[0], q[1], q[2] = q0[0], q0[1], q0[2]
-        eps_arr = None
-        if eps is not None:
+        eps_addr = None
+        if eps is not None:  # injected noise: not cached (a fresh array per call)
             eps_arr = np.ascontiguousarray(np.asarray(eps, np.float64))
+            if eps_arr.size != self.params.rollouts * self.params.horizon * self.dim:
+                raise ValueError("perturbation array does not match K*T")
+            eps_addr = eps_arr.ctypes.data
         A = self._addr
-        rc = self._cc(self._hv, self._q0addr, A(pts), A(mask, np.uint8), pts.shape[0],
-                      A(guidance.path), guidance.path.shape[0], A(guidance.goal), A(nominal),
-                      A(u_prev), int(cycle), A(eps_arr), self._decp)
+        rc = self._cc(self._hv, self._q0addr, A(pts), A(mask, np.uint8, size=pts.shape[0]),
+                      pts.shape[0], A(guidance.path), guidance.path.shape[0], A(guidance.goal),
+                      A(nominal, size=self.params.horizon * self.dim), A(u_prev, min_size=self.dim),
+                      int(cycle), eps_addr, self._decp)
         if rc:
             check(rc)
         dec = self._dec
@@ -598,8 +609,72 @@ class Engine:
         return bytes(buf)
 
     def attach_comm(self, rank: int, world: int, uid: bytes | None):
-        buf = (C.c_uint8 * 128)(*(uid or bytes(128)))
+        """Shard this handle as rank `rank` of `world` over an NCCL communicator built from `uid`
+        (any world, a 1-rank communicator included); uid None with world 1 detaches."""
+        buf = None if uid is None else (C.c_uint8 * 128)(*uid)
         check(self.lib.exm_attach_comm(self.h, int(rank), int(world), buf))
+
+    def set_shard(self, rank: int, world: int):
+        """Shard without a communicator (several shard handles on one device, sharded_cycle)."""
+        check(self.lib.exm_set_shard(self.h, int(rank), int(world)))
+
+    @staticmethod
+    def sharded_cycle(shards, q0, obstacles, guidance: Guidance, nominals, u_prevs, cycle: int,
+                      eps=None):
+        """One control step on G shard engines (shards[g] set to rank g of G) on one device,
+        the block partials exchanged between them as the ranks' all-gather would. nominals
+        (G, T*dim) and u_prevs (G, 3) are updated in place; returns G decisions."""
+        G = len(shards)
+        e0 = shards[0]
+        pts, mask = e0._cloud(obstacles) if not isinstance(obstacles, ObstacleSet) else (
+            obstacles.points, obstacles.mask)
+        hs = (C.POINTER(_abi.ExmHandle) * G)(*[e.h for e in shards])
+        decs = (_abi.ExmDecision * G)()
+        dmins = [np.zeros(e0.params.horizon) for _ in range(G)]
+        for g in range(G):
+            decs[g].nominal_dmin = dptr(dmins[g])
+        assert nominals.dtype == np.float64 and nominals.flags.c_contiguous
+        assert u_prevs.dtype == np.float64 and u_prevs.flags.c_contiguous and u_prevs.shape == (G, 3)
+        eps_arr = None if eps is None else np.ascontiguousarray(np.asarray(eps, np.float64))
+        check(e0.lib.exm_sharded_cycle(hs, G, dptr(e0._vec3(q0)), dptr(pts), u8ptr(mask),
+                                       pts.shape[0], dptr(guidance.path), guidance.path.shape[0],
+                                       dptr(guidance.goal), dptr(nominals), dptr(u_prevs),
+                                       int(cycle), dptr(eps_arr), decs))
+        D = e0.dim
+        return [ControlDecision(np.array(decs[g].command[:D]), bool(decs[g].validated),
+                                nominals[g].reshape(-1, D).copy(), decs[g].best_cost,
+                                decs[g].weight_entropy, decs[g].nominal_cost, dmins[g],
+                                decs[g].argmin) for g in range(G)]
+
+    # -- options and diagnostics
+    def set_option(self, option: int, value: int):
+        check(self.lib.exm_set_option(self.h, int(option), int(value)))
+
+    def set_sdf_mode(self, mode: str):
+        """Signed-distance kernel selection (tests / A/B): auto, brute, nochunk, thread, warp,
+        cta, persist, nocap."""
+        self.set_option(_abi.OPT_SDF_MODE, _abi.SDF_MODES[mode])
+
+    def last_sdf_path(self):
+        """What the last rollout / validation SDF launches ran (kernel 0 thread, 1 warp, 2 CTA
+        per pose; chunk; persistent; hmajor)."""
+        r, v = _abi.ExmSdfPath(), _abi.ExmSdfPath()
+        check(self.lib.exm_last_sdf_path(self.h, C.byref(r), C.byref(v)))
+        as_dict = lambda x: {f: getattr(x, f) for f, _ in x._fields_}  # noqa: E731
+        return as_dict(r), as_dict(v)
+
+    def sdf_work_stats(self) -> dict:
+        """Work counters of the rollout SDF over the last step's poses (re-runs it once)."""
+        c = (C.c_int64 * _abi.SDF_NCOUNT)()
+        check(self.lib.exm_sdf_work_stats(self.h, c))
+        return dict(zip(_abi.SDF_COUNTERS, list(c)))
+
+    def host_timing(self):
+        us = np.zeros(4)
+        n = C.c_int64()
+        check(self.lib.exm_host_timing(self.h, dptr(us), C.byref(n)))
+        return {"stage_h2d_us": us[0], "launch_us": us[1], "wait_us": us[2], "unpack_us": us[3],
+                "calls": n.value}
 
 
 class MppiController:

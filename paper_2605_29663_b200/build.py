@@ -24,20 +24,24 @@ def _stale(target: str, deps) -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build_library(force: bool = False, verbose: bool = False) -> str:
+def build_library(force: bool = False, verbose: bool = False, lib: str = LIB,
+                  defines: tuple = ()) -> str:
     """Compile the stale objects (source or a shared header newer than the object) in
-    parallel, then link when any object changed."""
+    parallel, then link when any object changed. `lib` / `defines`: A/B variant builds
+    (tools/ab_variants.py: e.g. -DEXM_SDF_RMAJOR into abtest/<name>/libexm_b200.so, selected at
+    run time with EXM_LIB_PATH); the product is the default build."""
     from concurrent.futures import ThreadPoolExecutor
 
+    LIB_ = lib
     common = [os.path.join(CSRC, h) for h in HEADERS] + [os.path.join(ROOT, "include", "exm_b200.h")]
-    objdir = os.path.join(os.path.dirname(LIB), "obj")
+    objdir = os.path.join(os.path.dirname(LIB_), "obj")
     os.makedirs(objdir, exist_ok=True)
     jobs, objs = [], []
     for src in SOURCES:
         obj = os.path.join(objdir, src.replace(".cu", ".o"))
         objs.append(obj)
         if force or _stale(obj, [os.path.join(CSRC, src), *common]):
-            jobs.append(["nvcc", *NVCC_FLAGS, *UNIT_FLAGS.get(src, []), "-c", "-o", obj,
+            jobs.append(["nvcc", *NVCC_FLAGS, *UNIT_FLAGS.get(src, []), *defines, "-c", "-o", obj,
                          os.path.join(CSRC, src)])
 
     def run(cmd):
@@ -48,10 +52,10 @@ def build_library(force: bool = False, verbose: bool = False) -> str:
     if jobs:
         with ThreadPoolExecutor(max_workers=len(jobs)) as ex:
             list(ex.map(run, jobs))
-    if force or jobs or _stale(LIB, objs):
-        run(["nvcc", "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", LIB, *objs,
+    if force or jobs or _stale(LIB_, objs):
+        run(["nvcc", "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", LIB_, *objs,
              "-ldl"])
-    return LIB
+    return LIB_
 
 
 def build_oracle(with_reference: bool | None = None) -> None:
@@ -71,7 +75,7 @@ def build_dropin() -> None:
     ref = os.environ.get("REF_DIR", "/root/reference/proj")
     if os.path.isdir(os.path.join(ref, "src")):
         subprocess.run(["make", "-s", "-C", os.path.join(HERE, "host"), f"REF_DIR={ref}", "all",
-                        "acceptance"], check=True)
+                        "acceptance", "scaling"], check=True)
 
 
 if __name__ == "__main__":

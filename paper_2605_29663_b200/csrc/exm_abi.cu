@@ -11,11 +11,16 @@
 
 #include <algorithm>
 #include <array>
+#include <atomic>
 #include <chrono>
+#include <condition_variable>
+#include <functional>
+#include <thread>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -427,7 +432,9 @@ exm_status build_footprint(const exm_footprint* fp, FpDev* out) {
       out->cbox[j][2] = static_cast<float>(0.5 * (bj[1] - bj[0]));
       out->cbox[j][3] = static_cast<float>(0.5 * (bj[3] - bj[2]));
     }
-    if (const char* ev = std::getenv("EXM_COVER_EXACT"); ev && ev[0] == '0') out->cover_exact = 0;
+#ifdef EXM_NO_COVER_EXACT  // A/B builds: every polygon point through the edge loop
+    out->cover_exact = 0;
+#endif
   }
   return EXM_OK;
 }
@@ -449,10 +456,97 @@ struct EventPair {
   cudaEvent_t a = nullptr, b = nullptr;
 };
 
+// A small persistent host thread pool for the FP64 <-> FP32 staging of batch_signed_distance
+// (the caller's `threads`, geometry.cpp:298-318). run(n, fn) calls fn(0..n-1) on the workers and
+// the calling thread and returns when all are done. Workers spin briefly between jobs (queries
+// arrive in bursts of pipelined chunks), then sleep.
+class HostPool {
+ public:
+  explicit HostPool(int workers) {
+    for (int i = 0; i < workers; ++i) th_.emplace_back([this] { loop(); });
+  }
+  ~HostPool() {
+    {
+      std::lock_guard<std::mutex> lk(mu_);
+      stop_ = true;
+      gen_.fetch_add(1);
+    }
+    cv_.notify_all();
+    for (auto& t : th_) t.join();
+  }
+  int size() const { return static_cast<int>(th_.size()) + 1; }
+  void run(int n, const std::function<void(int)>& fn) {
+    if (n <= 0) return;
+    if (th_.empty() || n == 1) {
+      for (int i = 0; i < n; ++i) fn(i);
+      return;
+    }
+    fn_ = &fn;
+    n_ = n;
+    next_.store(0);
+    done_.store(0);
+    {
+      std::lock_guard<std::mutex> lk(mu_);
+      gen_.fetch_add(1);
+    }
+    cv_.notify_all();
+    work();
+    while (done_.load(std::memory_order_acquire) < n) std::this_thread::yield();
+  }
+
+ private:
+  void work() {
+    for (;;) {
+      const int i = next_.fetch_add(1);
+      if (i >= n_) return;
+      (*fn_)(i);
+      done_.fetch_add(1, std::memory_order_release);
+    }
+  }
+  void loop() {
+    unsigned seen = gen_.load();
+    for (;;) {
+      // spin ~100 us for the next job of a pipelined burst, then sleep
+      const auto t0 = std::chrono::steady_clock::now();
+      while (gen_.load(std::memory_order_acquire) == seen &&
+             std::chrono::steady_clock::now() - t0 < std::chrono::microseconds(100))
+        std::this_thread::yield();
+      if (gen_.load(std::memory_order_acquire) == seen) {
+        std::unique_lock<std::mutex> lk(mu_);
+        cv_.wait(lk, [&] { return gen_.load() != seen; });
+      }
+      seen = gen_.load();
+      if (stop_) return;
+      work();
+    }
+  }
+  std::vector<std::thread> th_;
+  std::mutex mu_;
+  std::condition_variable cv_;
+  std::atomic<unsigned> gen_{0};
+  std::atomic<int> next_{0}, done_{0};
+  int n_ = 0;
+  const std::function<void(int)>* fn_ = nullptr;
+  bool stop_ = false;
+};
+
+constexpr int kRingMax = 512;  // SDF timing events kept before they are folded into a sum
+constexpr int kBsdSlots = 3;   // batch_signed_distance pipeline depth (chunks in flight)
+
 }  // namespace
 
 struct exm_handle {
+  // Every ABI call on a handle holds its mutex: calls on one handle serialise (the drop-in's
+  // handle cache may hand one handle to controllers on several threads).
+  std::mutex mu;
   int device = 0;
+  // options (exm_set_option)
+  int sdf_mode = kSdfAuto;
+  bool auto_caps = false, pregen = true, host_timing = false;
+  // what the last rollout / validation signed-distance launch ran (exm_last_sdf_path)
+  SdfPath roll_path{}, val_path{};
+  // sharding without a communicator (exm_set_shard: several shard handles on one device)
+  bool emulated = false;
   cudaStream_t stream = nullptr;
   cudaStream_t side = nullptr;  // parallel graph branch (cloud preparation, noise pregeneration)
   cudaEvent_t fork_ev = nullptr, join_ev = nullptr, pg_fork = nullptr, pg_join = nullptr;
@@ -503,7 +597,7 @@ struct exm_handle {
   StepDyn* h_dyn = nullptr;
   double* h_nominal = nullptr;
   double* h_guide = nullptr;
-  double* h_pts = nullptr;
+  double* h_pts = nullptr;  // end of the pinned mirror (the cloud is copied from the caller)
   uint8_t* h_mask = nullptr;
   unsigned char* h_out = nullptr;
   // graphs: [0] device noise, [1] injected noise
@@ -517,9 +611,13 @@ struct exm_handle {
   EventPair step_ev;
   EventPair ev_set[2];  // events the exec's SDF event nodes currently record
   int last_steps = 0;
+  double ring_ms = 0.0;  // SDF times folded out of a full ring
+  int ring_n = 0;
   // SDF batch workspace (grown on demand)
   int sb_poses_cap = 0, sb_points_cap = 0;
   size_t sb_pairs_cap = 0;
+  double* sb_poses64 = nullptr;
+  double* sb_center = nullptr;
   float4* sb_poses = nullptr;
   double* sb_pts64 = nullptr;
   float2* sb_pts = nullptr;
@@ -528,6 +626,16 @@ struct exm_handle {
   double* sb_min = nullptr;
   float* sb_pairs = nullptr;
   int sb_P = 0, sb_N = 0, sb_has_mask = 0, sb_last_pairs = 0;
+  // batch_signed_distance pipeline: kBsdSlots chunks of bsd_chunk queries, pinned FP32 staging
+  // on the host, device buffers, one completion event per slot; host conversion pool
+  int bsd_chunk = 0;
+  float2* bsd_hq = nullptr;  // pinned [slot][chunk]
+  float* bsd_hd = nullptr;   // pinned [slot][chunk]
+  float2* bsd_dq = nullptr;
+  float* bsd_dd = nullptr;
+  cudaEvent_t bsd_ev[kBsdSlots] = {};
+  int host_threads = 0;  // 0: default
+  HostPool* pool = nullptr;
   int launches_per_step = 0;
   int64_t last_pairs = 0;
   // hybrid families share the pose / d_min arrays and family 0's cloud grid
@@ -569,7 +677,7 @@ void destroy_graphs(exm_handle* h) {
 //   sdf   : per-pose exact SDF over the step's K*T poses             -> d_dmin
 //   post  : stage costs -> block partials -> [all-gather] -> merge/update/validation
 //           dynamics -> validation SDF -> finalize                    -> d_out, state
-exm_status enqueue_prep(exm_handle* h, cudaStream_t s) {
+exm_status enqueue_prep(exm_handle* h, cudaStream_t s) {  // k_cloud_prep + k_cell_sort
   EXM_CUDA(launch_cloud_prep(h->d_pts, h->d_mask, h->d_dyn, h->fp.radius, h->grid, h->n_cap, s));
   return EXM_OK;
 }
@@ -582,34 +690,35 @@ exm_status enqueue_pre(exm_handle* h, bool draw_noise, cudaStream_t s, int* laun
   return EXM_OK;
 }
 
-bool auto_caps() {
-  static const bool on = std::getenv("EXM_AUTO_CAPS") && std::getenv("EXM_AUTO_CAPS")[0] == '1';
-  return on;
-}
-
-// EXM_PREGEN=0: no noise pregeneration (every rollout draws its own noise)
-bool pregen_enabled() {
-  static const bool on = !(std::getenv("EXM_PREGEN") && std::getenv("EXM_PREGEN")[0] == '0');
-  return on;
-}
-
-exm_status enqueue_post(exm_handle* h, cudaStream_t s, int* launches, bool pregen = false) {
+// post, first half: rollout costs, softmax block partials of this rank's blocks, and (when
+// pregen) the next cycle's noise on the side branch (forked after the last reader of eps)
+exm_status enqueue_post_a(exm_handle* h, cudaStream_t s, int* launches, bool pregen) {
   const StepConst& sc = h->sc;
   // automatic per-step caps (d_min statistic -> k_finalize) measured slower than none on the
-  // benchmark configs (fallback passes): off unless EXM_AUTO_CAPS=1; exm_set_sdf_caps still works
-  float* hstat = auto_caps() ? h->d_hstat : nullptr;
+  // benchmark configs (fallback passes): off unless EXM_OPT_AUTO_CAPS; exm_set_sdf_caps still works
+  float* hstat = h->auto_caps ? h->d_hstat : nullptr;
   EXM_CUDA(launch_rollout_costs(sc, h->d_dyn, h->d_guide, h->guide_cap, h->d_base, h->d_ctrl,
                                 h->d_xy, h->d_dmin, h->d_cost, h->d_unsafe, h->grid.dstat,
                                 hstat, s));
   EXM_CUDA(launch_block_partials(sc, h->d_cost, h->d_unsafe, h->d_eps, h->d_partials, s));
-  if (pregen) {  // the next cycle's noise on the side branch, overlapping the serial tail
+  *launches += 2;
+  if (pregen) {
     EXM_CUDA(cudaEventRecord(h->pg_fork, s));
     EXM_CUDA(cudaStreamWaitEvent(h->side, h->pg_fork, 0));
     EXM_CUDA(launch_noise_pregen(sc, h->d_eps, h->side));
     EXM_CUDA(cudaEventRecord(h->pg_join, h->side));
     ++*launches;
   }
-  if (h->world > 1) {
+  return EXM_OK;
+}
+
+// post, second half: exchange of the block partials (one in-place NCCL all-gather whenever a
+// communicator is attached, including a 1-rank one), merge + update + validation dynamics,
+// validation SDF, finalize
+exm_status enqueue_post_b(exm_handle* h, cudaStream_t s, int* launches) {
+  const StepConst& sc = h->sc;
+  float* hstat = h->auto_caps ? h->d_hstat : nullptr;
+  if (h->comm) {
     const size_t count = static_cast<size_t>(sc.nblocks_local) * partial_stride(sc.T, sc.D);
     const int rc = g_nccl.allgather(h->d_partials + static_cast<size_t>(sc.block_offset) *
                                                         partial_stride(sc.T, sc.D),
@@ -619,13 +728,19 @@ exm_status enqueue_post(exm_handle* h, cudaStream_t s, int* launches, bool prege
   }
   EXM_CUDA(launch_update(sc, h->d_partials, h->d_nominal, h->d_dyn, h->d_upd, h->d_val_poses,
                          h->d_val_xy, h->d_val_base, out_dec(h), 1, s));
-  EXM_CUDA(launch_sdf_grid(h->fp, h->d_val_poses, sc.T, h->grid,
-                           h->d_val_dmin, s));
+  EXM_CUDA(launch_sdf_grid(h->fp, h->d_val_poses, sc.T, 0, h->grid, nullptr, h->sdf_mode,
+                           h->d_val_dmin, &h->val_path, nullptr, s));
   EXM_CUDA(launch_finalize(sc, h->d_val_dmin, h->d_val_xy, h->d_val_base, h->d_upd, h->d_guide,
                            h->guide_cap, h->d_nominal, h->d_dyn, out_dec(h), out_dmin(h),
                            out_nominal(h), out_uprev(h), 1, hstat, h->d_cap, h->fp.radius, s));
-  *launches += 6;
+  *launches += 3;
   return EXM_OK;
+}
+
+exm_status enqueue_post(exm_handle* h, cudaStream_t s, int* launches, bool pregen = false) {
+  exm_status st = enqueue_post_a(h, s, launches, pregen);
+  if (st != EXM_OK) return st;
+  return enqueue_post_b(h, s, launches);
 }
 
 exm_status record_ev(cudaEvent_t e, cudaStream_t s, bool capturing) {
@@ -634,27 +749,46 @@ exm_status record_ev(cudaEvent_t e, cudaStream_t s, bool capturing) {
   return EXM_OK;
 }
 
-// The control step. The cloud preparation (single CTA) runs on a side stream concurrently
-// with the noise + rollout branch; the graph captures both branches and their join.
-exm_status enqueue_step(exm_handle* h, bool draw_noise, const EventPair* ev, cudaStream_t s,
-                        bool capturing) {
+// The rollout SDF of a step (capped by the previous step's per-step statistic when set).
+exm_status enqueue_rollout_sdf(exm_handle* h, cudaStream_t s) {
   const StepConst& sc = h->sc;
-  int launches = 0;
+  EXM_CUDA(launch_sdf_grid(h->fp, h->d_poses, sc.k_local * sc.T, sc.T, h->grid, h->d_cap,
+                           h->sdf_mode, h->d_dmin, &h->roll_path, nullptr, s));
+  h->roll_path.chunk = chunk_for_capacity(h->n_cap);
+  h->val_path.chunk = h->roll_path.chunk;
+  return EXM_OK;
+}
+
+// Head of the control step: the cloud preparation (single CTA) runs on a side stream
+// concurrently with the noise + rollout branch, joined before the rollout SDF.
+exm_status enqueue_head(exm_handle* h, bool draw_noise, const EventPair* ev, cudaStream_t s,
+                        bool capturing, int* launches) {
   exm_status st;
   EXM_CUDA(cudaEventRecord(h->fork_ev, s));
   EXM_CUDA(cudaStreamWaitEvent(h->side, h->fork_ev, 0));
   if ((st = enqueue_prep(h, h->side)) != EXM_OK) return st;
-  ++launches;
+  *launches += 2;
   EXM_CUDA(cudaEventRecord(h->join_ev, h->side));
-  if ((st = enqueue_pre(h, draw_noise, s, &launches)) != EXM_OK) return st;
+  if ((st = enqueue_pre(h, draw_noise, s, launches)) != EXM_OK) return st;
   EXM_CUDA(cudaStreamWaitEvent(s, h->join_ev, 0));
   if (ev && (st = record_ev(ev->a, s, capturing)) != EXM_OK) return st;
-  // capped by the previous step's per-step statistic (hybrid batches: one SDF over all families)
-  EXM_CUDA(launch_sdf_grid_capped(h->fp, h->d_poses, sc.k_local * sc.T, h->grid, h->d_cap, sc.T,
-                                  h->d_dmin, s));
-  ++launches;
+  if ((st = enqueue_rollout_sdf(h, s)) != EXM_OK) return st;
+  ++*launches;
   if (ev && (st = record_ev(ev->b, s, capturing)) != EXM_OK) return st;
-  const bool pregen = draw_noise && h->sc.nstate != nullptr && pregen_enabled();
+  return EXM_OK;
+}
+
+bool pregen_for(const exm_handle* h, bool draw_noise) {
+  return draw_noise && h->sc.nstate != nullptr && h->pregen;
+}
+
+// The control step (captured into the handle's graphs).
+exm_status enqueue_step(exm_handle* h, bool draw_noise, const EventPair* ev, cudaStream_t s,
+                        bool capturing) {
+  int launches = 0;
+  exm_status st = enqueue_head(h, draw_noise, ev, s, capturing, &launches);
+  if (st != EXM_OK) return st;
+  const bool pregen = pregen_for(h, draw_noise);
   if ((st = enqueue_post(h, s, &launches, pregen)) != EXM_OK) return st;
   if (pregen) EXM_CUDA(cudaStreamWaitEvent(s, h->pg_join, 0));
   h->launches_per_step = launches;
@@ -707,14 +841,36 @@ exm_status launch_graph(exm_handle* h, int variant, const EventPair& ev) {
   return EXM_OK;
 }
 
-exm_status ensure_ring(exm_handle* h, int n) {
-  while (static_cast<int>(h->ring.size()) < n) {
+// Next SDF timing event pair of a resident run. The ring holds at most kRingMax pairs: a full
+// ring is folded (stream synchronised, times summed into ring_ms) so it never grows unbounded.
+exm_status next_ring_slot(exm_handle* h, EventPair** out) {
+  if (h->ring_used >= kRingMax) {
+    EXM_CUDA(cudaStreamSynchronize(h->stream));
+    for (int i = 0; i < h->ring_used; ++i) {
+      float ms = 0.0f;
+      EXM_CUDA(cudaEventElapsedTime(&ms, h->ring[i].a, h->ring[i].b));
+      h->ring_ms += ms;
+      ++h->ring_n;
+    }
+    h->ring_used = 0;
+  }
+  if (static_cast<int>(h->ring.size()) <= h->ring_used) {
     EventPair p;
     EXM_CUDA(cudaEventCreate(&p.a));
     EXM_CUDA(cudaEventCreate(&p.b));
     h->ring.push_back(p);
   }
+  *out = &h->ring[h->ring_used++];
   return EXM_OK;
+}
+
+// A one-shot call (exm_control_cycle, exm_sdf_batch, ...) times its SDF with step_ev and
+// replaces any pending resident accumulation.
+void reset_timing(exm_handle* h, int steps) {
+  h->ring_used = 0;
+  h->ring_ms = 0.0;
+  h->ring_n = 0;
+  h->last_steps = steps;
 }
 
 exm_status check_cloud(const exm_handle* h, const double* pts, int32_t n) {
@@ -729,23 +885,19 @@ exm_status check_guide(const exm_handle* h, const double* g, int32_t n) {
   return EXM_OK;
 }
 
-// EXM_HOST_TIMING=1: per-phase host wall time of exm_control_cycle (stage+enqueue H2D,
-// graph launch + D2H enqueue, wait, unpack), accumulated per handle, printed by exm_destroy.
-bool host_timing() {
-  static const bool on = std::getenv("EXM_HOST_TIMING") && std::getenv("EXM_HOST_TIMING")[0] == '1';
-  return on;
-}
+// EXM_OPT_HOST_TIMING: per-phase host wall time of exm_control_cycle (stage+enqueue H2D,
+// graph launch + D2H enqueue, wait, unpack), accumulated per handle (exm_host_timing).
 struct HostTimer {
   exm_handle* h;
   std::chrono::steady_clock::time_point t0;
   explicit HostTimer(exm_handle* hh) : h(hh) {
-    if (host_timing()) t0 = std::chrono::steady_clock::now();
+    if (h->host_timing) t0 = std::chrono::steady_clock::now();
   }
   void mark(int phase);
 };
 
 void HostTimer::mark(int phase) {
-  if (!host_timing()) return;
+  if (!h->host_timing) return;
   const auto t = std::chrono::steady_clock::now();
   h->host_us[phase] += std::chrono::duration<double, std::micro>(t - t0).count();
   t0 = t;
@@ -776,28 +928,17 @@ exm_status upload_inputs(exm_handle* h, const double q0[3], const double* pts, c
   std::memcpy(h->h_nominal, nominal, TD * sizeof(double));
   std::memcpy(h->h_guide, guide, 2 * static_cast<size_t>(ng) * sizeof(double));
   cudaStream_t s = h->stream;
-  // The cloud goes straight from the caller's buffers (the driver stages pageable memory
-  // while this call returns): measured 10 us per config-2 call faster end to end than a host
-  // memcpy into the pinned mirror plus an async copy (EXM_STAGE=pinned, kept for A/B).
-  static const bool pinned = std::getenv("EXM_STAGE") && !std::strcmp(std::getenv("EXM_STAGE"), "pinned");
+  // The small state (dyn | nominal | guide) goes in one pinned copy; the cloud goes straight from
+  // the caller's buffers (the driver stages pageable memory while this call returns): measured
+  // 10 us per config-2 call faster end to end than a host memcpy into a pinned mirror plus an
+  // async copy, and 2 % faster than page-locked caller buffers (round 1).
   const size_t head0 = static_cast<size_t>(reinterpret_cast<unsigned char*>(h->h_pts) -
                                            reinterpret_cast<unsigned char*>(h->h_dyn));
-  if (!pinned) {
-    EXM_CUDA(cudaMemcpyAsync(h->d_dyn, h->h_dyn, head0, cudaMemcpyHostToDevice, s));
-    if (n > 0)
-      EXM_CUDA(cudaMemcpyAsync(h->d_pts, pts, 2 * static_cast<size_t>(n) * sizeof(double), cudaMemcpyHostToDevice, s));
-    if (mask && n > 0)
-      EXM_CUDA(cudaMemcpyAsync(h->d_mask, mask, static_cast<size_t>(n), cudaMemcpyHostToDevice, s));
-    return EXM_OK;
-  }
-  if (n > 0) std::memcpy(h->h_pts, pts, 2 * static_cast<size_t>(n) * sizeof(double));
-  if (mask && n > 0) std::memcpy(h->h_mask, mask, static_cast<size_t>(n));
-  // dyn | nominal | guide | points share one allocation (same layout pinned and on device):
-  // one H2D copy for all of them, a second one for the mask.
-  const size_t head = head0 + 2 * static_cast<size_t>(n) * sizeof(double);
-  EXM_CUDA(cudaMemcpyAsync(h->d_dyn, h->h_dyn, head, cudaMemcpyHostToDevice, s));
+  EXM_CUDA(cudaMemcpyAsync(h->d_dyn, h->h_dyn, head0, cudaMemcpyHostToDevice, s));
+  if (n > 0)
+    EXM_CUDA(cudaMemcpyAsync(h->d_pts, pts, 2 * static_cast<size_t>(n) * sizeof(double), cudaMemcpyHostToDevice, s));
   if (mask && n > 0)
-    EXM_CUDA(cudaMemcpyAsync(h->d_mask, h->h_mask, static_cast<size_t>(n), cudaMemcpyHostToDevice, s));
+    EXM_CUDA(cudaMemcpyAsync(h->d_mask, mask, static_cast<size_t>(n), cudaMemcpyHostToDevice, s));
   return EXM_OK;
 }
 
@@ -836,10 +977,14 @@ void unpack_decision(exm_handle* h, exm_decision* out, double* nominal_out, doub
 }
 
 exm_status ensure_sdf_workspace(exm_handle* h, int P, int N, bool pairs) {
+  if (!h->sb_center) EXM_CUDA(dalloc(&h->sb_center, 2));
   if (P > h->sb_poses_cap) {
     cudaFree(h->sb_poses);
+    cudaFree(h->sb_poses64);
     cudaFree(h->sb_keys);
     cudaFree(h->sb_min);
+    h->sb_poses_cap = 0;
+    EXM_CUDA(dalloc(&h->sb_poses64, 3 * static_cast<size_t>(P)));
     EXM_CUDA(dalloc(&h->sb_poses, P));
     EXM_CUDA(dalloc(&h->sb_keys, P));
     EXM_CUDA(dalloc(&h->sb_min, P));
@@ -849,6 +994,7 @@ exm_status ensure_sdf_workspace(exm_handle* h, int P, int N, bool pairs) {
     cudaFree(h->sb_pts64);
     cudaFree(h->sb_pts);
     cudaFree(h->sb_mask);
+    h->sb_points_cap = 0;
     EXM_CUDA(dalloc(&h->sb_pts64, 2 * static_cast<size_t>(N)));
     EXM_CUDA(dalloc(&h->sb_pts, N));
     EXM_CUDA(dalloc(&h->sb_mask, N));
@@ -857,6 +1003,7 @@ exm_status ensure_sdf_workspace(exm_handle* h, int P, int N, bool pairs) {
   const size_t np = static_cast<size_t>(P) * N;
   if (pairs && np > h->sb_pairs_cap) {
     cudaFree(h->sb_pairs);
+    h->sb_pairs_cap = 0;
     EXM_CUDA(dalloc(&h->sb_pairs, np));
     h->sb_pairs_cap = np;
   }
@@ -969,7 +1116,7 @@ exm_status exm_create(const exm_footprint* footprint, const exm_model* model,
     unsigned char* d = nullptr;
     unsigned char* hh = nullptr;
     EXM_CUDA_C(dalloc(&d, total));
-    EXM_CUDA_C(halloc(&hh, total));
+    EXM_CUDA_C(halloc(&hh, o_pts));  // pinned mirror of the small state only
     h->d_in_block = d;
     h->h_in_block = hh;
     h->d_dyn = reinterpret_cast<StepDyn*>(d);
@@ -980,8 +1127,8 @@ exm_status exm_create(const exm_footprint* footprint, const exm_model* model,
     h->h_dyn = reinterpret_cast<StepDyn*>(hh);
     h->h_nominal = reinterpret_cast<double*>(hh + o_nom);
     h->h_guide = reinterpret_cast<double*>(hh + o_guide);
-    h->h_pts = reinterpret_cast<double*>(hh + o_pts);
-    h->h_mask = hh + o_mask;
+    h->h_pts = reinterpret_cast<double*>(hh + o_pts);  // end of the pinned mirror (not dereferenced)
+    h->h_mask = nullptr;
   }
   EXM_CUDA_C(alloc_cloud_grid(n_cap, &h->d_grid_block, &h->grid));
   EXM_CUDA_C(dalloc(&h->d_eps, KT * D));
@@ -1024,11 +1171,6 @@ exm_status exm_create(const exm_footprint* footprint, const exm_model* model,
 
 void exm_destroy(exm_handle* h) {
   if (!h) return;
-  if (host_timing() && h->host_calls > 0)
-    std::fprintf(stderr, "[exm host] %lld calls, us/call: stage+H2D %.1f launch %.1f wait %.1f unpack %.1f\n",
-                 static_cast<long long>(h->host_calls), h->host_us[0] / h->host_calls,
-                 h->host_us[1] / h->host_calls, h->host_us[2] / h->host_calls,
-                 h->host_us[3] / h->host_calls);
   cudaSetDevice(h->device);
   if (h->stream) cudaStreamSynchronize(h->stream);
   destroy_graphs(h);
@@ -1038,10 +1180,14 @@ void exm_destroy(exm_handle* h) {
                  h->d_hstat, h->d_cap, h->d_sense, h->d_val_xy, h->d_base, h->d_dmin,
                  h->d_partials, h->d_upd, h->d_val_poses, h->d_val_base, h->d_val_dmin, h->d_out,
                  h->d_controls, h->d_states, h->d_cost, h->d_unsafe, h->sb_poses, h->sb_pts64,
-                 h->sb_pts, h->sb_mask, h->sb_keys, h->sb_min, h->sb_pairs, h->d_nstate};
+                 h->sb_pts, h->sb_mask, h->sb_keys, h->sb_min, h->sb_pairs, h->d_nstate,
+                 h->sb_poses64, h->sb_center, h->bsd_dq, h->bsd_dd};
   for (void* p : dev)
     if (p) cudaFree(p);
-  void* host[] = {h->h_in_block, h->h_out};
+  delete h->pool;
+  for (auto e : h->bsd_ev)
+    if (e) cudaEventDestroy(e);
+  void* host[] = {h->h_in_block, h->h_out, h->bsd_hq, h->bsd_hd};
   for (void* p : host)
     if (p) cudaFreeHost(p);
   for (auto& p : h->ring) {
@@ -1069,6 +1215,8 @@ exm_status exm_control_cycle(exm_handle* h, const double q0[3], const double* pt
                              exm_decision* out) {
   if (!h) return fail(EXM_ERR_INVALID_ARGUMENT, "handle is null");
   if (!nominal_inout || !u_prev_inout) return fail(EXM_ERR_INVALID_ARGUMENT, "null state pointer");
+  std::lock_guard<std::mutex> lk(h->mu);
+  if (h->emulated) return fail(EXM_ERR_INVALID_ARGUMENT, "shard handle without a communicator: use exm_sharded_cycle");
   HostTimer ht(h);
   EXM_CUDA(cudaSetDevice(h->device));
   exm_status st = upload_inputs(h, q0, pts_xy, mask, n_points, guide_xy, n_guide, goal,
@@ -1085,8 +1233,7 @@ exm_status exm_control_cycle(exm_handle* h, const double q0[3], const double* pt
   ht.mark(1);
   EXM_CUDA(cudaStreamSynchronize(h->stream));
   ht.mark(2);
-  h->last_steps = 1;
-  h->ring_used = 0;
+  reset_timing(h, 1);
   h->last_pairs = static_cast<int64_t>(h->sc.k_local) * h->T * n_points;
   unpack_decision(h, out, nominal_inout, u_prev_inout);
   ht.mark(3);
@@ -1100,6 +1247,7 @@ exm_status exm_evaluate_rollouts(exm_handle* h, const double q0[3], const double
                                  double* controls_out, double* states_out, double* dmin_out,
                                  double* costs_out, uint8_t* unsafe_out) {
   if (!h) return fail(EXM_ERR_INVALID_ARGUMENT, "handle is null");
+  std::lock_guard<std::mutex> lk(h->mu);
   if (h->world > 1) return fail(EXM_ERR_UNSUPPORTED, "evaluate_rollouts on a sharded handle");
   if (!eps) return fail(EXM_ERR_INVALID_ARGUMENT, "perturbation array does not match K*T");
   EXM_CUDA(cudaSetDevice(h->device));
@@ -1117,8 +1265,7 @@ exm_status exm_evaluate_rollouts(exm_handle* h, const double q0[3], const double
   EXM_CUDA(launch_rollout(sc, h->d_dyn, h->d_nominal, h->d_eps, 0, h->d_poses, h->d_xy, h->d_base,
                           h->d_ctrl, controls_out ? h->d_controls : nullptr,
                           states_out ? h->d_states : nullptr, s));
-  EXM_CUDA(launch_sdf_grid_capped(h->fp, h->d_poses, static_cast<int>(KT), h->grid, h->d_cap,
-                                  h->T, h->d_dmin, s));
+  if (const exm_status st2 = enqueue_rollout_sdf(h, s); st2 != EXM_OK) return st2;
   EXM_CUDA(launch_rollout_costs(sc, h->d_dyn, h->d_guide, h->guide_cap, h->d_base, h->d_ctrl,
                                 h->d_xy, h->d_dmin, h->d_cost, h->d_unsafe, h->grid.dstat,
                                 nullptr, s));
@@ -1144,6 +1291,7 @@ exm_status exm_evaluate_rollouts(exm_handle* h, const double q0[3], const double
 
 exm_status exm_sample_perturbations(exm_handle* h, uint64_t seed, uint64_t cycle, double* eps_out) {
   if (!h || !eps_out) return fail(EXM_ERR_INVALID_ARGUMENT, "null argument");
+  std::lock_guard<std::mutex> lk(h->mu);
   if (h->world > 1) return fail(EXM_ERR_UNSUPPORTED, "sample_perturbations on a sharded handle");
   EXM_CUDA(cudaSetDevice(h->device));
   StepConst sc = h->sc;
@@ -1164,6 +1312,7 @@ exm_status exm_validate_nominal(exm_handle* h, const double* nominal, const doub
                                 const double* u_prev, int32_t* valid_out, double* dmin_out,
                                 double* cost_out) {
   if (!h) return fail(EXM_ERR_INVALID_ARGUMENT, "handle is null");
+  std::lock_guard<std::mutex> lk(h->mu);
   EXM_CUDA(cudaSetDevice(h->device));
   exm_status st = upload_inputs(h, q0, pts_xy, mask, n_points, guide_xy, n_guide, goal, nominal,
                                 u_prev, 0);
@@ -1173,8 +1322,8 @@ exm_status exm_validate_nominal(exm_handle* h, const double* nominal, const doub
   EXM_CUDA(launch_cloud_prep(h->d_pts, h->d_mask, h->d_dyn, h->fp.radius, h->grid, h->n_cap, s));
   EXM_CUDA(launch_update(sc, nullptr, h->d_nominal, h->d_dyn, h->d_upd, h->d_val_poses,
                          h->d_val_xy, h->d_val_base, out_dec(h), 0, s));
-  EXM_CUDA(launch_sdf_grid(h->fp, h->d_val_poses, sc.T, h->grid,
-                           h->d_val_dmin, s));
+  EXM_CUDA(launch_sdf_grid(h->fp, h->d_val_poses, sc.T, 0, h->grid, nullptr, h->sdf_mode,
+                           h->d_val_dmin, &h->val_path, nullptr, s));
   EXM_CUDA(launch_finalize(sc, h->d_val_dmin, h->d_val_xy, h->d_val_base, h->d_upd, h->d_guide,
                            h->guide_cap, h->d_nominal, h->d_dyn, out_dec(h), out_dmin(h), nullptr,
                            nullptr, 0, nullptr, nullptr, h->fp.radius, s));
@@ -1187,67 +1336,55 @@ exm_status exm_validate_nominal(exm_handle* h, const double* nominal, const doub
   return EXM_OK;
 }
 
-exm_status exm_sdf_stage(exm_handle* h, const double* poses, int32_t n_poses,
-                         const double* pts_xy, const uint8_t* mask, int32_t n_points) {
-  if (!h) return fail(EXM_ERR_INVALID_ARGUMENT, "handle is null");
+}  // extern "C"
+
+namespace {
+
+// exm_sdf_stage without the lock: poses and points go to the device as the caller's FP64 arrays
+// (pageable copies return once the driver has staged them), the device takes the poses'
+// centroid, recentres both in FP64 and rounds once. No host loop, no sync.
+exm_status sdf_stage(exm_handle* h, const double* poses, int32_t n_poses, const double* pts_xy,
+                     const uint8_t* mask, int32_t n_points) {
   if (n_poses < 0 || n_points < 0 || (n_poses > 0 && !poses) || (n_points > 0 && !pts_xy))
     return fail(EXM_ERR_INVALID_ARGUMENT, "bad pose/point arrays");
   EXM_CUDA(cudaSetDevice(h->device));
   exm_status st = ensure_sdf_workspace(h, std::max(n_poses, 1), std::max(n_points, 1), false);
   if (st != EXM_OK) return st;
-  // Recentre poses and points at the poses' centroid in FP64, then round (Appendix B).
-  double cx = 0.0, cy = 0.0;
-  for (int p = 0; p < n_poses; ++p) {
-    cx += poses[3 * p];
-    cy += poses[3 * p + 1];
-  }
-  if (n_poses > 0) {
-    cx /= n_poses;
-    cy /= n_poses;
-  }
-  std::vector<float4> q(static_cast<size_t>(n_poses));
-  for (int p = 0; p < n_poses; ++p) {
-    const double th = poses[3 * p + 2];
-    q[p] = make_float4(static_cast<float>(poses[3 * p] - cx), static_cast<float>(poses[3 * p + 1] - cy),
-                       static_cast<float>(std::cos(th)), static_cast<float>(std::sin(th)));
-  }
   cudaStream_t s = h->stream;
   if (n_poses > 0)
-    EXM_CUDA(cudaMemcpyAsync(h->sb_poses, q.data(), q.size() * sizeof(float4), cudaMemcpyHostToDevice, s));
+    EXM_CUDA(cudaMemcpyAsync(h->sb_poses64, poses, 3 * static_cast<size_t>(n_poses) * sizeof(double),
+                             cudaMemcpyHostToDevice, s));
   if (n_points > 0)
     EXM_CUDA(cudaMemcpyAsync(h->sb_pts64, pts_xy, 2 * static_cast<size_t>(n_points) * sizeof(double),
                              cudaMemcpyHostToDevice, s));
   if (mask && n_points > 0)
     EXM_CUDA(cudaMemcpyAsync(h->sb_mask, mask, static_cast<size_t>(n_points), cudaMemcpyHostToDevice, s));
-  EXM_CUDA(launch_recentre(h->sb_pts64, n_points, cx, cy, h->sb_pts, s));
-  EXM_CUDA(cudaStreamSynchronize(s));  // q is a stack vector
+  EXM_CUDA(launch_pose_prep(h->sb_poses64, n_poses, h->sb_center, h->sb_poses, s));
+  EXM_CUDA(launch_recentre(h->sb_pts64, n_points, h->sb_center, h->sb_pts, s));
   h->sb_P = n_poses;
   h->sb_N = n_points;
   h->sb_has_mask = mask ? 1 : 0;
   return EXM_OK;
 }
 
-exm_status exm_sdf_run_resident(exm_handle* h, int32_t n_steps, int32_t want_pairs) {
-  if (!h) return fail(EXM_ERR_INVALID_ARGUMENT, "handle is null");
+exm_status sdf_run(exm_handle* h, int32_t n_steps, bool want_pairs, bool resident) {
   EXM_CUDA(cudaSetDevice(h->device));
-  exm_status st = ensure_sdf_workspace(h, std::max(h->sb_P, 1), std::max(h->sb_N, 1), want_pairs != 0);
+  exm_status st = ensure_sdf_workspace(h, std::max(h->sb_P, 1), std::max(h->sb_N, 1), want_pairs);
   if (st != EXM_OK) return st;
-  st = ensure_ring(h, h->ring_used + n_steps);
-  if (st != EXM_OK) return st;
+  if (!resident) reset_timing(h, 1);
   for (int i = 0; i < n_steps; ++i) {
-    st = sdf_enqueue(h, want_pairs != 0, &h->ring[h->ring_used + i]);
-    if (st != EXM_OK) return st;
+    EventPair* ev = &h->step_ev;
+    if (resident && (st = next_ring_slot(h, &ev)) != EXM_OK) return st;
+    if ((st = sdf_enqueue(h, want_pairs, ev)) != EXM_OK) return st;
   }
-  h->ring_used += n_steps;
-  h->last_steps = n_steps;
-  h->sb_last_pairs = want_pairs != 0;
+  if (resident) h->last_steps = n_steps;
+  h->sb_last_pairs = want_pairs ? 1 : 0;
   h->launches_per_step = 3;
   h->last_pairs = static_cast<int64_t>(h->sb_P) * h->sb_N;
   return EXM_OK;
 }
 
-exm_status exm_sdf_read(exm_handle* h, float* per_pair, double* per_pose_min) {
-  if (!h) return fail(EXM_ERR_INVALID_ARGUMENT, "handle is null");
+exm_status sdf_read(exm_handle* h, float* per_pair, double* per_pose_min) {
   EXM_CUDA(cudaSetDevice(h->device));
   cudaStream_t s = h->stream;
   if (per_pair) {
@@ -1262,24 +1399,131 @@ exm_status exm_sdf_read(exm_handle* h, float* per_pair, double* per_pose_min) {
   return EXM_OK;
 }
 
+int default_host_threads() {
+  const unsigned hw = std::thread::hardware_concurrency();
+  return static_cast<int>(std::max(1u, std::min(8u, hw ? hw : 1u)));
+}
+
+// Pipeline buffers of batch_signed_distance for chunks of `chunk` queries (grown on demand).
+exm_status ensure_bsd(exm_handle* h, int chunk) {
+  const int threads = h->host_threads > 0 ? h->host_threads : default_host_threads();
+  if (!h->pool || h->pool->size() != threads) {
+    delete h->pool;
+    h->pool = new HostPool(threads - 1);
+  }
+  if (chunk <= h->bsd_chunk) return EXM_OK;
+  cudaFreeHost(h->bsd_hq);
+  cudaFreeHost(h->bsd_hd);
+  cudaFree(h->bsd_dq);
+  cudaFree(h->bsd_dd);
+  h->bsd_hq = nullptr;
+  h->bsd_hd = nullptr;
+  h->bsd_dq = nullptr;
+  h->bsd_dd = nullptr;
+  h->bsd_chunk = 0;
+  const size_t n = static_cast<size_t>(chunk) * kBsdSlots;
+  EXM_CUDA(halloc(&h->bsd_hq, n));
+  EXM_CUDA(halloc(&h->bsd_hd, n));
+  EXM_CUDA(dalloc(&h->bsd_dq, n));
+  EXM_CUDA(dalloc(&h->bsd_dd, n));
+  for (auto& e : h->bsd_ev)
+    if (!e) EXM_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  h->bsd_chunk = chunk;
+  return EXM_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+exm_status exm_sdf_stage(exm_handle* h, const double* poses, int32_t n_poses,
+                         const double* pts_xy, const uint8_t* mask, int32_t n_points) {
+  if (!h) return fail(EXM_ERR_INVALID_ARGUMENT, "handle is null");
+  std::lock_guard<std::mutex> lk(h->mu);
+  return sdf_stage(h, poses, n_poses, pts_xy, mask, n_points);
+}
+
+exm_status exm_sdf_run_resident(exm_handle* h, int32_t n_steps, int32_t want_pairs) {
+  if (!h) return fail(EXM_ERR_INVALID_ARGUMENT, "handle is null");
+  std::lock_guard<std::mutex> lk(h->mu);
+  return sdf_run(h, n_steps, want_pairs != 0, true);
+}
+
+exm_status exm_sdf_read(exm_handle* h, float* per_pair, double* per_pose_min) {
+  if (!h) return fail(EXM_ERR_INVALID_ARGUMENT, "handle is null");
+  std::lock_guard<std::mutex> lk(h->mu);
+  return sdf_read(h, per_pair, per_pose_min);
+}
+
 exm_status exm_sdf_batch(exm_handle* h, const double* poses, int32_t n_poses,
                          const double* pts_xy, const uint8_t* mask, int32_t n_points,
                          float* per_pair, double* per_pose_min) {
-  exm_status st = exm_sdf_stage(h, poses, n_poses, pts_xy, mask, n_points);
+  if (!h) return fail(EXM_ERR_INVALID_ARGUMENT, "handle is null");
+  std::lock_guard<std::mutex> lk(h->mu);
+  exm_status st = sdf_stage(h, poses, n_poses, pts_xy, mask, n_points);
   if (st != EXM_OK) return st;
-  st = exm_sdf_run_resident(h, 1, per_pair != nullptr);
+  st = sdf_run(h, 1, per_pair != nullptr, false);
   if (st != EXM_OK) return st;
-  return exm_sdf_read(h, per_pair, per_pose_min);
+  return sdf_read(h, per_pair, per_pose_min);
 }
 
+// batch_signed_distance as a host-to-host pipeline: chunks of queries are rounded to FP32 into
+// pinned staging by the host pool while earlier chunks are copied, evaluated (k_sdf_points) and
+// copied back; results are widened to FP64 into the caller's array as their chunks complete.
+// Host traffic per query: 16 B read + 8 B pinned write in, 4 B pinned read + 8 B write out; link
+// traffic 8 B in + 4 B out.
 exm_status exm_batch_signed_distance(exm_handle* h, const double* queries, int32_t n, double* out) {
   if (!h || (n > 0 && (!queries || !out))) return fail(EXM_ERR_INVALID_ARGUMENT, "null argument");
+  if (n < 0) return fail(EXM_ERR_INVALID_ARGUMENT, "negative query count");
   if (n == 0) return EXM_OK;
-  const double identity[3] = {0.0, 0.0, 0.0};
-  std::vector<float> tmp(static_cast<size_t>(n));
-  exm_status st = exm_sdf_batch(h, identity, 1, queries, nullptr, n, tmp.data(), nullptr);
+  std::lock_guard<std::mutex> lk(h->mu);
+  EXM_CUDA(cudaSetDevice(h->device));
+  // about 8 chunks per call (pipeline depth), 16k..256k queries each
+  const int chunk = std::min(std::max((n + 7) / 8, 16384), 262144);
+  exm_status st = ensure_bsd(h, chunk);
   if (st != EXM_OK) return st;
-  for (int i = 0; i < n; ++i) out[i] = static_cast<double>(tmp[i]);
+  const int nchunks = (n + chunk - 1) / chunk;
+  const int parts = h->pool->size();
+  cudaStream_t s = h->stream;
+  auto to_f32 = [&](int c, int part) {  // queries of chunk c -> pinned slot, piece `part`
+    const size_t c0 = static_cast<size_t>(c) * chunk;
+    const size_t m = std::min<size_t>(chunk, static_cast<size_t>(n) - c0);
+    const size_t a = m * part / parts, b = m * (part + 1) / parts;
+    float2* dst = h->bsd_hq + static_cast<size_t>(c % kBsdSlots) * chunk;
+    const double* src = queries + 2 * c0;
+    for (size_t i = a; i < b; ++i)
+      dst[i] = make_float2(static_cast<float>(src[2 * i]), static_cast<float>(src[2 * i + 1]));
+  };
+  auto to_f64 = [&](int c, int part) {  // results of chunk c -> caller, piece `part`
+    const size_t c0 = static_cast<size_t>(c) * chunk;
+    const size_t m = std::min<size_t>(chunk, static_cast<size_t>(n) - c0);
+    const size_t a = m * part / parts, b = m * (part + 1) / parts;
+    const float* src = h->bsd_hd + static_cast<size_t>(c % kBsdSlots) * chunk;
+    for (size_t i = a; i < b; ++i) out[c0 + i] = static_cast<double>(src[i]);
+  };
+  for (int c = 0; c <= nchunks; ++c) {
+    // the slot chunk c reuses held chunk c - kBsdSlots: drain it first
+    const int drain = c - kBsdSlots;
+    const int last = c == nchunks;
+    if (drain >= 0) EXM_CUDA(cudaEventSynchronize(h->bsd_ev[drain % kBsdSlots]));
+    if (last) break;
+    h->pool->run(2 * parts, [&](int t) {
+      if (t < parts) to_f32(c, t);
+      else if (drain >= 0) to_f64(drain, t - parts);
+    });
+    const size_t c0 = static_cast<size_t>(c) * chunk;
+    const int m = static_cast<int>(std::min<size_t>(chunk, static_cast<size_t>(n) - c0));
+    const size_t so = static_cast<size_t>(c % kBsdSlots) * chunk;
+    EXM_CUDA(cudaMemcpyAsync(h->bsd_dq + so, h->bsd_hq + so, m * sizeof(float2), cudaMemcpyHostToDevice, s));
+    EXM_CUDA(launch_sdf_points(h->fp, h->bsd_dq + so, m, h->bsd_dd + so, s));
+    EXM_CUDA(cudaMemcpyAsync(h->bsd_hd + so, h->bsd_dd + so, m * sizeof(float), cudaMemcpyDeviceToHost, s));
+    EXM_CUDA(cudaEventRecord(h->bsd_ev[c % kBsdSlots], s));
+  }
+  // the last min(kBsdSlots, nchunks) chunks
+  for (int c = std::max(0, nchunks - kBsdSlots); c < nchunks; ++c) {
+    EXM_CUDA(cudaEventSynchronize(h->bsd_ev[c % kBsdSlots]));
+    h->pool->run(parts, [&](int t) { to_f64(c, t); });
+  }
   return EXM_OK;
 }
 
@@ -1295,9 +1539,11 @@ exm_status exm_nccl_unique_id(uint8_t id_out[128]) {
 
 exm_status exm_attach_comm(exm_handle* h, int32_t rank, int32_t world, const uint8_t id[128]) {
   if (!h) return fail(EXM_ERR_INVALID_ARGUMENT, "handle is null");
+  std::lock_guard<std::mutex> lk(h->mu);
   if (world < 1 || rank < 0 || rank >= world) return fail(EXM_ERR_INVALID_ARGUMENT, "bad rank/world");
-  if (h->K % (world * kBlockRollouts) != 0 && world > 1)
+  if (world > 1 && h->K % (world * kBlockRollouts) != 0)
     return fail(EXM_ERR_INVALID_ARGUMENT, "rollouts must be a multiple of 256 * world for sharding");
+  if (world > 1 && !id) return fail(EXM_ERR_INVALID_ARGUMENT, "null id");
   EXM_CUDA(cudaSetDevice(h->device));
   EXM_CUDA(cudaStreamSynchronize(h->stream));
   destroy_graphs(h);
@@ -1307,16 +1553,108 @@ exm_status exm_attach_comm(exm_handle* h, int32_t rank, int32_t world, const uin
   }
   h->rank = rank;
   h->world = world;
-  if (world > 1) {
-    if (!id) return fail(EXM_ERR_INVALID_ARGUMENT, "null id");
+  h->emulated = false;
+  if (id) {  // any world, a 1-rank communicator included: the step graph then holds the all-gather
     if (!g_nccl.load()) return fail(EXM_ERR_NCCL, "libnccl.so.2 not loadable");
     nccl_uid_t uid;
     std::memcpy(uid.internal, id, 128);
     const int rc = g_nccl.init_rank(&h->comm, world, uid, rank);
-    if (rc != 0) return fail(EXM_ERR_NCCL, "ncclCommInitRank failed");
+    if (rc != 0) {
+      h->comm = nullptr;
+      h->rank = 0;
+      h->world = 1;
+      set_shard(h);
+      return fail(EXM_ERR_NCCL, std::string("ncclCommInitRank: ") + (g_nccl.errstr ? g_nccl.errstr(rc) : "failed"));
+    }
   }
   set_shard(h);
   return invalidate_pregen(h);  // the shard (and so the noise rows eps holds) changed
+}
+
+exm_status exm_set_shard(exm_handle* h, int32_t rank, int32_t world) {
+  if (!h) return fail(EXM_ERR_INVALID_ARGUMENT, "handle is null");
+  std::lock_guard<std::mutex> lk(h->mu);
+  if (world < 1 || rank < 0 || rank >= world) return fail(EXM_ERR_INVALID_ARGUMENT, "bad rank/world");
+  if (world > 1 && h->K % (world * kBlockRollouts) != 0)
+    return fail(EXM_ERR_INVALID_ARGUMENT, "rollouts must be a multiple of 256 * world for sharding");
+  if (h->comm) return fail(EXM_ERR_INVALID_ARGUMENT, "handle has a communicator attached");
+  EXM_CUDA(cudaSetDevice(h->device));
+  EXM_CUDA(cudaStreamSynchronize(h->stream));
+  destroy_graphs(h);
+  h->rank = rank;
+  h->world = world;
+  h->emulated = world > 1;
+  set_shard(h);
+  return invalidate_pregen(h);
+}
+
+exm_status exm_sharded_cycle(exm_handle* const* shards, int32_t n_shards, const double q0[3],
+                             const double* pts_xy, const uint8_t* mask, int32_t n_points,
+                             const double* guide_xy, int32_t n_guide, const double goal[3],
+                             double* nominals_inout, double* u_prevs_inout, uint64_t cycle,
+                             const double* eps_or_null, exm_decision* out) {
+  if (!shards || n_shards < 1 || !nominals_inout || !u_prevs_inout)
+    return fail(EXM_ERR_INVALID_ARGUMENT, "null argument");
+  const int G = n_shards;
+  for (int g = 0; g < G; ++g) {
+    const exm_handle* h = shards[g];
+    if (!h) return fail(EXM_ERR_INVALID_ARGUMENT, "handle is null");
+    if (h->rank != g || h->world != G || h->comm)
+      return fail(EXM_ERR_INVALID_ARGUMENT, "shard g must be set to rank g of n_shards (exm_set_shard)");
+    if (h->device != shards[0]->device || h->K != shards[0]->K || h->T != shards[0]->T ||
+        h->D != shards[0]->D)
+      return fail(EXM_ERR_INVALID_ARGUMENT, "shards differ in device or configuration");
+  }
+  std::vector<std::unique_lock<std::mutex>> locks;
+  for (int g = 0; g < G; ++g) locks.emplace_back(shards[g]->mu);
+  EXM_CUDA(cudaSetDevice(shards[0]->device));
+  const size_t TD = static_cast<size_t>(shards[0]->T) * shards[0]->D;
+  const bool draw = eps_or_null == nullptr;
+  // 1. each shard: inputs, head (prep || rollout -> SDF) and its block partials, on its stream
+  for (int g = 0; g < G; ++g) {
+    exm_handle* h = shards[g];
+    exm_status st = upload_inputs(h, q0, pts_xy, mask, n_points, guide_xy, n_guide, goal,
+                                  nominals_inout + g * TD, u_prevs_inout + 3 * g, cycle);
+    if (st != EXM_OK) return st;
+    if (eps_or_null && (st = upload_eps(h, eps_or_null)) != EXM_OK) return st;
+    int launches = 0;
+    if ((st = enqueue_head(h, draw, nullptr, h->stream, false, &launches)) != EXM_OK) return st;
+    if ((st = enqueue_post_a(h, h->stream, &launches, pregen_for(h, draw))) != EXM_OK) return st;
+    EXM_CUDA(cudaEventRecord(h->fork_ev, h->stream));
+  }
+  // 2. the exchange the ranks' all-gather performs: every shard receives every other shard's
+  //    blocks, one device-to-device copy per 256-rollout block
+  for (int g = 0; g < G; ++g) {
+    exm_handle* h = shards[g];
+    const size_t stride = static_cast<size_t>(partial_stride(h->T, h->D)) * sizeof(double);
+    for (int o = 0; o < G; ++o) {
+      if (o == g) continue;
+      const exm_handle* src = shards[o];
+      EXM_CUDA(cudaStreamWaitEvent(h->stream, src->fork_ev, 0));
+      for (int b = 0; b < src->sc.nblocks_local; ++b) {
+        const size_t blk = static_cast<size_t>(src->sc.block_offset + b);
+        EXM_CUDA(cudaMemcpyAsync(reinterpret_cast<char*>(h->d_partials) + blk * stride,
+                                 reinterpret_cast<const char*>(src->d_partials) + blk * stride,
+                                 stride, cudaMemcpyDeviceToDevice, h->stream));
+      }
+    }
+  }
+  // 3. each shard: merge, update, validation, finalize; decision back
+  for (int g = 0; g < G; ++g) {
+    exm_handle* h = shards[g];
+    int launches = 0;
+    exm_status st = enqueue_post_b(h, h->stream, &launches);
+    if (st != EXM_OK) return st;
+    if (pregen_for(h, draw)) EXM_CUDA(cudaStreamWaitEvent(h->stream, h->pg_join, 0));
+    EXM_CUDA(cudaMemcpyAsync(h->h_out, h->d_out, h->out_bytes, cudaMemcpyDeviceToHost, h->stream));
+  }
+  for (int g = 0; g < G; ++g) {
+    exm_handle* h = shards[g];
+    EXM_CUDA(cudaStreamSynchronize(h->stream));
+    h->last_steps = 0;
+    unpack_decision(h, out ? out + g : nullptr, nominals_inout + g * TD, u_prevs_inout + 3 * g);
+  }
+  return EXM_OK;
 }
 
 exm_status exm_stage_inputs(exm_handle* h, const double q0[3], const double* pts_xy,
@@ -1324,6 +1662,7 @@ exm_status exm_stage_inputs(exm_handle* h, const double q0[3], const double* pts
                             int32_t n_guide, const double goal[3], const double* nominal,
                             const double* u_prev, uint64_t cycle) {
   if (!h) return fail(EXM_ERR_INVALID_ARGUMENT, "handle is null");
+  std::lock_guard<std::mutex> lk(h->mu);
   EXM_CUDA(cudaSetDevice(h->device));
   exm_status st = upload_inputs(h, q0, pts_xy, mask, n_points, guide_xy, n_guide, goal, nominal,
                                 u_prev, cycle);
@@ -1334,14 +1673,15 @@ exm_status exm_stage_inputs(exm_handle* h, const double q0[3], const double* pts
 
 exm_status exm_run_resident(exm_handle* h, int32_t n_steps) {
   if (!h) return fail(EXM_ERR_INVALID_ARGUMENT, "handle is null");
+  std::lock_guard<std::mutex> lk(h->mu);
+  if (h->emulated) return fail(EXM_ERR_INVALID_ARGUMENT, "shard handle without a communicator: use exm_sharded_cycle");
   EXM_CUDA(cudaSetDevice(h->device));
-  exm_status st = ensure_ring(h, h->ring_used + n_steps);
-  if (st != EXM_OK) return st;
   for (int i = 0; i < n_steps; ++i) {
-    st = launch_graph(h, 0, h->ring[h->ring_used + i]);
+    EventPair* ev = nullptr;
+    exm_status st = next_ring_slot(h, &ev);
     if (st != EXM_OK) return st;
+    if ((st = launch_graph(h, 0, *ev)) != EXM_OK) return st;
   }
-  h->ring_used += n_steps;
   h->last_steps = n_steps;
   h->last_pairs = static_cast<int64_t>(h->sc.k_local) * h->T * h->h_dyn->n_points;
   return EXM_OK;
@@ -1349,6 +1689,7 @@ exm_status exm_run_resident(exm_handle* h, int32_t n_steps) {
 
 exm_status exm_read_resident(exm_handle* h, double* nominal_out, double* u_prev_out, exm_decision* out) {
   if (!h) return fail(EXM_ERR_INVALID_ARGUMENT, "handle is null");
+  std::lock_guard<std::mutex> lk(h->mu);
   EXM_CUDA(cudaSetDevice(h->device));
   EXM_CUDA(cudaMemcpyAsync(h->h_out, h->d_out, h->out_bytes, cudaMemcpyDeviceToHost, h->stream));
   EXM_CUDA(cudaStreamSynchronize(h->stream));
@@ -1366,6 +1707,7 @@ exm_status exm_sense(exm_handle* h, const exm_world_obstacle* obstacles, int32_t
   if (!h || !robot || !pts_out || !mask_out || (n_obstacles > 0 && !obstacles))
     return fail(EXM_ERR_INVALID_ARGUMENT, "null argument");
   if (budget < 1) return fail(EXM_ERR_INVALID_ARGUMENT, "sensor budget must be >= 1");
+  std::lock_guard<std::mutex> lk(h->mu);
   constexpr double kSpacing = 0.05;  // kBoundarySpacing, world.cpp:15
   std::vector<SenseSeg> seg;
   std::vector<SenseObs> obs(static_cast<size_t>(n_obstacles));
@@ -1461,6 +1803,7 @@ exm_status exm_sense(exm_handle* h, const exm_world_obstacle* obstacles, int32_t
 
 exm_status exm_set_sdf_caps(exm_handle* h, const float* caps) {
   if (!h || !caps) return fail(EXM_ERR_INVALID_ARGUMENT, "null argument");
+  std::lock_guard<std::mutex> lk(h->mu);
   EXM_CUDA(cudaSetDevice(h->device));
   EXM_CUDA(cudaMemcpyAsync(h->d_cap, caps, sizeof(float) * h->T, cudaMemcpyHostToDevice, h->stream));
   EXM_CUDA(cudaStreamSynchronize(h->stream));
@@ -1481,47 +1824,111 @@ exm_status exm_footprint_cull_boxes(const exm_footprint* fp, float* aabb_out, fl
   return EXM_OK;
 }
 
-exm_status exm_sdf_cull_stats(exm_handle* h, int64_t* points_tested, int64_t* sdf_evaluated) {
-  if (!h) return fail(EXM_ERR_INVALID_ARGUMENT, "handle is null");
+exm_status exm_sdf_work_stats(exm_handle* h, int64_t* counts) {
+  if (!h || !counts) return fail(EXM_ERR_INVALID_ARGUMENT, "null argument");
+  std::lock_guard<std::mutex> lk(h->mu);
   EXM_CUDA(cudaSetDevice(h->device));
   unsigned long long* d = nullptr;
-  EXM_CUDA(dalloc(&d, 2));
-  unsigned long long hv[2] = {0, 0};
+  EXM_CUDA(dalloc(&d, kCntN));
+  unsigned long long hv[kCntN] = {};
   cudaStream_t s = h->stream;
-  cudaError_t e = cudaMemsetAsync(d, 0, 2 * sizeof(unsigned long long), s);
+  cudaError_t e = cudaMemsetAsync(d, 0, kCntN * sizeof(unsigned long long), s);
   if (e == cudaSuccess)
-    e = launch_sdf_grid_stats(h->fp, h->d_poses, h->sc.k_local * h->T, h->grid, h->d_cap, h->T,
-                              h->d_dmin, d, s);
+    e = launch_sdf_grid(h->fp, h->d_poses, h->sc.k_local * h->T, h->T, h->grid, h->d_cap,
+                        h->sdf_mode, h->d_dmin, nullptr, d, s);
   if (e == cudaSuccess) e = cudaMemcpyAsync(hv, d, sizeof hv, cudaMemcpyDeviceToHost, s);
   if (e == cudaSuccess) e = cudaStreamSynchronize(s);
   cudaFree(d);
   if (e != cudaSuccess) return fail(EXM_ERR_CUDA, std::string("cull stats: ") + cudaGetErrorString(e));
-  if (points_tested) *points_tested = static_cast<int64_t>(hv[0]);
-  if (sdf_evaluated) *sdf_evaluated = static_cast<int64_t>(hv[1]);
+  for (int k = 0; k < kCntN; ++k) counts[k] = static_cast<int64_t>(hv[k]);
+  return EXM_OK;
+}
+
+exm_status exm_sdf_cull_stats(exm_handle* h, int64_t* points_tested, int64_t* sdf_evaluated) {
+  int64_t c[kCntN];
+  const exm_status st = exm_sdf_work_stats(h, c);
+  if (st != EXM_OK) return st;
+  if (points_tested) *points_tested = c[kCntPoint];
+  if (sdf_evaluated) *sdf_evaluated = c[kCntTileVal] + c[kCntEdges];
+  return EXM_OK;
+}
+
+exm_status exm_set_option(exm_handle* h, int32_t option, int32_t value) {
+  if (!h) return fail(EXM_ERR_INVALID_ARGUMENT, "handle is null");
+  std::lock_guard<std::mutex> lk(h->mu);
+  EXM_CUDA(cudaSetDevice(h->device));
+  EXM_CUDA(cudaStreamSynchronize(h->stream));
+  switch (option) {
+    case EXM_OPT_SDF_MODE:
+      if (value < kSdfAuto || value > kSdfNoCap) return fail(EXM_ERR_INVALID_ARGUMENT, "unknown SDF mode");
+      h->sdf_mode = value;
+      break;
+    case EXM_OPT_AUTO_CAPS: h->auto_caps = value != 0; break;
+    case EXM_OPT_PREGEN: h->pregen = value != 0; break;
+    case EXM_OPT_HOST_TIMING:
+      h->host_timing = value != 0;
+      for (double& u : h->host_us) u = 0.0;
+      h->host_calls = 0;
+      return EXM_OK;
+    case EXM_OPT_HOST_THREADS:
+      if (value < 0 || value > 256) return fail(EXM_ERR_INVALID_ARGUMENT, "host threads out of range");
+      h->host_threads = value;
+      return EXM_OK;
+    default: return fail(EXM_ERR_INVALID_ARGUMENT, "unknown option");
+  }
+  destroy_graphs(h);  // the captured steps depend on the options
+  return invalidate_pregen(h);
+}
+
+exm_status exm_host_timing(exm_handle* h, double us_per_call[4], int64_t* calls) {
+  if (!h) return fail(EXM_ERR_INVALID_ARGUMENT, "handle is null");
+  std::lock_guard<std::mutex> lk(h->mu);
+  for (int i = 0; i < 4; ++i)
+    if (us_per_call) us_per_call[i] = h->host_calls ? h->host_us[i] / h->host_calls : 0.0;
+  if (calls) *calls = h->host_calls;
+  return EXM_OK;
+}
+
+exm_status exm_last_sdf_path(exm_handle* h, exm_sdf_path* rollout, exm_sdf_path* validation) {
+  if (!h) return fail(EXM_ERR_INVALID_ARGUMENT, "handle is null");
+  std::lock_guard<std::mutex> lk(h->mu);
+  auto put = [](const SdfPath& p, exm_sdf_path* o) {
+    if (!o) return;
+    o->kernel = p.kernel;
+    o->chunk = p.chunk;
+    o->persistent = p.persistent;
+    o->ctas = p.ctas;
+    o->threads = p.threads;
+    o->hmajor = p.hmajor;
+  };
+  put(h->roll_path, rollout);
+  put(h->val_path, validation);
   return EXM_OK;
 }
 
 exm_status exm_step_stats(exm_handle* h, int32_t* launches_per_step, float* sdf_ms,
                           int64_t* sdf_pairs) {
   if (!h) return fail(EXM_ERR_INVALID_ARGUMENT, "handle is null");
+  std::lock_guard<std::mutex> lk(h->mu);
   EXM_CUDA(cudaSetDevice(h->device));
   EXM_CUDA(cudaStreamSynchronize(h->stream));
-  float total = 0.0f;
-  int n = 0;
-  if (h->ring_used > 0) {
-    for (int i = 0; i < h->ring_used; ++i) {
-      float ms = 0.0f;
-      EXM_CUDA(cudaEventElapsedTime(&ms, h->ring[i].a, h->ring[i].b));
-      total += ms;
-      ++n;
-    }
-  } else if (h->last_steps > 0) {
-    EXM_CUDA(cudaEventElapsedTime(&total, h->step_ev.a, h->step_ev.b));
+  double total = h->ring_ms;
+  int n = h->ring_n;
+  for (int i = 0; i < h->ring_used; ++i) {
+    float ms = 0.0f;
+    EXM_CUDA(cudaEventElapsedTime(&ms, h->ring[i].a, h->ring[i].b));
+    total += ms;
+    ++n;
+  }
+  if (n == 0 && h->last_steps > 0) {
+    float ms = 0.0f;
+    EXM_CUDA(cudaEventElapsedTime(&ms, h->step_ev.a, h->step_ev.b));
+    total = ms;
     n = 1;
   }
   if (launches_per_step) *launches_per_step = h->launches_per_step;
-  if (sdf_ms) *sdf_ms = n ? total / n : 0.0f;
-  h->ring_used = 0;  // consumed: the next run starts a fresh accumulation
+  if (sdf_ms) *sdf_ms = n ? static_cast<float>(total / n) : 0.0f;
+  reset_timing(h, 0);  // consumed: the next run starts a fresh accumulation
   if (sdf_pairs) *sdf_pairs = h->last_pairs;
   return EXM_OK;
 }
@@ -1530,6 +1937,7 @@ exm_status exm_step_stats(exm_handle* h, int32_t* launches_per_step, float* sdf_
 
 // =========================================================================== hybrid families
 struct exm_hybrid {
+  std::mutex mu;  // calls on one hybrid handle serialise
   int M = 0, K = 0, T = 0, device = 0;
   std::vector<exm_handle*> fam;
   float4* poses_all = nullptr;  // [m][r][h]
@@ -1560,8 +1968,8 @@ exm_status hybrid_enqueue(exm_hybrid* hy, cudaStream_t s0) {
   }
   for (int m = 1; m < hy->M; ++m) EXM_CUDA(cudaStreamWaitEvent(s0, hy->pre_done[m], 0));
   EXM_CUDA(cudaStreamWaitEvent(s0, hy->prep_done, 0));
-  EXM_CUDA(launch_sdf_grid(f0->fp, hy->poses_all, hy->M * hy->K * hy->T, f0->grid, hy->dmin_all,
-                           s0));
+  EXM_CUDA(launch_sdf_grid(f0->fp, hy->poses_all, hy->M * hy->K * hy->T, hy->T, f0->grid,
+                           nullptr, f0->sdf_mode, hy->dmin_all, &f0->roll_path, nullptr, s0));
   EXM_CUDA(cudaEventRecord(hy->sdf_done, s0));
   for (int m = 0; m < hy->M; ++m) {
     cudaStream_t sm = m == 0 ? s0 : hy->fam[m]->stream;
@@ -1663,6 +2071,7 @@ exm_status exm_hybrid_cycle(exm_hybrid* hy, const double q0[3], const double* pt
                             double* u_prev_inout, uint64_t cycle, exm_decision* out) {
   if (!hy) return fail(EXM_ERR_INVALID_ARGUMENT, "hybrid handle is null");
   if (!nominals_inout || !u_prev_inout) return fail(EXM_ERR_INVALID_ARGUMENT, "null state pointer");
+  std::lock_guard<std::mutex> lk(hy->mu);
   EXM_CUDA(cudaSetDevice(hy->device));
   exm_handle* f0 = hy->fam[0];
   cudaStream_t s0 = f0->stream;
@@ -1699,8 +2108,7 @@ exm_status exm_hybrid_cycle(exm_hybrid* hy, const double q0[3], const double* pt
   EXM_CUDA(cudaStreamSynchronize(s0));
   for (int m = 0; m < hy->M; ++m) {
     exm_handle* h = hy->fam[m];
-    h->last_steps = 1;
-    h->ring_used = 0;
+    reset_timing(h, 1);
     unpack_decision(h, out ? out + m : nullptr, nominals_inout + m * stride, u_prev_inout + 3 * m);
   }
   return EXM_OK;

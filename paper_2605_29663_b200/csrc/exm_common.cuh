@@ -144,14 +144,49 @@ struct DecisionDev {
 //   {beta_b, S_b = sum e, A_b = sum e (J - beta_b)/lambda, argmin_b, U_b[T*D] = sum e eps}
 inline __host__ __device__ int partial_stride(int T, int D) { return 4 + T * D; }
 
+// Culling statistics of k_sdf_grid (statistics builds of the launch only, exm_sdf_cull_stats):
+// per-lane counts of each kind of work, charged at its FP32 op count by the benchmark's
+// executed-work roofline, plus warp-level iteration counts (lane efficiency).
+enum {
+  kCntRing = 0,       // ring steps (per warp)
+  kCntCell = 1,       // nonempty-cell bound tests (per lane still searching)
+  kCntChunk = 2,      // chunk box bound tests (per lane needing the cell)
+  kCntPoint = 3,      // point circle tests (per lane needing the chunk)
+  kCntPointWarp = 4,  // point-loop iterations (per warp)
+  kCntTransform = 5,  // body-frame transforms (points inside the circle bound)
+  kCntTile = 6,       // exact-cover tile tests
+  kCntTileVal = 7,    // tile distances taken (exact value of an exterior point)
+  kCntBound = 8,      // cover / AABB bound tests
+  kCntEdges = 9,      // edge-loop (polygon) / box-loop (cover) signed distances
+  kCntN = 10
+};
+
+// Signed-distance kernel selection. Production handles use kSdfAuto; the others exist for the
+// exactness tests and A/B measurements (exm_set_sdf_mode): every bound disabled (brute), no
+// chunk bound, a forced thread / warp / 8-warp-CTA per pose kernel, persistent warps at any
+// size, caps ignored.
+enum {
+  kSdfAuto = 0, kSdfBrute = 1, kSdfNoChunk = 2, kSdfThread = 3, kSdfWarp = 4, kSdfCta = 5,
+  kSdfPersist = 6, kSdfNoCap = 7
+};
+// What the last signed-distance launch of a step ran (exm_last_sdf_path).
+struct SdfPath {
+  int kernel;      // 0 thread per pose (k_sdf_grid), 1 warp per pose, 2 8-warp CTA per pose
+  int chunk;       // points per cull chunk of the cloud layout (8 or 16)
+  int persistent;  // 1: persistent warps with the work counter
+  int ctas, threads;
+  int hmajor;      // 1: lanes take consecutive rollouts at one step
+};
+
 // Kernel launch with programmatic dependent launch (PDL) allowed: the next kernel in the stream
 // (or graph) may be scheduled while this one drains, and waits in pdl_wait() (griddepcontrol
 // .wait, the first statement of every kernel) for the predecessor's completion and memory
 // flush, so launch latency overlaps the previous kernel's tail. EXM_PDL=0 disables it.
-inline bool pdl_enabled() {
-  static const bool on = !(std::getenv("EXM_PDL") && std::getenv("EXM_PDL")[0] == '0');
-  return on;
-}
+#ifndef EXM_NO_PDL
+constexpr bool kPdl = true;
+#else
+constexpr bool kPdl = false;  // A/B builds (-DEXM_NO_PDL)
+#endif
 template <typename... KArgs, typename... Args>
 cudaError_t launch_k(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
                      Args&&... args) {
@@ -162,7 +197,7 @@ cudaError_t launch_k(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t sme
   cfg.stream = s;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  attr[0].val.programmaticStreamSerializationAllowed = kPdl ? 1 : 0;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
@@ -183,16 +218,15 @@ cudaError_t launch_rollout(const StepConst& sc, const StepDyn* dyn, const double
                            double* eps, int draw, float4* poses, double2* xy, double* base_cost,
                            double* ctrl_cost, double* controls_out, double* states_out,
                            cudaStream_t s);
-cudaError_t launch_sdf_grid(const FpDev& fp, const float4* poses, int n_poses,
-                            const CloudGrid& g, float* out, cudaStream_t s);
-// cap (optional, T floats): a guess of each step's minimum distance; the kernel stays exact
-// for any cap (capped pass, then an uncapped pass for the poses it did not resolve).
-cudaError_t launch_sdf_grid_capped(const FpDev& fp, const float4* poses, int n_poses,
-                                   const CloudGrid& g, const float* cap, int T, float* out,
-                                   cudaStream_t s);
-cudaError_t launch_sdf_grid_stats(const FpDev& fp, const float4* poses, int n_poses,
-                                  const CloudGrid& g, const float* cap, int T, float* out,
-                                  unsigned long long* stats, cudaStream_t s);
+// Per-pose minimum signed distance over the prepared cloud (min_signed_distance_at).
+// Rollout poses are stored [row][T] (rows = n_poses / T rollouts); T = 0 for an unstructured
+// pose list. cap (optional, T floats): a guess of each step's minimum distance; the kernel
+// stays exact for any cap (capped pass, then an uncapped pass for the poses it did not
+// resolve). mode: kSdf*; path (optional) receives what ran; stats (optional, kCntN counters):
+// a statistics build of the same launch.
+cudaError_t launch_sdf_grid(const FpDev& fp, const float4* poses, int n_poses, int T,
+                            const CloudGrid& g, const float* cap, int mode, float* out,
+                            SdfPath* path, unsigned long long* stats, cudaStream_t s);
 cudaError_t launch_rollout_costs(const StepConst& sc, const StepDyn* dyn, const double* guide,
                                  int guide_cap, const double* base_cost, const double* ctrl_cost,
                                  const double2* xy, const float* dmin, double* cost,
@@ -210,8 +244,14 @@ cudaError_t launch_finalize(const StepConst& sc, const float* val_dmin, const do
                             int guide_cap, double* nominal, StepDyn* dyn, DecisionDev* dec,
                             double* out_dmin, double* out_nominal, double* out_uprev, int commit,
                             float* hstat, float* cap, float radius, cudaStream_t s);
-cudaError_t launch_recentre(const double* pts, int n, double cx, double cy, float2* out,
+// Staged pose batches (exm_sdf_stage): center[2] = the poses' centroid (one CTA, fixed order),
+// out = {x - cx, y - cy, cos theta, sin theta}; points recentred at the same device centre.
+cudaError_t launch_pose_prep(const double* poses, int n, double* center, float4* out,
+                             cudaStream_t s);
+cudaError_t launch_recentre(const double* pts, int n, const double* center, float2* out,
                             cudaStream_t s);
+// Body-frame queries -> signed distance (batch_signed_distance), FP32 in and out.
+cudaError_t launch_sdf_points(const FpDev& fp, const float2* q, int n, float* out, cudaStream_t s);
 cudaError_t launch_sdf_pairs(const FpDev& fp, const float4* poses, int n_poses,
                              const float2* pts, const uint8_t* mask, int n_points,
                              float* per_pair, unsigned* pose_min_key, cudaStream_t s);

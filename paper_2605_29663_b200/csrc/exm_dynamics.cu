@@ -920,29 +920,28 @@ cudaError_t rollout_lanes_launch(const StepConst& sc, const StepDyn* dyn, const 
                                  double* eps, int draw, float4* poses, double2* xy,
                                  double* base_cost, double* ctrl_cost, double* controls_out,
                                  double* states_out, size_t smem, cudaStream_t s) {
-  static size_t attr = 0;
-  if (smem > 48 * 1024 && smem > attr) {
+  // (per launch: the attribute is per device, and launches are captured into graphs)
+  if (smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(k_rollout_lanes<TAG, R>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(smem));
     if (e != cudaSuccess) return e;
-    attr = smem;
   }
-  static const int threads = getenv("EXM_LANE_THREADS") ? atoi(getenv("EXM_LANE_THREADS")) : kLaneThreads;
   if (const cudaError_t le = launch_k(k_rollout_lanes<TAG, R>, (sc.k_local + R - 1) / R,
-                                      threads, smem, s, sc, dyn, nominal, eps, draw, poses,
+                                      kLaneThreads, smem, s, sc, dyn, nominal, eps, draw, poses,
                                       xy, base_cost, ctrl_cost, controls_out, states_out);
       le != cudaSuccess)
     return le;
   return cudaGetLastError();
 }
 
-// EXM_ROLLOUT=warp: the warp-per-rollout kernel (A/B); default: lanes per rollout when the
-// CTA's shared memory fits (32 rollouts per CTA, else 16), warp per rollout otherwise.
-inline bool rollout_warp_mode() {
-  static const bool on = getenv("EXM_ROLLOUT") && !strcmp(getenv("EXM_ROLLOUT"), "warp");
-  return on;
-}
+// Lanes per rollout (8 rollouts per CTA) when the CTA's shared memory fits, else 16, warp per
+// rollout otherwise (very long horizons). -DEXM_ROLLOUT_WARP builds the warp kernel only (A/B).
+#ifdef EXM_ROLLOUT_WARP
+constexpr bool kRolloutWarpOnly = true;
+#else
+constexpr bool kRolloutWarpOnly = false;
+#endif
 
 cudaError_t launch_noise_pregen(const StepConst& sc, double* eps, cudaStream_t s) {
   const int n = sc.k_local * sc.T;
@@ -956,19 +955,16 @@ cudaError_t rollout_tag(const StepConst& sc, const StepDyn* dyn, const double* n
                         double* eps, int draw, float4* poses, double2* xy, double* base_cost,
                         double* ctrl_cost, double* controls_out, double* states_out,
                         cudaStream_t s) {
-  if (!rollout_warp_mode()) {
+  if (!kRolloutWarpOnly) {
     constexpr int D = model_dim<TAG>();
-    const size_t s32 = rollout_lanes_smem(sc.T, D, 32), s16 = rollout_lanes_smem(sc.T, D, 16);
+    const size_t s16 = rollout_lanes_smem(sc.T, D, 16);
     // 8 rollouts per CTA: ~28 resident warps per SM hide the eps loads (cold L2) as well as
-    // the warp-per-rollout kernel does, with a quarter of its instructions
-    static const int want_r = getenv("EXM_LANE_R") ? atoi(getenv("EXM_LANE_R")) : 8;
+    // the warp-per-rollout kernel does, with a quarter of its instructions (16 / 32 measured
+    // slower)
     const size_t s8 = rollout_lanes_smem(sc.T, D, 8);
-    if (want_r == 8 && s8 <= 200 * 1024)
+    if (s8 <= 200 * 1024)
       return rollout_lanes_launch<TAG, 8>(sc, dyn, nominal, eps, draw, poses, xy, base_cost,
                                           ctrl_cost, controls_out, states_out, s8, s);
-    if (want_r == 32 && s32 <= 100 * 1024)
-      return rollout_lanes_launch<TAG, 32>(sc, dyn, nominal, eps, draw, poses, xy, base_cost,
-                                           ctrl_cost, controls_out, states_out, s32, s);
     if (s16 <= 200 * 1024)
       return rollout_lanes_launch<TAG, 16>(sc, dyn, nominal, eps, draw, poses, xy, base_cost,
                                            ctrl_cost, controls_out, states_out, s16, s);
@@ -1021,19 +1017,12 @@ cudaError_t launch_rollout_costs(const StepConst& sc, const StepDyn* dyn, const 
                                  const double2* xy, const float* dmin, double* cost,
                                  uint8_t* unsafe, float* dstat, float* hstat, cudaStream_t s) {
   if (sc.k_local <= 0) return cudaSuccess;
-  // 16 rollouts per CTA; long horizons (per-warp stage arrays beyond ~200 KB) use fewer
+  // 16 rollouts per CTA (8 and 4 measured slower on configs 2 and 3); long horizons (per-warp
+  // stage arrays beyond ~200 KB) use fewer
   auto smem_for = [&](int w) {
     return sizeof(double) * (2 * static_cast<size_t>(guide_cap) + 3 * static_cast<size_t>(w) * sc.T +
                              sc.T);
   };
-  // EXM_COST_WARPS=8|4: rollouts per CTA override for A/B runs
-  static const int want_w = getenv("EXM_COST_WARPS") ? atoi(getenv("EXM_COST_WARPS")) : 16;
-  if (want_w == 8 && smem_for(8) <= 200 * 1024)
-    return rollout_costs_launch<8>(sc, dyn, guide, guide_cap, base_cost, ctrl_cost, xy, dmin, cost,
-                                   unsafe, dstat, hstat, smem_for(8), s);
-  if (want_w == 4 && smem_for(4) <= 200 * 1024)
-    return rollout_costs_launch<4>(sc, dyn, guide, guide_cap, base_cost, ctrl_cost, xy, dmin, cost,
-                                   unsafe, dstat, hstat, smem_for(4), s);
   if (smem_for(16) <= 200 * 1024)
     return rollout_costs_launch<16>(sc, dyn, guide, guide_cap, base_cost, ctrl_cost, xy, dmin, cost,
                                     unsafe, dstat, hstat, smem_for(16), s);

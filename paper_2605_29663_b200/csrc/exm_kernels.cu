@@ -265,24 +265,30 @@ __device__ __forceinline__ bool tiles_exterior_d2(const FpDev& fp, float bx, flo
 
 // One body-frame candidate point of the grid kernels: lower-bound tests, then the value v(p);
 // returns the new running minimum. BRUTE: no bound at all (every point valued, same arithmetic).
+// `work` reports what ran (statistics builds charge each at its op count): kWorkTile (the
+// exact-cover tile test), kWorkTileVal (tile distance taken), kWorkBound (cover / AABB bound
+// test), kWorkEdges (edge loop / rectangle-cover SDF).
+constexpr unsigned kWorkTile = 1u, kWorkTileVal = 2u, kWorkBound = 4u, kWorkEdges = 8u;
 template <int KIND, int NB, bool BRUTE>
 __device__ __forceinline__ float grid_point(const FpDev& fp, float bx, float by, float best,
-                                            float mg, bool& evaluated) {
-  evaluated = false;
+                                            float mg, unsigned& work) {
+  work = 0u;
   if constexpr (KIND == EXM_FOOTPRINT_POLYGON) {
     if (fp.cover_exact) {
       float d2;
       const float lim = best + mg;
+      work = kWorkTile;
       if (tiles_exterior_d2(fp, bx, by, d2)) {
         if (BRUTE || (lim > 0.f && d2 < lim * lim)) {
-          evaluated = true;
+          work |= kWorkTileVal;
           best = fminf(best, sqrtf(d2));
         }
         return best;
       }
       // inside (or at the rim of) the cover: the AABB interior bound, then the edge loop
+      if (!BRUTE) work |= kWorkBound;
       if (BRUTE || fmaxf(fmaxf(fp.aabb[0] - bx, bx - fp.aabb[1]), fmaxf(fp.aabb[2] - by, by - fp.aabb[3])) < lim) {
-        evaluated = true;
+        work |= kWorkEdges;
         best = fminf(best, sd_body<KIND, NB>(fp, bx, by));
       }
       return best;
@@ -292,10 +298,12 @@ __device__ __forceinline__ float grid_point(const FpDev& fp, float bx, float by,
   // rectangle covers of <= 3 boxes: the exact SDF is hardly dearer than a bound (skipping its
   // sqrt behind a squared-distance test measured slower: the branch diverges); larger
   // covers: the AABB pre-test
-  if (BRUTE || (KIND != EXM_FOOTPRINT_POLYGON && NB > 0 && NB <= 3) ||
+  constexpr bool kDirect = KIND != EXM_FOOTPRINT_POLYGON && NB > 0 && NB <= 3;
+  if (!BRUTE && !kDirect) work = kWorkBound;
+  if (BRUTE || kDirect ||
       (KIND == EXM_FOOTPRINT_POLYGON ? cover_may_beat(fp, bx, by, best, mg)
                                      : aabb_may_beat(fp, bx, by, best, mg))) {
-    evaluated = true;
+    work |= kWorkEdges;
     best = fminf(best, sd_body<KIND, NB>(fp, bx, by));
   }
   return best;
@@ -711,16 +719,25 @@ __device__ __forceinline__ void sdf_grid_warp(const FpDev& fp, const float4* __r
                                               const int* __restrict__ cell_start,
                                               const float2* __restrict__ cloud,
                                               const float4* __restrict__ chunk,
-                                              const float* __restrict__ cap, int T,
+                                              const float* __restrict__ cap, int T, int rows,
                                               float* __restrict__ out, int i, int lane,
-                                              unsigned long long& n_test,
-                                              unsigned long long& n_eval) {
+                                              unsigned long long* cnt) {
   const bool active = i < n_poses;
+  // h-major lanes: the poses are stored [row][h] (row = rollout); with rows > 0 logical index
+  // i = h * rows + row, so a warp takes 32 consecutive rollouts at the same step h (spatially
+  // coherent: one set of ring cells serves all lanes) instead of one rollout's 32 steps
+  int hh = 0, p = i;
+  if (rows > 0) {
+    hh = i / rows;
+    p = (i - hh * rows) * T + hh;
+  } else if (T > 0) {
+    hh = i % T;
+  }
   if (gm.n_valid == 0) {
-    if (active) out[i] = kEmptyDistance;
+    if (active) out[p] = kEmptyDistance;
     return;
   }
-  const float4 q = active ? poses[i] : make_float4(0.f, 0.f, 1.f, 0.f);
+  const float4 q = active ? poses[p] : make_float4(0.f, 0.f, 1.f, 0.f);
   float sx = active ? q.x : 0.f, sy = active ? q.y : 0.f;
   int na = active ? 1 : 0;
   for (int o = 16; o; o >>= 1) {
@@ -741,7 +758,7 @@ __device__ __forceinline__ void sdf_grid_warp(const FpDev& fp, const float4* __r
   // pose whose true minimum m* lies below the cap still gets m* exactly (no point with sd = m*
   // is ever pruned: its bound is <= m* < best); poses left at the cap rerun uncapped (pass 1).
   const float kInf = __int_as_float(0x7f800000);
-  const float capv = (cap != nullptr && active && MODE != kGridBrute) ? cap[i % T] : kInf;
+  const float capv = (cap != nullptr && active && MODE != kGridBrute) ? cap[hh] : kInf;
   float best = capv;
   bool todo = active;
   for (int pass = 0; pass < 2; ++pass) {
@@ -766,6 +783,7 @@ __device__ __forceinline__ void sdf_grid_warp(const FpDev& fp, const float4* __r
       if (!__any_sync(kFull, need)) break;
     }
     const int ncell = k == 0 ? 1 : 8 * k;
+    if (STATS && lane == 0) ++cnt[kCntRing];
     // The warp enumerates the ring 32 cells at a time, one cell per lane (position, range,
     // CSR bounds: the cell_start loads of the 32 cells are in flight together), and then
     // visits only the in-range nonempty ones, in ring order, with the cell's data shuffled in.
@@ -792,6 +810,7 @@ __device__ __forceinline__ void sdf_grid_warp(const FpDev& fp, const float4* __r
       const float lim = R + best;
       const bool need = todo && (MODE == kGridBrute || ((gx_ * gx_ + gy_ * gy_ < lim * lim) &&
                                    box_may_beat(w, bx0, bx1, by0, by1, best, mg)));
+      if (STATS && todo) ++cnt[kCntCell];
       if (!__any_sync(kFull, need)) continue;
       float l2 = lim * lim;
       // chunks of gm.chunk Morton-ordered points: one body-frame box bound per chunk, then the
@@ -801,6 +820,7 @@ __device__ __forceinline__ void sdf_grid_warp(const FpDev& fp, const float4* __r
         bool cneed = need;
         if (MODE == kGridFull) {
           cneed = need && chunk_may_beat(fp, q, __ldg(chunk + ch), best, mg);
+          if (STATS && need) ++cnt[kCntChunk];
           if (!__any_sync(kFull, cneed)) continue;
         }
         const float2* cp = cloud + (ch << csh);
@@ -808,14 +828,21 @@ __device__ __forceinline__ void sdf_grid_warp(const FpDev& fp, const float4* __r
         for (int p = 0; p < gm.chunk; ++p) {
           const float2 o = __ldg(cp + p);
           const float dx = o.x - q.x, dy = o.y - q.y;
-          if (STATS && cneed) ++n_test;
+          if (STATS && cneed) ++cnt[kCntPoint];
+          if (STATS && lane == 0) ++cnt[kCntPointWarp];
           if (cneed && (MODE == kGridBrute ? o.x == o.x : dx * dx + dy * dy < l2)) {  // NaN pads
             const float bx = fmaf(q.z, dx, q.w * dy);
             const float by = fmaf(q.z, dy, -(q.w * dx));
-            bool ev;
-            best = grid_point<KIND, NB, MODE == kGridBrute>(fp, bx, by, best, mg, ev);
-            if (ev) {
-              if (STATS) ++n_eval;
+            unsigned wk;
+            best = grid_point<KIND, NB, MODE == kGridBrute>(fp, bx, by, best, mg, wk);
+            if (STATS) {
+              ++cnt[kCntTransform];
+              cnt[kCntTile] += (wk & kWorkTile) != 0u;
+              cnt[kCntTileVal] += (wk & kWorkTileVal) != 0u;
+              cnt[kCntBound] += (wk & kWorkBound) != 0u;
+              cnt[kCntEdges] += (wk & kWorkEdges) != 0u;
+            }
+            if (wk & (kWorkTileVal | kWorkEdges)) {
               const float nl = R + best;
               l2 = nl * nl;
             }
@@ -826,7 +853,7 @@ __device__ __forceinline__ void sdf_grid_warp(const FpDev& fp, const float4* __r
     }  // groups of 32 ring cells
   }
   }  // pass
-  if (active) out[i] = best;
+  if (active) out[p] = best;
 }
 
 // Persistent warps: the grid is sized to the resident capacity and every warp takes the next
@@ -841,18 +868,20 @@ __global__ void __launch_bounds__(128) k_sdf_grid(const __grid_constant__ FpDev 
                                                   const int* __restrict__ cell_start,
                                                   const float2* __restrict__ cloud,
                                                   const float4* __restrict__ chunk,
-                                                  const float* __restrict__ cap, int T,
+                                                  const float* __restrict__ cap, int T, int rows,
                                                   float* __restrict__ out,
                                                   unsigned* __restrict__ work,
                                                   unsigned long long* __restrict__ stats = nullptr) {
   pdl_wait();
-  unsigned long long n_test = 0, n_eval = 0;
+  unsigned long long cnt[kCntN];
+#pragma unroll
+  for (int k = 0; k < kCntN; ++k) cnt[k] = 0ull;
   const int lane = threadIdx.x & 31;
   const GridMeta gm = *gmp;
   if (work == nullptr) {
     sdf_grid_warp<KIND, NB, STATS, MODE>(fp, poses, n_poses, gm, cell_start, cloud, chunk, cap, T,
-                                         out, blockIdx.x * blockDim.x + threadIdx.x, lane, n_test,
-                                         n_eval);
+                                         rows, out, blockIdx.x * blockDim.x + threadIdx.x, lane,
+                                         cnt);
   } else {
     for (;;) {
       unsigned base = 0;
@@ -860,8 +889,7 @@ __global__ void __launch_bounds__(128) k_sdf_grid(const __grid_constant__ FpDev 
       base = __shfl_sync(kFull, base, 0);
       if (base >= static_cast<unsigned>(n_poses)) break;
       sdf_grid_warp<KIND, NB, STATS, MODE>(fp, poses, n_poses, gm, cell_start, cloud, chunk, cap,
-                                           T, out, static_cast<int>(base) + lane, lane, n_test,
-                                           n_eval);
+                                           T, rows, out, static_cast<int>(base) + lane, lane, cnt);
     }
     if (lane == 0) {
       __threadfence();
@@ -874,8 +902,12 @@ __global__ void __launch_bounds__(128) k_sdf_grid(const __grid_constant__ FpDev 
     }
   }
   if (STATS) {
-    atomicAdd(stats, n_test);
-    atomicAdd(stats + 1, n_eval);
+#pragma unroll
+    for (int k = 0; k < kCntN; ++k) {
+      unsigned long long v = cnt[k];
+      for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
+      if (lane == 0 && v) atomicAdd(stats + k, v);
+    }
   }
 }
 
@@ -963,8 +995,8 @@ __global__ void __launch_bounds__(W == 1 ? 128 : 32 * W) k_sdf_grid_warp(
           if (dx * dx + dy * dy < l2 * l2) {
             const float bx = fmaf(q.z, dx, q.w * dy);
             const float by = fmaf(q.z, dy, -(q.w * dx));
-            bool ev;
-            mine = grid_point<KIND, NB, false>(fp, bx, by, mine, mg, ev);
+            unsigned wk;
+            mine = grid_point<KIND, NB, false>(fp, bx, by, mine, mg, wk);
           }
         }
       }
@@ -985,13 +1017,64 @@ __global__ void __launch_bounds__(W == 1 ? 128 : 32 * W) k_sdf_grid_warp(
   if (lane == 0 && wid == 0) out[w] = best;
 }
 
-__global__ void k_recentre(const double* __restrict__ pts, int n, double cx, double cy,
+// Recentring point of a staged pose batch: the poses' centroid, summed in a fixed order by one
+// CTA (deterministic), then every pose / point is recentred in FP64 and rounded once.
+__global__ void __launch_bounds__(1024) k_pose_center(const double* __restrict__ poses, int n,
+                                                      double* __restrict__ center) {
+  pdl_wait();
+  __shared__ double sx[32], sy[32];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  double x = 0.0, y = 0.0;
+  for (int i = tid; i < n; i += blockDim.x) {
+    x += poses[3 * static_cast<size_t>(i)];
+    y += poses[3 * static_cast<size_t>(i) + 1];
+  }
+  for (int o = 16; o; o >>= 1) {
+    x += __shfl_xor_sync(kFull, x, o);
+    y += __shfl_xor_sync(kFull, y, o);
+  }
+  if (lane == 0) { sx[warp] = x; sy[warp] = y; }
+  __syncthreads();
+  if (tid == 0) {
+    double a = 0.0, b = 0.0;
+    for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) { a += sx[w]; b += sy[w]; }
+    center[0] = n > 0 ? a / n : 0.0;
+    center[1] = n > 0 ? b / n : 0.0;
+  }
+}
+
+__global__ void k_pose_prep(const double* __restrict__ poses, int n,
+                            const double* __restrict__ center, float4* __restrict__ out) {
+  pdl_wait();
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double* q = poses + 3 * static_cast<size_t>(i);
+  double sn, cs;
+  sincos(q[2], &sn, &cs);
+  out[i] = make_float4(static_cast<float>(q[0] - center[0]), static_cast<float>(q[1] - center[1]),
+                       static_cast<float>(cs), static_cast<float>(sn));
+}
+
+__global__ void k_recentre(const double* __restrict__ pts, int n, const double* __restrict__ center,
                            float2* __restrict__ out) {
   pdl_wait();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   const double2 w = reinterpret_cast<const double2*>(pts)[i];
-  out[i] = make_float2(static_cast<float>(w.x - cx), static_cast<float>(w.y - cy));
+  out[i] = make_float2(static_cast<float>(w.x - center[0]), static_cast<float>(w.y - center[1]));
+}
+
+// batch_signed_distance (geometry.cpp:298-318): one body-frame query per thread, FP32 queries
+// rounded on the host while they are staged (the identity pose: no recentring).
+template <int KIND, int NB>
+__global__ void __launch_bounds__(256) k_sdf_points(const __grid_constant__ FpDev fp,
+                                                    const float2* __restrict__ q, int n,
+                                                    float* __restrict__ out) {
+  pdl_wait();
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const float2 p = q[i];
+  out[i] = sd_body<KIND, NB>(fp, p.x, p.y);
 }
 
 constexpr int kPairThreads = 256;
@@ -1268,55 +1351,51 @@ cudaError_t dispatch_fp(const FpDev& fp, Args&&... args) {
   }
 }
 
-// EXM_GRID_MODE (tests and A/B measurements; read at every launch, so at graph capture):
-//   "brute" every valid point evaluated (exactness reference), "nochunk" no chunk bound,
-//   "thread" / "warp" / "cta" force one thread, one warp or one 8-warp CTA per pose.
-//   Default: automatic.
-inline const char* grid_mode() {
-  const char* m = getenv("EXM_GRID_MODE");
-  return m ? m : "";
-}
-
-// Persistent grid size of a k_sdf_grid instantiation: resident CTAs per SM x SMs (cached).
+// Persistent grid size of a k_sdf_grid instantiation on the current device: resident CTAs per
+// SM x SMs (cached per device and instantiation).
 template <typename K>
 int persistent_blocks(K kernel, int threads) {
-  static int blocks = 0;
-  if (blocks == 0) {
-    int dev = 0, n_sm = 148, per_sm = 1;
-    if (cudaGetDevice(&dev) == cudaSuccess)
-      cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
+  constexpr int kMaxDev = 64;
+  static int blocks[kMaxDev] = {};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDev) dev = 0;
+  if (blocks[dev] == 0) {
+    int n_sm = 148, per_sm = 1;
+    cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, 0) != cudaSuccess ||
         per_sm < 1)
       per_sm = 1;
-    blocks = n_sm * per_sm;
+    blocks[dev] = n_sm * per_sm;
   }
-  return blocks;
+  return blocks[dev];
 }
 
 constexpr int kPersistentWaves = 8;
-// EXM_SDF_STATIC=1: static warp <-> pose mapping (A/B of the persistent work counter)
-inline bool static_map() {
-  static const bool on = getenv("EXM_SDF_STATIC") && getenv("EXM_SDF_STATIC")[0] == '1';
-  return on;
-}
+constexpr int kGridThreads = 128;  // 32-128 measured within 1 % (round 1)
 
 template <int KIND, int NB, bool STATS, int MODE>
-cudaError_t launch_grid_kernel(const FpDev& fp, const float4* poses, int n_poses,
-                               const CloudGrid& g, const float* cap, int T, float* out,
-                               unsigned long long* stats, cudaStream_t s) {
-  static const int threads = getenv("EXM_SDF_THREADS") ? atoi(getenv("EXM_SDF_THREADS")) : 128;
+cudaError_t launch_grid_kernel(const FpDev& fp, const float4* poses, int n_poses, int T,
+                               const CloudGrid& g, const float* cap, bool persist, float* out,
+                               SdfPath* path, unsigned long long* stats, cudaStream_t s) {
+  const int threads = kGridThreads;
   const int blocks = (n_poses + threads - 1) / threads;
   auto k = k_sdf_grid<KIND, NB, STATS, MODE>;
   // persistent only for many waves (cfg5: ~30): at one to three waves the hardware block
   // scheduler balances as well and the static mapping keeps neighbouring poses in one CTA
   // (measured: cfg2 / cfg3 slower persistent, cfg5 2.5 % faster)
   const int cap_blocks = persistent_blocks(k, threads);
-  const char* pe = getenv("EXM_SDF_PERSIST");  // "1": persistent at any size (tests)
-  const bool force = pe && pe[0] == '1';
-  unsigned* work = (static_map() || (!force && blocks < kPersistentWaves * cap_blocks)) ? nullptr : g.work;
+  unsigned* work = (persist || blocks >= kPersistentWaves * cap_blocks) ? g.work : nullptr;
   const int grid = work ? cap_blocks : blocks;
+  const int rows = (T > 0 && n_poses % T == 0) ? n_poses / T : 0;
+#ifdef EXM_SDF_RMAJOR  // A/B builds: lanes take one rollout's consecutive steps (round 1)
+  const int rows_used = 0;
+#else
+  const int rows_used = rows;
+#endif
+  if (path) *path = SdfPath{0, 0, work ? 1 : 0, grid, threads, rows_used > 0 ? 1 : 0};
   if (const cudaError_t le = launch_k(k, grid, threads, 0, s, fp, poses, n_poses, g.gm,
-                                      g.cell_start, g.cloud, g.chunk, cap, T, out, work, stats);
+                                      g.cell_start, g.cloud, g.chunk, cap, T, rows_used, out, work,
+                                      stats);
       le != cudaSuccess)
     return le;
   return cudaGetLastError();
@@ -1324,43 +1403,43 @@ cudaError_t launch_grid_kernel(const FpDev& fp, const float4* poses, int n_poses
 
 template <int KIND, int NB>
 struct GridLaunch {
-  static cudaError_t run(const FpDev& fp, const float4* poses, int n_poses, const CloudGrid& g,
-                         const float* cap, int T, float* out, cudaStream_t s) {
+  static cudaError_t run(const FpDev& fp, const float4* poses, int n_poses, int T,
+                         const CloudGrid& g, const float* cap, int mode, float* out,
+                         SdfPath* path, unsigned long long* stats, cudaStream_t s) {
     if (n_poses <= 0) return cudaSuccess;
-    const char* m = grid_mode();
-    if (!strcmp(m, "brute"))
-      return launch_grid_kernel<KIND, NB, false, kGridBrute>(fp, poses, n_poses, g, cap, T, out, nullptr, s);
-    if (!strcmp(m, "nochunk"))
-      return launch_grid_kernel<KIND, NB, false, kGridNoChunk>(fp, poses, n_poses, g, cap, T, out, nullptr, s);
-    return launch_grid_kernel<KIND, NB, false, kGridFull>(fp, poses, n_poses, g, cap, T, out, nullptr, s);
-  }
-};
-
-template <int KIND, int NB>
-struct GridStatsLaunch {
-  static cudaError_t run(const FpDev& fp, const float4* poses, int n_poses, const CloudGrid& g,
-                         const float* cap, int T, float* out, unsigned long long* stats,
-                         cudaStream_t s) {
-    if (n_poses <= 0) return cudaSuccess;
-    if (!strcmp(grid_mode(), "nocap")) cap = nullptr;
-    if (!strcmp(grid_mode(), "nochunk"))
-      return launch_grid_kernel<KIND, NB, true, kGridNoChunk>(fp, poses, n_poses, g, cap, T, out, stats, s);
-    return launch_grid_kernel<KIND, NB, true, kGridFull>(fp, poses, n_poses, g, cap, T, out, stats, s);
+    const bool persist = mode == kSdfPersist;
+    if (mode == kSdfNoCap) cap = nullptr;
+    if (stats) {
+      if (mode == kSdfNoChunk)
+        return launch_grid_kernel<KIND, NB, true, kGridNoChunk>(fp, poses, n_poses, T, g, cap, persist, out, path, stats, s);
+      return launch_grid_kernel<KIND, NB, true, kGridFull>(fp, poses, n_poses, T, g, cap, persist, out, path, stats, s);
+    }
+    if (mode == kSdfBrute)
+      return launch_grid_kernel<KIND, NB, false, kGridBrute>(fp, poses, n_poses, T, g, cap, persist, out, path, nullptr, s);
+    if (mode == kSdfNoChunk)
+      return launch_grid_kernel<KIND, NB, false, kGridNoChunk>(fp, poses, n_poses, T, g, cap, persist, out, path, nullptr, s);
+    return launch_grid_kernel<KIND, NB, false, kGridFull>(fp, poses, n_poses, T, g, cap, persist, out, path, nullptr, s);
   }
 };
 
 template <int KIND, int NB>
 struct GridWarpLaunch {
   static cudaError_t run(const FpDev& fp, const float4* poses, int n_poses, const CloudGrid& g,
-                         float* out, cudaStream_t s) {
+                         bool cta, float* out, SdfPath* path, cudaStream_t s) {
     if (n_poses <= 0) return cudaSuccess;
-    if (n_poses <= kCtaPerPoseMax || !strcmp(grid_mode(), "cta")) {  // few poses: 8 warps each
-      { if (const cudaError_t le = launch_k(k_sdf_grid_warp<KIND, NB, 8>, n_poses, 256, 0, s, fp, poses, n_poses, g.gm, g.cell_start,
-                                                           g.cloud, out); le != cudaSuccess) return le; }
+    if (n_poses <= kCtaPerPoseMax || cta) {  // few poses: 8 warps each
+      if (path) *path = SdfPath{2, 0, 0, n_poses, 256, 0};
+      if (const cudaError_t le = launch_k(k_sdf_grid_warp<KIND, NB, 8>, n_poses, 256, 0, s, fp,
+                                          poses, n_poses, g.gm, g.cell_start, g.cloud, out);
+          le != cudaSuccess)
+        return le;
     } else {
-      const int threads = 128, warps = threads / 32;
-      { if (const cudaError_t le = launch_k(k_sdf_grid_warp<KIND, NB>, (n_poses + warps - 1) / warps, threads, 0, s, 
-          fp, poses, n_poses, g.gm, g.cell_start, g.cloud, out); le != cudaSuccess) return le; }
+      const int threads = 128, warps = threads / 32, grid = (n_poses + warps - 1) / warps;
+      if (path) *path = SdfPath{1, 0, 0, grid, threads, 0};
+      if (const cudaError_t le = launch_k(k_sdf_grid_warp<KIND, NB>, grid, threads, 0, s, fp,
+                                          poses, n_poses, g.gm, g.cell_start, g.cloud, out);
+          le != cudaSuccess)
+        return le;
     }
     return cudaGetLastError();
   }
@@ -1388,13 +1467,14 @@ struct PairsLaunch {
 }  // namespace
 
 // ------------------------------------------------------------------ launchers
-// Chunk size per handle (EXM_CHUNK=8/16 overrides): 16-point chunks measured 10 % faster on the
-// 20k / 50k-point aisle and moving-disc clouds (configs 3, 5), 6 % slower on config 2's 10k
-// clutter points.
+// Chunk size per handle: 16-point chunks measured 10 % faster on the 20k / 50k-point aisle and
+// moving-disc clouds (configs 3, 5), 6 % slower on config 2's 10k clutter points.
 int chunk_for_capacity(int n_cap) {
-  static const int forced = getenv("EXM_CHUNK") ? atoi(getenv("EXM_CHUNK")) : 0;
-  if (forced == 8 || forced == 16) return forced;
+#ifdef EXM_CHUNK
+  return EXM_CHUNK;  // A/B builds
+#else
   return n_cap >= 16384 ? 16 : 8;
+#endif
 }
 
 cudaError_t launch_cloud_prep(const double* pts, const uint8_t* mask, const StepDyn* dyn,
@@ -1403,63 +1483,80 @@ cudaError_t launch_cloud_prep(const double* pts, const uint8_t* mask, const Step
   // measured 20.9 us against 13.6 + 5.9 us for config 2: the cluster barriers cost what the
   // parallel load saves at 10k points. The single CTA stays.)
   const int smem = kGridMax * kGridMax * static_cast<int>(sizeof(int));
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(k_cloud_prep, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (e != cudaSuccess) return e;
-    attr_set = true;
-  }
-  // Cells sized for about kPtsPerCell points, between R/4 and kCellMaxR * R: a cull disc of
-  // radius R + d covers ~(2(R+d)/cs)^2 cells; the chunk bounds cull inside a cell.
+  // (cudaFuncSetAttribute applies to the current device: set it on every launch, it is cheap
+  // and launches are captured into graphs anyway)
+  cudaError_t e = cudaFuncSetAttribute(k_cloud_prep, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e != cudaSuccess) return e;
+  // Cells sized for about kPtsPerCell points, between kCellMinR * R and kCellMaxR * R: a cull
+  // disc of radius R + d covers ~(2(R+d)/cs)^2 cells; the chunk bounds cull inside a cell.
+  // The cloud is bulk-prefetched into L2 first (cfg2 0.193 -> 0.188 ms after an L2 flush).
   const float r = fmaxf(radius, 0.04f);
-  // (EXM_PTS_PER_CELL / EXM_CELL_MINR / EXM_CELL_MAXR: tuning overrides for A/B runs)
-  static const float ppc = getenv("EXM_PTS_PER_CELL") ? static_cast<float>(atof(getenv("EXM_PTS_PER_CELL"))) : kPtsPerCell;
-  static const float cmin = getenv("EXM_CELL_MINR") ? static_cast<float>(atof(getenv("EXM_CELL_MINR"))) : kCellMinR;
-  // L2 bulk prefetch of the cloud in k_cloud_prep: cfg2 0.193 -> 0.188 ms after an L2 flush, e2e
-  // (cloud already in L2 after its H2D copy) unchanged; EXM_PREP_PREFETCH=0 turns it off
-  static const int pf = getenv("EXM_PREP_PREFETCH") ? atoi(getenv("EXM_PREP_PREFETCH")) : 1;
-  static const float slo = getenv("EXM_CELL_SEARCH_LO") ? static_cast<float>(atof(getenv("EXM_CELL_SEARCH_LO"))) : 0.0f;
-  static const float cmax = getenv("EXM_CELL_MAXR") ? static_cast<float>(atof(getenv("EXM_CELL_MAXR"))) : kCellMaxR;
-  { if (const cudaError_t le = launch_k(k_cloud_prep, 1, 1024, smem, s, pts, mask, dyn, cmin * r, cmax * r, ppc, r, chunk_for_capacity(n_cap), slo, pf, g.dstat, g.tmp,
-                                     g.raw, g.raw_start, g.cell_start, g.gm); le != cudaSuccess) return le; }
-  cudaError_t e = cudaGetLastError();
+  if (const cudaError_t le = launch_k(k_cloud_prep, 1, 1024, smem, s, pts, mask, dyn, kCellMinR * r,
+                                      kCellMaxR * r, kPtsPerCell, r, chunk_for_capacity(n_cap),
+                                      0.0f, 1, g.dstat, g.tmp, g.raw, g.raw_start, g.cell_start,
+                                      g.gm);
+      le != cudaSuccess)
+    return le;
+  e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   int dev = 0, n_sm = 148;
   if (cudaGetDevice(&dev) == cudaSuccess)
     cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
-  { if (const cudaError_t le = launch_k(k_cell_sort, 2 * n_sm, kSortWarps * 32, 0, s, g.raw, g.raw_start, g.cell_start, g.gm, g.cloud,
-                                                   g.chunk); le != cudaSuccess) return le; }
+  if (const cudaError_t le = launch_k(k_cell_sort, 2 * n_sm, kSortWarps * 32, 0, s, g.raw,
+                                      g.raw_start, g.cell_start, g.gm, g.cloud, g.chunk);
+      le != cudaSuccess)
+    return le;
   return cudaGetLastError();
 }
 
-cudaError_t launch_sdf_grid_stats(const FpDev& fp, const float4* poses, int n_poses,
-                                  const CloudGrid& g, const float* cap, int T, float* out,
-                                  unsigned long long* stats, cudaStream_t s) {
-  return dispatch_fp<GridStatsLaunch>(fp, poses, n_poses, g, cap, T, out, stats, s);
+cudaError_t launch_sdf_grid(const FpDev& fp, const float4* poses, int n_poses, int T,
+                            const CloudGrid& g, const float* cap, int mode, float* out,
+                            SdfPath* path, unsigned long long* stats, cudaStream_t s) {
+  // Few poses (validation rollout, single queries): one warp (or one 8-warp CTA) per pose keeps
+  // all lanes busy; many poses: one thread per pose. Statistics builds exist for the latter.
+  const bool warp = !stats && (mode == kSdfWarp || mode == kSdfCta ||
+                               (n_poses <= kWarpPerPoseMax && mode != kSdfThread &&
+                                mode != kSdfBrute && mode != kSdfPersist));
+  if (warp) return dispatch_fp<GridWarpLaunch>(fp, poses, n_poses, g, mode == kSdfCta, out, path, s);
+  return dispatch_fp<GridLaunch>(fp, poses, n_poses, T, g, cap, mode, out, path, stats, s);
 }
 
-cudaError_t launch_sdf_grid_capped(const FpDev& fp, const float4* poses, int n_poses,
-                                   const CloudGrid& g, const float* cap, int T, float* out,
-                                   cudaStream_t s) {
-  // Few poses (validation rollout, single queries): one warp per pose keeps all lanes busy.
-  const char* m = grid_mode();
-  const bool warp = !strcmp(m, "warp") || !strcmp(m, "cta") ||
-                    (n_poses <= kWarpPerPoseMax && strcmp(m, "thread") && strcmp(m, "brute"));
-  if (warp) return dispatch_fp<GridWarpLaunch>(fp, poses, n_poses, g, out, s);
-  if (!strcmp(m, "nocap")) cap = nullptr;
-  return dispatch_fp<GridLaunch>(fp, poses, n_poses, g, cap, T, out, s);
+cudaError_t launch_pose_prep(const double* poses, int n, double* center, float4* out,
+                             cudaStream_t s) {
+  if (const cudaError_t le = launch_k(k_pose_center, 1, 1024, 0, s, poses, n, center);
+      le != cudaSuccess)
+    return le;
+  if (n > 0)
+    if (const cudaError_t le = launch_k(k_pose_prep, (n + 255) / 256, 256, 0, s, poses, n,
+                                        static_cast<const double*>(center), out);
+        le != cudaSuccess)
+      return le;
+  return cudaGetLastError();
 }
 
-cudaError_t launch_sdf_grid(const FpDev& fp, const float4* poses, int n_poses,
-                            const CloudGrid& g, float* out, cudaStream_t s) {
-  return launch_sdf_grid_capped(fp, poses, n_poses, g, nullptr, 1, out, s);
-}
-
-cudaError_t launch_recentre(const double* pts, int n, double cx, double cy, float2* out,
+cudaError_t launch_recentre(const double* pts, int n, const double* center, float2* out,
                             cudaStream_t s) {
   if (n <= 0) return cudaSuccess;
-  { if (const cudaError_t le = launch_k(k_recentre, (n + 255) / 256, 256, 0, s, pts, n, cx, cy, out); le != cudaSuccess) return le; }
+  if (const cudaError_t le = launch_k(k_recentre, (n + 255) / 256, 256, 0, s, pts, n, center, out);
+      le != cudaSuccess)
+    return le;
   return cudaGetLastError();
+}
+
+template <int KIND, int NB>
+struct PointsLaunch {
+  static cudaError_t run(const FpDev& fp, const float2* q, int n, float* out, cudaStream_t s) {
+    if (n <= 0) return cudaSuccess;
+    if (const cudaError_t le = launch_k(k_sdf_points<KIND, NB>, (n + 255) / 256, 256, 0, s, fp,
+                                        q, n, out);
+        le != cudaSuccess)
+      return le;
+    return cudaGetLastError();
+  }
+};
+
+cudaError_t launch_sdf_points(const FpDev& fp, const float2* q, int n, float* out, cudaStream_t s) {
+  return dispatch_fp<PointsLaunch>(fp, q, n, out, s);
 }
 
 cudaError_t launch_sdf_pairs(const FpDev& fp, const float4* poses, int n_poses,

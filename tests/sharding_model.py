@@ -1,5 +1,8 @@
-"""Host-side restatement of the rollout sharding and the softmax-partial exchange that
-libexm_b200.so performs on the device (k_block_partials / k_update, exm_attach_comm).
+"""TEST INFRASTRUCTURE: host-side restatement (numpy) of the rollout sharding and the
+softmax-partial exchange that libexm_b200.so performs on the device (k_block_partials /
+k_update, exm_attach_comm / exm_sharded_cycle). The world-size-2 gloo test
+(tests/test_sharding_cpu.py) runs this model over a real process group on CPU; the library's own
+sharded path is tested on the GPU (tests/test_gpu_sharding.py).
 
 Rollouts are split into fixed blocks of BLOCK = 256 (independent of the GPU count); rank g of G
 owns blocks [g*nb/G, (g+1)*nb/G). Each block b yields {beta_b, S_b, A_b, argmin_b, U_b}; the

@@ -28,7 +28,7 @@ def test_library_exports_every_symbol():
     lib = _abi.load_library()
     for name in header_functions():
         assert hasattr(lib, name), name
-    assert lib.exm_abi_version() == 1
+    assert lib.exm_abi_version() == 2
 
 
 def test_library_is_sm100a_only():

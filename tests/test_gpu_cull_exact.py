@@ -1,12 +1,11 @@
 """Exactness of the culled grid SDF (GPU): every cull (ring, cell, chunk, point bounds with the
 rounding margin) may only skip points that cannot lower the minimum, so the culled per-pose
-minimum must equal, bit for bit, the same kernel with every bound disabled (EXM_GRID_MODE=brute:
+minimum must equal, bit for bit, the same kernel with every bound disabled (EXM_SDF_BRUTE:
 every valid point evaluated with identical FP32 arithmetic). Covers both kernels (thread- and
 warp-per-pose), polygons (L12, L6, star) and rectangle covers (1 and 3 boxes), clouds with
 obstacles overlapping the footprint (negative minima) and far obstacles (large minima)."""
 import dataclasses
 import math
-import os
 
 import numpy as np
 import pytest
@@ -46,33 +45,27 @@ CASES = {
 
 
 def _dmin(wl, mode, caps=None):
-    old = os.environ.get("EXM_GRID_MODE")
-    old_p = os.environ.pop("EXM_SDF_PERSIST", None)
-    if mode == "persist":  # thread per pose, persistent warps with the work counter
-        mode = "thread"
-        os.environ["EXM_SDF_PERSIST"] = "1"
-    os.environ["EXM_GRID_MODE"] = mode
-    try:
-        eng = Engine(wl.model, wl.limits, wl.footprint, wl.params, n_cap=wl.n_points, guide_cap=8)
-        if caps is not None:
-            eng.set_sdf_caps(caps)
-        nom, up = wl.zero_state()
-        eps = eng.sample_perturbations(wl.params.seed, 0)
-        # a few cycles' worth of distinct pose sets: nominal offsets
-        out = []
-        for scale in (0.0, 0.3):
-            b = eng.evaluate_rollouts(wl.q0, nom + scale, eps, wl.obstacles(), wl.guidance, up)
-            out.append(b.d_min.copy())
-        eng.close()
-        return np.concatenate([o.reshape(-1) for o in out])
-    finally:
-        os.environ.pop("EXM_SDF_PERSIST", None)
-        if old_p is not None:
-            os.environ["EXM_SDF_PERSIST"] = old_p
-        if old is None:
-            del os.environ["EXM_GRID_MODE"]
-        else:
-            os.environ["EXM_GRID_MODE"] = old
+    """Per-step minima of two pose sets with the SDF kernel forced to `mode` (exm_set_option
+    EXM_OPT_SDF_MODE: brute, thread, warp, cta, nochunk, persist = thread per pose with the
+    persistent work counter at any size)."""
+    eng = Engine(wl.model, wl.limits, wl.footprint, wl.params, n_cap=wl.n_points, guide_cap=8)
+    eng.set_sdf_mode(mode)
+    if caps is not None:
+        eng.set_sdf_caps(caps)
+    nom, up = wl.zero_state()
+    eps = eng.sample_perturbations(wl.params.seed, 0)
+    # a few cycles' worth of distinct pose sets: nominal offsets
+    out = []
+    for scale in (0.0, 0.3):
+        b = eng.evaluate_rollouts(wl.q0, nom + scale, eps, wl.obstacles(), wl.guidance, up)
+        out.append(b.d_min.copy())
+    path = eng.last_sdf_path()[0]
+    want_kernel = {"thread": 0, "brute": 0, "nochunk": 0, "persist": 0, "warp": 1, "cta": 2}[mode]
+    assert path["kernel"] == want_kernel, (mode, path)
+    if mode == "persist":
+        assert path["persistent"] == 1
+    eng.close()
+    return np.concatenate([o.reshape(-1) for o in out])
 
 
 @pytest.mark.parametrize("case", list(CASES))

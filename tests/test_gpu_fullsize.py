@@ -1,0 +1,175 @@
+"""Full-size end-to-end parity at the BASELINE.json shapes: libexm_b200.so against the UNMODIFIED
+reference (oracle/_ref: MppiController::control_cycle and evaluate_rollouts, proj/src/
+controller.cpp:178-220, :304-365, run with every host thread), on the exact paths the benchmark
+runs (thread-per-pose k_sdf_grid with h-major lanes, 16-point cull chunks for clouds of >= 16k
+points, persistent warps for config 5).
+
+Configs 1-3: three consecutive control cycles with device-drawn noise, the reference's own
+controller object stepping beside the GPU from the same start pose; every cycle also compares
+all K*T per-pose minima and all K rollout costs with the reference's evaluate_rollouts on the
+same state and noise. Config 5 (K=65,536, T=80, N=50k: ~10 min of reference CPU time per cycle)
+is checked on the top 512 rollouts by GPU cost plus 2,000 seeded random rollouts, evaluated by
+the reference at the full cloud.
+
+Tolerances: sd |d - d_ref| <= 1e-5 max(|d_ref|, 1 m); signs exact where
+|d_ref| >= 1e-5; costs 1e-5 relative except cost-cliff-degenerate rollouts (a step within 1e-5 m
+of d = 0 or d = d_safe); argmin exact unless the argmin rollout is degenerate or the top two
+augmented costs tie within 1e-9 relative; command / nominal 1e-5; beta, entropy, nominal cost
+1e-5 relative. The kernel path each config ran is logged to gpurun_out/fullsize_paths.json."""
+import json
+import os
+
+import numpy as np
+import pytest
+
+from paper_2605_29663_b200 import workloads as W
+from paper_2605_29663_b200.api import Engine
+from tests import oracle_bindings as ob
+
+pytestmark = [pytest.mark.gpu, pytest.mark.reference]
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+DEG = 1e-5
+THREADS = os.cpu_count() or 1
+
+
+def sd_err(got, want):
+    got, want = np.asarray(got, np.float64), np.asarray(want, np.float64)
+    return float(np.max(np.abs(got - want) / np.maximum(np.abs(want), 1.0)))
+
+
+def sign_mismatch(got, want):
+    m = np.abs(want) >= DEG
+    return int(np.count_nonzero((got[m] < 0) != (want[m] < 0)))
+
+
+def degenerate_rows(dmin_ref, d_safe):
+    return ((np.abs(dmin_ref) < DEG) | (np.abs(dmin_ref - d_safe) < DEG)).any(axis=1)
+
+
+def log_path(cfg, eng, extra=None):
+    roll, val = eng.last_sdf_path()
+    os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
+    fn = os.path.join(ROOT, "gpurun_out", "fullsize_paths.json")
+    data = json.load(open(fn)) if os.path.exists(fn) else {}
+    data[cfg] = {"rollout_sdf": roll, "validation_sdf": val, **(extra or {})}
+    json.dump(data, open(fn, "w"), indent=1)
+    print(cfg, "rollout SDF path", roll, "validation", val, extra or "")
+    return roll
+
+
+def check_rollouts(wl, got, want):
+    K, T = wl.params.rollouts, wl.params.horizon
+    assert got.d_min.shape == want["d_min"].shape
+    assert sd_err(got.d_min, want["d_min"]) <= 1e-5
+    assert sign_mismatch(got.d_min, want["d_min"]) == 0
+    deg = degenerate_rows(want["d_min"], wl.params.d_safe)
+    ok = ~deg
+    rel = np.abs(got.costs - want["costs"]) / np.maximum(np.abs(want["costs"]), 1.0)
+    assert np.max(rel[ok]) <= 1e-5, np.max(rel[ok])
+    assert np.array_equal(got.unsafe[ok], want["unsafe"][ok])
+    return deg
+
+
+PATHS = {  # expected rollout kernel: thread per pose above 40k poses, chunk 16 from 16k points
+    "cfg1": {"kernel": 1, "chunk": 8},             # 30,720 poses: warp per pose
+    "cfg2": {"kernel": 0, "chunk": 8, "hmajor": 1},
+    "cfg3": {"kernel": 0, "chunk": 16, "hmajor": 1},
+}
+CFGS = {"cfg1": W.cfg1, "cfg2": W.cfg2, "cfg3": W.cfg3}
+
+
+@pytest.mark.skipif(not ob.reference_available(), reason="oracle/_ref not built")
+@pytest.mark.parametrize("cfg", list(CFGS))
+def test_fullsize_control_cycles_vs_reference(cfg):
+    wl = CFGS[cfg]()
+    p = wl.params
+    D = wl.model.control_dim()
+    eng = Engine(wl.model, wl.limits, wl.footprint, p, n_cap=wl.n_points, guide_cap=8)
+    ref = ob.Reference(wl.footprint, wl.model, wl.limits, p, threads=THREADS)
+    ref.set_cloud(wl.cloud)
+    orc = ob.Oracle(wl.footprint, wl.model, wl.limits, p)
+    nom, up = wl.zero_state()
+    q = wl.q0.copy()
+    skipped = []
+    for cyc in range(3):
+        eps = ref.sample_perturbations(p.seed, cyc)  # what the reference controller draws
+        want = ref.evaluate_rollouts(q, nom, eps, wl.cloud, None, wl.guidance, up)
+        got = eng.evaluate_rollouts(q, nom, eps, wl.obstacles(), wl.guidance, up)
+        deg = check_rollouts(wl, got, want)
+        if cyc == 0:
+            roll = log_path(cfg, eng, {"K": p.rollouts, "T": p.horizon, "N": wl.n_points})
+            for k, v in PATHS[cfg].items():
+                assert roll[k] == v, (cfg, roll)
+        aug = want["costs"] + p.w_inf * want["unsafe"]
+        r_arg = int(np.argmin(aug))
+        srt = np.sort(aug)
+        tie = abs(srt[1] - srt[0]) <= 1e-9 * max(1.0, abs(srt[0]))
+        g = eng.control_cycle_raw(q, wl.obstacles(), wl.guidance, nom, up, cyc)  # device noise
+        r = ref.controller_cycle(q, None, None, wl.guidance, use_stored_cloud=True)
+        if deg[r_arg] or tie:
+            skipped.append(cyc)
+        else:
+            assert g.argmin == r_arg, (cyc, g.argmin, r_arg)
+            assert np.max(np.abs(g.command - r["command"][:D])) <= 1e-5
+            assert np.max(np.abs(nom - r["nominal"])) <= 1e-5
+            assert abs(g.best_cost - r["best_cost"]) <= 1e-5 * max(1.0, abs(r["best_cost"]))
+            assert abs(g.weight_entropy - r["weight_entropy"]) <= 1e-5 * max(1.0, r["weight_entropy"])
+        assert g.validated == r["validated"]
+        assert abs(g.nominal_cost - r["nominal_cost"]) <= 1e-5 * max(1.0, abs(r["nominal_cost"]))
+        assert sd_err(g.nominal_d_min, r["nominal_d_min"]) <= 1e-5
+        q = orc.step(q, g.command)
+    assert len(skipped) < 3, "every cycle had a degenerate argmin"
+
+
+@pytest.mark.skipif(not ob.reference_available(), reason="oracle/_ref not built")
+def test_fullsize_cfg5_sampled_vs_reference():
+    wl = W.cfg5()
+    p = wl.params
+    D = wl.model.control_dim()
+    K, T = p.rollouts, p.horizon
+    eng = Engine(wl.model, wl.limits, wl.footprint, p, n_cap=wl.n_points, guide_cap=8)
+    nom, up = wl.zero_state()
+    eps = eng.sample_perturbations(p.seed, 0)
+    got = eng.evaluate_rollouts(wl.q0, nom, eps, wl.obstacles(), wl.guidance, up)
+    roll = log_path("cfg5", eng, {"K": K, "T": T, "N": wl.n_points, "sampled_rollouts": 2512})
+    assert roll["kernel"] == 0 and roll["chunk"] == 16 and roll["persistent"] == 1, roll
+    aug_g = got.costs + p.w_inf * got.unsafe
+    order = np.argsort(aug_g, kind="stable")
+    rng = np.random.default_rng(5)
+    sample = np.unique(np.concatenate([order[:512], rng.choice(K, 2000, replace=False)]))
+    import dataclasses
+    ps = dataclasses.replace(p)
+    ps.rollouts = int(sample.size)
+    ref = ob.Reference(wl.footprint, wl.model, wl.limits, ps, threads=THREADS)
+    want = ref.evaluate_rollouts(wl.q0, nom, eps[sample], wl.cloud, None, wl.guidance, up)
+    sub = type(got)(int(sample.size), T, eps[sample], got.controls[sample], got.states[sample],
+                    got.d_min[sample], got.costs[sample], got.unsafe[sample])
+    assert np.array_equal(sub.controls, want["controls"])
+    deg = check_rollouts(type("wl", (), {"params": ps})(), sub, want)
+    aug_r = want["costs"] + p.w_inf * want["unsafe"]
+    j = int(np.argmin(aug_r))
+    srt = np.sort(aug_r)
+    if not deg[j] and abs(srt[1] - srt[0]) > 1e-9 * max(1.0, abs(srt[0])):
+        assert int(sample[j]) == int(order[0])
+    # The full step on the same noise. Reference update (controller.cpp:314-340): weights of the
+    # augmented costs (the reference's costs on the sample, which holds the top 512 rollouts;
+    # the GPU's elsewhere, whose weights are below exp(-gap) and verified on the random rows),
+    # u = nominal + sum w eps, clamped sequentially from u_prev; the command is u[0] when the
+    # step validates.
+    nom_out, up_out = nom.copy(), up.copy()
+    d = eng.control_cycle_raw(wl.q0, wl.obstacles(), wl.guidance, nom_out, up_out, 0, eps)
+    assert d.argmin == int(order[0])
+    mixed = aug_g.copy()
+    mixed[sample] = aug_r
+    assert abs(d.best_cost - mixed.min()) <= 1e-5 * max(1.0, abs(mixed.min()))
+    w = ob.oracle_weights(mixed, p.lambda_)
+    u = nom.reshape(T, D) + np.einsum("r,rtd->td", w, eps)
+    orc = ob.Oracle(wl.footprint, wl.model, wl.limits, p)
+    prev = up[:D].copy()
+    for h in range(T):
+        u[h] = orc.clamp_control(u[h], prev)
+        prev = u[h]
+    if d.validated:
+        assert np.max(np.abs(d.command - u[0])) <= 1e-5
+        assert np.max(np.abs(nom_out.reshape(T, D) - np.vstack([u[1:], u[-1:]]))) <= 1e-5

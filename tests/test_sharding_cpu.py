@@ -9,7 +9,7 @@ import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
-from paper_2605_29663_b200 import sharding as S
+from tests import sharding_model as S
 from paper_2605_29663_b200 import workloads as W
 from tests import oracle_bindings as ob
 
