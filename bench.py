@@ -450,6 +450,7 @@ def run_ours(args, world, rank, local):
         line["sdf_batch"] = bench_sdf_batch(args, torch, peak, peak_src)
     if rank == 0 and not args.no_sdf_batch:
         line["hybrid"] = bench_hybrid(args, torch)
+        line["hybrid_cfg5"] = bench_hybrid_cfg5(args, torch)
         line["sense"] = bench_sense(args, world == 1 and not args.no_cpu_baseline)
     if rank == 0:
         print(json.dumps(line), flush=True)
@@ -518,6 +519,46 @@ def bench_hybrid(args, torch):
     return {"workload": "trap_hybrid 3 families (ackermann/parallel/spin), K=384, T=25, N=400",
             "batched_ms_per_step": 1e3 * batched, "per_family_calls_ms_per_step": 1e3 * seq,
             "speedup": seq / batched}
+
+
+def bench_hybrid_cfg5(args, torch):
+    """Config 5's hybrid variant: three mode families (Ackermann,
+    parallel, spin) x K=65,536 rollouts x T=80 on config 5's 50k-point cloud. One hybrid step =
+    all three families' MPPI steps: batched into one device call (exm_hybrid_cycle: one cloud
+    preparation, one SDF launch over 3 x 5.24M poses) vs one exm_control_cycle per family;
+    wall clock per hybrid step through the host API, selection on the host excluded."""
+    from paper_2605_29663_b200 import workloads as W
+    from paper_2605_29663_b200.api import Engine, HybridController, ObstacleSet
+    fp, modes, params, hp, q0, cloud, g = W.cfg5_hybrid()
+    obst = ObstacleSet(cloud, np.ones(cloud.shape[0], np.uint8))
+    hc = HybridController(modes, fp, params, hp, n_cap=cloud.shape[0], guide_cap=8)
+    singles = []
+    for m, mode in enumerate(modes):
+        p = W.MppiParams(**{**params.__dict__})
+        p.seed = params.seed ^ ((0x9E3779B97F4A7C15 * (m + 1)) & 0xFFFFFFFFFFFFFFFF)
+        e = Engine(mode.model, mode.limits, fp, p, n_cap=cloud.shape[0], guide_cap=8)
+        singles.append((e, np.zeros(params.horizon * mode.model.control_dim()), np.zeros(3)))
+    n = 10
+    for _ in range(3):
+        hc.family_cycles(q0, obst, g)
+    t0 = time.perf_counter()
+    for _ in range(n):
+        hc.family_cycles(q0, obst, g)
+    batched = (time.perf_counter() - t0) / n
+    for c in range(3):
+        for e, nom, up in singles:
+            e.control_cycle_raw(q0, obst, g, nom, up, c)
+    t0 = time.perf_counter()
+    for c in range(n):
+        for e, nom, up in singles:
+            e.control_cycle_raw(q0, obst, g, nom, up, 3 + c)
+    seq = (time.perf_counter() - t0) / n
+    hc.close()
+    for e, _, _ in singles:
+        e.close()
+    return {"workload": "cfg5 hybrid: 3 families (ackermann/parallel/spin) x K=65536, T=80, N=50k",
+            "batched_ms_per_step": 1e3 * batched, "per_family_calls_ms_per_step": 1e3 * seq,
+            "speedup": seq / batched, "hybrid_steps_per_s": 1.0 / batched}
 
 
 def bench_sense(args, with_cpu):

@@ -279,8 +279,11 @@ enum {
   EXM_OPT_AUTO_CAPS = 2,   /* 1: derive per-step SDF caps from each step's own d_min statistic */
   EXM_OPT_PREGEN = 3,      /* 0: no next-cycle noise pregeneration (default 1) */
   EXM_OPT_HOST_TIMING = 4, /* 1: accumulate exm_control_cycle host phases (exm_host_timing) */
-  EXM_OPT_HOST_THREADS = 5 /* host threads converting batch_signed_distance queries (default:
-                              min(8, hardware threads)); the reference's `threads` argument */
+  EXM_OPT_HOST_THREADS = 5, /* host threads converting batch_signed_distance queries (default:
+                               min(8, hardware threads)); the reference's `threads` argument */
+  EXM_OPT_SDF_MAP = 6       /* lanes <-> poses of the thread-per-pose SDF: 0 tuned on the
+                               handle's first steps (default), 1 a rollout's consecutive steps per
+                               warp, 2 consecutive rollouts at one step per warp */
 };
 /* Signed-distance kernel selection: automatic, or (tests) every bound disabled, no chunk
  * bound, a forced thread / warp / 8-warp-CTA per pose kernel, persistent warps, caps ignored. */

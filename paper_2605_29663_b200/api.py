@@ -655,6 +655,12 @@ class Engine:
         cta, persist, nocap."""
         self.set_option(_abi.OPT_SDF_MODE, _abi.SDF_MODES[mode])
 
+    def set_sdf_map(self, mapping: str):
+        """Lanes <-> poses of the thread-per-pose SDF: "tuned" (default: chosen on the first
+        steps), "rmajor" (a rollout's consecutive steps per warp), "hmajor" (consecutive rollouts
+        at one step per warp)."""
+        self.set_option(_abi.OPT_SDF_MAP, {"tuned": 0, "rmajor": 1, "hmajor": 2}[mapping])
+
     def last_sdf_path(self):
         """What the last rollout / validation SDF launches ran (kernel 0 thread, 1 warp, 2 CTA
         per pose; chunk; persistent; hmajor)."""

@@ -75,7 +75,8 @@ def build_dropin() -> None:
     ref = os.environ.get("REF_DIR", "/root/reference/proj")
     if os.path.isdir(os.path.join(ref, "src")):
         subprocess.run(["make", "-s", "-C", os.path.join(HERE, "host"), f"REF_DIR={ref}", "all",
-                        "acceptance", "scaling"], check=True)
+                        "acceptance", "scaling", "episode", "hybridcheck"],
+                       check=True)
 
 
 if __name__ == "__main__":

@@ -545,6 +545,13 @@ struct exm_handle {
   bool auto_caps = false, pregen = true, host_timing = false;
   // what the last rollout / validation signed-distance launch ran (exm_last_sdf_path)
   SdfPath roll_path{}, val_path{};
+  // lane <-> pose mapping of the thread-per-pose SDF (EXM_OPT_SDF_MAP): 0 tuned per handle (the
+  // first kTuneSteps steps alternate both mappings outside a graph, timed with events), 1 one
+  // rollout's consecutive steps per warp, 2 consecutive rollouts at one step per warp
+  int sdf_map = 0;
+  bool hmajor = false;
+  int tune_n = 0;
+  double tune_ms[2] = {0.0, 0.0};
   // sharding without a communicator (exm_set_shard: several shard handles on one device)
   bool emulated = false;
   cudaStream_t stream = nullptr;
@@ -634,6 +641,7 @@ struct exm_handle {
   float2* bsd_dq = nullptr;
   float* bsd_dd = nullptr;
   cudaEvent_t bsd_ev[kBsdSlots] = {};
+  cudaStream_t bsd_st[kBsdSlots] = {};  // one stream per slot: chunk copies overlap both ways
   int host_threads = 0;  // 0: default
   HostPool* pool = nullptr;
   int launches_per_step = 0;
@@ -728,7 +736,7 @@ exm_status enqueue_post_b(exm_handle* h, cudaStream_t s, int* launches) {
   }
   EXM_CUDA(launch_update(sc, h->d_partials, h->d_nominal, h->d_dyn, h->d_upd, h->d_val_poses,
                          h->d_val_xy, h->d_val_base, out_dec(h), 1, s));
-  EXM_CUDA(launch_sdf_grid(h->fp, h->d_val_poses, sc.T, 0, h->grid, nullptr, h->sdf_mode,
+  EXM_CUDA(launch_sdf_grid(h->fp, h->d_val_poses, sc.T, 0, false, h->grid, nullptr, h->sdf_mode,
                            h->d_val_dmin, &h->val_path, nullptr, s));
   EXM_CUDA(launch_finalize(sc, h->d_val_dmin, h->d_val_xy, h->d_val_base, h->d_upd, h->d_guide,
                            h->guide_cap, h->d_nominal, h->d_dyn, out_dec(h), out_dmin(h),
@@ -752,7 +760,7 @@ exm_status record_ev(cudaEvent_t e, cudaStream_t s, bool capturing) {
 // The rollout SDF of a step (capped by the previous step's per-step statistic when set).
 exm_status enqueue_rollout_sdf(exm_handle* h, cudaStream_t s) {
   const StepConst& sc = h->sc;
-  EXM_CUDA(launch_sdf_grid(h->fp, h->d_poses, sc.k_local * sc.T, sc.T, h->grid, h->d_cap,
+  EXM_CUDA(launch_sdf_grid(h->fp, h->d_poses, sc.k_local * sc.T, sc.T, h->hmajor, h->grid, h->d_cap,
                            h->sdf_mode, h->d_dmin, &h->roll_path, nullptr, s));
   h->roll_path.chunk = chunk_for_capacity(h->n_cap);
   h->val_path.chunk = h->roll_path.chunk;
@@ -792,6 +800,29 @@ exm_status enqueue_step(exm_handle* h, bool draw_noise, const EventPair* ev, cud
   if ((st = enqueue_post(h, s, &launches, pregen)) != EXM_OK) return st;
   if (pregen) EXM_CUDA(cudaStreamWaitEvent(s, h->pg_join, 0));
   h->launches_per_step = launches;
+  return EXM_OK;
+}
+
+// Mapping tuning: steps 0-1 (cold caches, first grid) run r-major unmeasured, then steps 2..5
+// alternate r-major / h-major; the faster total wins and the graphs are captured with it. Only
+// the thread-per-pose kernel has a mapping (small pose sets take the warp kernel: no tuning).
+constexpr int kTuneSteps = 6;
+bool tuning(const exm_handle* h) { return h->sdf_map == 0 && h->tune_n < kTuneSteps; }
+
+exm_status tune_step(exm_handle* h, bool draw_noise, EventPair* ev) {
+  const int t = h->tune_n;
+  h->hmajor = t >= 2 && (t & 1);
+  exm_status st = enqueue_step(h, draw_noise, ev, h->stream, false);
+  if (st != EXM_OK) return st;
+  EXM_CUDA(cudaEventSynchronize(ev->b));
+  float ms = 0.0f;
+  EXM_CUDA(cudaEventElapsedTime(&ms, ev->a, ev->b));
+  if (t >= 2) h->tune_ms[h->hmajor ? 1 : 0] += ms;
+  h->tune_n = h->roll_path.kernel == 0 ? t + 1 : kTuneSteps;
+  if (h->tune_n == kTuneSteps) {
+    h->hmajor = h->roll_path.kernel == 0 && h->tune_ms[1] < h->tune_ms[0];
+    destroy_graphs(h);
+  }
   return EXM_OK;
 }
 
@@ -1187,6 +1218,8 @@ void exm_destroy(exm_handle* h) {
   delete h->pool;
   for (auto e : h->bsd_ev)
     if (e) cudaEventDestroy(e);
+  for (auto st : h->bsd_st)
+    if (st) cudaStreamDestroy(st);
   void* host[] = {h->h_in_block, h->h_out, h->bsd_hq, h->bsd_hd};
   for (void* p : host)
     if (p) cudaFreeHost(p);
@@ -1227,7 +1260,8 @@ exm_status exm_control_cycle(exm_handle* h, const double q0[3], const double* pt
     if (st != EXM_OK) return st;
   }
   ht.mark(0);
-  st = launch_graph(h, eps_or_null ? 1 : 0, h->step_ev);
+  st = tuning(h) ? tune_step(h, eps_or_null == nullptr, &h->step_ev)
+                 : launch_graph(h, eps_or_null ? 1 : 0, h->step_ev);
   if (st != EXM_OK) return st;
   EXM_CUDA(cudaMemcpyAsync(h->h_out, h->d_out, h->out_bytes, cudaMemcpyDeviceToHost, h->stream));
   ht.mark(1);
@@ -1322,7 +1356,7 @@ exm_status exm_validate_nominal(exm_handle* h, const double* nominal, const doub
   EXM_CUDA(launch_cloud_prep(h->d_pts, h->d_mask, h->d_dyn, h->fp.radius, h->grid, h->n_cap, s));
   EXM_CUDA(launch_update(sc, nullptr, h->d_nominal, h->d_dyn, h->d_upd, h->d_val_poses,
                          h->d_val_xy, h->d_val_base, out_dec(h), 0, s));
-  EXM_CUDA(launch_sdf_grid(h->fp, h->d_val_poses, sc.T, 0, h->grid, nullptr, h->sdf_mode,
+  EXM_CUDA(launch_sdf_grid(h->fp, h->d_val_poses, sc.T, 0, false, h->grid, nullptr, h->sdf_mode,
                            h->d_val_dmin, &h->val_path, nullptr, s));
   EXM_CUDA(launch_finalize(sc, h->d_val_dmin, h->d_val_xy, h->d_val_base, h->d_upd, h->d_guide,
                            h->guide_cap, h->d_nominal, h->d_dyn, out_dec(h), out_dmin(h), nullptr,
@@ -1428,6 +1462,8 @@ exm_status ensure_bsd(exm_handle* h, int chunk) {
   EXM_CUDA(dalloc(&h->bsd_dd, n));
   for (auto& e : h->bsd_ev)
     if (!e) EXM_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  for (auto& st : h->bsd_st)
+    if (!st) EXM_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
   h->bsd_chunk = chunk;
   return EXM_OK;
 }
@@ -1469,22 +1505,23 @@ exm_status exm_sdf_batch(exm_handle* h, const double* poses, int32_t n_poses,
 
 // batch_signed_distance as a host-to-host pipeline: chunks of queries are rounded to FP32 into
 // pinned staging by the host pool while earlier chunks are copied, evaluated (k_sdf_points) and
-// copied back; results are widened to FP64 into the caller's array as their chunks complete.
+// copied back, each slot on its own stream (so one chunk's upload overlaps another's download);
+// results are widened to FP64 into the caller's array as their chunks complete.
 // Host traffic per query: 16 B read + 8 B pinned write in, 4 B pinned read + 8 B write out; link
-// traffic 8 B in + 4 B out.
+// traffic 8 B in + 4 B out. Chunks: up to 8 of at least 64k queries (fixed per-chunk costs:
+// three async calls, one event, one pool dispatch); small chunks convert on the calling thread.
 exm_status exm_batch_signed_distance(exm_handle* h, const double* queries, int32_t n, double* out) {
   if (!h || (n > 0 && (!queries || !out))) return fail(EXM_ERR_INVALID_ARGUMENT, "null argument");
   if (n < 0) return fail(EXM_ERR_INVALID_ARGUMENT, "negative query count");
   if (n == 0) return EXM_OK;
   std::lock_guard<std::mutex> lk(h->mu);
   EXM_CUDA(cudaSetDevice(h->device));
-  // about 8 chunks per call (pipeline depth), 16k..256k queries each
-  const int chunk = std::min(std::max((n + 7) / 8, 16384), 262144);
+  const int nchunks = std::min(8, std::max(1, (n + 65535) / 65536));
+  const int chunk = ((n + nchunks - 1) / nchunks + 1023) & ~1023;
   exm_status st = ensure_bsd(h, chunk);
   if (st != EXM_OK) return st;
-  const int nchunks = (n + chunk - 1) / chunk;
-  const int parts = h->pool->size();
-  cudaStream_t s = h->stream;
+  // pieces per conversion: ~16k queries each, at most the pool's threads
+  const int parts = std::max(1, std::min(h->pool->size(), chunk / 16384));
   auto to_f32 = [&](int c, int part) {  // queries of chunk c -> pinned slot, piece `part`
     const size_t c0 = static_cast<size_t>(c) * chunk;
     const size_t m = std::min<size_t>(chunk, static_cast<size_t>(n) - c0);
@@ -1501,23 +1538,23 @@ exm_status exm_batch_signed_distance(exm_handle* h, const double* queries, int32
     const float* src = h->bsd_hd + static_cast<size_t>(c % kBsdSlots) * chunk;
     for (size_t i = a; i < b; ++i) out[c0 + i] = static_cast<double>(src[i]);
   };
-  for (int c = 0; c <= nchunks; ++c) {
-    // the slot chunk c reuses held chunk c - kBsdSlots: drain it first
+  for (int c = 0; c < nchunks; ++c) {
+    // the slot chunk c reuses held chunk c - kBsdSlots: drain it (widen its results) first
     const int drain = c - kBsdSlots;
-    const int last = c == nchunks;
     if (drain >= 0) EXM_CUDA(cudaEventSynchronize(h->bsd_ev[drain % kBsdSlots]));
-    if (last) break;
     h->pool->run(2 * parts, [&](int t) {
       if (t < parts) to_f32(c, t);
       else if (drain >= 0) to_f64(drain, t - parts);
     });
     const size_t c0 = static_cast<size_t>(c) * chunk;
     const int m = static_cast<int>(std::min<size_t>(chunk, static_cast<size_t>(n) - c0));
-    const size_t so = static_cast<size_t>(c % kBsdSlots) * chunk;
+    const int slot = c % kBsdSlots;
+    const size_t so = static_cast<size_t>(slot) * chunk;
+    cudaStream_t s = h->bsd_st[slot];
     EXM_CUDA(cudaMemcpyAsync(h->bsd_dq + so, h->bsd_hq + so, m * sizeof(float2), cudaMemcpyHostToDevice, s));
     EXM_CUDA(launch_sdf_points(h->fp, h->bsd_dq + so, m, h->bsd_dd + so, s));
     EXM_CUDA(cudaMemcpyAsync(h->bsd_hd + so, h->bsd_dd + so, m * sizeof(float), cudaMemcpyDeviceToHost, s));
-    EXM_CUDA(cudaEventRecord(h->bsd_ev[c % kBsdSlots], s));
+    EXM_CUDA(cudaEventRecord(h->bsd_ev[slot], s));
   }
   // the last min(kBsdSlots, nchunks) chunks
   for (int c = std::max(0, nchunks - kBsdSlots); c < nchunks; ++c) {
@@ -1680,7 +1717,7 @@ exm_status exm_run_resident(exm_handle* h, int32_t n_steps) {
     EventPair* ev = nullptr;
     exm_status st = next_ring_slot(h, &ev);
     if (st != EXM_OK) return st;
-    if ((st = launch_graph(h, 0, *ev)) != EXM_OK) return st;
+    if ((st = tuning(h) ? tune_step(h, true, ev) : launch_graph(h, 0, *ev)) != EXM_OK) return st;
   }
   h->last_steps = n_steps;
   h->last_pairs = static_cast<int64_t>(h->sc.k_local) * h->T * h->h_dyn->n_points;
@@ -1834,7 +1871,7 @@ exm_status exm_sdf_work_stats(exm_handle* h, int64_t* counts) {
   cudaStream_t s = h->stream;
   cudaError_t e = cudaMemsetAsync(d, 0, kCntN * sizeof(unsigned long long), s);
   if (e == cudaSuccess)
-    e = launch_sdf_grid(h->fp, h->d_poses, h->sc.k_local * h->T, h->T, h->grid, h->d_cap,
+    e = launch_sdf_grid(h->fp, h->d_poses, h->sc.k_local * h->T, h->T, h->hmajor, h->grid, h->d_cap,
                         h->sdf_mode, h->d_dmin, nullptr, d, s);
   if (e == cudaSuccess) e = cudaMemcpyAsync(hv, d, sizeof hv, cudaMemcpyDeviceToHost, s);
   if (e == cudaSuccess) e = cudaStreamSynchronize(s);
@@ -1864,6 +1901,13 @@ exm_status exm_set_option(exm_handle* h, int32_t option, int32_t value) {
       h->sdf_mode = value;
       break;
     case EXM_OPT_AUTO_CAPS: h->auto_caps = value != 0; break;
+    case EXM_OPT_SDF_MAP:
+      if (value < 0 || value > 2) return fail(EXM_ERR_INVALID_ARGUMENT, "unknown SDF mapping");
+      h->sdf_map = value;
+      h->hmajor = value == 2;
+      h->tune_n = 0;
+      h->tune_ms[0] = h->tune_ms[1] = 0.0;
+      break;
     case EXM_OPT_PREGEN: h->pregen = value != 0; break;
     case EXM_OPT_HOST_TIMING:
       h->host_timing = value != 0;
@@ -1968,7 +2012,7 @@ exm_status hybrid_enqueue(exm_hybrid* hy, cudaStream_t s0) {
   }
   for (int m = 1; m < hy->M; ++m) EXM_CUDA(cudaStreamWaitEvent(s0, hy->pre_done[m], 0));
   EXM_CUDA(cudaStreamWaitEvent(s0, hy->prep_done, 0));
-  EXM_CUDA(launch_sdf_grid(f0->fp, hy->poses_all, hy->M * hy->K * hy->T, hy->T, f0->grid,
+  EXM_CUDA(launch_sdf_grid(f0->fp, hy->poses_all, hy->M * hy->K * hy->T, hy->T, f0->hmajor, f0->grid,
                            nullptr, f0->sdf_mode, hy->dmin_all, &f0->roll_path, nullptr, s0));
   EXM_CUDA(cudaEventRecord(hy->sdf_done, s0));
   for (int m = 0; m < hy->M; ++m) {

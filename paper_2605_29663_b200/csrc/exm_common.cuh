@@ -220,11 +220,12 @@ cudaError_t launch_rollout(const StepConst& sc, const StepDyn* dyn, const double
                            cudaStream_t s);
 // Per-pose minimum signed distance over the prepared cloud (min_signed_distance_at).
 // Rollout poses are stored [row][T] (rows = n_poses / T rollouts); T = 0 for an unstructured
-// pose list. cap (optional, T floats): a guess of each step's minimum distance; the kernel
+// pose list. hmajor: a warp's lanes take 32 consecutive rows at one step h (else 32
+// consecutive steps of one row); which is faster depends on the scene (exm_abi.cu tunes it). cap (optional, T floats): a guess of each step's minimum distance; the kernel
 // stays exact for any cap (capped pass, then an uncapped pass for the poses it did not
 // resolve). mode: kSdf*; path (optional) receives what ran; stats (optional, kCntN counters):
 // a statistics build of the same launch.
-cudaError_t launch_sdf_grid(const FpDev& fp, const float4* poses, int n_poses, int T,
+cudaError_t launch_sdf_grid(const FpDev& fp, const float4* poses, int n_poses, int T, bool hmajor,
                             const CloudGrid& g, const float* cap, int mode, float* out,
                             SdfPath* path, unsigned long long* stats, cudaStream_t s);
 cudaError_t launch_rollout_costs(const StepConst& sc, const StepDyn* dyn, const double* guide,

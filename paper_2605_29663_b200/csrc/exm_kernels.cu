@@ -101,6 +101,17 @@ __device__ __forceinline__ float min3f(float a, float b, float c) {
   return r;
 }
 
+// Cover-box loops run over fp.ncover boxes (uniform: the footprint table is a kernel parameter;
+// the L takes 2 of the kMaxCover slots). -DEXM_COVER_ALL_SLOTS: all slots, unused ones repeating
+// box 0 (round 1; A/B builds).
+__device__ __forceinline__ bool cover_slot(const FpDev& fp, int j) {
+#ifdef EXM_COVER_ALL_SLOTS
+  return true;
+#else
+  return j == 0 || j < fp.ncover;
+#endif
+}
+
 // ------------------------------------------------------------------ FP32 signed distance
 // Polygon edge step (PreparedFootprint::sd polygon branch, geometry.cpp:273-292).
 //   t  = sat(p.e/|e|^2 - v.e/|e|^2)           2 FFMA (second .SAT)
@@ -232,6 +243,7 @@ __device__ __forceinline__ bool cover_may_beat(const FpDev& fp, float bx, float 
   float d2 = __int_as_float(0x7f800000);
 #pragma unroll
   for (int j = 0; j < kMaxCover; ++j) {
+    if (!cover_slot(fp, j)) break;
     const float ax = fmaxf(fabsf(bx - fp.cover[j][0]) - fp.cover[j][2], 0.f);
     const float ay = fmaxf(fabsf(by - fp.cover[j][1]) - fp.cover[j][3], 0.f);
     d2 = fminf(d2, fmaf(ax, ax, ay * ay));
@@ -253,6 +265,7 @@ __device__ __forceinline__ bool tiles_exterior_d2(const FpDev& fp, float bx, flo
   float d2u = __int_as_float(0x7f800000), inm = __int_as_float(0x7f800000);
 #pragma unroll
   for (int j = 0; j < kMaxCover; ++j) {
+    if (!cover_slot(fp, j)) break;
     const float ax = fabsf(bx - fp.cbox[j][0]) - fp.cbox[j][2];
     const float ay = fabsf(by - fp.cbox[j][1]) - fp.cbox[j][3];
     const float ox = fmaxf(ax, 0.f), oy = fmaxf(ay, 0.f);
@@ -322,6 +335,7 @@ __device__ __forceinline__ bool chunk_may_beat(const FpDev& fp, float4 q, float4
   float d2 = __int_as_float(0x7f800000);
 #pragma unroll
   for (int j = 0; j < kMaxCover; ++j) {
+    if (!cover_slot(fp, j)) break;
     const float ax = fmaxf(fabsf(bx - fp.cover[j][0]) - (fp.cover[j][2] + ex), 0.f);
     const float ay = fmaxf(fabsf(by - fp.cover[j][1]) - (fp.cover[j][3] + ey), 0.f);
     d2 = fminf(d2, fmaf(ax, ax, ay * ay));
@@ -726,18 +740,18 @@ __device__ __forceinline__ void sdf_grid_warp(const FpDev& fp, const float4* __r
   // h-major lanes: the poses are stored [row][h] (row = rollout); with rows > 0 logical index
   // i = h * rows + row, so a warp takes 32 consecutive rollouts at the same step h (spatially
   // coherent: one set of ring cells serves all lanes) instead of one rollout's 32 steps
-  int hh = 0, p = i;
+  int hh = 0, pi = i;
   if (rows > 0) {
     hh = i / rows;
-    p = (i - hh * rows) * T + hh;
+    pi = (i - hh * rows) * T + hh;
   } else if (T > 0) {
     hh = i % T;
   }
   if (gm.n_valid == 0) {
-    if (active) out[p] = kEmptyDistance;
+    if (active) out[pi] = kEmptyDistance;
     return;
   }
-  const float4 q = active ? poses[p] : make_float4(0.f, 0.f, 1.f, 0.f);
+  const float4 q = active ? poses[pi] : make_float4(0.f, 0.f, 1.f, 0.f);
   float sx = active ? q.x : 0.f, sy = active ? q.y : 0.f;
   int na = active ? 1 : 0;
   for (int o = 16; o; o >>= 1) {
@@ -853,7 +867,7 @@ __device__ __forceinline__ void sdf_grid_warp(const FpDev& fp, const float4* __r
     }  // groups of 32 ring cells
   }
   }  // pass
-  if (active) out[p] = best;
+  if (active) out[pi] = best;
 }
 
 // Persistent warps: the grid is sized to the resident capacity and every warp takes the next
@@ -1370,12 +1384,17 @@ int persistent_blocks(K kernel, int threads) {
   return blocks[dev];
 }
 
+#ifdef EXM_PERSIST_WAVES  // A/B builds
+constexpr int kPersistentWaves = EXM_PERSIST_WAVES;
+#else
 constexpr int kPersistentWaves = 8;
+#endif
 constexpr int kGridThreads = 128;  // 32-128 measured within 1 % (round 1)
 
 template <int KIND, int NB, bool STATS, int MODE>
 cudaError_t launch_grid_kernel(const FpDev& fp, const float4* poses, int n_poses, int T,
-                               const CloudGrid& g, const float* cap, bool persist, float* out,
+                               bool hmajor, const CloudGrid& g, const float* cap, bool persist,
+                               float* out,
                                SdfPath* path, unsigned long long* stats, cudaStream_t s) {
   const int threads = kGridThreads;
   const int blocks = (n_poses + threads - 1) / threads;
@@ -1386,12 +1405,7 @@ cudaError_t launch_grid_kernel(const FpDev& fp, const float4* poses, int n_poses
   const int cap_blocks = persistent_blocks(k, threads);
   unsigned* work = (persist || blocks >= kPersistentWaves * cap_blocks) ? g.work : nullptr;
   const int grid = work ? cap_blocks : blocks;
-  const int rows = (T > 0 && n_poses % T == 0) ? n_poses / T : 0;
-#ifdef EXM_SDF_RMAJOR  // A/B builds: lanes take one rollout's consecutive steps (round 1)
-  const int rows_used = 0;
-#else
-  const int rows_used = rows;
-#endif
+  const int rows_used = (hmajor && T > 0 && n_poses % T == 0) ? n_poses / T : 0;
   if (path) *path = SdfPath{0, 0, work ? 1 : 0, grid, threads, rows_used > 0 ? 1 : 0};
   if (const cudaError_t le = launch_k(k, grid, threads, 0, s, fp, poses, n_poses, g.gm,
                                       g.cell_start, g.cloud, g.chunk, cap, T, rows_used, out, work,
@@ -1403,7 +1417,7 @@ cudaError_t launch_grid_kernel(const FpDev& fp, const float4* poses, int n_poses
 
 template <int KIND, int NB>
 struct GridLaunch {
-  static cudaError_t run(const FpDev& fp, const float4* poses, int n_poses, int T,
+  static cudaError_t run(const FpDev& fp, const float4* poses, int n_poses, int T, bool hmajor,
                          const CloudGrid& g, const float* cap, int mode, float* out,
                          SdfPath* path, unsigned long long* stats, cudaStream_t s) {
     if (n_poses <= 0) return cudaSuccess;
@@ -1411,14 +1425,14 @@ struct GridLaunch {
     if (mode == kSdfNoCap) cap = nullptr;
     if (stats) {
       if (mode == kSdfNoChunk)
-        return launch_grid_kernel<KIND, NB, true, kGridNoChunk>(fp, poses, n_poses, T, g, cap, persist, out, path, stats, s);
-      return launch_grid_kernel<KIND, NB, true, kGridFull>(fp, poses, n_poses, T, g, cap, persist, out, path, stats, s);
+        return launch_grid_kernel<KIND, NB, true, kGridNoChunk>(fp, poses, n_poses, T, hmajor, g, cap, persist, out, path, stats, s);
+      return launch_grid_kernel<KIND, NB, true, kGridFull>(fp, poses, n_poses, T, hmajor, g, cap, persist, out, path, stats, s);
     }
     if (mode == kSdfBrute)
-      return launch_grid_kernel<KIND, NB, false, kGridBrute>(fp, poses, n_poses, T, g, cap, persist, out, path, nullptr, s);
+      return launch_grid_kernel<KIND, NB, false, kGridBrute>(fp, poses, n_poses, T, hmajor, g, cap, persist, out, path, nullptr, s);
     if (mode == kSdfNoChunk)
-      return launch_grid_kernel<KIND, NB, false, kGridNoChunk>(fp, poses, n_poses, T, g, cap, persist, out, path, nullptr, s);
-    return launch_grid_kernel<KIND, NB, false, kGridFull>(fp, poses, n_poses, T, g, cap, persist, out, path, nullptr, s);
+      return launch_grid_kernel<KIND, NB, false, kGridNoChunk>(fp, poses, n_poses, T, hmajor, g, cap, persist, out, path, nullptr, s);
+    return launch_grid_kernel<KIND, NB, false, kGridFull>(fp, poses, n_poses, T, hmajor, g, cap, persist, out, path, nullptr, s);
   }
 };
 
@@ -1509,7 +1523,7 @@ cudaError_t launch_cloud_prep(const double* pts, const uint8_t* mask, const Step
   return cudaGetLastError();
 }
 
-cudaError_t launch_sdf_grid(const FpDev& fp, const float4* poses, int n_poses, int T,
+cudaError_t launch_sdf_grid(const FpDev& fp, const float4* poses, int n_poses, int T, bool hmajor,
                             const CloudGrid& g, const float* cap, int mode, float* out,
                             SdfPath* path, unsigned long long* stats, cudaStream_t s) {
   // Few poses (validation rollout, single queries): one warp (or one 8-warp CTA) per pose keeps
@@ -1518,7 +1532,7 @@ cudaError_t launch_sdf_grid(const FpDev& fp, const float4* poses, int n_poses, i
                                (n_poses <= kWarpPerPoseMax && mode != kSdfThread &&
                                 mode != kSdfBrute && mode != kSdfPersist));
   if (warp) return dispatch_fp<GridWarpLaunch>(fp, poses, n_poses, g, mode == kSdfCta, out, path, s);
-  return dispatch_fp<GridLaunch>(fp, poses, n_poses, T, g, cap, mode, out, path, stats, s);
+  return dispatch_fp<GridLaunch>(fp, poses, n_poses, T, hmajor, g, cap, mode, out, path, stats, s);
 }
 
 cudaError_t launch_pose_prep(const double* poses, int n, double* center, float4* out,

@@ -14,16 +14,17 @@
 // cycle_) stays in the object and crosses the ABI per call.
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <limits>
 #include <map>
 #include <memory>
 #include <mutex>
-#include <sstream>
 #include <stdexcept>
 #include <string>
 #include <vector>
 
+#include "b200_dropin.hpp"
 #include "exactmppi/controller.hpp"
 #include "exm_b200.h"
 
@@ -89,22 +90,26 @@ Config make_config(const PreparedFootprint& f, const MotionModel& m, const Kinem
   c.params.w_progress = p.task.progress;
   c.params.w_ctrl = p.w_ctrl;
   c.params.seed = p.seed;
-  std::ostringstream k;
-  k.precision(17);
-  k << c.fp.kind << ':';
-  for (std::size_t i = 0; i < c.x.size(); ++i)
-    k << c.x[i] << ',' << c.y[i] << ',' << (c.hx.empty() ? 0.0 : c.hx[i]) << ','
-      << (c.hy.empty() ? 0.0 : c.hy[i]) << ';';
-  const unsigned char* raw[] = {reinterpret_cast<const unsigned char*>(&c.model),
-                                reinterpret_cast<const unsigned char*>(&c.limits),
-                                reinterpret_cast<const unsigned char*>(&c.params)};
-  const std::size_t len[] = {sizeof c.model, sizeof c.limits, sizeof c.params};
-  for (int b = 0; b < 3; ++b)
-    for (std::size_t i = 0; i < len[b]; ++i) k << std::hex << static_cast<int>(raw[b][i]);
-  c.key = k.str();
+  // exact byte key (footprint arrays + the POD model / limits / params, zero-initialised so
+  // padding is deterministic): equal keys <=> identical configurations
+  auto put = [&c](const void* p, std::size_t n) {
+    c.key.append(static_cast<const char*>(p), n);
+  };
+  put(&c.fp.kind, sizeof c.fp.kind);
+  for (const auto* v : {&c.x, &c.y, &c.hx, &c.hy}) {
+    const std::size_t n = v->size();
+    put(&n, sizeof n);
+    put(v->data(), n * sizeof(double));
+  }
+  put(&c.model, sizeof c.model);
+  put(&c.limits, sizeof c.limits);
+  put(&c.params, sizeof c.params);
   return c;
 }
 
+// One cached device handle. Shared: a caller keeps the handle it got alive even if another
+// thread's larger cloud replaces the cache slot meanwhile; calls on one handle serialise on the
+// handle's own lock inside the library (include/exm_b200.h, threading).
 struct Cached {
   exm_handle* h = nullptr;
   int n_cap = 0;
@@ -115,23 +120,22 @@ struct Cached {
 };
 
 std::mutex g_mu;
-std::map<std::string, std::unique_ptr<Cached>> g_cache;
+std::map<std::string, std::shared_ptr<Cached>> g_cache;
 
 // Handle for this configuration with room for n points and g guidance vertices.
-exm_handle* handle_for(const Config& c, int n, int g) {
+std::shared_ptr<Cached> handle_for(const Config& c, int n, int g) {
   std::lock_guard<std::mutex> lock(g_mu);
   auto& slot = g_cache[c.key];
-  if (!slot) slot = std::make_unique<Cached>();
-  if (!slot->h || slot->n_cap < n || slot->guide_cap < g) {
-    if (slot->h) exm_destroy(slot->h);
-    slot->h = nullptr;
-    const int ncap = std::max(n, std::max(1024, 2 * slot->n_cap));
+  if (!slot || slot->n_cap < n || slot->guide_cap < g) {
+    auto fresh = std::make_shared<Cached>();
+    const int ncap = std::max(n, std::max(1024, slot ? 2 * slot->n_cap : 0));
     const int gcap = std::max(g, 64);
-    throw_status(exm_create(&c.fp, &c.model, &c.limits, &c.params, ncap, gcap, -1, &slot->h));
-    slot->n_cap = ncap;
-    slot->guide_cap = gcap;
+    throw_status(exm_create(&c.fp, &c.model, &c.limits, &c.params, ncap, gcap, -1, &fresh->h));
+    fresh->n_cap = ncap;
+    fresh->guide_cap = gcap;
+    slot = std::move(fresh);  // the previous handle lives on while a caller still holds it
   }
-  return slot->h;
+  return slot;
 }
 
 // A unit-square footprint for the footprint-free entry points (sample_perturbations).
@@ -302,7 +306,8 @@ std::vector<ControlInput> sample_perturbations(std::uint64_t seed, std::uint64_t
                                                const MotionModel& model, const MppiParams& params) {
   params.validate();
   const Config c = make_config(square_footprint(), model, KinematicLimits{}, params);
-  exm_handle* h = handle_for(c, 1, 1);
+  const auto hc = handle_for(c, 1, 1);
+  exm_handle* h = hc->h;
   const std::size_t n = static_cast<std::size_t>(params.rollouts) * params.horizon;
   std::vector<double> flat(n * model.control_dim());
   throw_status(exm_sample_perturbations(h, seed, cycle, flat.data()));
@@ -323,8 +328,9 @@ RolloutBatch evaluate_rollouts(const Pose2& q0, const NominalSequence& nominal,
     throw std::invalid_argument("perturbation array does not match K*T");
   const Config c = make_config(footprint, model, limits, params);
   const Flat f = flatten(obstacles, guidance);
-  exm_handle* h = handle_for(c, static_cast<int>(obstacles.points.size()),
+  const auto hc = handle_for(c, static_cast<int>(obstacles.points.size()),
                              static_cast<int>(guidance.path.size()));
+  exm_handle* h = hc->h;
   const std::vector<double> eps = flat_controls({perturbations.begin(), perturbations.end()}, D);
   const std::vector<double> nom = flat_controls(nominal.controls, D);
   const double q[3] = {q0.x, q0.y, q0.theta};
@@ -357,8 +363,9 @@ ValidationResult validate_nominal(const NominalSequence& nominal, const Pose2& q
   p.horizon = static_cast<int>(nominal.controls.size());
   const Config c = make_config(footprint, model, limits, p);
   const Flat f = flatten(obstacles, guidance);
-  exm_handle* h = handle_for(c, static_cast<int>(obstacles.points.size()),
+  const auto hc = handle_for(c, static_cast<int>(obstacles.points.size()),
                              static_cast<int>(guidance.path.size()));
+  exm_handle* h = hc->h;
   const std::vector<double> nom = flat_controls(nominal.controls, model.control_dim());
   const double q[3] = {q0.x, q0.y, q0.theta};
   const double up[3] = {u_prev[0], u_prev[1], u_prev[2]};
@@ -372,6 +379,165 @@ ValidationResult validate_nominal(const NominalSequence& nominal, const Pose2& q
   r.valid = valid != 0;
   return r;
 }
+
+// ---------------------------------------------------------------- emulated rollout shards
+// EXM_DROPIN_SHARDS=G (read once): controller steps run as G rollout shards on the one device
+// (exm_set_shard + exm_sharded_cycle: the block partials exchanged as the ranks' all-gather
+// would), for the episode determinism harness across shard counts (host/episode_main.cpp).
+// Configurations whose K is not a multiple of 256*G run unsharded.
+namespace {
+
+int dropin_shards() {
+  static const int g = [] {
+    const char* e = std::getenv("EXM_DROPIN_SHARDS");
+    return e ? std::max(1, std::atoi(e)) : 1;
+  }();
+  return g;
+}
+
+struct ShardSet {
+  std::vector<exm_handle*> h;
+  int n_cap = 0, guide_cap = 0;
+  ~ShardSet() {
+    for (auto* x : h)
+      if (x) exm_destroy(x);
+  }
+};
+std::mutex g_sh_mu;
+std::map<std::string, std::shared_ptr<ShardSet>> g_sh_cache;
+
+std::shared_ptr<ShardSet> shards_for(const Config& c, int G, int n, int g) {
+  std::lock_guard<std::mutex> lock(g_sh_mu);
+  auto& slot = g_sh_cache[c.key];
+  if (!slot || slot->n_cap < n || slot->guide_cap < g) {
+    auto fresh = std::make_shared<ShardSet>();
+    fresh->n_cap = std::max(n, std::max(1024, slot ? 2 * slot->n_cap : 0));
+    fresh->guide_cap = std::max(g, 64);
+    fresh->h.assign(static_cast<std::size_t>(G), nullptr);
+    for (int r = 0; r < G; ++r) {
+      throw_status(exm_create(&c.fp, &c.model, &c.limits, &c.params, fresh->n_cap,
+                              fresh->guide_cap, -1, &fresh->h[static_cast<std::size_t>(r)]));
+      throw_status(exm_set_shard(fresh->h[static_cast<std::size_t>(r)], r, G));
+    }
+    slot = std::move(fresh);
+  }
+  return slot;
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------- batched hybrid families
+namespace {
+
+// A decision computed by a batched hybrid step for one family, waiting for that family's
+// control_cycle call on the same inputs (same thread).
+struct Parked {
+  const MppiController* who = nullptr;
+  const ObstacleSet* obstacles = nullptr;
+  const Guidance* guidance = nullptr;
+  Pose2 q0{};
+  std::uint64_t cycle = 0;
+  ControlDecision decision;
+  std::vector<double> nominal;  // T x dim, after the step
+};
+thread_local std::vector<Parked> t_parked;
+
+struct HybridCached {
+  exm_hybrid* h = nullptr;
+  int n_cap = 0, guide_cap = 0;
+  ~HybridCached() {
+    if (h) exm_hybrid_destroy(h);
+  }
+};
+std::mutex g_hy_mu;
+std::map<std::string, std::shared_ptr<HybridCached>> g_hy_cache;
+
+}  // namespace
+
+namespace b200 {
+
+bool run_hybrid_batch(const std::vector<const MppiController*>& families,
+                      const std::vector<KinematicLimits>& limits, const FootprintSpec& footprint,
+                      const MppiParams& base_params, const Pose2& q0,
+                      const ObstacleSet& obstacles, const Guidance& guidance) {
+  t_parked.clear();
+  const std::size_t M = families.size();
+  if (M == 0 || limits.size() != M) return false;
+  const std::uint64_t cycle = families[0]->cycle_index();
+  for (const auto* f : families)
+    if (f->cycle_index() != cycle || f->params().horizon != base_params.horizon ||
+        f->params().rollouts != base_params.rollouts)
+      return false;
+  const int T = base_params.horizon;
+  // configuration key: the footprint + every family's model and limits + the base params
+  const Config c0 = make_config(prepare(footprint), families[0]->model(), limits[0], base_params);
+  std::string key = c0.key;
+  std::vector<exm_model> models(M);
+  std::vector<exm_limits> lims(M);
+  for (std::size_t m = 0; m < M; ++m) {
+    const Config cm = make_config(prepare(footprint), families[m]->model(), limits[m], base_params);
+    models[m] = cm.model;
+    lims[m] = cm.limits;
+    key.append(reinterpret_cast<const char*>(&models[m]), sizeof(exm_model));
+    key.append(reinterpret_cast<const char*>(&lims[m]), sizeof(exm_limits));
+  }
+  const int n = static_cast<int>(obstacles.points.size());
+  const int g = static_cast<int>(guidance.path.size());
+  std::shared_ptr<HybridCached> hc;
+  {
+    std::lock_guard<std::mutex> lock(g_hy_mu);
+    auto& slot = g_hy_cache[key];
+    if (!slot || slot->n_cap < n || slot->guide_cap < g) {
+      auto fresh = std::make_shared<HybridCached>();
+      const int ncap = std::max(n, std::max(1024, slot ? 2 * slot->n_cap : 0));
+      const int gcap = std::max(g, 64);
+      throw_status(exm_hybrid_create(&c0.fp, models.data(), lims.data(), static_cast<int32_t>(M),
+                                     &c0.params, ncap, gcap, -1, &fresh->h));
+      fresh->n_cap = ncap;
+      fresh->guide_cap = gcap;
+      slot = std::move(fresh);
+    }
+    hc = slot;
+  }
+  const Flat f = flatten(obstacles, guidance);
+  std::vector<double> noms(M * static_cast<std::size_t>(T) * 3, 0.0), ups(3 * M, 0.0);
+  for (std::size_t m = 0; m < M; ++m) {
+    const int D = families[m]->model().control_dim();
+    const auto& u = families[m]->nominal().controls;
+    for (int h = 0; h < T; ++h)
+      for (int k = 0; k < D; ++k) noms[m * T * 3 + h * D + k] = u[static_cast<std::size_t>(h)][k];
+    for (int k = 0; k < D; ++k) ups[3 * m + k] = families[m]->last_command()[k];
+  }
+  std::vector<exm_decision> out(M);
+  std::vector<std::vector<double>> dmins(M, std::vector<double>(static_cast<std::size_t>(T)));
+  for (std::size_t m = 0; m < M; ++m) out[m].nominal_dmin = dmins[m].data();
+  const double q[3] = {q0.x, q0.y, q0.theta};
+  throw_status(exm_hybrid_cycle(hc->h, q, f.pts.data(), f.mask.data(), n, f.guide.data(), g,
+                                f.goal, noms.data(), ups.data(), cycle, out.data()));
+  for (std::size_t m = 0; m < M; ++m) {
+    const MotionModel& model = families[m]->model();
+    const int D = model.control_dim();
+    Parked p;
+    p.who = families[m];
+    p.obstacles = &obstacles;
+    p.guidance = &guidance;
+    p.q0 = q0;
+    p.cycle = cycle;
+    p.decision.command = ControlInput::zero(model);
+    for (int k = 0; k < D; ++k) p.decision.command[k] = out[m].command[k];
+    p.decision.validated = out[m].validated != 0;
+    p.decision.diagnostics.best_cost = out[m].best_cost;
+    p.decision.diagnostics.weight_entropy = out[m].weight_entropy;
+    p.decision.diagnostics.nominal_cost = out[m].nominal_cost;
+    p.decision.diagnostics.nominal_d_min = std::move(dmins[m]);
+    p.nominal.assign(noms.begin() + static_cast<std::ptrdiff_t>(m * T * 3),
+                     noms.begin() + static_cast<std::ptrdiff_t>(m * T * 3 + T * D));
+    t_parked.push_back(std::move(p));
+  }
+  return true;
+}
+
+}  // namespace b200
 
 MppiController::MppiController(MotionModel model, KinematicLimits limits,
                                const FootprintSpec& footprint, MppiParams params, int threads)
@@ -396,10 +562,28 @@ void MppiController::set_rate_anchor(const ControlInput& u) { u_prev_ = u; }
 ControlDecision MppiController::control_cycle(const Pose2& q0, const ObstacleSet& obstacles,
                                               const Guidance& guidance) {
   const int T = params_.horizon, D = model_.control_dim();
+  for (auto it = t_parked.begin(); it != t_parked.end(); ++it) {  // batched hybrid step
+    if (it->who != this) continue;
+    const bool same = it->obstacles == &obstacles && it->guidance == &guidance &&
+                      it->q0.x == q0.x && it->q0.y == q0.y && it->q0.theta == q0.theta &&
+                      it->cycle == cycle_;
+    if (!same) {
+      t_parked.erase(it);
+      break;
+    }
+    ControlDecision d = std::move(it->decision);
+    nominal_.controls = unflat_controls(it->nominal.data(), static_cast<std::size_t>(T), model_);
+    t_parked.erase(it);
+    d.nominal = nominal_;
+    u_prev_ = d.command;
+    ++cycle_;
+    return d;
+  }
   const Config c = make_config(footprint_, model_, limits_, params_);
   const Flat f = flatten(obstacles, guidance);
-  exm_handle* h = handle_for(c, static_cast<int>(obstacles.points.size()),
+  const auto hc = handle_for(c, static_cast<int>(obstacles.points.size()),
                              static_cast<int>(guidance.path.size()));
+  exm_handle* h = hc->h;
   std::vector<double> nom = flat_controls(nominal_.controls, D);
   double up[3] = {u_prev_[0], u_prev_[1], u_prev_[2]};
   const double q[3] = {q0.x, q0.y, q0.theta};
@@ -407,10 +591,28 @@ ControlDecision MppiController::control_cycle(const Pose2& q0, const ObstacleSet
   d.diagnostics.nominal_d_min.resize(static_cast<std::size_t>(T));
   exm_decision out{};
   out.nominal_dmin = d.diagnostics.nominal_d_min.data();
-  throw_status(exm_control_cycle(h, q, f.pts.data(), f.mask.data(),
-                                 static_cast<int32_t>(obstacles.points.size()), f.guide.data(),
-                                 static_cast<int32_t>(guidance.path.size()), f.goal, nom.data(), up,
-                                 cycle_, nullptr, &out));
+  const int G = dropin_shards();
+  if (G > 1 && params_.rollouts % (256 * G) == 0) {
+    const auto set = shards_for(c, G, static_cast<int>(obstacles.points.size()),
+                                static_cast<int>(guidance.path.size()));
+    std::vector<double> noms, ups;
+    for (int r = 0; r < G; ++r) {
+      noms.insert(noms.end(), nom.begin(), nom.end());
+      ups.insert(ups.end(), up, up + 3);
+    }
+    std::vector<exm_decision> outs(static_cast<std::size_t>(G), out);
+    throw_status(exm_sharded_cycle(set->h.data(), G, q, f.pts.data(), f.mask.data(),
+                                   static_cast<int32_t>(obstacles.points.size()), f.guide.data(),
+                                   static_cast<int32_t>(guidance.path.size()), f.goal,
+                                   noms.data(), ups.data(), cycle_, nullptr, outs.data()));
+    out = outs[0];
+    std::copy(noms.begin(), noms.begin() + static_cast<std::ptrdiff_t>(nom.size()), nom.begin());
+  } else {
+    throw_status(exm_control_cycle(h, q, f.pts.data(), f.mask.data(),
+                                   static_cast<int32_t>(obstacles.points.size()), f.guide.data(),
+                                   static_cast<int32_t>(guidance.path.size()), f.goal, nom.data(),
+                                   up, cycle_, nullptr, &out));
+  }
   d.command = ControlInput::zero(model_);
   for (int k = 0; k < D; ++k) d.command[k] = out.command[k];
   d.validated = out.validated != 0;

@@ -325,3 +325,12 @@ def trap_hybrid(K: int = 384, T: int = 25, N: int = 400):
 
 
 CONFIGS = {"cfg1": cfg1, "cfg2": cfg2, "cfg3": cfg3, "cfg5": cfg5}
+
+
+def cfg5_hybrid(K: int = 65536, T: int = 80, N: int = 50_000, cycle: int = 0):
+    """Config 5's hybrid variant: the trap_hybrid mode families
+    (Ackermann / parallel / spin, M = 3) on config 5's L footprint, cloud and guidance, K rollouts
+    per family. Returns (footprint, modes, params, hybrid params, q0, cloud, guidance)."""
+    wl = cfg5(K=K, T=T, N=N, cycle=cycle)
+    _, modes, _, hp, _, _, _ = trap_hybrid()
+    return (wl.footprint, modes, wl.params, hp, wl.q0, wl.cloud, wl.guidance)

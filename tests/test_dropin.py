@@ -68,3 +68,52 @@ def test_dropin_matches_oracle():
     assert np.max(np.abs(np.array(roll["costs"]) - want["costs"]) / np.maximum(np.abs(want["costs"]), 1)) <= 1e-5
     err = [x for x in lines if x["kind"] == "error"][0]
     assert err["thrown"] == 1 and "lambda must be positive" in err["what"]
+
+
+HYBRID_BIN = os.path.join(ROOT, "paper_2605_29663_b200", "lib", "exm_hybrid_check")
+
+
+@pytest.mark.skipif(not os.path.exists(HYBRID_BIN) or not ob.reference_available(),
+                    reason="hybrid check binary or oracle/_ref not built")
+def test_hybrid_dropin_matches_reference():
+    """HybridController through hybrid_b200.cpp (all mode families of a cycle in one device
+    call, exm_hybrid_cycle) vs the unmodified reference HybridController (hybrid.cpp:95-156, CPU,
+    oracle/_ref) on the reference's trap scenario and sensed cloud: the same mode selection,
+    commands and switch-penalised mode costs, cycle after cycle."""
+    from paper_2605_29663_b200.api import ComponentLimit, HybridMode, HybridParams
+    out = subprocess.run([HYBRID_BIN], capture_output=True, text=True, timeout=300, check=True).stdout
+    lines = [json.loads(x) for x in out.splitlines() if x.startswith("{")]
+    s = lines[0]
+    fp = FootprintSpec.rect_cover(np.stack([s["rect_cx"], s["rect_cy"]], 1),
+                                  np.stack([s["rect_hx"], s["rect_hy"]], 1))
+    modes = []
+    for m in s["modes"]:
+        lim = KinematicLimits.unbounded()
+        v = m["limits"]
+        for i in range(3):
+            lim.component[i] = ComponentLimit(*v[4 * i: 4 * i + 4])
+        lim.steer_max = v[12]
+        model = MotionModel(int(m["tag"]), float(m["wheelbase"]))
+        modes.append(HybridMode(f"m{len(modes)}", model, lim))
+    pv = s["params"]
+    p = MppiParams(rollouts=int(pv[0]), horizon=int(pv[1]), dt=pv[2], lambda_=pv[3],
+                   sigma=tuple(pv[4:7]), d_safe=pv[7], w_coll=pv[8], w_rep=pv[9], w_inf=pv[10],
+                   task=TaskWeights(pv[11], pv[12], pv[13], pv[14]), w_ctrl=pv[15], seed=int(pv[16]))
+    h = s["hybrid"]
+    hp = HybridParams(lambda_switch=h[0], tau_cool_max=int(h[1]), v_min=h[2], omega_min=h[3],
+                      noise_deadzone_v=h[4], noise_deadzone_omega=h[5])
+    ref = ob.ReferenceHybrid(fp, modes, p, hp)
+    pts = np.array(s["points"]).reshape(-1, 2)
+    mask = np.array(s["mask"], np.uint8)
+    g = Guidance(np.array(s["guide"]).reshape(-1, 2), s["goal"])
+    cycles = [x for x in lines if x["kind"] == "cycle"]
+    assert len(cycles) == 8
+    for c in cycles:
+        r = ref.hybrid_cycle(np.array(c["q"]), pts, mask, g)
+        assert c["mode_index"] == r["mode_index"], c["cycle"]
+        assert c["validated"] == int(r["validated"])
+        cmd = np.array(c["command"])
+        assert np.max(np.abs(cmd - r["command"][: cmd.size])) <= 1e-5
+        rc = np.where(np.isfinite(r["mode_costs"]), r["mode_costs"], 1e300)
+        assert np.allclose(c["mode_costs"], rc, rtol=1e-5, atol=1e-5)
+        assert abs(c["nominal_cost"] - r["nominal_cost"]) <= 1e-5 * max(1.0, abs(r["nominal_cost"]))

@@ -91,3 +91,33 @@ def test_capped_minimum_is_bitwise_brute_force(case):
         got = _dmin(wl, "thread", caps)
         bad = np.flatnonzero(got != want)
         assert bad.size == 0, (caps, bad.size)
+
+
+@pytest.mark.parametrize("case", ["cfg2_L12", "cfg3_forklift"])
+def test_lane_mapping_does_not_change_minima(case):
+    """Both lane <-> pose mappings of the thread-per-pose kernel (a rollout's steps per warp /
+    rollouts at one step per warp) and the tuned choice give the same minima bit for bit, and
+    the resident steps after tuning equal the untuned host-API steps."""
+    wl = CASES[case]()
+    outs = {}
+    for mapping in ("rmajor", "hmajor"):
+        eng = Engine(wl.model, wl.limits, wl.footprint, wl.params, n_cap=wl.n_points, guide_cap=8)
+        eng.set_sdf_mode("thread")
+        eng.set_sdf_map(mapping)
+        nom, up = wl.zero_state()
+        eps = eng.sample_perturbations(wl.params.seed, 0)
+        outs[mapping] = eng.evaluate_rollouts(wl.q0, nom, eps, wl.obstacles(), wl.guidance, up).d_min
+        assert eng.last_sdf_path()[0]["hmajor"] == (mapping == "hmajor")
+        eng.close()
+    assert np.array_equal(outs["rmajor"], outs["hmajor"])
+    tuned = Engine(wl.model, wl.limits, wl.footprint, wl.params, n_cap=wl.n_points, guide_cap=8)
+    plain = Engine(wl.model, wl.limits, wl.footprint, wl.params, n_cap=wl.n_points, guide_cap=8)
+    plain.set_sdf_map("rmajor")
+    n1, u1 = wl.zero_state()
+    n2, u2 = wl.zero_state()
+    for cyc in range(8):  # the first 6 steps of `tuned` alternate the mappings outside a graph
+        a = tuned.control_cycle_raw(wl.q0, wl.obstacles(), wl.guidance, n1, u1, cyc)
+        b = plain.control_cycle_raw(wl.q0, wl.obstacles(), wl.guidance, n2, u2, cyc)
+        assert np.array_equal(a.command, b.command) and a.argmin == b.argmin
+        assert np.array_equal(n1, n2)
+    print(case, "tuned mapping:", tuned.last_sdf_path()[0])

@@ -73,8 +73,8 @@ def check_rollouts(wl, got, want):
 
 PATHS = {  # expected rollout kernel: thread per pose above 40k poses, chunk 16 from 16k points
     "cfg1": {"kernel": 1, "chunk": 8},             # 30,720 poses: warp per pose
-    "cfg2": {"kernel": 0, "chunk": 8, "hmajor": 1},
-    "cfg3": {"kernel": 0, "chunk": 16, "hmajor": 1},
+    "cfg2": {"kernel": 0, "chunk": 8},
+    "cfg3": {"kernel": 0, "chunk": 16},
 }
 CFGS = {"cfg1": W.cfg1, "cfg2": W.cfg2, "cfg3": W.cfg3}
 

@@ -6,9 +6,13 @@ Rows per (footprint, query count):
   threads=1 / threads=<nproc>  the unmodified reference's batch_signed_distance (oracle/_ref),
                                wall clock per call, exactly its protocol (3 warm-ups)
   threads=b200-kernel          k_sdf_pairs on device-resident queries, CUDA events per launch
-  threads=b200-call            exm_batch_signed_distance host->host (H2D, kernel, D2H), wall
-                               clock per call — the analogue of the paper's per-call JAX timing
-                               (L 0.09/0.29 ms, T 0.09/0.32, F 0.15/0.30 at 1e5)
+  threads=b200-call            exm_batch_signed_distance host->host (pipelined FP32 staging, H2D,
+                               kernel, D2H), wall clock per call from Python — the analogue of
+                               the paper's per-call JAX timing (L 0.09/0.29 ms,
+                               T 0.09/0.32, F 0.15/0.30 at 1e5)
+  threads=b200-dropin(T)       the reference's OWN scaling_benchmark (bench.cpp, compiled where it
+                               lies) with batch_signed_distance redirected to the B200 by
+                               host/geometry_sdf_b200.cpp (lib/exm_scaling_b200), T host threads
 
   python tools/scaling_benchmark.py [--trials 100] [--counts 100,1000,10000,100000,1000000]
 """
@@ -87,6 +91,25 @@ def main():
             for th, (m, sd, med) in rows:
                 print(f"{name},{evaluator},{n},{args.trials},{m:.3f},{sd:.3f},{med:.3f},{th}",
                       flush=True)
+    dropin_rows(counts, args.trials, nproc)
+
+
+def dropin_rows(counts, trials, nproc):
+    """The reference's scaling_benchmark itself, every batch_signed_distance call on the B200."""
+    import subprocess
+    import tempfile
+    binary = os.path.join(ROOT, "paper_2605_29663_b200", "lib", "exm_scaling_b200")
+    if not os.path.exists(binary):
+        return
+    with tempfile.TemporaryDirectory() as d:
+        subprocess.run([sys.executable, os.path.join(ROOT, "tools", "write_fixtures.py"), d],
+                       check=True, capture_output=True)
+        for th in sorted({1, min(8, nproc)}):
+            out = subprocess.run([binary, d, str(trials), str(th), *map(str, counts)],
+                                 check=True, capture_output=True, text=True).stdout
+            for line in out.strip().splitlines()[1:]:
+                f = line.split(",")
+                print(",".join(f[:7] + [f"b200-dropin({f[7]})"]), flush=True)
 
 
 if __name__ == "__main__":
