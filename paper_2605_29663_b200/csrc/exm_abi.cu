@@ -104,7 +104,7 @@ cudaError_t alloc_cloud_grid(int n_cap, void** block, CloudGrid* g) {
   auto up = [](size_t b) { return (b + 15) & ~static_cast<size_t>(15); };
   const size_t o_raw = up(n * sizeof(float2)), o_cloud = o_raw + up(n * sizeof(float2));
   const size_t o_chunk = o_cloud + up(cap * sizeof(float2));
-  const size_t o_rs = o_chunk + up((cap / 8 + 1) * sizeof(float4));  // chunks of >= 8 points
+  const size_t o_rs = o_chunk + up((cap / 4 + 1) * sizeof(float4));  // chunks of >= 4 points
   const size_t o_cs = o_rs + up(cells * sizeof(int)), o_gm = o_cs + up(cells * sizeof(int));
   const size_t o_ds = o_gm + up(sizeof(GridMeta));
   char* d = nullptr;

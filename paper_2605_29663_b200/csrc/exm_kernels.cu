@@ -829,7 +829,7 @@ __device__ __forceinline__ void sdf_grid_warp(const FpDev& fp, const float4* __r
       float l2 = lim * lim;
       // chunks of gm.chunk Morton-ordered points: one body-frame box bound per chunk, then the
       // per-point bounds and the exact SDF for the points of the chunks some lane still needs
-      const int csh = gm.chunk == 16 ? 4 : 3;
+      const int csh = gm.chunk == 16 ? 4 : (gm.chunk == 8 ? 3 : 2);
       for (int ch = s >> csh; ch < e >> csh; ++ch) {
         bool cneed = need;
         if (MODE == kGridFull) {
