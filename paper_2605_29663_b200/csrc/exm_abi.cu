@@ -15,6 +15,7 @@
 #include <chrono>
 #include <condition_variable>
 #include <functional>
+#include <limits>
 #include <thread>
 #include <cmath>
 #include <cstdio>
@@ -608,9 +609,9 @@ struct exm_handle {
   uint8_t* h_mask = nullptr;
   unsigned char* h_out = nullptr;
   // graphs: [0] device noise, [1] injected noise
-  cudaGraphExec_t exec[2] = {nullptr, nullptr};
-  cudaGraph_t graph[2] = {nullptr, nullptr};  // kept alive: exec node updates need its nodes
-  cudaGraphNode_t ev_node[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};
+  cudaGraphExec_t exec[2] = {};
+  cudaGraph_t graph[2] = {};  // kept alive: exec node updates need its nodes
+  cudaGraphNode_t ev_node[2][2] = {};
   EventPair graph_ev;
   // per-step SDF timing ring (resident runs)
   std::vector<EventPair> ring;
@@ -790,6 +791,11 @@ bool pregen_for(const exm_handle* h, bool draw_noise) {
   return draw_noise && h->sc.nstate != nullptr && h->pregen;
 }
 
+size_t head_bytes(const exm_handle* h) {  // dyn | nominal | guide of the pinned mirror
+  return static_cast<size_t>(reinterpret_cast<const unsigned char*>(h->h_pts) -
+                             reinterpret_cast<const unsigned char*>(h->h_dyn));
+}
+
 // The control step (captured into the handle's graphs).
 exm_status enqueue_step(exm_handle* h, bool draw_noise, const EventPair* ev, cudaStream_t s,
                         bool capturing) {
@@ -935,10 +941,25 @@ void HostTimer::mark(int phase) {
   if (phase == 3) ++h->host_calls;
 }
 
-// Stage the per-step inputs into pinned memory and enqueue their H2D copies.
-exm_status upload_inputs(exm_handle* h, const double q0[3], const double* pts, const uint8_t* mask,
-                         int32_t n, const double* guide, int32_t ng, const double goal[3],
-                         const double* nominal, const double* u_prev, uint64_t cycle) {
+int default_host_threads() {
+  const unsigned hw = std::thread::hardware_concurrency();
+  return static_cast<int>(std::max(1u, std::min(8u, hw ? hw : 1u)));
+}
+
+// The handle's host pool (EXM_OPT_HOST_THREADS threads, the caller's thread included).
+HostPool* ensure_pool(exm_handle* h) {
+  const int threads = h->host_threads > 0 ? h->host_threads : default_host_threads();
+  if (!h->pool || h->pool->size() != threads) {
+    delete h->pool;
+    h->pool = new HostPool(threads - 1);
+  }
+  return h->pool;
+}
+
+// The per-step state of the pinned mirror (StepDyn, nominal, guidance).
+exm_status fill_head(exm_handle* h, const double q0[3], const double* pts, const uint8_t* mask,
+                     int32_t n, const double* guide, int32_t ng, const double goal[3],
+                     const double* nominal, const double* u_prev, uint64_t cycle) {
   exm_status st = check_cloud(h, pts, n);
   if (st != EXM_OK) return st;
   st = check_guide(h, guide, ng);
@@ -955,17 +976,23 @@ exm_status upload_inputs(exm_handle* h, const double q0[3], const double* pts, c
   d.n_guide = ng;
   d.use_mask = mask ? 1 : 0;
   d.reserved = 0;
-  const size_t TD = static_cast<size_t>(h->T) * h->D;
-  std::memcpy(h->h_nominal, nominal, TD * sizeof(double));
+  std::memcpy(h->h_nominal, nominal, static_cast<size_t>(h->T) * h->D * sizeof(double));
   std::memcpy(h->h_guide, guide, 2 * static_cast<size_t>(ng) * sizeof(double));
+  return EXM_OK;
+}
+
+// Stage the per-step inputs into pinned memory and enqueue their H2D copies.
+exm_status upload_inputs(exm_handle* h, const double q0[3], const double* pts, const uint8_t* mask,
+                         int32_t n, const double* guide, int32_t ng, const double goal[3],
+                         const double* nominal, const double* u_prev, uint64_t cycle) {
+  exm_status st = fill_head(h, q0, pts, mask, n, guide, ng, goal, nominal, u_prev, cycle);
+  if (st != EXM_OK) return st;
   cudaStream_t s = h->stream;
   // The small state (dyn | nominal | guide) goes in one pinned copy; the cloud goes straight from
   // the caller's buffers (the driver stages pageable memory while this call returns): measured
   // 10 us per config-2 call faster end to end than a host memcpy into a pinned mirror plus an
   // async copy, and 2 % faster than page-locked caller buffers (round 1).
-  const size_t head0 = static_cast<size_t>(reinterpret_cast<unsigned char*>(h->h_pts) -
-                                           reinterpret_cast<unsigned char*>(h->h_dyn));
-  EXM_CUDA(cudaMemcpyAsync(h->d_dyn, h->h_dyn, head0, cudaMemcpyHostToDevice, s));
+  EXM_CUDA(cudaMemcpyAsync(h->d_dyn, h->h_dyn, head_bytes(h), cudaMemcpyHostToDevice, s));
   if (n > 0)
     EXM_CUDA(cudaMemcpyAsync(h->d_pts, pts, 2 * static_cast<size_t>(n) * sizeof(double), cudaMemcpyHostToDevice, s));
   if (mask && n > 0)
@@ -1252,14 +1279,17 @@ exm_status exm_control_cycle(exm_handle* h, const double q0[3], const double* pt
   if (h->emulated) return fail(EXM_ERR_INVALID_ARGUMENT, "shard handle without a communicator: use exm_sharded_cycle");
   HostTimer ht(h);
   EXM_CUDA(cudaSetDevice(h->device));
-  exm_status st = upload_inputs(h, q0, pts_xy, mask, n_points, guide_xy, n_guide, goal,
-                                nominal_inout, u_prev_inout, cycle);
+  exm_status st;
+  // inputs: the small state via the pinned mirror, the cloud straight from the caller's pageable
+  // buffers (the driver stages them while this call returns). Measured against rounding the cloud
+  // to FP32 on the host into pinned memory (async copy, or H2D/D2H memcpy nodes in the graph):
+  // those are 8 and 11 us per config-2 call slower end to end (round 2).
+  st = upload_inputs(h, q0, pts_xy, mask, n_points, guide_xy, n_guide, goal, nominal_inout,
+                     u_prev_inout, cycle);
+  if (st == EXM_OK && eps_or_null) st = upload_eps(h, eps_or_null);
   if (st != EXM_OK) return st;
-  if (eps_or_null) {
-    st = upload_eps(h, eps_or_null);
-    if (st != EXM_OK) return st;
-  }
   ht.mark(0);
+  // the handle's first steps run as plain launches, both lane mappings timed (tune_step)
   st = tuning(h) ? tune_step(h, eps_or_null == nullptr, &h->step_ev)
                  : launch_graph(h, eps_or_null ? 1 : 0, h->step_ev);
   if (st != EXM_OK) return st;
@@ -1433,18 +1463,9 @@ exm_status sdf_read(exm_handle* h, float* per_pair, double* per_pose_min) {
   return EXM_OK;
 }
 
-int default_host_threads() {
-  const unsigned hw = std::thread::hardware_concurrency();
-  return static_cast<int>(std::max(1u, std::min(8u, hw ? hw : 1u)));
-}
-
 // Pipeline buffers of batch_signed_distance for chunks of `chunk` queries (grown on demand).
 exm_status ensure_bsd(exm_handle* h, int chunk) {
-  const int threads = h->host_threads > 0 ? h->host_threads : default_host_threads();
-  if (!h->pool || h->pool->size() != threads) {
-    delete h->pool;
-    h->pool = new HostPool(threads - 1);
-  }
+  ensure_pool(h);
   if (chunk <= h->bsd_chunk) return EXM_OK;
   cudaFreeHost(h->bsd_hq);
   cudaFreeHost(h->bsd_hd);

@@ -727,7 +727,14 @@ __device__ __forceinline__ bool box_may_beat(const WBox& w, float bx0, float bx1
 // at all: every valid point is evaluated, the same arithmetic without culling — the reference
 // the exactness tests compare the culled minimum with, bit for bit).
 constexpr int kGridNoChunk = 0, kGridFull = 1, kGridBrute = 2;
-template <int KIND, int NB, bool STATS, int MODE>
+// Read-only load of the cloud structure: from shared memory (SMEM: the CTA staged it by TMA) or
+// through the read-only data path.
+template <bool SMEM, typename V>
+__device__ __forceinline__ V ldro(const V* p) {
+  if constexpr (SMEM) return *p;
+  else return __ldg(p);
+}
+template <int KIND, int NB, bool STATS, int MODE, bool SMEM = false>
 __device__ __forceinline__ void sdf_grid_warp(const FpDev& fp, const float4* __restrict__ poses,
                                               int n_poses, const GridMeta& gm,
                                               const int* __restrict__ cell_start,
@@ -807,8 +814,8 @@ __device__ __forceinline__ void sdf_grid_warp(const FpDev& fp, const float4* __r
         ring_cell(k, t0 + lane, ci, cj, c_i, c_j);
         if (c_i >= 0 && c_j >= 0 && c_i < gm.gx && c_j < gm.gy) {
           const int c = c_j * gm.gx + c_i;
-          c_s = __ldg(cell_start + c);
-          c_e = __ldg(cell_start + c + 1);
+          c_s = ldro<SMEM>(cell_start + c);
+          c_e = ldro<SMEM>(cell_start + c + 1);
         }
       }
       unsigned cells = __ballot_sync(kFull, c_s != c_e);
@@ -833,14 +840,14 @@ __device__ __forceinline__ void sdf_grid_warp(const FpDev& fp, const float4* __r
       for (int ch = s >> csh; ch < e >> csh; ++ch) {
         bool cneed = need;
         if (MODE == kGridFull) {
-          cneed = need && chunk_may_beat(fp, q, __ldg(chunk + ch), best, mg);
+          cneed = need && chunk_may_beat(fp, q, ldro<SMEM>(chunk + ch), best, mg);
           if (STATS && need) ++cnt[kCntChunk];
           if (!__any_sync(kFull, cneed)) continue;
         }
         const float2* cp = cloud + (ch << csh);
 #pragma unroll 1
         for (int p = 0; p < gm.chunk; ++p) {
-          const float2 o = __ldg(cp + p);
+          const float2 o = ldro<SMEM>(cp + p);
           const float dx = o.x - q.x, dy = o.y - q.y;
           if (STATS && cneed) ++cnt[kCntPoint];
           if (STATS && lane == 0) ++cnt[kCntPointWarp];
@@ -921,6 +928,77 @@ __global__ void __launch_bounds__(128) k_sdf_grid(const __grid_constant__ FpDev 
       unsigned long long v = cnt[k];
       for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
       if (lane == 0 && v) atomicAdd(stats + k, v);
+    }
+  }
+}
+
+// The cloud structure staged into shared memory by TMA bulk copies and shared by a persistent
+// 1,024-thread CTA per SM (the north star's "point cloud staged into shared memory by TMA and
+// broadcast across a CTA of poses"): cell table, chunk boxes and points (≤ smem_bytes; larger
+// clouds fall back to the read-only data path in the same launch). Warps take 32 poses at a time
+// from the work counter. A/B variant of k_sdf_grid (-DEXM_SDF_SMEM builds).
+template <int KIND, int NB>
+__global__ void __launch_bounds__(1024, 1) k_sdf_grid_smem(
+    const __grid_constant__ FpDev fp, const float4* __restrict__ poses, int n_poses,
+    const GridMeta* __restrict__ gmp, const int* __restrict__ cell_start,
+    const float2* __restrict__ cloud, const float4* __restrict__ chunk,
+    const float* __restrict__ cap, int T, int rows, float* __restrict__ out,
+    unsigned* __restrict__ work, int smem_bytes) {
+  pdl_wait();
+  extern __shared__ __align__(128) unsigned char s_cloud_mem[];
+  __shared__ __align__(8) uint64_t bar;
+  __shared__ int s_fit;
+  __shared__ unsigned s_off[3];
+  const int lane = threadIdx.x & 31;
+  const GridMeta gm = *gmp;
+  if (threadIdx.x == 0) {
+    const int cells = gm.n_valid > 0 ? gm.gx * gm.gy : 0;
+    const int npad = cells ? cell_start[cells] : 0;
+    auto r16 = [](unsigned b) { return (b + 15u) & ~15u; };
+    const unsigned b_cell = r16(4u * static_cast<unsigned>(cells + 1));
+    const unsigned b_chunk = 16u * static_cast<unsigned>(npad / (gm.chunk > 0 ? gm.chunk : 8));
+    const unsigned b_cloud = r16(8u * static_cast<unsigned>(npad));
+    s_off[0] = 0;
+    s_off[1] = b_cell;
+    s_off[2] = b_cell + b_chunk;
+    const bool fit = cells > 0 && b_cell + b_chunk + b_cloud <= static_cast<unsigned>(smem_bytes);
+    s_fit = fit;
+    if (fit) {
+      mbar_init(&bar, 1);
+      mbar_expect_tx(&bar, b_cell + b_chunk + b_cloud);
+      tma_bulk_g2s(s_cloud_mem, cell_start, b_cell, &bar);
+      if (b_chunk) tma_bulk_g2s(s_cloud_mem + b_cell, chunk, b_chunk, &bar);
+      if (b_cloud) tma_bulk_g2s(s_cloud_mem + b_cell + b_chunk, cloud, b_cloud, &bar);
+    }
+  }
+  __syncthreads();
+  const bool fit = s_fit != 0;
+  if (fit) mbar_wait(&bar, 0);
+  const int* cs = fit ? reinterpret_cast<const int*>(s_cloud_mem) : cell_start;
+  const float4* ck = fit ? reinterpret_cast<const float4*>(s_cloud_mem + s_off[1]) : chunk;
+  const float2* cl = fit ? reinterpret_cast<const float2*>(s_cloud_mem + s_off[2]) : cloud;
+  unsigned long long cnt[kCntN];
+  for (;;) {
+    unsigned base = 0;
+    if (lane == 0) base = atomicAdd(work, 32u);
+    base = __shfl_sync(kFull, base, 0);
+    if (base >= static_cast<unsigned>(n_poses)) break;
+    if (fit)
+      sdf_grid_warp<KIND, NB, false, kGridFull, true>(fp, poses, n_poses, gm, cs, cl, ck, cap, T,
+                                                      rows, out, static_cast<int>(base) + lane,
+                                                      lane, cnt);
+    else
+      sdf_grid_warp<KIND, NB, false, kGridFull, false>(fp, poses, n_poses, gm, cs, cl, ck, cap, T,
+                                                       rows, out, static_cast<int>(base) + lane,
+                                                       lane, cnt);
+  }
+  if (lane == 0) {
+    __threadfence();
+    const unsigned warps = gridDim.x * (blockDim.x >> 5);
+    if (atomicAdd(work + 1, 1u) == warps - 1) {
+      work[0] = 0u;
+      work[1] = 0u;
+      __threadfence();
     }
   }
 }
@@ -1406,6 +1484,23 @@ cudaError_t launch_grid_kernel(const FpDev& fp, const float4* poses, int n_poses
   unsigned* work = (persist || blocks >= kPersistentWaves * cap_blocks) ? g.work : nullptr;
   const int grid = work ? cap_blocks : blocks;
   const int rows_used = (hmajor && T > 0 && n_poses % T == 0) ? n_poses / T : 0;
+#ifdef EXM_SDF_SMEM
+  if constexpr (!STATS && MODE == kGridFull) {
+    constexpr int kSmem = 220 * 1024;
+    auto ks = k_sdf_grid_smem<KIND, NB>;
+    cudaError_t e = cudaFuncSetAttribute(ks, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
+    if (e != cudaSuccess) return e;
+    int dev = 0, n_sm = 148;
+    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
+    if (path) *path = SdfPath{0, 0, 1, n_sm, 1024, rows_used > 0 ? 1 : 0};
+    if (const cudaError_t le = launch_k(ks, n_sm, 1024, kSmem, s, fp, poses, n_poses, g.gm,
+                                        g.cell_start, g.cloud, g.chunk, cap, T, rows_used, out,
+                                        g.work, kSmem);
+        le != cudaSuccess)
+      return le;
+    return cudaGetLastError();
+  }
+#endif
   if (path) *path = SdfPath{0, 0, work ? 1 : 0, grid, threads, rows_used > 0 ? 1 : 0};
   if (const cudaError_t le = launch_k(k, grid, threads, 0, s, fp, poses, n_poses, g.gm,
                                       g.cell_start, g.cloud, g.chunk, cap, T, rows_used, out, work,
