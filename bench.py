@@ -561,48 +561,68 @@ def bench_hybrid_cfg5(args, torch):
             "speedup": seq / batched, "hybrid_steps_per_s": 1.0 / batched}
 
 
-def bench_sense(args, with_cpu):
-    """sense() (world.cpp:182-243) for the config-5 world (omni_gap walls + 64
-    discs displaced along their trails, the cycle-10 positions) seen from q0, range 10 m, budget
-    720: exm_sense (host API: host obstacles in, host ObstacleSet out) vs the reference's own
-    sense() from oracle/_ref on one host core (the reference is single-threaded here)."""
-    import math as _m
+def cfg5_world():
+    """The config-5 world as the reference scenario holds it: the two omni_gap walls (static) and
+    64 discs on 2-waypoint ping-pong trails (world.hpp TrailMotion)."""
     from paper_2605_29663_b200 import workloads as W
-    from paper_2605_29663_b200.api import Engine, WorldObstacle
+    from paper_2605_29663_b200.api import Trail, WorldObstacle
     obs = [WorldObstacle.polygon(p) for p in W.OMNI_WALLS]
-    t = 1.0
+    trails = [None] * len(obs)
     for k in range(64):
         ax, ay = W.uniform_range(9, k, 0, -8.0, 8.0), W.uniform_range(9, k, 1, -8.0, 8.0)
         bx, by = W.uniform_range(9, k, 2, -8.0, 8.0), W.uniform_range(9, k, 3, -8.0, 8.0)
-        r = W.uniform_range(9, k, 4, 0.2, 0.5)
-        v = W.uniform_range(9, k, 5, 0.0, 0.2)
-        L = _m.hypot(bx - ax, by - ay)
-        sarc = (v * t) % (2 * L) if L > 0 else 0.0
-        sarc = sarc if sarc <= L else 2 * L - sarc
-        f = sarc / L if L > 0 else 0.0
-        obs.append(WorldObstacle.disc((ax, ay), r, (f * (bx - ax), f * (by - ay))))
+        obs.append(WorldObstacle.disc((ax, ay), W.uniform_range(9, k, 4, 0.2, 0.5)))
+        trails.append(Trail([[ax, ay], [bx, by]], W.uniform_range(9, k, 5, 0.0, 0.2)))
+    return obs, trails
+
+
+def bench_sense(args, with_cpu):
+    """one world cycle of the config-5 scene — step_world (world.cpp:127-157, the
+    64 discs' trails) then sense() (:182-243) from q0, range 10 m, budget 720 — with the world kept
+    on the device (exm_world_step + exm_world_sense: host ObstacleSet out) vs the reference's own
+    step_world + sense from oracle/_ref on one host core (the reference is single-threaded here).
+    Also the one-shot exm_sense (obstacle geometry and offsets from the host each call)."""
+    from paper_2605_29663_b200 import workloads as W
+    from paper_2605_29663_b200.api import Engine, WorldObstacle
+    obs, trails = cfg5_world()
     wl = W.cfg1(K=32, T=4)
     eng = Engine(wl.model, wl.limits, wl.footprint, wl.params, n_cap=16, guide_cap=4)
     robot = np.array([-4.0, 0.0, 0.0])
-    for _ in range(3):
-        cloud = eng.sense(obs, robot, 10.0, 720, 7, 0)
+    world = eng.world(obs, trails, 10.0, 720, 7)
+    for c in range(3):
+        world.step(0.1)
+        cloud = world.sense(robot, c)
     n = max(20, args.steps // 4)
     t0 = time.perf_counter()
     for c in range(n):
-        cloud = eng.sense(obs, robot, 10.0, 720, 7, c)
+        world.step(0.1)
+        cloud = world.sense(robot, c)
     gpu = (time.perf_counter() - t0) / n
-    out = {"workload": "cfg5 world: 2 walls + 64 moving discs, range 10 m, budget 720",
-           "visible_points": int(cloud.mask.sum()), "exm_sense_ms": 1e3 * gpu}
+    arc, _, off = world.state()
+    moved = [WorldObstacle(o.vertices, o.center, o.radius, tuple(off[i])) for i, o in enumerate(obs)]
+    for _ in range(3):
+        eng.sense(moved, robot, 10.0, 720, 7, 0)
+    t0 = time.perf_counter()
+    for c in range(n):
+        eng.sense(moved, robot, 10.0, 720, 7, c)
+    one_shot = (time.perf_counter() - t0) / n
+    world.close()
+    out = {"workload": "cfg5 world: 2 walls + 64 discs on trails, step 0.1 s + sense, range 10 m, budget 720",
+           "visible_points": int(cloud.mask.sum()), "exm_world_step_sense_ms": 1e3 * gpu,
+           "exm_sense_one_shot_ms": 1e3 * one_shot}
     if with_cpu:
-        sys.path.insert(0, ROOT)
-        from tests.oracle_bindings import reference_available, reference_sense
+        from tests.oracle_bindings import ReferenceWorld, reference_available
         if reference_available():
-            reference_sense(obs, robot, 10.0, 720, 7, 0)
+            ref = ReferenceWorld(obs, trails, 10.0, 720, 7)
+            for c in range(3):
+                ref.step(0.1)
+                ref.sense(robot, c)
             t0 = time.perf_counter()
             for c in range(n):
-                reference_sense(obs, robot, 10.0, 720, 7, c)
+                ref.step(0.1)
+                ref.sense(robot, c)
             cpu = (time.perf_counter() - t0) / n
-            out.update({"reference_sense_ms": 1e3 * cpu, "cores": 1, "speedup": cpu / gpu})
+            out.update({"reference_step_sense_ms": 1e3 * cpu, "cores": 1, "speedup": cpu / gpu})
     return out
 
 

@@ -338,6 +338,31 @@ exm_status exm_sense(exm_handle* h, const exm_world_obstacle* obstacles, int32_t
                      const double robot[3], double range, int32_t budget, uint64_t seed,
                      uint64_t sample_key, double* pts_out, uint8_t* mask_out, int32_t* n_valid);
 
+/* ---- device world: moving obstacles (step_world, world.cpp:127-157) + sense ----------------
+ * A scenario's obstacles (shapes as exm_world_obstacle, whose `offset` is ignored here) with
+ * their trail motion (world.hpp TrailMotion: >= 2 waypoints, the shape's coordinates at the first
+ * one, speed >= 0, ping-pong or clamped), the sensor (range, budget) and the scenario seed, kept on
+ * the device with the world state (WorldState: arc position and direction per obstacle, initially
+ * 0 / +1). exm_world_step advances it by dt exactly as step_world; exm_world_sense is sense()
+ * (world.cpp:182-243) with the current obstacle_offset of every obstacle (:159-164), computed on
+ * the device. exm_world_state reads the state back (arc[n], dir[n], offsets[2n]; any may be NULL).
+ * Errors: budget < 1 ("sensor budget must be >= 1"), dt <= 0 ("step_world requires dt > 0"). */
+typedef struct exm_world exm_world;
+typedef struct exm_world_trail {
+  int32_t n_waypoints;     /* < 2: static obstacle */
+  int32_t ping_pong;       /* 1: reflect at the ends, 0: clamp */
+  const double* waypoints; /* 2 * n_waypoints */
+  double speed;            /* m/s */
+} exm_world_trail;
+exm_status exm_world_create(exm_handle* h, const exm_world_obstacle* obstacles,
+                            const exm_world_trail* trails_or_null, int32_t n_obstacles,
+                            double range, int32_t budget, uint64_t seed, exm_world** out);
+void exm_world_destroy(exm_world* w);
+exm_status exm_world_step(exm_world* w, double dt);
+exm_status exm_world_sense(exm_world* w, const double robot[3], uint64_t sample_key,
+                           double* pts_out, uint8_t* mask_out, int32_t* n_valid);
+exm_status exm_world_state(exm_world* w, double* arc_out, int32_t* dir_out, double* offsets_out);
+
 /* Per-step hints for the culled signed distance (T floats, +inf = none): the rollout SDF first
  * prunes every point whose lower bound reaches cap[h], then re-runs without cap the poses it
  * left unresolved, so results are exact for any caps; good caps (a little above the step's

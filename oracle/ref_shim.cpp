@@ -387,3 +387,90 @@ extern "C" int ref_sense(const exm_world_obstacle* obs, int n, const double robo
     return 1;
   }
 }
+
+// ---- world with trails (test infrastructure for exm_world_*): the reference's Scenario +
+// WorldState, step_world and sense (world.hpp) ----
+struct RefWorld {
+  Scenario sc;
+  WorldState st;
+};
+
+extern "C" void* ref_world_create(const exm_world_obstacle* obs, const int32_t* n_wp,
+                                  const double* const* wp, const double* speed,
+                                  const int32_t* ping_pong, int n, double range, int budget,
+                                  uint64_t seed) {
+  try {
+    auto w = std::make_unique<RefWorld>();
+    w->sc.sensor.range = range;
+    w->sc.sensor.budget = budget;
+    w->sc.seed = seed;
+    for (int i = 0; i < n; ++i) {
+      const exm_world_obstacle& o = obs[i];
+      Obstacle ob;
+      if (o.kind == EXM_OBSTACLE_DISC) {
+        ob.shape = Disc{{o.x[0], o.y[0]}, o.radius};
+      } else {
+        std::vector<Point2> v;
+        for (int k = 0; k < o.count; ++k) v.push_back({o.x[k], o.y[k]});
+        ob.shape = PolygonFootprint::make(v);
+      }
+      if (n_wp[i] >= 2) {
+        TrailMotion m;
+        for (int k = 0; k < n_wp[i]; ++k) m.waypoints.push_back({wp[i][2 * k], wp[i][2 * k + 1]});
+        m.speed = speed[i];
+        m.ping_pong = ping_pong[i] != 0;
+        ob.motion = m;
+      }
+      w->sc.obstacles.push_back(std::move(ob));
+    }
+    w->st = WorldState::initial(w->sc);
+    return w.release();
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return nullptr;
+  }
+}
+
+extern "C" void ref_world_destroy(void* w) { delete static_cast<RefWorld*>(w); }
+
+extern "C" int ref_world_step(void* wp, double dt) {
+  auto* w = static_cast<RefWorld*>(wp);
+  try {
+    w->st = step_world(w->sc, w->st, dt);
+    return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return 1;
+  }
+}
+
+extern "C" void ref_world_state(void* wp, double* arc, int32_t* dir, double* offsets) {
+  auto* w = static_cast<RefWorld*>(wp);
+  for (std::size_t i = 0; i < w->sc.obstacles.size(); ++i) {
+    arc[i] = w->st.arc[i];
+    dir[i] = w->st.direction[i];
+    const Point2 o = obstacle_offset(w->sc, w->st, i);
+    offsets[2 * i] = o.x;
+    offsets[2 * i + 1] = o.y;
+  }
+}
+
+extern "C" int ref_world_sense(void* wp, const double robot[3], uint64_t key, double* pts_out,
+                               uint8_t* mask_out, int* n_valid) {
+  auto* w = static_cast<RefWorld*>(wp);
+  try {
+    const ObstacleSet set = sense(w->sc, w->st, Pose2{robot[0], robot[1], robot[2]}, key);
+    int nv = 0;
+    for (std::size_t i = 0; i < set.points.size(); ++i) {
+      pts_out[2 * i] = set.points[i].x;
+      pts_out[2 * i + 1] = set.points[i].y;
+      mask_out[i] = set.mask[i];
+      nv += set.mask[i] != 0;
+    }
+    *n_valid = nv;
+    return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return 1;
+  }
+}

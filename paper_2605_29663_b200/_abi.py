@@ -39,6 +39,18 @@ class ExmWorldObstacle(C.Structure):
 OBSTACLE_POLYGON, OBSTACLE_DISC = 0, 1
 
 
+class ExmWorldTrail(C.Structure):
+    _fields_ = [("n_waypoints", C.c_int32), ("ping_pong", C.c_int32),
+                ("waypoints", C.POINTER(C.c_double)), ("speed", C.c_double)]
+
+
+class ExmWorld(C.Structure):
+    pass
+
+
+_Wp = C.POINTER(ExmWorld)
+
+
 class ExmFootprint(C.Structure):
     _fields_ = [("kind", C.c_int32), ("count", C.c_int32), ("x", _dp), ("y", _dp),
                 ("hx", _dp), ("hy", _dp)]
@@ -146,6 +158,13 @@ SIGNATURES = {
     "exm_host_timing": (C.c_int32, [_Hp, _dp, C.POINTER(C.c_int64)]),
     "exm_last_sdf_path": (C.c_int32, [_Hp, C.POINTER(ExmSdfPath), C.POINTER(ExmSdfPath)]),
     "exm_sdf_work_stats": (C.c_int32, [_Hp, C.POINTER(C.c_int64)]),
+    "exm_world_create": (C.c_int32, [_Hp, C.POINTER(ExmWorldObstacle), C.POINTER(ExmWorldTrail),
+                                     C.c_int32, C.c_double, C.c_int32, C.c_uint64,
+                                     C.POINTER(_Wp)]),
+    "exm_world_destroy": (None, [_Wp]),
+    "exm_world_step": (C.c_int32, [_Wp, C.c_double]),
+    "exm_world_sense": (C.c_int32, [_Wp, _dp, C.c_uint64, _dp, _u8p, C.POINTER(C.c_int32)]),
+    "exm_world_state": (C.c_int32, [_Wp, _dp, C.POINTER(C.c_int32), _dp]),
 }
 
 _lib = None

@@ -72,6 +72,78 @@ class WorldObstacle:
         return o, (x, y)
 
 
+@dataclass
+class Trail:
+    """TrailMotion (world.hpp): >= 2 waypoints (the shape's coordinates sit at the first), speed
+    (m/s), ping-pong (reflect at the ends) or clamp."""
+    waypoints: np.ndarray
+    speed: float
+    ping_pong: bool = True
+
+    def __post_init__(self):
+        self.waypoints = np.ascontiguousarray(np.asarray(self.waypoints, np.float64).reshape(-1, 2))
+
+
+def world_trails_c(trails, n):
+    """ctypes array of exm_world_trail (None entries: static) plus the buffers it points into."""
+    arr = (_abi.ExmWorldTrail * max(n, 1))()
+    keep = []
+    for i, t in enumerate(trails or []):
+        if t is None:
+            continue
+        wp = t.waypoints
+        keep.append(wp)
+        arr[i] = _abi.ExmWorldTrail(wp.shape[0], 1 if t.ping_pong else 0, dptr(wp), float(t.speed))
+    return arr, keep
+
+
+class DeviceWorld:
+    """Moving obstacles kept on the device (exm_world_*): step_world (world.cpp:127-157) and
+    sense() (:182-243) with the current obstacle offsets, no host round trip of the world state."""
+
+    def __init__(self, engine, obstacles, trails, sensor_range: float, budget: int, seed: int):
+        self.eng, self.budget, self.n = engine, int(budget), len(obstacles)
+        self.lib = engine.lib
+        arr, keep = world_obstacles_c(obstacles)
+        tarr, tkeep = world_trails_c(trails, self.n)
+        w = C.POINTER(_abi.ExmWorld)()
+        check(self.lib.exm_world_create(engine.h, arr, tarr, self.n, float(sensor_range),
+                                        self.budget, int(seed), C.byref(w)))
+        del keep, tkeep
+        self.w = w
+
+    def step(self, dt: float):
+        check(self.lib.exm_world_step(self.w, float(dt)))
+
+    def sense(self, robot, sample_key: int) -> "ObstacleSet":
+        pts = np.empty((self.budget, 2))
+        mask = np.empty(self.budget, np.uint8)
+        n = C.c_int32()
+        r = np.ascontiguousarray(np.asarray(robot, np.float64).reshape(3))
+        check(self.lib.exm_world_sense(self.w, dptr(r), int(sample_key), dptr(pts), u8ptr(mask),
+                                       C.byref(n)))
+        return ObstacleSet(pts, mask)
+
+    def state(self):
+        arc = np.empty(max(self.n, 1))
+        d = np.empty(max(self.n, 1), np.int32)
+        off = np.empty((max(self.n, 1), 2))
+        check(self.lib.exm_world_state(self.w, dptr(arc), d.ctypes.data_as(C.POINTER(C.c_int32)),
+                                       dptr(off)))
+        return arc[: self.n], d[: self.n], off[: self.n]
+
+    def close(self):
+        if getattr(self, "w", None):
+            self.lib.exm_world_destroy(self.w)
+            self.w = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
 def world_obstacles_c(obstacles):
     """ctypes array of exm_world_obstacle plus the buffers it points into."""
     items = [o._c() for o in obstacles]
@@ -576,6 +648,10 @@ class Engine:
                                  dptr(pts), u8ptr(mask), C.byref(n)))
         del keep
         return ObstacleSet(pts, mask)
+
+    def world(self, obstacles, trails, sensor_range: float, budget: int, seed: int) -> DeviceWorld:
+        """A device world on this handle's device and stream (exm_world_create)."""
+        return DeviceWorld(self, obstacles, trails, sensor_range, budget, seed)
 
     def set_sdf_caps(self, caps):
         """Per-step cap hints of the culled SDF (exm_set_sdf_caps; exact for any values)."""

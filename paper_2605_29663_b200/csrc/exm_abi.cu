@@ -531,6 +531,8 @@ class HostPool {
   bool stop_ = false;
 };
 
+void world_free(exm_world* w);  // sensing workspace (defined with the world API below)
+
 constexpr int kRingMax = 512;  // SDF timing events kept before they are folded into a sum
 constexpr int kBsdSlots = 3;   // batch_signed_distance pipeline depth (chunks in flight)
 
@@ -553,6 +555,7 @@ struct exm_handle {
   bool hmajor = false;
   int tune_n = 0;
   double tune_ms[2] = {0.0, 0.0};
+  exm_world* sense_ws = nullptr;  // exm_sense's reused workspace
   // sharding without a communicator (exm_set_shard: several shard handles on one device)
   bool emulated = false;
   cudaStream_t stream = nullptr;
@@ -579,8 +582,6 @@ struct exm_handle {
   float4* d_poses = nullptr;
   double2* d_xy = nullptr;
   double* d_ctrl = nullptr;       // control cost per (r, h)
-  void* d_sense = nullptr;        // exm_sense workspace (segments, obstacles, output)
-  size_t sense_bytes = 0;
   float* d_hstat = nullptr;       // per-step d_min statistic {sum[T], sum of squares[T], count}
   float* d_cap = nullptr;         // per-step SDF caps for the next step (T; +inf: none)
   double* d_base = nullptr;
@@ -1235,7 +1236,7 @@ void exm_destroy(exm_handle* h) {
   if (h->comm && g_nccl.destroy) g_nccl.destroy(h->comm);
   if (h->borrowed_poses) h->d_poses = nullptr, h->d_dmin = nullptr;
   void* dev[] = {h->d_in_block, h->d_grid_block, h->d_eps, h->d_poses, h->d_xy, h->d_ctrl,
-                 h->d_hstat, h->d_cap, h->d_sense, h->d_val_xy, h->d_base, h->d_dmin,
+                 h->d_hstat, h->d_cap, h->d_val_xy, h->d_base, h->d_dmin,
                  h->d_partials, h->d_upd, h->d_val_poses, h->d_val_base, h->d_val_dmin, h->d_out,
                  h->d_controls, h->d_states, h->d_cost, h->d_unsafe, h->sb_poses, h->sb_pts64,
                  h->sb_pts, h->sb_mask, h->sb_keys, h->sb_min, h->sb_pairs, h->d_nstate,
@@ -1243,6 +1244,7 @@ void exm_destroy(exm_handle* h) {
   for (void* p : dev)
     if (p) cudaFree(p);
   delete h->pool;
+  world_free(h->sense_ws);
   for (auto e : h->bsd_ev)
     if (e) cudaEventDestroy(e);
   for (auto st : h->bsd_st)
@@ -1757,48 +1759,79 @@ exm_status exm_read_resident(exm_handle* h, double* nominal_out, double* u_prev_
 
 void* exm_stream(exm_handle* h) { return h ? static_cast<void*>(h->stream) : nullptr; }
 
-// Sensing: segment table in the reference's sampling order (world.cpp:39-65) built on the
-// host with the reference's arithmetic, then one device kernel (exm_world.cu).
-exm_status exm_sense(exm_handle* h, const exm_world_obstacle* obstacles, int32_t n_obstacles,
-                     const double robot[3], double range, int32_t budget, uint64_t seed,
-                     uint64_t sample_key, double* pts_out, uint8_t* mask_out, int32_t* n_valid) {
-  if (!h || !robot || !pts_out || !mask_out || (n_obstacles > 0 && !obstacles))
-    return fail(EXM_ERR_INVALID_ARGUMENT, "null argument");
-  if (budget < 1) return fail(EXM_ERR_INVALID_ARGUMENT, "sensor budget must be >= 1");
-  std::lock_guard<std::mutex> lk(h->mu);
-  constexpr double kSpacing = 0.05;  // kBoundarySpacing, world.cpp:15
+}  // extern "C"
+
+// ---------------------------------------------------------------------------- sensing / world
+// The device world (exm_world_*) and one-shot sensing (exm_sense) share this layout: base
+// geometry (segments in the reference's sampling order, world.cpp:39-65; obstacles and polygon
+// vertices for the line of sight), trails, and the per-obstacle state and offsets, in one device
+// block; outputs staged through pinned memory.
+struct exm_world {
+  exm_handle* h = nullptr;
+  int nseg = 0, n_obs = 0, budget = 0, sample_cap = 0;
+  // capacities of the device block (a handle's one-shot sensing workspace is reused)
+  int cap_seg = 0, cap_obs = 0, cap_verts = 0, cap_wp = 0, cap_budget = 0;
+  void* bins = nullptr;  // BinState of the three sensing launches
+  double range = 0.0;
+  uint64_t seed = 0;
+  void* d_block = nullptr;
+  SenseSeg* seg = nullptr;
+  SenseObs* obs = nullptr;
+  double2* verts = nullptr;
+  TrailDev* trails = nullptr;
+  double2* waypoints = nullptr;
+  double* arc = nullptr;
+  int* dir = nullptr;
+  double2* offsets = nullptr;
+  int* seg_scratch = nullptr;
+  double* d_scratch = nullptr;
+  int* bin_scratch = nullptr;
+  double* out_pts = nullptr;  // budget x 2, then mask (budget bytes), then n (int)
+  uint8_t* out_mask = nullptr;
+  int* out_n = nullptr;
+  unsigned char* h_out = nullptr;  // pinned mirror of the output block
+  size_t out_bytes = 0;
+};
+
+namespace {
+
+struct WorldHost {
   std::vector<SenseSeg> seg;
-  std::vector<SenseObs> obs(static_cast<size_t>(n_obstacles));
-  std::vector<double2> verts;
-  int total = 0;
-  for (int i = 0; i < n_obstacles; ++i) {
-    const exm_world_obstacle& o = obstacles[i];
-    const double ox = o.offset[0], oy = o.offset[1];
-    SenseObs& so = obs[static_cast<size_t>(i)];
-    so = {};
-    so.ox = ox;
-    so.oy = oy;
+  std::vector<SenseObs> obs;
+  std::vector<double2> verts, waypoints, offsets;
+  std::vector<TrailDev> trails;
+  int sample_bound = 0;  // samples at zero offsets + one per segment (offsets move counts by rounding)
+};
+
+exm_status build_world(const exm_world_obstacle* o_in, int n, const exm_world_trail* tr,
+                       WorldHost* w) {
+  constexpr double kSpacing = 0.05;  // kBoundarySpacing, world.cpp:15
+  w->obs.assign(static_cast<size_t>(n), SenseObs{});
+  w->trails.assign(static_cast<size_t>(n), TrailDev{});
+  w->offsets.assign(static_cast<size_t>(n), make_double2(0.0, 0.0));
+  long long bound = 0;
+  for (int i = 0; i < n; ++i) {
+    const exm_world_obstacle& o = o_in[i];
+    SenseObs& so = w->obs[static_cast<size_t>(i)];
+    w->offsets[static_cast<size_t>(i)] = make_double2(o.offset[0], o.offset[1]);
     if (o.kind == EXM_OBSTACLE_POLYGON) {
       if (o.count < 3 || !o.x || !o.y) return fail(EXM_ERR_INVALID_ARGUMENT, "obstacle polygon needs at least 3 vertices");
       so.kind = 0;
       so.count = o.count;
-      so.first = static_cast<int>(verts.size());
-      for (int v = 0; v < o.count; ++v) verts.push_back(make_double2(o.x[v], o.y[v]));
+      so.first = static_cast<int>(w->verts.size());
+      for (int v = 0; v < o.count; ++v) w->verts.push_back(make_double2(o.x[v], o.y[v]));
       for (int v = 0; v < o.count; ++v) {
-        const int w = v + 1 == o.count ? 0 : v + 1;
+        const int u = v + 1 == o.count ? 0 : v + 1;
         SenseSeg g = {};
         g.kind = 0;
         g.obs = i;
-        g.ax = o.x[v] + ox;
-        g.ay = o.y[v] + oy;
-        g.bx = o.x[w] + ox;
-        g.by = o.y[w] + oy;
+        g.ax = o.x[v];
+        g.ay = o.y[v];
+        g.bx = o.x[u];
+        g.by = o.y[u];
         const double ex = g.bx - g.ax, ey = g.by - g.ay;
-        const double len = std::sqrt(ex * ex + ey * ey);
-        g.steps = std::max(1, static_cast<int>(std::ceil(len / kSpacing)));
-        g.start = total;
-        total += g.steps;
-        seg.push_back(g);
+        bound += std::max(1, static_cast<int>(std::ceil(std::sqrt(ex * ex + ey * ey) / kSpacing))) + 1;
+        w->seg.push_back(g);
       }
     } else if (o.kind == EXM_OBSTACLE_DISC) {
       if (!o.x || !o.y || !(o.radius >= 0.0)) return fail(EXM_ERR_INVALID_ARGUMENT, "bad disc obstacle");
@@ -1811,51 +1844,241 @@ exm_status exm_sense(exm_handle* h, const exm_world_obstacle* obstacles, int32_t
       g.obs = i;
       g.ax = o.x[0];
       g.ay = o.y[0];
-      g.bx = ox;
-      g.by = oy;
       g.r = o.radius;
-      const double circumference = 2.0 * kPiHost * o.radius;
-      g.steps = std::max(8, static_cast<int>(std::ceil(circumference / kSpacing)));
-      g.start = total;
-      total += g.steps;
-      seg.push_back(g);
+      bound += std::max(8, static_cast<int>(std::ceil(2.0 * kPiHost * o.radius / kSpacing))) + 1;
+      w->seg.push_back(g);
     } else {
       return fail(EXM_ERR_INVALID_ARGUMENT, "unknown obstacle kind");
     }
+    if (tr && tr[i].n_waypoints >= 2) {  // TrailMotion (world.hpp): waypoints >= 2, speed >= 0
+      if (!tr[i].waypoints || !(tr[i].speed >= 0.0))
+        return fail(EXM_ERR_INVALID_ARGUMENT, "bad obstacle trail");
+      TrailDev& t = w->trails[static_cast<size_t>(i)];
+      t.first = static_cast<int>(w->waypoints.size());
+      t.n = tr[i].n_waypoints;
+      t.ping_pong = tr[i].ping_pong ? 1 : 0;
+      t.speed = tr[i].speed;
+      for (int k = 0; k < t.n; ++k)
+        w->waypoints.push_back(make_double2(tr[i].waypoints[2 * k], tr[i].waypoints[2 * k + 1]));
+    }
   }
-  EXM_CUDA(cudaSetDevice(h->device));
-  cudaStream_t s = h->stream;
-  auto up = [](size_t b) { return (b + 255) & ~static_cast<size_t>(255); };  // region alignment
-  const size_t b_seg = up(std::max<size_t>(seg.size(), 1) * sizeof(SenseSeg));
-  const size_t b_obs = up(std::max<size_t>(obs.size(), 1) * sizeof(SenseObs));
-  const size_t b_ver = up(std::max<size_t>(verts.size(), 1) * sizeof(double2));
-  const size_t b_out = static_cast<size_t>(budget) * (2 * sizeof(double) + 1) + 16;
-  const size_t need = b_seg + b_obs + b_ver + b_out + 64;
-  if (need > h->sense_bytes) {
-    if (h->d_sense) cudaFree(h->d_sense);
-    h->d_sense = nullptr;
-    h->sense_bytes = 0;
-    EXM_CUDA(cudaMalloc(&h->d_sense, need));
-    h->sense_bytes = need;
+  w->sample_bound = static_cast<int>(std::min<long long>(bound + 64, 1 << 26));
+  return EXM_OK;
+}
+
+void world_free(exm_world* w) {
+  if (!w) return;
+  if (w->d_block) cudaFree(w->d_block);
+  if (w->h_out) cudaFreeHost(w->h_out);
+  delete w;
+}
+
+// Device block of a world (geometry + state + scratch + outputs) with room for `wh`; reuses `w`
+// when its capacities suffice (a handle's one-shot sensing workspace), else reallocates.
+exm_status world_reserve(exm_handle* h, const WorldHost& wh, int budget, exm_world** io) {
+  exm_world* w = *io;
+  const int nseg = static_cast<int>(wh.seg.size()), n_obs = static_cast<int>(wh.obs.size());
+  const int nv = static_cast<int>(wh.verts.size()), nw = static_cast<int>(wh.waypoints.size());
+  if (w && w->cap_seg >= nseg && w->cap_obs >= n_obs && w->cap_verts >= nv && w->cap_wp >= nw &&
+      w->cap_budget >= budget && w->sample_cap >= wh.sample_bound) {
+    w->nseg = nseg;
+    w->n_obs = n_obs;
+    w->budget = budget;
+    w->out_n = reinterpret_cast<int*>(
+        (reinterpret_cast<uintptr_t>(w->out_mask + budget) + 3) & ~static_cast<uintptr_t>(3));
+    return EXM_OK;
   }
-  char* d = static_cast<char*>(h->d_sense);
-  SenseSeg* d_seg = reinterpret_cast<SenseSeg*>(d);
-  SenseObs* d_obs = reinterpret_cast<SenseObs*>(d + b_seg);
-  double2* d_ver = reinterpret_cast<double2*>(d + b_seg + b_obs);
-  double* d_pts = reinterpret_cast<double*>(d + b_seg + b_obs + b_ver);
-  int* d_n = reinterpret_cast<int*>(d_pts + 2 * static_cast<size_t>(budget));
-  uint8_t* d_mask = reinterpret_cast<uint8_t*>(d_n + 4);
-  if (!seg.empty()) EXM_CUDA(cudaMemcpyAsync(d_seg, seg.data(), seg.size() * sizeof(SenseSeg), cudaMemcpyHostToDevice, s));
-  if (!obs.empty()) EXM_CUDA(cudaMemcpyAsync(d_obs, obs.data(), obs.size() * sizeof(SenseObs), cudaMemcpyHostToDevice, s));
-  if (!verts.empty()) EXM_CUDA(cudaMemcpyAsync(d_ver, verts.data(), verts.size() * sizeof(double2), cudaMemcpyHostToDevice, s));
-  EXM_CUDA(launch_sense(d_seg, static_cast<int>(seg.size()), total, d_obs, n_obstacles, d_ver,
-                        robot[0], robot[1], range, budget, seed, sample_key, d_pts, d_mask, d_n, s));
-  int n_host = 0;
-  EXM_CUDA(cudaMemcpyAsync(pts_out, d_pts, 2 * static_cast<size_t>(budget) * sizeof(double), cudaMemcpyDeviceToHost, s));
-  EXM_CUDA(cudaMemcpyAsync(mask_out, d_mask, static_cast<size_t>(budget), cudaMemcpyDeviceToHost, s));
-  EXM_CUDA(cudaMemcpyAsync(&n_host, d_n, sizeof(int), cudaMemcpyDeviceToHost, s));
+  world_free(w);
+  *io = nullptr;
+  w = new exm_world();
+  w->h = h;
+  w->nseg = nseg;
+  w->n_obs = n_obs;
+  w->budget = budget;
+  w->cap_seg = std::max(nseg, 1);
+  w->cap_obs = std::max(n_obs, 1);
+  w->cap_verts = std::max(nv, 1);
+  w->cap_wp = std::max(nw, 1);
+  w->cap_budget = budget;
+  w->sample_cap = wh.sample_bound;
+  auto up = [](size_t b) { return (b + 255) & ~static_cast<size_t>(255); };
+  size_t off = 0;
+  const size_t o_seg = off; off += up(w->cap_seg * sizeof(SenseSeg));
+  const size_t o_obs = off; off += up(w->cap_obs * sizeof(SenseObs));
+  const size_t o_ver = off; off += up(w->cap_verts * sizeof(double2));
+  const size_t o_tr = off; off += up(w->cap_obs * sizeof(TrailDev));
+  const size_t o_wp = off; off += up(w->cap_wp * sizeof(double2));
+  const size_t o_off = off; off += up(w->cap_obs * sizeof(double2));
+  const size_t o_arc = off; off += up(w->cap_obs * sizeof(double));
+  const size_t o_dir = off; off += up(w->cap_obs * sizeof(int));
+  const size_t o_ss = off; off += up(2 * static_cast<size_t>(w->cap_seg) * sizeof(int));
+  const size_t o_ds = off; off += up(static_cast<size_t>(w->sample_cap) * sizeof(double));
+  const size_t o_bs = off; off += up(static_cast<size_t>(w->sample_cap) * sizeof(int));
+  const size_t o_bins = off; off += up(sense_bin_state_bytes());
+  const size_t o_out = off;
+  w->out_bytes = static_cast<size_t>(budget) * (2 * sizeof(double) + 1) + 16;
+  off += up(w->out_bytes);
+  cudaError_t e = cudaMalloc(&w->d_block, off);
+  if (e == cudaSuccess) e = cudaMallocHost(reinterpret_cast<void**>(&w->h_out), w->out_bytes);
+  if (e != cudaSuccess) {
+    world_free(w);
+    return fail(EXM_ERR_CUDA, std::string("world alloc: ") + cudaGetErrorString(e));
+  }
+  char* d = static_cast<char*>(w->d_block);
+  w->seg = reinterpret_cast<SenseSeg*>(d + o_seg);
+  w->obs = reinterpret_cast<SenseObs*>(d + o_obs);
+  w->verts = reinterpret_cast<double2*>(d + o_ver);
+  w->trails = reinterpret_cast<TrailDev*>(d + o_tr);
+  w->waypoints = reinterpret_cast<double2*>(d + o_wp);
+  w->offsets = reinterpret_cast<double2*>(d + o_off);
+  w->arc = reinterpret_cast<double*>(d + o_arc);
+  w->dir = reinterpret_cast<int*>(d + o_dir);
+  w->seg_scratch = reinterpret_cast<int*>(d + o_ss);
+  w->d_scratch = reinterpret_cast<double*>(d + o_ds);
+  w->bin_scratch = reinterpret_cast<int*>(d + o_bs);
+  w->bins = d + o_bins;
+  w->out_pts = reinterpret_cast<double*>(d + o_out);
+  w->out_mask = reinterpret_cast<uint8_t*>(w->out_pts + 2 * static_cast<size_t>(budget));
+  // n after the mask, 4-byte aligned (out_bytes leaves room for it)
+  w->out_n = reinterpret_cast<int*>(
+      (reinterpret_cast<uintptr_t>(w->out_mask + budget) + 3) & ~static_cast<uintptr_t>(3));
+  *io = w;
+  return EXM_OK;
+}
+
+// Geometry, trails and the initial state (WorldState::initial: arc 0, direction +1) to the device.
+exm_status world_upload(exm_world* w, const WorldHost& wh, double range, uint64_t seed) {
+  w->range = range;
+  w->seed = seed;
+  cudaStream_t s = w->h->stream;
+  // the geometry copies are small; pageable copies return once the driver has staged them
+  auto h2d = [&](void* dst, const void* src, size_t bytes) {
+    return bytes ? cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, s) : cudaSuccess;
+  };
+  const size_t n_o = wh.obs.size();
+  std::vector<double> arc0(n_o, 0.0);
+  std::vector<int> dir0(n_o, 1);
+  cudaError_t e;
+  if ((e = h2d(w->seg, wh.seg.data(), wh.seg.size() * sizeof(SenseSeg))) != cudaSuccess ||
+      (e = h2d(w->obs, wh.obs.data(), n_o * sizeof(SenseObs))) != cudaSuccess ||
+      (e = h2d(w->verts, wh.verts.data(), wh.verts.size() * sizeof(double2))) != cudaSuccess ||
+      (e = h2d(w->trails, wh.trails.data(), wh.trails.size() * sizeof(TrailDev))) != cudaSuccess ||
+      (e = h2d(w->waypoints, wh.waypoints.data(), wh.waypoints.size() * sizeof(double2))) != cudaSuccess ||
+      (e = h2d(w->offsets, wh.offsets.data(), n_o * sizeof(double2))) != cudaSuccess ||
+      (e = h2d(w->arc, arc0.data(), n_o * sizeof(double))) != cudaSuccess ||
+      (e = h2d(w->dir, dir0.data(), n_o * sizeof(int))) != cudaSuccess)
+    return fail(EXM_ERR_CUDA, std::string("world upload: ") + cudaGetErrorString(e));
+  return EXM_OK;
+}
+
+// sense() on the device with the world's current offsets; the padded ObstacleSet back to the host.
+exm_status world_sense(exm_world* w, const double robot[3], uint64_t sample_key, double* pts_out,
+                       uint8_t* mask_out, int32_t* n_valid) {
+  cudaStream_t s = w->h->stream;
+  EXM_CUDA(launch_sense(w->seg, w->nseg, w->obs, w->n_obs, w->verts, w->offsets, robot[0],
+                        robot[1], w->range, w->budget, w->seed, sample_key, w->seg_scratch,
+                        w->d_scratch, w->bin_scratch, w->sample_cap, w->bins, w->out_pts,
+                        w->out_mask, w->out_n, s));
+  EXM_CUDA(cudaMemcpyAsync(w->h_out, w->out_pts, w->out_bytes, cudaMemcpyDeviceToHost, s));
   EXM_CUDA(cudaStreamSynchronize(s));
-  if (n_valid) *n_valid = n_host;
+  const size_t b = static_cast<size_t>(w->budget);
+  std::memcpy(pts_out, w->h_out, 2 * b * sizeof(double));
+  std::memcpy(mask_out, w->h_out + 2 * b * sizeof(double), b);
+  if (n_valid)
+    *n_valid = *reinterpret_cast<const int*>(
+        w->h_out + (reinterpret_cast<const unsigned char*>(w->out_n) -
+                    reinterpret_cast<const unsigned char*>(w->out_pts)));
+  return EXM_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+// sense(scenario, state, robot, sample_key) (world.cpp:182-243) for obstacles displaced by the
+// given offsets: a transient world (geometry built on the host, no trails), one device launch.
+exm_status exm_sense(exm_handle* h, const exm_world_obstacle* obstacles, int32_t n_obstacles,
+                     const double robot[3], double range, int32_t budget, uint64_t seed,
+                     uint64_t sample_key, double* pts_out, uint8_t* mask_out, int32_t* n_valid) {
+  if (!h || !robot || !pts_out || !mask_out || (n_obstacles > 0 && !obstacles))
+    return fail(EXM_ERR_INVALID_ARGUMENT, "null argument");
+  if (budget < 1) return fail(EXM_ERR_INVALID_ARGUMENT, "sensor budget must be >= 1");
+  std::lock_guard<std::mutex> lk(h->mu);
+  WorldHost wh;
+  exm_status st = build_world(obstacles, n_obstacles, nullptr, &wh);
+  if (st != EXM_OK) return st;
+  EXM_CUDA(cudaSetDevice(h->device));
+  if ((st = world_reserve(h, wh, budget, &h->sense_ws)) != EXM_OK) return st;
+  if ((st = world_upload(h->sense_ws, wh, range, seed)) != EXM_OK) return st;
+  return world_sense(h->sense_ws, robot, sample_key, pts_out, mask_out, n_valid);
+}
+
+exm_status exm_world_create(exm_handle* h, const exm_world_obstacle* obstacles,
+                            const exm_world_trail* trails, int32_t n_obstacles, double range,
+                            int32_t budget, uint64_t seed, exm_world** out) {
+  if (!out) return fail(EXM_ERR_INVALID_ARGUMENT, "out world pointer is null");
+  *out = nullptr;
+  if (!h || (n_obstacles > 0 && !obstacles)) return fail(EXM_ERR_INVALID_ARGUMENT, "null argument");
+  if (budget < 1) return fail(EXM_ERR_INVALID_ARGUMENT, "sensor budget must be >= 1");
+  std::lock_guard<std::mutex> lk(h->mu);
+  WorldHost wh;
+  exm_status st = build_world(obstacles, n_obstacles, trails, &wh);
+  if (st != EXM_OK) return st;
+  EXM_CUDA(cudaSetDevice(h->device));
+  exm_world* w = nullptr;
+  if ((st = world_reserve(h, wh, budget, &w)) != EXM_OK) return st;
+  if ((st = world_upload(w, wh, range, seed)) != EXM_OK) {
+    world_free(w);
+    return st;
+  }
+  // offsets of the initial state (arc 0: the shapes sit at their first waypoint)
+  if (const cudaError_t e = launch_world_step(w->trails, w->waypoints, w->n_obs, 1.0, 0, w->arc,
+                                              w->dir, w->offsets, h->stream);
+      e != cudaSuccess) {
+    world_free(w);
+    return fail(EXM_ERR_CUDA, std::string("world init: ") + cudaGetErrorString(e));
+  }
+  *out = w;
+  return EXM_OK;
+}
+
+void exm_world_destroy(exm_world* w) {
+  if (!w) return;
+  std::lock_guard<std::mutex> lk(w->h->mu);
+  cudaSetDevice(w->h->device);
+  cudaStreamSynchronize(w->h->stream);
+  world_free(w);
+}
+
+exm_status exm_world_step(exm_world* w, double dt) {
+  if (!w) return fail(EXM_ERR_INVALID_ARGUMENT, "world is null");
+  if (!(dt > 0.0)) return fail(EXM_ERR_INVALID_ARGUMENT, "step_world requires dt > 0");
+  std::lock_guard<std::mutex> lk(w->h->mu);
+  EXM_CUDA(cudaSetDevice(w->h->device));
+  EXM_CUDA(launch_world_step(w->trails, w->waypoints, w->n_obs, dt, 1, w->arc, w->dir, w->offsets,
+                             w->h->stream));
+  return EXM_OK;
+}
+
+exm_status exm_world_sense(exm_world* w, const double robot[3], uint64_t sample_key,
+                           double* pts_out, uint8_t* mask_out, int32_t* n_valid) {
+  if (!w || !robot || !pts_out || !mask_out) return fail(EXM_ERR_INVALID_ARGUMENT, "null argument");
+  std::lock_guard<std::mutex> lk(w->h->mu);
+  EXM_CUDA(cudaSetDevice(w->h->device));
+  return world_sense(w, robot, sample_key, pts_out, mask_out, n_valid);
+}
+
+exm_status exm_world_state(exm_world* w, double* arc_out, int32_t* dir_out, double* offsets_out) {
+  if (!w) return fail(EXM_ERR_INVALID_ARGUMENT, "world is null");
+  std::lock_guard<std::mutex> lk(w->h->mu);
+  EXM_CUDA(cudaSetDevice(w->h->device));
+  cudaStream_t s = w->h->stream;
+  const size_t n = static_cast<size_t>(w->n_obs);
+  if (arc_out && n) EXM_CUDA(cudaMemcpyAsync(arc_out, w->arc, n * sizeof(double), cudaMemcpyDeviceToHost, s));
+  if (dir_out && n) EXM_CUDA(cudaMemcpyAsync(dir_out, w->dir, n * sizeof(int), cudaMemcpyDeviceToHost, s));
+  if (offsets_out && n)
+    EXM_CUDA(cudaMemcpyAsync(offsets_out, w->offsets, n * sizeof(double2), cudaMemcpyDeviceToHost, s));
+  EXM_CUDA(cudaStreamSynchronize(s));
   return EXM_OK;
 }
 

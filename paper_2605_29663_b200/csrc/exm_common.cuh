@@ -85,12 +85,13 @@ inline size_t cloud_capacity(int n_cap) {
 }
 
 // Sensing (exm_world.cu): boundary-sample segments in the reference's sampling order and the
-// obstacles for the line-of-sight test (world.cpp:39-65, :167-179). Built on the host.
+// obstacles for the line-of-sight test (world.cpp:39-65, :167-179), as base geometry: every
+// obstacle's current trail offset comes from a device array (offsets[obs]), so the sample counts
+// of displaced polygon edges (which depend on the offset through rounding) are formed on the
+// device, as is the whole world state of the device world (exm_world_*).
 struct SenseSeg {
-  int kind;   // 0 polygon edge a -> b (vertices + offset), 1 disc (centre a, offset b, radius r)
-  int steps;  // samples on this segment
-  int start;  // global index of its first sample
-  int obs;
+  int kind;   // 0 polygon edge a -> b (base vertices), 1 disc (base centre a, radius r)
+  int obs;    // obstacle index (offset)
   double ax, ay, bx, by, r;
 };
 struct SenseObs {
@@ -98,7 +99,14 @@ struct SenseObs {
   int count;
   int first;
   int reserved;
-  double cx, cy, ox, oy, r;  // disc centre, offset, radius
+  double cx, cy, r;  // disc centre (base), radius
+};
+// Trail motion of one obstacle (world.hpp TrailMotion) and its state (WorldState).
+struct TrailDev {
+  int first, n;     // waypoints[first .. first + n) (n < 2: static)
+  int ping_pong;
+  int reserved;
+  double speed;
 };
 
 // Per-step small inputs, uploaded with one copy (host API) or kept resident.
@@ -256,10 +264,22 @@ cudaError_t launch_sdf_points(const FpDev& fp, const float2* q, int n, float* ou
 cudaError_t launch_sdf_pairs(const FpDev& fp, const float4* poses, int n_poses,
                              const float2* pts, const uint8_t* mask, int n_points,
                              float* per_pair, unsigned* pose_min_key, cudaStream_t s);
-cudaError_t launch_sense(const SenseSeg* seg, int nseg, int n_samples, const SenseObs* obs,
-                         int n_obs, const double2* verts, double rx, double ry, double range,
-                         int budget, uint64_t seed, uint64_t sample_key, double* pts_out,
-                         uint8_t* mask_out, int* n_out, cudaStream_t s);
+// sense (world.cpp:182-243) over base geometry displaced by offsets[n_obs]; scratch: 2 ints per
+// segment, a double and an int per sample (sample_cap samples; more fall back to recomputation),
+// bin_state (sense_bin_state_bytes()).
+cudaError_t launch_sense(const SenseSeg* seg, int nseg, const SenseObs* obs, int n_obs,
+                         const double2* verts, const double2* offsets, double rx, double ry,
+                         double range, int budget, uint64_t seed, uint64_t sample_key,
+                         int* seg_scratch, double* d_scratch, int* bin_scratch, int sample_cap,
+                         void* bin_state, double* pts_out, uint8_t* mask_out, int* n_out,
+                         cudaStream_t s);
+size_t sense_bin_state_bytes();
+// step_world (world.cpp:127-157) + obstacle_offset (:159-164) for n_obs obstacles on the device:
+// arc / direction advanced by dt (dt > 0) when `advance`, then offsets[i] = trail point - first
+// waypoint.
+cudaError_t launch_world_step(const TrailDev* trails, const double2* waypoints, int n_obs,
+                              double dt, int advance, double* arc, int* dir, double2* offsets,
+                              cudaStream_t s);
 cudaError_t launch_min_keys_to_double(const unsigned* keys, int n, double* out, cudaStream_t s);
 cudaError_t launch_fill_u32(unsigned* p, unsigned v, int n, cudaStream_t s);
 

@@ -422,3 +422,70 @@ def reference_sense(obstacles, robot, sensor_range, budget, seed, sample_key):
     if rc:
         raise ValueError(L.ref_last_error().decode())
     return pts, mask, n.value
+
+
+class ReferenceWorld:
+    """The reference's Scenario + WorldState with trail motion: step_world and sense
+    (world.cpp:127-243) through oracle/_ref (ref_world_*)."""
+
+    def __init__(self, obstacles, trails, sensor_range, budget, seed):
+        from paper_2605_29663_b200.api import world_obstacles_c
+        L = ref_lib()
+        if not hasattr(L, "_world_ready"):
+            L.ref_world_create.restype = C.c_void_p
+            L.ref_world_create.argtypes = [C.c_void_p, C.POINTER(C.c_int32), C.POINTER(_dp), _dp,
+                                           C.POINTER(C.c_int32), C.c_int, C.c_double, C.c_int,
+                                           C.c_uint64]
+            L.ref_world_destroy.argtypes = [C.c_void_p]
+            L.ref_world_step.restype = C.c_int
+            L.ref_world_step.argtypes = [C.c_void_p, C.c_double]
+            L.ref_world_state.argtypes = [C.c_void_p, _dp, C.POINTER(C.c_int32), _dp]
+            L.ref_world_sense.restype = C.c_int
+            L.ref_world_sense.argtypes = [C.c_void_p, _dp, C.c_uint64, _dp, _u8p,
+                                          C.POINTER(C.c_int32)]
+            L._world_ready = True
+        self.L, self.n, self.budget = L, len(obstacles), int(budget)
+        arr, self._keep = world_obstacles_c(obstacles)
+        n = self.n
+        nwp = (C.c_int32 * max(n, 1))()
+        wps = (_dp * max(n, 1))()
+        spd = np.zeros(max(n, 1))
+        pp = (C.c_int32 * max(n, 1))()
+        self._wp = []
+        for i, t in enumerate(trails or []):
+            if t is None:
+                continue
+            w = np.ascontiguousarray(t.waypoints)
+            self._wp.append(w)
+            nwp[i], wps[i], spd[i], pp[i] = w.shape[0], _p(w), t.speed, 1 if t.ping_pong else 0
+        self._spd = spd
+        self.ctx = L.ref_world_create(C.cast(arr, C.c_void_p), nwp, wps, _p(spd), pp, n,
+                                      float(sensor_range), self.budget, int(seed))
+        if not self.ctx:
+            raise ValueError(L.ref_last_error().decode())
+
+    def __del__(self):
+        try:
+            self.L.ref_world_destroy(self.ctx)
+        except Exception:
+            pass
+
+    def step(self, dt):
+        if self.L.ref_world_step(self.ctx, float(dt)):
+            raise ValueError(self.L.ref_last_error().decode())
+
+    def state(self):
+        arc = np.empty(max(self.n, 1))
+        d = np.empty(max(self.n, 1), np.int32)
+        off = np.empty((max(self.n, 1), 2))
+        self.L.ref_world_state(self.ctx, _p(arc), d.ctypes.data_as(C.POINTER(C.c_int32)), _p(off))
+        return arc[: self.n], d[: self.n], off[: self.n]
+
+    def sense(self, robot, key):
+        pts = np.empty((self.budget, 2))
+        mask = np.empty(self.budget, np.uint8)
+        n = C.c_int32()
+        if self.L.ref_world_sense(self.ctx, _p(_c(robot)), int(key), _p(pts),
+                                  mask.ctypes.data_as(_u8p), C.byref(n)):
+            raise ValueError(self.L.ref_last_error().decode())
+        return pts, mask, n.value

@@ -9,7 +9,7 @@ import pytest
 
 from paper_2605_29663_b200 import workloads as W
 from paper_2605_29663_b200.api import Engine, WorldObstacle
-from tests.oracle_bindings import reference_available, reference_sense
+from tests.oracle_bindings import ReferenceWorld, reference_available, reference_sense
 
 pytestmark = [pytest.mark.gpu,
               pytest.mark.skipif(not reference_available(), reason="oracle/_ref not built")]
@@ -83,3 +83,54 @@ def test_sensed_cloud_drives_a_control_cycle():
     nom, up = wl.zero_state()
     d = eng.control_cycle_raw(wl.q0, cloud, wl.guidance, nom, up, 0, None)
     assert np.all(np.isfinite(d.command))
+
+
+def _moving_world(seed=11):
+    """omni_gap walls (static) + 24 discs on 2-waypoint ping-pong trails + two trap polygons, one
+    on a clamped 3-waypoint trail, one on a ping-pong 3-waypoint trail (cfg5-style motion)."""
+    from paper_2605_29663_b200.api import Trail
+    obs = [WorldObstacle.polygon(p) for p in W.OMNI_WALLS]
+    trails = [None] * len(obs)
+    for k in range(24):
+        ax, ay = W.uniform_range(seed, k, 0, -6.0, 6.0), W.uniform_range(seed, k, 1, -6.0, 6.0)
+        bx, by = W.uniform_range(seed, k, 2, -6.0, 6.0), W.uniform_range(seed, k, 3, -6.0, 6.0)
+        obs.append(WorldObstacle.disc((ax, ay), W.uniform_range(seed, k, 4, 0.2, 0.5)))
+        trails.append(Trail([[ax, ay], [bx, by]], W.uniform_range(seed, k, 5, 0.0, 1.5)))
+    p0, p1 = W.TRAP_OBSTACLES[3], W.TRAP_OBSTACLES[2]
+    obs += [WorldObstacle.polygon(p0), WorldObstacle.polygon(p1)]
+    trails += [Trail([p0[0], [p0[0][0] + 1.0, p0[0][1] + 0.3], [p0[0][0] + 1.5, p0[0][1] - 0.7]], 0.9,
+                     ping_pong=False),
+               Trail([p1[0], [p1[0][0] - 0.4, p1[0][1]], [p1[0][0] - 0.4, p1[0][1] + 0.6]], 1.3)]
+    return obs, trails
+
+
+def test_device_world_steps_and_senses_like_the_reference():
+    """step_world (world.cpp:127-157) on the device: arc, direction and obstacle offsets bit for
+    bit against the reference over 80 steps (reflections and clamps included), and sense() from
+    the device state against the reference's sense() on its own state."""
+    eng = _engine()
+    obs, trails = _moving_world()
+    dev = eng.world(obs, trails, 10.0, 400, 7)
+    ref = ReferenceWorld(obs, trails, 10.0, 400, 7)
+    a0, d0, o0 = dev.state()
+    ra, rd, ro = ref.state()
+    assert np.array_equal(a0, ra) and np.array_equal(d0, rd) and np.array_equal(o0, ro)
+    rng = np.random.default_rng(4)
+    for step in range(80):
+        dt = 0.1 if step % 7 else 0.37
+        dev.step(dt)
+        ref.step(dt)
+        a, d, o = dev.state()
+        ra, rd, ro = ref.state()
+        assert np.array_equal(a, ra) and np.array_equal(d, rd), step
+        assert np.array_equal(o, ro), step
+        if step % 10 == 9:
+            robot = np.array([rng.uniform(-4, 4), rng.uniform(-2, 2), 0.0])
+            got = dev.sense(robot, 50 + step)
+            pts, mask, n = ref.sense(robot, 50 + step)
+            assert np.array_equal(got.mask, mask), step
+            assert np.allclose(got.points, pts, rtol=0, atol=1e-12), step
+    assert (d == -1).any(), "no trail reflected: the test does not cover ping-pong"
+    with pytest.raises(ValueError, match="dt > 0"):
+        dev.step(0.0)
+    dev.close()
