@@ -883,7 +883,13 @@ __device__ __forceinline__ void sdf_grid_warp(const FpDev& fp, const float4* __r
 // busy SMs). The last warp to finish resets the counter pair for the next launch.
 // work == nullptr: static mapping, warp <-> poses blockIdx.x * 128 + warp * 32 + lane.
 template <int KIND, int NB, bool STATS = false, int MODE = kGridFull>
-__global__ void __launch_bounds__(128) k_sdf_grid(const __grid_constant__ FpDev fp,
+#ifndef EXM_GRID_MINB  // A/B builds: minimum resident CTAs per SM (caps registers)
+#define EXM_GRID_MINB 1
+#endif
+#ifndef EXM_GRID_THREADS  // A/B builds: threads per CTA (32-128 measured within 1 %, round 1)
+#define EXM_GRID_THREADS 128
+#endif
+__global__ void __launch_bounds__(EXM_GRID_THREADS, EXM_GRID_MINB) k_sdf_grid(const __grid_constant__ FpDev fp,
                                                   const float4* __restrict__ poses, int n_poses,
                                                   const GridMeta* __restrict__ gmp,
                                                   const int* __restrict__ cell_start,
@@ -1467,7 +1473,7 @@ constexpr int kPersistentWaves = EXM_PERSIST_WAVES;
 #else
 constexpr int kPersistentWaves = 8;
 #endif
-constexpr int kGridThreads = 128;  // 32-128 measured within 1 % (round 1)
+constexpr int kGridThreads = EXM_GRID_THREADS;
 
 template <int KIND, int NB, bool STATS, int MODE>
 cudaError_t launch_grid_kernel(const FpDev& fp, const float4* poses, int n_poses, int T,

@@ -316,3 +316,105 @@ def test_task_cost_polyline_edge_cases(case):
     g = eng.validate_nominal(nom, wl.q0, wl.obstacles(), wl.guidance, up)
     o = orc.validate_nominal(nom, wl.q0, wl.cloud, None, wl.guidance, up)
     assert g[0] == o[0] and abs(g[2] - o[2]) <= 1e-5 * max(1.0, abs(o[2]))
+
+
+@pytest.mark.parametrize("n", [1, 2047, 65536 + 3, 300_001])
+@pytest.mark.parametrize("threads", [1, 3, 8])
+def test_batch_signed_distance_pipeline_chunks(n, threads):
+    """exm_batch_signed_distance's pipeline (up to 8 chunks of >= 64k queries over three
+    slot streams, host threads staging FP32 / widening FP64): every query, odd sizes and chunk
+    boundaries, each host thread count, against the oracle (geometry.cpp:298-318)."""
+    from paper_2605_29663_b200 import _abi
+    wl = W.cfg1(K=4, T=2)
+    wl.footprint = W.footprint("t_shape")
+    eng, orc = engine_and_oracle(wl)
+    eng.set_option(_abi.OPT_HOST_THREADS, threads)
+    q = W.benchmark_queries(n, 12.0, 5 + n)
+    got = eng.batch_signed_distance(q)
+    want = orc.batch_signed_distance(q)
+    assert got.shape == want.shape
+    assert sd_close(got, want) <= SD_TOL and sign_mismatch(got, want) == 0
+    again = eng.batch_signed_distance(q)  # buffers reused: identical
+    assert np.array_equal(got, again)
+
+
+def test_sdf_batch_recentres_on_device():
+    """exm_sdf_stage: poses and points recentred at the poses' centroid on the device (no host
+    loop); far-from-origin inputs keep the 1e-5 bound, the run/read split equals one-shot."""
+    wl = W.cfg2(K=4, T=2, N=800)
+    eng, orc = engine_and_oracle(wl)
+    shift = np.array([1.5e3, -2.25e3])
+    poses = W.cfg4_poses(64) * np.array([0.5, 0.5, 1.0]) + np.r_[shift, 0.0]
+    pts = wl.cloud + shift
+    mins = eng.sdf_batch(poses, pts)
+    want = orc.sdf_batch(poses, pts)
+    assert sd_close(mins, want) <= SD_TOL
+    eng.sdf_stage(poses, pts)
+    eng.sdf_run_resident(3, False)
+    m2, _ = eng.sdf_read()
+    assert np.array_equal(m2, mins)
+    st = eng.step_stats()
+    assert st["sdf_ms"] > 0 and st["launches_per_step"] == 3
+
+
+def test_sdf_timing_ring_is_bounded():
+    """Round 1 leaked two events per exm_sdf_batch call; the ring now folds at 512 entries and
+    one-shot calls never use it: thousands of calls keep working and step_stats stays valid."""
+    wl = W.cfg2(K=4, T=2, N=200)
+    eng, _ = engine_and_oracle(wl)
+    poses = W.cfg4_poses(8)
+    for _ in range(1500):
+        eng.sdf_batch(poses, wl.cloud)
+    eng.sdf_stage(poses, wl.cloud)
+    eng.sdf_run_resident(1200, False)  # more than one fold of the resident ring
+    st = eng.step_stats()
+    assert st["sdf_ms"] > 0.0
+
+
+def test_option_and_argument_errors():
+    from paper_2605_29663_b200 import _abi
+    wl = W.cfg2(K=256, T=8, N=100)
+    eng, _ = engine_and_oracle(wl)
+    with pytest.raises(ValueError, match="unknown option"):
+        eng.set_option(99, 1)
+    with pytest.raises(ValueError, match="SDF mode"):
+        eng.set_option(_abi.OPT_SDF_MODE, 42)
+    with pytest.raises(ValueError, match="mapping"):
+        eng.set_option(_abi.OPT_SDF_MAP, 7)
+    nom, up = wl.zero_state()
+    with pytest.raises(ValueError):  # nominal of the wrong length (checked before the ABI call)
+        eng.control_cycle_raw(wl.q0, wl.obstacles(), wl.guidance, np.zeros(5), up, 0)
+    from paper_2605_29663_b200.api import ObstacleSet
+    with pytest.raises(ValueError, match="mask length"):
+        ObstacleSet(wl.cloud, np.ones(3, np.uint8))
+
+
+def test_concurrent_calls_on_one_handle_serialise():
+    """Every ABI call holds its handle's lock (ctypes releases the GIL, so the four threads below
+    really call concurrently): each thread's sequence of control cycles on the shared handle
+    equals the same sequence run alone."""
+    import threading
+    wl = W.cfg2(K=512, T=12, N=1500)
+    shared, _ = engine_and_oracle(wl)
+    alone, _ = engine_and_oracle(wl)
+    qs = [wl.q0 + np.array([0.1 * t, -0.05 * t, 0.02 * t]) for t in range(4)]
+    want = []
+    for t in range(4):
+        nom, up = wl.zero_state()
+        want.append([alone.control_cycle_raw(qs[t], wl.obstacles(), wl.guidance, nom, up, 10 * t + c).command
+                     for c in range(5)])
+    got = [None] * 4
+    obst = wl.obstacles()
+
+    def run(t):
+        nom, up = wl.zero_state()
+        got[t] = [shared.control_cycle_raw(qs[t], obst, wl.guidance, nom, up, 10 * t + c).command
+                  for c in range(5)]
+    th = [threading.Thread(target=run, args=(t,)) for t in range(4)]
+    for x in th:
+        x.start()
+    for x in th:
+        x.join()
+    for t in range(4):
+        for c in range(5):
+            assert np.array_equal(got[t][c], want[t][c]), (t, c)

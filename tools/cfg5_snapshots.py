@@ -28,7 +28,6 @@ def main():
         eng.run_resident(5)
         torch.cuda.synchronize()
         eng.step_stats()
-        eng.cull_stats()
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         with torch.cuda.stream(ext):
             a.record(ext)
@@ -37,10 +36,11 @@ def main():
             b.record(ext)
         torch.cuda.synchronize()
         st = eng.step_stats()
-        tested, evaluated = eng.cull_stats()
-        pairs = wl.params.rollouts * wl.params.horizon * wl.n_points * steps
+        c = eng.sdf_work_stats()
+        poses = wl.params.rollouts * wl.params.horizon
+        per = {k: round(v / poses, 1) for k, v in c.items()}
         print(f"snapshot {j}: step {a.elapsed_time(b) / steps:.3f} ms  sdf {st['sdf_ms']:.3f} ms  "
-              f"point-tested {tested / pairs:.5f}  exact {evaluated / pairs:.5f} of pairs", flush=True)
+              f"per pose {per}", flush=True)
 
 
 if __name__ == "__main__":
