@@ -21,6 +21,7 @@ std::invalid_argument maps to ValueError. Arrays are numpy float64 (uint8 masks)
 from __future__ import annotations
 
 import ctypes as C
+import threading
 import json
 import math
 from dataclasses import dataclass, field
@@ -415,6 +416,18 @@ class RolloutBatch:
 
 
 # ------------------------------------------------------------------------------ engine
+class _CallScratch:
+    """Fixed-address host buffers of Engine.control_cycle_raw (one set per calling thread)."""
+
+    def __init__(self, horizon: int):
+        self.q0 = np.zeros(3)
+        self.q0addr = self.q0.ctypes.data
+        self.dmin = np.zeros(int(horizon))
+        self.dec = _abi.ExmDecision()
+        self.dec.nominal_dmin = dptr(self.dmin)
+        self.decp = C.addressof(self.dec)
+
+
 class Engine:
     """One device handle (libexm_b200.so). Sized at construction for (K, T, n_cap, guide_cap)."""
 
@@ -434,12 +447,9 @@ class Engine:
         # lean host path of control_cycle_raw: fixed-address scratch and cached addresses
         self._cc = _abi.fast_control_cycle(self.lib)
         self._hv = C.cast(h, C.c_void_p).value
-        self._q0buf = np.zeros(3)
-        self._q0addr = self._q0buf.ctypes.data
-        self._dminbuf = np.zeros(int(params.horizon))
-        self._dec = _abi.ExmDecision()
-        self._dec.nominal_dmin = dptr(self._dminbuf)
-        self._decp = C.addressof(self._dec)
+        # per-thread call scratch (q0, decision, nominal d_min): the library serialises calls on
+        # one handle, and each thread keeps its own host buffers
+        self._tls = threading.local()
         self._addrs: dict = {}
 
     def _addr(self, a, dtype=np.float64, min_size: int = 0, size: int = -1):
@@ -547,7 +557,10 @@ class Engine:
             pts, mask = obstacles.points, obstacles.mask  # validated at ObstacleSet creation
         else:
             pts, mask = self._cloud(obstacles)
-        q = self._q0buf
+        sc = getattr(self._tls, "s", None)
+        if sc is None:
+            sc = self._tls.s = _CallScratch(self.params.horizon)
+        q = sc.q0
         q[0], q[1], q[2] = q0[0], q0[1], q0[2]
         eps_addr = None
         if eps is not None:  # injected noise: not cached (a fresh array per call)
@@ -556,13 +569,13 @@ class Engine:
                 raise ValueError("perturbation array does not match K*T")
             eps_addr = eps_arr.ctypes.data
         A = self._addr
-        rc = self._cc(self._hv, self._q0addr, A(pts), A(mask, np.uint8, size=pts.shape[0]),
+        rc = self._cc(self._hv, sc.q0addr, A(pts), A(mask, np.uint8, size=pts.shape[0]),
                       pts.shape[0], A(guidance.path), guidance.path.shape[0], A(guidance.goal),
                       A(nominal, size=self.params.horizon * self.dim), A(u_prev, min_size=self.dim),
-                      int(cycle), eps_addr, self._decp)
+                      int(cycle), eps_addr, sc.decp)
         if rc:
             check(rc)
-        dec = self._dec
+        dec = sc.dec
         D = self.dim
         cmd = np.empty(D)
         c = dec.command
@@ -570,7 +583,7 @@ class Engine:
             cmd[i] = c[i]
         return ControlDecision(cmd, bool(dec.validated), nominal.reshape(-1, D).copy(),
                                dec.best_cost, dec.weight_entropy, dec.nominal_cost,
-                               self._dminbuf.copy(), dec.argmin)
+                               sc.dmin.copy(), dec.argmin)
 
     def batch_signed_distance(self, queries) -> np.ndarray:
         q = np.ascontiguousarray(np.asarray(queries, np.float64).reshape(-1, 2))

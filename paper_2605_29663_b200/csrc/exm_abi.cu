@@ -580,7 +580,7 @@ struct exm_handle {
   void* d_grid_block = nullptr;
   double* d_eps = nullptr;
   float4* d_poses = nullptr;
-  double2* d_xy = nullptr;
+  double* d_task = nullptr;  // task cost per (r, h), formed by the rollout kernel
   double* d_ctrl = nullptr;       // control cost per (r, h)
   float* d_hstat = nullptr;       // per-step d_min statistic {sum[T], sum of squares[T], count}
   float* d_cap = nullptr;         // per-step SDF caps for the next step (T; +inf: none)
@@ -683,7 +683,7 @@ void destroy_graphs(exm_handle* h) {
 
 // Phases of one control step (all stream-ordered, capturable):
 //   prep  : cloud preparation (mask, recentre, grid, in-cell sort, chunk boxes) -> grid
-//   pre   : [noise] -> rollout                                       -> d_poses, d_xy, d_base
+//   pre   : [noise] -> rollout                                       -> d_poses, d_task, d_base
 //   sdf   : per-pose exact SDF over the step's K*T poses             -> d_dmin
 //   post  : stage costs -> block partials -> [all-gather] -> merge/update/validation
 //           dynamics -> validation SDF -> finalize                    -> d_out, state
@@ -695,7 +695,8 @@ exm_status enqueue_prep(exm_handle* h, cudaStream_t s) {  // k_cloud_prep + k_ce
 exm_status enqueue_pre(exm_handle* h, bool draw_noise, cudaStream_t s, int* launches) {
   const StepConst& sc = h->sc;
   EXM_CUDA(launch_rollout(sc, h->d_dyn, h->d_nominal, h->d_eps, draw_noise ? 1 : 0, h->d_poses,
-                          h->d_xy, h->d_base, h->d_ctrl, nullptr, nullptr, s));
+                          h->d_task, h->d_guide, h->guide_cap, h->d_base, h->d_ctrl, nullptr,
+                          nullptr, s));
   ++*launches;
   return EXM_OK;
 }
@@ -707,9 +708,8 @@ exm_status enqueue_post_a(exm_handle* h, cudaStream_t s, int* launches, bool pre
   // automatic per-step caps (d_min statistic -> k_finalize) measured slower than none on the
   // benchmark configs (fallback passes): off unless EXM_OPT_AUTO_CAPS; exm_set_sdf_caps still works
   float* hstat = h->auto_caps ? h->d_hstat : nullptr;
-  EXM_CUDA(launch_rollout_costs(sc, h->d_dyn, h->d_guide, h->guide_cap, h->d_base, h->d_ctrl,
-                                h->d_xy, h->d_dmin, h->d_cost, h->d_unsafe, h->grid.dstat,
-                                hstat, s));
+  EXM_CUDA(launch_rollout_costs(sc, h->d_task, h->d_base, h->d_ctrl, h->d_dmin, h->d_cost,
+                                h->d_unsafe, h->grid.dstat, hstat, s));
   EXM_CUDA(launch_block_partials(sc, h->d_cost, h->d_unsafe, h->d_eps, h->d_partials, s));
   *launches += 2;
   if (pregen) {
@@ -1195,7 +1195,7 @@ exm_status exm_create(const exm_footprint* footprint, const exm_model* model,
   EXM_CUDA_C(cudaMemset(h->d_nstate, 0xff, 2 * sizeof(uint64_t)));
   h->sc.nstate = h->d_nstate;
   EXM_CUDA_C(dalloc(&h->d_poses, KT));
-  EXM_CUDA_C(dalloc(&h->d_xy, KT));
+  EXM_CUDA_C(dalloc(&h->d_task, KT));
   EXM_CUDA_C(dalloc(&h->d_ctrl, KT));
   EXM_CUDA_C(dalloc(&h->d_hstat, 2 * static_cast<size_t>(h->T) + 1));
   EXM_CUDA_C(cudaMemset(h->d_hstat, 0, (2 * static_cast<size_t>(h->T) + 1) * sizeof(float)));
@@ -1235,7 +1235,7 @@ void exm_destroy(exm_handle* h) {
   destroy_graphs(h);
   if (h->comm && g_nccl.destroy) g_nccl.destroy(h->comm);
   if (h->borrowed_poses) h->d_poses = nullptr, h->d_dmin = nullptr;
-  void* dev[] = {h->d_in_block, h->d_grid_block, h->d_eps, h->d_poses, h->d_xy, h->d_ctrl,
+  void* dev[] = {h->d_in_block, h->d_grid_block, h->d_eps, h->d_poses, h->d_task, h->d_ctrl,
                  h->d_hstat, h->d_cap, h->d_val_xy, h->d_base, h->d_dmin,
                  h->d_partials, h->d_upd, h->d_val_poses, h->d_val_base, h->d_val_dmin, h->d_out,
                  h->d_controls, h->d_states, h->d_cost, h->d_unsafe, h->sb_poses, h->sb_pts64,
@@ -1328,13 +1328,13 @@ exm_status exm_evaluate_rollouts(exm_handle* h, const double q0[3], const double
   cudaStream_t s = h->stream;
   const StepConst& sc = h->sc;
   EXM_CUDA(launch_cloud_prep(h->d_pts, h->d_mask, h->d_dyn, h->fp.radius, h->grid, h->n_cap, s));
-  EXM_CUDA(launch_rollout(sc, h->d_dyn, h->d_nominal, h->d_eps, 0, h->d_poses, h->d_xy, h->d_base,
-                          h->d_ctrl, controls_out ? h->d_controls : nullptr,
+  EXM_CUDA(launch_rollout(sc, h->d_dyn, h->d_nominal, h->d_eps, 0, h->d_poses, h->d_task,
+                          h->d_guide, h->guide_cap, h->d_base, h->d_ctrl,
+                          controls_out ? h->d_controls : nullptr,
                           states_out ? h->d_states : nullptr, s));
   if (const exm_status st2 = enqueue_rollout_sdf(h, s); st2 != EXM_OK) return st2;
-  EXM_CUDA(launch_rollout_costs(sc, h->d_dyn, h->d_guide, h->guide_cap, h->d_base, h->d_ctrl,
-                                h->d_xy, h->d_dmin, h->d_cost, h->d_unsafe, h->grid.dstat,
-                                nullptr, s));
+  EXM_CUDA(launch_rollout_costs(sc, h->d_task, h->d_base, h->d_ctrl, h->d_dmin, h->d_cost,
+                                h->d_unsafe, h->grid.dstat, nullptr, s));
   if (controls_out)
     EXM_CUDA(cudaMemcpyAsync(controls_out, h->d_controls, KT * h->D * sizeof(double), cudaMemcpyDeviceToHost, s));
   if (states_out)

@@ -221,24 +221,18 @@ cudaError_t launch_cloud_prep(const double* pts, const uint8_t* mask, const Step
                               float radius, const CloudGrid& g, int n_cap, cudaStream_t s);
 int chunk_for_capacity(int n_cap);
 // draw != 0: the rollout kernel draws the device noise into eps; else eps is read (injected).
-// base_cost: terminal goal cost per rollout; ctrl_cost: control cost per (r, h).
+// task: the task cost of every pre-step state (r, h) (guidance: guide_cap doubles x 2, n_guide
+// and goal in dyn); base_cost: terminal goal cost per rollout; ctrl_cost: control cost per (r, h).
 cudaError_t launch_rollout(const StepConst& sc, const StepDyn* dyn, const double* nominal,
-                           double* eps, int draw, float4* poses, double2* xy, double* base_cost,
+                           double* eps, int draw, float4* poses, double* task,
+                           const double* guide, int guide_cap, double* base_cost,
                            double* ctrl_cost, double* controls_out, double* states_out,
                            cudaStream_t s);
-// Per-pose minimum signed distance over the prepared cloud (min_signed_distance_at).
-// Rollout poses are stored [row][T] (rows = n_poses / T rollouts); T = 0 for an unstructured
-// pose list. hmajor: a warp's lanes take 32 consecutive rows at one step h (else 32
-// consecutive steps of one row); which is faster depends on the scene (exm_abi.cu tunes it). cap (optional, T floats): a guess of each step's minimum distance; the kernel
-// stays exact for any cap (capped pass, then an uncapped pass for the poses it did not
-// resolve). mode: kSdf*; path (optional) receives what ran; stats (optional, kCntN counters):
-// a statistics build of the same launch.
 cudaError_t launch_sdf_grid(const FpDev& fp, const float4* poses, int n_poses, int T, bool hmajor,
                             const CloudGrid& g, const float* cap, int mode, float* out,
                             SdfPath* path, unsigned long long* stats, cudaStream_t s);
-cudaError_t launch_rollout_costs(const StepConst& sc, const StepDyn* dyn, const double* guide,
-                                 int guide_cap, const double* base_cost, const double* ctrl_cost,
-                                 const double2* xy, const float* dmin, double* cost,
+cudaError_t launch_rollout_costs(const StepConst& sc, const double* task, const double* base_cost,
+                                 const double* ctrl_cost, const float* dmin, double* cost,
                                  uint8_t* unsafe, float* dstat, float* hstat, cudaStream_t s);
 cudaError_t launch_block_partials(const StepConst& sc, const double* cost, const uint8_t* unsafe,
                                   const double* eps, double* partials, cudaStream_t s);

@@ -169,11 +169,14 @@ constexpr float kCapSlack = 0.02f;
 // doubles of shared memory per warp. Returns the terminal goal cost in every lane.
 __host__ __device__ constexpr int rollout_warp_scratch(int T, int D) { return T * (D + 5); }
 
+// xy_row (optional): pre-step positions; task_row (optional, with guide): the task cost of every
+// pre-step state (controller.cpp:103-118), formed here off the step's critical path.
 template <int TAG>
 __device__ double rollout_warp(const StepConst& sc, const StepDyn& dyn, const double* nominal,
                                const double* eps_in, double* eps_out, uint64_t row_key,
                                float4* poses_row, double2* xy_row, double* controls_row,
-                               double* states_row, double* ctrl_out, double* scratch) {
+                               double* states_row, double* ctrl_out, double* scratch,
+                               double* task_row = nullptr, const double* guide = nullptr) {
   constexpr int D = model_dim<TAG>();
   const int T = sc.T, lane = threadIdx.x & 31;
   double* s_u = scratch;          // T*D controls (clamped in place)
@@ -277,7 +280,11 @@ __device__ double rollout_warp(const StepConst& sc, const StepDyn& dyn, const do
   for (int h = lane; h < T; h += 32) {
     poses_row[h] = make_float4(static_cast<float>(s_x[h] - qx0), static_cast<float>(s_y[h] - qy0),
                                static_cast<float>(s_c[h]), static_cast<float>(s_s[h]));
-    xy_row[h] = make_double2(s_x[h], s_y[h]);
+    if (xy_row) xy_row[h] = make_double2(s_x[h], s_y[h]);
+    if (task_row) {
+      const double q[3] = {s_x[h], s_y[h], 0.0};
+      task_row[h] = task_cost(sc, q, guide, dyn.n_guide, dyn.goal, false);
+    }
     if (states_row) {
       states_row[3 * h] = s_x[h];
       states_row[3 * h + 1] = s_y[h];
@@ -319,19 +326,22 @@ __global__ void k_noise_pregen(const StepConst sc, double* __restrict__ eps) {
 template <int TAG>
 __global__ void __launch_bounds__(kRolloutWarps * 32) k_rollout(
     const StepConst sc, const StepDyn* __restrict__ dynp, const double* __restrict__ nominal,
-    double* __restrict__ eps, int draw, float4* __restrict__ poses, double2* __restrict__ xy,
-    double* __restrict__ base_cost, double* __restrict__ ctrl_cost,
-    double* __restrict__ controls_out, double* __restrict__ states_out) {
+    double* __restrict__ eps, int draw, float4* __restrict__ poses, double* __restrict__ task,
+    const double* __restrict__ guide, int guide_cap, double* __restrict__ base_cost,
+    double* __restrict__ ctrl_cost, double* __restrict__ controls_out,
+    double* __restrict__ states_out) {
   pdl_wait();
   // One warp per rollout (rollout_warp). draw: the perturbations are drawn here (device noise,
   // written to eps for the softmax update); else eps holds injected perturbations.
   extern __shared__ double sm[];
   const int TD = sc.T * sc.D;
-  double* nom = sm;
+  double* s_guide = sm;
+  double* nom = sm + 2 * guide_cap;
   const int warp = threadIdx.x >> 5;
-  double* scratch = sm + TD + warp * rollout_warp_scratch(sc.T, sc.D);
+  double* scratch = nom + TD + warp * rollout_warp_scratch(sc.T, sc.D);
   for (int i = threadIdx.x; i < TD; i += blockDim.x) nom[i] = nominal[i];
   const StepDyn dyn = *dynp;
+  for (int i = threadIdx.x; i < 2 * dyn.n_guide; i += blockDim.x) s_guide[i] = guide[i];
   const bool gen = draw && !(sc.nstate && sc.nstate[1] == dyn.cycle);  // else pregenerated
   if (draw && sc.nstate && blockIdx.x == 0 && threadIdx.x == 0) sc.nstate[0] = dyn.cycle;
   __syncthreads();
@@ -341,10 +351,10 @@ __global__ void __launch_bounds__(kRolloutWarps * 32) k_rollout(
   double* eps_row = eps + row * sc.D;
   const double b = rollout_warp<TAG>(
       sc, dyn, nom, gen ? nullptr : eps_row, gen ? eps_row : nullptr,
-      gen ? noise_row_key(sc, dyn.cycle, r) : 0ull, poses + row, xy + row,
+      gen ? noise_row_key(sc, dyn.cycle, r) : 0ull, poses + row, nullptr,
       controls_out ? controls_out + row * sc.D : nullptr,
       states_out ? states_out + static_cast<size_t>(r) * (sc.T + 1) * 3 : nullptr, ctrl_cost + row,
-      scratch);
+      scratch, task + row, s_guide);
   if ((threadIdx.x & 31) == 0) base_cost[r] = b;
 }
 
@@ -357,18 +367,19 @@ __global__ void __launch_bounds__(kRolloutWarps * 32) k_rollout(
 // Shared memory ([item][R + 1] rows: conflict-free lanes over r):
 //   u[T*D], a[T] (heading increments -> pre-step headings), x[T], y[T] doubles, cs[T] float2
 constexpr int kLaneThreads = 256;
-__host__ __device__ constexpr size_t rollout_lanes_smem(int T, int D, int R) {
+__host__ __device__ constexpr size_t rollout_lanes_smem(int T, int D, int R, int guide_cap) {
   return sizeof(double) * (static_cast<size_t>(T) * (D + 3) * (R + 1) + static_cast<size_t>(T) * D +
-                           3 * R) +
+                           3 * R + 2 * static_cast<size_t>(guide_cap)) +
          sizeof(uint64_t) * R + sizeof(float2) * static_cast<size_t>(T) * (R + 1);
 }
 
 template <int TAG, int R>
 __global__ void __launch_bounds__(1024) k_rollout_lanes(
     const StepConst sc, const StepDyn* __restrict__ dynp, const double* __restrict__ nominal,
-    double* __restrict__ eps, int draw, float4* __restrict__ poses, double2* __restrict__ xy,
-    double* __restrict__ base_cost, double* __restrict__ ctrl_cost,
-    double* __restrict__ controls_out, double* __restrict__ states_out) {
+    double* __restrict__ eps, int draw, float4* __restrict__ poses, double* __restrict__ task,
+    const double* __restrict__ guide, int guide_cap, double* __restrict__ base_cost,
+    double* __restrict__ ctrl_cost, double* __restrict__ controls_out,
+    double* __restrict__ states_out) {
   pdl_wait();
   constexpr int D = model_dim<TAG>();
   constexpr int P = R + 1;
@@ -380,7 +391,8 @@ __global__ void __launch_bounds__(1024) k_rollout_lanes(
   double* s_y = s_x + static_cast<size_t>(T) * P;
   double* s_nom = s_y + static_cast<size_t>(T) * P;  // [TD]
   double* s_end = s_nom + TD;                 // [3][R]: x_T, y_T, theta_T
-  uint64_t* s_key = reinterpret_cast<uint64_t*>(s_end + 3 * R);
+  double* s_guide = s_end + 3 * R;            // [2 * guide_cap]: the guidance polyline
+  uint64_t* s_key = reinterpret_cast<uint64_t*>(s_guide + 2 * guide_cap);
   float2* s_cs = reinterpret_cast<float2*>(s_key + R);  // [T][P]
   const int r0 = blockIdx.x * R;
   const int nr = min(R, sc.k_local - r0);
@@ -390,6 +402,7 @@ __global__ void __launch_bounds__(1024) k_rollout_lanes(
   const bool gen = draw && !(sc.nstate && sc.nstate[1] == dyn.cycle);
   if (draw && sc.nstate && blockIdx.x == 0 && tid == 0) sc.nstate[0] = dyn.cycle;
   for (int i = tid; i < TD; i += nthr) s_nom[i] = nominal[i];
+  for (int i = tid; i < 2 * dyn.n_guide; i += nthr) s_guide[i] = guide[i];
   if (gen && tid < R) s_key[tid] = noise_row_key(sc, dyn.cycle, r0 + tid);
   __syncthreads();
   // 1. u = clamp_velocity(nominal + eps); eps drawn here (device noise) or loaded, kPre
@@ -491,7 +504,9 @@ __global__ void __launch_bounds__(1024) k_rollout_lanes(
     }
   }
   __syncthreads();
-  // 7. stores (rows of consecutive h: coalesced) and the terminal cost
+  // 7. stores (rows of consecutive h: coalesced), the task cost of every pre-step state
+  //    (controller.cpp:103-118: d_min-independent, so formed here, beside the cloud preparation,
+  //    instead of in the step's serial tail) and the terminal cost
   const double qx0 = dyn.q0[0], qy0 = dyn.q0[1];
   for (int idx = tid; idx < nr * T; idx += nthr) {
     const int r = idx / T, h = idx - r * T;
@@ -499,7 +514,8 @@ __global__ void __launch_bounds__(1024) k_rollout_lanes(
     const float2 cs = s_cs[h * P + r];
     const size_t g = static_cast<size_t>(r0) * T + idx;
     poses[g] = make_float4(static_cast<float>(x - qx0), static_cast<float>(y - qy0), cs.x, cs.y);
-    xy[g] = make_double2(x, y);
+    const double q[3] = {x, y, 0.0};
+    task[g] = task_cost(sc, q, s_guide, dyn.n_guide, dyn.goal, false);
     if (states_out) {
       double* srow = states_out + static_cast<size_t>(r0 + r) * (T + 1) * 3;
       srow[3 * h] = x;
@@ -533,18 +549,17 @@ __global__ void __launch_bounds__(1024) k_rollout_lanes(
 // the next step's cell size (k_cloud_prep).
 template <int kCostWarps>
 __global__ void __launch_bounds__(kCostWarps * 32) k_rollout_costs(
-    const StepConst sc, const StepDyn* __restrict__ dynp, const double* __restrict__ guide,
-    const double* __restrict__ base_cost, const double* __restrict__ ctrl_cost,
-    const double2* __restrict__ xy, const float* __restrict__ dmin, double* __restrict__ cost,
-    uint8_t* __restrict__ unsafe, float* __restrict__ dstat, float* __restrict__ hstat) {
+    const StepConst sc, const double* __restrict__ task, const double* __restrict__ base_cost,
+    const double* __restrict__ ctrl_cost, const float* __restrict__ dmin,
+    double* __restrict__ cost, uint8_t* __restrict__ unsafe, float* __restrict__ dstat,
+    float* __restrict__ hstat) {
   pdl_wait();
-  extern __shared__ double g[];  // guide (2*ng), per warp: task[T], obst[T], ctrl[T]; then 2T floats
+  extern __shared__ double g[];  // per warp: task[T], obst[T], ctrl[T]; then 2T floats
   __shared__ float red[2][kCostWarps];
-  const int ng = dynp->n_guide, T = sc.T;
+  const int ng = 0, T = sc.T;
   float* sh = reinterpret_cast<float*>(g + 2 * ng + kCostWarps * 3 * T);
   // every kHstatEvery-th block samples the per-step d_min statistic (k_finalize -> caps)
   const bool sampled = hstat != nullptr && blockIdx.x % kHstatEvery == 0;
-  for (int i = threadIdx.x; i < 2 * ng; i += blockDim.x) g[i] = guide[i];
   if (sampled)
     for (int i = threadIdx.x; i < 2 * T; i += blockDim.x) sh[i] = 0.f;
   __syncthreads();
@@ -561,9 +576,7 @@ __global__ void __launch_bounds__(kCostWarps * 32) k_rollout_costs(
     for (int h = lane; h < T; h += 32) {
       const float df = dmin[row + h];
       const double d = static_cast<double>(df);
-      const double2 p = xy[row + h];
-      const double q[3] = {p.x, p.y, 0.0};
-      s_t[h] = task_cost(sc, q, g, ng, dynp->goal, false);
+      s_t[h] = task[row + h];  // formed by the rollout kernel
       s_o[h] = obstacle_cost(sc, d);
       s_c[h] = ctrl_cost[row + h];  // staged: the serial sum below reads shared memory only
       bad |= d < sc.d_safe;
@@ -917,9 +930,10 @@ cudaError_t launch_noise(const StepConst& sc, const StepDyn* dyn, double* eps, c
 
 template <int TAG, int R>
 cudaError_t rollout_lanes_launch(const StepConst& sc, const StepDyn* dyn, const double* nominal,
-                                 double* eps, int draw, float4* poses, double2* xy,
-                                 double* base_cost, double* ctrl_cost, double* controls_out,
-                                 double* states_out, size_t smem, cudaStream_t s) {
+                                 double* eps, int draw, float4* poses, double* task,
+                                 const double* guide, int guide_cap, double* base_cost,
+                                 double* ctrl_cost, double* controls_out, double* states_out,
+                                 size_t smem, cudaStream_t s) {
   // (per launch: the attribute is per device, and launches are captured into graphs)
   if (smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(k_rollout_lanes<TAG, R>,
@@ -929,7 +943,8 @@ cudaError_t rollout_lanes_launch(const StepConst& sc, const StepDyn* dyn, const 
   }
   if (const cudaError_t le = launch_k(k_rollout_lanes<TAG, R>, (sc.k_local + R - 1) / R,
                                       kLaneThreads, smem, s, sc, dyn, nominal, eps, draw, poses,
-                                      xy, base_cost, ctrl_cost, controls_out, states_out);
+                                      task, guide, guide_cap, base_cost, ctrl_cost, controls_out,
+                                      states_out);
       le != cudaSuccess)
     return le;
   return cudaGetLastError();
@@ -952,54 +967,61 @@ cudaError_t launch_noise_pregen(const StepConst& sc, double* eps, cudaStream_t s
 
 template <int TAG>
 cudaError_t rollout_tag(const StepConst& sc, const StepDyn* dyn, const double* nominal,
-                        double* eps, int draw, float4* poses, double2* xy, double* base_cost,
-                        double* ctrl_cost, double* controls_out, double* states_out,
-                        cudaStream_t s) {
+                        double* eps, int draw, float4* poses, double* task, const double* guide,
+                        int guide_cap, double* base_cost, double* ctrl_cost,
+                        double* controls_out, double* states_out, cudaStream_t s) {
   if (!kRolloutWarpOnly) {
     constexpr int D = model_dim<TAG>();
-    const size_t s16 = rollout_lanes_smem(sc.T, D, 16);
+    const size_t s16 = rollout_lanes_smem(sc.T, D, 16, guide_cap);
     // 8 rollouts per CTA: ~28 resident warps per SM hide the eps loads (cold L2) as well as
     // the warp-per-rollout kernel does, with a quarter of its instructions (16 / 32 measured
     // slower)
-    const size_t s8 = rollout_lanes_smem(sc.T, D, 8);
+    const size_t s8 = rollout_lanes_smem(sc.T, D, 8, guide_cap);
     if (s8 <= 200 * 1024)
-      return rollout_lanes_launch<TAG, 8>(sc, dyn, nominal, eps, draw, poses, xy, base_cost,
-                                          ctrl_cost, controls_out, states_out, s8, s);
+      return rollout_lanes_launch<TAG, 8>(sc, dyn, nominal, eps, draw, poses, task, guide,
+                                          guide_cap, base_cost, ctrl_cost, controls_out,
+                                          states_out, s8, s);
     if (s16 <= 200 * 1024)
-      return rollout_lanes_launch<TAG, 16>(sc, dyn, nominal, eps, draw, poses, xy, base_cost,
-                                           ctrl_cost, controls_out, states_out, s16, s);
+      return rollout_lanes_launch<TAG, 16>(sc, dyn, nominal, eps, draw, poses, task, guide,
+                                           guide_cap, base_cost, ctrl_cost, controls_out,
+                                           states_out, s16, s);
   }
   const int threads = kRolloutWarps * 32;
-  const size_t smem = sizeof(double) * (static_cast<size_t>(sc.T) * sc.D +
+  const size_t smem = sizeof(double) * (2 * static_cast<size_t>(guide_cap) +
+                                        static_cast<size_t>(sc.T) * sc.D +
                                         kRolloutWarps * static_cast<size_t>(rollout_warp_scratch(sc.T, sc.D)));
   if (smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(k_rollout<TAG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(smem));
     if (e != cudaSuccess) return e;
   }
-  { if (const cudaError_t le = launch_k(k_rollout<TAG>, (sc.k_local + kRolloutWarps - 1) / kRolloutWarps, threads, smem, s, 
-      sc, dyn, nominal, eps, draw, poses, xy, base_cost, ctrl_cost, controls_out, states_out); le != cudaSuccess) return le; }
+  if (const cudaError_t le = launch_k(k_rollout<TAG>, (sc.k_local + kRolloutWarps - 1) / kRolloutWarps,
+                                      threads, smem, s, sc, dyn, nominal, eps, draw, poses, task,
+                                      guide, guide_cap, base_cost, ctrl_cost, controls_out,
+                                      states_out);
+      le != cudaSuccess)
+    return le;
   return cudaGetLastError();
 }
 
 cudaError_t launch_rollout(const StepConst& sc, const StepDyn* dyn, const double* nominal,
-                           double* eps, int draw, float4* poses, double2* xy, double* base_cost,
+                           double* eps, int draw, float4* poses, double* task,
+                           const double* guide, int guide_cap, double* base_cost,
                            double* ctrl_cost, double* controls_out, double* states_out,
                            cudaStream_t s) {
   switch (sc.tag) {
-    case EXM_MODEL_DIFF: return rollout_tag<EXM_MODEL_DIFF>(sc, dyn, nominal, eps, draw, poses, xy, base_cost, ctrl_cost, controls_out, states_out, s);
-    case EXM_MODEL_ACKERMANN: return rollout_tag<EXM_MODEL_ACKERMANN>(sc, dyn, nominal, eps, draw, poses, xy, base_cost, ctrl_cost, controls_out, states_out, s);
-    case EXM_MODEL_OMNI: return rollout_tag<EXM_MODEL_OMNI>(sc, dyn, nominal, eps, draw, poses, xy, base_cost, ctrl_cost, controls_out, states_out, s);
-    case EXM_MODEL_SPIN: return rollout_tag<EXM_MODEL_SPIN>(sc, dyn, nominal, eps, draw, poses, xy, base_cost, ctrl_cost, controls_out, states_out, s);
-    case EXM_MODEL_PARALLEL: return rollout_tag<EXM_MODEL_PARALLEL>(sc, dyn, nominal, eps, draw, poses, xy, base_cost, ctrl_cost, controls_out, states_out, s);
+    case EXM_MODEL_DIFF: return rollout_tag<EXM_MODEL_DIFF>(sc, dyn, nominal, eps, draw, poses, task, guide, guide_cap, base_cost, ctrl_cost, controls_out, states_out, s);
+    case EXM_MODEL_ACKERMANN: return rollout_tag<EXM_MODEL_ACKERMANN>(sc, dyn, nominal, eps, draw, poses, task, guide, guide_cap, base_cost, ctrl_cost, controls_out, states_out, s);
+    case EXM_MODEL_OMNI: return rollout_tag<EXM_MODEL_OMNI>(sc, dyn, nominal, eps, draw, poses, task, guide, guide_cap, base_cost, ctrl_cost, controls_out, states_out, s);
+    case EXM_MODEL_SPIN: return rollout_tag<EXM_MODEL_SPIN>(sc, dyn, nominal, eps, draw, poses, task, guide, guide_cap, base_cost, ctrl_cost, controls_out, states_out, s);
+    case EXM_MODEL_PARALLEL: return rollout_tag<EXM_MODEL_PARALLEL>(sc, dyn, nominal, eps, draw, poses, task, guide, guide_cap, base_cost, ctrl_cost, controls_out, states_out, s);
   }
   return cudaErrorInvalidValue;
 }
 
 template <int W>
-cudaError_t rollout_costs_launch(const StepConst& sc, const StepDyn* dyn, const double* guide,
-                                 int guide_cap, const double* base_cost, const double* ctrl_cost,
-                                 const double2* xy, const float* dmin, double* cost,
+cudaError_t rollout_costs_launch(const StepConst& sc, const double* task, const double* base_cost,
+                                 const double* ctrl_cost, const float* dmin, double* cost,
                                  uint8_t* unsafe, float* dstat, float* hstat, size_t smem,
                                  cudaStream_t s) {
   if (smem > 48 * 1024) {
@@ -1007,30 +1029,31 @@ cudaError_t rollout_costs_launch(const StepConst& sc, const StepDyn* dyn, const 
                                          static_cast<int>(smem));
     if (e != cudaSuccess) return e;
   }
-  { if (const cudaError_t le = launch_k(k_rollout_costs<W>, (sc.k_local + W - 1) / W, W * 32, smem, s,
-      sc, dyn, guide, base_cost, ctrl_cost, xy, dmin, cost, unsafe, dstat, hstat); le != cudaSuccess) return le; }
+  if (const cudaError_t le = launch_k(k_rollout_costs<W>, (sc.k_local + W - 1) / W, W * 32, smem, s,
+                                      sc, task, base_cost, ctrl_cost, dmin, cost, unsafe, dstat,
+                                      hstat);
+      le != cudaSuccess)
+    return le;
   return cudaGetLastError();
 }
 
-cudaError_t launch_rollout_costs(const StepConst& sc, const StepDyn* dyn, const double* guide,
-                                 int guide_cap, const double* base_cost, const double* ctrl_cost,
-                                 const double2* xy, const float* dmin, double* cost,
+cudaError_t launch_rollout_costs(const StepConst& sc, const double* task, const double* base_cost,
+                                 const double* ctrl_cost, const float* dmin, double* cost,
                                  uint8_t* unsafe, float* dstat, float* hstat, cudaStream_t s) {
   if (sc.k_local <= 0) return cudaSuccess;
   // 16 rollouts per CTA (8 and 4 measured slower on configs 2 and 3); long horizons (per-warp
   // stage arrays beyond ~200 KB) use fewer
   auto smem_for = [&](int w) {
-    return sizeof(double) * (2 * static_cast<size_t>(guide_cap) + 3 * static_cast<size_t>(w) * sc.T +
-                             sc.T);
+    return sizeof(double) * (3 * static_cast<size_t>(w) * sc.T + sc.T);
   };
   if (smem_for(16) <= 200 * 1024)
-    return rollout_costs_launch<16>(sc, dyn, guide, guide_cap, base_cost, ctrl_cost, xy, dmin, cost,
-                                    unsafe, dstat, hstat, smem_for(16), s);
+    return rollout_costs_launch<16>(sc, task, base_cost, ctrl_cost, dmin, cost, unsafe, dstat, hstat,
+                                    smem_for(16), s);
   if (smem_for(4) <= 200 * 1024)
-    return rollout_costs_launch<4>(sc, dyn, guide, guide_cap, base_cost, ctrl_cost, xy, dmin, cost,
-                                   unsafe, dstat, hstat, smem_for(4), s);
-  return rollout_costs_launch<1>(sc, dyn, guide, guide_cap, base_cost, ctrl_cost, xy, dmin, cost,
-                                 unsafe, dstat, hstat, smem_for(1), s);
+    return rollout_costs_launch<4>(sc, task, base_cost, ctrl_cost, dmin, cost, unsafe, dstat, hstat,
+                                   smem_for(4), s);
+  return rollout_costs_launch<1>(sc, task, base_cost, ctrl_cost, dmin, cost, unsafe, dstat, hstat,
+                                 smem_for(1), s);
 }
 
 cudaError_t launch_block_partials(const StepConst& sc, const double* cost, const uint8_t* unsafe,

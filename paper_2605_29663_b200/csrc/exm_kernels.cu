@@ -883,13 +883,17 @@ __device__ __forceinline__ void sdf_grid_warp(const FpDev& fp, const float4* __r
 // busy SMs). The last warp to finish resets the counter pair for the next launch.
 // work == nullptr: static mapping, warp <-> poses blockIdx.x * 128 + warp * 32 + lane.
 template <int KIND, int NB, bool STATS = false, int MODE = kGridFull>
-#ifndef EXM_GRID_MINB  // A/B builds: minimum resident CTAs per SM (caps registers)
-#define EXM_GRID_MINB 1
-#endif
 #ifndef EXM_GRID_THREADS  // A/B builds: threads per CTA (32-128 measured within 1 %, round 1)
 #define EXM_GRID_THREADS 128
 #endif
-__global__ void __launch_bounds__(EXM_GRID_THREADS, EXM_GRID_MINB) k_sdf_grid(const __grid_constant__ FpDev fp,
+// (-DEXM_GRID_MINB=n A/B builds: at least n resident CTAs per SM, capping registers; the product
+// build leaves the register count to ptxas: 64, i.e. 8 CTAs of 128 threads per SM)
+#ifdef EXM_GRID_MINB
+#define EXM_GRID_BOUNDS __launch_bounds__(EXM_GRID_THREADS, EXM_GRID_MINB)
+#else
+#define EXM_GRID_BOUNDS __launch_bounds__(EXM_GRID_THREADS)
+#endif
+__global__ void EXM_GRID_BOUNDS k_sdf_grid(const __grid_constant__ FpDev fp,
                                                   const float4* __restrict__ poses, int n_poses,
                                                   const GridMeta* __restrict__ gmp,
                                                   const int* __restrict__ cell_start,
