@@ -986,6 +986,8 @@ exm_status fill_head(exm_handle* h, const double q0[3], const double* pts, const
 exm_status upload_inputs(exm_handle* h, const double q0[3], const double* pts, const uint8_t* mask,
                          int32_t n, const double* guide, int32_t ng, const double goal[3],
                          const double* nominal, const double* u_prev, uint64_t cycle) {
+  // a mask without a zero byte selects every point: no mask copy (memchr scans 10 kB in < 1 us)
+  if (mask && n > 0 && !std::memchr(mask, 0, static_cast<size_t>(n))) mask = nullptr;
   exm_status st = fill_head(h, q0, pts, mask, n, guide, ng, goal, nominal, u_prev, cycle);
   if (st != EXM_OK) return st;
   cudaStream_t s = h->stream;
