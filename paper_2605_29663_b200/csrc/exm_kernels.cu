@@ -845,6 +845,33 @@ __device__ __forceinline__ void sdf_grid_warp(const FpDev& fp, const float4* __r
           if (!__any_sync(kFull, cneed)) continue;
         }
         const float2* cp = cloud + (ch << csh);
+#ifdef EXM_PAIR_POINTS
+        // A/B builds: two points per iteration, both valued whenever either passes its circle
+        // test (independent chains for the scheduler; extra values never change the exact min)
+#pragma unroll 1
+        for (int p = 0; p < gm.chunk; p += 2) {
+          const float4 o2 = ldro<SMEM>(reinterpret_cast<const float4*>(cp + p));
+          const float dx0 = o2.x - q.x, dy0 = o2.y - q.y, dx1 = o2.z - q.x, dy1 = o2.w - q.y;
+          if (STATS && cneed) cnt[kCntPoint] += 2;
+          if (STATS && lane == 0) cnt[kCntPointWarp] += 2;
+          const bool a0 = cneed && (MODE == kGridBrute ? o2.x == o2.x : dx0 * dx0 + dy0 * dy0 < l2);
+          const bool a1 = cneed && (MODE == kGridBrute ? o2.z == o2.z : dx1 * dx1 + dy1 * dy1 < l2);
+          if (a0 || a1) {
+            unsigned w0, w1;
+            const float b0 = grid_point<KIND, NB, MODE == kGridBrute>(
+                fp, fmaf(q.z, dx0, q.w * dy0), fmaf(q.z, dy0, -(q.w * dx0)), best, mg, w0);
+            const float b1 = grid_point<KIND, NB, MODE == kGridBrute>(
+                fp, fmaf(q.z, dx1, q.w * dy1), fmaf(q.z, dy1, -(q.w * dx1)), best, mg, w1);
+            // a NaN pad valued in brute mode never wins (fminf ignores NaN)
+            best = fminf(best, fminf(MODE == kGridBrute && !a0 ? best : b0,
+                                     MODE == kGridBrute && !a1 ? best : b1));
+            if ((w0 | w1) & (kWorkTileVal | kWorkEdges)) {
+              const float nl = R + best;
+              l2 = nl * nl;
+            }
+          }
+        }
+#else
 #pragma unroll 1
         for (int p = 0; p < gm.chunk; ++p) {
           const float2 o = ldro<SMEM>(cp + p);
@@ -869,6 +896,7 @@ __device__ __forceinline__ void sdf_grid_warp(const FpDev& fp, const float4* __r
             }
           }
         }
+#endif
       }
     }  // cells of this group
     }  // groups of 32 ring cells
@@ -882,7 +910,6 @@ __device__ __forceinline__ void sdf_grid_warp(const FpDev& fp, const float4* __r
 // magnitude between open space and clutter, so a static mapping ends in a long tail of a few
 // busy SMs). The last warp to finish resets the counter pair for the next launch.
 // work == nullptr: static mapping, warp <-> poses blockIdx.x * 128 + warp * 32 + lane.
-template <int KIND, int NB, bool STATS = false, int MODE = kGridFull>
 #ifndef EXM_GRID_THREADS  // A/B builds: threads per CTA (32-128 measured within 1 %, round 1)
 #define EXM_GRID_THREADS 128
 #endif
@@ -893,6 +920,7 @@ template <int KIND, int NB, bool STATS = false, int MODE = kGridFull>
 #else
 #define EXM_GRID_BOUNDS __launch_bounds__(EXM_GRID_THREADS)
 #endif
+template <int KIND, int NB, bool STATS = false, int MODE = kGridFull>
 __global__ void EXM_GRID_BOUNDS k_sdf_grid(const __grid_constant__ FpDev fp,
                                                   const float4* __restrict__ poses, int n_poses,
                                                   const GridMeta* __restrict__ gmp,
