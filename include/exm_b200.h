@@ -216,6 +216,8 @@ exm_status exm_hybrid_create(const exm_footprint* footprint, const exm_model* mo
                              const exm_params* params, int32_t n_cap, int32_t guide_cap,
                              int32_t device, exm_hybrid** out);
 void exm_hybrid_destroy(exm_hybrid* hy);
+/* exm_set_option on every family handle (the hybrid step graph is re-captured). */
+exm_status exm_hybrid_set_option(exm_hybrid* hy, int32_t option, int32_t value);
 exm_status exm_hybrid_cycle(exm_hybrid* hy, const double q0[3], const double* pts_xy,
                             const uint8_t* mask, int32_t n_points, const double* guide_xy,
                             int32_t n_guide, const double goal[3], double* nominals_inout,
@@ -281,9 +283,15 @@ enum {
   EXM_OPT_HOST_TIMING = 4, /* 1: accumulate exm_control_cycle host phases (exm_host_timing) */
   EXM_OPT_HOST_THREADS = 5, /* host threads converting batch_signed_distance queries (default:
                                min(8, hardware threads)); the reference's `threads` argument */
-  EXM_OPT_SDF_MAP = 6       /* lanes <-> poses of the thread-per-pose SDF: 0 tuned on the
+  EXM_OPT_SDF_MAP = 6,      /* lanes <-> poses of the thread-per-pose SDF: 0 tuned on the
                                handle's first steps (default), 1 a rollout's consecutive steps per
                                warp, 2 consecutive rollouts at one step per warp */
+  EXM_OPT_SDF_THRESHOLD = 7 /* 1 (default): the rollout minima of exm_control_cycle /
+                               exm_hybrid_cycle / exm_sharded_cycle are resolved exactly only below
+                               d_safe (the obstacle cost is identically 0 and the rollout is not
+                               unsafe at or above it, controller.cpp:98-101, :162, and no rollout
+                               minimum is returned), so decisions are unchanged; 0: every rollout
+                               minimum exact. exm_evaluate_rollouts is always exact. */
 };
 /* Signed-distance kernel selection: automatic, or (tests) every bound disabled, no chunk
  * bound, a forced thread / warp / 8-warp-CTA per pose kernel, persistent warps, caps ignored. */

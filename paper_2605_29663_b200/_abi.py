@@ -88,6 +88,7 @@ class ExmSdfPath(C.Structure):
 
 # exm_set_option options and EXM_SDF_* modes (include/exm_b200.h)
 OPT_SDF_MODE, OPT_AUTO_CAPS, OPT_PREGEN, OPT_HOST_TIMING, OPT_HOST_THREADS, OPT_SDF_MAP = 1, 2, 3, 4, 5, 6
+OPT_SDF_THRESHOLD = 7
 SDF_MODES = {"auto": 0, "brute": 1, "nochunk": 2, "thread": 3, "warp": 4, "cta": 5,
              "persist": 6, "nocap": 7}
 SDF_NCOUNT = 10
@@ -132,6 +133,7 @@ SIGNATURES = {
                                       C.POINTER(ExmLimits), C.c_int32, C.POINTER(ExmParams),
                                       C.c_int32, C.c_int32, C.c_int32, C.POINTER(_HYp)]),
     "exm_hybrid_destroy": (None, [_HYp]),
+    "exm_hybrid_set_option": (C.c_int32, [_HYp, C.c_int32, C.c_int32]),
     "exm_hybrid_cycle": (C.c_int32, [_HYp, _dp, _dp, _u8p, C.c_int32, _dp, C.c_int32, _dp, _dp,
                                      _dp, C.c_uint64, C.POINTER(ExmDecision)]),
     "exm_nccl_unique_id": (C.c_int32, [C.POINTER(C.c_uint8)]),

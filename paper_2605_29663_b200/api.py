@@ -750,6 +750,12 @@ class Engine:
         at one step per warp)."""
         self.set_option(_abi.OPT_SDF_MAP, {"tuned": 0, "rmajor": 1, "hmajor": 2}[mapping])
 
+    def set_sdf_threshold(self, on: bool):
+        """True (default): the control cycle resolves rollout minima exactly only below d_safe
+        (the decision is unchanged: the obstacle cost is 0 and the rollout safe at or above it);
+        False: every rollout minimum exact. evaluate_rollouts is always exact."""
+        self.set_option(_abi.OPT_SDF_THRESHOLD, 1 if on else 0)
+
     def last_sdf_path(self):
         """What the last rollout / validation SDF launches ran (kernel 0 thread, 1 warp, 2 CTA
         per pose; chunk; persistent; hmajor)."""
@@ -973,6 +979,10 @@ class HybridController:
             self.close()
         except Exception:
             pass
+
+    def set_option(self, option: int, value: int):
+        """exm_set_option on every family (e.g. _abi.OPT_SDF_THRESHOLD)."""
+        check(self.lib.exm_hybrid_set_option(self.h, int(option), int(value)))
 
     def family_cycles(self, q0, obstacles: ObstacleSet, guidance: Guidance):
         """One device call: every family's MppiController::control_cycle."""

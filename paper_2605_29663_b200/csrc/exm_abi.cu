@@ -546,6 +546,10 @@ struct exm_handle {
   // options (exm_set_option)
   int sdf_mode = kSdfAuto;
   bool auto_caps = false, pregen = true, host_timing = false;
+  // EXM_OPT_SDF_THRESHOLD: the control cycle's rollout minima are resolved only below d_safe
+  // (sdf_thr = the least float whose double value is >= d_safe; results min(exact, sdf_thr))
+  bool sdf_threshold = true;
+  float sdf_thr = HUGE_VALF;
   // what the last rollout / validation signed-distance launch ran (exm_last_sdf_path)
   SdfPath roll_path{}, val_path{};
   // lane <-> pose mapping of the thread-per-pose SDF (EXM_OPT_SDF_MAP): 0 tuned per handle (the
@@ -759,11 +763,26 @@ exm_status record_ev(cudaEvent_t e, cudaStream_t s, bool capturing) {
   return EXM_OK;
 }
 
+// Threshold of the rollout SDF (EXM_OPT_SDF_THRESHOLD): a minimum at or above d_safe costs
+// exactly 0 in obstacle_cost (w_coll [d < 0] + w_rep max(d_safe - d, 0)^2, controller.cpp:98-101)
+// and leaves the rollout safe (d < d_safe, :162); the control cycle returns no rollout minimum.
+// So the search of a pose stops once no point can come nearer than d_safe, and the pose reports
+// the least float t with double(t) >= d_safe: every cost and flag is what the exact minimum gives.
+float rollout_threshold(const exm_handle* h, bool exact) {
+  return (exact || !h->sdf_threshold) ? HUGE_VALF : h->sdf_thr;
+}
+float least_float_at_or_above(double d) {
+  float f = static_cast<float>(d);
+  if (static_cast<double>(f) < d) f = std::nextafter(f, HUGE_VALF);
+  return f;
+}
+
 // The rollout SDF of a step (capped by the previous step's per-step statistic when set).
-exm_status enqueue_rollout_sdf(exm_handle* h, cudaStream_t s) {
+exm_status enqueue_rollout_sdf(exm_handle* h, cudaStream_t s, bool exact = false) {
   const StepConst& sc = h->sc;
   EXM_CUDA(launch_sdf_grid(h->fp, h->d_poses, sc.k_local * sc.T, sc.T, h->hmajor, h->grid, h->d_cap,
-                           h->sdf_mode, h->d_dmin, &h->roll_path, nullptr, s));
+                           h->sdf_mode, h->d_dmin, &h->roll_path, nullptr, s,
+                           rollout_threshold(h, exact)));
   h->roll_path.chunk = chunk_for_capacity(h->n_cap);
   h->val_path.chunk = h->roll_path.chunk;
   return EXM_OK;
@@ -1129,6 +1148,7 @@ exm_status exm_create(const exm_footprint* footprint, const exm_model* model,
   sc.dt = params->dt;
   sc.lambda = params->lambda;
   sc.d_safe = params->d_safe;
+  h->sdf_thr = least_float_at_or_above(params->d_safe);
   sc.w_coll = params->w_coll;
   sc.w_rep = params->w_rep;
   sc.w_inf = params->w_inf;
@@ -1334,7 +1354,7 @@ exm_status exm_evaluate_rollouts(exm_handle* h, const double q0[3], const double
                           h->d_guide, h->guide_cap, h->d_base, h->d_ctrl,
                           controls_out ? h->d_controls : nullptr,
                           states_out ? h->d_states : nullptr, s));
-  if (const exm_status st2 = enqueue_rollout_sdf(h, s); st2 != EXM_OK) return st2;
+  if (const exm_status st2 = enqueue_rollout_sdf(h, s, true); st2 != EXM_OK) return st2;
   EXM_CUDA(launch_rollout_costs(sc, h->d_task, h->d_base, h->d_ctrl, h->d_dmin, h->d_cost,
                                 h->d_unsafe, h->grid.dstat, nullptr, s));
   if (controls_out)
@@ -2118,7 +2138,7 @@ exm_status exm_sdf_work_stats(exm_handle* h, int64_t* counts) {
   cudaError_t e = cudaMemsetAsync(d, 0, kCntN * sizeof(unsigned long long), s);
   if (e == cudaSuccess)
     e = launch_sdf_grid(h->fp, h->d_poses, h->sc.k_local * h->T, h->T, h->hmajor, h->grid, h->d_cap,
-                        h->sdf_mode, h->d_dmin, nullptr, d, s);
+                        h->sdf_mode, h->d_dmin, nullptr, d, s, rollout_threshold(h, false));
   if (e == cudaSuccess) e = cudaMemcpyAsync(hv, d, sizeof hv, cudaMemcpyDeviceToHost, s);
   if (e == cudaSuccess) e = cudaStreamSynchronize(s);
   cudaFree(d);
@@ -2147,6 +2167,7 @@ exm_status exm_set_option(exm_handle* h, int32_t option, int32_t value) {
       h->sdf_mode = value;
       break;
     case EXM_OPT_AUTO_CAPS: h->auto_caps = value != 0; break;
+    case EXM_OPT_SDF_THRESHOLD: h->sdf_threshold = value != 0; break;
     case EXM_OPT_SDF_MAP:
       if (value < 0 || value > 2) return fail(EXM_ERR_INVALID_ARGUMENT, "unknown SDF mapping");
       h->sdf_map = value;
@@ -2258,8 +2279,10 @@ exm_status hybrid_enqueue(exm_hybrid* hy, cudaStream_t s0) {
   }
   for (int m = 1; m < hy->M; ++m) EXM_CUDA(cudaStreamWaitEvent(s0, hy->pre_done[m], 0));
   EXM_CUDA(cudaStreamWaitEvent(s0, hy->prep_done, 0));
+  float thr = 0.f;  // the loosest family threshold keeps every family's minima below its own exact
+  for (int m = 0; m < hy->M; ++m) thr = std::max(thr, rollout_threshold(hy->fam[m], false));
   EXM_CUDA(launch_sdf_grid(f0->fp, hy->poses_all, hy->M * hy->K * hy->T, hy->T, f0->hmajor, f0->grid,
-                           nullptr, f0->sdf_mode, hy->dmin_all, &f0->roll_path, nullptr, s0));
+                           nullptr, f0->sdf_mode, hy->dmin_all, &f0->roll_path, nullptr, s0, thr));
   EXM_CUDA(cudaEventRecord(hy->sdf_done, s0));
   for (int m = 0; m < hy->M; ++m) {
     cudaStream_t sm = m == 0 ? s0 : hy->fam[m]->stream;
@@ -2290,6 +2313,19 @@ void exm_hybrid_destroy(exm_hybrid* hy) {
   if (hy->poses_all) cudaFree(hy->poses_all);
   if (hy->dmin_all) cudaFree(hy->dmin_all);
   delete hy;
+}
+
+exm_status exm_hybrid_set_option(exm_hybrid* hy, int32_t option, int32_t value) {
+  if (!hy) return fail(EXM_ERR_INVALID_ARGUMENT, "hybrid handle is null");
+  std::lock_guard<std::mutex> lk(hy->mu);
+  for (exm_handle* h : hy->fam)
+    if (const exm_status st = exm_set_option(h, option, value); st != EXM_OK) return st;
+  cudaSetDevice(hy->device);
+  if (hy->exec) cudaGraphExecDestroy(hy->exec);  // the hybrid step graph is re-captured
+  if (hy->graph) cudaGraphDestroy(hy->graph);
+  hy->exec = nullptr;
+  hy->graph = nullptr;
+  return EXM_OK;
 }
 
 exm_status exm_hybrid_create(const exm_footprint* footprint, const exm_model* models,

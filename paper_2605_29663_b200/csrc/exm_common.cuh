@@ -2,6 +2,7 @@
 // (exm_kernels.cu) of libexm_b200.so. Nothing here crosses the public C ABI.
 #pragma once
 
+#include <cmath>
 #include <cstdint>
 #include <cstdlib>
 #include <utility>
@@ -230,7 +231,8 @@ cudaError_t launch_rollout(const StepConst& sc, const StepDyn* dyn, const double
                            cudaStream_t s);
 cudaError_t launch_sdf_grid(const FpDev& fp, const float4* poses, int n_poses, int T, bool hmajor,
                             const CloudGrid& g, const float* cap, int mode, float* out,
-                            SdfPath* path, unsigned long long* stats, cudaStream_t s);
+                            SdfPath* path, unsigned long long* stats, cudaStream_t s,
+                            float thr = HUGE_VALF);  // results: min(exact minimum, thr)
 cudaError_t launch_rollout_costs(const StepConst& sc, const double* task, const double* base_cost,
                                  const double* ctrl_cost, const float* dmin, double* cost,
                                  uint8_t* unsafe, float* dstat, float* hstat, cudaStream_t s);

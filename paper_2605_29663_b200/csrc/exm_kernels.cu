@@ -359,12 +359,24 @@ __device__ __forceinline__ float unkey(unsigned k) {
 }
 
 // ------------------------------------------------------------------ kernels
-constexpr float kPtsPerCell = 16.0f;  // swept 8-64 (tools/cfg5_snapshots.py): cfg2/cfg3 flat over 16-32, cfg5 snapshots -3 % at 16
+#ifndef EXM_PTS_PER_CELL  // A/B builds override the cell-size constants below
+#define EXM_PTS_PER_CELL 16.0f
+#endif
+#ifndef EXM_CELL_MIN_R
+#define EXM_CELL_MIN_R 0.18f
+#endif
+#ifndef EXM_CELL_MAX_R
+#define EXM_CELL_MAX_R 0.5f
+#endif
+#ifndef EXM_CELL_SEARCH_FRAC
+#define EXM_CELL_SEARCH_FRAC 0.385f
+#endif
+constexpr float kPtsPerCell = EXM_PTS_PER_CELL;  // swept 8-64 (tools/cfg5_snapshots.py): cfg2/cfg3 flat over 16-32, cfg5 snapshots -3 % at 16
 constexpr int kPrepCache = 12;  // cloud points per k_cloud_prep thread kept in registers
-constexpr float kCellMinR = 0.18f;       // cell edge >= kCellMinR * R (swept 0.12-0.25: cfg3 1.99 -> 1.88 ms,
+constexpr float kCellMinR = EXM_CELL_MIN_R;       // cell edge >= kCellMinR * R (swept 0.12-0.25: cfg3 1.99 -> 1.88 ms,
                                           // cfg5 snapshots -1 %, cfg1/cfg2 flat; cfg3 is alignment-sensitive)
-constexpr float kCellMaxR = 0.5f;        // cell edge <= kCellMaxR * R ...
-constexpr float kCellSearchFrac = 0.385f;  // ... or <= this fraction of R + mean d_min
+constexpr float kCellMaxR = EXM_CELL_MAX_R;       // cell edge <= kCellMaxR * R ...
+constexpr float kCellSearchFrac = EXM_CELL_SEARCH_FRAC;  // ... or <= this fraction of R + mean d_min
 // Below this many poses one thread per pose leaves most SMs idle (< ~16 warps each): use one
 // warp per pose instead.
 // (measured on config 2's cloud: 25.6k poses warp 45 us / thread 64 us, 51.2k poses warp 76 us
@@ -740,8 +752,8 @@ __device__ __forceinline__ void sdf_grid_warp(const FpDev& fp, const float4* __r
                                               const int* __restrict__ cell_start,
                                               const float2* __restrict__ cloud,
                                               const float4* __restrict__ chunk,
-                                              const float* __restrict__ cap, int T, int rows,
-                                              float* __restrict__ out, int i, int lane,
+                                              const float* __restrict__ cap, float thr, int T,
+                                              int rows, float* __restrict__ out, int i, int lane,
                                               unsigned long long* cnt) {
   const bool active = i < n_poses;
   // h-major lanes: the poses are stored [row][h] (row = rollout); with rows > 0 logical index
@@ -779,14 +791,16 @@ __device__ __forceinline__ void sdf_grid_warp(const FpDev& fp, const float4* __r
   // pose whose true minimum m* lies below the cap still gets m* exactly (no point with sd = m*
   // is ever pruned: its bound is <= m* < best); poses left at the cap rerun uncapped (pass 1).
   const float kInf = __int_as_float(0x7f800000);
-  const float capv = (cap != nullptr && active && MODE != kGridBrute) ? cap[hh] : kInf;
+  // thr: results are min(exact minimum, thr) (+inf: exact everywhere); minima below thr are
+  // exact, so thr acts as a cap that is never re-run
+  const float capv = fminf((cap != nullptr && active && MODE != kGridBrute) ? cap[hh] : kInf, thr);
   float best = capv;
   bool todo = active;
   for (int pass = 0; pass < 2; ++pass) {
   if (pass == 1) {
-    todo = active && !(best < capv);
+    todo = active && !(best < capv) && capv < thr;
     if (!__any_sync(kFull, todo)) break;
-    if (todo) best = kInf;
+    if (todo) best = thr;
   }
   for (int k = 0; k <= kmax; ++k) {
     if (k > 0) {
@@ -966,8 +980,8 @@ __global__ void EXM_GRID_BOUNDS k_sdf_grid(const __grid_constant__ FpDev fp,
                                                   const int* __restrict__ cell_start,
                                                   const float2* __restrict__ cloud,
                                                   const float4* __restrict__ chunk,
-                                                  const float* __restrict__ cap, int T, int rows,
-                                                  float* __restrict__ out,
+                                                  const float* __restrict__ cap, float thr, int T,
+                                                  int rows, float* __restrict__ out,
                                                   unsigned* __restrict__ work,
                                                   unsigned long long* __restrict__ stats = nullptr) {
   pdl_wait();
@@ -977,8 +991,8 @@ __global__ void EXM_GRID_BOUNDS k_sdf_grid(const __grid_constant__ FpDev fp,
   const int lane = threadIdx.x & 31;
   const GridMeta gm = *gmp;
   if (work == nullptr) {
-    sdf_grid_warp<KIND, NB, STATS, MODE>(fp, poses, n_poses, gm, cell_start, cloud, chunk, cap, T,
-                                         rows, out, blockIdx.x * blockDim.x + threadIdx.x, lane,
+    sdf_grid_warp<KIND, NB, STATS, MODE>(fp, poses, n_poses, gm, cell_start, cloud, chunk, cap, thr,
+                                         T, rows, out, blockIdx.x * blockDim.x + threadIdx.x, lane,
                                          cnt);
   } else {
     for (;;) {
@@ -987,7 +1001,7 @@ __global__ void EXM_GRID_BOUNDS k_sdf_grid(const __grid_constant__ FpDev fp,
       base = __shfl_sync(kFull, base, 0);
       if (base >= static_cast<unsigned>(n_poses)) break;
       sdf_grid_warp<KIND, NB, STATS, MODE>(fp, poses, n_poses, gm, cell_start, cloud, chunk, cap,
-                                           T, rows, out, static_cast<int>(base) + lane, lane, cnt);
+                                           thr, T, rows, out, static_cast<int>(base) + lane, lane, cnt);
     }
     if (lane == 0) {
       __threadfence();
@@ -1019,7 +1033,7 @@ __global__ void __launch_bounds__(1024, 1) k_sdf_grid_smem(
     const __grid_constant__ FpDev fp, const float4* __restrict__ poses, int n_poses,
     const GridMeta* __restrict__ gmp, const int* __restrict__ cell_start,
     const float2* __restrict__ cloud, const float4* __restrict__ chunk,
-    const float* __restrict__ cap, int T, int rows, float* __restrict__ out,
+    const float* __restrict__ cap, float thr, int T, int rows, float* __restrict__ out,
     unsigned* __restrict__ work, int smem_bytes) {
   pdl_wait();
   extern __shared__ __align__(128) unsigned char s_cloud_mem[];
@@ -1061,7 +1075,7 @@ __global__ void __launch_bounds__(1024, 1) k_sdf_grid_smem(
     base = __shfl_sync(kFull, base, 0);
     if (base >= static_cast<unsigned>(n_poses)) break;
     if (fit)
-      sdf_grid_warp<KIND, NB, false, kGridFull, true>(fp, poses, n_poses, gm, cs, cl, ck, cap, T,
+      sdf_grid_warp<KIND, NB, false, kGridFull, true>(fp, poses, n_poses, gm, cs, cl, ck, cap, thr, T,
                                                       rows, out, static_cast<int>(base) + lane,
                                                       lane, cnt);
     else
@@ -1090,7 +1104,7 @@ template <int KIND, int NB, int W = 1>
 __global__ void __launch_bounds__(W == 1 ? 128 : 32 * W) k_sdf_grid_warp(
     const __grid_constant__ FpDev fp, const float4* __restrict__ poses, int n_poses,
     const GridMeta* __restrict__ gmp, const int* __restrict__ cell_start,
-    const float2* __restrict__ cloud, float* __restrict__ out) {
+    const float2* __restrict__ cloud, float thr, float* __restrict__ out) {
   pdl_wait();
   __shared__ float s_best[W];
   const int lane = threadIdx.x & 31;
@@ -1108,7 +1122,7 @@ __global__ void __launch_bounds__(W == 1 ? 128 : 32 * W) k_sdf_grid_warp(
   const int cj = min(gm.gy - 1, max(0, static_cast<int>(floorf((q.y - gm.y0) * gm.inv_cs))));
   const float mg = gm.margin;
   const float R = fp.radius + mg;
-  float best = __int_as_float(0x7f800000);
+  float best = thr;  // min(exact minimum, thr)
   const int kmax = max(max(ci, gm.gx - 1 - ci), max(cj, gm.gy - 1 - cj));
   for (int k = 0; k <= kmax; ++k) {
     if (k > 0) {
@@ -1548,8 +1562,8 @@ constexpr int kGridThreads = EXM_GRID_THREADS;
 
 template <int KIND, int NB, bool STATS, int MODE>
 cudaError_t launch_grid_kernel(const FpDev& fp, const float4* poses, int n_poses, int T,
-                               bool hmajor, const CloudGrid& g, const float* cap, bool persist,
-                               float* out,
+                               bool hmajor, const CloudGrid& g, const float* cap, float thr,
+                               bool persist, float* out,
                                SdfPath* path, unsigned long long* stats, cudaStream_t s) {
   const int threads = kGridThreads;
   const int blocks = (n_poses + threads - 1) / threads;
@@ -1571,7 +1585,7 @@ cudaError_t launch_grid_kernel(const FpDev& fp, const float4* poses, int n_poses
     if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
     if (path) *path = SdfPath{0, 0, 1, n_sm, 1024, rows_used > 0 ? 1 : 0};
     if (const cudaError_t le = launch_k(ks, n_sm, 1024, kSmem, s, fp, poses, n_poses, g.gm,
-                                        g.cell_start, g.cloud, g.chunk, cap, T, rows_used, out,
+                                        g.cell_start, g.cloud, g.chunk, cap, thr, T, rows_used, out,
                                         g.work, kSmem);
         le != cudaSuccess)
       return le;
@@ -1580,8 +1594,8 @@ cudaError_t launch_grid_kernel(const FpDev& fp, const float4* poses, int n_poses
 #endif
   if (path) *path = SdfPath{0, 0, work ? 1 : 0, grid, threads, rows_used > 0 ? 1 : 0};
   if (const cudaError_t le = launch_k(k, grid, threads, 0, s, fp, poses, n_poses, g.gm,
-                                      g.cell_start, g.cloud, g.chunk, cap, T, rows_used, out, work,
-                                      stats);
+                                      g.cell_start, g.cloud, g.chunk, cap, thr, T, rows_used, out,
+                                      work, stats);
       le != cudaSuccess)
     return le;
   return cudaGetLastError();
@@ -1590,40 +1604,40 @@ cudaError_t launch_grid_kernel(const FpDev& fp, const float4* poses, int n_poses
 template <int KIND, int NB>
 struct GridLaunch {
   static cudaError_t run(const FpDev& fp, const float4* poses, int n_poses, int T, bool hmajor,
-                         const CloudGrid& g, const float* cap, int mode, float* out,
+                         const CloudGrid& g, const float* cap, float thr, int mode, float* out,
                          SdfPath* path, unsigned long long* stats, cudaStream_t s) {
     if (n_poses <= 0) return cudaSuccess;
     const bool persist = mode == kSdfPersist;
     if (mode == kSdfNoCap) cap = nullptr;
     if (stats) {
       if (mode == kSdfNoChunk)
-        return launch_grid_kernel<KIND, NB, true, kGridNoChunk>(fp, poses, n_poses, T, hmajor, g, cap, persist, out, path, stats, s);
-      return launch_grid_kernel<KIND, NB, true, kGridFull>(fp, poses, n_poses, T, hmajor, g, cap, persist, out, path, stats, s);
+        return launch_grid_kernel<KIND, NB, true, kGridNoChunk>(fp, poses, n_poses, T, hmajor, g, cap, thr, persist, out, path, stats, s);
+      return launch_grid_kernel<KIND, NB, true, kGridFull>(fp, poses, n_poses, T, hmajor, g, cap, thr, persist, out, path, stats, s);
     }
     if (mode == kSdfBrute)
-      return launch_grid_kernel<KIND, NB, false, kGridBrute>(fp, poses, n_poses, T, hmajor, g, cap, persist, out, path, nullptr, s);
+      return launch_grid_kernel<KIND, NB, false, kGridBrute>(fp, poses, n_poses, T, hmajor, g, cap, thr, persist, out, path, nullptr, s);
     if (mode == kSdfNoChunk)
-      return launch_grid_kernel<KIND, NB, false, kGridNoChunk>(fp, poses, n_poses, T, hmajor, g, cap, persist, out, path, nullptr, s);
-    return launch_grid_kernel<KIND, NB, false, kGridFull>(fp, poses, n_poses, T, hmajor, g, cap, persist, out, path, nullptr, s);
+      return launch_grid_kernel<KIND, NB, false, kGridNoChunk>(fp, poses, n_poses, T, hmajor, g, cap, thr, persist, out, path, nullptr, s);
+    return launch_grid_kernel<KIND, NB, false, kGridFull>(fp, poses, n_poses, T, hmajor, g, cap, thr, persist, out, path, nullptr, s);
   }
 };
 
 template <int KIND, int NB>
 struct GridWarpLaunch {
   static cudaError_t run(const FpDev& fp, const float4* poses, int n_poses, const CloudGrid& g,
-                         bool cta, float* out, SdfPath* path, cudaStream_t s) {
+                         bool cta, float thr, float* out, SdfPath* path, cudaStream_t s) {
     if (n_poses <= 0) return cudaSuccess;
     if (n_poses <= kCtaPerPoseMax || cta) {  // few poses: 8 warps each
       if (path) *path = SdfPath{2, 0, 0, n_poses, 256, 0};
       if (const cudaError_t le = launch_k(k_sdf_grid_warp<KIND, NB, 8>, n_poses, 256, 0, s, fp,
-                                          poses, n_poses, g.gm, g.cell_start, g.cloud, out);
+                                          poses, n_poses, g.gm, g.cell_start, g.cloud, thr, out);
           le != cudaSuccess)
         return le;
     } else {
       const int threads = 128, warps = threads / 32, grid = (n_poses + warps - 1) / warps;
       if (path) *path = SdfPath{1, 0, 0, grid, threads, 0};
       if (const cudaError_t le = launch_k(k_sdf_grid_warp<KIND, NB>, grid, threads, 0, s, fp,
-                                          poses, n_poses, g.gm, g.cell_start, g.cloud, out);
+                                          poses, n_poses, g.gm, g.cell_start, g.cloud, thr, out);
           le != cudaSuccess)
         return le;
     }
@@ -1697,14 +1711,14 @@ cudaError_t launch_cloud_prep(const double* pts, const uint8_t* mask, const Step
 
 cudaError_t launch_sdf_grid(const FpDev& fp, const float4* poses, int n_poses, int T, bool hmajor,
                             const CloudGrid& g, const float* cap, int mode, float* out,
-                            SdfPath* path, unsigned long long* stats, cudaStream_t s) {
+                            SdfPath* path, unsigned long long* stats, cudaStream_t s, float thr) {
   // Few poses (validation rollout, single queries): one warp (or one 8-warp CTA) per pose keeps
   // all lanes busy; many poses: one thread per pose. Statistics builds exist for the latter.
   const bool warp = !stats && (mode == kSdfWarp || mode == kSdfCta ||
                                (n_poses <= kWarpPerPoseMax && mode != kSdfThread &&
                                 mode != kSdfBrute && mode != kSdfPersist));
-  if (warp) return dispatch_fp<GridWarpLaunch>(fp, poses, n_poses, g, mode == kSdfCta, out, path, s);
-  return dispatch_fp<GridLaunch>(fp, poses, n_poses, T, hmajor, g, cap, mode, out, path, stats, s);
+  if (warp) return dispatch_fp<GridWarpLaunch>(fp, poses, n_poses, g, mode == kSdfCta, thr, out, path, s);
+  return dispatch_fp<GridLaunch>(fp, poses, n_poses, T, hmajor, g, cap, thr, mode, out, path, stats, s);
 }
 
 cudaError_t launch_pose_prep(const double* poses, int n, double* center, float4* out,

@@ -10,7 +10,7 @@ for r in 1 2; do for lib in "$@"; do
 import sys, json
 for l in sys.stdin:
     if l.startswith('{'):
-        d = json.loads(l); print('$lib', d['cfg'], d['sdf_ms'])
+        d = json.loads(l); print('$lib', d['cfg'], 'sdf', d['sdf_ms'], 'step', d.get('step_ms'))
     else: print(l.strip())
 " | tee -a $out/ab.txt
 done; done

@@ -3,6 +3,7 @@
 import json
 import os
 import sys
+import time
 
 import numpy as np
 
@@ -24,12 +25,15 @@ for cfg in sys.argv[1:]:
     eng.step_stats()
     eng.run_resident(20)
     st = eng.step_stats()
+    t0 = time.perf_counter()
+    eng.run_resident(50)  # whole resident steps (graph launches back to back), wall clock
+    step_ms = (time.perf_counter() - t0) / 50 * 1e3
     c = eng.sdf_work_stats()
     ops, _ = bench.executed_ops(c, wl.footprint)
     poses = wl.params.rollouts * wl.params.horizon
     per_pose = {k: round(v / poses, 2) for k, v in c.items()}
     eff = c["point_tests"] / (32.0 * c["point_iters_warp"]) if c["point_iters_warp"] else None
     print(json.dumps({"cfg": cfg, "lib": os.environ.get("EXM_LIB_PATH", "base"),
-                      "sdf_ms": round(st["sdf_ms"], 4), "tflops_exec": round(ops / st["sdf_ms"] / 1e9, 2),
+                      "sdf_ms": round(st["sdf_ms"], 4), "step_ms": round(step_ms, 4), "tflops_exec": round(ops / st["sdf_ms"] / 1e9, 2),
                       "lane_eff_points": eff and round(eff, 3), "path": eng.last_sdf_path()[0],
                       "per_pose": per_pose}), flush=True)
