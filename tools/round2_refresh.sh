@@ -28,4 +28,7 @@ python tools/ncu_targets.py pairs 2 > /dev/null 2>&1 && \
       -k regex:"k_sdf_pairs" -s 1 -c 1 -f -o "$out/ncu_sdf_pairs_cfg4" \
       python tools/ncu_targets.py pairs 2 > /dev/null 2>&1 && \
   python tools/ncu_summary.py "$out/ncu_sdf_pairs_cfg4.ncu-rep" > "$out/${tag}_ncu_sdf_pairs_cfg4.json"
+[ -f "$out/ncu_sdf_grid_cfg2.ncu-rep" ] && \
+  ncu -i "$out/ncu_sdf_grid_cfg2.ncu-rep" --page source --csv --print-source cuda,sass > "$out/sdf_grid_src.csv" 2>/dev/null && \
+  python tools/ncu_lines.py "$out/sdf_grid_src.csv" 40 > "$out/${tag}_ncu_lines_sdf_grid_cfg2.txt" && rm -f "$out/sdf_grid_src.csv"
 rm -f "$out"/*.ncu-rep

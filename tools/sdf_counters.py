@@ -25,8 +25,10 @@ for cfg in sys.argv[1:]:
     eng.step_stats()
     eng.run_resident(20)
     st = eng.step_stats()
+    torch.cuda.synchronize()
     t0 = time.perf_counter()
     eng.run_resident(50)  # whole resident steps (graph launches back to back), wall clock
+    torch.cuda.synchronize()
     step_ms = (time.perf_counter() - t0) / 50 * 1e3
     c = eng.sdf_work_stats()
     ops, _ = bench.executed_ops(c, wl.footprint)
