@@ -19,6 +19,10 @@ import bench  # noqa: E402
 for cfg in sys.argv[1:]:
     wl = {"cfg1": W.cfg1, "cfg2": W.cfg2, "cfg3": W.cfg3, "cfg5": W.cfg5}[cfg]()
     eng = Engine(wl.model, wl.limits, wl.footprint, wl.params, n_cap=wl.n_points, guide_cap=8)
+    if os.environ.get("SDF_MODE"):  # A/B of the kernel choice: thread / warp / cta / persist
+        eng.set_sdf_mode(os.environ["SDF_MODE"])
+    if os.environ.get("SDF_THRESHOLD") == "0":
+        eng.set_sdf_threshold(False)
     nom, up = wl.zero_state()
     eng.stage(wl.q0, wl.obstacles(), wl.guidance, nom, up, 0)
     eng.run_resident(10)
@@ -35,7 +39,7 @@ for cfg in sys.argv[1:]:
     poses = wl.params.rollouts * wl.params.horizon
     per_pose = {k: round(v / poses, 2) for k, v in c.items()}
     eff = c["point_tests"] / (32.0 * c["point_iters_warp"]) if c["point_iters_warp"] else None
-    print(json.dumps({"cfg": cfg, "lib": os.environ.get("EXM_LIB_PATH", "base"),
+    print(json.dumps({"cfg": cfg, "lib": os.environ.get("EXM_LIB_PATH", "base"), "mode": os.environ.get("SDF_MODE", "auto"),
                       "sdf_ms": round(st["sdf_ms"], 4), "step_ms": round(step_ms, 4), "tflops_exec": round(ops / st["sdf_ms"] / 1e9, 2),
                       "lane_eff_points": eff and round(eff, 3), "path": eng.last_sdf_path()[0],
                       "per_pose": per_pose}), flush=True)
