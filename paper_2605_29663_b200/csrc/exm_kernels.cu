@@ -369,7 +369,7 @@ __device__ __forceinline__ float unkey(unsigned k) {
 #define EXM_CELL_MAX_R 0.5f
 #endif
 #ifndef EXM_CELL_SEARCH_FRAC
-#define EXM_CELL_SEARCH_FRAC 0.385f
+#define EXM_CELL_SEARCH_FRAC 1.25f
 #endif
 constexpr float kPtsPerCell = EXM_PTS_PER_CELL;  // swept 8-64 (tools/cfg5_snapshots.py): cfg2/cfg3 flat over 16-32, cfg5 snapshots -3 % at 16
 constexpr int kPrepCache = 12;  // cloud points per k_cloud_prep thread kept in registers
@@ -377,6 +377,9 @@ constexpr float kCellMinR = EXM_CELL_MIN_R;       // cell edge >= kCellMinR * R 
                                           // cfg5 snapshots -1 %, cfg1/cfg2 flat; cfg3 is alignment-sensitive)
 constexpr float kCellMaxR = EXM_CELL_MAX_R;       // cell edge <= kCellMaxR * R ...
 constexpr float kCellSearchFrac = EXM_CELL_SEARCH_FRAC;  // ... or <= this fraction of R + mean d_min
+// (with the control cycle's d_safe threshold the mean d_min is the capped one, and the search
+// disc radius <= R + d_safe; swept 0.25-2.0: cfg1 step 0.079 -> 0.058 ms and cfg2 0.145 ->
+// 0.142 ms at 1.25 against the unthresholded 0.385; cfg3 / cfg5 flat: density-sized cells)
 // Below this many poses one thread per pose leaves most SMs idle (< ~16 warps each): use one
 // warp per pose instead.
 // (measured on config 2's cloud: 25.6k poses warp 45 us / thread 64 us, 51.2k poses warp 76 us
