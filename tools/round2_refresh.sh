@@ -18,6 +18,10 @@ python tools/ncu_targets.py step 30 > /dev/null 2>&1 && \
   ncu --metrics gpu__time_duration.sum --clock-control none --cache-control none --csv \
       --log-file "$out/launches_step_cfg2_warm.csv" python tools/ncu_targets.py step 30 > /dev/null 2>&1
 python tools/launch_table.py "$out/launches_step_cfg2_warm.csv" 30 > "$out/launches_step_cfg2_warm.txt"
+python tools/ncu_targets.py cfg3 20 > /dev/null 2>&1 && \
+  ncu --metrics gpu__time_duration.sum --clock-control none --cache-control none --csv \
+      --log-file "$out/launches_step_cfg3_warm.csv" python tools/ncu_targets.py cfg3 20 > /dev/null 2>&1
+python tools/launch_table.py "$out/launches_step_cfg3_warm.csv" 20 > "$out/launches_step_cfg3_warm.txt"
 python tools/ncu_targets.py step 26 > /dev/null 2>&1 && \
   ncu --set full --clock-control none --import-source on --kernel-name-base mangled \
       -k regex:"10k_sdf_gridI" -s 25 -c 1 -f -o "$out/ncu_sdf_grid_cfg2" \
