@@ -380,6 +380,12 @@ exm_status exm_world_state(exm_world* w, double* arc_out, int32_t* dir_out, doub
  * geometry.cpp:357-375). */
 exm_status exm_set_sdf_caps(exm_handle* h, const float* caps);
 
+/* Page-locked host memory (cudaHostAlloc, portable): input buffers (the cloud, the mask)
+ * allocated here are uploaded by DMA without the driver's staging copy (cudaMemcpyAsync from
+ * pageable memory copies through a bounce buffer on the calling thread). NULL on failure. */
+void* exm_host_alloc(size_t bytes);
+void exm_host_free(void* p);
+
 /* Diagnostics (host only, no GPU needed): validates a footprint exactly as exm_create does and
  * returns the body-frame cull geometry the SDF kernels bound with: the bounding box
  * {xmin, xmax, ymin, ymax} (aabb_out[4]) and n_out <= 3 axis-aligned boxes

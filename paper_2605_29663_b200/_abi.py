@@ -148,6 +148,8 @@ SIGNATURES = {
     "exm_sense": (C.c_int32, [_Hp, C.POINTER(ExmWorldObstacle), C.c_int32, _dp, C.c_double,
                               C.c_int32, C.c_uint64, C.c_uint64, _dp, _u8p,
                               C.POINTER(C.c_int32)]),
+    "exm_host_alloc": (C.c_void_p, [C.c_size_t]),
+    "exm_host_free": (None, [C.c_void_p]),
     "exm_footprint_cull_boxes": (C.c_int32, [C.POINTER(ExmFootprint), C.POINTER(C.c_float),
                                              C.POINTER(C.c_float), C.POINTER(C.c_int32)]),
     "exm_step_stats": (C.c_int32, [_Hp, C.POINTER(C.c_int32), C.POINTER(C.c_float),

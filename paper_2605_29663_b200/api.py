@@ -358,6 +358,27 @@ class Guidance:
         self.goal = np.ascontiguousarray(np.asarray(self.goal, dtype=np.float64).reshape(3))
 
 
+class _PinnedBuffer:
+    """exm_host_alloc'd bytes, freed with the object."""
+
+    def __init__(self, nbytes: int):
+        self.lib = _abi.load_library()
+        self.n = max(int(nbytes), 1)
+        self.p = self.lib.exm_host_alloc(self.n)
+        if not self.p:
+            raise MemoryError("exm_host_alloc failed")
+
+    def view(self):
+        v = (C.c_uint8 * self.n).from_address(self.p)
+        v._owner = self  # numpy views hold the ctypes array, which holds the allocation
+        return v
+
+    def __del__(self):
+        if getattr(self, "p", None):
+            self.lib.exm_host_free(self.p)
+            self.p = None
+
+
 @dataclass
 class ObstacleSet:
     points: np.ndarray
@@ -379,6 +400,21 @@ class ObstacleSet:
         mask = np.zeros(capacity, np.uint8)
         mask[: v.shape[0]] = 1
         return ObstacleSet(pts, mask)
+
+    @staticmethod
+    def pinned(points, mask=None) -> "ObstacleSet":
+        """The same set in page-locked host memory (exm_host_alloc): a sensor loop that writes
+        its cloud into these arrays gets DMA uploads without the driver's staging copy."""
+        src = ObstacleSet(points, np.ones(len(points), np.uint8) if mask is None else mask)
+        n = src.points.shape[0]
+        buf = _PinnedBuffer(16 * n + n)
+        pts = np.frombuffer(buf.view(), dtype=np.float64, count=2 * n).reshape(n, 2)
+        m = np.frombuffer(buf.view(), dtype=np.uint8, count=n, offset=16 * n)
+        pts[:] = src.points
+        m[:] = src.mask
+        out = ObstacleSet(pts, m)
+        out._pinned = buf  # keeps the allocation alive with the arrays
+        return out
 
     @staticmethod
     def all_masked(capacity: int) -> "ObstacleSet":

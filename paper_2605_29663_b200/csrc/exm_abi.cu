@@ -2113,6 +2113,19 @@ exm_status exm_set_sdf_caps(exm_handle* h, const float* caps) {
   return EXM_OK;
 }
 
+void* exm_host_alloc(size_t bytes) {
+  void* p = nullptr;
+  if (bytes == 0 || cudaHostAlloc(&p, bytes, cudaHostAllocPortable) != cudaSuccess) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  return p;
+}
+
+void exm_host_free(void* p) {
+  if (p) cudaFreeHost(p);
+}
+
 exm_status exm_footprint_cull_boxes(const exm_footprint* fp, float* aabb_out, float* boxes_out,
                                     int32_t* n_out) {
   FpDev d;

@@ -418,3 +418,27 @@ def test_concurrent_calls_on_one_handle_serialise():
     for t in range(4):
         for c in range(5):
             assert np.array_equal(got[t][c], want[t][c]), (t, c)
+
+
+def test_pinned_obstacle_set_same_decisions():
+    """ObstacleSet.pinned (exm_host_alloc page-locked buffers, DMA uploads) gives the same
+    decisions as pageable numpy buffers; its arrays outlive the ObstacleSet object."""
+    from paper_2605_29663_b200.api import ObstacleSet
+    wl = W.cfg2(K=1024, T=30, N=10_000)
+    obst = wl.obstacles()
+    pinned = ObstacleSet.pinned(obst.points, obst.mask)
+    pts_view = pinned.points
+    assert np.array_equal(pts_view, obst.points) and np.array_equal(pinned.mask, obst.mask)
+    outs = []
+    for o in (obst, pinned):
+        eng = Engine(wl.model, wl.limits, wl.footprint, wl.params, n_cap=wl.n_points, guide_cap=8)
+        nom, up = wl.zero_state()
+        outs.append([eng.control_cycle_raw(wl.q0, o, wl.guidance, nom, up, c) for c in range(3)])
+        eng.close()
+    for a, b in zip(*outs):
+        assert np.array_equal(a.command, b.command) and a.argmin == b.argmin
+        assert a.best_cost == b.best_cost
+    del pinned
+    import gc
+    gc.collect()
+    assert np.array_equal(pts_view, obst.points)  # the view keeps the allocation alive
