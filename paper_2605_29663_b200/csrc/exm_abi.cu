@@ -1011,9 +1011,10 @@ exm_status upload_inputs(exm_handle* h, const double q0[3], const double* pts, c
   if (st != EXM_OK) return st;
   cudaStream_t s = h->stream;
   // The small state (dyn | nominal | guide) goes in one pinned copy; the cloud goes straight from
-  // the caller's buffers (the driver stages pageable memory while this call returns): measured
-  // 10 us per config-2 call faster end to end than a host memcpy into a pinned mirror plus an
-  // async copy, and 2 % faster than page-locked caller buffers (round 1).
+  // the caller's buffers: pageable ones are staged by the driver on this thread (measured 10 us
+  // per config-2 call faster than a host memcpy into a pinned mirror plus an async copy), and
+  // page-locked ones (exm_host_alloc) are a plain DMA: 180 vs 187 us per config-2 call
+  // (tools/host_timing.py, round 2; host staging 4.7 vs 12.2 us).
   EXM_CUDA(cudaMemcpyAsync(h->d_dyn, h->h_dyn, head_bytes(h), cudaMemcpyHostToDevice, s));
   if (n > 0)
     EXM_CUDA(cudaMemcpyAsync(h->d_pts, pts, 2 * static_cast<size_t>(n) * sizeof(double), cudaMemcpyHostToDevice, s));
