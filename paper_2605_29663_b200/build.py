@@ -15,6 +15,11 @@ NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo", "-O3", 
 # Per-unit flags: the FP64 dynamics round every product and sum separately, as the reference's
 # x86-64 build does (no FMA contraction); the FP32 signed-distance kernels fuse explicitly.
 UNIT_FLAGS = {"exm_dynamics.cu": ["-fmad=false"], "exm_world.cu": ["-fmad=false"]}
+# exm_kernels.cu is compiled as this many units (-DEXM_PART=k): its signed-distance kernel
+# instantiations (footprint kind x edge count x mode) are split between them and compile in
+# parallel. The unit holding the 64-edge polygon (the fully unrolled every-pair kernel of
+# config 4) takes ~8.5 minutes, the others under one minute.
+KERNEL_PARTS = 4
 
 
 def _stale(target: str, deps) -> bool:
@@ -37,12 +42,22 @@ def build_library(force: bool = False, verbose: bool = False, lib: str = LIB,
     objdir = os.path.join(os.path.dirname(LIB_), "obj")
     os.makedirs(objdir, exist_ok=True)
     jobs, objs = [], []
+    units = []  # (source, object, extra flags): the SDF kernels' instantiations in KERNEL_PARTS
     for src in SOURCES:
-        obj = os.path.join(objdir, src.replace(".cu", ".o"))
+        if src == "exm_kernels.cu":
+            for k in range(KERNEL_PARTS):
+                units.append((src, src.replace(".cu", f"_p{k}.o"),
+                              [f"-DEXM_PART={k}", f"-DEXM_NPARTS={KERNEL_PARTS}"]))
+        else:
+            units.append((src, src.replace(".cu", ".o"), []))
+    # the longest compiles first (the kernel parts), so the pool's tail is short
+    units.sort(key=lambda u: u[0] != "exm_kernels.cu")
+    for src, oname, extra in units:
+        obj = os.path.join(objdir, oname)
         objs.append(obj)
         if force or _stale(obj, [os.path.join(CSRC, src), *common]):
-            jobs.append(["nvcc", *NVCC_FLAGS, *UNIT_FLAGS.get(src, []), *defines, "-c", "-o", obj,
-                         os.path.join(CSRC, src)])
+            jobs.append(["nvcc", *NVCC_FLAGS, *UNIT_FLAGS.get(src, []), *extra, *defines, "-c",
+                         "-o", obj, os.path.join(CSRC, src)])
 
     def run(cmd):
         if verbose:
@@ -50,7 +65,7 @@ def build_library(force: bool = False, verbose: bool = False, lib: str = LIB,
         subprocess.run(cmd, check=True)
 
     if jobs:
-        with ThreadPoolExecutor(max_workers=len(jobs)) as ex:
+        with ThreadPoolExecutor(max_workers=min(len(jobs), max(os.cpu_count() or 1, 1))) as ex:
             list(ex.map(run, jobs))
     if force or jobs or _stale(LIB_, objs):
         run(["nvcc", "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", LIB_, *objs,

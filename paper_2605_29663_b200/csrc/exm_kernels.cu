@@ -15,7 +15,21 @@
 
 #include "exm_device.cuh"
 
-#ifdef EXM_TIMING  // phase timestamps of k_cloud_prep (diagnostic builds only)
+// The (footprint kind, edge count) instantiations of the signed-distance kernels are split over
+// EXM_NPARTS translation units compiled in parallel from this file (build.py: -DEXM_PART=k
+// -DEXM_NPARTS=P); part 0 also holds every non-templated kernel and the exported launchers,
+// which route each footprint to the part that instantiated it. Without the macros: one unit.
+#ifndef EXM_NPARTS
+#define EXM_NPARTS 1
+#endif
+#ifndef EXM_PART
+#define EXM_PART 0
+#endif
+#if EXM_NPARTS < 1 || EXM_NPARTS > 4 || EXM_PART < 0 || EXM_PART >= EXM_NPARTS
+#error "EXM_PART / EXM_NPARTS out of range (at most 4 parts)"
+#endif
+
+#if defined(EXM_TIMING) && EXM_PART == 0  // phase timestamps of k_cloud_prep (diagnostic builds only)
 __device__ long long g_probe_prep[16];
 #define EXM_PROBE_P(i) \
   do {                 \
@@ -423,6 +437,7 @@ __device__ __forceinline__ GridMeta make_gridmeta(float mnx, float mxx, float mn
   return g;
 }
 
+#if EXM_PART == 0
 // Single-CTA cloud preparation: mask compaction, FP64 recentring at q0 then FP32 rounding,
 // bounding box, uniform grid (cell >= cs_target, <= kGridMax per axis), counting sort.
 __global__ void __launch_bounds__(1024) k_cloud_prep(const double* __restrict__ pts,
@@ -690,6 +705,8 @@ __global__ void __launch_bounds__(kSortWarps * 32) k_cell_sort(
   for (int c = blockIdx.x * kSortWarps + wid; c < cells; c += gridDim.x * kSortWarps)
     sort_cell(c, lane, hist, raw, raw_start, cell_start, gm, cloud, chunk);
 }
+
+#endif  // EXM_PART == 0
 
 // Ring c (Chebyshev radius k >= 1) around (ci, cj): 8k cells, enumerated row/column-wise.
 __device__ __forceinline__ void ring_cell(int k, int t, int ci, int cj, int& i, int& j) {
@@ -1205,6 +1222,7 @@ __global__ void __launch_bounds__(W == 1 ? 128 : 32 * W) k_sdf_grid_warp(
 
 // Recentring point of a staged pose batch: the poses' centroid, summed in a fixed order by one
 // CTA (deterministic), then every pose / point is recentred in FP64 and rounded once.
+#if EXM_PART == 0
 __global__ void __launch_bounds__(1024) k_pose_center(const double* __restrict__ poses, int n,
                                                       double* __restrict__ center) {
   pdl_wait();
@@ -1249,6 +1267,7 @@ __global__ void k_recentre(const double* __restrict__ pts, int n, const double* 
   const double2 w = reinterpret_cast<const double2*>(pts)[i];
   out[i] = make_float2(static_cast<float>(w.x - center[0]), static_cast<float>(w.y - center[1]));
 }
+#endif  // EXM_PART == 0
 
 // batch_signed_distance (geometry.cpp:298-318): one body-frame query per thread, FP32 queries
 // rounded on the host while they are staged (the identity pose: no recentring).
@@ -1494,6 +1513,7 @@ __global__ void __launch_bounds__(kPairThreads, 2) k_sdf_pairs_poly(
   }
 }
 
+#if EXM_PART == 0
 __global__ void k_keys_to_double(const unsigned* __restrict__ keys, int n,
                                  double* __restrict__ out) {
   pdl_wait();
@@ -1508,32 +1528,69 @@ __global__ void k_fill_u32(unsigned* p, unsigned v, int n) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) p[i] = v;
 }
+#endif  // EXM_PART == 0
 
 // ------------------------------------------------------------------ dispatch
+// (kind, edge count) -> instantiation index; the part that instantiates it is index % EXM_NPARTS.
+__host__ __device__ constexpr int combo_index(int kind, int count) {
+  if (kind == EXM_FOOTPRINT_POLYGON) {
+    switch (count) {
+      case 3: return 0;
+      case 4: return 1;
+      case 5: return 2;
+      case 6: return 3;
+      case 7: return 4;
+      case 8: return 5;
+      case 10: return 6;
+      case 12: return 7;
+      case 16: return 8;
+      case 32: return 9;
+      case 64: return 10;
+      default: return 11;
+    }
+  }
+  switch (count) {
+    case 1: return 12;
+    case 2: return 13;
+    case 3: return 14;
+    case 4: return 15;
+    default: return 16;
+  }
+}
+
+template <template <int, int> class Launch, int KIND, int NB, typename... Args>
+cudaError_t run_combo(const FpDev& fp, Args&&... args) {
+  if constexpr (combo_index(KIND, NB) % EXM_NPARTS == EXM_PART)
+    return Launch<KIND, NB>::run(fp, args...);
+  else
+    return cudaErrorInvalidValue;  // instantiated by another part: the launchers route there
+}
+
 template <template <int, int> class Launch, typename... Args>
 cudaError_t dispatch_fp(const FpDev& fp, Args&&... args) {
+  constexpr int P = EXM_FOOTPRINT_POLYGON, R = EXM_FOOTPRINT_RECT_COVER;
   if (fp.kind == EXM_FOOTPRINT_POLYGON) {
     switch (fp.count) {
-      case 3: return Launch<EXM_FOOTPRINT_POLYGON, 3>::run(fp, args...);
-      case 4: return Launch<EXM_FOOTPRINT_POLYGON, 4>::run(fp, args...);
-      case 5: return Launch<EXM_FOOTPRINT_POLYGON, 5>::run(fp, args...);
-      case 6: return Launch<EXM_FOOTPRINT_POLYGON, 6>::run(fp, args...);
-      case 7: return Launch<EXM_FOOTPRINT_POLYGON, 7>::run(fp, args...);
-      case 8: return Launch<EXM_FOOTPRINT_POLYGON, 8>::run(fp, args...);
-      case 10: return Launch<EXM_FOOTPRINT_POLYGON, 10>::run(fp, args...);
-      case 12: return Launch<EXM_FOOTPRINT_POLYGON, 12>::run(fp, args...);
-      case 16: return Launch<EXM_FOOTPRINT_POLYGON, 16>::run(fp, args...);
-      case 32: return Launch<EXM_FOOTPRINT_POLYGON, 32>::run(fp, args...);
-      case 64: return Launch<EXM_FOOTPRINT_POLYGON, 64>::run(fp, args...);
-      default: return Launch<EXM_FOOTPRINT_POLYGON, 0>::run(fp, args...);
+      case 3: return run_combo<Launch, P, 3>(fp, args...);
+      case 4: return run_combo<Launch, P, 4>(fp, args...);
+      case 5: return run_combo<Launch, P, 5>(fp, args...);
+      case 6: return run_combo<Launch, P, 6>(fp, args...);
+      case 7: return run_combo<Launch, P, 7>(fp, args...);
+      case 8: return run_combo<Launch, P, 8>(fp, args...);
+      case 10: return run_combo<Launch, P, 10>(fp, args...);
+      case 12: return run_combo<Launch, P, 12>(fp, args...);
+      case 16: return run_combo<Launch, P, 16>(fp, args...);
+      case 32: return run_combo<Launch, P, 32>(fp, args...);
+      case 64: return run_combo<Launch, P, 64>(fp, args...);
+      default: return run_combo<Launch, P, 0>(fp, args...);
     }
   }
   switch (fp.count) {
-    case 1: return Launch<EXM_FOOTPRINT_RECT_COVER, 1>::run(fp, args...);
-    case 2: return Launch<EXM_FOOTPRINT_RECT_COVER, 2>::run(fp, args...);
-    case 3: return Launch<EXM_FOOTPRINT_RECT_COVER, 3>::run(fp, args...);
-    case 4: return Launch<EXM_FOOTPRINT_RECT_COVER, 4>::run(fp, args...);
-    default: return Launch<EXM_FOOTPRINT_RECT_COVER, 0>::run(fp, args...);
+    case 1: return run_combo<Launch, R, 1>(fp, args...);
+    case 2: return run_combo<Launch, R, 2>(fp, args...);
+    case 3: return run_combo<Launch, R, 3>(fp, args...);
+    case 4: return run_combo<Launch, R, 4>(fp, args...);
+    default: return run_combo<Launch, R, 0>(fp, args...);
   }
 }
 
@@ -1670,6 +1727,91 @@ struct PairsLaunch {
 }  // namespace
 
 // ------------------------------------------------------------------ launchers
+template <int KIND, int NB>
+struct PointsLaunch {
+  static cudaError_t run(const FpDev& fp, const float2* q, int n, float* out, cudaStream_t s) {
+    if (n <= 0) return cudaSuccess;
+    if (const cudaError_t le = launch_k(k_sdf_points<KIND, NB>, (n + 255) / 256, 256, 0, s, fp,
+                                        q, n, out);
+        le != cudaSuccess)
+      return le;
+    return cudaGetLastError();
+  }
+};
+
+// This part's share of the signed-distance launchers (named per part: sdf_*_p<k>).
+#define EXM_PASTE2(a, b) a##b
+#define EXM_PASTE(a, b) EXM_PASTE2(a, b)
+#define EXM_PART_FNS(k)                                                                          \
+  cudaError_t EXM_PASTE(sdf_grid_p, k)(const FpDev& fp, const float4* poses, int n_poses, int T,  \
+                                       bool hmajor, const CloudGrid& g, const float* cap,         \
+                                       float thr, int mode, bool warp, float* out, SdfPath* path, \
+                                       unsigned long long* stats, cudaStream_t s);                \
+  cudaError_t EXM_PASTE(sdf_points_p, k)(const FpDev& fp, const float2* q, int n, float* out,     \
+                                         cudaStream_t s);                                         \
+  cudaError_t EXM_PASTE(sdf_pairs_p, k)(const FpDev& fp, const float4* poses, int n_poses,        \
+                                        const float2* pts, const uint8_t* mask, int n_points,     \
+                                        float* per_pair, unsigned* pose_min_key, cudaStream_t s);
+EXM_PART_FNS(EXM_PART)
+
+cudaError_t EXM_PASTE(sdf_grid_p, EXM_PART)(const FpDev& fp, const float4* poses, int n_poses,
+                                            int T, bool hmajor, const CloudGrid& g,
+                                            const float* cap, float thr, int mode, bool warp,
+                                            float* out, SdfPath* path, unsigned long long* stats,
+                                            cudaStream_t s) {
+  if (warp) return dispatch_fp<GridWarpLaunch>(fp, poses, n_poses, g, mode == kSdfCta, thr, out, path, s);
+  return dispatch_fp<GridLaunch>(fp, poses, n_poses, T, hmajor, g, cap, thr, mode, out, path, stats, s);
+}
+
+cudaError_t EXM_PASTE(sdf_points_p, EXM_PART)(const FpDev& fp, const float2* q, int n, float* out,
+                                              cudaStream_t s) {
+  return dispatch_fp<PointsLaunch>(fp, q, n, out, s);
+}
+
+cudaError_t EXM_PASTE(sdf_pairs_p, EXM_PART)(const FpDev& fp, const float4* poses, int n_poses,
+                                             const float2* pts, const uint8_t* mask, int n_points,
+                                             float* per_pair, unsigned* pose_min_key,
+                                             cudaStream_t s) {
+  return dispatch_fp<PairsLaunch>(fp, poses, n_poses, pts, mask, n_points, per_pair,
+                                  pose_min_key, s);
+}
+
+#if EXM_PART == 0
+#if EXM_NPARTS > 1
+EXM_PART_FNS(1)
+#endif
+#if EXM_NPARTS > 2
+EXM_PART_FNS(2)
+#endif
+#if EXM_NPARTS > 3
+EXM_PART_FNS(3)
+#endif
+// Route a footprint to the part that instantiated its kernels.
+#if EXM_NPARTS > 3
+#define EXM_ROUTE(fn, ...)                                                        \
+  switch (combo_index(fp.kind, fp.count) % EXM_NPARTS) {                         \
+    case 1: return EXM_PASTE(fn, 1)(__VA_ARGS__);                                \
+    case 2: return EXM_PASTE(fn, 2)(__VA_ARGS__);                                \
+    case 3: return EXM_PASTE(fn, 3)(__VA_ARGS__);                                \
+    default: return EXM_PASTE(fn, 0)(__VA_ARGS__);                               \
+  }
+#elif EXM_NPARTS > 2
+#define EXM_ROUTE(fn, ...)                                                        \
+  switch (combo_index(fp.kind, fp.count) % EXM_NPARTS) {                         \
+    case 1: return EXM_PASTE(fn, 1)(__VA_ARGS__);                                \
+    case 2: return EXM_PASTE(fn, 2)(__VA_ARGS__);                                \
+    default: return EXM_PASTE(fn, 0)(__VA_ARGS__);                               \
+  }
+#elif EXM_NPARTS > 1
+#define EXM_ROUTE(fn, ...)                                                        \
+  switch (combo_index(fp.kind, fp.count) % EXM_NPARTS) {                         \
+    case 1: return EXM_PASTE(fn, 1)(__VA_ARGS__);                                \
+    default: return EXM_PASTE(fn, 0)(__VA_ARGS__);                               \
+  }
+#else
+#define EXM_ROUTE(fn, ...) return EXM_PASTE(fn, 0)(__VA_ARGS__);
+#endif
+
 // Chunk size per handle: 16-point chunks measured 10 % faster on the 20k / 50k-point aisle and
 // moving-disc clouds (configs 3, 5), 6 % slower on config 2's 10k clutter points.
 int chunk_for_capacity(int n_cap) {
@@ -1720,8 +1862,7 @@ cudaError_t launch_sdf_grid(const FpDev& fp, const float4* poses, int n_poses, i
   const bool warp = !stats && (mode == kSdfWarp || mode == kSdfCta ||
                                (n_poses <= kWarpPerPoseMax && mode != kSdfThread &&
                                 mode != kSdfBrute && mode != kSdfPersist));
-  if (warp) return dispatch_fp<GridWarpLaunch>(fp, poses, n_poses, g, mode == kSdfCta, thr, out, path, s);
-  return dispatch_fp<GridLaunch>(fp, poses, n_poses, T, hmajor, g, cap, thr, mode, out, path, stats, s);
+  EXM_ROUTE(sdf_grid_p, fp, poses, n_poses, T, hmajor, g, cap, thr, mode, warp, out, path, stats, s)
 }
 
 cudaError_t launch_pose_prep(const double* poses, int n, double* center, float4* out,
@@ -1746,27 +1887,14 @@ cudaError_t launch_recentre(const double* pts, int n, const double* center, floa
   return cudaGetLastError();
 }
 
-template <int KIND, int NB>
-struct PointsLaunch {
-  static cudaError_t run(const FpDev& fp, const float2* q, int n, float* out, cudaStream_t s) {
-    if (n <= 0) return cudaSuccess;
-    if (const cudaError_t le = launch_k(k_sdf_points<KIND, NB>, (n + 255) / 256, 256, 0, s, fp,
-                                        q, n, out);
-        le != cudaSuccess)
-      return le;
-    return cudaGetLastError();
-  }
-};
-
 cudaError_t launch_sdf_points(const FpDev& fp, const float2* q, int n, float* out, cudaStream_t s) {
-  return dispatch_fp<PointsLaunch>(fp, q, n, out, s);
+  EXM_ROUTE(sdf_points_p, fp, q, n, out, s)
 }
 
 cudaError_t launch_sdf_pairs(const FpDev& fp, const float4* poses, int n_poses,
                              const float2* pts, const uint8_t* mask, int n_points,
                              float* per_pair, unsigned* pose_min_key, cudaStream_t s) {
-  return dispatch_fp<PairsLaunch>(fp, poses, n_poses, pts, mask, n_points, per_pair,
-                                  pose_min_key, s);
+  EXM_ROUTE(sdf_pairs_p, fp, poses, n_poses, pts, mask, n_points, per_pair, pose_min_key, s)
 }
 
 cudaError_t launch_min_keys_to_double(const unsigned* keys, int n, double* out, cudaStream_t s) {
@@ -1780,5 +1908,6 @@ cudaError_t launch_fill_u32(unsigned* p, unsigned v, int n, cudaStream_t s) {
   { if (const cudaError_t le = launch_k(k_fill_u32, (n + 255) / 256, 256, 0, s, p, v, n); le != cudaSuccess) return le; }
   return cudaGetLastError();
 }
+#endif  // EXM_PART == 0
 
 }  // namespace exm
