@@ -31,6 +31,7 @@
 #define EXM_B200_H
 
 #include <stdint.h>
+#include <stddef.h>
 
 #ifdef __cplusplus
 extern "C" {
