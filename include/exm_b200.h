@@ -287,12 +287,20 @@ enum {
   EXM_OPT_SDF_MAP = 6,      /* lanes <-> poses of the thread-per-pose SDF: 0 tuned on the
                                handle's first steps (default), 1 a rollout's consecutive steps per
                                warp, 2 consecutive rollouts at one step per warp */
-  EXM_OPT_SDF_THRESHOLD = 7 /* 1 (default): the rollout minima of exm_control_cycle /
+  EXM_OPT_SDF_THRESHOLD = 7, /* 1 (default): the rollout minima of exm_control_cycle /
                                exm_hybrid_cycle / exm_sharded_cycle are resolved exactly only below
                                d_safe (the obstacle cost is identically 0 and the rollout is not
                                unsafe at or above it, controller.cpp:98-101, :162, and no rollout
                                minimum is returned), so decisions are unchanged; 0: every rollout
                                minimum exact. exm_evaluate_rollouts is always exact. */
+  EXM_OPT_SDF_FP64 = 8      /* 1: exm_evaluate_rollouts computes its minima in FP64 with the
+                               reference's own arithmetic (min_signed_distance_at over
+                               PreparedFootprint::sd, geometry.cpp:260-295, :357-375; brute force,
+                               one thread per pose) and its costs from them: minima and costs then
+                               agree with the reference to the ulps of cos/sin (its 1e-9
+                               batch-vs-scalar check, acceptance_main.cpp:260-300). 0 (default):
+                               the FP32 culled kernels (within 1e-5 m). The control cycle is not
+                               affected. */
 };
 /* Signed-distance kernel selection: automatic, or (tests) every bound disabled, no chunk
  * bound, a forced thread / warp / 8-warp-CTA per pose kernel, persistent warps, caps ignored. */

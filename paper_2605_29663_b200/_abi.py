@@ -89,6 +89,7 @@ class ExmSdfPath(C.Structure):
 # exm_set_option options and EXM_SDF_* modes (include/exm_b200.h)
 OPT_SDF_MODE, OPT_AUTO_CAPS, OPT_PREGEN, OPT_HOST_TIMING, OPT_HOST_THREADS, OPT_SDF_MAP = 1, 2, 3, 4, 5, 6
 OPT_SDF_THRESHOLD = 7
+OPT_SDF_FP64 = 8
 SDF_MODES = {"auto": 0, "brute": 1, "nochunk": 2, "thread": 3, "warp": 4, "cta": 5,
              "persist": 6, "nocap": 7}
 SDF_NCOUNT = 10

@@ -792,6 +792,13 @@ class Engine:
         False: every rollout minimum exact. evaluate_rollouts is always exact."""
         self.set_option(_abi.OPT_SDF_THRESHOLD, 1 if on else 0)
 
+    def set_sdf_fp64(self, on: bool):
+        """True: evaluate_rollouts computes its minima (and the costs built on them) in FP64 with
+        the reference's own arithmetic (min_signed_distance_at over PreparedFootprint::sd,
+        geometry.cpp:260-295, :357-375), brute force; False (default): the FP32 culled kernels.
+        The control cycle is not affected."""
+        self.set_option(_abi.OPT_SDF_FP64, 1 if on else 0)
+
     def last_sdf_path(self):
         """What the last rollout / validation SDF launches ran (kernel 0 thread, 1 warp, 2 CTA
         per pose; chunk; persistent; hmajor)."""

@@ -8,13 +8,17 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "lib", "libexm_b200.so")
-SOURCES = ["exm_kernels.cu", "exm_dynamics.cu", "exm_world.cu", "exm_abi.cu"]
+SOURCES = ["exm_kernels.cu", "exm_dynamics.cu", "exm_world.cu", "exm_exact64.cu", "exm_abi.cu"]
 HEADERS = ["exm_common.cuh", "exm_device.cuh"]
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo", "-O3", "-std=c++17",
               "-Xcompiler", "-fPIC", "-Xcompiler", "-Wall"]
 # Per-unit flags: the FP64 dynamics round every product and sum separately, as the reference's
 # x86-64 build does (no FMA contraction); the FP32 signed-distance kernels fuse explicitly.
-UNIT_FLAGS = {"exm_dynamics.cu": ["-fmad=false"], "exm_world.cu": ["-fmad=false"]}
+UNIT_FLAGS = {"exm_dynamics.cu": ["-fmad=false"], "exm_world.cu": ["-fmad=false"],
+              "exm_exact64.cu": ["-fmad=false"]}
+# Unit-private headers (a change rebuilds only the units that include them).
+UNIT_DEPS = {"exm_dynamics.cu": ["exm_exact64.cuh"], "exm_exact64.cu": ["exm_exact64.cuh"],
+             "exm_abi.cu": ["exm_exact64.cuh"]}
 # exm_kernels.cu is compiled as this many units (-DEXM_PART=k): its signed-distance kernel
 # instantiations (footprint kind x edge count x mode) are split between them and compile in
 # parallel. The unit holding the 64-edge polygon (the fully unrolled every-pair kernel of
@@ -55,7 +59,8 @@ def build_library(force: bool = False, verbose: bool = False, lib: str = LIB,
     for src, oname, extra in units:
         obj = os.path.join(objdir, oname)
         objs.append(obj)
-        if force or _stale(obj, [os.path.join(CSRC, src), *common]):
+        deps = [os.path.join(CSRC, d) for d in UNIT_DEPS.get(src, [])]
+        if force or _stale(obj, [os.path.join(CSRC, src), *common, *deps]):
             jobs.append(["nvcc", *NVCC_FLAGS, *UNIT_FLAGS.get(src, []), *extra, *defines, "-c",
                          "-o", obj, os.path.join(CSRC, src)])
 

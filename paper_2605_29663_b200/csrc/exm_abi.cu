@@ -27,6 +27,7 @@
 
 #include "../../include/exm_b200.h"
 #include "exm_common.cuh"
+#include "exm_exact64.cuh"
 
 using namespace exm;
 
@@ -284,6 +285,49 @@ std::vector<std::array<double, 4>> cover_boxes(const std::vector<double>& x,
   for (size_t i = 0; i < n; ++i)
     if (!segment_covered(x[i], y[i], x[(i + 1) % n], y[(i + 1) % n], grown)) return {whole};
   return boxes;
+}
+
+// PreparedFootprint in FP64 (geometry.cpp:230-257) for the EXM_OPT_SDF_FP64 path, from a
+// footprint build_footprint has validated (same counter-clockwise orientation as the FP32 table).
+void build_footprint64(const exm_footprint* fp, FpDev64* out) {
+  std::memset(out, 0, sizeof *out);
+  const int n = fp->count;
+  out->kind = fp->kind;
+  out->count = n;
+  double radius = 0.0;
+  if (fp->kind == EXM_FOOTPRINT_POLYGON) {
+    std::vector<double> x(fp->x, fp->x + n), y(fp->y, fp->y + n);
+    double area2 = 0.0;
+    for (int i = 0; i < n; ++i) area2 += x[i] * y[(i + 1) % n] - y[i] * x[(i + 1) % n];
+    if (area2 < 0.0) {
+      std::reverse(x.begin(), x.end());
+      std::reverse(y.begin(), y.end());
+    }
+    for (int i = 0; i < n; ++i) {
+      const double ax = x[i], ay = y[i], bx = x[(i + 1) % n], by = y[(i + 1) % n];
+      double* v = out->v[i];
+      v[0] = ax;
+      v[1] = ay;
+      v[2] = bx - ax;
+      v[3] = by - ay;
+      v[4] = 1.0 / ((bx - ax) * (bx - ax) + (by - ay) * (by - ay));
+      radius = std::max(radius, std::sqrt(ax * ax + ay * ay));
+    }
+  } else {
+    for (int i = 0; i < n; ++i) {
+      const double cx = fp->x[i], cy = fp->y[i], hx = fp->hx[i], hy = fp->hy[i];
+      double* v = out->v[i];
+      v[0] = cx;
+      v[1] = cy;
+      v[2] = hx;
+      v[3] = hy;
+      // FootprintSpec::bounding_radius over the cover's outline corners (geometry.cpp:127-145)
+      const double xs[2] = {cx - hx, cx + hx}, ys[2] = {cy - hy, cy + hy};
+      for (double vx : xs)
+        for (double vy : ys) radius = std::max(radius, std::sqrt(vx * vx + vy * vy));
+    }
+  }
+  out->radius = radius;
 }
 
 exm_status build_footprint(const exm_footprint* fp, FpDev* out) {
@@ -550,6 +594,11 @@ struct exm_handle {
   // (sdf_thr = the least float whose double value is >= d_safe; results min(exact, sdf_thr))
   bool sdf_threshold = true;
   float sdf_thr = HUGE_VALF;
+  // EXM_OPT_SDF_FP64: exm_evaluate_rollouts takes its minima from the FP64 brute-force kernel
+  // (the reference's arithmetic) instead of the FP32 culled one
+  bool sdf_fp64 = false;
+  FpDev64 fp64{};
+  double* d_dmin64 = nullptr;
   // what the last rollout / validation signed-distance launch ran (exm_last_sdf_path)
   SdfPath roll_path{}, val_path{};
   // lane <-> pose mapping of the thread-per-pose SDF (EXM_OPT_SDF_MAP): 0 tuned per handle (the
@@ -1135,6 +1184,7 @@ exm_status exm_create(const exm_footprint* footprint, const exm_model* model,
   auto* h = new exm_handle();
   h->device = dev;
   h->fp = fp;
+  build_footprint64(footprint, &h->fp64);
   h->K = params->rollouts;
   h->T = params->horizon;
   h->D = D;
@@ -1263,7 +1313,7 @@ void exm_destroy(exm_handle* h) {
                  h->d_partials, h->d_upd, h->d_val_poses, h->d_val_base, h->d_val_dmin, h->d_out,
                  h->d_controls, h->d_states, h->d_cost, h->d_unsafe, h->sb_poses, h->sb_pts64,
                  h->sb_pts, h->sb_mask, h->sb_keys, h->sb_min, h->sb_pairs, h->d_nstate,
-                 h->sb_poses64, h->sb_center, h->bsd_dq, h->bsd_dd};
+                 h->sb_poses64, h->sb_center, h->bsd_dq, h->bsd_dd, h->d_dmin64};
   for (void* p : dev)
     if (p) cudaFree(p);
   delete h->pool;
@@ -1346,25 +1396,40 @@ exm_status exm_evaluate_rollouts(exm_handle* h, const double q0[3], const double
   st = upload_eps(h, eps);
   if (st != EXM_OK) return st;
   const size_t KT = static_cast<size_t>(h->K) * h->T;
+  const bool fp64 = h->sdf_fp64;
   if (controls_out && !h->d_controls) EXM_CUDA(dalloc(&h->d_controls, KT * h->D));
-  if (states_out && !h->d_states) EXM_CUDA(dalloc(&h->d_states, static_cast<size_t>(h->K) * (h->T + 1) * 3));
+  if ((states_out || fp64) && !h->d_states)
+    EXM_CUDA(dalloc(&h->d_states, static_cast<size_t>(h->K) * (h->T + 1) * 3));
+  if (fp64 && !h->d_dmin64) EXM_CUDA(dalloc(&h->d_dmin64, KT));
   cudaStream_t s = h->stream;
   const StepConst& sc = h->sc;
-  EXM_CUDA(launch_cloud_prep(h->d_pts, h->d_mask, h->d_dyn, h->fp.radius, h->grid, h->n_cap, s));
+  if (!fp64)
+    EXM_CUDA(launch_cloud_prep(h->d_pts, h->d_mask, h->d_dyn, h->fp.radius, h->grid, h->n_cap, s));
   EXM_CUDA(launch_rollout(sc, h->d_dyn, h->d_nominal, h->d_eps, 0, h->d_poses, h->d_task,
                           h->d_guide, h->guide_cap, h->d_base, h->d_ctrl,
                           controls_out ? h->d_controls : nullptr,
-                          states_out ? h->d_states : nullptr, s));
-  if (const exm_status st2 = enqueue_rollout_sdf(h, s, true); st2 != EXM_OK) return st2;
-  EXM_CUDA(launch_rollout_costs(sc, h->d_task, h->d_base, h->d_ctrl, h->d_dmin, h->d_cost,
-                                h->d_unsafe, h->grid.dstat, nullptr, s));
+                          (states_out || fp64) ? h->d_states : nullptr, s));
+  if (fp64) {
+    // the mask upload_inputs skipped is all ones
+    const bool use_mask = mask && n_points > 0 && std::memchr(mask, 0, static_cast<size_t>(n_points));
+    EXM_CUDA(launch_sdf_exact64(h->fp64, h->d_states, h->K, h->T, h->d_pts,
+                                use_mask ? h->d_mask : nullptr, n_points, h->d_dmin64, s));
+    EXM_CUDA(launch_rollout_costs_dmin64(sc, h->d_task, h->d_base, h->d_ctrl, h->d_dmin64,
+                                         h->d_cost, h->d_unsafe, h->grid.dstat, s));
+  } else {
+    if (const exm_status st2 = enqueue_rollout_sdf(h, s, true); st2 != EXM_OK) return st2;
+    EXM_CUDA(launch_rollout_costs(sc, h->d_task, h->d_base, h->d_ctrl, h->d_dmin, h->d_cost,
+                                  h->d_unsafe, h->grid.dstat, nullptr, s));
+  }
   if (controls_out)
     EXM_CUDA(cudaMemcpyAsync(controls_out, h->d_controls, KT * h->D * sizeof(double), cudaMemcpyDeviceToHost, s));
   if (states_out)
     EXM_CUDA(cudaMemcpyAsync(states_out, h->d_states, static_cast<size_t>(h->K) * (h->T + 1) * 3 * sizeof(double),
                              cudaMemcpyDeviceToHost, s));
   std::vector<float> dmin_f;
-  if (dmin_out) {
+  if (dmin_out && fp64) {
+    EXM_CUDA(cudaMemcpyAsync(dmin_out, h->d_dmin64, KT * sizeof(double), cudaMemcpyDeviceToHost, s));
+  } else if (dmin_out) {
     dmin_f.resize(KT);
     EXM_CUDA(cudaMemcpyAsync(dmin_f.data(), h->d_dmin, KT * sizeof(float), cudaMemcpyDeviceToHost, s));
   }
@@ -1373,7 +1438,7 @@ exm_status exm_evaluate_rollouts(exm_handle* h, const double q0[3], const double
   if (unsafe_out)
     EXM_CUDA(cudaMemcpyAsync(unsafe_out, h->d_unsafe, h->K, cudaMemcpyDeviceToHost, s));
   EXM_CUDA(cudaStreamSynchronize(s));
-  if (dmin_out)
+  if (dmin_out && !fp64)
     for (size_t i = 0; i < KT; ++i) dmin_out[i] = static_cast<double>(dmin_f[i]);
   return EXM_OK;
 }
@@ -2182,6 +2247,7 @@ exm_status exm_set_option(exm_handle* h, int32_t option, int32_t value) {
       break;
     case EXM_OPT_AUTO_CAPS: h->auto_caps = value != 0; break;
     case EXM_OPT_SDF_THRESHOLD: h->sdf_threshold = value != 0; break;
+    case EXM_OPT_SDF_FP64: h->sdf_fp64 = value != 0; return EXM_OK;  // evaluate_rollouts only
     case EXM_OPT_SDF_MAP:
       if (value < 0 || value > 2) return fail(EXM_ERR_INVALID_ARGUMENT, "unknown SDF mapping");
       h->sdf_map = value;

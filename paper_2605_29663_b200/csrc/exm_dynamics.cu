@@ -15,6 +15,7 @@
 // Compiled with -fmad=false: like the reference's x86-64 build, no multiply-add is fused, so
 // every FP64 product and sum is rounded where the reference rounds it.
 #include "exm_device.cuh"
+#include "exm_exact64.cuh"
 
 #ifdef EXM_TIMING  // phase timestamps of k_update (diagnostic builds only)
 __device__ long long g_probe[16];
@@ -552,7 +553,7 @@ __global__ void __launch_bounds__(kCostWarps * 32) k_rollout_costs(
     const StepConst sc, const double* __restrict__ task, const double* __restrict__ base_cost,
     const double* __restrict__ ctrl_cost, const float* __restrict__ dmin,
     double* __restrict__ cost, uint8_t* __restrict__ unsafe, float* __restrict__ dstat,
-    float* __restrict__ hstat) {
+    float* __restrict__ hstat, const double* __restrict__ dmin64) {
   pdl_wait();
   extern __shared__ double g[];  // per warp: task[T], obst[T], ctrl[T]; then 2T floats
   __shared__ float red[2][kCostWarps];
@@ -574,8 +575,9 @@ __global__ void __launch_bounds__(kCostWarps * 32) k_rollout_costs(
   if (live) {
     const size_t row = static_cast<size_t>(r) * T;
     for (int h = lane; h < T; h += 32) {
-      const float df = dmin[row + h];
-      const double d = static_cast<double>(df);
+      // dmin64: the FP64 minima of exm_evaluate_rollouts under EXM_OPT_SDF_FP64
+      const float df = dmin64 ? static_cast<float>(dmin64[row + h]) : dmin[row + h];
+      const double d = dmin64 ? dmin64[row + h] : static_cast<double>(df);
       s_t[h] = task[row + h];  // formed by the rollout kernel
       s_o[h] = obstacle_cost(sc, d);
       s_c[h] = ctrl_cost[row + h];  // staged: the serial sum below reads shared memory only
@@ -1023,7 +1025,7 @@ template <int W>
 cudaError_t rollout_costs_launch(const StepConst& sc, const double* task, const double* base_cost,
                                  const double* ctrl_cost, const float* dmin, double* cost,
                                  uint8_t* unsafe, float* dstat, float* hstat, size_t smem,
-                                 cudaStream_t s) {
+                                 cudaStream_t s, const double* dmin64 = nullptr) {
   if (smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(k_rollout_costs<W>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(smem));
@@ -1031,7 +1033,7 @@ cudaError_t rollout_costs_launch(const StepConst& sc, const double* task, const 
   }
   if (const cudaError_t le = launch_k(k_rollout_costs<W>, (sc.k_local + W - 1) / W, W * 32, smem, s,
                                       sc, task, base_cost, ctrl_cost, dmin, cost, unsafe, dstat,
-                                      hstat);
+                                      hstat, dmin64);
       le != cudaSuccess)
     return le;
   return cudaGetLastError();
@@ -1054,6 +1056,24 @@ cudaError_t launch_rollout_costs(const StepConst& sc, const double* task, const 
                                    smem_for(4), s);
   return rollout_costs_launch<1>(sc, task, base_cost, ctrl_cost, dmin, cost, unsafe, dstat, hstat,
                                  smem_for(1), s);
+}
+
+cudaError_t launch_rollout_costs_dmin64(const StepConst& sc, const double* task,
+                                        const double* base_cost, const double* ctrl_cost,
+                                        const double* dmin64, double* cost, uint8_t* unsafe,
+                                        float* dstat, cudaStream_t s) {
+  if (sc.k_local <= 0) return cudaSuccess;
+  auto smem_for = [&](int w) {
+    return sizeof(double) * (3 * static_cast<size_t>(w) * sc.T + sc.T);
+  };
+  if (smem_for(16) <= 200 * 1024)
+    return rollout_costs_launch<16>(sc, task, base_cost, ctrl_cost, nullptr, cost, unsafe, dstat,
+                                    nullptr, smem_for(16), s, dmin64);
+  if (smem_for(4) <= 200 * 1024)
+    return rollout_costs_launch<4>(sc, task, base_cost, ctrl_cost, nullptr, cost, unsafe, dstat,
+                                   nullptr, smem_for(4), s, dmin64);
+  return rollout_costs_launch<1>(sc, task, base_cost, ctrl_cost, nullptr, cost, unsafe, dstat,
+                                 nullptr, smem_for(1), s, dmin64);
 }
 
 cudaError_t launch_block_partials(const StepConst& sc, const double* cost, const uint8_t* unsafe,

@@ -131,6 +131,9 @@ std::shared_ptr<Cached> handle_for(const Config& c, int n, int g) {
     const int ncap = std::max(n, std::max(1024, slot ? 2 * slot->n_cap : 0));
     const int gcap = std::max(g, 64);
     throw_status(exm_create(&c.fp, &c.model, &c.limits, &c.params, ncap, gcap, -1, &fresh->h));
+    // evaluate_rollouts returns the reference's FP64 minima and costs (its callers check them
+    // against scalar loops at 1e-9, acceptance_main.cpp:260-300); the control cycle keeps FP32
+    throw_status(exm_set_option(fresh->h, EXM_OPT_SDF_FP64, 1));
     fresh->n_cap = ncap;
     fresh->guide_cap = gcap;
     slot = std::move(fresh);  // the previous handle lives on while a caller still holds it

@@ -9,8 +9,9 @@ Expected outcome: criteria 1, 2, 4, 5, 7, 9 PASS with the reference's recorded b
 (proj/test_output.txt). Criterion 3 measures the CPU evaluators' cost shape (rectangle cover
 >= 1.5x faster than the polygon at 1e5 queries, log-log slope ~1 over 1e4..1e6): on the B200
 both evaluators cost the same per-call staging, so its outcome is reported, not asserted.
-Criterion 6 contains a 1e-9 batch-vs-scalar d_min check that an FP32 signed distance cannot meet
-by design (north-star tolerance is 1e-5); criterion 8 needs the CLI (CLI11 absent; its episode
+Criterion 6's 1e-9 batch-vs-scalar d_min and cost check passes because the drop-in's
+evaluate_rollouts runs with EXM_OPT_SDF_FP64 (FP64 minima in the reference's own arithmetic,
+csrc/exm_exact64.cu; the control cycle keeps the FP32 kernels); criterion 8 needs the CLI (CLI11 absent; its episode
 determinism is covered by tests/test_episode_b200.py)."""
 import os
 import re
@@ -34,10 +35,11 @@ def test_reference_acceptance_suite_on_b200(tmp_path):
     res = {int(m.group(2)): (m.group(1), m.group(3))
            for m in re.finditer(r"\[(PASS|FAIL)\] criterion (\d+): (.*)", out)}
     print("criterion 3 on the B200:", res[3])
-    for c in (1, 2, 4, 5, 7, 9):
+    for c in (1, 2, 4, 5, 6, 7, 9):
         assert res[c][0] == "PASS", (c, res[c][1])
     # behavioural numbers identical to the reference's recorded run (proj/test_output.txt:31-33)
     assert "hybrid 10/10" in res[7][1] and "median 8.2 s" in res[7][1]
     assert "DoN 1.05 exact 10/10" in res[4][1] and "hull 0/10" in res[4][1]
     assert "DoN 1: exact 10/10, hull 0/10" in res[5][1]
-    assert res[6][0] == "FAIL" and "all hold" in res[6][1]  # only the 1e-9 d_min check trips
+    # the 1e-9 batch-vs-scalar check holds through the FP64 evaluate_rollouts path
+    assert res[6][0] == "PASS" and "all hold" in res[6][1], res[6][1]
