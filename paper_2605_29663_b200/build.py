@@ -87,7 +87,7 @@ def build_oracle(with_reference: bool | None = None) -> None:
     if with_reference is None:
         with_reference = os.path.isdir(os.path.join(ref, "src"))
     if with_reference:
-        subprocess.run(["make", "-s", "-C", odir, "ref", f"REF_DIR={ref}"], check=True)
+        subprocess.run(["make", "-s", "-C", odir, "ref", "refunit", f"REF_DIR={ref}"], check=True)
 
 
 def build_dropin() -> None:
@@ -95,7 +95,7 @@ def build_dropin() -> None:
     ref = os.environ.get("REF_DIR", "/root/reference/proj")
     if os.path.isdir(os.path.join(ref, "src")):
         subprocess.run(["make", "-s", "-C", os.path.join(HERE, "host"), f"REF_DIR={ref}", "all",
-                        "acceptance", "scaling", "episode", "hybridcheck"],
+                        "acceptance", "scaling", "episode", "hybridcheck", "refunit"],
                        check=True)
 
 
