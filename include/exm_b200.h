@@ -293,7 +293,9 @@ enum {
                                unsafe at or above it, controller.cpp:98-101, :162, and no rollout
                                minimum is returned), so decisions are unchanged; 0: every rollout
                                minimum exact. exm_evaluate_rollouts is always exact. */
-  EXM_OPT_SDF_FP64 = 8      /* 1: exm_evaluate_rollouts computes its minima in FP64 with the
+  EXM_OPT_SDF_FP64 = 8      /* 1: exm_batch_signed_distance evaluates PreparedFootprint::sd in
+                               FP64 (16 B in / 8 B out per query on the link), and
+                               exm_evaluate_rollouts computes its minima in FP64 with the
                                reference's own arithmetic (min_signed_distance_at over
                                PreparedFootprint::sd, geometry.cpp:260-295, :357-375; brute force,
                                one thread per pose) and its costs from them: minima and costs then

@@ -1629,7 +1629,11 @@ exm_status exm_batch_signed_distance(exm_handle* h, const double* queries, int32
   EXM_CUDA(cudaSetDevice(h->device));
   const int nchunks = std::min(8, std::max(1, (n + 65535) / 65536));
   const int chunk = ((n + nchunks - 1) / nchunks + 1023) & ~1023;
-  exm_status st = ensure_bsd(h, chunk);
+  // EXM_OPT_SDF_FP64: FP64 queries and results (16 B / 8 B, two staging elements per query)
+  // evaluated by the reference's arithmetic (k_sdf_points64); else rounded to FP32
+  const bool f64 = h->sdf_fp64;
+  const int cap = f64 ? 2 * chunk : chunk;  // staging elements per slot
+  exm_status st = ensure_bsd(h, cap);
   if (st != EXM_OK) return st;
   // pieces per conversion: ~16k queries each, at most the pool's threads
   const int parts = std::max(1, std::min(h->pool->size(), chunk / 16384));
@@ -1637,8 +1641,12 @@ exm_status exm_batch_signed_distance(exm_handle* h, const double* queries, int32
     const size_t c0 = static_cast<size_t>(c) * chunk;
     const size_t m = std::min<size_t>(chunk, static_cast<size_t>(n) - c0);
     const size_t a = m * part / parts, b = m * (part + 1) / parts;
-    float2* dst = h->bsd_hq + static_cast<size_t>(c % kBsdSlots) * chunk;
+    float2* dst = h->bsd_hq + static_cast<size_t>(c % kBsdSlots) * cap;
     const double* src = queries + 2 * c0;
+    if (f64) {
+      std::memcpy(reinterpret_cast<double*>(dst) + 2 * a, src + 2 * a, (b - a) * 2 * sizeof(double));
+      return;
+    }
     for (size_t i = a; i < b; ++i)
       dst[i] = make_float2(static_cast<float>(src[2 * i]), static_cast<float>(src[2 * i + 1]));
   };
@@ -1646,7 +1654,11 @@ exm_status exm_batch_signed_distance(exm_handle* h, const double* queries, int32
     const size_t c0 = static_cast<size_t>(c) * chunk;
     const size_t m = std::min<size_t>(chunk, static_cast<size_t>(n) - c0);
     const size_t a = m * part / parts, b = m * (part + 1) / parts;
-    const float* src = h->bsd_hd + static_cast<size_t>(c % kBsdSlots) * chunk;
+    const float* src = h->bsd_hd + static_cast<size_t>(c % kBsdSlots) * cap;
+    if (f64) {
+      std::memcpy(out + c0 + a, reinterpret_cast<const double*>(src) + a, (b - a) * sizeof(double));
+      return;
+    }
     for (size_t i = a; i < b; ++i) out[c0 + i] = static_cast<double>(src[i]);
   };
   for (int c = 0; c < nchunks; ++c) {
@@ -1660,11 +1672,16 @@ exm_status exm_batch_signed_distance(exm_handle* h, const double* queries, int32
     const size_t c0 = static_cast<size_t>(c) * chunk;
     const int m = static_cast<int>(std::min<size_t>(chunk, static_cast<size_t>(n) - c0));
     const int slot = c % kBsdSlots;
-    const size_t so = static_cast<size_t>(slot) * chunk;
+    const size_t so = static_cast<size_t>(slot) * cap;
     cudaStream_t s = h->bsd_st[slot];
-    EXM_CUDA(cudaMemcpyAsync(h->bsd_dq + so, h->bsd_hq + so, m * sizeof(float2), cudaMemcpyHostToDevice, s));
-    EXM_CUDA(launch_sdf_points(h->fp, h->bsd_dq + so, m, h->bsd_dd + so, s));
-    EXM_CUDA(cudaMemcpyAsync(h->bsd_hd + so, h->bsd_dd + so, m * sizeof(float), cudaMemcpyDeviceToHost, s));
+    const size_t qb = f64 ? 2 * sizeof(double) : sizeof(float2), rb = f64 ? sizeof(double) : sizeof(float);
+    EXM_CUDA(cudaMemcpyAsync(h->bsd_dq + so, h->bsd_hq + so, m * qb, cudaMemcpyHostToDevice, s));
+    if (f64)
+      EXM_CUDA(launch_sdf_points64(h->fp64, reinterpret_cast<const double*>(h->bsd_dq + so), m,
+                                   reinterpret_cast<double*>(h->bsd_dd + so), s));
+    else
+      EXM_CUDA(launch_sdf_points(h->fp, h->bsd_dq + so, m, h->bsd_dd + so, s));
+    EXM_CUDA(cudaMemcpyAsync(h->bsd_hd + so, h->bsd_dd + so, m * rb, cudaMemcpyDeviceToHost, s));
     EXM_CUDA(cudaEventRecord(h->bsd_ev[slot], s));
   }
   // the last min(kBsdSlots, nchunks) chunks
@@ -2247,7 +2264,7 @@ exm_status exm_set_option(exm_handle* h, int32_t option, int32_t value) {
       break;
     case EXM_OPT_AUTO_CAPS: h->auto_caps = value != 0; break;
     case EXM_OPT_SDF_THRESHOLD: h->sdf_threshold = value != 0; break;
-    case EXM_OPT_SDF_FP64: h->sdf_fp64 = value != 0; return EXM_OK;  // evaluate_rollouts only
+    case EXM_OPT_SDF_FP64: h->sdf_fp64 = value != 0; return EXM_OK;  // not in the step graphs
     case EXM_OPT_SDF_MAP:
       if (value < 0 || value > 2) return fail(EXM_ERR_INVALID_ARGUMENT, "unknown SDF mapping");
       h->sdf_map = value;

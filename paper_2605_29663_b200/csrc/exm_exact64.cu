@@ -82,7 +82,28 @@ __global__ void __launch_bounds__(kExactThreads) k_sdf_exact64(
   out[i] = any ? best : empty;
 }
 
+__global__ void __launch_bounds__(kExactThreads) k_sdf_points64(const __grid_constant__ FpDev64 fp,
+                                                                const double2* __restrict__ q,
+                                                                int n, double* __restrict__ out) {
+  pdl_wait();
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double2 p = q[i];
+  out[i] = sd64(fp, p.x, p.y);
+}
+
 }  // namespace
+
+cudaError_t launch_sdf_points64(const FpDev64& fp, const double* q, int n, double* out,
+                                cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  if (const cudaError_t le = launch_k(k_sdf_points64, (n + kExactThreads - 1) / kExactThreads,
+                                      kExactThreads, 0, s, fp, reinterpret_cast<const double2*>(q),
+                                      n, out);
+      le != cudaSuccess)
+    return le;
+  return cudaGetLastError();
+}
 
 cudaError_t launch_sdf_exact64(const FpDev64& fp, const double* states, int K, int T,
                                const double* pts, const uint8_t* mask, int n, double* out,

@@ -20,6 +20,10 @@ cudaError_t launch_sdf_exact64(const FpDev64& fp, const double* states, int K, i
                                const double* pts, const uint8_t* mask, int n, double* out,
                                cudaStream_t s);
 
+// out[i] = PreparedFootprint::sd(q[i]) in FP64 (batch_signed_distance, geometry.cpp:298-318).
+cudaError_t launch_sdf_points64(const FpDev64& fp, const double* q, int n, double* out,
+                                cudaStream_t s);
+
 // launch_rollout_costs with FP64 minima (the FP64 path of exm_evaluate_rollouts).
 cudaError_t launch_rollout_costs_dmin64(const StepConst& sc, const double* task,
                                         const double* base_cost, const double* ctrl_cost,

@@ -8,7 +8,7 @@ import numpy as np
 import pytest
 
 from paper_2605_29663_b200 import workloads as W
-from paper_2605_29663_b200.api import Engine
+from paper_2605_29663_b200.api import Engine, FootprintSpec
 from tests import oracle_bindings as ob
 
 pytestmark = [pytest.mark.gpu,
@@ -70,3 +70,23 @@ def test_fp64_empty_cloud_and_option_off():
     fp32 = eng.evaluate_rollouts(wl.q0, nom, eps, obs, wl.guidance, up)
     assert np.max(np.abs(fp32.d_min - fp64.d_min) / np.maximum(np.abs(fp64.d_min), 1.0)) <= 1e-5
     assert not np.array_equal(fp32.d_min, fp64.d_min)  # the FP32 path really ran
+
+
+@pytest.mark.parametrize("fp_name", ["l12", "star64", "forklift", "box"])
+@pytest.mark.parametrize("n", [1, 1000, 300_000])
+def test_fp64_batch_signed_distance_matches_reference(fp_name, n):
+    """batch_signed_distance (geometry.cpp:298-318) under EXM_OPT_SDF_FP64, through the chunked
+    host pipeline (n = 300k: several chunks over the three staging slots), against the reference
+    at its own 1e-12 (proj/tests/test_geometry.cpp:307-320)."""
+    fp = {"l12": W.l12_footprint, "star64": W.star64_footprint, "forklift": W.forklift_footprint,
+          "box": lambda: FootprintSpec.rect_cover([[0, 0]], [[0.5, 0.25]])}[fp_name]()
+    wl = W.cfg2(K=256, T=4, N=16)
+    eng = Engine(wl.model, wl.limits, fp, wl.params, n_cap=16, guide_cap=8)
+    eng.set_sdf_fp64(True)
+    ref = ob.Reference(fp, wl.model, wl.limits, wl.params)
+    q = np.random.default_rng(n).uniform(-3.0, 3.0, size=(n, 2))
+    got, want = eng.batch_signed_distance(q), ref.batch_signed_distance(q)
+    assert np.all(np.abs(got - want) <= 1e-12 * (1.0 + np.maximum(np.abs(got), np.abs(want))))
+    eng.set_sdf_fp64(False)
+    f32 = eng.batch_signed_distance(q)
+    assert np.max(np.abs(f32 - want) / np.maximum(np.abs(want), 1.0)) <= 1e-5

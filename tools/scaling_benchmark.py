@@ -10,9 +10,10 @@ Rows per (footprint, query count):
                                kernel, D2H), wall clock per call from Python — the analogue of
                                the paper's per-call JAX timing (L 0.09/0.29 ms,
                                T 0.09/0.32, F 0.15/0.30 at 1e5)
-  threads=b200-dropin(T)       the reference's OWN scaling_benchmark (bench.cpp, compiled where it
+  threads=b200-dropin-P(T)     the reference's OWN scaling_benchmark (bench.cpp, compiled where it
                                lies) with batch_signed_distance redirected to the B200 by
-                               host/geometry_sdf_b200.cpp (lib/exm_scaling_b200), T host threads
+                               host/geometry_sdf_b200.cpp (lib/exm_scaling_b200), T host threads,
+                               P = fp64 (the drop-in's default) or fp32 (EXM_DROPIN_SDF_FP32=1)
 
   python tools/scaling_benchmark.py [--trials 100] [--counts 100,1000,10000,100000,1000000]
 """
@@ -104,12 +105,16 @@ def dropin_rows(counts, trials, nproc):
     with tempfile.TemporaryDirectory() as d:
         subprocess.run([sys.executable, os.path.join(ROOT, "tools", "write_fixtures.py"), d],
                        check=True, capture_output=True)
-        for th in sorted({1, min(8, nproc)}):
-            out = subprocess.run([binary, d, str(trials), str(th), *map(str, counts)],
-                                 check=True, capture_output=True, text=True).stdout
-            for line in out.strip().splitlines()[1:]:
-                f = line.split(",")
-                print(",".join(f[:7] + [f"b200-dropin({f[7]})"]), flush=True)
+        # the drop-in's default is FP64 (EXM_OPT_SDF_FP64, the reference's arithmetic);
+        # EXM_DROPIN_SDF_FP32=1 rows time the FP32 kernel through the same call
+        for prec, fp32 in (("fp64", "0"), ("fp32", "1")):
+            env = dict(os.environ, EXM_DROPIN_SDF_FP32=fp32)
+            for th in sorted({1, min(8, nproc)}):
+                out = subprocess.run([binary, d, str(trials), str(th), *map(str, counts)],
+                                     check=True, capture_output=True, text=True, env=env).stdout
+                for line in out.strip().splitlines()[1:]:
+                    f = line.split(",")
+                    print(",".join(f[:7] + [f"b200-dropin-{prec}({f[7]})"]), flush=True)
 
 
 if __name__ == "__main__":
