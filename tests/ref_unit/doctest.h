@@ -1,7 +1,7 @@
 // TEST INFRASTRUCTURE ONLY. A minimal stand-in for the doctest header the reference's unit
 // tests include (proj/tests/test_*.cpp; doctest itself is fetched by the reference's CMake and
 // is not in this image). It implements exactly what those files use: TEST_CASE, CHECK,
-// CHECK_FALSE, REQUIRE, CHECK_THROWS_AS and doctest::Approx with doctest's comparison rule
+// CHECK_FALSE, REQUIRE, CHECK_THROWS_AS, CHECK_THROWS_WITH_AS (+ doctest::Contains) and doctest::Approx with doctest's comparison rule
 // (|a - b| < eps * (scale + max(|a|, |b|)), eps default 100 * FLT_EPSILON, scale 1), and a main
 // that runs every case and prints one "[PASS]/[FAIL] case" line each plus a summary.
 #pragma once
@@ -11,6 +11,7 @@
 #include <cstdio>
 #include <exception>
 #include <limits>
+#include <string>
 #include <vector>
 
 namespace doctest {
@@ -40,7 +41,19 @@ class Approx {
   double scale_ = 1.0;
 };
 
+class Contains {
+ public:
+  explicit Contains(const char* s) : s_(s) {}
+  bool matches(const std::string& what) const { return what.find(s_) != std::string::npos; }
+
+ private:
+  std::string s_;
+};
+
 namespace detail {
+
+inline bool message_matches(const Contains& c, const std::string& what) { return c.matches(what); }
+inline bool message_matches(const char* exact, const std::string& what) { return what == exact; }
 
 struct Case {
   const char* name;
@@ -101,6 +114,18 @@ inline void report(bool ok, const char* what, const char* expr, const char* file
     } catch (...) {                                                                          \
     }                                                                                        \
     ::doctest::detail::report(doctest_ok_, "CHECK_THROWS_AS", #expr, __FILE__, __LINE__);    \
+  } while (0)
+
+#define CHECK_THROWS_WITH_AS(expr, with, ...)                                                \
+  do {                                                                                       \
+    bool doctest_ok_ = false;                                                                \
+    try {                                                                                    \
+      static_cast<void>(expr);                                                               \
+    } catch (const __VA_ARGS__& e) {                                                         \
+      doctest_ok_ = ::doctest::detail::message_matches(with, e.what());                     \
+    } catch (...) {                                                                          \
+    }                                                                                        \
+    ::doctest::detail::report(doctest_ok_, "CHECK_THROWS_WITH_AS", #expr, __FILE__, __LINE__); \
   } while (0)
 
 #ifdef DOCTEST_CONFIG_IMPLEMENT_WITH_MAIN
