@@ -799,7 +799,10 @@ __global__ void __launch_bounds__(256) k_update(const StepConst sc,
       sf[b] = exp(-z);
     }
     __syncthreads();
-    if (tid == 0) {  // block order: deterministic, independent of the GPU count
+    // block order: deterministic, independent of the GPU count. On the CTA's last thread, which
+    // holds no U column when T * D < blockDim (every benchmark config), so warp 0's U sums do
+    // not wait behind the serial S / A chains, the division and the log
+    if (tid == blockDim.x - 1) {
       double S = 0.0, A = 0.0;
       for (int b = 0; b < nb; ++b) {
         S += sf[b] * sS[b];
