@@ -755,10 +755,17 @@ __global__ void __launch_bounds__(256) k_update(const StepConst sc,
   pdl_wait();
   extern __shared__ double sm_u[];  // T*D updated controls, nb factors, nb betas; then scratch
   __shared__ double s_beta, s_S;
+  __shared__ StepDyn s_dyn;  // staged now: its load overlaps the merge instead of the rollout
   const int tid = threadIdx.x, lane = tid & 31;
   const int nb = sc.nblocks_total;
   const int stride = partial_stride(sc.T, sc.D);
   const int TD = sc.T * sc.D;
+  static_assert(sizeof(StepDyn) % sizeof(uint64_t) == 0, "StepDyn copied as 8-byte words");
+  constexpr int kDynWords = sizeof(StepDyn) / sizeof(uint64_t);
+  if (tid >= blockDim.x - kDynWords)  // the last threads (idle in the U sums of every config)
+    reinterpret_cast<uint64_t*>(&s_dyn)[tid - (blockDim.x - kDynWords)] =
+        reinterpret_cast<const uint64_t*>(dynp)[tid - (blockDim.x - kDynWords)];
+  const double nom0 = tid < TD ? nominal[tid] : 0.0;  // this thread's first nominal control
   double* s_upd = sm_u;
   double* sf = sm_u + TD;
   EXM_PROBE(0);
@@ -827,18 +834,17 @@ __global__ void __launch_bounds__(256) k_update(const StepConst sc,
 #pragma unroll 16
         for (int b = 0; b < nb; ++b) u += sf[b] * partials[static_cast<size_t>(b) * stride + 4 + o];
       }
-      s_upd[o] = nominal[o] + u / s_S;
+      s_upd[o] = (k == 0 ? nom0 : nominal[o]) + u / s_S;
     }
   } else {
-    for (int o = tid; o < TD; o += blockDim.x) s_upd[o] = nominal[o];
+    for (int o = tid; o < TD; o += blockDim.x) s_upd[o] = o == tid ? nom0 : nominal[o];
   }
   __syncthreads();
   EXM_PROBE(3);
   if (tid < 32) {
     // warp 0 clamps sequentially from u_prev and writes the clamped sequence back; the
     // reference's second clamp inside validate_nominal is idempotent on it.
-    const StepDyn dyn = *dynp;
-    const double b = rollout_warp<TAG>(sc, dyn, s_upd, nullptr, nullptr, 0ull, val_poses, val_xy,
+    const double b = rollout_warp<TAG>(sc, s_dyn, s_upd, nullptr, nullptr, 0ull, val_poses, val_xy,
                                        upd, nullptr, val_base + 1,
                                        sf + (merge ? 5 * nb : 0));
     if (tid == 0) *val_base = b;
