@@ -865,6 +865,13 @@ __global__ void __launch_bounds__(64) k_finalize(
   __shared__ int s_ok;
   const int tid = threadIdx.x;
   const int T = sc.T, D = sc.D;
+  // every load of this thread's first step issued together with the header loads (one L2
+  // round trip instead of one after the guide has been staged)
+  const bool first = tid < T;
+  const float dmin0 = first ? val_dmin[tid] : 0.f;
+  const double2 xy0 = first ? val_xy[tid] : make_double2(0.0, 0.0);
+  const double ctrl0 = first ? val_base[1 + tid] : 0.0;
+  const double goal[3] = {dyn->goal[0], dyn->goal[1], dyn->goal[2]};
   const int ng = dyn->n_guide;
   double* g = sm2;
   double* c_t = sm2 + 2 * ng;
@@ -874,13 +881,15 @@ __global__ void __launch_bounds__(64) k_finalize(
   if (tid == 0) s_ok = 1;
   __syncthreads();
   for (int h = tid; h < T; h += blockDim.x) {
-    const double d = static_cast<double>(val_dmin[h]);
+    const bool f = h == tid;
+    const double d = static_cast<double>(f ? dmin0 : val_dmin[h]);
     if (out_dmin) out_dmin[h] = d;
     if (d < sc.d_safe) atomicAnd(&s_ok, 0);
-    const double q[3] = {val_xy[h].x, val_xy[h].y, 0.0};
-    c_t[h] = task_cost(sc, q, g, ng, dyn->goal, false);
+    const double2 xy = f ? xy0 : val_xy[h];
+    const double q[3] = {xy.x, xy.y, 0.0};
+    c_t[h] = task_cost(sc, q, g, ng, goal, false);
     c_o[h] = obstacle_cost(sc, d);
-    c_c[h] = val_base[1 + h];
+    c_c[h] = f ? ctrl0 : val_base[1 + h];
   }
   __syncthreads();
   const int ok = s_ok;
