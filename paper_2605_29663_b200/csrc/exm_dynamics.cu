@@ -548,7 +548,7 @@ __global__ void __launch_bounds__(1024) k_rollout_lanes(
 // in exactly the reference's order (with k_rollout's control and terminal costs), so J_r is
 // the reference's value for the same d_min. Also accumulates the search-radius statistic of
 // the next step's cell size (k_cloud_prep).
-template <int kCostWarps>
+template <int kCostWarps, bool kF64 = false>
 __global__ void __launch_bounds__(kCostWarps * 32) k_rollout_costs(
     const StepConst sc, const double* __restrict__ task, const double* __restrict__ base_cost,
     const double* __restrict__ ctrl_cost, const float* __restrict__ dmin,
@@ -575,9 +575,10 @@ __global__ void __launch_bounds__(kCostWarps * 32) k_rollout_costs(
   if (live) {
     const size_t row = static_cast<size_t>(r) * T;
     for (int h = lane; h < T; h += 32) {
-      // dmin64: the FP64 minima of exm_evaluate_rollouts under EXM_OPT_SDF_FP64
-      const float df = dmin64 ? static_cast<float>(dmin64[row + h]) : dmin[row + h];
-      const double d = dmin64 ? dmin64[row + h] : static_cast<double>(df);
+      // kF64: the FP64 minima of exm_evaluate_rollouts under EXM_OPT_SDF_FP64 (a separate
+      // instantiation: the control cycle's FP32 kernel carries no extra branch)
+      const float df = kF64 ? static_cast<float>(dmin64[row + h]) : dmin[row + h];
+      const double d = kF64 ? dmin64[row + h] : static_cast<double>(df);
       s_t[h] = task[row + h];  // formed by the rollout kernel
       s_o[h] = obstacle_cost(sc, d);
       s_c[h] = ctrl_cost[row + h];  // staged: the serial sum below reads shared memory only
@@ -1039,17 +1040,17 @@ cudaError_t launch_rollout(const StepConst& sc, const StepDyn* dyn, const double
   return cudaErrorInvalidValue;
 }
 
-template <int W>
+template <int W, bool kF64 = false>
 cudaError_t rollout_costs_launch(const StepConst& sc, const double* task, const double* base_cost,
                                  const double* ctrl_cost, const float* dmin, double* cost,
                                  uint8_t* unsafe, float* dstat, float* hstat, size_t smem,
                                  cudaStream_t s, const double* dmin64 = nullptr) {
   if (smem > 48 * 1024) {
-    cudaError_t e = cudaFuncSetAttribute(k_rollout_costs<W>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaError_t e = cudaFuncSetAttribute(k_rollout_costs<W, kF64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(smem));
     if (e != cudaSuccess) return e;
   }
-  if (const cudaError_t le = launch_k(k_rollout_costs<W>, (sc.k_local + W - 1) / W, W * 32, smem, s,
+  if (const cudaError_t le = launch_k(k_rollout_costs<W, kF64>, (sc.k_local + W - 1) / W, W * 32, smem, s,
                                       sc, task, base_cost, ctrl_cost, dmin, cost, unsafe, dstat,
                                       hstat, dmin64);
       le != cudaSuccess)
@@ -1085,12 +1086,12 @@ cudaError_t launch_rollout_costs_dmin64(const StepConst& sc, const double* task,
     return sizeof(double) * (3 * static_cast<size_t>(w) * sc.T + sc.T);
   };
   if (smem_for(16) <= 200 * 1024)
-    return rollout_costs_launch<16>(sc, task, base_cost, ctrl_cost, nullptr, cost, unsafe, dstat,
+    return rollout_costs_launch<16, true>(sc, task, base_cost, ctrl_cost, nullptr, cost, unsafe, dstat,
                                     nullptr, smem_for(16), s, dmin64);
   if (smem_for(4) <= 200 * 1024)
-    return rollout_costs_launch<4>(sc, task, base_cost, ctrl_cost, nullptr, cost, unsafe, dstat,
+    return rollout_costs_launch<4, true>(sc, task, base_cost, ctrl_cost, nullptr, cost, unsafe, dstat,
                                    nullptr, smem_for(4), s, dmin64);
-  return rollout_costs_launch<1>(sc, task, base_cost, ctrl_cost, nullptr, cost, unsafe, dstat,
+  return rollout_costs_launch<1, true>(sc, task, base_cost, ctrl_cost, nullptr, cost, unsafe, dstat,
                                  nullptr, smem_for(1), s, dmin64);
 }
 
